@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the Line-DG hot path on B200 (BASELINE.json metric).
+
+One step = one pass of the hot path over the configuration's synthetic input:
+residual (GDOF/s) + analytic Jacobian assembly + block-SpMV on a seeded N(0,1)
+vector (BASELINE.json config 2: "residual + Jacobian + block-SpMV"), fp64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
+
+value      = DOFs processed per second through the whole step (all ranks), GDOF/s,
+             inputs resident in HBM, L2 flushed (512 MB write) between steps.
+e2e        = same metric through the reference-facing host-buffer C-ABI calls
+             (ldg_residual_host, ldg_jacobian_assemble_host, ldg_bsr_spmv_host):
+             H2D of U and x and D2H of R and y inside the timed region.
+roofline   = the step's dominant kernel: algorithmic bytes per launch / mean
+             CUDA-event duration vs the measured HBM copy bandwidth.
+cpu_baseline = the CPU oracle (oracle/, a port of the reference algorithm;
+             the reference's own hot-path sources do not exist) on this host.
+--impl reference runs only that CPU implementation (all host threads).
+Multi-GPU: the north star keeps the path on one GPU ("nothing across GPUs"),
+so N > 1 runs N independent replicas (weak scaling, no collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1204_1533_b200 import CONFIGS, LDG_K11, LDG_K12, LDG_K21  # noqa: E402
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def sizes(cfg, case, m):
+    """Algorithmic bytes per launch (adapted to this store:
+    no column-index stream)."""
+    D, E, npe = case.dim, case.E, case.npe
+    NL, nq, p = case.NL, case.nq, case.p
+    N = E * npe
+    met = D * NL * nq * D + 2 * D * NL * D + npe
+    conn = 8 * 2 * D * E + 4 * E
+    U = 8 * N * m
+    out = {}
+    second = cfg.physics.second_order()
+    if not second:
+        out["residual"] = 2 * U + 8 * met * E + conn
+    else:
+        out["gradient"] = U + 8 * met * E + conn + U * D
+        out["residual"] = U + U * D + 8 * met * E + conn + U
+    ns11 = D * p + 1 + 2 * D
+    out["jacobian"] = 8 * N * ns11 * m * m + U * (2 if second else 1) + 8 * met * E + conn
+    out["spmv"] = 8 * N * ns11 * m * m + 2 * U + conn
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "", 1).isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "", 1).isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU leg
+def cpu_step_fn(cfg, case, U, x):
+    from oracle.pyoracle import Oracle  # CPU baseline leg only
+
+    ora = Oracle(case, cfg.physics)
+    src = cfg.source_for(case)
+    if src is not None:
+        ora.set_source(src)
+
+    def step():
+        ora.residual(U)
+        ora.assemble(U)
+        ora.spmv(LDG_K11, x)
+    return ora, step
+
+
+def run_cpu(cfg, case, U, x, steps, warmup, budget_s=20.0):
+    from oracle.pyoracle import Oracle
+
+    threads = Oracle.max_threads()
+    Oracle.set_threads(threads)
+    _, step = cpu_step_fn(cfg, case, U, x)
+    t0 = time.perf_counter()
+    for _ in range(max(1, warmup)):
+        step()
+        if time.perf_counter() - t0 > budget_s / 2:
+            break
+    times = []
+    for _ in range(max(1, steps)):
+        t = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t)
+        if sum(times) > budget_s:
+            break
+    dofs = case.E * case.npe * cfg.physics.components(case.dim)
+    return dofs, times, threads
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1, help="BASELINE.json config index (1 = 2-D Euler p=4 128^2)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    m = cfg.physics.components(cfg.dim)
+    workload = {"workload": cfg.name, "config_index": args.config, "elements": cfg.n ** cfg.dim,
+                "p": cfg.p, "dofs": cfg.dofs(), "step": "residual + Jacobian assembly + K11 block-SpMV",
+                "l2": "flushed between steps (512 MB write)", "parallelism": "replicas" if world > 1 else "1 GPU"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        case, U = cfg.build()
+        x = case.normal_vector(m, cfg.vector_seed)
+        dofs, times, threads = run_cpu(cfg, case, U, x, args.steps, args.warmup, budget_s=max(30.0, args.cpu_budget))
+        t = statistics.mean(times)
+        val = dofs / t / 1e9
+        line = {"metric": "residual GDOF/s, Jacobian assembly + block-SpMV GB/s (fp64), % HBM roofline, 1 B200",
+                "impl": "reference", "value": val, "unit": "GDOF/s", "n_gpus": args.gpus, "steps": len(times),
+                "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config shapes)",
+                "config": workload,
+                "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "port",
+                                 "sample": f"full {cfg.name} step (all {case.E} elements) x {len(times)}"},
+                "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    from paper_1204_1533_b200 import LineDG
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    case, U = cfg.build()
+    x = case.normal_vector(m, cfg.vector_seed)
+    N = case.E * case.npe
+    dofs = N * m
+    ctx = LineDG(case, cfg.physics)
+    src = cfg.source_for(case)
+    if src is not None:
+        ctx.set_source(src)
+    Ud = torch.from_numpy(U).cuda()
+    xd = torch.from_numpy(x).cuda()
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 512 MB > 126 MB L2
+    ctx.set_sync_errors(False)
+
+    def step(ev):
+        ev[0].record()
+        R = ctx.residual(Ud)
+        ev[1].record()
+        ctx.assemble_jacobians(Ud)
+        ev[2].record()
+        y = ctx.spmv(LDG_K11, xd)
+        ev[3].record()
+        return R, y
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    ctx.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches()
+    for k in range(args.steps):
+        flush.zero_()
+        step(evs[k])
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = ctx.kernel_launches() - launches0
+    clocks = sampler.stop()
+    ctx.synchronize()  # surfaces any physical-state failure of the timed steps
+    t_res = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    t_jac = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    t_spv = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    ms = statistics.mean(e[0].elapsed_time(e[3]) for e in evs)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * dofs / (ms * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer C-ABI (pinned host memory)
+    Uh = torch.from_numpy(U).pin_memory().numpy()
+    xh = torch.from_numpy(x).pin_memory().numpy()
+    ctx.set_sync_errors(True)
+    e2e_times = []
+    for k in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        ctx.residual(Uh)
+        ctx.assemble_jacobians(Uh)
+        ctx.spmv(LDG_K11, xh)
+        t1.record()
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            e2e_times.append(t0.elapsed_time(t1))
+    e2e_ms = statistics.mean(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel
+    hbm, peak_src = peaks()
+    by = sizes(cfg, case, m)
+    kern = {"residual": t_res, "jacobian": t_jac, "spmv": t_spv}
+    dom = max(kern, key=kern.get)
+    breakdown = {}
+    for name, tms in kern.items():
+        b = by[name] if name != "residual" else by["residual"] + by.get("gradient", 0)
+        gbs = b / (tms * 1e-3) / 1e9
+        breakdown[name] = {"ms": tms, "GB/s": gbs, "frac_hbm": gbs / hbm, "alg_bytes": b}
+    breakdown["residual"]["GDOF/s"] = dofs / (t_res * 1e-3) / 1e9
+    bdom = by[dom] if dom != "residual" else by["residual"] + by.get("gradient", 0)
+    achieved = bdom / (kern[dom] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
+        except Exception:
+            traffic = None
+
+    line = {"metric": "residual GDOF/s, Jacobian assembly + block-SpMV GB/s (fp64), % HBM roofline, 1 B200",
+            "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json config shapes)", "config": workload,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src},
+            "breakdown": breakdown,
+            "e2e": {"value": world * dofs / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 3 * 8 * dofs, "d2h_bytes_per_step": 2 * 8 * dofs},
+            "gpu_launches": launches, "clocks": clocks,
+            "jacobian_store_bytes": ctx.jacobian_bytes()}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cd, times, threads = run_cpu(cfg, case, U, x, max(2, min(args.steps, 10)), 1, args.cpu_budget)
+        line["cpu_baseline"] = {"value": cd / statistics.mean(times) / 1e9, "unit": "GDOF/s", "cores": threads,
+                                "kind": "port", "sample": f"full {cfg.name} step x {len(times)} (oracle, OpenMP)"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

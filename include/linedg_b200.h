@@ -1,0 +1,208 @@
+/*
+ * linedg_b200.h -- C-ABI of the B200 (sm_100a) Line-DG hot path.
+ *
+ * This is the drop-in boundary for the part of the reference library
+ * `linedg` whose sources are listed but absent from the reference tree
+ * (reference proj/src/CMakeLists.txt:6-8: discretization.cpp, assembly.cpp,
+ * sparse.cpp).  Their C++ surface is reconstructed from SPEC.md:
+ *
+ *   residual_first_order(ctx, U, t)            SPEC.md:218-226   -> ldg_residual (first-order physics)
+ *   gradient_residual(ctx, U, Q, t)            SPEC.md:228-236   -> ldg_gradient
+ *   residual_second_order(ctx, U, Q, t)        SPEC.md:238-246   -> ldg_residual_uq
+ *   residual_primal(ctx, U, t)                 SPEC.md:248-256   -> ldg_residual (second-order physics)
+ *   assemble_jacobians(ctx, U, t, Analytic)    SPEC.md:409-417   -> ldg_jacobian_assemble
+ *   split_matvec(blocks, alpha_dt, v)          SPEC.md:419-427   -> ldg_split_matvec
+ *   CscMatrix export / triplet export          SPEC.md:391-394, 465 -> ldg_export_triplets
+ *
+ * Inputs are the reference's own setup objects, flattened (no Eigen, no C++
+ * types): NodalBasis1D (reference basis.hpp:17-43), QuadMesh/Face/elem_face
+ * (mesh.hpp:15-39), SwitchAssignment (mesh.hpp:74-89), ElementMapping
+ * (mapping.hpp:19-33), GasModel (physics.hpp:10-14).  Grid functions use the
+ * reference GridFunction layout value(e,node,c) = data[(e*npe+node)*m+c]
+ * (field.hpp:8-9); the auxiliary gradient uses ((e*npe+node)*m+c)*D+d
+ * (field.hpp:38-40 generalised to D).
+ *
+ * Device entry points take DEVICE pointers and are stream-ordered on the
+ * stream given to ldg_create; the *_host variants take HOST pointers and
+ * synchronise.  Every entry point returns an ldg_status; the message of the
+ * last failure is available from ldg_last_error().  Status codes mirror the
+ * reference exception taxonomy (errors.hpp:10-28):
+ *   LDG_ERR_PHYSICAL_STATE  <-> physical_state_error (state via ldg_last_error_state)
+ *   LDG_ERR_CONFIG          <-> config_error
+ *   LDG_ERR_SOLVER          <-> solver_error
+ */
+#ifndef LINEDG_B200_H
+#define LINEDG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+typedef enum ldg_status {
+  LDG_OK = 0,
+  LDG_ERR_PHYSICAL_STATE = 1,
+  LDG_ERR_CONFIG = 2,
+  LDG_ERR_SOLVER = 3,
+  LDG_ERR_CUDA = 4,
+  LDG_ERR_INVALID_ARGUMENT = 5
+} ldg_status;
+
+/* --------------------------------------------------------------- physics */
+typedef enum ldg_physics_kind {
+  LDG_POISSON = 0,         /* PoissonModel       physics.hpp:98-118  (m = 1)   */
+  LDG_EULER = 1,           /* EulerModel         physics.hpp:138-162 (m = D+2) */
+  LDG_NAVIER_STOKES = 2    /* NavierStokesModel  physics.hpp:164-187 (m = D+2) */
+} ldg_physics_kind;
+
+typedef enum ldg_riemann_kind {
+  LDG_ROE = 0,  /* roe_flux, Harten entropy fix 0.05(|u.n|+a)  physics.hpp:196-198 */
+  LDG_LLF = 1   /* local Lax-Friedrichs (extension; not in the reference)                      */
+} ldg_riemann_kind;
+
+typedef enum ldg_bc_kind {
+  LDG_BC_DIRICHLET = 0     /* constant state g_D; Euler: Riemann flux vs g_D */
+} ldg_bc_kind;
+
+typedef struct ldg_bc {
+  int32_t tag;             /* mesh boundary tag (Face::tag, mesh.hpp:24) */
+  int32_t kind;            /* ldg_bc_kind */
+  double value[8];         /* g_D per component (first m used) */
+} ldg_bc;
+
+typedef struct ldg_physics {
+  int32_t kind;            /* ldg_physics_kind */
+  int32_t riemann;         /* ldg_riemann_kind (Euler / Navier-Stokes) */
+  double gamma;            /* GasModel::gamma   (physics.hpp:11) */
+  double mu;               /* GasModel::mu      (physics.hpp:12) */
+  double prandtl;          /* GasModel::prandtl (physics.hpp:13) */
+  double c11;              /* LdgParams::C11 interior, >= 0 */
+  double c22;              /* LdgParams::C22; must be 0 (residual_primal) */
+  double c11_bd;           /* boundary C11 coefficient: C11_bd = c11_bd * p^2 / h_face */
+  int32_t n_bc;            /* number of boundary conditions */
+  const ldg_bc* bcs;       /* BoundaryTable (physics.hpp:35): one entry per boundary tag */
+} ldg_physics;
+
+/* ----------------------------------------------------------------- setup */
+/* Flattened reference setup objects.  D = dim, np = p+1, npe = np^D,
+ * NL = np^(D-1) lines per direction, nq = n_quad.                         */
+typedef struct ldg_setup {
+  int32_t dim;             /* 2 (reference) or 3 (hexahedral extension) */
+  int32_t p;
+  int32_t n_quad;          /* (3p+2)/2, basis.cpp:176 */
+  int32_t n_elems;
+  int32_t n_faces;
+  /* NodalBasis1D (basis.hpp:17-33); matrices row-major [i][q] */
+  const double* nodes;          /* [np]      */
+  const double* quad_points;    /* [nq]      */
+  const double* quad_weights;   /* [nq]      */
+  const double* phi_at_quad;    /* [np][nq]  */
+  const double* dphi_at_quad;   /* [np][nq]  */
+  const double* mass;           /* [np][np]  SPD */
+  /* QuadMesh faces (mesh.hpp:15-26) and elem_face (mesh.hpp:32).
+   * face_orient: 2-D = Face::reversed (0/1); 3-D = dihedral code o in [0,8)
+   * mapping elem_l's face parameter (a,b) to elem_r's:
+   *   (x,y) = (o&1) ? (b,a) : (a,b);  a' = (o&2) ? p-x : x;  b' = (o&4) ? p-y : y.  */
+  const int32_t* face_elem_l;
+  const int32_t* face_face_l;
+  const int32_t* face_elem_r;   /* -1 on boundary faces */
+  const int32_t* face_face_r;
+  const int32_t* face_orient;
+  const int32_t* face_tag;      /* -1 on interior faces */
+  const int32_t* elem_face;     /* [E][2D] */
+  const int8_t* switch_plus;    /* [E][D] SwitchAssignment::plus_sign (mesh.hpp:76); NULL for first-order */
+  /* ElementMapping (mapping.hpp:19-33) */
+  const double* jac_at_nodes;   /* [E][npe]                */
+  const double* nvec_quad;      /* [E][D][NL][nq][D]       */
+  const double* normal_end;     /* [E][D][2][NL][D]        */
+  const double* node_coords;    /* [E][npe][D] (nodes_xy); optional, may be NULL */
+} ldg_setup;
+
+/* ------------------------------------------------------------ Jacobians */
+typedef enum ldg_matrix {
+  LDG_K11 = 0,   /* dR/dU  block m x m              */
+  LDG_K12 = 1,   /* dR/dQ  block m x mD (second-order physics) */
+  LDG_K21 = 2    /* dD/dU  block mD x m, component-diagonal, U-independent */
+} ldg_matrix;
+
+/* Node-level pattern of one matrix in the REFERENCE numbering:
+ * row/col are global node ids e*npe+node.  Sorted by (row, col). */
+typedef struct ldg_pattern_info {
+  int64_t n_rows;          /* global nodes                      */
+  int64_t nnzb;            /* structural node blocks            */
+  int32_t block_rows;      /* scalar rows per block (m, or mD for K21) */
+  int32_t block_cols;      /* scalar cols per block             */
+} ldg_pattern_info;
+
+typedef struct ldg_ctx ldg_ctx;
+
+/* Creation binds the context to one CUDA stream (cudaStream_t, may be NULL
+ * for the legacy default stream).  All tables are copied; the setup memory
+ * may be freed after return. */
+int ldg_create(const ldg_setup* setup, const ldg_physics* physics, void* cuda_stream,
+               ldg_ctx** out);
+void ldg_destroy(ldg_ctx* ctx);
+const char* ldg_last_error(const ldg_ctx* ctx);        /* ctx may be NULL (creation errors) */
+/* After LDG_ERR_PHYSICAL_STATE: offending element, node and state (m doubles). */
+int ldg_last_error_state(const ldg_ctx* ctx, int32_t* elem, int32_t* node, double* state);
+int ldg_components(const ldg_ctx* ctx);               /* m */
+int64_t ldg_num_dofs(const ldg_ctx* ctx);             /* E * npe * m */
+
+/* Optional nodal source S (E*npe*m doubles, host pointer), added to R
+ * (PoissonModel::source_fn evaluated at the nodes, physics.hpp:102). */
+int ldg_set_source(ldg_ctx* ctx, const double* source_host);
+
+/* Residual.  First-order physics: R = S - (1/J) sum_dir r.
+ * Second-order physics: residual_primal, Q = D(U) is computed first and
+ * written to Q_or_null when non-NULL.  Device pointers.                 */
+int ldg_residual(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
+/* residual_second_order R(U,Q) for a given Q (device pointers). */
+int ldg_residual_uq(ldg_ctx* ctx, const double* U, const double* Q, double t, double* R);
+/* gradient_residual: Q = (1/J) sum_dir d (device pointers). */
+int ldg_gradient(ldg_ctx* ctx, const double* U, double t, double* Q);
+
+/* Jacobians (analytic), stored on the device in the line-structured block
+ * store.  Second-order physics uses Q = D(U), computed internally. */
+int ldg_jacobian_assemble(ldg_ctx* ctx, const double* U, double t);
+int ldg_pattern_info_get(const ldg_ctx* ctx, int which, ldg_pattern_info* info);
+/* y = K x for K in {K11, K12, K21} (device pointers; x, y in reference numbering). */
+int ldg_bsr_spmv(ldg_ctx* ctx, int which, const double* x, double* y);
+/* y = v - alpha_dt (K11 v + K12 (K21 v)); first-order: y = v - alpha_dt K11 v */
+int ldg_split_matvec(ldg_ctx* ctx, double alpha_dt, const double* v, double* y);
+/* Export of the node pattern (host arrays of nnzb int64) and block values
+ * (host array nnzb*block_rows*block_cols, row-major blocks), reference numbering.
+ * Any pointer may be NULL. */
+int ldg_export_blocks(ldg_ctx* ctx, int which, int64_t* rows, int64_t* cols, double* vals);
+
+/* Same, restricted to the rows of the listed reference elements (all if
+ * elems == NULL); *nnzb_out receives the number of blocks written.         */
+int ldg_export_blocks_subset(ldg_ctx* ctx, int which, const int32_t* elems, int32_t n_elems,
+                             int64_t* rows, int64_t* cols, double* vals, int64_t* nnzb_out);
+
+/* Error synchronisation.  By default every device entry point waits for its
+ * kernels and reports a physical-state failure synchronously, like the
+ * reference's exceptions.  ldg_set_sync_errors(ctx, 0) makes the device entry
+ * points fully asynchronous (stream-ordered); ldg_synchronize() then waits and
+ * reports any failure recorded since the last check.                       */
+int ldg_set_sync_errors(ldg_ctx* ctx, int on);
+int ldg_synchronize(ldg_ctx* ctx);
+
+/* Host-buffer variants (end-to-end path: H2D, kernels, D2H, synchronise). */
+int ldg_residual_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
+int ldg_jacobian_assemble_host(ldg_ctx* ctx, const double* U, double t);
+int ldg_bsr_spmv_host(ldg_ctx* ctx, int which, const double* x, double* y);
+int ldg_split_matvec_host(ldg_ctx* ctx, double alpha_dt, const double* v, double* y);
+
+/* Instrumentation: number of kernel launches issued by this context so far,
+ * and the device-side byte footprint of the Jacobian store. */
+int64_t ldg_kernel_launches(const ldg_ctx* ctx);
+int64_t ldg_jacobian_bytes(const ldg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LINEDG_B200_H */

@@ -1,0 +1,1157 @@
+// oracle.cpp -- TEST INFRASTRUCTURE ONLY: the CPU parity oracle and the CPU
+// baseline of the Line-DG hot path.  Never linked or loaded by the product.
+//
+// A from-scratch CPU restatement of the reference operations whose sources
+// are absent from the reference tree (proj/src/CMakeLists.txt:5-8):
+//   line_divergence / residual_first_order
+//   gradient_residual
+//   residual_second_order / residual_primal
+//   assemble_jacobians (Analytic + FD)
+//   CscMatrix, split_matvec
+// It follows the reference's numerics literally where they are specified:
+// r = M^-1 b through the Cholesky factor of M column by column
+// (basis.cpp:81-88, 185-189), fluxes at the quadrature points of the
+// interpolated state, point-wise endpoint fluxes with the
+// precomputed non-normalised normals, dU/dt =
+// S - (1/J)(r^1 + ... + r^D), exact Jacobians through Dual<N>
+// (dual.hpp:8-10).  Inputs are the flattened reference setup objects
+// (include/linedg_b200.h: ldg_setup), read verbatim.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "linedg_b200.h"
+#include "oracle_physics.hpp"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace ora {
+
+namespace {
+constexpr int MAXNP = 8, MAXNQ = 12, MAXM = 5, MAXD = 3;
+}
+
+// Node-level block matrix (compressed rows) with dense br x bc blocks.
+struct BlockMat {
+  int br = 0, bc = 0;
+  int64_t nrows = 0;
+  std::vector<int64_t> rowptr;  // nrows+1
+  std::vector<int64_t> col;     // node columns, ascending per row
+  std::vector<double> val;      // nnzb * br * bc
+  bool built = false;
+  bool subset = false;
+  int64_t find(int64_t row, int64_t c) const {
+    const int64_t* b = col.data() + rowptr[row];
+    const int64_t* e = col.data() + rowptr[row + 1];
+    const int64_t* it = std::lower_bound(b, e, c);
+    return (it != e && *it == c) ? (it - col.data()) : -1;
+  }
+};
+
+struct Ctx {
+  int D = 2, p = 1, np = 2, nq = 2, npe = 4, NL = 2, m = 1, E = 0;
+  int kind = LDG_EULER, riemann = LDG_ROE;
+  bool second = false, has_inv = false, vis_u = false;
+  Gas gas;
+  double c11 = 0.0, c11_bd = 0.0;
+  std::vector<double> qw, phi, dphi, L;  // L: Cholesky factor of M (lower, row-major)
+  std::vector<int8_t> sw;
+  std::vector<double> jac, invJ, nvec, nend, source;
+  // Endpoint table [E][D][2][NL]: neighbour element / node, or boundary.
+  std::vector<int32_t> ep_elem, ep_node, ep_bc;  // ep_bc: -1 interior, else index in bcv
+  std::vector<std::vector<double>> bcv;          // Dirichlet states
+  BlockMat K[3];
+  std::string err;
+  std::vector<double> err_state;
+  int err_elem = -1, err_node = -1;
+
+  int node_on_line(int dir, int line, int t) const {
+    if (D == 2) return dir == 0 ? t + np * line : line + np * t;
+    const int l1 = line % np, l2 = line / np;
+    const int st[3] = {1, np, np * np};
+    const int a1 = dir == 0 ? 1 : 0, a2 = dir == 2 ? 1 : 2;
+    return t * st[dir] + l1 * st[a1] + l2 * st[a2];
+  }
+  size_t epi(int e, int dir, int side, int line) const {
+    return ((static_cast<size_t>(e) * D + dir) * 2 + side) * NL + line;
+  }
+  const double* nv(int e, int dir, int line, int q) const {
+    return &nvec[((((static_cast<size_t>(e) * D + dir) * NL + line) * nq) + q) * D];
+  }
+  const double* ne(int e, int dir, int side, int line) const {
+    return &nend[epi(e, dir, side, line) * D];
+  }
+  int sign(int e, int dir, int side) const {
+    const int s = sw.empty() ? 1 : sw[static_cast<size_t>(e) * D + dir];
+    return side ? s : -s;
+  }
+  // Cholesky solve of one column in place (basis.cpp:81-88).
+  void mass_solve(double* x, int stride) const {
+    double y[MAXNP];
+    for (int i = 0; i < np; ++i) {
+      double s = x[i * stride];
+      for (int j = 0; j < i; ++j) s -= L[i * np + j] * y[j];
+      y[i] = s / L[i * np + i];
+    }
+    for (int i = np - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int j = i + 1; j < np; ++j) s -= L[j * np + i] * x[j * stride];
+      x[i * stride] = s / L[i * np + i];
+    }
+  }
+};
+
+namespace {
+
+// Face node of local face lf at face parameter(s): 2-D follows
+// face_node_indices (mesh.cpp:51-65); 3-D: node with index side*p along the
+// face direction and (a,b) along the two transverse axes in increasing order.
+int face_node(const Ctx& c, int lf, int a, int b) {
+  const int p = c.p, np = c.np;
+  if (c.D == 2) {
+    switch (lf) {
+      case 0: return a;
+      case 1: return p + np * a;
+      case 2: return (p - a) + np * p;
+      default: return np * (p - a);
+    }
+  }
+  const int dir = lf / 2, side = lf % 2;
+  const int st[3] = {1, np, np * np};
+  const int a1 = dir == 0 ? 1 : 0, a2 = dir == 2 ? 1 : 2;
+  return side * p * st[dir] + a * st[a1] + b * st[a2];
+}
+
+int lface_of(int D, int dir, int side) {
+  if (D == 2) return dir == 0 ? (side ? 1 : 3) : (side ? 2 : 0);
+  return 2 * dir + side;
+}
+
+void dihedral(int o, int a, int b, int p, int& ao, int& bo) {
+  int x = a, y = b;
+  if (o & 1) std::swap(x, y);
+  ao = (o & 2) ? p - x : x;
+  bo = (o & 4) ? p - y : y;
+}
+
+void build_endpoints(Ctx& c, const ldg_setup& s, const ldg_physics& ph) {
+  const size_t n = static_cast<size_t>(c.E) * c.D * 2 * c.NL;
+  c.ep_elem.assign(n, -1);
+  c.ep_node.assign(n, -1);
+  c.ep_bc.assign(n, -1);
+  std::map<int, int> tag2bc;
+  for (int i = 0; i < ph.n_bc; ++i) {
+    tag2bc[ph.bcs[i].tag] = static_cast<int>(c.bcv.size());
+    c.bcv.emplace_back(ph.bcs[i].value, ph.bcs[i].value + c.m);
+  }
+  const int F = 2 * c.D;
+  for (int e = 0; e < c.E; ++e)
+    for (int dir = 0; dir < c.D; ++dir)
+      for (int side = 0; side < 2; ++side) {
+        const int lf = lface_of(c.D, dir, side);
+        const int fid = s.elem_face[static_cast<size_t>(e) * F + lf];
+        if (fid < 0 || fid >= s.n_faces) throw std::runtime_error("oracle: bad elem_face entry");
+        const bool bdry = s.face_elem_r[fid] < 0;
+        int bci = -1;
+        if (bdry) {
+          auto it = tag2bc.find(s.face_tag[fid]);
+          if (it == tag2bc.end())
+            throw std::runtime_error("oracle: no boundary condition for tag " +
+                                     std::to_string(s.face_tag[fid]));
+          bci = it->second;
+        }
+        const bool is_left = s.face_elem_l[fid] == e && s.face_face_l[fid] == lf;
+        const int oe = is_left ? s.face_elem_r[fid] : s.face_elem_l[fid];
+        const int olf = is_left ? s.face_face_r[fid] : s.face_face_l[fid];
+        const int code = s.face_orient[fid];
+        for (int line = 0; line < c.NL; ++line) {
+          const size_t k = c.epi(e, dir, side, line);
+          if (bdry) {
+            c.ep_bc[k] = bci;
+            continue;
+          }
+          const int own = c.node_on_line(dir, line, side ? c.p : 0);
+          int na = -1, nb = 0;
+          if (c.D == 2) {
+            int kk = -1;
+            for (int t = 0; t <= c.p; ++t)
+              if (face_node(c, lf, t, 0) == own) kk = t;
+            na = code ? c.p - kk : kk;  // Face::reversed (mesh.hpp:18-22)
+          } else {
+            const int a = line % c.np, b = line / c.np;
+            if (is_left) {
+              dihedral(code, a, b, c.p, na, nb);
+            } else {  // inverse transform
+              for (int x = 0; x <= c.p && na < 0; ++x)
+                for (int y = 0; y <= c.p; ++y) {
+                  int ra, rb;
+                  dihedral(code, x, y, c.p, ra, rb);
+                  if (ra == a && rb == b) {
+                    na = x;
+                    nb = y;
+                    break;
+                  }
+                }
+            }
+          }
+          c.ep_elem[k] = oe;
+          c.ep_node[k] = face_node(c, olf, na, nb);
+        }
+      }
+}
+
+// ----------------------------------------------------------- point fluxes
+
+// Physical flux dotted with n: inviscid + viscous parts.
+template <class T>
+void flux_dot(const Ctx& c, const T* u, const T* q, const double* n, T* out) {
+  const int D = c.D, m = c.m;
+  T F[MAXM * MAXD], G[MAXM * MAXD];
+  for (int i = 0; i < m * D; ++i) F[i] = 0.0;
+  if (c.has_inv) euler_flux(D, u, c.gas, F);
+  if (c.second) {
+    if (c.kind == LDG_POISSON) {
+      for (int d = 0; d < D; ++d) G[d] = -q[d];
+    } else {
+      ns_viscous_flux(D, u, q, c.gas, G);
+    }
+    for (int i = 0; i < m * D; ++i) F[i] = F[i] + G[i];
+  }
+  for (int cc = 0; cc < m; ++cc) {
+    T s = 0.0;
+    for (int d = 0; d < D; ++d) s = s + F[cc * D + d] * n[d];
+    out[cc] = s;
+  }
+}
+
+// Viscous flux only, dotted with n.
+template <class T>
+void vflux_dot(const Ctx& c, const T* u, const T* q, const double* n, T* out) {
+  const int D = c.D, m = c.m;
+  T G[MAXM * MAXD];
+  if (c.kind == LDG_POISSON) {
+    for (int d = 0; d < D; ++d) G[d] = -q[d];
+  } else {
+    ns_viscous_flux(D, u, q, c.gas, G);
+  }
+  for (int cc = 0; cc < m; ++cc) {
+    T s = 0.0;
+    for (int d = 0; d < D; ++d) s = s + G[cc * D + d] * n[d];
+    out[cc] = s;
+  }
+}
+
+double norm_of(const double* n, int D) {
+  double s = 0.0;
+  for (int d = 0; d < D; ++d) s += n[d] * n[d];
+  return std::sqrt(s);
+}
+
+// Endpoint numerical flux F_hat . n (inviscid Riemann + LDG viscous switch
+// flux; Dirichlet: PAPER.md:569-574).
+//   interior: uo/qo are the neighbour's node values; bc == nullptr
+//   boundary: bc = g_D, uo/qo ignored
+template <class T>
+void endpoint_flux(const Ctx& c, const T* ui, const T* qi, const T* uo, const T* qo,
+                   const double* bc, const double* n, int S, T* out) {
+  const int m = c.m, D = c.D;
+  for (int k = 0; k < m; ++k) out[k] = 0.0;
+  const double nn = norm_of(n, D);
+  if (c.has_inv) {
+    T g[MAXM];
+    const T* other = uo;
+    if (bc) {
+      for (int k = 0; k < m; ++k) g[k] = bc[k];
+      other = g;
+    }
+    if (c.riemann == LDG_ROE) roe_flux(D, other, ui, n, c.gas, out);
+    else llf_flux(D, other, ui, n, c.gas, out);
+  }
+  if (c.second) {
+    T fv[MAXM];
+    if (bc) {
+      vflux_dot(c, ui, qi, n, fv);
+      const double c11 = c.c11_bd * c.p * c.p / std::pow(nn, 1.0 / (D - 1));
+      for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k] + c11 * nn * (ui[k] - bc[k]);
+    } else {
+      if (S > 0) vflux_dot(c, uo, qo, n, fv);
+      else vflux_dot(c, ui, qi, n, fv);
+      for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k];
+      if (c.c11 != 0.0)
+        for (int k = 0; k < m; ++k) out[k] = out[k] + c.c11 * nn * (ui[k] - uo[k]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- gather
+
+struct LineData {
+  double u[MAXNP][MAXM];
+  double q[MAXNP][MAXM * MAXD];
+  double uo[2][MAXM], qo[2][MAXM * MAXD];
+  const double* bc[2];
+};
+
+void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const double* Q,
+                 LineData& L) {
+  const int m = c.m, mD = c.m * c.D;
+  for (int t = 0; t < c.np; ++t) {
+    const size_t nd = static_cast<size_t>(e) * c.npe + c.node_on_line(dir, line, t);
+    for (int k = 0; k < m; ++k) L.u[t][k] = U[nd * m + k];
+    if (Q)
+      for (int k = 0; k < mD; ++k) L.q[t][k] = Q[nd * mD + k];
+  }
+  for (int side = 0; side < 2; ++side) {
+    const size_t k = c.epi(e, dir, side, line);
+    L.bc[side] = nullptr;
+    if (c.ep_bc[k] >= 0) {
+      L.bc[side] = c.bcv[c.ep_bc[k]].data();
+      continue;
+    }
+    const size_t nd = static_cast<size_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
+    for (int q = 0; q < m; ++q) L.uo[side][q] = U[nd * m + q];
+    if (Q)
+      for (int q = 0; q < mD; ++q) L.qo[side][q] = Q[nd * mD + q];
+  }
+}
+
+// --------------------------------------------------------------- residual
+
+// r^(dir) of one line (before the 1/J scaling), b = M^-1(...).
+void line_residual(const Ctx& c, int e, int dir, int line, const LineData& L, double r[][MAXM]) {
+  const int m = c.m, np = c.np, nq = c.nq, D = c.D, mD = m * D;
+  for (int i = 0; i < np; ++i)
+    for (int k = 0; k < m; ++k) r[i][k] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    double uq[MAXM] = {0}, qq[MAXM * MAXD] = {0};
+    for (int t = 0; t < np; ++t) {
+      const double ph = c.phi[t * nq + q];
+      for (int k = 0; k < m; ++k) uq[k] += ph * L.u[t][k];
+      if (c.second)
+        for (int k = 0; k < mD; ++k) qq[k] += ph * L.q[t][k];
+    }
+    double ft[MAXM];
+    flux_dot(c, uq, qq, c.nv(e, dir, line, q), ft);
+    for (int i = 0; i < np; ++i) {
+      const double w = c.qw[q] * c.dphi[i * nq + q];
+      for (int k = 0; k < m; ++k) r[i][k] -= w * ft[k];
+    }
+  }
+  for (int side = 0; side < 2; ++side) {
+    const int ie = side ? c.p : 0;
+    double fh[MAXM];
+    endpoint_flux<double>(c, L.u[ie], L.q[ie], L.uo[side], L.qo[side], L.bc[side],
+                          c.ne(e, dir, side, line), c.sign(e, dir, side), fh);
+    for (int k = 0; k < m; ++k) r[ie][k] += fh[k];
+  }
+  for (int k = 0; k < m; ++k) c.mass_solve(&r[0][k], MAXM);
+}
+
+void elem_residual(const Ctx& c, int e, const double* U, const double* Q, double* R) {
+  const int m = c.m, npe = c.npe;
+  std::vector<double> acc(static_cast<size_t>(npe) * m, 0.0);
+  LineData L;
+  double r[MAXNP][MAXM];
+  for (int dir = 0; dir < c.D; ++dir)
+    for (int line = 0; line < c.NL; ++line) {
+      gather_line(c, e, dir, line, U, Q, L);
+      line_residual(c, e, dir, line, L, r);
+      for (int t = 0; t < c.np; ++t) {
+        const int nd = c.node_on_line(dir, line, t);
+        for (int k = 0; k < m; ++k) acc[nd * m + k] += r[t][k];
+      }
+    }
+  for (int nd = 0; nd < npe; ++nd) {
+    const size_t g = static_cast<size_t>(e) * npe + nd;
+    for (int k = 0; k < m; ++k) {
+      const double s = c.source.empty() ? 0.0 : c.source[g * m + k];
+      R[g * m + k] = s - c.invJ[g] * acc[nd * m + k];
+    }
+  }
+}
+
+// d^(dir) of one line: M^-1 [u_hat (x) n at the ends - sum_q w phi' u_q (x) nvec_q].
+void line_gradient(const Ctx& c, int e, int dir, int line, const LineData& L,
+                   double d[][MAXM * MAXD]) {
+  const int m = c.m, np = c.np, nq = c.nq, D = c.D, mD = m * D;
+  for (int i = 0; i < np; ++i)
+    for (int k = 0; k < mD; ++k) d[i][k] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    double uq[MAXM] = {0};
+    for (int t = 0; t < np; ++t)
+      for (int k = 0; k < m; ++k) uq[k] += c.phi[t * nq + q] * L.u[t][k];
+    const double* nvq = c.nv(e, dir, line, q);
+    for (int i = 0; i < np; ++i) {
+      const double w = c.qw[q] * c.dphi[i * nq + q];
+      for (int k = 0; k < m; ++k)
+        for (int dd = 0; dd < D; ++dd) d[i][k * D + dd] -= w * (uq[k] * nvq[dd]);
+    }
+  }
+  for (int side = 0; side < 2; ++side) {
+    const int ie = side ? c.p : 0;
+    const double* n = c.ne(e, dir, side, line);
+    const double* uh;
+    if (L.bc[side]) uh = L.bc[side];  // u_hat = g_D
+    else uh = c.sign(e, dir, side) > 0 ? L.u[ie] : L.uo[side];
+    for (int k = 0; k < m; ++k)
+      for (int dd = 0; dd < D; ++dd) d[ie][k * D + dd] += uh[k] * n[dd];
+  }
+  for (int k = 0; k < mD; ++k) c.mass_solve(&d[0][k], MAXM * MAXD);
+}
+
+void elem_gradient(const Ctx& c, int e, const double* U, double* Q) {
+  const int mD = c.m * c.D, npe = c.npe;
+  std::vector<double> acc(static_cast<size_t>(npe) * mD, 0.0);
+  LineData L;
+  double d[MAXNP][MAXM * MAXD];
+  for (int dir = 0; dir < c.D; ++dir)
+    for (int line = 0; line < c.NL; ++line) {
+      gather_line(c, e, dir, line, U, nullptr, L);
+      line_gradient(c, e, dir, line, L, d);
+      for (int t = 0; t < c.np; ++t) {
+        const int nd = c.node_on_line(dir, line, t);
+        for (int k = 0; k < mD; ++k) acc[nd * mD + k] += d[t][k];
+      }
+    }
+  for (int nd = 0; nd < npe; ++nd) {
+    const size_t g = static_cast<size_t>(e) * npe + nd;
+    for (int k = 0; k < mD; ++k) Q[g * mD + k] = c.invJ[g] * acc[nd * mD + k];
+  }
+}
+
+template <class F>
+void for_elems(const Ctx& c, const std::vector<int>* subset, F&& f) {
+  const int n = subset ? static_cast<int>(subset->size()) : c.E;
+  std::atomic<bool> failed{false};
+  std::string msg;
+  std::vector<double> st;
+  int se = -1;
+  std::mutex mu;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int i = 0; i < n; ++i) {
+    if (failed.load(std::memory_order_relaxed)) continue;
+    const int e = subset ? (*subset)[i] : i;
+    try {
+      f(e);
+    } catch (const physical_state_error& ex) {
+      std::lock_guard<std::mutex> g(mu);
+      if (!failed.exchange(true)) {
+        msg = ex.what();
+        st = ex.state;
+        se = e;
+      }
+    }
+  }
+  if (failed) {
+    physical_state_error ex(msg + " (element " + std::to_string(se) + ")", st);
+    throw ex;
+  }
+}
+
+// --------------------------------------------------------------- Jacobians
+
+// Structural rules (shared definition of the pattern):
+//   K11 volume blocks exist iff the flux depends on u at quadrature points;
+//   endpoint blocks exist for every u the endpoint flux depends on.
+struct Contrib {
+  int64_t row, col;
+};
+
+void pattern_line(const Ctx& c, int e, int dir, int line, int which, std::vector<Contrib>& out) {
+  const int64_t base = static_cast<int64_t>(e) * c.npe;
+  auto own = [&](int t) { return base + c.node_on_line(dir, line, t); };
+  const bool vol = which == LDG_K11 ? (c.has_inv || (c.second && c.vis_u)) : c.second;
+  if (which != LDG_K11 && !c.second) return;
+  for (int i = 0; i < c.np; ++i) {
+    if (vol)
+      for (int t = 0; t < c.np; ++t) out.push_back({own(i), own(t)});
+    for (int side = 0; side < 2; ++side) {
+      const size_t k = c.epi(e, dir, side, line);
+      const int ie = side ? c.p : 0;
+      const bool bd = c.ep_bc[k] >= 0;
+      const int64_t nbr = bd ? -1 : static_cast<int64_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
+      const int S = c.sign(e, dir, side);
+      if (which == LDG_K11) {
+        bool in = false, outn = false;
+        if (c.has_inv) {
+          in = true;
+          outn = !bd;
+        }
+        if (c.second) {
+          if (bd) {
+            in = in || c.vis_u || c.c11_bd != 0.0;
+          } else {
+            if (c.vis_u) {
+              if (S > 0) outn = true;
+              else in = true;
+            }
+            if (c.c11 != 0.0) in = outn = true;
+          }
+        }
+        if (in) out.push_back({own(i), own(ie)});
+        if (outn) out.push_back({own(i), nbr});
+      } else if (which == LDG_K12) {
+        if (bd || S <= 0) out.push_back({own(i), own(ie)});
+        else out.push_back({own(i), nbr});
+      } else {  // K21: u_hat
+        if (bd) continue;
+        if (S > 0) out.push_back({own(i), own(ie)});
+        else out.push_back({own(i), nbr});
+      }
+    }
+  }
+}
+
+void build_pattern(Ctx& c, int which, const std::vector<int>* subset) {
+  BlockMat& K = c.K[which];
+  K.nrows = static_cast<int64_t>(c.E) * c.npe;
+  K.br = which == LDG_K21 ? c.m * c.D : c.m;
+  K.bc = which == LDG_K12 ? c.m * c.D : c.m;
+  std::vector<std::vector<int64_t>> rows_of(c.E);
+  const int n = subset ? static_cast<int>(subset->size()) : c.E;
+  std::vector<char> active(c.E, subset ? 0 : 1);
+  if (subset)
+    for (int e : *subset) active[e] = 1;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int i = 0; i < n; ++i) {
+    const int e = subset ? (*subset)[i] : i;
+    std::vector<Contrib> v;
+    for (int dir = 0; dir < c.D; ++dir)
+      for (int line = 0; line < c.NL; ++line) pattern_line(c, e, dir, line, which, v);
+    std::sort(v.begin(), v.end(), [](const Contrib& a, const Contrib& b) {
+      return a.row != b.row ? a.row < b.row : a.col < b.col;
+    });
+    v.erase(std::unique(v.begin(), v.end(),
+                        [](const Contrib& a, const Contrib& b) { return a.row == b.row && a.col == b.col; }),
+            v.end());
+    std::vector<int64_t> flat;
+    flat.reserve(2 * v.size());
+    for (const auto& x : v) {
+      flat.push_back(x.row);
+      flat.push_back(x.col);
+    }
+    rows_of[e].swap(flat);
+  }
+  K.rowptr.assign(K.nrows + 1, 0);
+  for (int e = 0; e < c.E; ++e)
+    for (size_t k = 0; k < rows_of[e].size(); k += 2) K.rowptr[rows_of[e][k] + 1]++;
+  for (int64_t r = 0; r < K.nrows; ++r) K.rowptr[r + 1] += K.rowptr[r];
+  K.col.assign(K.rowptr[K.nrows], 0);
+  for (int e = 0; e < c.E; ++e) {
+    int64_t last = -1, pos = 0;
+    for (size_t k = 0; k < rows_of[e].size(); k += 2) {
+      const int64_t r = rows_of[e][k];
+      if (r != last) {
+        pos = K.rowptr[r];
+        last = r;
+      }
+      K.col[pos++] = rows_of[e][k + 1];
+    }
+  }
+  K.val.assign(K.col.size() * K.br * K.bc, 0.0);
+  K.built = true;
+}
+
+// Analytic Jacobian of one element's rows.  NU = m (u-derivative slots),
+// NQ = m*D (q-derivative slots).
+template <int NU, int NQ>
+void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
+  const int m = c.m, np = c.np, nq = c.nq, D = c.D, mD = m * D;
+  const int64_t base = static_cast<int64_t>(e) * c.npe;
+  LineData L;
+  using DU = Dual<NU>;
+  using DQ = Dual<NQ>;
+  auto addblk = [&](int which, int64_t row, int64_t col, const double* blk, double scale) {
+    BlockMat& K = c.K[which];
+    const int64_t pos = K.find(row, col);
+    if (pos < 0) throw std::logic_error("oracle: contribution outside the pattern");
+    double* v = &K.val[pos * K.br * K.bc];
+    for (int i = 0; i < K.br * K.bc; ++i) v[i] += scale * blk[i];
+  };
+  for (int dir = 0; dir < D; ++dir)
+    for (int line = 0; line < c.NL; ++line) {
+      gather_line(c, e, dir, line, U, Q, L);
+      auto own = [&](int t) { return base + c.node_on_line(dir, line, t); };
+      // ---------------- K11 / K12 volume: dB[i][t] = -sum_q w dphi_i phi_t dft/du
+      const bool vol11 = c.has_inv || (c.second && c.vis_u);
+      // v11[t][i][a][b] (a: residual comp, b: u comp); v12[t][i][a][b] (b: q comp)
+      std::vector<double> v11(static_cast<size_t>(np) * np * m * m, 0.0);
+      std::vector<double> v12(c.second ? static_cast<size_t>(np) * np * m * mD : 0, 0.0);
+      for (int q = 0; q < nq; ++q) {
+        double uq[MAXM] = {0}, qq[MAXM * MAXD] = {0};
+        for (int t = 0; t < np; ++t) {
+          const double ph = c.phi[t * nq + q];
+          for (int k = 0; k < m; ++k) uq[k] += ph * L.u[t][k];
+          if (c.second)
+            for (int k = 0; k < mD; ++k) qq[k] += ph * L.q[t][k];
+        }
+        const double* nvq = c.nv(e, dir, line, q);
+        double A[MAXM][MAXM * MAXD];
+        if (vol11) {
+          DU du[MAXM], dq[MAXM * MAXD], f[MAXM];
+          for (int k = 0; k < m; ++k) {
+            du[k] = DU(uq[k]);
+            du[k].d[k] = 1.0;
+          }
+          for (int k = 0; k < mD; ++k) dq[k] = DU(qq[k]);
+          flux_dot(c, du, dq, nvq, f);
+          for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) A[a][b] = f[a].d[b];
+          for (int i = 0; i < np; ++i) {
+            const double w = c.qw[q] * c.dphi[i * nq + q];
+            for (int t = 0; t < np; ++t) {
+              const double wt = w * c.phi[t * nq + q];
+              double* dst = &v11[((static_cast<size_t>(t) * np + i) * m) * m];
+              for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) dst[a * m + b] -= wt * A[a][b];
+            }
+          }
+        }
+        if (c.second) {
+          DQ du[MAXM], dq[MAXM * MAXD], f[MAXM];
+          for (int k = 0; k < m; ++k) du[k] = DQ(uq[k]);
+          for (int k = 0; k < mD; ++k) {
+            dq[k] = DQ(qq[k]);
+            dq[k].d[k] = 1.0;
+          }
+          vflux_dot(c, du, dq, nvq, f);
+          for (int i = 0; i < np; ++i) {
+            const double w = c.qw[q] * c.dphi[i * nq + q];
+            for (int t = 0; t < np; ++t) {
+              const double wt = w * c.phi[t * nq + q];
+              double* dst = &v12[((static_cast<size_t>(t) * np + i) * m) * mD];
+              for (int a = 0; a < m; ++a)
+                for (int b = 0; b < mD; ++b) dst[a * mD + b] -= wt * f[a].d[b];
+            }
+          }
+        }
+      }
+      // ---------------- endpoints
+      // e11[side][which-col 0=own end,1=nbr][a][b], e12 likewise
+      double e11[2][2][MAXM * MAXM] = {}, e12[2][2][MAXM * MAXM * MAXD] = {};
+      bool has11[2][2] = {}, has12[2][2] = {};
+      for (int side = 0; side < 2; ++side) {
+        const int ie = side ? c.p : 0;
+        const double* n = c.ne(e, dir, side, line);
+        const int S = c.sign(e, dir, side);
+        const bool bd = L.bc[side] != nullptr;
+        // d/du_in and d/du_out with q fixed
+        for (int pass = 0; pass < (bd ? 1 : 2); ++pass) {
+          DU ui[MAXM], uo[MAXM], qi[MAXM * MAXD], qo[MAXM * MAXD], f[MAXM];
+          for (int k = 0; k < m; ++k) {
+            ui[k] = DU(L.u[ie][k]);
+            uo[k] = DU(bd ? 0.0 : L.uo[side][k]);
+            if (pass == 0) ui[k].d[k] = 1.0;
+            else uo[k].d[k] = 1.0;
+          }
+          for (int k = 0; k < mD; ++k) {
+            qi[k] = DU(c.second ? L.q[ie][k] : 0.0);
+            qo[k] = DU(c.second && !bd ? L.qo[side][k] : 0.0);
+          }
+          endpoint_flux<DU>(c, ui, qi, uo, qo, L.bc[side], n, S, f);
+          for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) e11[side][pass][a * m + b] = f[a].d[b];
+          has11[side][pass] = true;
+        }
+        if (c.second) {
+          const int pass = (bd || S <= 0) ? 0 : 1;
+          DQ ui[MAXM], uo[MAXM], qi[MAXM * MAXD], qo[MAXM * MAXD], f[MAXM];
+          for (int k = 0; k < m; ++k) {
+            ui[k] = DQ(L.u[ie][k]);
+            uo[k] = DQ(bd ? 0.0 : L.uo[side][k]);
+          }
+          for (int k = 0; k < mD; ++k) {
+            qi[k] = DQ(L.q[ie][k]);
+            qo[k] = DQ(bd ? 0.0 : L.qo[side][k]);
+            if (pass == 0) qi[k].d[k] = 1.0;
+            else qo[k].d[k] = 1.0;
+          }
+          endpoint_flux<DQ>(c, ui, qi, uo, qo, L.bc[side], n, S, f);
+          for (int a = 0; a < m; ++a)
+            for (int b = 0; b < mD; ++b) e12[side][pass][a * mD + b] = f[a].d[b];
+          has12[side][pass] = true;
+        }
+      }
+      // ---------------- apply M^-1 along i and scatter into rows
+      // K11: columns own(t) (volume + own-end terms) and nbr(side)
+      std::vector<Contrib> pat;
+      pattern_line(c, e, dir, line, LDG_K11, pat);
+      auto has_pat = [&](const std::vector<Contrib>& pv, int64_t row, int64_t col) {
+        for (const auto& x : pv)
+          if (x.row == row && x.col == col) return true;
+        return false;
+      };
+      {
+        // columns: t in [0,np) own nodes, then side 0/1 neighbours
+        for (int cidx = 0; cidx < np + 2; ++cidx) {
+          double col[MAXNP][MAXM * MAXM];
+          for (int i = 0; i < np; ++i)
+            for (int k = 0; k < m * m; ++k) col[i][k] = 0.0;
+          int64_t gcol;
+          if (cidx < np) {
+            gcol = own(cidx);
+            for (int i = 0; i < np; ++i)
+              for (int k = 0; k < m * m; ++k)
+                col[i][k] = v11[((static_cast<size_t>(cidx) * np + i) * m) * m + k];
+            for (int side = 0; side < 2; ++side) {
+              const int ie = side ? c.p : 0;
+              if (ie == cidx && has11[side][0])
+                for (int k = 0; k < m * m; ++k) col[ie][k] += e11[side][0][k];
+            }
+          } else {
+            const int side = cidx - np;
+            if (L.bc[side] || !has11[side][1]) continue;
+            const size_t k = c.epi(e, dir, side, line);
+            gcol = static_cast<int64_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
+            const int ie = side ? c.p : 0;
+            for (int kk = 0; kk < m * m; ++kk) col[ie][kk] = e11[side][1][kk];
+          }
+          for (int k = 0; k < m * m; ++k) c.mass_solve(&col[0][k], MAXM * MAXM);
+          for (int i = 0; i < np; ++i) {
+            if (!has_pat(pat, own(i), gcol)) continue;
+            addblk(LDG_K11, own(i), gcol, col[i], -c.invJ[own(i)]);
+          }
+        }
+      }
+      if (c.second) {
+        std::vector<Contrib> p12;
+        pattern_line(c, e, dir, line, LDG_K12, p12);
+        for (int cidx = 0; cidx < np + 2; ++cidx) {
+          std::vector<double> col(static_cast<size_t>(np) * m * mD, 0.0);
+          int64_t gcol;
+          if (cidx < np) {
+            gcol = own(cidx);
+            for (int i = 0; i < np; ++i)
+              for (int k = 0; k < m * mD; ++k)
+                col[i * m * mD + k] = v12[((static_cast<size_t>(cidx) * np + i) * m) * mD + k];
+            for (int side = 0; side < 2; ++side) {
+              const int ie = side ? c.p : 0;
+              if (ie == cidx && has12[side][0])
+                for (int k = 0; k < m * mD; ++k) col[ie * m * mD + k] += e12[side][0][k];
+            }
+          } else {
+            const int side = cidx - np;
+            if (L.bc[side] || !has12[side][1]) continue;
+            const size_t k = c.epi(e, dir, side, line);
+            gcol = static_cast<int64_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
+            const int ie = side ? c.p : 0;
+            for (int kk = 0; kk < m * mD; ++kk) col[ie * m * mD + kk] = e12[side][1][kk];
+          }
+          for (int k = 0; k < m * mD; ++k) c.mass_solve(&col[k], m * mD);
+          for (int i = 0; i < np; ++i) {
+            if (!has_pat(p12, own(i), gcol)) continue;
+            addblk(LDG_K12, own(i), gcol, &col[i * m * mD], -c.invJ[own(i)]);
+          }
+        }
+        // K21 (U-independent): D scalars per node pair, expanded to the
+        // component-diagonal mD x m block on storage.
+        std::vector<Contrib> p21;
+        pattern_line(c, e, dir, line, LDG_K21, p21);
+        for (int cidx = 0; cidx < np + 2; ++cidx) {
+          double col[MAXNP][MAXD] = {};
+          int64_t gcol;
+          if (cidx < np) {
+            gcol = own(cidx);
+            for (int q = 0; q < nq; ++q) {
+              const double* nvq = c.nv(e, dir, line, q);
+              const double ph = c.phi[cidx * nq + q];
+              for (int i = 0; i < np; ++i) {
+                const double w = c.qw[q] * c.dphi[i * nq + q];
+                for (int dd = 0; dd < D; ++dd) col[i][dd] -= w * (ph * nvq[dd]);
+              }
+            }
+            for (int side = 0; side < 2; ++side) {
+              const int ie = side ? c.p : 0;
+              if (ie == cidx && !L.bc[side] && c.sign(e, dir, side) > 0) {
+                const double* n = c.ne(e, dir, side, line);
+                for (int dd = 0; dd < D; ++dd) col[ie][dd] += n[dd];
+              }
+            }
+          } else {
+            const int side = cidx - np;
+            if (L.bc[side] || c.sign(e, dir, side) > 0) continue;
+            const size_t k = c.epi(e, dir, side, line);
+            gcol = static_cast<int64_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
+            const int ie = side ? c.p : 0;
+            const double* n = c.ne(e, dir, side, line);
+            for (int dd = 0; dd < D; ++dd) col[ie][dd] = n[dd];
+          }
+          for (int dd = 0; dd < D; ++dd) c.mass_solve(&col[0][dd], MAXD);
+          for (int i = 0; i < np; ++i) {
+            if (!has_pat(p21, own(i), gcol)) continue;
+            double blk[MAXM * MAXD * MAXM] = {};
+            for (int k = 0; k < m; ++k)
+              for (int dd = 0; dd < D; ++dd) blk[(k * D + dd) * m + k] = col[i][dd];
+            addblk(LDG_K21, own(i), gcol, blk, c.invJ[own(i)]);
+          }
+        }
+      }
+    }
+}
+
+using JacFn = void (*)(Ctx&, int, const double*, const double*);
+JacFn pick_jac(int m, int D) {
+  if (m == 1 && D == 2) return elem_jacobian<1, 2>;
+  if (m == 1 && D == 3) return elem_jacobian<1, 3>;
+  if (m == 4 && D == 2) return elem_jacobian<4, 8>;
+  if (m == 5 && D == 3) return elem_jacobian<5, 15>;
+  throw std::runtime_error("oracle: unsupported (m, D) for the Jacobian");
+}
+
+}  // namespace
+
+// -------------------------------------------------------------- public ops
+
+void residual(const Ctx& c, const double* U, const double* Q, double* R,
+              const std::vector<int>* subset = nullptr) {
+  for_elems(c, subset, [&](int e) { elem_residual(c, e, U, Q, R); });
+}
+void gradient(const Ctx& c, const double* U, double* Q, const std::vector<int>* subset = nullptr) {
+  for_elems(c, subset, [&](int e) { elem_gradient(c, e, U, Q); });
+}
+
+}  // namespace ora
+
+// ===================================================================== C-ABI
+using namespace ora;
+
+struct lo_ctx {
+  Ctx c;
+};
+
+namespace {
+thread_local std::string g_err;
+thread_local std::vector<double> g_state;
+thread_local int g_elem = -1;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return LDG_OK;
+  } catch (const physical_state_error& ex) {
+    g_err = ex.what();
+    g_state = ex.state;
+    return LDG_ERR_PHYSICAL_STATE;
+  } catch (const std::invalid_argument& ex) {
+    g_err = ex.what();
+    return LDG_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return LDG_ERR_CONFIG;
+  }
+}
+
+std::vector<int> subset_of(const int32_t* elems, int32_t n) {
+  return std::vector<int>(elems, elems + n);
+}
+}  // namespace
+
+extern "C" {
+
+const char* lo_last_error(void) { return g_err.c_str(); }
+int lo_last_error_state(double* state, int32_t* n) {
+  *n = static_cast<int32_t>(g_state.size());
+  if (state) std::copy(g_state.begin(), g_state.end(), state);
+  return LDG_OK;
+}
+void lo_set_threads(int32_t n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+int32_t lo_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+int lo_create(const ldg_setup* s, const ldg_physics* ph, lo_ctx** out) {
+  return guarded([&] {
+    auto x = std::make_unique<lo_ctx>();
+    Ctx& c = x->c;
+    c.D = s->dim;
+    c.p = s->p;
+    c.np = c.p + 1;
+    c.nq = s->n_quad;
+    c.npe = c.D == 2 ? c.np * c.np : c.np * c.np * c.np;
+    c.NL = c.D == 2 ? c.np : c.np * c.np;
+    c.E = s->n_elems;
+    if (c.np > MAXNP || c.nq > MAXNQ) throw std::invalid_argument("oracle: p too large");
+    c.kind = ph->kind;
+    c.riemann = ph->riemann;
+    c.gas.gamma = ph->gamma;
+    c.gas.mu = ph->mu;
+    c.gas.prandtl = ph->prandtl;
+    c.c11 = ph->c11;
+    c.c11_bd = ph->c11_bd;
+    if (ph->c22 != 0.0) throw std::runtime_error("residual_primal requires C22 = 0 (SPEC.md:250-252)");
+    c.m = c.kind == LDG_POISSON ? 1 : c.D + 2;
+    c.has_inv = c.kind != LDG_POISSON;
+    c.second = c.kind == LDG_POISSON || (c.kind == LDG_NAVIER_STOKES && c.gas.mu != 0.0);
+    c.vis_u = c.kind == LDG_NAVIER_STOKES;
+    const int np = c.np, nq = c.nq;
+    c.qw.assign(s->quad_weights, s->quad_weights + nq);
+    c.phi.assign(s->phi_at_quad, s->phi_at_quad + np * nq);
+    c.dphi.assign(s->dphi_at_quad, s->dphi_at_quad + np * nq);
+    c.L.assign(s->mass, s->mass + np * np);
+    for (int k = 0; k < np; ++k) {  // lower Cholesky, in place
+      double d = c.L[k * np + k];
+      for (int j = 0; j < k; ++j) d -= c.L[k * np + j] * c.L[k * np + j];
+      if (!(d > 0.0)) throw std::runtime_error("oracle: mass matrix not SPD");
+      d = std::sqrt(d);
+      c.L[k * np + k] = d;
+      for (int i = k + 1; i < np; ++i) {
+        double v = c.L[i * np + k];
+        for (int j = 0; j < k; ++j) v -= c.L[i * np + j] * c.L[k * np + j];
+        c.L[i * np + k] = v / d;
+      }
+      for (int j = k + 1; j < np; ++j) c.L[k * np + j] = 0.0;
+    }
+    const size_t nn = static_cast<size_t>(c.E) * c.npe;
+    c.jac.assign(s->jac_at_nodes, s->jac_at_nodes + nn);
+    c.invJ.resize(nn);
+    for (size_t i = 0; i < nn; ++i) c.invJ[i] = 1.0 / c.jac[i];
+    c.nvec.assign(s->nvec_quad, s->nvec_quad + static_cast<size_t>(c.E) * c.D * c.NL * nq * c.D);
+    c.nend.assign(s->normal_end, s->normal_end + static_cast<size_t>(c.E) * c.D * 2 * c.NL * c.D);
+    if (c.second) {
+      if (!s->switch_plus) throw std::runtime_error("second-order physics needs switches");
+      c.sw.assign(s->switch_plus, s->switch_plus + static_cast<size_t>(c.E) * c.D);
+    }
+    build_endpoints(c, *s, *ph);
+    *out = x.release();
+  });
+}
+
+void lo_destroy(lo_ctx* x) { delete x; }
+int32_t lo_components(const lo_ctx* x) { return x->c.m; }
+
+int lo_set_source(lo_ctx* x, const double* S) {
+  return guarded([&] {
+    const size_t n = static_cast<size_t>(x->c.E) * x->c.npe * x->c.m;
+    if (S) x->c.source.assign(S, S + n);
+    else x->c.source.clear();
+  });
+}
+
+int lo_gradient(lo_ctx* x, const double* U, double t, double* Q) {
+  (void)t;
+  return guarded([&] { gradient(x->c, U, Q); });
+}
+
+int lo_residual_uq(lo_ctx* x, const double* U, const double* Q, double t, double* R) {
+  (void)t;
+  return guarded([&] { residual(x->c, U, Q, R); });
+}
+
+// Residual, optionally restricted to a subset of elements (rows of other
+// elements are left untouched).  Second-order physics computes Q = D(U)
+// first (on the needed elements plus their neighbours: here, all).
+int lo_residual(lo_ctx* x, const double* U, double t, double* R, double* Qout,
+                const int32_t* elems, int32_t n_sub) {
+  (void)t;
+  return guarded([&] {
+    Ctx& c = x->c;
+    std::vector<int> sub;
+    const std::vector<int>* sp = nullptr;
+    if (elems) {
+      sub = subset_of(elems, n_sub);
+      sp = &sub;
+    }
+    if (c.second) {
+      std::vector<double> Qv;
+      double* Q = Qout;
+      if (!Q) {
+        Qv.assign(static_cast<size_t>(c.E) * c.npe * c.m * c.D, 0.0);
+        Q = Qv.data();
+      }
+      gradient(c, U, Q);
+      residual(c, U, Q, R, sp);
+    } else {
+      residual(c, U, nullptr, R, sp);
+    }
+  });
+}
+
+// Analytic assembly (mode 0) of K11 (+K12, K21 for second-order physics),
+// optionally only for the rows of a subset of elements.
+int lo_assemble(lo_ctx* x, const double* U, double t, const int32_t* elems, int32_t n_sub) {
+  (void)t;
+  return guarded([&] {
+    Ctx& c = x->c;
+    std::vector<int> sub;
+    const std::vector<int>* sp = nullptr;
+    if (elems) {
+      sub = subset_of(elems, n_sub);
+      sp = &sub;
+    }
+    const int nm = c.second ? 3 : 1;
+    // The pattern depends only on the mesh: build it once for full assemblies
+    // (values are re-zeroed), rebuild for element subsets.
+    for (int w = 0; w < nm; ++w) {
+      if (sp || !c.K[w].built || c.K[w].subset) {
+        build_pattern(c, w, sp);
+        c.K[w].subset = sp != nullptr;
+      } else {
+        std::fill(c.K[w].val.begin(), c.K[w].val.end(), 0.0);
+      }
+    }
+    std::vector<double> Qv;
+    const double* Q = nullptr;
+    if (c.second) {
+      Qv.assign(static_cast<size_t>(c.E) * c.npe * c.m * c.D, 0.0);
+      gradient(c, U, Qv.data());
+      Q = Qv.data();
+    }
+    JacFn f = pick_jac(c.m, c.D);
+    for_elems(c, sp, [&](int e) { f(c, e, U, Q); });
+  });
+}
+
+// Assembly from an explicit Q (K11 and K12 at (U,Q)); for FD comparisons.
+int lo_assemble_uq(lo_ctx* x, const double* U, const double* Q) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    const int nm = c.second ? 3 : 1;
+    for (int w = 0; w < nm; ++w) {
+      build_pattern(c, w, nullptr);
+      c.K[w].subset = false;
+    }
+    JacFn f = pick_jac(c.m, c.D);
+    for_elems(c, nullptr, [&](int e) { f(c, e, U, Q); });
+  });
+}
+
+int lo_pattern_info(const lo_ctx* x, int32_t which, int64_t* nnzb, int32_t* br, int32_t* bc) {
+  return guarded([&] {
+    const BlockMat& K = x->c.K[which];
+    if (!K.built) throw std::runtime_error("oracle: matrix not assembled");
+    *nnzb = static_cast<int64_t>(K.col.size());
+    *br = K.br;
+    *bc = K.bc;
+  });
+}
+
+int lo_export_blocks(const lo_ctx* x, int32_t which, int64_t* rows, int64_t* cols, double* vals) {
+  return guarded([&] {
+    const BlockMat& K = x->c.K[which];
+    if (!K.built) throw std::runtime_error("oracle: matrix not assembled");
+    for (int64_t r = 0; r < K.nrows; ++r)
+      for (int64_t k = K.rowptr[r]; k < K.rowptr[r + 1]; ++k) {
+        if (rows) rows[k] = r;
+        if (cols) cols[k] = K.col[k];
+      }
+    if (vals) std::copy(K.val.begin(), K.val.end(), vals);
+  });
+}
+
+// Scalar compressed-column export: colptr (ncols+1),
+// rowidx/vals (nnz).  Component-diagonal structure of K21 is kept dense per
+// block (zeros included), as for all blocks.
+int lo_export_csc(const lo_ctx* x, int32_t which, int64_t* colptr, int64_t* rowidx, double* vals,
+                  int64_t* nnz_out) {
+  return guarded([&] {
+    const Ctx& c = x->c;
+    const BlockMat& K = c.K[which];
+    if (!K.built) throw std::runtime_error("oracle: matrix not assembled");
+    const int64_t ncols = K.nrows * K.bc;
+    const int64_t nnz = static_cast<int64_t>(K.col.size()) * K.br * K.bc;
+    if (nnz_out) *nnz_out = nnz;
+    if (!colptr) return;
+    std::fill(colptr, colptr + ncols + 1, 0);
+    for (size_t k = 0; k < K.col.size(); ++k)
+      for (int b = 0; b < K.bc; ++b) colptr[K.col[k] * K.bc + b + 1] += K.br;
+    for (int64_t j = 0; j < ncols; ++j) colptr[j + 1] += colptr[j];
+    std::vector<int64_t> fill(colptr, colptr + ncols);
+    for (int64_t r = 0; r < K.nrows; ++r)  // rows ascending -> sorted within columns
+      for (int a = 0; a < K.br; ++a)
+        for (int64_t k = K.rowptr[r]; k < K.rowptr[r + 1]; ++k)
+          for (int b = 0; b < K.bc; ++b) {
+            const int64_t j = K.col[k] * K.bc + b;
+            const int64_t pos = fill[j]++;
+            rowidx[pos] = r * K.br + a;
+            vals[pos] = K.val[(k * K.br + a) * K.bc + b];
+          }
+  });
+}
+
+int lo_spmv(const lo_ctx* x, int32_t which, const double* v, double* y) {
+  return guarded([&] {
+    const BlockMat& K = x->c.K[which];
+    if (!K.built) throw std::runtime_error("oracle: matrix not assembled");
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < K.nrows; ++r) {
+      double acc[MAXM * MAXD] = {0};
+      for (int64_t k = K.rowptr[r]; k < K.rowptr[r + 1]; ++k) {
+        const double* blk = &K.val[k * K.br * K.bc];
+        const double* xv = v + K.col[k] * K.bc;
+        for (int a = 0; a < K.br; ++a)
+          for (int b = 0; b < K.bc; ++b) acc[a] += blk[a * K.bc + b] * xv[b];
+      }
+      for (int a = 0; a < K.br; ++a) y[r * K.br + a] = acc[a];
+    }
+  });
+}
+
+// y = v - alpha_dt (K11 v + K12 (K21 v))
+int lo_split_matvec(const lo_ctx* x, double adt, const double* v, double* y) {
+  return guarded([&] {
+    const Ctx& c = x->c;
+    const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
+    std::vector<double> a(n), w, b;
+    if (lo_spmv(x, LDG_K11, v, a.data()) != LDG_OK) throw std::runtime_error(g_err);
+    if (c.second) {
+      w.assign(n * c.D, 0.0);
+      b.assign(n, 0.0);
+      if (lo_spmv(x, LDG_K21, v, w.data()) != LDG_OK) throw std::runtime_error(g_err);
+      if (lo_spmv(x, LDG_K12, w.data(), b.data()) != LDG_OK) throw std::runtime_error(g_err);
+      for (size_t i = 0; i < n; ++i) a[i] = a[i] + b[i];
+    }
+    for (size_t i = 0; i < n; ++i) y[i] = v[i] - adt * a[i];
+  });
+}
+
+// Central-difference Jacobian of one matrix, dense (for <= a few hundred
+// unknowns): K11 via R(U +- h e_j, Q), K12 via R(U, Q +- h e_j), K21 via
+// D(U +- h e_j); step h = 1e-7 (1 + |x_j|).  Output row-major
+// dense nrows x ncols scalars.
+int lo_fd_dense(lo_ctx* x, int32_t which, const double* U, const double* Q, double* out) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    const size_t nu = static_cast<size_t>(c.E) * c.npe * c.m;
+    const size_t nqd = nu * c.D;
+    const size_t ncols = which == LDG_K12 ? nqd : nu;
+    const size_t nrows = which == LDG_K21 ? nqd : nu;
+    std::vector<double> Up(U, U + nu), Qp;
+    if (Q) Qp.assign(Q, Q + nqd);
+    std::vector<double> rp(nrows), rm(nrows);
+    auto eval = [&](double* r) {
+      if (which == LDG_K21) gradient(c, Up.data(), r);
+      else residual(c, Up.data(), c.second ? Qp.data() : nullptr, r);
+    };
+    for (size_t j = 0; j < ncols; ++j) {
+      double* xj = which == LDG_K12 ? &Qp[j] : &Up[j];
+      const double x0 = *xj, h = 1e-7 * (1.0 + std::abs(x0));
+      *xj = x0 + h;
+      eval(rp.data());
+      *xj = x0 - h;
+      eval(rm.data());
+      *xj = x0;
+      for (size_t i = 0; i < nrows; ++i) out[i * ncols + j] = (rp[i] - rm[i]) / (2.0 * h);
+    }
+  });
+}
+
+}  // extern "C"

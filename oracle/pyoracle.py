@@ -1,0 +1,209 @@
+"""TEST INFRASTRUCTURE ONLY -- Python handle on the CPU oracle
+(oracle/liblinedg_oracle.so, built from oracle/oracle.cpp).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+import this module.  It is the parity checker, never the thing measured or
+shipped.  The oracle restates the reference's hot-path operations whose
+sources are absent from the reference tree (see oracle/oracle.cpp header);
+it is pinned by the SPEC.md known-answer tests and the Table-1 integer
+goldens (tests/test_oracle_kats.py) and, for the setup inputs, by the
+reference's own basis/mesh/mapping sources compiled against an Eigen shim
+(oracle/ref_build, tests/test_setup_vs_reference.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_lp = C.POINTER(C.c_int64)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(_HERE, "liblinedg_oracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"oracle library not built: {path} (run make)")
+        L = C.CDLL(path)
+        vp = C.c_void_p
+        L.lo_last_error.restype = C.c_char_p
+        L.lo_last_error_state.argtypes = [_dp, C.POINTER(C.c_int32)]
+        L.lo_set_threads.argtypes = [C.c_int32]
+        L.lo_set_threads.restype = None
+        L.lo_max_threads.restype = C.c_int32
+        L.lo_create.argtypes = [vp, vp, C.POINTER(vp)]
+        L.lo_destroy.argtypes = [vp]
+        L.lo_destroy.restype = None
+        L.lo_components.argtypes = [vp]
+        L.lo_set_source.argtypes = [vp, _dp]
+        L.lo_gradient.argtypes = [vp, _dp, C.c_double, _dp]
+        L.lo_residual_uq.argtypes = [vp, _dp, _dp, C.c_double, _dp]
+        L.lo_residual.argtypes = [vp, _dp, C.c_double, _dp, _dp, _ip, C.c_int32]
+        L.lo_assemble.argtypes = [vp, _dp, C.c_double, _ip, C.c_int32]
+        L.lo_assemble_uq.argtypes = [vp, _dp, _dp]
+        L.lo_pattern_info.argtypes = [vp, C.c_int32, _lp, _ip, _ip]
+        L.lo_export_blocks.argtypes = [vp, C.c_int32, _lp, _lp, _dp]
+        L.lo_export_csc.argtypes = [vp, C.c_int32, _lp, _lp, _dp, _lp]
+        L.lo_spmv.argtypes = [vp, C.c_int32, _dp, _dp]
+        L.lo_split_matvec.argtypes = [vp, C.c_double, _dp, _dp]
+        L.lo_fd_dense.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
+        _lib = L
+    return _lib
+
+
+class OraclePhysicalStateError(RuntimeError):
+    def __init__(self, msg, state):
+        super().__init__(msg)
+        self.state = state
+
+
+def _d(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+class Oracle:
+    def __init__(self, case, physics):
+        self.L = lib()
+        self.case = case
+        self._ph = physics.to_c()
+        h = C.c_void_p()
+        self._check(self.L.lo_create(C.cast(case.setup_ptr, C.c_void_p), C.cast(C.pointer(self._ph), C.c_void_p),
+                                     C.byref(h)))
+        self.h = h
+        self.m = self.L.lo_components(h)
+        self.dim = case.dim
+        self.n_dofs = case.E * case.npe * self.m
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.lo_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st == 0:
+            return
+        msg = self.L.lo_last_error().decode()
+        if st == 1:
+            buf = np.zeros(8)
+            n = C.c_int32()
+            self.L.lo_last_error_state(_d(buf), C.byref(n))
+            raise OraclePhysicalStateError(msg, buf[: n.value].copy())
+        raise RuntimeError(f"oracle status {st}: {msg}")
+
+    @staticmethod
+    def set_threads(n: int):
+        lib().lo_set_threads(n)
+
+    @staticmethod
+    def max_threads() -> int:
+        return lib().lo_max_threads()
+
+    def set_source(self, S):
+        a = None if S is None else np.ascontiguousarray(S, dtype=np.float64)
+        self._check(self.L.lo_set_source(self.h, _d(a)))
+
+    def residual(self, U, t=0.0, elems: Optional[Sequence[int]] = None, want_q=False):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        R = np.zeros(self.n_dofs)
+        Q = np.zeros(self.n_dofs * self.dim) if want_q else None
+        el = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
+        self._check(self.L.lo_residual(self.h, _d(U), t, _d(R), _d(Q),
+                                       None if el is None else el.ctypes.data_as(_ip),
+                                       0 if el is None else len(el)))
+        return (R, Q) if want_q else R
+
+    def gradient(self, U, t=0.0):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        Q = np.zeros(self.n_dofs * self.dim)
+        self._check(self.L.lo_gradient(self.h, _d(U), t, _d(Q)))
+        return Q
+
+    def residual_uq(self, U, Q, t=0.0):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        R = np.zeros(self.n_dofs)
+        self._check(self.L.lo_residual_uq(self.h, _d(U), _d(Q), t, _d(R)))
+        return R
+
+    def assemble(self, U, t=0.0, elems: Optional[Sequence[int]] = None):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        el = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
+        self._check(self.L.lo_assemble(self.h, _d(U), t, None if el is None else el.ctypes.data_as(_ip),
+                                       0 if el is None else len(el)))
+
+    def assemble_uq(self, U, Q):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        self._check(self.L.lo_assemble_uq(self.h, _d(U), _d(Q)))
+
+    def export_blocks(self, which):
+        nnzb = C.c_int64()
+        br = C.c_int32()
+        bc = C.c_int32()
+        self._check(self.L.lo_pattern_info(self.h, which, C.byref(nnzb), C.byref(br), C.byref(bc)))
+        rows = np.empty(nnzb.value, dtype=np.int64)
+        cols = np.empty(nnzb.value, dtype=np.int64)
+        vals = np.empty(nnzb.value * br.value * bc.value)
+        self._check(self.L.lo_export_blocks(self.h, which, rows.ctypes.data_as(_lp), cols.ctypes.data_as(_lp),
+                                            _d(vals)))
+        return rows, cols, vals.reshape(nnzb.value, br.value, bc.value)
+
+    def export_csc(self, which):
+        nnz = C.c_int64()
+        self._check(self.L.lo_export_csc(self.h, which, None, None, None, C.byref(nnz)))
+        nnzb = C.c_int64()
+        br = C.c_int32()
+        bc = C.c_int32()
+        self._check(self.L.lo_pattern_info(self.h, which, C.byref(nnzb), C.byref(br), C.byref(bc)))
+        ncols = self.case.E * self.case.npe * bc.value
+        colptr = np.zeros(ncols + 1, dtype=np.int64)
+        rowidx = np.zeros(nnz.value, dtype=np.int64)
+        vals = np.zeros(nnz.value)
+        self._check(self.L.lo_export_csc(self.h, which, colptr.ctypes.data_as(_lp), rowidx.ctypes.data_as(_lp),
+                                         _d(vals), None))
+        return colptr, rowidx, vals
+
+    def spmv(self, which, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        ny = self.n_dofs * (self.dim if which == 2 else 1)
+        y = np.zeros(ny)
+        self._check(self.L.lo_spmv(self.h, which, _d(x), _d(y)))
+        return y
+
+    def split_matvec(self, adt, v):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        y = np.zeros(self.n_dofs)
+        self._check(self.L.lo_split_matvec(self.h, adt, _d(v), _d(y)))
+        return y
+
+    def fd_dense(self, which, U, Q=None):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        Qa = None if Q is None else np.ascontiguousarray(Q, dtype=np.float64)
+        nu = self.n_dofs
+        nrows = nu * self.dim if which == 2 else nu
+        ncols = nu * self.dim if which == 1 else nu
+        out = np.zeros(nrows * ncols)
+        self._check(self.L.lo_fd_dense(self.h, which, _d(U), _d(Qa), _d(out)))
+        return out.reshape(nrows, ncols)
+
+    def dense(self, which):
+        """Dense scalar matrix from the assembled blocks."""
+        rows, cols, vals = self.export_blocks(which)
+        br, bc = vals.shape[1], vals.shape[2]
+        nr = self.case.E * self.case.npe * br
+        nc = self.case.E * self.case.npe * bc
+        A = np.zeros((nr, nc))
+        for r, c, v in zip(rows, cols, vals):
+            A[r * br:(r + 1) * br, c * bc:(c + 1) * bc] += v
+        return A

@@ -1,0 +1,839 @@
+// ldg_capi.cu -- context, host-side table preparation and the C-ABI of the
+// B200 Line-DG hot path (include/linedg_b200.h).
+//
+// Host work done once per context (setup, never on the hot path):
+//   * fold the basis: M^-1 from the Cholesky factor of M (basis.cpp:185-189),
+//     dq = -M^-1 Phi' W, lifting columns M^-1[:,0], M^-1[:,p], line-block
+//     coefficients cc[i][t][q] = dq[i][q] phi[t][q];
+//   * derive, from the reference Face / elem_face / reversed tables
+//     (mesh.hpp:15-32), for every element line end the neighbour element and
+//     the affine map line -> neighbour node (c0 + c1 l1 + c2 l2), plus the
+//     LDG switch sign at that end (mesh.hpp:74-89);
+//   * re-lay the ElementMapping tables (mapping.hpp:19-33) per element in
+//     processing order, with 1/J precomputed, and upload.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ldg_ops.cuh"
+#include "linedg_b200.h"
+
+// ---------------------------------------------------------------- dispatch
+#define LDG_FOR_PH(X, D, P) X(D, P, 0, 0) X(D, P, 1, 0) X(D, P, 1, 1) X(D, P, 2, 0) X(D, P, 2, 1)
+#define LDG_FOR_ALL(X)                                                                    \
+  LDG_FOR_PH(X, 2, 1) LDG_FOR_PH(X, 2, 2) LDG_FOR_PH(X, 2, 3) LDG_FOR_PH(X, 2, 4)        \
+  LDG_FOR_PH(X, 3, 1) LDG_FOR_PH(X, 3, 2) LDG_FOR_PH(X, 3, 3) LDG_FOR_PH(X, 3, 4)
+LDG_FOR_ALL(LDG_DECLARE_OPS)
+
+namespace {
+
+const ldg::Ops* find_ops(int D, int P, int PH, int RI) {
+#define LDG_MATCH(d, p, ph, ri) \
+  if (D == d && P == p && PH == ph && RI == ri) return LDG_OPS_NAME(d, p, ph, ri)();
+  LDG_FOR_ALL(LDG_MATCH)
+#undef LDG_MATCH
+  return nullptr;
+}
+
+struct ldg_error : std::runtime_error {
+  int status;
+  ldg_error(int s, const std::string& w) : std::runtime_error(w), status(s) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw ldg_error(LDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+thread_local std::string g_create_err;
+
+}  // namespace
+
+struct ldg_ctx {
+  const ldg::Ops* ops = nullptr;
+  ldg::DevCtx dc;
+  int D = 2, p = 1, np = 2, nq = 2, npe = 4, NL = 2, m = 1, E = 0;
+  int kind = 0, riemann = 0, ph = 0;
+  bool second = false, has_inv = false, vis_u = false;
+  double c11 = 0.0, c11bd = 0.0;
+  std::vector<double> phi, dq, mi, cc;
+  std::vector<int32_t> order, inv_order;
+  std::vector<int2> conn;
+  // device
+  int32_t* d_order = nullptr;
+  double* d_metric = nullptr;
+  int2* d_conn = nullptr;
+  double* d_bcv = nullptr;
+  double* d_source = nullptr;
+  ldg::DevError* h_err = nullptr;
+  ldg::DevError* d_err = nullptr;
+  double* d_Q = nullptr;  // workspace Q = D(U)
+  double* d_w = nullptr;  // workspace w = K21 v
+  double* d_K11 = nullptr;
+  double* d_K12 = nullptr;
+  double* d_K21 = nullptr;
+  size_t n11 = 0, n12 = 0, n21 = 0;
+  bool jac_valid = false, k21_valid = false;
+  double* d_hu = nullptr;  // staging for host variants
+  double* d_hr = nullptr;
+  double* d_hx = nullptr;
+  double* d_hy = nullptr;
+  cudaStream_t stream = nullptr;
+  long long launches = 0;
+  bool sync_errors = true;
+  std::string err;
+  int err_elem = -1, err_node = -1;
+  double err_state[8] = {0};
+
+  size_t nU() const { return static_cast<size_t>(E) * npe * m; }
+  size_t nQ() const { return nU() * D; }
+
+  ~ldg_ctx() {
+    cudaFree(d_order);
+    cudaFree(d_metric);
+    cudaFree(d_conn);
+    cudaFree(d_bcv);
+    cudaFree(d_source);
+    cudaFree(d_Q);
+    cudaFree(d_w);
+    cudaFree(d_K11);
+    cudaFree(d_K12);
+    cudaFree(d_K21);
+    cudaFree(d_hu);
+    cudaFree(d_hr);
+    cudaFree(d_hx);
+    cudaFree(d_hy);
+    if (h_err) cudaFreeHost(h_err);
+  }
+
+  int node_on_line(int dir, int line, int t) const {
+    if (D == 2) return dir == 0 ? t + np * line : line + np * t;
+    const int l1 = line % np, l2 = line / np;
+    if (dir == 0) return t + np * l1 + np * np * l2;
+    if (dir == 1) return l1 + np * t + np * np * l2;
+    return l1 + np * l2 + np * np * t;
+  }
+  void line_of(int dir, int nd, int& line, int& pos) const {
+    const int x0 = nd % np, x1 = (nd / np) % np, x2 = nd / (np * np);
+    if (D == 2) {
+      line = dir == 0 ? x1 : x0;
+      pos = dir == 0 ? x0 : x1;
+    } else if (dir == 0) {
+      line = x1 + np * x2;
+      pos = x0;
+    } else if (dir == 1) {
+      line = x0 + np * x2;
+      pos = x1;
+    } else {
+      line = x0 + np * x1;
+      pos = x2;
+    }
+  }
+  const int2& cn(int k, int dir, int side) const {
+    return conn[(static_cast<size_t>(k) * D + dir) * 2 + side];
+  }
+  static int csign(const int2& c) { return (c.y >> 24) & 1 ? 1 : -1; }
+  int cnode(const int2& c, int line) const {
+    const int c0 = c.y & 0xff;
+    const int c1 = static_cast<int8_t>((c.y >> 8) & 0xff);
+    const int c2 = static_cast<int8_t>((c.y >> 16) & 0xff);
+    return c0 + c1 * (line % np) + c2 * (line / np);
+  }
+
+  // ---- structural pattern: which slots of a row exist
+  bool in_dep(int k, int dir, int side) const {
+    const int2& c = cn(k, dir, side);
+    const bool bd = c.x < 0;
+    if (has_inv) return true;
+    if (!second) return false;
+    if (bd) return vis_u || c11bd != 0.0;
+    return (vis_u && csign(c) <= 0) || c11 != 0.0;
+  }
+  bool out_dep(int k, int dir, int side) const {
+    const int2& c = cn(k, dir, side);
+    if (c.x < 0) return false;
+    if (has_inv) return true;
+    if (!second) return false;
+    return (vis_u && csign(c) > 0) || c11 != 0.0;
+  }
+  int nslots(int which) const { return which == LDG_K11 ? D * p + 1 + 2 * D : D * p + 1 + D; }
+  // Column node (reference numbering) of `slot` for row (k, nd); -1 if none;
+  // `present` = structural presence.
+  int64_t slot_col(int which, int k, int nd, int slot, bool& present) const {
+    const int64_t e = order[k];
+    const int x[3] = {nd % np, (nd / np) % np, nd / (np * np)};
+    const int st[3] = {1, np, np * np};
+    const int nin = D * p + 1;
+    present = false;
+    if (slot < nin) {
+      int dir, t;
+      if (slot < np) {
+        dir = 0;
+        t = slot;
+      } else {
+        const int z = slot - np;
+        dir = 1 + z / p;
+        t = z % p;
+        if (t >= x[dir]) ++t;
+      }
+      auto dep = [&](int d, int tt) {
+        if (which != LDG_K11) return second;  // K12, K21: volume terms always
+        const bool vol = has_inv || (second && vis_u);
+        return vol || (tt == 0 && in_dep(k, d, 0)) || (tt == p && in_dep(k, d, 1));
+      };
+      if (dir == 0 && t == x[0]) {  // self column: any direction
+        for (int d = 0; d < D; ++d) present = present || dep(d, x[d]);
+      } else {
+        present = dep(dir, t);
+      }
+      return e * npe + nd + static_cast<int64_t>(t - x[dir]) * st[dir];
+    }
+    int dir, side;
+    const int z = slot - nin;
+    if (which == LDG_K11) {
+      dir = z >> 1;
+      side = z & 1;
+    } else {
+      dir = z;
+      const bool plus1 = csign(cn(k, dir, 1)) > 0;
+      side = which == LDG_K12 ? (plus1 ? 1 : 0) : (plus1 ? 0 : 1);
+    }
+    const int2& c = cn(k, dir, side);
+    if (c.x < 0) return -1;
+    if (which == LDG_K11) present = out_dep(k, dir, side);
+    else present = second;
+    int line, pos;
+    line_of(dir, nd, line, pos);
+    return static_cast<int64_t>(c.x) * npe + cnode(c, line);
+  }
+};
+
+namespace {
+
+int face_of(int D, int dir, int side) {
+  if (D == 2) return dir == 0 ? (side ? 1 : 3) : (side ? 2 : 0);
+  return 2 * dir + side;
+}
+
+// 2-D reference face parameterisation (mesh.cpp:51-65).
+int face_param_2d(int p, int lf, int nd) {
+  const int np = p + 1, i = nd % np, j = nd / np;
+  switch (lf) {
+    case 0: return i;
+    case 1: return j;
+    case 2: return p - i;
+    default: return p - j;
+  }
+}
+int face_node_2d(int p, int lf, int k) {
+  const int np = p + 1;
+  switch (lf) {
+    case 0: return k;
+    case 1: return p + np * k;
+    case 2: return (p - k) + np * p;
+    default: return np * (p - k);
+  }
+}
+// 3-D: face (dir, side), parameters along the transverse axes in increasing order.
+int face_node_3d(int p, int lf, int a, int b) {
+  const int np = p + 1, dir = lf / 2, side = lf % 2;
+  const int st[3] = {1, np, np * np};
+  const int a1 = dir == 0 ? 1 : 0, a2 = dir == 2 ? 1 : 2;
+  return side * p * st[dir] + a * st[a1] + b * st[a2];
+}
+void dihedral(int o, int a, int b, int p, int& ao, int& bo) {
+  int x = a, y = b;
+  if (o & 1) std::swap(x, y);
+  ao = (o & 2) ? p - x : x;
+  bo = (o & 4) ? p - y : y;
+}
+
+// Cholesky-based inverse of the SPD mass matrix.
+std::vector<double> spd_inverse(const double* A, int n) {
+  std::vector<double> L(A, A + n * n);
+  for (int k = 0; k < n; ++k) {
+    double d = L[k * n + k];
+    for (int j = 0; j < k; ++j) d -= L[k * n + j] * L[k * n + j];
+    if (!(d > 0.0)) throw ldg_error(LDG_ERR_CONFIG, "mass matrix is not SPD");
+    d = std::sqrt(d);
+    L[k * n + k] = d;
+    for (int i = k + 1; i < n; ++i) {
+      double s = L[i * n + k];
+      for (int j = 0; j < k; ++j) s -= L[i * n + j] * L[k * n + j];
+      L[i * n + k] = s / d;
+    }
+  }
+  std::vector<double> inv(n * n, 0.0);
+  for (int c = 0; c < n; ++c) {
+    std::vector<double> y(n, 0.0), x(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      double s = i == c ? 1.0 : 0.0;
+      for (int j = 0; j < i; ++j) s -= L[i * n + j] * y[j];
+      y[i] = s / L[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int j = i + 1; j < n; ++j) s -= L[j * n + i] * x[j];
+      x[i] = s / L[i * n + i];
+    }
+    for (int i = 0; i < n; ++i) inv[i * n + c] = x[i];
+  }
+  return inv;
+}
+
+void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
+  std::map<int, int> tag2bc;
+  std::vector<double> bcv;
+  for (int i = 0; i < ph.n_bc; ++i) {
+    if (ph.bcs[i].kind != LDG_BC_DIRICHLET)
+      throw ldg_error(LDG_ERR_CONFIG, "unsupported boundary-condition kind");
+    tag2bc[ph.bcs[i].tag] = i;
+    for (int k = 0; k < c.m; ++k) bcv.push_back(ph.bcs[i].value[k]);
+  }
+  if (bcv.empty()) bcv.push_back(0.0);
+  const int F = 2 * c.D, P = c.p;
+  c.conn.assign(static_cast<size_t>(c.E) * c.D * 2, int2{0, 0});
+  for (int k = 0; k < c.E; ++k) {
+    const int e = c.order[k];
+    for (int dir = 0; dir < c.D; ++dir) {
+      int splus = 1;
+      if (c.second) splus = s.switch_plus[static_cast<size_t>(e) * c.D + dir] >= 0 ? 1 : -1;
+      for (int side = 0; side < 2; ++side) {
+        const int S = side ? splus : -splus;
+        const int flag = S > 0 ? (1 << 24) : 0;
+        const int lf = face_of(c.D, dir, side);
+        const int fid = s.elem_face[static_cast<size_t>(e) * F + lf];
+        if (fid < 0 || fid >= s.n_faces)
+          throw ldg_error(LDG_ERR_CONFIG, "elem_face entry out of range for element " + std::to_string(e));
+        int2& out = c.conn[(static_cast<size_t>(k) * c.D + dir) * 2 + side];
+        if (s.face_elem_r[fid] < 0) {
+          auto it = tag2bc.find(s.face_tag[fid]);
+          if (it == tag2bc.end())
+            throw ldg_error(LDG_ERR_CONFIG, "no boundary condition for boundary tag " +
+                                                std::to_string(s.face_tag[fid]));
+          out.x = -1 - it->second;
+          out.y = flag;
+          continue;
+        }
+        const bool is_left = s.face_elem_l[fid] == e && s.face_face_l[fid] == lf;
+        const int oe = is_left ? s.face_elem_r[fid] : s.face_elem_l[fid];
+        const int olf = is_left ? s.face_face_r[fid] : s.face_face_l[fid];
+        const int code = s.face_orient[fid];
+        auto nbr_node = [&](int line) {
+          const int own = c.node_on_line(dir, line, side ? P : 0);
+          if (c.D == 2) {
+            const int kk = face_param_2d(P, lf, own);
+            return face_node_2d(P, olf, code ? P - kk : kk);
+          }
+          const int a = line % c.np, b = line / c.np;
+          int na = -1, nb = -1;
+          if (is_left) {
+            dihedral(code, a, b, P, na, nb);
+          } else {
+            for (int xx = 0; xx <= P && na < 0; ++xx)
+              for (int yy = 0; yy <= P; ++yy) {
+                int ra, rb;
+                dihedral(code, xx, yy, P, ra, rb);
+                if (ra == a && rb == b) {
+                  na = xx;
+                  nb = yy;
+                  break;
+                }
+              }
+          }
+          return face_node_3d(P, olf, na, nb);
+        };
+        const int f00 = nbr_node(0);
+        const int c1 = c.np > 1 ? nbr_node(1) - f00 : 0;
+        const int c2 = c.D == 3 ? nbr_node(c.np) - f00 : 0;
+        for (int line = 0; line < c.NL; ++line) {
+          const int pred = f00 + c1 * (line % c.np) + c2 * (line / c.np);
+          if (pred != nbr_node(line)) throw ldg_error(LDG_ERR_CONFIG, "non-affine face node map");
+        }
+        if (f00 < 0 || f00 > 255 || c1 < -128 || c1 > 127 || c2 < -128 || c2 > 127)
+          throw ldg_error(LDG_ERR_CONFIG, "face node map out of packing range");
+        out.x = oe;
+        out.y = (f00 & 0xff) | ((c1 & 0xff) << 8) | ((c2 & 0xff) << 16) | flag;
+      }
+    }
+  }
+  ck(cudaMalloc(&c.d_bcv, bcv.size() * sizeof(double)), "cudaMalloc bcv");
+  ck(cudaMemcpy(c.d_bcv, bcv.data(), bcv.size() * sizeof(double), cudaMemcpyHostToDevice), "upload bcv");
+  ck(cudaMalloc(&c.d_conn, c.conn.size() * sizeof(int2)), "cudaMalloc conn");
+  ck(cudaMemcpy(c.d_conn, c.conn.data(), c.conn.size() * sizeof(int2), cudaMemcpyHostToDevice),
+     "upload conn");
+}
+
+template <class F>
+int guarded(ldg_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const ldg_error& ex) {
+    if (c) c->err = ex.what();
+    else g_create_err = ex.what();
+    return ex.status;
+  } catch (const std::exception& ex) {
+    if (c) c->err = ex.what();
+    else g_create_err = ex.what();
+    return LDG_ERR_INVALID_ARGUMENT;
+  }
+}
+
+// Completes a stream-ordered operation: surfaces launch errors and, when
+// error synchronisation is on, waits and reports a physical-state failure
+// recorded by any kernel (errors.hpp:10-18).
+int finish(ldg_ctx* c, cudaError_t launch) {
+  ck(launch, "kernel launch");
+  if (!c->sync_errors) return LDG_OK;
+  ck(cudaStreamSynchronize(c->stream), "stream synchronize");
+  if (c->h_err->flag) {
+    c->err_elem = c->h_err->elem;
+    c->err_node = c->h_err->node;
+    std::memcpy(c->err_state, c->h_err->state, sizeof(c->err_state));
+    c->err = "physical state error: non-positive density or pressure (element " +
+             std::to_string(c->err_elem) + ", node " + std::to_string(c->err_node) + ")";
+    c->h_err->flag = 0;
+    return LDG_ERR_PHYSICAL_STATE;
+  }
+  return LDG_OK;
+}
+
+double* ensure(double*& p, size_t n) {
+  if (!p) ck(cudaMalloc(&p, n * sizeof(double)), "cudaMalloc workspace");
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ldg_last_error(const ldg_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx** out) {
+  return guarded(nullptr, [&]() -> int {
+    if (!s || !ph || !out) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw ldg_error(LDG_ERR_CUDA, "no CUDA device: the B200 hot path has no CPU fallback");
+    auto c = std::make_unique<ldg_ctx>();
+    c->D = s->dim;
+    c->p = s->p;
+    c->np = c->p + 1;
+    c->nq = s->n_quad;
+    c->E = s->n_elems;
+    if (c->D != 2 && c->D != 3) throw ldg_error(LDG_ERR_CONFIG, "dim must be 2 or 3");
+    if (c->nq != (3 * c->p + 2) / 2) throw ldg_error(LDG_ERR_CONFIG, "n_quad must be (3p+2)/2");
+    if (ph->c22 != 0.0)
+      throw ldg_error(LDG_ERR_CONFIG, "residual_primal requires C22 = 0 (SPEC.md:250-252)");
+    c->npe = c->D == 2 ? c->np * c->np : c->np * c->np * c->np;
+    c->NL = c->D == 2 ? c->np : c->np * c->np;
+    c->kind = ph->kind;
+    c->riemann = ph->riemann;
+    c->m = ph->kind == LDG_POISSON ? 1 : c->D + 2;
+    c->has_inv = ph->kind != LDG_POISSON;
+    c->second = ph->kind == LDG_POISSON || (ph->kind == LDG_NAVIER_STOKES && ph->mu != 0.0);
+    c->vis_u = c->second && ph->kind == LDG_NAVIER_STOKES;
+    // Navier-Stokes with mu = 0 is the first-order Euler operator.
+    c->ph = ph->kind == LDG_POISSON ? ldg::PH_POISSON : (c->second ? ldg::PH_NS : ldg::PH_EULER);
+    const int ri = c->ph == ldg::PH_POISSON ? 0 : ph->riemann;
+    c->ops = find_ops(c->D, c->p, c->ph, ri);
+    if (!c->ops)
+      throw ldg_error(LDG_ERR_CONFIG, "no sm_100a kernel instantiation for dim=" + std::to_string(c->D) +
+                                          " p=" + std::to_string(c->p));
+    if (c->second && !s->switch_plus)
+      throw ldg_error(LDG_ERR_CONFIG, "second-order physics needs the LDG switch table");
+    c->c11 = ph->c11;
+    c->c11bd = ph->c11_bd;
+    c->stream = static_cast<cudaStream_t>(stream);
+
+    // Basis folding.
+    const int np = c->np, nq = c->nq;
+    const std::vector<double> minv = spd_inverse(s->mass, np);
+    c->phi.assign(s->phi_at_quad, s->phi_at_quad + np * nq);
+    c->dq.assign(np * nq, 0.0);
+    for (int i = 0; i < np; ++i)
+      for (int q = 0; q < nq; ++q) {
+        double acc = 0.0;
+        for (int kk = 0; kk < np; ++kk) acc += minv[i * np + kk] * s->dphi_at_quad[kk * nq + q];
+        c->dq[i * nq + q] = -acc * s->quad_weights[q];
+      }
+    c->mi.assign(np * 2, 0.0);
+    for (int i = 0; i < np; ++i) {
+      c->mi[i * 2 + 0] = minv[i * np + 0];
+      c->mi[i * 2 + 1] = minv[i * np + c->p];
+    }
+    c->cc.assign(np * np * nq, 0.0);
+    for (int i = 0; i < np; ++i)
+      for (int t = 0; t < np; ++t)
+        for (int q = 0; q < nq; ++q) c->cc[(i * np + t) * nq + q] = c->dq[i * nq + q] * c->phi[t * nq + q];
+
+    // Processing order (identity; the store is laid out in this order).
+    c->order.resize(c->E);
+    c->inv_order.resize(c->E);
+    for (int k = 0; k < c->E; ++k) c->order[k] = c->inv_order[k] = k;
+    ck(cudaMalloc(&c->d_order, c->E * sizeof(int32_t)), "cudaMalloc order");
+    ck(cudaMemcpy(c->d_order, c->order.data(), c->E * sizeof(int32_t), cudaMemcpyHostToDevice), "upload order");
+
+    build_connectivity(*c, *s, *ph);
+
+    // Metric in processing order, 1/J precomputed.
+    const ldg::Ops& o = *c->ops;
+    std::vector<double> met(static_cast<size_t>(c->E) * o.METP, 0.0);
+    for (int k = 0; k < c->E; ++k) {
+      const size_t e = c->order[k];
+      double* dst = &met[static_cast<size_t>(k) * o.METP];
+      std::memcpy(dst, s->nvec_quad + e * o.MET_NV, o.MET_NV * sizeof(double));
+      std::memcpy(dst + o.MET_NV, s->normal_end + e * o.MET_NE, o.MET_NE * sizeof(double));
+      for (int n = 0; n < c->npe; ++n) {
+        const double J = s->jac_at_nodes[e * c->npe + n];
+        if (!(J > 0.0)) throw ldg_error(LDG_ERR_CONFIG, "non-positive mapping Jacobian");
+        dst[o.MET_NV + o.MET_NE + n] = 1.0 / J;
+      }
+    }
+    ck(cudaMalloc(&c->d_metric, met.size() * sizeof(double)), "cudaMalloc metric");
+    ck(cudaMemcpy(c->d_metric, met.data(), met.size() * sizeof(double), cudaMemcpyHostToDevice),
+       "upload metric");
+    ck(cudaHostAlloc(&c->h_err, sizeof(ldg::DevError), cudaHostAllocMapped), "cudaHostAlloc error word");
+    std::memset(c->h_err, 0, sizeof(ldg::DevError));
+    ck(cudaHostGetDevicePointer(&c->d_err, c->h_err, 0), "map error word");
+
+    ldg::DevCtx& d = c->dc;
+    d.stream = c->stream;
+    d.phi = c->phi.data();
+    d.dq = c->dq.data();
+    d.mi = c->mi.data();
+    d.cc = c->cc.data();
+    d.pp.gamma = ph->gamma;
+    d.pp.mu = ph->mu;
+    d.pp.kap = ph->prandtl > 0.0 ? ph->mu * ph->gamma / ph->prandtl : 0.0;
+    d.pp.c11 = ph->c11;
+    d.pp.c11bd = ph->c11_bd * c->p * c->p;
+    d.order = c->d_order;
+    d.metric = c->d_metric;
+    d.conn = c->d_conn;
+    d.bcv = c->d_bcv;
+    d.source = nullptr;
+    d.err = c->d_err;
+    d.E = c->E;
+    d.launches = &c->launches;
+    *out = c.release();
+    return LDG_OK;
+  });
+}
+
+void ldg_destroy(ldg_ctx* c) { delete c; }
+
+int ldg_last_error_state(const ldg_ctx* c, int32_t* elem, int32_t* node, double* state) {
+  if (!c) return LDG_ERR_INVALID_ARGUMENT;
+  if (elem) *elem = c->err_elem;
+  if (node) *node = c->err_node;
+  if (state) std::memcpy(state, c->err_state, sizeof(double) * c->m);
+  return LDG_OK;
+}
+int ldg_components(const ldg_ctx* c) { return c->m; }
+int64_t ldg_num_dofs(const ldg_ctx* c) { return static_cast<int64_t>(c->nU()); }
+int64_t ldg_kernel_launches(const ldg_ctx* c) { return c->launches; }
+int64_t ldg_jacobian_bytes(const ldg_ctx* c) {
+  return static_cast<int64_t>((c->n11 + c->n12 + c->n21) * sizeof(double));
+}
+int ldg_set_sync_errors(ldg_ctx* c, int on) {
+  c->sync_errors = on != 0;
+  return LDG_OK;
+}
+int ldg_synchronize(ldg_ctx* c) {
+  return guarded(c, [&]() -> int {
+    const bool was = c->sync_errors;
+    c->sync_errors = true;
+    const int st = finish(c, cudaSuccess);
+    c->sync_errors = was;
+    return st;
+  });
+}
+
+int ldg_set_source(ldg_ctx* c, const double* S) {
+  return guarded(c, [&]() -> int {
+    if (!S) {
+      cudaFree(c->d_source);
+      c->d_source = nullptr;
+    } else {
+      ensure(c->d_source, c->nU());
+      ck(cudaMemcpy(c->d_source, S, c->nU() * sizeof(double), cudaMemcpyHostToDevice), "upload source");
+    }
+    c->dc.source = c->d_source;
+    return LDG_OK;
+  });
+}
+
+int ldg_gradient(ldg_ctx* c, const double* U, double t, double* Q) {
+  (void)t;
+  return guarded(c, [&]() -> int {
+    if (!c->second) throw ldg_error(LDG_ERR_CONFIG, "gradient_residual needs second-order physics");
+    return finish(c, c->ops->gradient(c->dc, U, Q));
+  });
+}
+
+int ldg_residual_uq(ldg_ctx* c, const double* U, const double* Q, double t, double* R) {
+  (void)t;
+  return guarded(c, [&]() -> int {
+    if (!c->second) return finish(c, c->ops->residual(c->dc, U, nullptr, R));
+    return finish(c, c->ops->residual(c->dc, U, Q, R));
+  });
+}
+
+int ldg_residual(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
+  (void)t;
+  return guarded(c, [&]() -> int {
+    if (!c->second) return finish(c, c->ops->residual(c->dc, U, nullptr, R));
+    double* q = Q ? Q : ensure(c->d_Q, c->nQ());
+    ck(c->ops->gradient(c->dc, U, q), "gradient launch");
+    return finish(c, c->ops->residual(c->dc, U, q, R));
+  });
+}
+
+int ldg_jacobian_assemble(ldg_ctx* c, const double* U, double t) {
+  (void)t;
+  return guarded(c, [&]() -> int {
+    const ldg::Ops& o = *c->ops;
+    if (o.jac_smem > 227 * 1024)
+      throw ldg_error(LDG_ERR_CONFIG, "Jacobian tile of this configuration exceeds shared memory (" +
+                                          std::to_string(o.jac_smem) + " B)");
+    const size_t rows = static_cast<size_t>(c->E) * c->npe;
+    if (!c->d_K11) {
+      c->n11 = rows * o.NS11 * o.B11;
+      ck(cudaMalloc(&c->d_K11, c->n11 * sizeof(double)), "cudaMalloc K11");
+      if (c->second) {
+        c->n12 = rows * o.NS12 * o.B12;
+        c->n21 = rows * o.NS12 * c->D;
+        ck(cudaMalloc(&c->d_K12, c->n12 * sizeof(double)), "cudaMalloc K12");
+        ck(cudaMalloc(&c->d_K21, c->n21 * sizeof(double)), "cudaMalloc K21");
+      }
+    }
+    const double* q = nullptr;
+    if (c->second) {
+      q = ensure(c->d_Q, c->nQ());
+      ck(o.gradient(c->dc, U, c->d_Q), "gradient launch");
+      // K21 is U- and t-independent: assembled once.
+      if (!c->k21_valid) {
+        ck(o.k21(c->dc, c->d_K21), "K21 launch");
+        c->k21_valid = true;
+      }
+    }
+    const int st = finish(c, o.jacobian(c->dc, U, q, c->d_K11, c->d_K12));
+    c->jac_valid = st == LDG_OK;
+    return st;
+  });
+}
+
+int ldg_pattern_info_get(const ldg_ctx* cc, int which, ldg_pattern_info* info) {
+  ldg_ctx* c = const_cast<ldg_ctx*>(cc);
+  return guarded(c, [&]() -> int {
+    if (which < 0 || which > 2 || (which != LDG_K11 && !c->second))
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "matrix not available for this physics");
+    int64_t nnzb = 0;
+    std::vector<int64_t> cols;
+    for (int k = 0; k < c->E; ++k)
+      for (int nd = 0; nd < c->npe; ++nd) {
+        cols.clear();
+        for (int sl = 0; sl < c->nslots(which); ++sl) {
+          bool pres;
+          const int64_t col = c->slot_col(which, k, nd, sl, pres);
+          if (pres && col >= 0) cols.push_back(col);
+        }
+        std::sort(cols.begin(), cols.end());
+        nnzb += std::unique(cols.begin(), cols.end()) - cols.begin();
+      }
+    info->n_rows = static_cast<int64_t>(c->E) * c->npe;
+    info->nnzb = nnzb;
+    info->block_rows = which == LDG_K21 ? c->m * c->D : c->m;
+    info->block_cols = which == LDG_K12 ? c->m * c->D : c->m;
+    return LDG_OK;
+  });
+}
+
+// Export of rows of the given reference elements (all if elems == NULL).
+int ldg_export_blocks_subset(ldg_ctx* c, int which, const int32_t* elems, int32_t n_elems,
+                             int64_t* rows, int64_t* cols, double* vals, int64_t* nnzb_out) {
+  return guarded(c, [&]() -> int {
+    if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+    if (which < 0 || which > 2 || (which != LDG_K11 && !c->second))
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "matrix not available for this physics");
+    const ldg::Ops& o = *c->ops;
+    const int NT = o.NT, NS = c->nslots(which);
+    const int bsz = which == LDG_K11 ? o.B11 : (which == LDG_K12 ? o.B12 : c->D);
+    const double* dsrc = which == LDG_K11 ? c->d_K11 : (which == LDG_K12 ? c->d_K12 : c->d_K21);
+    const int br = which == LDG_K21 ? c->m * c->D : c->m;
+    const int bc = which == LDG_K12 ? c->m * c->D : c->m;
+    const size_t per_elem = static_cast<size_t>(c->npe) * NS * bsz;
+    std::vector<int32_t> list;
+    if (elems) list.assign(elems, elems + n_elems);
+    else {
+      list.resize(c->E);
+      for (int e = 0; e < c->E; ++e) list[e] = e;
+    }
+    std::vector<double> chunk(per_elem);
+    int64_t pos = 0;
+    std::vector<std::pair<int64_t, int>> cl;
+    for (const int32_t e : list) {
+      if (e < 0 || e >= c->E) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "element out of range");
+      const int k = c->inv_order[e];
+      if (vals)
+        ck(cudaMemcpy(chunk.data(), dsrc + static_cast<size_t>(k) * per_elem, per_elem * sizeof(double),
+                      cudaMemcpyDeviceToHost),
+           "download Jacobian");
+      for (int nd = 0; nd < c->npe; ++nd) {
+        const int tile = nd / NT, r = nd % NT;
+        cl.clear();
+        for (int sl = 0; sl < NS; ++sl) {
+          bool pres;
+          const int64_t col = c->slot_col(which, k, nd, sl, pres);
+          if (pres && col >= 0) cl.emplace_back(col, sl);
+        }
+        std::sort(cl.begin(), cl.end());
+        for (size_t a = 0; a < cl.size();) {
+          size_t b = a;
+          while (b < cl.size() && cl[b].first == cl[a].first) ++b;
+          if (rows) rows[pos] = static_cast<int64_t>(e) * c->npe + nd;
+          if (cols) cols[pos] = cl[a].first;
+          if (vals) {
+            double* blk = vals + pos * br * bc;
+            std::fill(blk, blk + br * bc, 0.0);
+            for (size_t z = a; z < b; ++z) {
+              const int sl = cl[z].second;
+              auto at = [&](int ab) {
+                return chunk[((static_cast<size_t>(tile) * NS + sl) * bsz + ab) * NT + r];
+              };
+              if (which == LDG_K11) {
+                for (int ab = 0; ab < bsz; ++ab) blk[ab] += at(ab);
+              } else if (which == LDG_K12) {
+                const int a0 = c->ph == ldg::PH_NS ? 1 : 0;
+                for (int aa = 0; aa < o.R12; ++aa)
+                  for (int bb = 0; bb < o.MD; ++bb) blk[(aa + a0) * bc + bb] += at(aa * o.MD + bb);
+              } else {
+                for (int cc2 = 0; cc2 < c->m; ++cc2)
+                  for (int d = 0; d < c->D; ++d) blk[(cc2 * c->D + d) * bc + cc2] += at(d);
+              }
+            }
+          }
+          ++pos;
+          a = b;
+        }
+      }
+    }
+    if (nnzb_out) *nnzb_out = pos;
+    return LDG_OK;
+  });
+}
+
+int ldg_export_blocks(ldg_ctx* c, int which, int64_t* rows, int64_t* cols, double* vals) {
+  return ldg_export_blocks_subset(c, which, nullptr, 0, rows, cols, vals, nullptr);
+}
+
+int ldg_bsr_spmv(ldg_ctx* c, int which, const double* x, double* y) {
+  return guarded(c, [&]() -> int {
+    if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+    const ldg::Ops& o = *c->ops;
+    if (which == LDG_K11) return finish(c, o.spmv11(c->dc, c->d_K11, x, y));
+    if (!c->second) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "matrix not available for this physics");
+    if (which == LDG_K12) return finish(c, o.spmv12(c->dc, c->d_K12, x, y));
+    if (which == LDG_K21) return finish(c, o.spmv21(c->dc, c->d_K21, x, y));
+    throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "unknown matrix");
+  });
+}
+
+int ldg_split_matvec(ldg_ctx* c, double adt, const double* v, double* y) {
+  return guarded(c, [&]() -> int {
+    if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+    const ldg::Ops& o = *c->ops;
+    const double* w = nullptr;
+    if (c->second) {
+      ensure(c->d_w, c->nQ());
+      ck(o.spmv21(c->dc, c->d_K21, v, c->d_w), "K21 launch");
+      w = c->d_w;
+    }
+    return finish(c, o.split(c->dc, c->d_K11, c->d_K12, v, w, adt, y));
+  });
+}
+
+// ------------------------------------------------------------ host variants
+int ldg_residual_host(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
+  return guarded(c, [&]() -> int {
+    ensure(c->d_hu, c->nU());
+    ensure(c->d_hr, c->nU());
+    ck(cudaMemcpyAsync(c->d_hu, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
+    double* dq = c->second ? ensure(c->d_Q, c->nQ()) : nullptr;
+    const bool was = c->sync_errors;
+    c->sync_errors = false;
+    int st = ldg_residual(c, c->d_hu, t, c->d_hr, dq);
+    c->sync_errors = was;
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(R, c->d_hr, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H R");
+    if (Q && dq)
+      ck(cudaMemcpyAsync(Q, dq, c->nQ() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H Q");
+    const bool w2 = c->sync_errors;
+    c->sync_errors = true;
+    st = finish(c, cudaSuccess);
+    c->sync_errors = w2;
+    return st;
+  });
+}
+
+int ldg_jacobian_assemble_host(ldg_ctx* c, const double* U, double t) {
+  return guarded(c, [&]() -> int {
+    ensure(c->d_hu, c->nU());
+    ck(cudaMemcpyAsync(c->d_hu, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
+    const bool was = c->sync_errors;
+    c->sync_errors = true;
+    const int st = ldg_jacobian_assemble(c, c->d_hu, t);
+    c->sync_errors = was;
+    return st;
+  });
+}
+
+int ldg_bsr_spmv_host(ldg_ctx* c, int which, const double* x, double* y) {
+  return guarded(c, [&]() -> int {
+    const size_t nx = which == LDG_K12 ? c->nQ() : c->nU();
+    const size_t ny = which == LDG_K21 ? c->nQ() : c->nU();
+    double* dx = ensure(c->d_hx, c->nQ());
+    double* dy = ensure(c->d_hy, c->nQ());
+    ck(cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D x");
+    const bool was = c->sync_errors;
+    c->sync_errors = false;
+    int st = ldg_bsr_spmv(c, which, dx, dy);
+    c->sync_errors = was;
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H y");
+    const bool w2 = c->sync_errors;
+    c->sync_errors = true;
+    st = finish(c, cudaSuccess);
+    c->sync_errors = w2;
+    return st;
+  });
+}
+
+int ldg_split_matvec_host(ldg_ctx* c, double adt, const double* v, double* y) {
+  return guarded(c, [&]() -> int {
+    ensure(c->d_hu, c->nU());
+    ensure(c->d_hr, c->nU());
+    ck(cudaMemcpyAsync(c->d_hu, v, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D v");
+    const bool was = c->sync_errors;
+    c->sync_errors = false;
+    int st = ldg_split_matvec(c, adt, c->d_hu, c->d_hr);
+    c->sync_errors = was;
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(y, c->d_hr, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H y");
+    const bool w2 = c->sync_errors;
+    c->sync_errors = true;
+    st = finish(c, cudaSuccess);
+    c->sync_errors = w2;
+    return st;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,349 @@
+// ldg_device.cuh -- compile-time configuration, device forward-mode scalar
+// and point physics for the sm_100a Line-DG kernels.
+//
+// Physics follows the reference plug-in semantics (physics.hpp:37-93):
+// riemann(u_out, u_in, n) with the outward non-normalised normal, F_hat.n =
+// |n| F_hat.n_unit; Roe with the Harten fix on the
+// acoustic waves (physics.hpp:194-198); Navier-Stokes stress and
+// heat flux from conservative gradients.  The device code
+// works directly with normal fluxes F.n (never forms the D x m tensor).
+#pragma once
+
+#include <cstdint>
+
+#include "linedg_b200.h"
+
+namespace ldg {
+
+enum { PH_POISSON = 0, PH_EULER = 1, PH_NS = 2 };
+
+template <int D_, int P_, int PH_, int RI_>
+struct Cfg {
+  static constexpr int D = D_, P = P_, PH = PH_, RI = RI_;
+  static constexpr int NP = P + 1;
+  static constexpr int NQ = (3 * P + 2) / 2;              // basis.cpp:176
+  static constexpr int NPE = D == 2 ? NP * NP : NP * NP * NP;
+  static constexpr int NL = D == 2 ? NP : NP * NP;        // lines per direction
+  static constexpr int LPE = D * NL;                      // lines per element
+  static constexpr int M = PH == PH_POISSON ? 1 : D + 2;  // components
+  static constexpr int MD = M * D;
+  static constexpr bool HAS_INV = PH != PH_POISSON;
+  static constexpr bool SECOND = PH != PH_EULER;          // LDG auxiliary gradient present
+  static constexpr bool VIS_U = PH == PH_NS;              // viscous flux depends on u
+  // Metric tables per element (processing order), padded to 16 bytes.
+  static constexpr int MET_NV = D * NL * NQ * D;
+  static constexpr int MET_NE = D * 2 * NL * D;
+  static constexpr int MET = MET_NV + MET_NE + NPE;
+  static constexpr int METP = (MET + 1) / 2 * 2;
+  // Line-structured Jacobian store: rows tiled by NT = NP^2 rows (2-D: one
+  // element, 3-D: one slab x2 = const).
+  static constexpr int NT = NP * NP;
+  static constexpr int TPE = NPE / NT;                    // tiles per element
+  static constexpr int NS11 = D * P + 1 + 2 * D;          // K11 node-columns per row
+  static constexpr int NS12 = D * P + 1 + D;              // K12 / K21 node-columns per row
+  static constexpr int B11 = M * M;
+  static constexpr int R12 = PH == PH_NS ? M - 1 : M;     // K12 rows stored (density row dropped)
+  static constexpr int B12 = R12 * MD;
+  static constexpr int B21 = D;                           // component-diagonal scalars
+};
+
+// Basis tables folded for the line operators (host-built once):
+//   dq[i][q] = -(M^-1 Phi' W)[i][q]   volume operator,
+//   mi[i][s] = M^-1[i][s ? p : 0]     endpoint lifting,
+//   cc[i][t][q] = dq[i][q] phi[t][q]  Jacobian line blocks.
+template <int NP, int NQ>
+struct BasisTab {
+  double phi[NP][NQ];
+  double dq[NP][NQ];
+  double mi[NP][2];
+  double cc[NP][NP][NQ];
+};
+
+struct DevError {
+  int flag;       // 0 ok, 1 physical state
+  int elem;
+  int node;
+  int pad;
+  double state[8];
+};
+
+struct PhysParams {
+  double gamma, mu, kap;  // kap = mu * gamma / Pr
+  double c11, c11bd;      // interior C11; boundary coefficient c11_bd * p^2
+};
+
+// ------------------------------------------------------------ Dual<N>
+template <int N>
+struct Dual {
+  double v;
+  double d[N];
+  __device__ __forceinline__ Dual() {}
+  __device__ __forceinline__ Dual(double x) : v(x) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = 0.0;
+  }
+};
+template <int N> __device__ __forceinline__ Dual<N> operator+(const Dual<N>& a, const Dual<N>& b) {
+  Dual<N> r; r.v = a.v + b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] + b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator-(const Dual<N>& a, const Dual<N>& b) {
+  Dual<N> r; r.v = a.v - b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] - b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator-(const Dual<N>& a) {
+  Dual<N> r; r.v = -a.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = -a.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator*(const Dual<N>& a, const Dual<N>& b) {
+  Dual<N> r; r.v = a.v * b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * b.v + a.v * b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator/(const Dual<N>& a, const Dual<N>& b) {
+  Dual<N> r; r.v = a.v / b.v;
+  const double ib = 1.0 / b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = (a.d[i] - r.v * b.d[i]) * ib;
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator+(const Dual<N>& a, double b) {
+  Dual<N> r = a; r.v += b; return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator+(double a, const Dual<N>& b) { return b + a; }
+template <int N> __device__ __forceinline__ Dual<N> operator-(const Dual<N>& a, double b) {
+  Dual<N> r = a; r.v -= b; return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator-(double a, const Dual<N>& b) {
+  Dual<N> r; r.v = a - b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = -b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator*(const Dual<N>& a, double b) {
+  Dual<N> r; r.v = a.v * b;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * b;
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator*(double a, const Dual<N>& b) { return b * a; }
+template <int N> __device__ __forceinline__ Dual<N> operator/(const Dual<N>& a, double b) {
+  const double ib = 1.0 / b;
+  Dual<N> r; r.v = a.v / b;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * ib;
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> operator/(double a, const Dual<N>& b) {
+  return Dual<N>(a) / b;
+}
+template <int N> __device__ __forceinline__ Dual<N> dsqrt(const Dual<N>& a) {
+  Dual<N> r; r.v = sqrt(a.v);
+  const double s = 0.5 / r.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = s * a.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dual<N> dabs(const Dual<N>& a) { return a.v >= 0.0 ? a : -a; }
+template <int N> __device__ __forceinline__ Dual<N> dmax(const Dual<N>& a, const Dual<N>& b) {
+  return a.v >= b.v ? a : b;
+}
+__device__ __forceinline__ double dsqrt(double a) { return sqrt(a); }
+__device__ __forceinline__ double dabs(double a) { return a >= 0.0 ? a : -a; }
+__device__ __forceinline__ double dmax(double a, double b) { return a >= b ? a : b; }
+__device__ __forceinline__ double val(double a) { return a; }
+template <int N> __device__ __forceinline__ double val(const Dual<N>& a) { return a.v; }
+
+// Records the first physical-state failure (errors.hpp:10-18).
+template <class T, int M>
+__device__ __noinline__ void report_bad_state(DevError* err, int elem, int node, const T* u) {
+  if (atomicCAS(&err->flag, 0, 1) == 0) {
+    err->elem = elem;
+    err->node = node;
+    for (int c = 0; c < M && c < 8; ++c) err->state[c] = val(u[c]);
+  }
+}
+
+// ------------------------------------------------------------- physics
+// Normal Euler flux F(u).n for a (non-normalised) vector n; returns p.
+// ok = false on rho <= 0 or p <= 0.
+template <int D, class T>
+__device__ __forceinline__ T euler_fn(const T* u, const double* n, double gamma, T* fn, bool& ok) {
+  const T rho = u[0];
+  const T irho = 1.0 / rho;
+  T mom2 = u[1] * u[1];
+  T mn = u[1] * n[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) {
+    mom2 = mom2 + u[1 + d] * u[1 + d];
+    mn = mn + u[1 + d] * n[d];
+  }
+  const T p = (gamma - 1.0) * (u[D + 1] - 0.5 * mom2 * irho);
+  ok = ok && (val(rho) > 0.0) && (val(p) > 0.0);
+  const T un = mn * irho;
+  fn[0] = mn;
+#pragma unroll
+  for (int i = 0; i < D; ++i) fn[1 + i] = u[1 + i] * un + p * n[i];
+  fn[D + 1] = un * (u[D + 1] + p);
+  return p;
+}
+
+// Roe flux (u_out = R, u_in = L), outward normal n.
+template <int D, class T>
+__device__ __forceinline__ void roe_fn(const T* uo, const T* ui, const double* n, double gamma,
+                                       T* fh, bool& ok) {
+  double nn = n[0] * n[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+  nn = sqrt(nn);
+  const double inn = 1.0 / nn;
+  double nb[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) nb[d] = n[d] * inn;
+  T fl[D + 2], fr[D + 2];
+  const T pL = euler_fn<D>(ui, nb, gamma, fl, ok);
+  const T pR = euler_fn<D>(uo, nb, gamma, fr, ok);
+  const T irL = 1.0 / ui[0], irR = 1.0 / uo[0];
+  const T sL = dsqrt(ui[0]), sR = dsqrt(uo[0]);
+  const T isw = 1.0 / (sL + sR);
+  const T wL = sL * isw, wR = sR * isw;
+  T vL[D], vR[D], vt[D];
+  T q2 = 0.0, unt = 0.0, dun = 0.0, vtdv = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    vL[d] = ui[1 + d] * irL;
+    vR[d] = uo[1 + d] * irR;
+    vt[d] = wL * vL[d] + wR * vR[d];
+    q2 = q2 + vt[d] * vt[d];
+    unt = unt + vt[d] * nb[d];
+  }
+  const T HL = (ui[D + 1] + pL) * irL, HR = (uo[D + 1] + pR) * irR;
+  const T Ht = wL * HL + wR * HR;
+  const T a2 = (gamma - 1.0) * (Ht - 0.5 * q2);
+  ok = ok && (val(a2) > 0.0);
+  const T a = dsqrt(a2);
+  const T ia2 = 1.0 / a2;
+  const T rt = sL * sR;
+  const T drho = uo[0] - ui[0], dp = pR - pL;
+  T dv[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    dv[d] = vR[d] - vL[d];
+    dun = dun + dv[d] * nb[d];
+    vtdv = vtdv + vt[d] * dv[d];
+  }
+  T l1 = dabs(unt - a), l2 = dabs(unt), l3 = dabs(unt + a);
+  const T del = 0.05 * (l2 + a);
+  if (val(l1) < val(del)) l1 = (l1 * l1 + del * del) / (2.0 * del);
+  if (val(l3) < val(del)) l3 = (l3 * l3 + del * del) / (2.0 * del);
+  const T ra = rt * a * dun;
+  const T al1 = 0.5 * (dp - ra) * ia2;
+  const T al3 = 0.5 * (dp + ra) * ia2;
+  const T al2 = drho - dp * ia2;
+  const T w1 = l1 * al1, w3 = l3 * al3;
+  const T hn = 0.5 * nn;
+  fh[0] = hn * (fl[0] + fr[0] - (w1 + l2 * al2 + w3));
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const T dis = w1 * (vt[i] - a * nb[i]) + l2 * (al2 * vt[i] + rt * (dv[i] - dun * nb[i])) +
+                  w3 * (vt[i] + a * nb[i]);
+    fh[1 + i] = hn * (fl[1 + i] + fr[1 + i] - dis);
+  }
+  const T dise = w1 * (Ht - unt * a) + l2 * (al2 * (0.5 * q2) + rt * (vtdv - unt * dun)) +
+                 w3 * (Ht + unt * a);
+  fh[D + 1] = hn * (fl[D + 1] + fr[D + 1] - dise);
+}
+
+// Local Lax-Friedrichs (extension, config 4).
+template <int D, class T>
+__device__ __forceinline__ void llf_fn(const T* uo, const T* ui, const double* n, double gamma,
+                                       T* fh, bool& ok) {
+  double nn = n[0] * n[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+  nn = sqrt(nn);
+  const double inn = 1.0 / nn;
+  double nb[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) nb[d] = n[d] * inn;
+  T fl[D + 2], fr[D + 2];
+  const T pL = euler_fn<D>(ui, n, gamma, fl, ok);
+  const T pR = euler_fn<D>(uo, n, gamma, fr, ok);
+  T mL = ui[1] * nb[0], mR = uo[1] * nb[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) {
+    mL = mL + ui[1 + d] * nb[d];
+    mR = mR + uo[1 + d] * nb[d];
+  }
+  const T irL = 1.0 / ui[0], irR = 1.0 / uo[0];
+  const T lam = dmax(dabs(mL * irL) + dsqrt(gamma * pL * irL), dabs(mR * irR) + dsqrt(gamma * pR * irR));
+  const T hl = 0.5 * nn * lam;
+#pragma unroll
+  for (int c = 0; c < D + 2; ++c) fh[c] = 0.5 * (fl[c] + fr[c]) + hl * (ui[c] - uo[c]);
+}
+
+// Viscous normal flux F_vis(u, q).n.  Poisson: -q.n.  Navier-Stokes: minus
+// the +tau stress tensor dotted with n.  q layout q[c*D+d].
+template <int D, int PH, class T, class TQ, class TR>
+__device__ __forceinline__ void visc_fn(const T* u, const TQ* q, const double* n, const PhysParams& pp,
+                                        TR* fv, bool& ok) {
+  if (PH == PH_POISSON) {
+    TR s = -(q[0] * n[0]);
+#pragma unroll
+    for (int d = 1; d < D; ++d) s = s - q[d] * n[d];
+    fv[0] = s;
+  } else {
+    const T rho = u[0];
+    ok = ok && (val(rho) > 0.0);
+    const T irho = 1.0 / rho;
+    T vel[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) vel[i] = u[1 + i] * irho;
+    const T E = u[D + 1] * irho;
+    TR gv[D][D], gE[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) gv[i][d] = (q[(1 + i) * D + d] - vel[i] * q[d]) * irho;
+      gE[d] = (q[(D + 1) * D + d] - E * q[d]) * irho;
+    }
+    TR div = gv[0][0];
+#pragma unroll
+    for (int k = 1; k < D; ++k) div = div + gv[k][k];
+    const double mu = pp.mu;
+    // tau . n and the heat term
+    TR tn[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      TR s = (mu * (gv[i][0] + gv[0][i])) * n[0];
+#pragma unroll
+      for (int j = 1; j < D; ++j) s = s + (mu * (gv[i][j] + gv[j][i])) * n[j];
+      tn[i] = s - ((2.0 / 3.0) * mu) * div * n[i];
+    }
+    fv[0] = TR(0.0);
+    TR en = TR(0.0);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      fv[1 + i] = -tn[i];
+      en = en + vel[i] * tn[i];
+    }
+    TR hn = TR(0.0);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      TR ugv = vel[0] * gv[0][j];
+#pragma unroll
+      for (int i = 1; i < D; ++i) ugv = ugv + vel[i] * gv[i][j];
+      hn = hn + (gE[j] - ugv) * n[j];
+    }
+    fv[D + 1] = -(en + pp.kap * hn);
+  }
+}
+
+}  // namespace ldg

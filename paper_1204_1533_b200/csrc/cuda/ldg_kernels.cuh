@@ -1,0 +1,1032 @@
+// ldg_kernels.cuh -- sm_100a kernels of the Line-DG hot path.
+//
+// Work decomposition:
+//   * residual / gradient: one thread per 1-D coordinate line (all m
+//     components), EPB elements per CTA.  The element's nodal states are
+//     staged in shared memory; the (p+1) x n_q line contractions run in
+//     registers with the basis tables as compile-time-indexed constant-bank
+//     operands; per-direction line results meet in shared memory, so no
+//     atomics are needed (PAPER.md:285 sums r^(n) over directions).
+//   * Jacobian: one CTA per row tile (2-D: one element, 3-D: one x2-slab of
+//     an element).  Flux Jacobians at quadrature points / line ends come
+//     from a forward-mode Dual<N>; the line blocks
+//     B(i,t) = sum_q dq[i][q] phi[t][q] A_q are formed by one thread per
+//     (line, a, b) with all coefficients as constants, staged in shared
+//     memory in the store's layout and written with 16-byte coalesced
+//     stores.  Rows are never shared between CTAs: no atomics.
+//   * SpMV: one thread per node row; the store is interleaved so a warp's
+//     value loads are contiguous; in-element column nodes are implied by the
+//     row's position on its lines, neighbour columns come from the face
+//     connectivity (no column-index stream).
+#pragma once
+
+#include "ldg_device.cuh"
+
+namespace ldg {
+
+template <class C>
+struct KParams {
+  BasisTab<C::NP, C::NQ> bt;
+  PhysParams pp;
+  const int32_t* order;  // processing index k -> reference element e
+  const double* metric;  // [k][METP]
+  const int2* conn;      // [k][D][2]
+  const double* bcv;     // [nbc][M]
+  const double* source;  // reference numbering, may be null
+  DevError* err;
+  int E;                 // elements
+};
+
+// ---------------------------------------------------------------- helpers
+
+template <class C>
+__device__ __forceinline__ int node_on_line(int dir, int line, int t) {
+  constexpr int NP = C::NP;
+  if (C::D == 2) return dir == 0 ? t + NP * line : line + NP * t;
+  const int l1 = line % NP, l2 = line / NP;
+  if (dir == 0) return t + NP * l1 + NP * NP * l2;
+  if (dir == 1) return l1 + NP * t + NP * NP * l2;
+  return l1 + NP * l2 + NP * NP * t;
+}
+
+// Line index of the dir-line through node `nd`, and the node's position on it.
+template <class C>
+__device__ __forceinline__ void line_of(int dir, int nd, int& line, int& pos) {
+  constexpr int NP = C::NP;
+  const int x0 = nd % NP, x1 = (nd / NP) % NP, x2 = nd / (NP * NP);
+  if (C::D == 2) {
+    line = dir == 0 ? x1 : x0;
+    pos = dir == 0 ? x0 : x1;
+  } else {
+    if (dir == 0) { line = x1 + NP * x2; pos = x0; }
+    else if (dir == 1) { line = x0 + NP * x2; pos = x1; }
+    else { line = x0 + NP * x1; pos = x2; }
+  }
+}
+
+__device__ __forceinline__ int conn_node(int packed, int line, int NP) {
+  const int c0 = packed & 0xff;
+  const int c1 = static_cast<int8_t>((packed >> 8) & 0xff);
+  const int c2 = static_cast<int8_t>((packed >> 16) & 0xff);
+  return c0 + c1 * (line % NP) + c2 * (line / NP);
+}
+__device__ __forceinline__ int conn_sign(int packed) { return (packed >> 24) & 1 ? 1 : -1; }
+
+// K11 slot of column node `col` on the dir-line through row (pos = row's
+// position on that line).  Slots: dir-0 line nodes t (self included), then
+// for dir d >= 1 the P non-self nodes, then neighbours 2*dir+side.
+template <class C>
+__device__ __forceinline__ int inel_slot(int dir, int pos, int t) {
+  if (dir == 0) return t;
+  return C::NP + (dir - 1) * C::P + (t < pos ? t : t - 1);
+}
+
+template <class C>
+__device__ __forceinline__ void cp_elem(double* dst, const double* __restrict__ src, int n, int tid,
+                                        int nthr) {
+  // 16-byte vector copy when both sides are aligned (n even and src aligned).
+  if ((n & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (int i = tid; i < n / 2; i += nthr) d2[i] = __ldg(s2 + i);
+  } else {
+    for (int i = tid; i < n; i += nthr) dst[i] = __ldg(src + i);
+  }
+}
+
+
+// Physical-state failure on a line: report the first nodal state on the line
+// that is itself non-physical (rho <= 0 or p <= 0), else the line's first node
+// (the failure was at an interpolated quadrature state).
+template <class C>
+__device__ __noinline__ void report_line(const KParams<C>& kp, int e, int dir, int line,
+                                         const double* su) {
+  constexpr int M = C::M, D = C::D;
+  int bad = node_on_line<C>(dir, line, 0);
+  if (C::HAS_INV) {
+    for (int t = 0; t < C::NP; ++t) {
+      const int nd = node_on_line<C>(dir, line, t);
+      const double* u = su + nd * M;
+      double m2 = 0.0;
+      for (int d = 0; d < D; ++d) m2 += u[1 + d] * u[1 + d];
+      const double p = (kp.pp.gamma - 1.0) * (u[D + 1] - 0.5 * m2 / u[0]);
+      if (!(u[0] > 0.0) || !(p > 0.0)) {
+        bad = nd;
+        break;
+      }
+    }
+  }
+  report_bad_state<double, M>(kp.err, e, bad, su + bad * M);
+}
+
+// ===================================================================== residual
+// FIRST: first-order physics (Q absent).  Otherwise R(U, Q).
+template <class C, int EPB>
+__global__ void __launch_bounds__((EPB * C::LPE + 31) / 32 * 32)
+k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+           double* __restrict__ R) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
+                MD = C::MD, LPE = C::LPE;
+  extern __shared__ double smem[];
+  double* su = smem;                                   // [EPB][NPE*M]
+  double* sq = su + EPB * NPE * M;                     // [EPB][NPE*MD]
+  double* sacc = sq + (C::SECOND ? EPB * NPE * MD : 0);  // [EPB][D][NPE*M]
+  const int k0 = blockIdx.x * EPB;
+  const int nb = min(EPB, kp.E - k0);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int le = 0; le < nb; ++le) {
+    const size_t e = kp.order[k0 + le];
+    cp_elem<C>(su + le * NPE * M, U + e * (NPE * M), NPE * M, tid, nthr);
+    if (C::SECOND) cp_elem<C>(sq + le * NPE * MD, Q + e * (NPE * MD), NPE * MD, tid, nthr);
+  }
+  __syncthreads();
+  const int le = tid / LPE;
+  if (le < nb) {
+    const int rem = tid - le * LPE;
+    const int dir = rem / NL, line = rem - dir * NL;
+    const int k = k0 + le;
+    const int e = kp.order[k];
+    const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+    const double* nvl = mk + (dir * NL + line) * NQ * D;
+    const double* sul = su + le * NPE * M;
+    const double* sql = sq + le * NPE * MD;
+    bool ok = true;
+    // Neighbour traces at both line ends.
+    double uo[2][M], qo[2][MD];
+    const double* bcp[2] = {nullptr, nullptr};
+    int sg[2];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+      sg[side] = conn_sign(cn.y);
+      if (cn.x >= 0) {
+        const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+#pragma unroll
+        for (int c = 0; c < M; ++c) uo[side][c] = __ldg(U + nd * M + c);
+        if (C::SECOND && sg[side] > 0) {
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qo[side][c] = __ldg(Q + nd * MD + c);
+        }
+      } else {
+        bcp[side] = kp.bcv + (-1 - cn.x) * M;
+      }
+    }
+    double r[NP][M];
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int c = 0; c < M; ++c) r[i][c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double uq[M], qq[C::SECOND ? MD : 1];
+#pragma unroll
+      for (int c = 0; c < M; ++c) uq[c] = 0.0;
+      if (C::SECOND) {
+#pragma unroll
+        for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        const int nd = node_on_line<C>(dir, line, t);
+        const double ph = kp.bt.phi[t][q];
+#pragma unroll
+        for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
+        if (C::SECOND) {
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qq[c] += ph * sql[nd * MD + c];
+        }
+      }
+      double nv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) nv[d] = __ldg(nvl + q * D + d);
+      double f[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) f[c] = 0.0;
+      if (C::HAS_INV) euler_fn<D>(uq, nv, kp.pp.gamma, f, ok);
+      if (C::SECOND) {
+        double fv[M];
+        visc_fn<D, C::PH, double, double, double>(uq, qq, nv, kp.pp, fv, ok);
+#pragma unroll
+        for (int c = 0; c < M; ++c) f[c] += fv[c];
+      }
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c) r[i][c] += kp.bt.dq[i][q] * f[c];
+    }
+    // Endpoint numerical fluxes, lifted by the M^-1 columns 0 and p.
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int ie = side ? C::P : 0;
+      const int nd = node_on_line<C>(dir, line, ie);
+      const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
+      double n[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) n[d] = __ldg(nep + d);
+      double ui[M], fh[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        ui[c] = sul[nd * M + c];
+        fh[c] = 0.0;
+      }
+      if (C::HAS_INV) {
+        double g[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) g[c] = bcp[side] ? __ldg(bcp[side] + c) : uo[side][c];
+        if (C::RI == LDG_ROE) roe_fn<D>(g, ui, n, kp.pp.gamma, fh, ok);
+        else llf_fn<D>(g, ui, n, kp.pp.gamma, fh, ok);
+      }
+      if (C::SECOND) {
+        double nn = n[0] * n[0];
+#pragma unroll
+        for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+        nn = sqrt(nn);
+        double fv[M];
+        if (bcp[side]) {
+          double qi[MD];
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
+          visc_fn<D, C::PH, double, double, double>(ui, qi, n, kp.pp, fv, ok);
+          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - __ldg(bcp[side] + c));
+        } else {
+          if (sg[side] > 0) {
+            visc_fn<D, C::PH, double, double, double>(uo[side], qo[side], n, kp.pp, fv, ok);
+          } else {
+            double qi[MD];
+#pragma unroll
+            for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
+            visc_fn<D, C::PH, double, double, double>(ui, qi, n, kp.pp, fv, ok);
+          }
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] += fv[c];
+          if (kp.pp.c11 != 0.0) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[side][c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c) r[i][c] += kp.bt.mi[i][side] * fh[c];
+    }
+    if (!ok) report_line<C>(kp, e, dir, line, sul);
+    double* acc = sacc + (le * D + dir) * NPE * M;
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      const int nd = node_on_line<C>(dir, line, t);
+#pragma unroll
+      for (int c = 0; c < M; ++c) acc[nd * M + c] = r[t][c];
+    }
+  }
+  __syncthreads();
+  // dU/dt = S - (1/J) sum_dir r^(dir)
+  for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
+    const int l = idx / (NPE * M), off = idx - l * NPE * M;
+    const int nd = off / M;
+    const int k = k0 + l;
+    const size_t e = kp.order[k];
+    const double* a = sacc + l * D * NPE * M + off;
+    double s = a[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) s = s + a[d * NPE * M];
+    const double invJ = __ldg(kp.metric + static_cast<size_t>(k) * C::METP + C::MET_NV + C::MET_NE + nd);
+    const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
+    R[e * (NPE * M) + off] = src - invJ * s;
+  }
+}
+
+// ===================================================================== gradient
+// Q = (1/J) sum_dir d^(dir),  d = M^-1 [u_hat (x) n |ends - sum_q w phi' u_q (x) nvec_q]
+template <class C, int EPB>
+__global__ void __launch_bounds__((EPB * C::LPE + 31) / 32 * 32)
+k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict__ Q) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
+                MD = C::MD, LPE = C::LPE;
+  extern __shared__ double smem[];
+  double* su = smem;                   // [EPB][NPE*M]
+  double* sacc = su + EPB * NPE * M;   // [EPB][D][NPE*MD]
+  const int k0 = blockIdx.x * EPB;
+  const int nb = min(EPB, kp.E - k0);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int le = 0; le < nb; ++le) {
+    const size_t e = kp.order[k0 + le];
+    cp_elem<C>(su + le * NPE * M, U + e * (NPE * M), NPE * M, tid, nthr);
+  }
+  __syncthreads();
+  const int le = tid / LPE;
+  if (le < nb) {
+    const int rem = tid - le * LPE;
+    const int dir = rem / NL, line = rem - dir * NL;
+    const int k = k0 + le;
+    const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+    const double* nvl = mk + (dir * NL + line) * NQ * D;
+    const double* sul = su + le * NPE * M;
+    double g[NP][MD];
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int c = 0; c < MD; ++c) g[i][c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double uq[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) uq[c] = 0.0;
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        const int nd = node_on_line<C>(dir, line, t);
+        const double ph = kp.bt.phi[t][q];
+#pragma unroll
+        for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
+      }
+      double nv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) nv[d] = __ldg(nvl + q * D + d);
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+#pragma unroll
+          for (int d = 0; d < D; ++d) g[i][c * D + d] += kp.bt.dq[i][q] * (uq[c] * nv[d]);
+    }
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+      const int ie = side ? C::P : 0;
+      const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
+      double uh[M];
+      if (cn.x < 0) {  // Dirichlet: u_hat = g_D
+#pragma unroll
+        for (int c = 0; c < M; ++c) uh[c] = __ldg(kp.bcv + (-1 - cn.x) * M + c);
+      } else if (conn_sign(cn.y) > 0) {  // S = +1: own trace
+        const int nd = node_on_line<C>(dir, line, ie);
+#pragma unroll
+        for (int c = 0; c < M; ++c) uh[c] = sul[nd * M + c];
+      } else {
+        const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+#pragma unroll
+        for (int c = 0; c < M; ++c) uh[c] = __ldg(U + nd * M + c);
+      }
+      double n[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) n[d] = __ldg(nep + d);
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+#pragma unroll
+          for (int d = 0; d < D; ++d) g[i][c * D + d] += kp.bt.mi[i][side] * (uh[c] * n[d]);
+    }
+    double* acc = sacc + (le * D + dir) * NPE * MD;
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      const int nd = node_on_line<C>(dir, line, t);
+#pragma unroll
+      for (int c = 0; c < MD; ++c) acc[nd * MD + c] = g[t][c];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nb * NPE * MD; idx += nthr) {
+    const int l = idx / (NPE * MD), off = idx - l * NPE * MD;
+    const int nd = off / MD;
+    const int k = k0 + l;
+    const size_t e = kp.order[k];
+    const double* a = sacc + l * D * NPE * MD + off;
+    double s = a[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) s = s + a[d * NPE * MD];
+    const double invJ = __ldg(kp.metric + static_cast<size_t>(k) * C::METP + C::MET_NV + C::MET_NE + nd);
+    Q[e * (NPE * MD) + off] = invJ * s;
+  }
+}
+
+// ===================================================================== Jacobian
+// Lines intersecting tile `s` of an element: 2-D: all D*NL lines (full).
+// 3-D: dir-0 and dir-1 lines of slab s (full) and every dir-2 line (row s only).
+template <class C>
+struct TileLines {
+  static constexpr int NLT = C::D == 2 ? C::D * C::NL : 2 * C::NP + C::NP * C::NP;
+  __device__ static __forceinline__ void get(int tl, int s, int& dir, int& line) {
+    if (C::D == 2) {
+      dir = tl / C::NL;
+      line = tl - dir * C::NL;
+    } else if (tl < 2 * C::NP) {
+      dir = tl / C::NP;
+      line = (tl - dir * C::NP) + C::NP * s;
+    } else {
+      dir = 2;
+      line = tl - 2 * C::NP;
+    }
+  }
+};
+
+// K11 (+ K12 for second-order physics) of one row tile.  Store layout:
+//   K11[((T*NS11 + slot)*B11 + a*M + b)*NT + r]       T = k*TPE + tile, r = row in tile
+//   K12[((T*NS12 + slot)*B12 + a'*MD + b)*NT + r]     a' = stored row (NS: a-1)
+template <class C>
+struct JacSmem {
+  static constexpr int NLT = TileLines<C>::NLT;
+  static constexpr int NDA = C::SECOND ? C::MD : 1;  // q-derivative slots
+  static constexpr int U = C::NPE * C::M;
+  static constexpr int Q = C::SECOND ? C::NPE * C::MD : 0;
+  static constexpr int UO = NLT * 2 * C::M;
+  static constexpr int QO = C::SECOND ? NLT * 2 * C::MD : 0;
+  static constexpr int A = NLT * C::NQ * C::B11;              // dF/du . nvec at quad points
+  static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
+  static constexpr int EIN = NLT * 2 * C::B11;                // endpoint d/du_in
+  static constexpr int EOUT = NLT * 2 * C::B11;               // endpoint d/du_out
+  static constexpr int EQ = C::SECOND ? NLT * 2 * C::M * C::MD : 0;  // endpoint d/dq (selected side)
+  static constexpr int ST11 = C::NS11 * C::B11 * C::NT;
+  static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
+  static constexpr int STG = ST11 > ST12 ? ST11 : ST12;
+  static constexpr int DG = (C::D - 1) * C::NT * (C::B11 > C::B12 ? C::B11 : C::B12);  // diag scratch
+  static constexpr int TOTAL = U + Q + UO + QO + A + BQ + EIN + EOUT + EQ + STG + DG + C::NT;
+};
+
+template <class C>
+__global__ void __launch_bounds__(256)
+k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+           double* __restrict__ K11, double* __restrict__ K12) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
+                MD = C::MD, NT = C::NT, P = C::P, B11 = C::B11;
+  using SM = JacSmem<C>;
+  constexpr int NLT = SM::NLT;
+  extern __shared__ double smem[];
+  double* su = smem;
+  double* sq = su + SM::U;
+  double* suo = sq + SM::Q;
+  double* sqo = suo + SM::UO;
+  double* sA = sqo + SM::QO;
+  double* sBq = sA + SM::A;
+  double* sEin = sBq + SM::BQ;
+  double* sEout = sEin + SM::EIN;
+  double* sEq = sEout + SM::EOUT;
+  double* stg = sEq + SM::EQ;
+  double* sdg = stg + SM::STG;
+  double* sinvJ = sdg + SM::DG;
+
+  const int T = blockIdx.x;               // tile id
+  const int k = T / C::TPE, s = T - k * C::TPE;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const size_t e = kp.order[k];
+  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+
+  // ---- phase 0: stage element states, neighbour traces, 1/J of the tile rows
+  cp_elem<C>(su, U + e * (NPE * M), NPE * M, tid, nthr);
+  if (C::SECOND) cp_elem<C>(sq, Q + e * (NPE * MD), NPE * MD, tid, nthr);
+  for (int r = tid; r < NT; r += nthr) sinvJ[r] = __ldg(mk + C::MET_NV + C::MET_NE + s * NT + r);
+  for (int idx = tid; idx < NLT * 2; idx += nthr) {
+    const int tl = idx >> 1, side = idx & 1;
+    int dir, line;
+    TileLines<C>::get(tl, s, dir, line);
+    const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+    if (cn.x >= 0) {
+      const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+#pragma unroll
+      for (int c = 0; c < M; ++c) suo[idx * M + c] = __ldg(U + nd * M + c);
+      if (C::SECOND) {
+#pragma unroll
+        for (int c = 0; c < MD; ++c) sqo[idx * MD + c] = __ldg(Q + nd * MD + c);
+      }
+    }
+  }
+  for (int i = tid; i < SM::STG; i += nthr) stg[i] = 0.0;
+  __syncthreads();
+
+  // ---- phase 1: flux Jacobians (forward-mode Dual<M> / Dual<MD>)
+  constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
+  for (int w = tid; w < NLT * NQ; w += nthr) {
+    const int tl = w / NQ, q = w - tl * NQ;
+    int dir, line;
+    TileLines<C>::get(tl, s, dir, line);
+    double nv[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
+    double uq[M], qq[C::SECOND ? MD : 1];
+#pragma unroll
+    for (int c = 0; c < M; ++c) uq[c] = 0.0;
+    if (C::SECOND) {
+#pragma unroll
+      for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      const int nd = node_on_line<C>(dir, line, t);
+      const double ph = kp.bt.phi[t][q];
+#pragma unroll
+      for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
+      if (C::SECOND) {
+#pragma unroll
+        for (int c = 0; c < MD; ++c) qq[c] += ph * sq[nd * MD + c];
+      }
+    }
+    bool ok = true;
+    if (VOL11) {
+      Dual<M> du[M], f[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        du[c] = Dual<M>(uq[c]);
+        du[c].d[c] = 1.0;
+        f[c] = Dual<M>(0.0);
+      }
+      if (C::HAS_INV) euler_fn<D>(du, nv, kp.pp.gamma, f, ok);
+      if (C::VIS_U) {
+        Dual<M> fv[M];
+        visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(du, qq, nv, kp.pp, fv, ok);
+#pragma unroll
+        for (int c = 0; c < M; ++c) f[c] = f[c] + fv[c];
+      }
+      double* a = sA + (tl * NQ + q) * B11;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+#pragma unroll
+        for (int b = 0; b < M; ++b) a[c * M + b] = f[c].d[b];
+    }
+    if (C::SECOND) {
+      Dual<SM::NDA> dq[SM::NDA], fv[M];
+#pragma unroll
+      for (int c = 0; c < SM::NDA; ++c) {
+        dq[c] = Dual<SM::NDA>(qq[c]);
+        dq[c].d[c] = 1.0;
+      }
+      visc_fn<D, C::PH, double, Dual<SM::NDA>, Dual<SM::NDA>>(uq, dq, nv, kp.pp, fv, ok);
+      double* bq = sBq + (tl * NQ + q) * M * MD;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+#pragma unroll
+        for (int b = 0; b < MD; ++b) bq[c * MD + b] = fv[c].d[b];
+    }
+    if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
+  }
+  // endpoint items: (tile line, side, pass) pass 0: d/du_in, 1: d/du_out, 2: d/dq (selected side)
+  constexpr int NPASS = C::SECOND ? 3 : 2;
+  for (int w = tid; w < NLT * 2 * NPASS; w += nthr) {
+    const int pass = w % NPASS, idx = w / NPASS, tl = idx >> 1, side = idx & 1;
+    int dir, line;
+    TileLines<C>::get(tl, s, dir, line);
+    const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+    const bool bd = cn.x < 0;
+    const int S = conn_sign(cn.y);
+    if (pass == 1 && bd) continue;
+    const int ie = side ? P : 0;
+    const int nd = node_on_line<C>(dir, line, ie);
+    double n[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
+    double nn = n[0] * n[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+    nn = sqrt(nn);
+    const double* bcp = bd ? kp.bcv + (-1 - cn.x) * M : nullptr;
+    bool ok = true;
+    if (pass < 2) {
+      Dual<M> ui[M], uo[M], fh[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        ui[c] = Dual<M>(su[nd * M + c]);
+        uo[c] = Dual<M>(bd ? __ldg(bcp + c) : suo[idx * M + c]);
+        if (pass == 0) ui[c].d[c] = 1.0;
+        else uo[c].d[c] = 1.0;
+        fh[c] = Dual<M>(0.0);
+      }
+      if (C::HAS_INV) {
+        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      }
+      if (C::SECOND) {
+        Dual<M> fv[M];
+        if (bd) {
+          visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(ui, sq + nd * MD, n, kp.pp, fv, ok);
+          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
+        } else {
+          if (S > 0) visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(uo, sqo + idx * MD, n, kp.pp, fv, ok);
+          else visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(ui, sq + nd * MD, n, kp.pp, fv, ok);
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
+          if (kp.pp.c11 != 0.0) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
+          }
+        }
+      }
+      double* dst = (pass == 0 ? sEin : sEout) + idx * B11;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+#pragma unroll
+        for (int b = 0; b < M; ++b) dst[c * M + b] = fh[c].d[b];
+    } else if (C::SECOND) {
+      // viscous endpoint flux w.r.t. the q of the switch-selected side
+      const bool out = !bd && S > 0;
+      Dual<SM::NDA> dqv[SM::NDA], fv[M];
+      const double* qsrc = out ? sqo + idx * MD : sq + nd * MD;
+#pragma unroll
+      for (int c = 0; c < SM::NDA; ++c) {
+        dqv[c] = Dual<SM::NDA>(qsrc[c]);
+        dqv[c].d[c] = 1.0;
+      }
+      const double* usrc = out ? suo + idx * M : su + nd * M;
+      visc_fn<D, C::PH, double, Dual<SM::NDA>, Dual<SM::NDA>>(usrc, dqv, n, kp.pp, fv, ok);
+      double* dst = sEq + idx * M * MD;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+#pragma unroll
+        for (int b = 0; b < MD; ++b) dst[c * MD + b] = fv[c].d[b];
+    }
+    if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
+  }
+  __syncthreads();
+
+  // ---- phase 2: K11 line blocks into the staging tile
+  // Each item = (tile line, a, b).  Row i of the line (all i for full lines,
+  // i = s for 3-D dir-2 lines) gets, for column t on the line,
+  //   B(i,t) = sum_q cc[i][t][q] A_q[a][b] + [t == end] mi[i][side] Ein[a][b]
+  // and for neighbour (side): mi[i][side] Eout[a][b]; scaled by -1/J_row.
+  auto row_slot_store = [&](int dir, int line, int i, int t, double v, double* base, int bsz,
+                            int ab, int nslot_unused) {
+    (void)nslot_unused;
+    const int nd = node_on_line<C>(dir, line, i);
+    const int r = nd - s * NT;
+    if (t == i && dir > 0) {
+      sdg[((dir - 1) * NT + r) * bsz + ab] = v;
+    } else {
+      const int slot = inel_slot<C>(dir, i, t);
+      base[(slot * bsz + ab) * NT + r] = v;
+    }
+  };
+  for (int w = tid; w < NLT * B11; w += nthr) {
+    const int tl = w / B11, ab = w - tl * B11;
+    int dir, line;
+    TileLines<C>::get(tl, s, dir, line);
+    const bool full = C::D == 2 || dir < 2;
+    double av[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? sA[(tl * NQ + q) * B11 + ab] : 0.0;
+    const double ein0 = sEin[(tl * 2 + 0) * B11 + ab], ein1 = sEin[(tl * 2 + 1) * B11 + ab];
+    const double eo0 = sEout[(tl * 2 + 0) * B11 + ab], eo1 = sEout[(tl * 2 + 1) * B11 + ab];
+    const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
+    const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    auto body = [&](const int i) {
+      const int nd = node_on_line<C>(dir, line, i);
+      const double sc = -sinvJ[nd - s * NT];
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        double v = 0.0;
+        if (VOL11) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * av[q];
+        }
+        if (t == 0) v += kp.bt.mi[i][0] * ein0;
+        if (t == P) v += kp.bt.mi[i][1] * ein1;
+        row_slot_store(dir, line, i, t, sc * v, stg, B11, ab, 0);
+      }
+      const int r = nd - s * NT;
+      if (c0.x >= 0) stg[((C::D * P + 1 + 2 * dir + 0) * B11 + ab) * NT + r] = sc * (kp.bt.mi[i][0] * eo0);
+      if (c1.x >= 0) stg[((C::D * P + 1 + 2 * dir + 1) * B11 + ab) * NT + r] = sc * (kp.bt.mi[i][1] * eo1);
+    };
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) body(i);
+    } else {
+      body(s);
+    }
+  }
+  __syncthreads();
+  // diagonal: slot x0 += contributions of the dir >= 1 lines (dir order)
+  for (int w = tid; w < NT * B11; w += nthr) {
+    const int r = w / B11, ab = w - r * B11;
+    const int x0 = r % NP;
+    double v = stg[(x0 * B11 + ab) * NT + r];
+#pragma unroll
+    for (int d = 1; d < D; ++d) v = v + sdg[((d - 1) * NT + r) * B11 + ab];
+    stg[(x0 * B11 + ab) * NT + r] = v;
+  }
+  __syncthreads();
+  {
+    double2* dst = reinterpret_cast<double2*>(K11 + static_cast<size_t>(T) * SM::ST11);
+    const double2* src = reinterpret_cast<const double2*>(stg);
+    if ((SM::ST11 & 1) == 0) {
+      for (int i = tid; i < SM::ST11 / 2; i += nthr) dst[i] = src[i];
+    } else {
+      double* d1 = K11 + static_cast<size_t>(T) * SM::ST11;
+      for (int i = tid; i < SM::ST11; i += nthr) d1[i] = stg[i];
+    }
+  }
+  if (!C::SECOND) return;
+  __syncthreads();
+
+  // ---- phase 3: K12 = dR/dQ (rows a' of the stored block)
+  constexpr int B12 = C::B12, R12 = C::R12, A0 = C::PH == PH_NS ? 1 : 0;
+  for (int i = tid; i < SM::ST12; i += nthr) stg[i] = 0.0;
+  __syncthreads();
+  for (int w = tid; w < NLT * B12; w += nthr) {
+    const int tl = w / B12, ab = w - tl * B12;
+    const int a = ab / MD + A0, b = ab % MD;
+    int dir, line;
+    TileLines<C>::get(tl, s, dir, line);
+    const bool full = C::D == 2 || dir < 2;
+    double bv[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) bv[q] = sBq[(tl * NQ + q) * M * MD + a * MD + b];
+    const double eq0 = sEq[(tl * 2 + 0) * M * MD + a * MD + b];
+    const double eq1 = sEq[(tl * 2 + 1) * M * MD + a * MD + b];
+    const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
+    const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    // own-end dependence when boundary or S <= 0; neighbour slot otherwise
+    const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
+    const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
+    auto body = [&](const int i) {
+      const int nd = node_on_line<C>(dir, line, i);
+      const double sc = -sinvJ[nd - s * NT];
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * bv[q];
+        if (t == 0 && own0) v += kp.bt.mi[i][0] * eq0;
+        if (t == P && own1) v += kp.bt.mi[i][1] * eq1;
+        row_slot_store(dir, line, i, t, sc * v, stg, B12, ab, 0);
+      }
+      const int r = nd - s * NT;
+      if (!own0) stg[((C::D * P + 1 + dir) * B12 + ab) * NT + r] = sc * (kp.bt.mi[i][0] * eq0);
+      if (!own1) stg[((C::D * P + 1 + dir) * B12 + ab) * NT + r] = sc * (kp.bt.mi[i][1] * eq1);
+    };
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) body(i);
+    } else {
+      body(s);
+    }
+  }
+  __syncthreads();
+  for (int w = tid; w < NT * B12; w += nthr) {
+    const int r = w / B12, ab = w - r * B12;
+    const int x0 = r % NP;
+    double v = stg[(x0 * B12 + ab) * NT + r];
+#pragma unroll
+    for (int d = 1; d < D; ++d) v = v + sdg[((d - 1) * NT + r) * B12 + ab];
+    stg[(x0 * B12 + ab) * NT + r] = v;
+  }
+  __syncthreads();
+  {
+    double* d1 = K12 + static_cast<size_t>(T) * SM::ST12;
+    if ((SM::ST12 & 1) == 0) {
+      double2* dst = reinterpret_cast<double2*>(d1);
+      const double2* src = reinterpret_cast<const double2*>(stg);
+      for (int i = tid; i < SM::ST12 / 2; i += nthr) dst[i] = src[i];
+    } else {
+      for (int i = tid; i < SM::ST12; i += nthr) d1[i] = stg[i];
+    }
+  }
+}
+
+// K21 = dQ/dU (U-independent; D scalars per node pair):
+//   K21[((T*NS12 + slot)*D + d)*NT + r]
+template <class C>
+__global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __restrict__ K21) {
+  constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, D = C::D, NT = C::NT, P = C::P;
+  constexpr int NLT = TileLines<C>::NLT;
+  constexpr int ST = C::NS12 * D * NT;
+  __shared__ double stg[ST];
+  __shared__ double sdg[(D - 1) * NT * D + 1];
+  const int T = blockIdx.x;
+  const int k = T / C::TPE, s = T - k * C::TPE;
+  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+  for (int i = threadIdx.x; i < ST; i += blockDim.x) stg[i] = 0.0;
+  __syncthreads();
+  for (int w = threadIdx.x; w < NLT * D; w += blockDim.x) {
+    const int tl = w / D, d = w - tl * D;
+    int dir, line;
+    TileLines<C>::get(tl, s, dir, line);
+    const bool full = C::D == 2 || dir < 2;
+    double nvd[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) nvd[q] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
+    const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
+    const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    const double n0 = __ldg(mk + C::MET_NV + ((dir * 2 + 0) * NL + line) * D + d);
+    const double n1 = __ldg(mk + C::MET_NV + ((dir * 2 + 1) * NL + line) * D + d);
+    // u_hat = own trace where S = +1, neighbour where S = -1, g_D on boundaries
+    const bool own0 = c0.x >= 0 && conn_sign(c0.y) > 0, nbr0 = c0.x >= 0 && conn_sign(c0.y) <= 0;
+    const bool own1 = c1.x >= 0 && conn_sign(c1.y) > 0, nbr1 = c1.x >= 0 && conn_sign(c1.y) <= 0;
+    auto body = [&](const int i) {
+      const int nd = node_on_line<C>(dir, line, i);
+      const int r = nd - s * NT;
+      const double sc = __ldg(mk + C::MET_NV + C::MET_NE + nd);
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * nvd[q];
+        if (t == 0 && own0) v += kp.bt.mi[i][0] * n0;
+        if (t == P && own1) v += kp.bt.mi[i][1] * n1;
+        if (t == i && dir > 0) sdg[((dir - 1) * NT + r) * D + d] = sc * v;
+        else stg[(inel_slot<C>(dir, i, t) * D + d) * NT + r] = sc * v;
+      }
+      if (nbr0) stg[((C::D * P + 1 + dir) * D + d) * NT + r] = sc * (kp.bt.mi[i][0] * n0);
+      if (nbr1) stg[((C::D * P + 1 + dir) * D + d) * NT + r] = sc * (kp.bt.mi[i][1] * n1);
+    };
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) body(i);
+    } else {
+      body(s);
+    }
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < NT * D; w += blockDim.x) {
+    const int r = w / D, d = w - r * D;
+    const int x0 = r % NP;
+    double v = stg[(x0 * D + d) * NT + r];
+#pragma unroll
+    for (int dd = 1; dd < C::D; ++dd) v = v + sdg[((dd - 1) * NT + r) * D + d];
+    stg[(x0 * D + d) * NT + r] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ST; i += blockDim.x) K21[static_cast<size_t>(T) * ST + i] = stg[i];
+}
+
+// ===================================================================== SpMV
+// Column node of `slot` for the row at node nd of element e (reference id).
+// NBR = number of neighbour slots per direction (2 for K11, 1 for K12/K21
+// where `nsel` picks the side by the switch).
+template <class C, int NSIN>
+__device__ __forceinline__ int64_t slot_col(const KParams<C>& kp, int k, size_t e, int nd, int slot,
+                                            int kind /*0: K11, 1: K12, 2: K21*/) {
+  constexpr int NP = C::NP, D = C::D, P = C::P, NPE = C::NPE;
+  const int x[3] = {nd % NP, (nd / NP) % NP, nd / (NP * NP)};
+  const int st[3] = {1, NP, NP * NP};
+  if (slot < NSIN) {
+    int dir, t;
+    if (slot < NP) {
+      dir = 0;
+      t = slot;
+    } else {
+      const int z = slot - NP;
+      dir = 1 + z / P;
+      t = z % P;
+      if (t >= x[dir]) ++t;
+    }
+    return static_cast<int64_t>(e) * NPE + nd + (t - x[dir]) * st[dir];
+  }
+  int dir, side;
+  const int z = slot - NSIN;
+  if (kind == 0) {
+    dir = z >> 1;
+    side = z & 1;
+  } else {
+    dir = z;
+    const int2 cs = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    // K12: the side whose switch is +1; K21: the side whose switch is -1.
+    const bool plus1 = conn_sign(cs.y) > 0;
+    side = kind == 1 ? (plus1 ? 1 : 0) : (plus1 ? 0 : 1);
+  }
+  const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+  if (cn.x < 0) return -1;
+  int line, pos;
+  line_of<C>(dir, nd, line, pos);
+  return static_cast<int64_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+}
+
+// y = K11 x  (FUSE: y = v - adt (K11 v + K12 w), used by the split matvec)
+template <class C, bool SPLIT>
+__global__ void __launch_bounds__(128)
+k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __restrict__ V12,
+         const double* __restrict__ x, const double* __restrict__ w, double adt, double* __restrict__ y) {
+  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
+  if (row >= nrows) return;
+  const int64_t T = row / NT;
+  const int r = static_cast<int>(row - T * NT);
+  const int k = static_cast<int>(T / C::TPE);
+  const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
+  const int nd = s * NT + r;
+  const size_t e = kp.order[k];
+  double acc[M];
+#pragma unroll
+  for (int a = 0; a < M; ++a) acc[a] = 0.0;
+  const double* vb = V11 + T * (C::NS11 * C::B11 * NT) + r;
+#pragma unroll
+  for (int slot = 0; slot < C::NS11; ++slot) {
+    const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 0);
+    double xv[M];
+    if (col >= 0) {
+#pragma unroll
+      for (int b = 0; b < M; ++b) xv[b] = __ldg(x + col * M + b);
+    } else {
+#pragma unroll
+      for (int b = 0; b < M; ++b) xv[b] = 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < M; ++a)
+#pragma unroll
+      for (int b = 0; b < M; ++b) acc[a] += __ldg(vb + ((slot * C::B11) + a * M + b) * NT) * xv[b];
+  }
+  if (SPLIT && C::SECOND) {
+    constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+    const double* vq = V12 + T * (C::NS12 * C::B12 * NT) + r;
+#pragma unroll
+    for (int slot = 0; slot < C::NS12; ++slot) {
+      const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
+      if (col < 0) continue;
+      double wv[MD];
+#pragma unroll
+      for (int b = 0; b < MD; ++b) wv[b] = __ldg(w + col * MD + b);
+#pragma unroll
+      for (int a = 0; a < C::R12; ++a)
+#pragma unroll
+        for (int b = 0; b < MD; ++b) acc[a + A0] += __ldg(vq + ((slot * C::B12) + a * MD + b) * NT) * wv[b];
+    }
+  }
+  const size_t yo = (e * NPE + nd) * M;
+#pragma unroll
+  for (int a = 0; a < M; ++a) {
+    if (SPLIT) y[yo + a] = __ldg(x + yo + a) - adt * acc[a];
+    else y[yo + a] = acc[a];
+  }
+}
+
+// y = K12 w  (w: m*D per node)
+template <class C>
+__global__ void __launch_bounds__(128)
+k_spmv12(const KParams<C> kp, const double* __restrict__ V12, const double* __restrict__ w,
+         double* __restrict__ y) {
+  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD;
+  constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
+  if (row >= nrows) return;
+  const int64_t T = row / NT;
+  const int r = static_cast<int>(row - T * NT);
+  const int k = static_cast<int>(T / C::TPE);
+  const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
+  const int nd = s * NT + r;
+  const size_t e = kp.order[k];
+  double acc[M];
+#pragma unroll
+  for (int a = 0; a < M; ++a) acc[a] = 0.0;
+  const double* vq = V12 + T * (C::NS12 * C::B12 * NT) + r;
+#pragma unroll
+  for (int slot = 0; slot < C::NS12; ++slot) {
+    const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
+    if (col < 0) continue;
+    double wv[MD];
+#pragma unroll
+    for (int b = 0; b < MD; ++b) wv[b] = __ldg(w + col * MD + b);
+#pragma unroll
+    for (int a = 0; a < C::R12; ++a)
+#pragma unroll
+      for (int b = 0; b < MD; ++b) acc[a + A0] += __ldg(vq + ((slot * C::B12) + a * MD + b) * NT) * wv[b];
+  }
+  const size_t yo = (e * NPE + nd) * M;
+#pragma unroll
+  for (int a = 0; a < M; ++a) y[yo + a] = acc[a];
+}
+
+// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c])
+template <class C>
+__global__ void __launch_bounds__(128)
+k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __restrict__ v,
+         double* __restrict__ w) {
+  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, D = C::D;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
+  if (row >= nrows) return;
+  const int64_t T = row / NT;
+  const int r = static_cast<int>(row - T * NT);
+  const int k = static_cast<int>(T / C::TPE);
+  const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
+  const int nd = s * NT + r;
+  const size_t e = kp.order[k];
+  double acc[M][D];
+#pragma unroll
+  for (int c = 0; c < M; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[c][d] = 0.0;
+  const double* vb = V21 + T * (C::NS12 * D * NT) + r;
+#pragma unroll
+  for (int slot = 0; slot < C::NS12; ++slot) {
+    const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 2);
+    if (col < 0) continue;
+    double kv[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + (slot * D + d) * NT);
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const double xv = __ldg(v + col * M + c);
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[c][d] += kv[d] * xv;
+    }
+  }
+  const size_t wo = (e * NPE + nd) * M * D;
+#pragma unroll
+  for (int c = 0; c < M; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) w[wo + c * D + d] = acc[c][d];
+}
+
+}  // namespace ldg

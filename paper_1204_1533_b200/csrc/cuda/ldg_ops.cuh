@@ -1,0 +1,157 @@
+// ldg_ops.cuh -- host-side launchers, one table of function pointers per
+// compile-time configuration (D, p, physics, Riemann solver).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "ldg_kernels.cuh"
+
+namespace ldg {
+
+// Everything a launcher needs, independent of the template configuration.
+struct DevCtx {
+  cudaStream_t stream = nullptr;
+  // basis tables (host copies, folded): phi[np][nq], dq[np][nq], mi[np][2], cc[np][np][nq]
+  const double* phi = nullptr;
+  const double* dq = nullptr;
+  const double* mi = nullptr;
+  const double* cc = nullptr;
+  PhysParams pp{};
+  const int32_t* order = nullptr;
+  const double* metric = nullptr;
+  const int2* conn = nullptr;
+  const double* bcv = nullptr;
+  const double* source = nullptr;
+  DevError* err = nullptr;
+  int E = 0;
+  long long* launches = nullptr;
+};
+
+struct Ops {
+  int D, P, PH, RI, M, NP, NQ, NPE, NL, MD, NS11, NS12, B11, B12, R12, NT, TPE, METP, MET_NV, MET_NE;
+  size_t jac_smem;
+  cudaError_t (*residual)(const DevCtx&, const double* U, const double* Q, double* R);
+  cudaError_t (*gradient)(const DevCtx&, const double* U, double* Q);
+  cudaError_t (*jacobian)(const DevCtx&, const double* U, const double* Q, double* K11, double* K12);
+  cudaError_t (*k21)(const DevCtx&, double* K21);
+  cudaError_t (*spmv11)(const DevCtx&, const double* V11, const double* x, double* y);
+  cudaError_t (*spmv12)(const DevCtx&, const double* V12, const double* w, double* y);
+  cudaError_t (*spmv21)(const DevCtx&, const double* V21, const double* v, double* w);
+  cudaError_t (*split)(const DevCtx&, const double* V11, const double* V12, const double* v,
+                       const double* w, double adt, double* y);
+};
+
+template <class C>
+struct Launch {
+  static constexpr int EPB = 128 / C::LPE > 0 ? 128 / C::LPE : 1;
+  static constexpr int RTHREADS = (EPB * C::LPE + 31) / 32 * 32;
+
+  static KParams<C> params(const DevCtx& d) {
+    KParams<C> kp;
+    std::memcpy(kp.bt.phi, d.phi, sizeof(kp.bt.phi));
+    std::memcpy(kp.bt.dq, d.dq, sizeof(kp.bt.dq));
+    std::memcpy(kp.bt.mi, d.mi, sizeof(kp.bt.mi));
+    std::memcpy(kp.bt.cc, d.cc, sizeof(kp.bt.cc));
+    kp.pp = d.pp;
+    kp.order = d.order;
+    kp.metric = d.metric;
+    kp.conn = d.conn;
+    kp.bcv = d.bcv;
+    kp.source = d.source;
+    kp.err = d.err;
+    kp.E = d.E;
+    return kp;
+  }
+  static void count(const DevCtx& d) {
+    if (d.launches) ++*d.launches;
+  }
+
+  static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
+    const size_t smem = sizeof(double) *
+                        (EPB * C::NPE * C::M + (C::SECOND ? EPB * C::NPE * C::MD : 0) + EPB * C::D * C::NPE * C::M);
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      init = true;
+    }
+    const int grid = (d.E + EPB - 1) / EPB;
+    k_residual<C, EPB><<<grid, RTHREADS, smem, d.stream>>>(params(d), U, Q, R);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t gradient(const DevCtx& d, const double* U, double* Q) {
+    if (!C::SECOND) return cudaSuccess;
+    const size_t smem = sizeof(double) * (EPB * C::NPE * C::M + EPB * C::D * C::NPE * C::MD);
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_gradient<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      init = true;
+    }
+    const int grid = (d.E + EPB - 1) / EPB;
+    k_gradient<C, EPB><<<grid, RTHREADS, smem, d.stream>>>(params(d), U, Q);
+    count(d);
+    return cudaGetLastError();
+  }
+  static constexpr size_t jac_smem() { return sizeof(double) * JacSmem<C>::TOTAL; }
+  static cudaError_t jacobian(const DevCtx& d, const double* U, const double* Q, double* K11, double* K12) {
+    const size_t smem = jac_smem();
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      init = true;
+    }
+    k_jacobian<C><<<d.E * C::TPE, 256, smem, d.stream>>>(params(d), U, Q, K11, K12);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t k21(const DevCtx& d, double* K21) {
+    if (!C::SECOND) return cudaSuccess;
+    k_k21<C><<<d.E * C::TPE, 128, 0, d.stream>>>(params(d), K21);
+    count(d);
+    return cudaGetLastError();
+  }
+  static int rgrid(const DevCtx& d) {
+    const long long rows = static_cast<long long>(d.E) * C::NPE;
+    return static_cast<int>((rows + 127) / 128);
+  }
+  static cudaError_t spmv11(const DevCtx& d, const double* V11, const double* x, double* y) {
+    k_spmv11<C, false><<<rgrid(d), 128, 0, d.stream>>>(params(d), V11, nullptr, x, nullptr, 0.0, y);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t spmv12(const DevCtx& d, const double* V12, const double* w, double* y) {
+    if (!C::SECOND) return cudaSuccess;
+    k_spmv12<C><<<rgrid(d), 128, 0, d.stream>>>(params(d), V12, w, y);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t spmv21(const DevCtx& d, const double* V21, const double* v, double* w) {
+    if (!C::SECOND) return cudaSuccess;
+    k_spmv21<C><<<rgrid(d), 128, 0, d.stream>>>(params(d), V21, v, w);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t split(const DevCtx& d, const double* V11, const double* V12, const double* v,
+                           const double* w, double adt, double* y) {
+    k_spmv11<C, true><<<rgrid(d), 128, 0, d.stream>>>(params(d), V11, V12, v, w, adt, y);
+    count(d);
+    return cudaGetLastError();
+  }
+
+  static const Ops* table() {
+    static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
+                            C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
+                            C::MET_NV, C::MET_NE, jac_smem(), residual, gradient, jacobian, k21,
+                            spmv11, spmv12, spmv21, split};
+    return &ops;
+  }
+};
+
+}  // namespace ldg
+
+#define LDG_OPS_NAME(D, P, PH, RI) ldg_ops_##D##_##P##_##PH##_##RI
+#define LDG_DECLARE_OPS(D, P, PH, RI) const ldg::Ops* LDG_OPS_NAME(D, P, PH, RI)();
+#define LDG_DEFINE_OPS(D, P, PH, RI) \
+  const ldg::Ops* LDG_OPS_NAME(D, P, PH, RI)() { return ldg::Launch<ldg::Cfg<D, P, PH, RI>>::table(); }

@@ -1,0 +1,175 @@
+"""GPU (sm_100a) vs CPU oracle parity through the C-ABI.
+
+Bar (BASELINE.json north_star): residuals, gradients and Jacobian values to a
+normwise relative L-infinity error <= 1e-12 (err = max|a-b| / max|b|,
+SURVEY.md Appendix B), node sparsity patterns and indexing bit-exact.
+"""
+import numpy as np
+import pytest
+
+from paper_1204_1533_b200 import CONFIGS, LDG_K11, LDG_K12, LDG_K21, Case, Physics, _abi
+from paper_1204_1533_b200.linedg import ConfigError, LineDG, PhysicalStateError
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - GPU marker tests only run on the box
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle.pyoracle import Oracle  # noqa: E402  (test infrastructure)
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    den = np.abs(b).max()
+    return np.abs(a - b).max() / (den if den > 0 else 1.0)
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# (config index, n, rotate override)
+SMALL = [(0, 4, None), (0, 4, False), (1, 4, None), (1, 4, True), (2, 4, None), (2, 4, True),
+         (3, 2, None), (3, 3, False), (4, 2, None), (4, 2, True)]
+
+
+def small_ids():
+    return [f"C{c + 1}-n{n}-rot{r}" for c, n, r in SMALL]
+
+
+@pytest.fixture(scope="module", params=SMALL, ids=small_ids())
+def setup(request):
+    ci, n, rot = request.param
+    cfg = CONFIGS[ci]
+    case, U = cfg.build(n=n, rotate=rot)
+    src = cfg.source_for(case)
+    gpu = LineDG(case, cfg.physics)
+    ora = Oracle(case, cfg.physics)
+    if src is not None:
+        gpu.set_source(src)
+        ora.set_source(src)
+    return cfg, case, U, gpu, ora
+
+
+def test_residual(setup):
+    cfg, case, U, gpu, ora = setup
+    R_ref = ora.residual(U)
+    R = host(gpu.residual(dev(U)))
+    assert rel(R, R_ref) <= TOL, rel(R, R_ref)
+
+
+def test_residual_host_path(setup):
+    cfg, case, U, gpu, ora = setup
+    R_ref = ora.residual(U)
+    R = gpu.residual(U)  # numpy in -> host path through the C-ABI
+    assert rel(R, R_ref) <= TOL
+
+
+def test_gradient_and_second_order(setup):
+    cfg, case, U, gpu, ora = setup
+    if not cfg.physics.second_order():
+        pytest.skip("first-order physics")
+    Q_ref = ora.gradient(U)
+    Q = host(gpu.gradient_residual(dev(U)))
+    assert rel(Q, Q_ref) <= TOL
+    # R(U, Q) at an independent Q exercises the K12 path of the residual
+    rng = np.random.default_rng(7)
+    Qr = Q_ref + 0.1 * np.abs(Q_ref).max() * rng.standard_normal(Q_ref.shape)
+    R_ref = ora.residual_uq(U, Qr)
+    R = host(gpu.residual_second_order(dev(U), dev(Qr)))
+    assert rel(R, R_ref) <= TOL
+
+
+def _matrices(cfg):
+    return (LDG_K11, LDG_K12, LDG_K21) if cfg.physics.second_order() else (LDG_K11,)
+
+
+def test_jacobian_pattern_and_values(setup):
+    cfg, case, U, gpu, ora = setup
+    ora.assemble(U)
+    gpu.assemble_jacobians(dev(U))
+    for w in _matrices(cfg):
+        r0, c0, v0 = ora.export_blocks(w)
+        r1, c1, v1 = gpu.export_blocks(w)
+        assert np.array_equal(r0, r1), f"K{w} rows differ"
+        assert np.array_equal(c0, c1), f"K{w} cols differ"
+        assert v1.shape == v0.shape
+        assert rel(v1, v0) <= TOL, (w, rel(v1, v0))
+        info = gpu.pattern_info(w)
+        assert info.nnzb == len(r0)
+
+
+def test_spmv_and_split(setup):
+    cfg, case, U, gpu, ora = setup
+    ora.assemble(U)
+    gpu.assemble_jacobians(dev(U))
+    m = gpu.m
+    x = case.normal_vector(m, cfg.vector_seed)
+    y_ref = ora.spmv(LDG_K11, x)
+    y = host(gpu.spmv(LDG_K11, dev(x)))
+    assert rel(y, y_ref) <= TOL
+    if cfg.physics.second_order():
+        w_ref = ora.spmv(LDG_K21, x)
+        w = host(gpu.spmv(LDG_K21, dev(x)))
+        assert rel(w, w_ref) <= TOL
+        z_ref = ora.spmv(LDG_K12, w_ref)
+        z = host(gpu.spmv(LDG_K12, dev(w_ref)))
+        assert rel(z, z_ref) <= TOL
+    for adt in (0.0, 1e-3, 0.37):
+        s_ref = ora.split_matvec(adt, x)
+        s = host(gpu.split_matvec(adt, dev(x)))
+        assert rel(s, s_ref) <= TOL
+    # alpha_dt = 0 returns v bitwise
+    assert np.array_equal(host(gpu.split_matvec(0.0, dev(x))), x)
+
+
+def test_physical_state_error():
+    cfg = CONFIGS[1]
+    case, U = cfg.build(n=4)
+    gpu = LineDG(case, cfg.physics)
+    U = U.copy()
+    U[4 * 37] = -1.0  # negative density at node 37
+    with pytest.raises(PhysicalStateError) as ei:
+        gpu.residual(dev(U))
+    st = ei.value.state
+    rho, mom, E = st[0], st[1:3], st[3]
+    p = 0.4 * (E - 0.5 * (mom @ mom) / rho) if rho != 0 else -1
+    assert rho <= 0 or p <= 0
+
+
+def test_missing_boundary_condition_is_config_error():
+    case = Case.lattice(2, 3, 2)
+    with pytest.raises(ConfigError):
+        LineDG(case, Physics(_abi.LDG_EULER))
+
+
+@pytest.mark.slow
+def test_full_c2_residual_and_jacobian_rows():
+    cfg = CONFIGS[1]
+    case, U = cfg.build()
+    gpu = LineDG(case, cfg.physics)
+    ora = Oracle(case, cfg.physics)
+    R_ref = ora.residual(U)
+    R = host(gpu.residual(dev(U)))
+    assert rel(R, R_ref) <= TOL
+    rng = np.random.default_rng(3)
+    elems = np.sort(rng.choice(case.E, 64, replace=False)).astype(np.int32)
+    ora.assemble(U, elems=elems)
+    gpu.assemble_jacobians(dev(U))
+    r0, c0, v0 = ora.export_blocks(LDG_K11)
+    keep = np.isin(r0 // case.npe, elems)
+    r1, c1, v1 = gpu.export_blocks(LDG_K11, elems=elems)
+    assert np.array_equal(r0[keep], r1) and np.array_equal(c0[keep], c1)
+    assert rel(v1, v0[keep]) <= TOL
+    # Table 1 on the full config mesh: 2p+5 node columns per K11 row (periodic)
+    info = gpu.pattern_info(LDG_K11)
+    assert info.nnzb == (2 * cfg.p + 5) * case.E * case.npe
