@@ -195,6 +195,43 @@ __device__ __forceinline__ T euler_fn(const T* u, const double* n, double gamma,
   return p;
 }
 
+// Closed-form d(F(u).n)/du (row-major M x M) for the Euler flux.
+template <int D>
+__device__ __forceinline__ void euler_jac_n(const double* u, const double* n, double gamma, double* A,
+                                            bool& ok) {
+  constexpr int M = D + 2;
+  const double g1 = gamma - 1.0;
+  const double rho = u[0], irho = 1.0 / rho;
+  double v[D], un = 0.0, q2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    v[d] = u[1 + d] * irho;
+    un += v[d] * n[d];
+    q2 += v[d] * v[d];
+  }
+  const double p = g1 * (u[D + 1] - 0.5 * rho * q2);
+  ok = ok && (rho > 0.0) && (p > 0.0);
+  const double H = (u[D + 1] + p) * irho;
+  const double hq = 0.5 * g1 * q2;
+  A[0] = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) A[1 + j] = n[j];
+  A[D + 1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double* r = A + (1 + i) * M;
+    r[0] = hq * n[i] - v[i] * un;
+#pragma unroll
+    for (int j = 0; j < D; ++j) r[1 + j] = v[i] * n[j] - g1 * v[j] * n[i] + (i == j ? un : 0.0);
+    r[D + 1] = g1 * n[i];
+  }
+  double* r = A + (D + 1) * M;
+  r[0] = un * (hq - H);
+#pragma unroll
+  for (int j = 0; j < D; ++j) r[1 + j] = H * n[j] - g1 * un * v[j];
+  r[D + 1] = gamma * un;
+}
+
 // Roe flux (u_out = R, u_in = L), outward normal n.
 template <int D, class T>
 __device__ __forceinline__ void roe_fn(const T* uo, const T* ui, const double* n, double gamma,

@@ -119,6 +119,34 @@ __device__ __noinline__ void report_line(const KParams<C>& kp, int e, int dir, i
   report_bad_state<double, M>(kp.err, e, bad, su + bad * M);
 }
 
+// Staged tile -> global.  TMA bulk copy (cp.async.bulk, SASS UBLKCP) when the
+// size and both addresses are 16-byte multiples, else 16/8-byte stores.
+// Must be reached by all threads of the CTA; returns with the smem source
+// free for reuse.
+__device__ __forceinline__ void store_tile(double* __restrict__ gdst, const double* ssrc, int n, int tid,
+                                           int nthr) {
+  const unsigned bytes = static_cast<unsigned>(n) * 8u;
+  const bool bulk = (bytes % 16u) == 0 && ((reinterpret_cast<uintptr_t>(gdst) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(ssrc) & 15) == 0);
+  if (bulk) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(saddr),
+                   "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+    __syncthreads();
+  } else {
+    __syncthreads();
+    for (int i = tid; i < n; i += nthr) gdst[i] = ssrc[i];
+    __syncthreads();
+  }
+}
+
 // ===================================================================== residual
 // FIRST: first-order physics (Q absent).  Otherwise R(U, Q).
 template <class C, int EPB>
@@ -433,7 +461,8 @@ struct JacSmem {
   static constexpr int Q = C::SECOND ? C::NPE * C::MD : 0;
   static constexpr int UO = NLT * 2 * C::M;
   static constexpr int QO = C::SECOND ? NLT * 2 * C::MD : 0;
-  static constexpr int A = NLT * C::NQ * C::B11;              // dF/du . nvec at quad points
+  static constexpr int A = C::HAS_INV ? NLT * C::NQ * C::B11 : 0;  // dFinv/du . nvec at quad points
+  static constexpr int AV = C::VIS_U ? NLT * C::NQ * C::B11 : 0;    // dFvis/du . nvec
   static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
   static constexpr int EIN = NLT * 2 * C::B11;                // endpoint d/du_in
   static constexpr int EOUT = NLT * 2 * C::B11;               // endpoint d/du_out
@@ -442,11 +471,11 @@ struct JacSmem {
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
   static constexpr int STG = ST11 > ST12 ? ST11 : ST12;
   static constexpr int DG = (C::D - 1) * C::NT * (C::B11 > C::B12 ? C::B11 : C::B12);  // diag scratch
-  static constexpr int TOTAL = U + Q + UO + QO + A + BQ + EIN + EOUT + EQ + STG + DG + C::NT;
+  static constexpr int TOTAL = U + Q + UO + QO + A + AV + BQ + EIN + EOUT + EQ + STG + DG + C::NT;
 };
 
 template <class C>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128, 3)
 k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
            double* __restrict__ K11, double* __restrict__ K12) {
   constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
@@ -459,7 +488,8 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   double* suo = sq + SM::Q;
   double* sqo = suo + SM::UO;
   double* sA = sqo + SM::QO;
-  double* sBq = sA + SM::A;
+  double* sAv = sA + SM::A;
+  double* sBq = sAv + SM::AV;
   double* sEin = sBq + SM::BQ;
   double* sEout = sEin + SM::EIN;
   double* sEq = sEout + SM::EOUT;
@@ -495,148 +525,167 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   for (int i = tid; i < SM::STG; i += nthr) stg[i] = 0.0;
   __syncthreads();
 
-  // ---- phase 1: flux Jacobians (forward-mode Dual<M> / Dual<MD>)
+  // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
-  for (int w = tid; w < NLT * NQ; w += nthr) {
-    const int tl = w / NQ, q = w - tl * NQ;
-    int dir, line;
-    TileLines<C>::get(tl, s, dir, line);
-    double nv[D];
+  if (C::HAS_INV) {
+    for (int w = tid; w < NLT * NQ; w += nthr) {
+      const int tl = w / NQ, q = w - tl * NQ;
+      int dir, line;
+      TileLines<C>::get(tl, s, dir, line);
+      double nv[D], uq[M];
 #pragma unroll
-    for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
-    double uq[M], qq[C::SECOND ? MD : 1];
+      for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
 #pragma unroll
-    for (int c = 0; c < M; ++c) uq[c] = 0.0;
-    if (C::SECOND) {
+      for (int c = 0; c < M; ++c) uq[c] = 0.0;
 #pragma unroll
-      for (int c = 0; c < MD; ++c) qq[c] = 0.0;
-    }
+      for (int t = 0; t < NP; ++t) {
+        const int nd = node_on_line<C>(dir, line, t);
+        const double ph = kp.bt.phi[t][q];
 #pragma unroll
-    for (int t = 0; t < NP; ++t) {
-      const int nd = node_on_line<C>(dir, line, t);
-      const double ph = kp.bt.phi[t][q];
-#pragma unroll
-      for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
-      if (C::SECOND) {
-#pragma unroll
-        for (int c = 0; c < MD; ++c) qq[c] += ph * sq[nd * MD + c];
+        for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
       }
+      bool ok = true;
+      euler_jac_n<D>(uq, nv, kp.pp.gamma, sA + (tl * NQ + q) * B11, ok);
+      if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
-    bool ok = true;
-    if (VOL11) {
-      Dual<M> du[M], f[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        du[c] = Dual<M>(uq[c]);
-        du[c].d[c] = 1.0;
-        f[c] = Dual<M>(0.0);
-      }
-      if (C::HAS_INV) euler_fn<D>(du, nv, kp.pp.gamma, f, ok);
-      if (C::VIS_U) {
-        Dual<M> fv[M];
-        visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(du, qq, nv, kp.pp, fv, ok);
-#pragma unroll
-        for (int c = 0; c < M; ++c) f[c] = f[c] + fv[c];
-      }
-      double* a = sA + (tl * NQ + q) * B11;
-#pragma unroll
-      for (int c = 0; c < M; ++c)
-#pragma unroll
-        for (int b = 0; b < M; ++b) a[c * M + b] = f[c].d[b];
-    }
-    if (C::SECOND) {
-      Dual<SM::NDA> dq[SM::NDA], fv[M];
-#pragma unroll
-      for (int c = 0; c < SM::NDA; ++c) {
-        dq[c] = Dual<SM::NDA>(qq[c]);
-        dq[c].d[c] = 1.0;
-      }
-      visc_fn<D, C::PH, double, Dual<SM::NDA>, Dual<SM::NDA>>(uq, dq, nv, kp.pp, fv, ok);
-      double* bq = sBq + (tl * NQ + q) * M * MD;
-#pragma unroll
-      for (int c = 0; c < M; ++c)
-#pragma unroll
-        for (int b = 0; b < MD; ++b) bq[c * MD + b] = fv[c].d[b];
-    }
-    if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
   }
-  // endpoint items: (tile line, side, pass) pass 0: d/du_in, 1: d/du_out, 2: d/dq (selected side)
-  constexpr int NPASS = C::SECOND ? 3 : 2;
-  for (int w = tid; w < NLT * 2 * NPASS; w += nthr) {
-    const int pass = w % NPASS, idx = w / NPASS, tl = idx >> 1, side = idx & 1;
+  // ---- phase 1b: endpoint flux Jacobian columns, one seeded component per
+  // item (forward mode, Dual<1>): pass 0 = d/du_in, pass 1 = d/du_out.
+  for (int w = tid; w < NLT * 2 * 2 * M; w += nthr) {
+    const int bcol = w % M, rest = w / M, pass = rest & 1, idx = rest >> 1;
+    const int tl = idx >> 1, side = idx & 1;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
     const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
     const bool bd = cn.x < 0;
-    const int S = conn_sign(cn.y);
     if (pass == 1 && bd) continue;
-    const int ie = side ? P : 0;
-    const int nd = node_on_line<C>(dir, line, ie);
+    const int S = conn_sign(cn.y);
+    const int nd = node_on_line<C>(dir, line, side ? P : 0);
     double n[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
-    double nn = n[0] * n[0];
-#pragma unroll
-    for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-    nn = sqrt(nn);
     const double* bcp = bd ? kp.bcv + (-1 - cn.x) * M : nullptr;
+    using D1 = Dual<1>;
+    D1 ui[M], uo[M], fh[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) {  // seed by select: no dynamic register indexing
+      ui[c] = D1(su[nd * M + c]);
+      uo[c] = D1(bd ? __ldg(bcp + c) : suo[idx * M + c]);
+      ui[c].d[0] = (pass == 0 && c == bcol) ? 1.0 : 0.0;
+      uo[c].d[0] = (pass == 1 && c == bcol) ? 1.0 : 0.0;
+      fh[c] = D1(0.0);
+    }
     bool ok = true;
-    if (pass < 2) {
-      Dual<M> ui[M], uo[M], fh[M];
+    if (C::HAS_INV) {
+      if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+    }
+    if (C::SECOND) {
+      double nn = n[0] * n[0];
 #pragma unroll
-      for (int c = 0; c < M; ++c) {
-        ui[c] = Dual<M>(su[nd * M + c]);
-        uo[c] = Dual<M>(bd ? __ldg(bcp + c) : suo[idx * M + c]);
-        if (pass == 0) ui[c].d[c] = 1.0;
-        else uo[c].d[c] = 1.0;
-        fh[c] = Dual<M>(0.0);
-      }
-      if (C::HAS_INV) {
-        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-      }
-      if (C::SECOND) {
-        Dual<M> fv[M];
-        if (bd) {
-          visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(ui, sq + nd * MD, n, kp.pp, fv, ok);
-          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+      for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+      nn = sqrt(nn);
+      D1 fv[M];
+      if (bd) {
+        visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
+        const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
 #pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
-        } else {
-          if (S > 0) visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(uo, sqo + idx * MD, n, kp.pp, fv, ok);
-          else visc_fn<D, C::PH, Dual<M>, double, Dual<M>>(ui, sq + nd * MD, n, kp.pp, fv, ok);
+        for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
+      } else {
+        if (S > 0) visc_fn<D, C::PH, D1, double, D1>(uo, sqo + idx * MD, n, kp.pp, fv, ok);
+        else visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
 #pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
-          if (kp.pp.c11 != 0.0) {
+        for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
+        if (kp.pp.c11 != 0.0) {
 #pragma unroll
-            for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
-          }
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
         }
       }
-      double* dst = (pass == 0 ? sEin : sEout) + idx * B11;
+    }
+    double* dst = (pass == 0 ? sEin : sEout) + idx * B11;
 #pragma unroll
-      for (int c = 0; c < M; ++c)
+    for (int c = 0; c < M; ++c) dst[c * M + bcol] = fh[c].d[0];
+    if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
+  }
+  // ---- phase 1c (second-order): viscous flux derivatives, one seed per item
+  if (C::SECOND) {
+    constexpr int NSU = C::VIS_U ? M : 0, NSEED = NSU + MD;
+    for (int w = tid; w < NLT * NQ * NSEED; w += nthr) {
+      const int sd = w % NSEED, tq = w / NSEED, tl = tq / NQ, q = tq - tl * NQ;
+      int dir, line;
+      TileLines<C>::get(tl, s, dir, line);
+      double nv[D], uq[M], qq[MD];
 #pragma unroll
-        for (int b = 0; b < M; ++b) dst[c * M + b] = fh[c].d[b];
-    } else if (C::SECOND) {
-      // viscous endpoint flux w.r.t. the q of the switch-selected side
-      const bool out = !bd && S > 0;
-      Dual<SM::NDA> dqv[SM::NDA], fv[M];
-      const double* qsrc = out ? sqo + idx * MD : sq + nd * MD;
+      for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
 #pragma unroll
-      for (int c = 0; c < SM::NDA; ++c) {
-        dqv[c] = Dual<SM::NDA>(qsrc[c]);
-        dqv[c].d[c] = 1.0;
+      for (int c = 0; c < M; ++c) uq[c] = 0.0;
+#pragma unroll
+      for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        const int nd = node_on_line<C>(dir, line, t);
+        const double ph = kp.bt.phi[t][q];
+#pragma unroll
+        for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
+#pragma unroll
+        for (int c = 0; c < MD; ++c) qq[c] += ph * sq[nd * MD + c];
       }
+      bool ok = true;
+      using D1 = Dual<1>;
+      D1 fv[M];
+      if (sd < NSU) {
+        D1 du[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          du[c] = D1(uq[c]);
+          du[c].d[0] = c == sd ? 1.0 : 0.0;
+        }
+        visc_fn<D, C::PH, D1, double, D1>(du, qq, nv, kp.pp, fv, ok);
+        double* a = sAv + (tl * NQ + q) * B11;
+#pragma unroll
+        for (int c = 0; c < M; ++c) a[c * M + sd] = fv[c].d[0];
+      } else {
+        const int bq = sd - NSU;
+        D1 dq[MD];
+#pragma unroll
+        for (int c = 0; c < MD; ++c) {
+          dq[c] = D1(qq[c]);
+          dq[c].d[0] = c == bq ? 1.0 : 0.0;
+        }
+        visc_fn<D, C::PH, double, D1, D1>(uq, dq, nv, kp.pp, fv, ok);
+        double* bqp = sBq + (tl * NQ + q) * M * MD;
+#pragma unroll
+        for (int c = 0; c < M; ++c) bqp[c * MD + bq] = fv[c].d[0];
+      }
+      if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
+    }
+    // endpoint d/dq of the switch-selected side's viscous flux
+    for (int w = tid; w < NLT * 2 * MD; w += nthr) {
+      const int bq = w % MD, idx = w / MD, tl = idx >> 1, side = idx & 1;
+      int dir, line;
+      TileLines<C>::get(tl, s, dir, line);
+      const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+      const bool out = cn.x >= 0 && conn_sign(cn.y) > 0;
+      const int nd = node_on_line<C>(dir, line, side ? P : 0);
+      double n[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
+      using D1 = Dual<1>;
+      const double* qsrc = out ? sqo + idx * MD : sq + nd * MD;
       const double* usrc = out ? suo + idx * M : su + nd * M;
-      visc_fn<D, C::PH, double, Dual<SM::NDA>, Dual<SM::NDA>>(usrc, dqv, n, kp.pp, fv, ok);
+      D1 dqv[MD], fv[M];
+#pragma unroll
+      for (int c = 0; c < MD; ++c) {
+        dqv[c] = D1(qsrc[c]);
+        dqv[c].d[0] = c == bq ? 1.0 : 0.0;
+      }
+      bool ok = true;
+      visc_fn<D, C::PH, double, D1, D1>(usrc, dqv, n, kp.pp, fv, ok);
       double* dst = sEq + idx * M * MD;
 #pragma unroll
-      for (int c = 0; c < M; ++c)
-#pragma unroll
-        for (int b = 0; b < MD; ++b) dst[c * MD + b] = fv[c].d[b];
+      for (int c = 0; c < M; ++c) dst[c * MD + bq] = fv[c].d[0];
+      if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
-    if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
   }
   __syncthreads();
 
@@ -664,7 +713,8 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     const bool full = C::D == 2 || dir < 2;
     double av[NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? sA[(tl * NQ + q) * B11 + ab] : 0.0;
+    for (int q = 0; q < NQ; ++q)
+      av[q] = (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
     const double ein0 = sEin[(tl * 2 + 0) * B11 + ab], ein1 = sEin[(tl * 2 + 1) * B11 + ab];
     const double eo0 = sEout[(tl * 2 + 0) * B11 + ab], eo1 = sEout[(tl * 2 + 1) * B11 + ab];
     const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
@@ -705,18 +755,8 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     stg[(x0 * B11 + ab) * NT + r] = v;
   }
   __syncthreads();
-  {
-    double2* dst = reinterpret_cast<double2*>(K11 + static_cast<size_t>(T) * SM::ST11);
-    const double2* src = reinterpret_cast<const double2*>(stg);
-    if ((SM::ST11 & 1) == 0) {
-      for (int i = tid; i < SM::ST11 / 2; i += nthr) dst[i] = src[i];
-    } else {
-      double* d1 = K11 + static_cast<size_t>(T) * SM::ST11;
-      for (int i = tid; i < SM::ST11; i += nthr) d1[i] = stg[i];
-    }
-  }
+  store_tile(K11 + static_cast<size_t>(T) * SM::ST11, stg, SM::ST11, tid, nthr);
   if (!C::SECOND) return;
-  __syncthreads();
 
   // ---- phase 3: K12 = dR/dQ (rows a' of the stored block)
   constexpr int B12 = C::B12, R12 = C::R12, A0 = C::PH == PH_NS ? 1 : 0;
@@ -771,16 +811,7 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     stg[(x0 * B12 + ab) * NT + r] = v;
   }
   __syncthreads();
-  {
-    double* d1 = K12 + static_cast<size_t>(T) * SM::ST12;
-    if ((SM::ST12 & 1) == 0) {
-      double2* dst = reinterpret_cast<double2*>(d1);
-      const double2* src = reinterpret_cast<const double2*>(stg);
-      for (int i = tid; i < SM::ST12 / 2; i += nthr) dst[i] = src[i];
-    } else {
-      for (int i = tid; i < SM::ST12; i += nthr) d1[i] = stg[i];
-    }
-  }
+  store_tile(K12 + static_cast<size_t>(T) * SM::ST12, stg, SM::ST12, tid, nthr);
 }
 
 // K21 = dQ/dU (U-independent; D scalars per node pair):

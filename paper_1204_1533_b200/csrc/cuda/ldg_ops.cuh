@@ -102,7 +102,7 @@ struct Launch {
       cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       init = true;
     }
-    k_jacobian<C><<<d.E * C::TPE, 256, smem, d.stream>>>(params(d), U, Q, K11, K12);
+    k_jacobian<C><<<d.E * C::TPE, 128, smem, d.stream>>>(params(d), U, Q, K11, K12);
     count(d);
     return cudaGetLastError();
   }
