@@ -74,6 +74,7 @@ struct Launch {
     static bool init = false;
     if (!init) {
       cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       init = true;
     }
     const int grid = (d.E + EPB - 1) / EPB;
@@ -87,6 +88,7 @@ struct Launch {
     static bool init = false;
     if (!init) {
       cudaFuncSetAttribute(k_gradient<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_gradient<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       init = true;
     }
     const int grid = (d.E + EPB - 1) / EPB;
@@ -100,6 +102,7 @@ struct Launch {
     static bool init = false;
     if (!init) {
       cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       init = true;
     }
     k_jacobian<C><<<d.E * C::TPE, 128, smem, d.stream>>>(params(d), U, Q, K11, K12);
