@@ -122,6 +122,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def _kernels_per_step(ctx, step, stream, torch):
+    """Kernel launches the library issues for one step (its own counter)."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    n0 = ctx.kernel_launches()
+    with torch.cuda.stream(stream):
+        step(ev)
+    stream.synchronize()
+    return ctx.kernel_launches() - n0
+
+
 # ---------------------------------------------------------------- CPU leg
 def cpu_step_fn(cfg, case, U, x):
     from oracle.pyoracle import Oracle  # CPU baseline leg only
@@ -179,7 +189,7 @@ def main():
     m = cfg.physics.components(cfg.dim)
     workload = {"workload": cfg.name, "config_index": args.config, "elements": cfg.n ** cfg.dim,
                 "p": cfg.p, "dofs": cfg.dofs(), "step": "residual + Jacobian assembly + K11 block-SpMV",
-                "l2": "flushed between steps (512 MB write)", "parallelism": "replicas" if world > 1 else "1 GPU"}
+                "l2": "flushed between steps (512 MB write + 512 MB read)", "parallelism": "replicas" if world > 1 else "1 GPU"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -213,49 +223,82 @@ def main():
     x = case.normal_vector(m, cfg.vector_seed)
     N = case.E * case.npe
     dofs = N * m
-    ctx = LineDG(case, cfg.physics)
+    stream = torch.cuda.Stream()
+    ctx = LineDG(case, cfg.physics, stream=stream)
     src = cfg.source_for(case)
     if src is not None:
         ctx.set_source(src)
     Ud = torch.from_numpy(U).cuda()
     xd = torch.from_numpy(x).cuda()
-    flush = torch.empty(128 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 512 MB > 126 MB L2
+    # L2 flush between steps: write 512 MB (> 126 MB L2), then read another
+    # 512 MB so the lines left in L2 are clean (no write-back lands in the
+    # next timed kernel).
+    fbuf = torch.empty(128 * 1024 * 1024, dtype=torch.int32, device="cuda")
+    rbuf = torch.ones(128 * 1024 * 1024, dtype=torch.int32, device="cuda")
+    fsink = torch.empty((), dtype=torch.int64, device="cuda")
+
+    class _Flush:
+        @staticmethod
+        def zero_():
+            fbuf.zero_()
+            torch.sum(rbuf, dim=0, out=fsink)
+
+    flush = _Flush()
+    torch.cuda.synchronize()
     ctx.set_sync_errors(False)
 
     def step(ev):
-        ev[0].record()
-        R = ctx.residual(Ud)
-        ev[1].record()
+        ev[0].record(stream)
+        ctx.residual(Ud)
+        ev[1].record(stream)
         ctx.assemble_jacobians(Ud)
-        ev[2].record()
-        y = ctx.spmv(LDG_K11, xd)
-        ev[3].record()
-        return R, y
+        ev[2].record(stream)
+        ctx.spmv(LDG_K11, xd)
+        ev[3].record(stream)
 
-    for _ in range(args.warmup):
-        flush.zero_()
-        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup)):
+            flush.zero_()
+            step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
     ctx.synchronize()
+    # Each op of the step is captured once as a CUDA graph and replayed; the
+    # event pairs around the replays time each kernel on the launching
+    # stream.  The 512 MB L2-flush kernel ahead of every step keeps the host
+    # ahead of the GPU, so no host launch gap falls inside a timed interval.
+    ops = [lambda: ctx.residual(Ud), lambda: ctx.assemble_jacobians(Ud), lambda: ctx.spmv(LDG_K11, xd)]
+    graphs = []
+    for op in ops:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            op()
+        graphs.append(g)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sampler = ClockSampler(local)
     sampler.start()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    launches0 = ctx.kernel_launches()
-    for k in range(args.steps):
-        flush.zero_()
-        step(evs[k])
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            for i, g in enumerate(graphs):
+                g.replay()
+                evs[k][i + 1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    launches = ctx.kernel_launches() - launches0
     clocks = sampler.stop()
     ctx.synchronize()  # surfaces any physical-state failure of the timed steps
-    t_res = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    t_jac = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-    t_spv = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
-    ms = statistics.mean(e[0].elapsed_time(e[3]) for e in evs)
+    per = [(e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[0].elapsed_time(e[3]))
+           for e in evs]
+    # kernels per step: counted by the library while capturing the step
+    n_per_step = _kernels_per_step(ctx, step, stream, torch)
+    launches = n_per_step * args.steps
+    t_res = statistics.mean(p[0] for p in per)
+    t_jac = statistics.mean(p[1] for p in per)
+    t_spv = statistics.mean(p[2] for p in per)
+    ms = statistics.mean(p[3] for p in per)
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -267,16 +310,18 @@ def main():
     xh = torch.from_numpy(x).pin_memory().numpy()
     ctx.set_sync_errors(True)
     e2e_times = []
+    torch.cuda.set_stream(stream)
     for k in range(args.warmup + args.steps):
-        flush.zero_()
+        with torch.cuda.stream(stream):
+            flush.zero_()
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
+        t0.record(stream)
         ctx.residual(Uh)
         ctx.assemble_jacobians(Uh)
         ctx.spmv(LDG_K11, xh)
-        t1.record()
+        t1.record(stream)
         torch.cuda.synchronize()
         if k >= args.warmup:
             e2e_times.append(t0.elapsed_time(t1))

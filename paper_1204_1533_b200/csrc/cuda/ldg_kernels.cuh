@@ -326,6 +326,191 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
   }
 }
 
+// Sub-warp residual: a group of G = n_q lanes per line (one lane per
+// quadrature point), GPW = 32 / G groups per warp.  Lane j interpolates the
+// state to its quadrature point and evaluates the flux there; the projection
+// r_i = sum_q dq[i][q] f_q is a lane transpose through warp shuffles (lane i
+// gathers f_q from lanes q); lanes 0 and 1 evaluate the endpoint numerical
+// fluxes of sides 0 and 1 and broadcast them for the M^-1 lifting.
+template <class C>
+struct SubWarp {
+  static constexpr int G = C::NQ;
+  static constexpr int GPW = 32 / G;
+  static constexpr int EPB_RAW = (6 * GPW + C::LPE - 1) / C::LPE;
+  static constexpr int EPB = EPB_RAW < 1 ? 1 : EPB_RAW;
+  static constexpr int LINES = EPB * C::LPE;
+  static constexpr int WARPS = (LINES + GPW - 1) / GPW;
+  static constexpr int THREADS = WARPS * 32;
+};
+
+template <class C>
+__global__ void __launch_bounds__(SubWarp<C>::THREADS, 2)
+k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+              double* __restrict__ R) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD,
+                LPE = C::LPE, P = C::P;
+  using SW = SubWarp<C>;
+  constexpr int EPB = SW::EPB, G = SW::G, GPW = SW::GPW;
+  extern __shared__ double smem[];
+  double* su = smem;                                      // [EPB][NPE*M]
+  double* sq = su + EPB * NPE * M;                        // [EPB][NPE*MD]
+  double* sacc = sq + (C::SECOND ? EPB * NPE * MD : 0);   // [EPB][D][NPE*M]
+  double* sphi = sacc + EPB * D * NPE * M;                // [NP][NQ]
+  double* sdq = sphi + NP * NQ;                           // [NP][NQ]
+  const int k0 = blockIdx.x * EPB;
+  const int nb = min(EPB, kp.E - k0);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < NP * NQ; i += nthr) {
+    sphi[i] = (&kp.bt.phi[0][0])[i];
+    sdq[i] = (&kp.bt.dq[0][0])[i];
+  }
+  for (int i = tid; i < NP * 2; i += nthr) sdq[NP * NQ + i] = (&kp.bt.mi[0][0])[i];
+  for (int le = 0; le < nb; ++le) {
+    const size_t e = kp.order[k0 + le];
+    cp_elem<C>(su + le * NPE * M, U + e * (NPE * M), NPE * M, tid, nthr);
+    if (C::SECOND) cp_elem<C>(sq + le * NPE * MD, Q + e * (NPE * MD), NPE * MD, tid, nthr);
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane / G, j = lane - g * G;
+  const int gl = warp * GPW + g;  // line within the CTA
+  const int le = gl / LPE;
+  const bool act = g < GPW && le < nb;
+  const int rem = gl - le * LPE;
+  const int dir = rem / NL, line = rem - dir * NL;
+  const int k = k0 + (act ? le : 0);
+  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+  const double* sul = su + (act ? le : 0) * NPE * M;
+  const double* sql = sq + (act ? le : 0) * NPE * MD;
+  bool ok = true;
+  // quadrature-point flux (lane j < NQ)
+  double f[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) f[c] = 0.0;
+  if (act) {
+    double uq[M], qq[C::SECOND ? MD : 1];
+#pragma unroll
+    for (int c = 0; c < M; ++c) uq[c] = 0.0;
+    if (C::SECOND) {
+#pragma unroll
+      for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      const int nd = node_on_line<C>(dir, line, t);
+      const double ph = sphi[t * NQ + j];
+#pragma unroll
+      for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
+      if (C::SECOND) {
+#pragma unroll
+        for (int c = 0; c < MD; ++c) qq[c] += ph * sql[nd * MD + c];
+      }
+    }
+    double nv[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + j) * D + d);
+    if (C::HAS_INV) euler_fn<D>(uq, nv, kp.pp.gamma, f, ok);
+    if (C::SECOND) {
+      double fv[M];
+      visc_fn<D, C::PH, double, double, double>(uq, qq, nv, kp.pp, fv, ok);
+#pragma unroll
+      for (int c = 0; c < M; ++c) f[c] += fv[c];
+    }
+  }
+  // endpoint numerical flux: lane 0 -> side 0, lane 1 -> side 1
+  double fh[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) fh[c] = 0.0;
+  if (act && j < 2) {
+    const int side = j;
+    const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+    const int S = conn_sign(cn.y);
+    const int nd = node_on_line<C>(dir, line, side ? P : 0);
+    double n[D], ui[M], uo[M];
+#pragma unroll
+    for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
+    const double* bcp = cn.x < 0 ? kp.bcv + (-1 - cn.x) * M : nullptr;
+    size_t ond = 0;
+    if (!bcp) ond = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      ui[c] = sul[nd * M + c];
+      uo[c] = bcp ? __ldg(bcp + c) : __ldg(U + ond * M + c);
+    }
+    if (C::HAS_INV) {
+      if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+    }
+    if (C::SECOND) {
+      double nn = n[0] * n[0];
+#pragma unroll
+      for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+      nn = sqrt(nn);
+      double fv[M];
+      if (bcp) {
+        visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+        const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+        for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - uo[c]);
+      } else {
+        if (S > 0) {
+          double qo[MD];
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qo[c] = __ldg(Q + ond * MD + c);
+          visc_fn<D, C::PH, double, double, double>(uo, qo, n, kp.pp, fv, ok);
+        } else {
+          visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) fh[c] += fv[c];
+        if (kp.pp.c11 != 0.0) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
+        }
+      }
+    }
+  }
+  // lane transpose: lane i < NP forms r_i
+  const int base = g * G;
+  double r[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) r[c] = 0.0;
+  const int i = j < NP ? j : 0;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double w = sdq[i * NQ + q];
+#pragma unroll
+    for (int c = 0; c < M; ++c) r[c] += w * __shfl_sync(0xffffffffu, f[c], base + q);
+  }
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    const double fm = __shfl_sync(0xffffffffu, fh[c], base + 0);
+    const double fp = __shfl_sync(0xffffffffu, fh[c], base + 1);
+    r[c] += sdq[NP * NQ + i * 2 + 0] * fm + sdq[NP * NQ + i * 2 + 1] * fp;
+  }
+  if (act && j < NP) {
+    double* acc = sacc + (le * D + dir) * NPE * M;
+    const int nd = node_on_line<C>(dir, line, j);
+#pragma unroll
+    for (int c = 0; c < M; ++c) acc[nd * M + c] = r[c];
+  }
+  if (!ok) report_line<C>(kp, kp.order[k], dir, line, sul);
+  __syncthreads();
+  for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
+    const int l = idx / (NPE * M), off = idx - l * NPE * M;
+    const int nd = off / M;
+    const int kk = k0 + l;
+    const size_t e = kp.order[kk];
+    const double* a = sacc + l * D * NPE * M + off;
+    double sum = a[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
+    const double invJ = __ldg(kp.metric + static_cast<size_t>(kk) * C::METP + C::MET_NV + C::MET_NE + nd);
+    const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
+    R[e * (NPE * M) + off] = src - invJ * sum;
+  }
+}
+
 // ===================================================================== gradient
 // Q = (1/J) sum_dir d^(dir),  d = M^-1 [u_hat (x) n |ends - sum_q w phi' u_q (x) nvec_q]
 template <class C, int EPB>
@@ -522,7 +707,6 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       }
     }
   }
-  for (int i = tid; i < SM::STG; i += nthr) stg[i] = 0.0;
   __syncthreads();
 
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
@@ -549,10 +733,12 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
   }
-  // ---- phase 1b: endpoint flux Jacobian columns, one seeded component per
-  // item (forward mode, Dual<1>): pass 0 = d/du_in, pass 1 = d/du_out.
-  for (int w = tid; w < NLT * 2 * 2 * M; w += nthr) {
-    const int bcol = w % M, rest = w / M, pass = rest & 1, idx = rest >> 1;
+  // ---- phase 1b: endpoint flux Jacobian columns.  One item per (line end,
+  // pass); pass 0 = d/du_in, 1 = d/du_out.  The seeded components run
+  // sequentially in one thread (forward mode, Dual<1>), so the primal part of
+  // the flux is common to all seeds and is computed once by the compiler.
+  for (int w = tid; w < NLT * 2 * 2; w += nthr) {
+    const int pass = w & 1, idx = w >> 1;
     const int tl = idx >> 1, side = idx & 1;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
@@ -564,47 +750,56 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     double n[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
+    double nn = n[0] * n[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+    nn = sqrt(nn);
     const double* bcp = bd ? kp.bcv + (-1 - cn.x) * M : nullptr;
-    using D1 = Dual<1>;
-    D1 ui[M], uo[M], fh[M];
+    double uiv[M], uov[M];
 #pragma unroll
-    for (int c = 0; c < M; ++c) {  // seed by select: no dynamic register indexing
-      ui[c] = D1(su[nd * M + c]);
-      uo[c] = D1(bd ? __ldg(bcp + c) : suo[idx * M + c]);
-      ui[c].d[0] = (pass == 0 && c == bcol) ? 1.0 : 0.0;
-      uo[c].d[0] = (pass == 1 && c == bcol) ? 1.0 : 0.0;
-      fh[c] = D1(0.0);
-    }
-    bool ok = true;
-    if (C::HAS_INV) {
-      if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-      else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-    }
-    if (C::SECOND) {
-      double nn = n[0] * n[0];
-#pragma unroll
-      for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-      nn = sqrt(nn);
-      D1 fv[M];
-      if (bd) {
-        visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
-        const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
-#pragma unroll
-        for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
-      } else {
-        if (S > 0) visc_fn<D, C::PH, D1, double, D1>(uo, sqo + idx * MD, n, kp.pp, fv, ok);
-        else visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
-#pragma unroll
-        for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
-        if (kp.pp.c11 != 0.0) {
-#pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
-        }
-      }
+    for (int c = 0; c < M; ++c) {
+      uiv[c] = su[nd * M + c];
+      uov[c] = bd ? __ldg(bcp + c) : suo[idx * M + c];
     }
     double* dst = (pass == 0 ? sEin : sEout) + idx * B11;
+    bool ok = true;
+    using D1 = Dual<1>;
 #pragma unroll
-    for (int c = 0; c < M; ++c) dst[c * M + bcol] = fh[c].d[0];
+    for (int bcol = 0; bcol < M; ++bcol) {
+      D1 ui[M], uo[M], fh[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        ui[c] = D1(uiv[c]);
+        uo[c] = D1(uov[c]);
+        ui[c].d[0] = (pass == 0 && c == bcol) ? 1.0 : 0.0;
+        uo[c].d[0] = (pass == 1 && c == bcol) ? 1.0 : 0.0;
+        fh[c] = D1(0.0);
+      }
+      if (C::HAS_INV) {
+        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      }
+      if (C::SECOND) {
+        D1 fv[M];
+        if (bd) {
+          visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
+          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
+        } else {
+          if (S > 0) visc_fn<D, C::PH, D1, double, D1>(uo, sqo + idx * MD, n, kp.pp, fv, ok);
+          else visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
+          if (kp.pp.c11 != 0.0) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) dst[c * M + bcol] = fh[c].d[0];
+    }
     if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
   }
   // ---- phase 1c (second-order): viscous flux derivatives, one seed per item
@@ -734,8 +929,8 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
         row_slot_store(dir, line, i, t, sc * v, stg, B11, ab, 0);
       }
       const int r = nd - s * NT;
-      if (c0.x >= 0) stg[((C::D * P + 1 + 2 * dir + 0) * B11 + ab) * NT + r] = sc * (kp.bt.mi[i][0] * eo0);
-      if (c1.x >= 0) stg[((C::D * P + 1 + 2 * dir + 1) * B11 + ab) * NT + r] = sc * (kp.bt.mi[i][1] * eo1);
+      stg[((C::D * P + 1 + 2 * dir + 0) * B11 + ab) * NT + r] = c0.x >= 0 ? sc * (kp.bt.mi[i][0] * eo0) : 0.0;
+      stg[((C::D * P + 1 + 2 * dir + 1) * B11 + ab) * NT + r] = c1.x >= 0 ? sc * (kp.bt.mi[i][1] * eo1) : 0.0;
     };
     if (full) {
 #pragma unroll

@@ -69,16 +69,17 @@ struct Launch {
   }
 
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
-    const size_t smem = sizeof(double) *
-                        (EPB * C::NPE * C::M + (C::SECOND ? EPB * C::NPE * C::MD : 0) + EPB * C::D * C::NPE * C::M);
+    using SW = SubWarp<C>;
+    const size_t smem = sizeof(double) * (SW::EPB * C::NPE * C::M + (C::SECOND ? SW::EPB * C::NPE * C::MD : 0) +
+                                          SW::EPB * C::D * C::NPE * C::M + 2 * C::NP * C::NQ + 2 * C::NP);
     static bool init = false;
     if (!init) {
-      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(k_residual_sw<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_residual_sw<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       init = true;
     }
-    const int grid = (d.E + EPB - 1) / EPB;
-    k_residual<C, EPB><<<grid, RTHREADS, smem, d.stream>>>(params(d), U, Q, R);
+    const int grid = (d.E + SW::EPB - 1) / SW::EPB;
+    k_residual_sw<C><<<grid, SW::THREADS, smem, d.stream>>>(params(d), U, Q, R);
     count(d);
     return cudaGetLastError();
   }
