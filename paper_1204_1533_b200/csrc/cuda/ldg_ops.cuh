@@ -68,7 +68,24 @@ struct Launch {
     if (d.launches) ++*d.launches;
   }
 
+  // Residual: thread-per-line kernel (k_residual).  The sub-warp variant
+  // (k_residual_sw) is kept for comparison: it measured slower on B200
+  // (profiles/ncu_r1_summary.md).
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
+    const size_t smem = sizeof(double) *
+                        (EPB * C::NPE * C::M + (C::SECOND ? EPB * C::NPE * C::MD : 0) + EPB * C::D * C::NPE * C::M);
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      init = true;
+    }
+    const int grid = (d.E + EPB - 1) / EPB;
+    k_residual<C, EPB><<<grid, RTHREADS, smem, d.stream>>>(params(d), U, Q, R);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t residual_sw(const DevCtx& d, const double* U, const double* Q, double* R) {
     using SW = SubWarp<C>;
     const size_t smem = sizeof(double) * (SW::EPB * C::NPE * C::M + (C::SECOND ? SW::EPB * C::NPE * C::MD : 0) +
                                           SW::EPB * C::D * C::NPE * C::M + 2 * C::NP * C::NQ + 2 * C::NP);
