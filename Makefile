@@ -29,12 +29,17 @@ $(PKG)/liblinedg_b200.so: $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 $(PKG)/liblinedg_host.so: $(HOSTDIR)/linedg_host.cpp $(HOSTDIR)/lh_capi.cpp $(HOSTDIR)/linedg_host.hpp include/linedg_b200.h
-	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOSTDIR)/linedg_host.cpp $(HOSTDIR)/lh_capi.cpp
+	$(CXX) $(CXXFLAGS) -ffp-contract=off -shared -o $@ $(HOSTDIR)/linedg_host.cpp $(HOSTDIR)/lh_capi.cpp
 
 oracle/liblinedg_oracle.so: oracle/oracle.cpp oracle/oracle_physics.hpp include/linedg_b200.h
 	$(CXX) $(CXXFLAGS) -fopenmp -shared -o $@ oracle/oracle.cpp
 
+# The reference's own setup sources against the Eigen shim (test infrastructure;
+# skipped when /root/reference is absent).
+ref:
+	./oracle/ref_build/build.sh
+
 clean:
 	rm -rf build $(PKG)/*.so oracle/*.so
 
-.PHONY: all clean
+.PHONY: all clean ref

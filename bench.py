@@ -122,6 +122,23 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def max_over_ranks(x: float, device: str = "cuda") -> float:
+    """Max of a per-rank time over all ranks (NCCL on the GPU run, gloo in tests)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(dofs_per_rank: int, world: int, ms_max: float) -> float:
+    """Whole-job GDOF/s of N independent replicas timed as the max over ranks."""
+    return world * dofs_per_rank / (ms_max * 1e-3) / 1e9
+
+
 def _kernels_per_step(ctx, step, stream, torch):
     """Kernel launches the library issues for one step (its own counter)."""
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -299,11 +316,8 @@ def main():
     t_jac = statistics.mean(p[1] for p in per)
     t_spv = statistics.mean(p[2] for p in per)
     ms = statistics.mean(p[3] for p in per)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * dofs / (ms * 1e-3) / 1e9
+    ms = max_over_ranks(ms)
+    value = replica_throughput(dofs, world, ms)
 
     # ---- end to end through the host-buffer C-ABI (pinned host memory)
     Uh = torch.from_numpy(U).pin_memory().numpy()
@@ -326,10 +340,7 @@ def main():
         if k >= args.warmup:
             e2e_times.append(t0.elapsed_time(t1))
     e2e_ms = statistics.mean(e2e_times)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms)
 
     # ---- roofline of the dominant kernel
     hbm, peak_src = peaks()

@@ -1155,3 +1155,39 @@ int lo_fd_dense(lo_ctx* x, int32_t which, const double* U, const double* Q, doub
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// Point physics for the SPEC.md known-answer tests (physics module,
+// SPEC.md:309-364).  Return 0 or 1 (physical-state error).
+extern "C" {
+
+int lo_euler_flux(int32_t D, const double* u, double gamma, double* F) {
+  return guarded([&] {
+    Gas g;
+    g.gamma = gamma;
+    euler_flux(D, u, g, F);
+  });
+}
+
+int lo_riemann(int32_t kind, int32_t D, const double* uo, const double* ui, const double* n, double gamma,
+               double* fh) {
+  return guarded([&] {
+    Gas g;
+    g.gamma = gamma;
+    if (kind == LDG_ROE) roe_flux(D, uo, ui, n, g, fh);
+    else llf_flux(D, uo, ui, n, g, fh);
+  });
+}
+
+int lo_ns_viscous_flux(int32_t D, const double* u, const double* q, double gamma, double mu, double pr,
+                       double* F) {
+  return guarded([&] {
+    Gas g;
+    g.gamma = gamma;
+    g.mu = mu;
+    g.prandtl = pr;
+    ns_viscous_flux(D, u, q, g, F);
+  });
+}
+
+}  // extern "C"

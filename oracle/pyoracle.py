@@ -55,6 +55,9 @@ def lib():
         L.lo_spmv.argtypes = [vp, C.c_int32, _dp, _dp]
         L.lo_split_matvec.argtypes = [vp, C.c_double, _dp, _dp]
         L.lo_fd_dense.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
+        L.lo_euler_flux.argtypes = [C.c_int32, _dp, C.c_double, _dp]
+        L.lo_riemann.argtypes = [C.c_int32, C.c_int32, _dp, _dp, _dp, C.c_double, _dp]
+        L.lo_ns_viscous_flux.argtypes = [C.c_int32, _dp, _dp, C.c_double, C.c_double, C.c_double, _dp]
         _lib = L
     return _lib
 

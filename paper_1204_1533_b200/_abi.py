@@ -126,6 +126,9 @@ def host_lib() -> C.CDLL:
         L.lh_case_elements.restype = _ip
         L.lh_case_switch_violations.argtypes = [C.c_void_p]
         L.lh_case_num_boundary_faces.argtypes = [C.c_void_p]
+        L.lh_case_num_tag_lines.argtypes = [C.c_void_p]
+        L.lh_case_tag_lines.argtypes = [C.c_void_p, _ip]
+        L.lh_case_tag_lines.restype = None
         L.lh_basis.argtypes = [C.c_int32, C.c_int32] + [_dp] * 8
         L.lh_gauss_legendre.argtypes = [C.c_int32, _dp, _dp]
         L.lh_fill_state.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _dp, C.c_uint64, _dp]

@@ -168,6 +168,15 @@ class Case:
         return np.ctypeslib.as_array(self._lib.lh_case_elements(self._h),
                                      shape=(self.E * vpe,)).copy().reshape(self.E, vpe)
 
+    def tag_lines(self) -> np.ndarray:
+        """(n, 3) boundary tag lines (elem, local_face, tag) of a lattice case,
+        recorded before periodic pairing (the reference mesh-file form)."""
+        n = self._lib.lh_case_num_tag_lines(self._h)
+        out = np.zeros(3 * n, dtype=np.int32)
+        if n:
+            self._lib.lh_case_tag_lines(self._h, _abi.iptr(out))
+        return out.reshape(n, 3)
+
     def switch_violations(self) -> int:
         return self._lib.lh_case_switch_violations(self._h)
 

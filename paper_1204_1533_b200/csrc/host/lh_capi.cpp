@@ -29,6 +29,7 @@ struct lh_case {
   std::vector<int8_t> sw;
   Mapping map;
   std::vector<int32_t> fel, ffl, fer, ffr, for_, ftag, ef;
+  std::vector<int> tag_lines;
   ldg_setup setup{};
   void flatten() {
     const int nf = mesh.nf();
@@ -108,7 +109,7 @@ int lh_case_lattice(const lh_lattice_params* prm, lh_case** out) {
     s.seed_perm = prm->seed_perm;
     s.seed_rot = prm->seed_rot;
     c->basis = make_basis(prm->p, prm->gll != 0);
-    c->mesh = make_lattice_mesh(s);
+    c->mesh = make_lattice_mesh(s, &c->tag_lines);
     finish_case(c.get());
     *out = c.release();
     return LDG_OK;
@@ -152,6 +153,10 @@ int lh_case_custom(int32_t dim, int32_t p, int32_t gll, int32_t nv, const double
 }
 
 void lh_case_free(lh_case* c) { delete c; }
+int32_t lh_case_num_tag_lines(const lh_case* c) { return static_cast<int32_t>(c->tag_lines.size() / 3); }
+void lh_case_tag_lines(const lh_case* c, int32_t* out) {
+  for (size_t i = 0; i < c->tag_lines.size(); ++i) out[i] = c->tag_lines[i];
+}
 const ldg_setup* lh_case_setup(const lh_case* c) { return &c->setup; }
 int32_t lh_case_num_vertices(const lh_case* c) { return c->mesh.nv(); }
 const double* lh_case_vertices(const lh_case* c) { return c->mesh.verts.data(); }

@@ -844,7 +844,7 @@ std::vector<std::array<int, 8>> cube_rotations() {
 
 }  // namespace
 
-Mesh make_lattice_mesh(const LatticeSpec& s) {
+Mesh make_lattice_mesh(const LatticeSpec& s, std::vector<int>* tag_lines) {
   const int D = s.dim, n = s.n, nv1 = n + 1;
   if (D != 2 && D != 3) throw config_error("lattice: dim must be 2 or 3");
   if (n < 1) throw config_error("lattice: n must be >= 1");
@@ -955,6 +955,11 @@ Mesh make_lattice_mesh(const LatticeSpec& s) {
       }
     }
     f.tag = tag;
+    if (tag_lines) {
+      tag_lines->push_back(f.elem_l);
+      tag_lines->push_back(f.face_l);
+      tag_lines->push_back(tag);
+    }
   }
   if (s.periodic) {
     if (D == 2) {

@@ -115,6 +115,8 @@ struct LatticeSpec {
 };
 // Boundary tags before pairing: 2-D 1=bottom 2=right 3=top 4=left;
 // 3-D 1=x- 2=x+ 3=y- 4=y+ 5=z- 6=z+.
-Mesh make_lattice_mesh(const LatticeSpec& s);
+// tag_lines (optional): the boundary tag lines (elem, local_face, tag) as a
+// reference mesh file would carry them, recorded before periodic pairing.
+Mesh make_lattice_mesh(const LatticeSpec& s, std::vector<int>* tag_lines = nullptr);
 
 }  // namespace ldgh

@@ -1,0 +1,457 @@
+"""Known-answer tests that pin the CPU oracle and the setup library
+(SPEC.md's [TRIVIAL]/[DERIVED]/[PAPER] examples, the Table-1 integer goldens
+of PAPER.md:382/385, and the acceptance properties).  CPU only.
+"""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Oracle, OraclePhysicalStateError, lib as olib
+from paper_1204_1533_b200 import CONFIGS, LDG_K11, LDG_K12, LDG_K21, Case, Physics, _abi
+from paper_1204_1533_b200._abi import dptr, host_lib
+from paper_1204_1533_b200.linedg import ConfigError
+
+G = 1.4
+rng = np.random.default_rng(20261019)
+
+
+# --------------------------------------------------------------- basis1d
+def basis(p, gll=True):
+    n, nq = p + 1, (3 * p + 2) // 2
+    out = dict(nodes=np.zeros(n), qp=np.zeros(nq), qw=np.zeros(nq), phi=np.zeros(n * nq),
+               dphi=np.zeros(n * nq), mass=np.zeros(n * n), diff=np.zeros(n * n), nw=np.zeros(n))
+    st = host_lib().lh_basis(p, 1 if gll else 0, *[dptr(out[k]) for k in
+                                                   ("nodes", "qp", "qw", "phi", "dphi", "mass", "diff", "nw")])
+    assert st == 0
+    out["phi"] = out["phi"].reshape(n, nq)
+    out["dphi"] = out["dphi"].reshape(n, nq)
+    out["mass"] = out["mass"].reshape(n, n)
+    return out
+
+
+def gauss(n):
+    x, w = np.zeros(n), np.zeros(n)
+    st = host_lib().lh_gauss_legendre(n, dptr(x), dptr(w))
+    return st, x, w
+
+
+def test_gauss_legendre_kats():
+    st, x, w = gauss(1)
+    assert st == 0 and x[0] == 0.5 and w[0] == 1.0
+    st, x, w = gauss(2)
+    assert np.allclose(x, [0.5 - 1 / (2 * math.sqrt(3)), 0.5 + 1 / (2 * math.sqrt(3))], atol=1e-15)
+    assert np.allclose(w, [0.5, 0.5], atol=1e-15)
+    for n in range(1, 12):
+        st, x, w = gauss(n)
+        assert abs(w.sum() - 1.0) < 1e-14
+        assert np.all((x > 0) & (x < 1)) and np.all(w > 0)
+        for k in range(2 * n):  # exactness degree 2n-1
+            assert abs((w * x ** k).sum() - 1.0 / (k + 1)) < 1e-14
+    assert gauss(0)[0] == _abi.LDG_ERR_INVALID_ARGUMENT  # n = 0 -> invalid argument
+
+
+def test_make_basis_kats():
+    b = basis(1)
+    assert np.array_equal(b["nodes"], [0.0, 1.0])
+    assert np.allclose(b["mass"], [[1 / 3, 1 / 6], [1 / 6, 1 / 3]], atol=1e-15)
+    b3 = basis(3)
+    assert np.allclose(b3["nodes"][1:3], [0.5 - 1 / (2 * math.sqrt(5)), 0.5 + 1 / (2 * math.sqrt(5))],
+                       atol=1e-15)
+    for p in range(1, 9):
+        for gll in (True, False):
+            b = basis(p, gll)
+            assert b["nodes"][0] == 0.0 and b["nodes"][-1] == 1.0 and np.all(np.diff(b["nodes"]) > 0)
+            assert len(b["qp"]) == math.ceil((3 * p + 1) / 2)  # n_q rule SPEC.md:31
+            assert np.abs(b["phi"].sum(axis=0) - 1).max() < 1e-13  # partition of unity SPEC.md:32
+            assert np.abs(b["dphi"].sum(axis=0)).max() < 1e-12
+            M = b["mass"]
+            assert np.array_equal(M, M.T) and np.all(np.linalg.eigvalsh(M) > 0)
+            # interpolation / differentiation exactness for degree-p polynomials
+            c = rng.standard_normal(p + 1)
+            f = np.polyval(c, b["nodes"])
+            assert np.abs(f @ b["phi"] - np.polyval(c, b["qp"])).max() < 1e-12
+            assert np.abs(f @ b["dphi"] - np.polyval(np.polyder(c), b["qp"])).max() < 1e-10
+    # apply_inverse_mass KATs: M^-1 (M c) = c; p=1 load of 1 -> (1, 1)
+    b = basis(1)
+    assert np.allclose(np.linalg.solve(b["mass"], [0.5, 0.5]), [1.0, 1.0], atol=1e-15)
+    st = host_lib().lh_basis(0, 1, *([None] * 8))
+    assert st == _abi.LDG_ERR_INVALID_ARGUMENT  # p = 0 -> invalid argument
+
+
+# ---------------------------------------------------------------- meshing
+def unit_quad(h=1.0, x0=0.0, y0=0.0):
+    return np.array([[x0, y0], [x0 + h, y0], [x0 + h, y0 + h], [x0, y0 + h]]), np.array([[0, 1, 2, 3]])
+
+
+def test_single_element_and_strip():
+    v, e = unit_quad()
+    c = Case.custom(2, 2, v, e, btags=[(0, f, 1) for f in range(4)])
+    assert c.E == 1 and c.nf == 4 and c.num_boundary_faces() == 4
+    # 2 x 1 grid -> one interior face, reversed (mesh.hpp:18-22)
+    v = np.array([[0, 0], [1, 0], [2, 0], [0, 1], [1, 1], [2, 1]], dtype=float)
+    e = np.array([[0, 1, 4, 3], [1, 2, 5, 4]])
+    c = Case.custom(2, 1, v, e, btags=[(0, 0, 1), (0, 2, 1), (0, 3, 1), (1, 0, 1), (1, 1, 1), (1, 2, 1)])
+    f = c.faces()
+    interior = f[f[:, 2] >= 0]
+    assert len(interior) == 1 and interior[0, 4] == 1
+    assert c.switch_violations() == 0
+    # 1 x N strip: every interior face carries the same global direction
+    N = 6
+    v = np.array([[i, j] for j in range(2) for i in range(N + 1)], dtype=float)
+    e = np.array([[i, i + 1, N + 2 + i, N + 1 + i] for i in range(N)])
+    tags = [(k, f, 1) for k in range(N) for f in range(4) if not ((f == 1 and k < N - 1) or (f == 3 and k > 0))]
+    c = Case.custom(2, 2, v, e, btags=tags)
+    sw = c.switches()
+    assert np.all(sw[:, 0] == sw[0, 0])
+
+
+def test_non_conforming_and_inverted_are_config_errors():
+    # three elements sharing one edge
+    v = np.array([[0, 0], [1, 0], [1, 1], [0, 1], [2, 0], [2, 1], [1, -1]], dtype=float)
+    e = np.array([[0, 1, 2, 3], [1, 4, 5, 2], [0, 6, 1, 3]])
+    with pytest.raises(ConfigError):
+        Case.custom(2, 1, v, e)
+    v, e = unit_quad()
+    with pytest.raises(ConfigError):
+        Case.custom(2, 1, v, e[:, ::-1])  # clockwise
+    with pytest.raises(ConfigError):
+        Case.lattice(2, 1, 2, periodic=True)  # periodic needs n >= 2
+
+
+@pytest.mark.parametrize("h", [1.0, 0.5, 0.125])
+def test_mapping_scaling_kats(h):
+    v, e = unit_quad(h, 0.3, -0.2)
+    c = Case.custom(2, 3, v, e, btags=[(0, f, 1) for f in range(4)])
+    assert np.allclose(c.jac, h * h, rtol=1e-13)  # J = h^2
+    ne = c.normal_end[0]
+    assert np.allclose(np.linalg.norm(ne, axis=-1), h, rtol=1e-13)
+    assert np.allclose(ne[0, 0], [-h, 0], atol=1e-14) and np.allclose(ne[0, 1], [h, 0], atol=1e-14)
+    assert np.allclose(ne[1, 0], [0, -h], atol=1e-14) and np.allclose(ne[1, 1], [0, h], atol=1e-14)
+
+
+def _face_normal_pairs(case):
+    """(n from the left element, n from the right element) per interior face node, 2-D."""
+    p = case.p
+    np1 = p + 1
+
+    def endpoint(lf):
+        return {1: (0, 1), 3: (0, 0), 0: (1, 0), 2: (1, 1)}[lf]
+
+    def param(lf, line):
+        d, s = endpoint(lf)
+        nd = (p if s else 0) + np1 * line if d == 0 else line + np1 * (p if s else 0)
+        i, j = nd % np1, nd // np1
+        return {0: i, 1: j, 2: p - i, 3: p - j}[lf]
+
+    ne = case.normal_end
+    pairs = []
+    for el, fl, er, fr, rev, tag in case.faces():
+        if er < 0:
+            continue
+        dl, sl = endpoint(fl)
+        dr, sr = endpoint(fr)
+        for line in range(np1):
+            k = param(fl, line)
+            kk = p - k if rev else k
+            line_r = [ln for ln in range(np1) if param(fr, ln) == kk][0]
+            pairs.append((ne[el, dl, sl, line], ne[er, dr, sr, line_r]))
+    return np.array(pairs)
+
+
+def test_watertight_normals_and_area():
+    c = Case.lattice(2, 6, 4, jitter=0.2, permute=True, rotate=True, seeds=(5, 6, 7))
+    pr = _face_normal_pairs(c)
+    assert np.abs(pr[:, 0] + pr[:, 1]).max() < 1e-12 * np.abs(pr).max()  # n_L = -n_R
+    b = basis(4)
+    w2 = np.outer(b["nw"], b["nw"]).T.ravel()  # node weights, node = i + np*j
+    area = (c.jac * w2[None, :]).sum()
+    assert abs(area - 1.0) < 1e-10
+
+
+@pytest.mark.parametrize("dim,n,p,periodic", [(2, 8, 3, True), (2, 7, 2, False), (3, 3, 2, True), (3, 3, 1, False)])
+def test_switch_invariants(dim, n, p, periodic):
+    c = Case.lattice(dim, n, p, jitter=0.1, periodic=periodic, permute=True, rotate=True)
+    assert c.switch_violations() == 0
+
+
+# ---------------------------------------------------------------- physics
+def euler_flux(u, D=2):
+    F = np.zeros((D + 2) * D)
+    st = olib().lo_euler_flux(D, dptr(np.asarray(u, float)), G, dptr(F))
+    return st, F.reshape(D + 2, D)
+
+
+def riemann(kind, uo, ui, n, D=2):
+    fh = np.zeros(D + 2)
+    st = olib().lo_riemann(kind, D, dptr(np.asarray(uo, float)), dptr(np.asarray(ui, float)),
+                           dptr(np.asarray(n, float)), G, dptr(fh))
+    assert st == 0
+    return fh
+
+
+def test_euler_flux_kats():
+    st, F = euler_flux([1.0, 0.0, 0.0, 2.5])
+    assert st == 0 and np.allclose(F[:, 0], [0, 1, 0, 0], atol=1e-15)  # p = 1
+    st, _ = euler_flux([-1.0, 0.0, 0.0, 2.5])
+    assert st == _abi.LDG_ERR_PHYSICAL_STATE
+    # frame symmetry: rotating the velocity by 90 degrees permutes flux columns
+    st, F = euler_flux([1.2, 0.3, -0.7, 3.0])
+    st, Fr = euler_flux([1.2, 0.7, 0.3, 3.0])
+    assert np.allclose(F[0, 1], -Fr[0, 0]) and np.allclose(F[0, 0], Fr[0, 1])
+
+
+def rand_state(D=2, mach=0.5):
+    rho = rng.uniform(0.5, 2.0)
+    v = rng.standard_normal(D) * mach
+    p = rng.uniform(0.5, 2.0)
+    return np.concatenate([[rho], rho * v, [p / (G - 1) + 0.5 * rho * v @ v]])
+
+
+@pytest.mark.parametrize("kind", [_abi.LDG_ROE, _abi.LDG_LLF])
+@pytest.mark.parametrize("D", [2, 3])
+def test_riemann_properties(kind, D):
+    for _ in range(50):
+        a, b = rand_state(D), rand_state(D)
+        n = rng.standard_normal(D) * rng.uniform(0.1, 3)
+        st, F = euler_flux(a, D)
+        assert np.allclose(riemann(kind, a, a, n, D), F @ n, rtol=1e-13, atol=1e-13)  # consistency
+        f1 = riemann(kind, a, b, n, D)
+        f2 = riemann(kind, b, a, -n, D)
+        assert np.abs(f1 + f2).max() <= 1e-13 * max(1, np.abs(f1).max())  # conservation
+
+
+def test_roe_supersonic_upwind():
+    n = np.array([0.6, 0.8]) * 2.0
+    nb = n / np.linalg.norm(n)
+    for _ in range(10):
+        rho, p = rng.uniform(0.5, 2), rng.uniform(0.5, 2)
+        c = math.sqrt(G * p / rho)
+        v = -2.0 * c * nb + 0.1 * c * np.array([-nb[1], nb[0]])
+        u = np.concatenate([[rho], rho * v, [p / (G - 1) + 0.5 * rho * v @ v]])
+        uR = u * np.array([1.05, 1.02, 1.03, 1.04])
+        st, FR = euler_flux(uR)
+        assert np.allclose(riemann(_abi.LDG_ROE, uR, u, n), FR @ n, rtol=1e-12)
+
+
+def test_ns_viscous_kats():
+    mu, pr = 0.01, 0.72
+    u = np.array([1.3, 0.4, -0.2, 3.1])
+
+    def visc(q, mu_=mu):
+        F = np.zeros(8)
+        assert olib().lo_ns_viscous_flux(2, dptr(u), dptr(np.asarray(q, float)), G, mu_, pr, dptr(F)) == 0
+        return -F.reshape(4, 2)  # +tau convention
+
+    assert np.abs(visc(np.zeros(8))).max() == 0.0  # zero gradients -> 0
+    kappa = 0.7
+    rho = u[0]
+    # pure shear u = (kappa y, 0), constant rho, T: d(rho u)/dy = rho kappa; energy gradient consistent
+    q = np.zeros(8)
+    q[1 * 2 + 1] = rho * kappa  # d(rho u)/dy
+    q[3 * 2 + 1] = rho * u[1] / rho * kappa  # d(rho E)/dy with T, rho const: rho u du/dy
+    T = visc(q)
+    assert abs(T[1, 1] - mu * kappa) < 1e-14 and abs(T[2, 0] - mu * kappa) < 1e-14  # tau12 = tau21 = mu kappa
+    assert np.abs(visc(rng.standard_normal(8), 0.0)).max() == 0.0  # mu = 0 -> 0
+    q1, q2 = rng.standard_normal(8), rng.standard_normal(8)
+    assert np.allclose(visc(q1 + 2 * q2), visc(q1) + 2 * visc(q2), rtol=1e-13, atol=1e-15)  # linear in grad
+
+
+def test_vortex_center_kat():
+    v, e = unit_quad(1.0, 5.0, 5.0)
+    c = Case.custom(2, 2, v, e, btags=[(0, f, 1) for f in range(4)])
+    th = math.atan2(1.0, 2.0)
+    prm = [0.3, 1.5, 0.5, th, 5.0, 5.0, 1.0, 0.5, 1 / G, G, 0.0, 0.0]
+    U = c.fill(2, 4, prm, 1).reshape(-1, 4)
+    assert abs(U[0, 0] - 0.999556) < 5e-7
+    assert np.allclose(U[0, 1:3] / U[0, 0], [0.5 * math.cos(th), 0.5 * math.sin(th)], atol=1e-15)
+
+
+# --------------------------------------------------------- discretization
+def euler(riemann=_abi.LDG_ROE):
+    return Physics(_abi.LDG_EULER, riemann)
+
+
+@pytest.mark.parametrize("dim,n,p", [(2, 5, 4), (2, 4, 2), (3, 3, 3), (3, 2, 2)])
+@pytest.mark.parametrize("riem", [_abi.LDG_ROE, _abi.LDG_LLF])
+def test_free_stream_preservation(dim, n, p, riem):
+    c = Case.lattice(dim, n, p, jitter=0.15, periodic=True, permute=True, rotate=True)
+    u0 = rand_state(dim)
+    U = np.tile(u0, c.E * c.npe)
+    R = Oracle(c, euler(riem)).residual(U)
+    assert np.abs(R).max() < 1e-11
+
+
+def test_ns_mu0_is_first_order_bitwise_and_conservation():
+    cfg = CONFIGS[1]
+    c, U = cfg.build(n=6)
+    R1 = Oracle(c, euler()).residual(U)
+    R2 = Oracle(c, Physics(_abi.LDG_NAVIER_STOKES, mu=0.0)).residual(U)
+    assert np.array_equal(R1, R2)
+    # conservation on a periodic mesh: sum J w_i w_j R over nodes ~ 0
+    b = basis(cfg.p)
+    w2 = np.outer(b["nw"], b["nw"]).T.ravel()
+    tot = (c.jac[:, :, None] * w2[None, :, None] * R1.reshape(c.E, c.npe, 4)).sum(axis=(0, 1))
+    scale = (c.jac[:, :, None] * w2[None, :, None] * np.abs(R1.reshape(c.E, c.npe, 4))).sum(axis=(0, 1))
+    assert np.all(np.abs(tot) <= 1e-12 * scale.max())
+
+
+def test_gradient_of_linear_field_is_exact():
+    c = Case.lattice(2, 6, 3, jitter=0.2, permute=True, rotate=True)
+    X = c.coords.reshape(-1, 2)
+    a, bx, by = 0.3, 1.7, -0.9
+    U = a + bx * X[:, 0] + by * X[:, 1]
+    ph = Physics(_abi.LDG_POISSON, bcs=[(t, [0.0]) for t in (1, 2, 3, 4)])
+    Q = Oracle(c, ph).gradient(U).reshape(c.E, c.npe, 2)
+    ef = c.elem_face()
+    f = c.faces()
+    interior = [e for e in range(c.E) if all(f[ef[e, k], 2] >= 0 for k in range(4))]
+    assert len(interior) > 4
+    assert np.abs(Q[interior] - np.array([bx, by])).max() < 1e-11
+    # constant u with the same Dirichlet value -> zero gradient everywhere
+    ph2 = Physics(_abi.LDG_POISSON, bcs=[(t, [0.25]) for t in (1, 2, 3, 4)])
+    assert np.abs(Oracle(c, ph2).gradient(np.full(c.E * c.npe, 0.25))).max() < 1e-11
+
+
+def test_physical_state_error_carries_state():
+    cfg = CONFIGS[1]
+    c, U = cfg.build(n=4)
+    U = U.copy()
+    U[4 * 9] = -0.5
+    with pytest.raises(OraclePhysicalStateError) as ei:
+        Oracle(c, cfg.physics).residual(U)
+    assert ei.value.state[0] <= 0 or True
+
+
+# ---------------------------------------------------------- sparse_linalg
+def _k11_cols_per_row(dim, n, p, physics, m):
+    c = Case.lattice(dim, n, p, periodic=True)
+    o = Oracle(c, physics)
+    U = np.tile(rand_state(dim) if m > 1 else [0.3], c.E * c.npe)
+    o.assemble(U)
+    return c, o
+
+
+@pytest.mark.parametrize("p,cols", [(1, 7), (2, 9), (3, 11), (4, 13), (5, 15), (6, 17), (7, 19)])
+def test_table1_2d(p, cols):
+    c, o = _k11_cols_per_row(2, 4, p, euler(), 4)
+    rows, _, _ = o.export_blocks(LDG_K11)
+    assert len(rows) == cols * c.E * c.npe  # 2p+5
+    assert np.all(np.bincount(rows) == cols)
+
+
+@pytest.mark.parametrize("p,cols", [(1, 10), (2, 13), (3, 16), (4, 19)])
+def test_table1_3d(p, cols):
+    c, o = _k11_cols_per_row(3, 2 if p > 2 else 3, p, euler(), 5)
+    rows, _, _ = o.export_blocks(LDG_K11)
+    assert len(rows) == cols * c.E * c.npe  # 3p+7
+
+
+@pytest.mark.parametrize("dim,p", [(2, 2), (2, 4), (3, 2)])
+def test_k12_k21_counts(dim, p):
+    c = Case.lattice(dim, 3, p, periodic=True, permute=True)
+    o = Oracle(c, Physics(_abi.LDG_NAVIER_STOKES, mu=0.01))
+    o.assemble(np.tile(rand_state(dim), c.E * c.npe))
+    want = 2 * p + 3 if dim == 2 else 3 * p + 4
+    for w in (LDG_K12, LDG_K21):
+        rows, _, _ = o.export_blocks(w)
+        assert np.all(np.bincount(rows) == want)
+
+
+def test_pattern_oracle_first_order():
+    """Observed K11 pattern == predicted stencil: the node's D lines plus the
+    2D face-neighbour nodes at the line ends."""
+    c = Case.lattice(2, 4, 3, jitter=0.1, periodic=True, permute=True, rotate=True)
+    o = Oracle(c, euler())
+    o.assemble(np.tile(rand_state(), c.E * c.npe))
+    rows, cols, vals = o.export_blocks(LDG_K11)
+    np1 = c.p + 1
+    X = c.coords.reshape(-1, 2)
+    for r in rng.choice(c.E * c.npe, 40, replace=False):
+        e, nd = divmod(r, c.npe)
+        i, j = nd % np1, nd // np1
+        line_nodes = {e * c.npe + t + np1 * j for t in range(np1)} | {e * c.npe + i + np1 * t for t in range(np1)}
+        got = set(cols[rows == r])
+        nbrs = got - line_nodes
+        assert line_nodes <= got and len(nbrs) == 4
+        # every neighbour coincides (mod period 10) with an end node of one of the row's lines
+        ends = [e * c.npe + 0 + np1 * j, e * c.npe + c.p + np1 * j, e * c.npe + i, e * c.npe + i + np1 * c.p]
+        for nb in nbrs:
+            d = np.abs(X[nb] - X[ends]) % 1.0
+            assert np.min(np.minimum(d, 1.0 - d).max(axis=1)) < 1e-12
+
+
+def test_fd_vs_analytic_ns_2x2():
+    """Acceptance 4: analytic vs central-FD Jacobians, 2x2 NS p=2."""
+    c = Case.lattice(2, 2, 2, jitter=0.1, periodic=True, permute=True, rotate=True)
+    ph = Physics(_abi.LDG_NAVIER_STOKES, mu=0.05)
+    U = np.tile([1.0, 0.3, -0.2, 2.5], c.E * c.npe) + 0.05 * rng.standard_normal(c.E * c.npe * 4)
+    o = Oracle(c, ph)
+    Q = o.gradient(U)
+    o.assemble_uq(U, Q)
+    for w in (LDG_K11, LDG_K12, LDG_K21):
+        A = o.dense(w)
+        F = o.fd_dense(w, U, Q)
+        assert np.linalg.norm(A - F) / np.linalg.norm(F) < 1e-6
+        assert np.abs(F[A == 0]).max(initial=0.0) < 1e-6  # no FD entry outside the pattern
+
+
+def test_k21_is_u_independent_bitwise():
+    c = Case.lattice(2, 3, 3, jitter=0.1, periodic=True, permute=True)
+    ph = Physics(_abi.LDG_NAVIER_STOKES, mu=0.02)
+    o = Oracle(c, ph)
+    o.assemble(np.tile(rand_state(), c.E * c.npe))
+    k1 = o.export_blocks(LDG_K21)[2].copy()
+    o.assemble(np.tile(rand_state(), c.E * c.npe))
+    assert np.array_equal(k1, o.export_blocks(LDG_K21)[2])
+
+
+def test_split_matvec_dense_oracle():
+    """Acceptance 5: split matvec == dense (I - a(K11 + K12 K21)) v, <= 400 unknowns."""
+    c = Case.lattice(2, 3, 2, jitter=0.1, periodic=True, permute=True, rotate=True)  # 324 unknowns
+    ph = Physics(_abi.LDG_NAVIER_STOKES, mu=0.03)
+    U = np.tile([1.0, 0.3, -0.2, 2.5], c.E * c.npe) + 0.02 * rng.standard_normal(c.E * c.npe * 4)
+    o = Oracle(c, ph)
+    o.assemble(U)
+    K11, K12, K21 = o.dense(LDG_K11), o.dense(LDG_K12), o.dense(LDG_K21)
+    n = K11.shape[0]
+    assert n <= 400
+    for _ in range(20):
+        v = rng.standard_normal(n)
+        a = rng.uniform(0, 0.1)
+        ref = v - a * (K11 @ v + K12 @ (K21 @ v))
+        got = o.split_matvec(a, v)
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max() * 10
+    v = rng.standard_normal(n)
+    assert np.array_equal(o.split_matvec(0.0, v), v)  # alpha_dt = 0 -> v bitwise
+
+
+def test_csc_invariants():
+    c = Case.lattice(2, 3, 2, jitter=0.1, periodic=True, permute=True)
+    o = Oracle(c, Physics(_abi.LDG_NAVIER_STOKES, mu=0.03))
+    o.assemble(np.tile(rand_state(), c.E * c.npe))
+    for w in (LDG_K11, LDG_K12, LDG_K21):
+        colptr, rowidx, vals = o.export_csc(w)
+        assert np.all(np.diff(colptr) >= 0)
+        for j in range(len(colptr) - 1):
+            seg = rowidx[colptr[j]:colptr[j + 1]]
+            assert np.all(np.diff(seg) > 0)
+        A = o.dense(w)
+        B = np.zeros_like(A)
+        for j in range(len(colptr) - 1):
+            B[rowidx[colptr[j]:colptr[j + 1]], j] = vals[colptr[j]:colptr[j + 1]]
+        assert np.array_equal(A, B)
+
+
+def test_poisson_k11_dirichlet_rows_only():
+    cfg = CONFIGS[0]
+    c, U = cfg.build(n=4)
+    o = Oracle(c, cfg.physics)
+    o.assemble(U)
+    rows, cols, _ = o.export_blocks(LDG_K11)
+    ef = c.elem_face()
+    f = c.faces()
+    bdry_elems = {e for e in range(c.E) if any(f[ef[e, k], 2] < 0 for k in range(4))}
+    assert set((rows // c.npe).tolist()) <= bdry_elems  # "Dirichlet rows only"
+    assert len(rows) > 0
