@@ -79,6 +79,7 @@ struct ldg_ctx {
   double* d_K11 = nullptr;
   double* d_K12 = nullptr;
   double* d_K21 = nullptr;
+  double* d_SE = nullptr;  // endpoint flux-Jacobian scratch
   size_t n11 = 0, n12 = 0, n21 = 0;
   bool jac_valid = false, k21_valid = false;
   double* d_hu = nullptr;  // staging for host variants
@@ -106,6 +107,7 @@ struct ldg_ctx {
     cudaFree(d_K11);
     cudaFree(d_K12);
     cudaFree(d_K21);
+    cudaFree(d_SE);
     cudaFree(d_hu);
     cudaFree(d_hr);
     cudaFree(d_hx);
@@ -625,7 +627,8 @@ int ldg_jacobian_assemble(ldg_ctx* c, const double* U, double t) {
         c->k21_valid = true;
       }
     }
-    const int st = finish(c, o.jacobian(c->dc, U, q, c->d_K11, c->d_K12));
+    ensure(c->d_SE, static_cast<size_t>(c->E) * o.endjac_per_elem);
+    const int st = finish(c, o.jacobian(c->dc, U, q, c->d_SE, c->d_K11, c->d_K12));
     c->jac_valid = st == LDG_OK;
     return st;
   });

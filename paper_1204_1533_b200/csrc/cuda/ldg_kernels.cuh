@@ -119,6 +119,75 @@ __device__ __noinline__ void report_line(const KParams<C>& kp, int e, int dir, i
   report_bad_state<double, M>(kp.err, e, bad, su + bad * M);
 }
 
+// ------------------------------------------------------ async copy helpers
+// TMA 1-D bulk copies global -> shared completing on an mbarrier
+// (cp.async.bulk ... mbarrier::complete_tx, SASS UBLKCP) and Ampere-style
+// cp.async gathers (LDGSTS) for the scattered neighbour traces.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Staged tile -> global, asynchronous: TMA bulk copy (cp.async.bulk, SASS
+// UBLKCP) issued by thread 0 when size and both addresses are 16-byte
+// multiples (else plain stores).  store_wait() returns once the copy has read
+// the staging buffer (thread 0 waits on its bulk group, then a CTA barrier).
+__device__ __forceinline__ void store_issue(double* __restrict__ gdst, const double* ssrc, int n, int tid,
+                                            int nthr) {
+  const unsigned bytes = static_cast<unsigned>(n) * 8u;
+  const bool bulk = (bytes % 16u) == 0 && aligned16(gdst) && aligned16(ssrc);
+  if (bulk) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                   "r"(smem_u32(ssrc)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  } else {
+    __syncthreads();
+    for (int i = tid; i < n; i += nthr) gdst[i] = ssrc[i];
+  }
+}
+__device__ __forceinline__ void store_wait(int tid) {
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  __syncthreads();
+}
+
 // Staged tile -> global.  TMA bulk copy (cp.async.bulk, SASS UBLKCP) when the
 // size and both addresses are 16-byte multiples, else 16/8-byte stores.
 // Must be reached by all threads of the CTA; returns with the smem source
@@ -511,6 +580,262 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
   }
 }
 
+// ================================================= residual, persistent + TMA
+// Persistent CTAs walk batches of EPB elements (grid-stride).  Two smem
+// buffers: while batch i is computed from buffer i%2, the TMA engine fills the
+// other buffer with batch i+1 (element states -- one bulk copy per element,
+// the batch's metric and connectivity -- one bulk copy each, all completing on
+// one mbarrier); the scattered neighbour traces of batch i+1 are gathered with
+// cp.async as soon as its connectivity has landed.  Compute is the
+// thread-per-line scheme of k_residual with every operand in shared memory.
+template <class C, int EPB>
+struct ResP {
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int U = ev(EPB * C::NPE * C::M);
+  static constexpr int Q = C::SECOND ? ev(EPB * C::NPE * C::MD) : 0;
+  static constexpr int MET = EPB * C::METP;
+  static constexpr int CONN = ev(EPB * C::D * 2);  // int2 entries, 8 B each
+  static constexpr int NB = ev(EPB * C::LPE * 2 * C::M);
+  static constexpr int NBQ = C::SECOND ? ev(EPB * C::LPE * 2 * C::MD) : 0;
+  static constexpr int BUF = U + Q + MET + CONN + NB + NBQ;
+  static constexpr int ACC = EPB * C::D * C::NPE * C::M;
+  static constexpr int TOTAL = 2 + 2 * BUF + ACC;  // 2 doubles hold the two mbarriers
+  static constexpr bool TMA = (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0);
+  static constexpr int THREADS = (EPB * C::LPE + 31) / 32 * 32;
+};
+
+template <class C, int EPB>
+__global__ void __launch_bounds__(ResP<C, EPB>::THREADS)
+k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+             double* __restrict__ R) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD,
+                LPE = C::LPE, P = C::P;
+  using RP = ResP<C, EPB>;
+  extern __shared__ __align__(16) double smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* const bufs = smem + 2;
+  double* const sacc = bufs + 2 * RP::BUF;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nbatch = (kp.E + EPB - 1) / EPB;
+  const int G = gridDim.x;
+  if (static_cast<int>(blockIdx.x) >= nbatch) return;
+  auto bU = [&](int bi) { return bufs + bi * RP::BUF; };
+  auto bQ = [&](int bi) { return bufs + bi * RP::BUF + RP::U; };
+  auto bMET = [&](int bi) { return bufs + bi * RP::BUF + RP::U + RP::Q; };
+  auto bCONN = [&](int bi) { return reinterpret_cast<int2*>(bufs + bi * RP::BUF + RP::U + RP::Q + RP::MET); };
+  auto bNB = [&](int bi) { return bufs + bi * RP::BUF + RP::U + RP::Q + RP::MET + RP::CONN; };
+  auto bNBQ = [&](int bi) { return bufs + bi * RP::BUF + RP::U + RP::Q + RP::MET + RP::CONN + RP::NB; };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // bulk loads of one batch into buffer bi (thread 0 issues; TMA path)
+  auto issue = [&](int batch, int bi) {
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    unsigned bytes = nb * (NPE * M * 8) + nb * C::METP * 8 + nb * D * 2 * 8;
+    if (C::SECOND) bytes += nb * (NPE * MD * 8);
+    mbar_expect_tx(&bar[bi], bytes);
+    for (int le = 0; le < nb; ++le) {
+      const size_t e = __ldg(kp.order + k0 + le);
+      tma_load_1d(bU(bi) + le * NPE * M, U + e * (NPE * M), NPE * M * 8, &bar[bi]);
+      if (C::SECOND) tma_load_1d(bQ(bi) + le * NPE * MD, Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
+    }
+    tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k0) * C::METP, nb * C::METP * 8, &bar[bi]);
+    tma_load_1d(bCONN(bi), kp.conn + static_cast<size_t>(k0) * D * 2, nb * D * 2 * 8, &bar[bi]);
+  };
+  // synchronous fallback (element chunks not 16-byte aligned)
+  auto load_sync = [&](int batch, int bi) {
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    for (int le = 0; le < nb; ++le) {
+      const size_t e = kp.order[k0 + le];
+      for (int i = tid; i < NPE * M; i += nthr) bU(bi)[le * NPE * M + i] = __ldg(U + e * (NPE * M) + i);
+      if (C::SECOND)
+        for (int i = tid; i < NPE * MD; i += nthr) bQ(bi)[le * NPE * MD + i] = __ldg(Q + e * (NPE * MD) + i);
+    }
+    for (int i = tid; i < nb * C::METP; i += nthr) bMET(bi)[i] = __ldg(kp.metric + static_cast<size_t>(k0) * C::METP + i);
+    for (int i = tid; i < nb * D * 2; i += nthr) bCONN(bi)[i] = __ldg(kp.conn + static_cast<size_t>(k0) * D * 2 + i);
+    __syncthreads();
+  };
+  // neighbour-trace gathers of buffer bi (all threads; needs its connectivity)
+  auto gather = [&](int batch, int bi) {
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    const int2* sc = bCONN(bi);
+    for (int w = tid; w < nb * LPE * 2; w += nthr) {
+      const int side = w & 1, lw = w >> 1, le = lw / LPE, rem = lw - le * LPE;
+      const int dir = rem / NL, line = rem - dir * NL;
+      const int2 cn = sc[(le * D + dir) * 2 + side];
+      if (cn.x < 0) continue;
+      const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+      double* dst = bNB(bi) + w * M;
+#pragma unroll
+      for (int c = 0; c < M; ++c) cp_async8(dst + c, U + nd * M + c);
+      if (C::SECOND && conn_sign(cn.y) > 0) {
+        double* dq = bNBQ(bi) + w * MD;
+#pragma unroll
+        for (int c = 0; c < MD; ++c) cp_async8(dq + c, Q + nd * MD + c);
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int b0 = blockIdx.x;
+  if (RP::TMA) {
+    if (tid == 0) {
+      issue(b0, 0);
+      if (b0 + G < nbatch) issue(b0 + G, 1);
+    }
+    mbar_wait(&bar[0], 0);
+  } else {
+    load_sync(b0, 0);
+  }
+  gather(b0, 0);
+  for (int batch = b0, it = 0; batch < nbatch; batch += G, ++it) {
+    const int cur = it & 1, nxt = cur ^ 1;
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- lines
+    const int le = tid / LPE;
+    if (le < nb) {
+      const int rem = tid - le * LPE;
+      const int dir = rem / NL, line = rem - dir * NL;
+      const double* mk = bMET(cur) + le * C::METP;
+      const double* nvl = mk + (dir * NL + line) * NQ * D;
+      const double* sul = bU(cur) + le * NPE * M;
+      const double* sql = bQ(cur) + le * NPE * MD;
+      bool ok = true;
+      double r[NP][M];
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c) r[i][c] = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double uq[M], qq[C::SECOND ? MD : 1];
+#pragma unroll
+        for (int c = 0; c < M; ++c) uq[c] = 0.0;
+        if (C::SECOND) {
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+          const int nd = node_on_line<C>(dir, line, t);
+          const double ph = kp.bt.phi[t][q];
+#pragma unroll
+          for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
+          if (C::SECOND) {
+#pragma unroll
+            for (int c = 0; c < MD; ++c) qq[c] += ph * sql[nd * MD + c];
+          }
+        }
+        double nv[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) nv[d] = nvl[q * D + d];
+        double f[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) f[c] = 0.0;
+        if (C::HAS_INV) euler_fn<D>(uq, nv, kp.pp.gamma, f, ok);
+        if (C::SECOND) {
+          double fv[M];
+          visc_fn<D, C::PH, double, double, double>(uq, qq, nv, kp.pp, fv, ok);
+#pragma unroll
+          for (int c = 0; c < M; ++c) f[c] += fv[c];
+        }
+#pragma unroll
+        for (int i = 0; i < NP; ++i)
+#pragma unroll
+          for (int c = 0; c < M; ++c) r[i][c] += kp.bt.dq[i][q] * f[c];
+      }
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int2 cn = bCONN(cur)[(le * D + dir) * 2 + side];
+        const int S = conn_sign(cn.y);
+        const int ie = side ? P : 0;
+        const int nd = node_on_line<C>(dir, line, ie);
+        const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
+        const int w = ((le * LPE + rem) << 1) | side;
+        double n[D], ui[M], uo[M], fh[M];
+#pragma unroll
+        for (int d = 0; d < D; ++d) n[d] = nep[d];
+        const double* bcp = cn.x < 0 ? kp.bcv + (-1 - cn.x) * M : nullptr;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          ui[c] = sul[nd * M + c];
+          uo[c] = bcp ? __ldg(bcp + c) : bNB(cur)[w * M + c];
+          fh[c] = 0.0;
+        }
+        if (C::HAS_INV) {
+          if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+          else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        }
+        if (C::SECOND) {
+          double nn = n[0] * n[0];
+#pragma unroll
+          for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+          nn = sqrt(nn);
+          double fv[M];
+          if (bcp) {
+            visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+            const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - uo[c]);
+          } else {
+            if (S > 0) visc_fn<D, C::PH, double, double, double>(uo, bNBQ(cur) + w * MD, n, kp.pp, fv, ok);
+            else visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] += fv[c];
+            if (kp.pp.c11 != 0.0) {
+#pragma unroll
+              for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NP; ++i)
+#pragma unroll
+          for (int c = 0; c < M; ++c) r[i][c] += kp.bt.mi[i][side] * fh[c];
+      }
+      if (!ok) report_line<C>(kp, kp.order[k0 + le], dir, line, sul);
+      double* acc = sacc + (le * D + dir) * NPE * M;
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        const int nd = node_on_line<C>(dir, line, t);
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[nd * M + c] = r[t][c];
+      }
+    }
+    __syncthreads();
+    // ---- dU/dt = S - (1/J) sum_dir r
+    for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
+      const int l = idx / (NPE * M), off = idx - l * NPE * M;
+      const int nd = off / M;
+      const size_t e = kp.order[k0 + l];
+      const double* a = sacc + l * D * NPE * M + off;
+      double sum = a[0];
+#pragma unroll
+      for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
+      const double invJ = bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
+      const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
+      R[e * (NPE * M) + off] = src - invJ * sum;
+    }
+    // ---- next batch: its bulk data was issued one iteration ago
+    const int nbn = batch + G;
+    if (nbn < nbatch) {
+      if (RP::TMA) mbar_wait(&bar[nxt], ((it + 1) >> 1) & 1);
+      else {
+        __syncthreads();
+        load_sync(nbn, nxt);
+      }
+      gather(nbn, nxt);
+    }
+    __syncthreads();  // buffer `cur` is free
+    if (RP::TMA && tid == 0 && batch + 2 * G < nbatch) issue(batch + 2 * G, cur);
+  }
+}
+
 // ===================================================================== gradient
 // Q = (1/J) sum_dir d^(dir),  d = M^-1 [u_hat (x) n |ends - sum_q w phi' u_q (x) nvec_q]
 template <class C, int EPB>
@@ -635,6 +960,170 @@ struct TileLines {
   }
 };
 
+// Endpoint flux Jacobians of every element line end, into a per-element
+// scratch consumed by k_jacobian:
+//   SE[k][gs][Ein (m*m) | Eout (m*m) | Eq (m*mD, second-order)]
+//   gs = (dir*2 + side)*NL + line  (the order of the metric's endpoint normals)
+// Ein = dFhat/du_in, Eout = dFhat/du_out (Riemann + LDG viscous + C11 terms,
+// each element with its own normal), Eq = dFhat_vis/dq of the switch-selected
+// side.  One thread per (line end, pass); SEEDS components are seeded per
+// thread in sequence (forward mode, Dual<1>), sharing the primal.
+template <class C>
+struct EndJac {
+  static constexpr int NPASS = C::SECOND ? 3 : 2;
+  static constexpr int EQS = C::SECOND ? C::M * C::MD : 0;
+  static constexpr int SLOT = 2 * C::B11 + EQS;               // doubles per line end
+  static constexpr int PER_ELEM = 2 * C::D * C::NL * SLOT;    // doubles per element
+};
+
+template <class C, int SEEDS>
+__global__ void __launch_bounds__(128)
+k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+         double* __restrict__ SE, int k_begin, int k_end) {
+  constexpr int NP = C::NP, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD, P = C::P,
+                B11 = C::B11;
+  using EJ = EndJac<C>;
+  constexpr int NSP = (M + SEEDS - 1) / SEEDS;         // u-seed groups per pass
+  constexpr int NSQ = (MD + SEEDS - 1) / SEEDS;        // q-seed groups
+  constexpr int IPS = 2 * NSP + (C::SECOND ? NSQ : 0);  // items per line end
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nitems = static_cast<int64_t>(k_end - k_begin) * 2 * D * NL * IPS;
+  if (item >= nitems) return;
+  const int sub = static_cast<int>(item % IPS);
+  const int64_t gslot = item / IPS;
+  const int k = k_begin + static_cast<int>(gslot / (2 * D * NL));
+  const int gs = static_cast<int>(gslot - static_cast<int64_t>(k - k_begin) * (2 * D * NL));
+  const int ds = gs / NL, line = gs - ds * NL, dir = ds >> 1, side = ds & 1;
+  const size_t e = kp.order[k];
+  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+  const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+  const bool bd = cn.x < 0;
+  const int S = conn_sign(cn.y);
+  const int nd = node_on_line<C>(dir, line, side ? P : 0);
+  double* slot = SE + static_cast<size_t>(k) * EJ::PER_ELEM + static_cast<size_t>(gs) * EJ::SLOT;
+  int pass, g0;
+  if (sub < NSP) {
+    pass = 0;
+    g0 = sub * SEEDS;
+  } else if (sub < 2 * NSP) {
+    pass = 1;
+    g0 = (sub - NSP) * SEEDS;
+  } else {
+    pass = 2;
+    g0 = (sub - 2 * NSP) * SEEDS;
+  }
+  double n[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + (ds * NL + line) * D + d);
+  double nn = n[0] * n[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+  nn = sqrt(nn);
+  const double* bcp = bd ? kp.bcv + (-1 - cn.x) * M : nullptr;
+  const size_t own = e * NPE + nd;
+  const size_t onb = bd ? 0 : static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+  double uiv[M], uov[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    uiv[c] = __ldg(U + own * M + c);
+    uov[c] = bd ? __ldg(bcp + c) : __ldg(U + onb * M + c);
+  }
+  bool ok = true;
+  using D1 = Dual<1>;
+  if (pass < 2) {
+    if (pass == 1 && bd) {
+#pragma unroll
+      for (int j = 0; j < SEEDS; ++j)
+        if (g0 + j < M)
+#pragma unroll
+          for (int c = 0; c < M; ++c) slot[B11 + c * M + g0 + j] = 0.0;
+      return;
+    }
+    double qiv[C::SECOND ? MD : 1], qov[C::SECOND ? MD : 1];
+    if (C::SECOND) {
+#pragma unroll
+      for (int c = 0; c < MD; ++c) {
+        qiv[c] = __ldg(Q + own * MD + c);
+        qov[c] = bd ? 0.0 : __ldg(Q + onb * MD + c);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < SEEDS; ++j) {
+      const int b = g0 + j;
+      if (b >= M) break;
+      D1 ui[M], uo[M], fh[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        ui[c] = D1(uiv[c]);
+        uo[c] = D1(uov[c]);
+        ui[c].d[0] = (pass == 0 && c == b) ? 1.0 : 0.0;
+        uo[c].d[0] = (pass == 1 && c == b) ? 1.0 : 0.0;
+        fh[c] = D1(0.0);
+      }
+      if (C::HAS_INV) {
+        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      }
+      if (C::SECOND) {
+        D1 fv[M];
+        if (bd) {
+          visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
+          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
+        } else {
+          if (S > 0) visc_fn<D, C::PH, D1, double, D1>(uo, qov, n, kp.pp, fv, ok);
+          else visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
+#pragma unroll
+          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
+          if (kp.pp.c11 != 0.0) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) slot[pass * B11 + c * M + b] = fh[c].d[0];
+    }
+  } else if (C::SECOND) {
+    const bool out = !bd && S > 0;
+    const size_t src = out ? onb : own;
+    double usrc[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) usrc[c] = out ? uov[c] : uiv[c];
+    double qv[MD];
+#pragma unroll
+    for (int c = 0; c < MD; ++c) qv[c] = __ldg(Q + src * MD + c);
+#pragma unroll
+    for (int j = 0; j < SEEDS; ++j) {
+      const int b = g0 + j;
+      if (b >= MD) break;
+      D1 dqv[MD], fv[M];
+#pragma unroll
+      for (int c = 0; c < MD; ++c) {
+        dqv[c] = D1(qv[c]);
+        dqv[c].d[0] = c == b ? 1.0 : 0.0;
+      }
+      visc_fn<D, C::PH, double, D1, D1>(usrc, dqv, n, kp.pp, fv, ok);
+#pragma unroll
+      for (int c = 0; c < M; ++c) slot[2 * B11 + c * MD + b] = fv[c].d[0];
+    }
+  }
+  if (!ok) {
+    // a non-physical state at this line end: report the offending nodal state
+    double m2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) m2 += uiv[1 + d] * uiv[1 + d];
+    const bool own_bad =
+        C::HAS_INV && (!(uiv[0] > 0.0) || !((kp.pp.gamma - 1.0) * (uiv[D + 1] - 0.5 * m2 / uiv[0]) > 0.0));
+    double st[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) st[c] = (own_bad || bd) ? uiv[c] : uov[c];
+    report_bad_state<double, M>(kp.err, own_bad || bd ? static_cast<int>(e) : cn.x,
+                                own_bad || bd ? nd : conn_node(cn.y, line, NP), st);
+  }
+}
+
 // K11 (+ K12 for second-order physics) of one row tile.  Store layout:
 //   K11[((T*NS11 + slot)*B11 + a*M + b)*NT + r]       T = k*TPE + tile, r = row in tile
 //   K12[((T*NS12 + slot)*B12 + a'*MD + b)*NT + r]     a' = stored row (NS: a-1)
@@ -644,71 +1133,37 @@ struct JacSmem {
   static constexpr int NDA = C::SECOND ? C::MD : 1;  // q-derivative slots
   static constexpr int U = C::NPE * C::M;
   static constexpr int Q = C::SECOND ? C::NPE * C::MD : 0;
-  static constexpr int UO = NLT * 2 * C::M;
-  static constexpr int QO = C::SECOND ? NLT * 2 * C::MD : 0;
+  static constexpr int UO = 0;  // neighbour traces: consumed by k_endjac only
+  static constexpr int QO = 0;
   static constexpr int A = C::HAS_INV ? NLT * C::NQ * C::B11 : 0;  // dFinv/du . nvec at quad points
   static constexpr int AV = C::VIS_U ? NLT * C::NQ * C::B11 : 0;    // dFvis/du . nvec
   static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
-  static constexpr int EIN = NLT * 2 * C::B11;                // endpoint d/du_in
-  static constexpr int EOUT = NLT * 2 * C::B11;               // endpoint d/du_out
-  static constexpr int EQ = C::SECOND ? NLT * 2 * C::M * C::MD : 0;  // endpoint d/dq (selected side)
+  static constexpr int SEC = NLT * 2 * EndJac<C>::SLOT;       // endpoint flux Jacobians (tile lines)
   static constexpr int ST11 = C::NS11 * C::B11 * C::NT;
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
   static constexpr int STG = ST11 > ST12 ? ST11 : ST12;
   static constexpr int DG = (C::D - 1) * C::NT * (C::B11 > C::B12 ? C::B11 : C::B12);  // diag scratch
-  static constexpr int TOTAL = U + Q + UO + QO + A + AV + BQ + EIN + EOUT + EQ + STG + DG + C::NT;
+  static constexpr int TOTAL = U + Q + A + AV + BQ + SEC + STG + DG;
 };
 
-template <class C>
-__global__ void __launch_bounds__(128, 3)
-k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-           double* __restrict__ K11, double* __restrict__ K12) {
-  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
-                MD = C::MD, NT = C::NT, P = C::P, B11 = C::B11;
+// Phases 1-3 of one Jacobian row tile, all operands in shared memory (or
+// read-only global for the metric of the one-shot kernel):
+//   su/sq element state and gradient, mk metric of the element (1/J
+//   included), sE endpoint flux Jacobians indexed by eidx(tl,dir,line,side).
+// K11t / K12t: this tile's destination in the store.  The tile leaves through
+// an asynchronous bulk store; callers wait (store_wait) before the staging
+// buffer is reused or the CTA exits.
+template <class C, class EIdx>
+__device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, const int s, const size_t e,
+                                         const double* su, const double* sq, const double* mk,
+                                         const double* sE, EIdx eidx, double* sA, double* sAv, double* sBq,
+                                         double* stg, double* sdg, double* __restrict__ K11t,
+                                         double* __restrict__ K12t, const int tid, const int nthr) {
+  constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, M = C::M, D = C::D, MD = C::MD, NT = C::NT, P = C::P,
+                B11 = C::B11;
   using SM = JacSmem<C>;
+  using EJ = EndJac<C>;
   constexpr int NLT = SM::NLT;
-  extern __shared__ double smem[];
-  double* su = smem;
-  double* sq = su + SM::U;
-  double* suo = sq + SM::Q;
-  double* sqo = suo + SM::UO;
-  double* sA = sqo + SM::QO;
-  double* sAv = sA + SM::A;
-  double* sBq = sAv + SM::AV;
-  double* sEin = sBq + SM::BQ;
-  double* sEout = sEin + SM::EIN;
-  double* sEq = sEout + SM::EOUT;
-  double* stg = sEq + SM::EQ;
-  double* sdg = stg + SM::STG;
-  double* sinvJ = sdg + SM::DG;
-
-  const int T = blockIdx.x;               // tile id
-  const int k = T / C::TPE, s = T - k * C::TPE;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const size_t e = kp.order[k];
-  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-
-  // ---- phase 0: stage element states, neighbour traces, 1/J of the tile rows
-  cp_elem<C>(su, U + e * (NPE * M), NPE * M, tid, nthr);
-  if (C::SECOND) cp_elem<C>(sq, Q + e * (NPE * MD), NPE * MD, tid, nthr);
-  for (int r = tid; r < NT; r += nthr) sinvJ[r] = __ldg(mk + C::MET_NV + C::MET_NE + s * NT + r);
-  for (int idx = tid; idx < NLT * 2; idx += nthr) {
-    const int tl = idx >> 1, side = idx & 1;
-    int dir, line;
-    TileLines<C>::get(tl, s, dir, line);
-    const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-    if (cn.x >= 0) {
-      const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
-#pragma unroll
-      for (int c = 0; c < M; ++c) suo[idx * M + c] = __ldg(U + nd * M + c);
-      if (C::SECOND) {
-#pragma unroll
-        for (int c = 0; c < MD; ++c) sqo[idx * MD + c] = __ldg(Q + nd * MD + c);
-      }
-    }
-  }
-  __syncthreads();
-
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
   if (C::HAS_INV) {
@@ -718,7 +1173,7 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       TileLines<C>::get(tl, s, dir, line);
       double nv[D], uq[M];
 #pragma unroll
-      for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
+      for (int d = 0; d < D; ++d) nv[d] = mk[((dir * NL + line) * NQ + q) * D + d];
 #pragma unroll
       for (int c = 0; c < M; ++c) uq[c] = 0.0;
 #pragma unroll
@@ -733,75 +1188,6 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
   }
-  // ---- phase 1b: endpoint flux Jacobian columns.  One item per (line end,
-  // pass); pass 0 = d/du_in, 1 = d/du_out.  The seeded components run
-  // sequentially in one thread (forward mode, Dual<1>), so the primal part of
-  // the flux is common to all seeds and is computed once by the compiler.
-  for (int w = tid; w < NLT * 2 * 2; w += nthr) {
-    const int pass = w & 1, idx = w >> 1;
-    const int tl = idx >> 1, side = idx & 1;
-    int dir, line;
-    TileLines<C>::get(tl, s, dir, line);
-    const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-    const bool bd = cn.x < 0;
-    if (pass == 1 && bd) continue;
-    const int S = conn_sign(cn.y);
-    const int nd = node_on_line<C>(dir, line, side ? P : 0);
-    double n[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
-    double nn = n[0] * n[0];
-#pragma unroll
-    for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-    nn = sqrt(nn);
-    const double* bcp = bd ? kp.bcv + (-1 - cn.x) * M : nullptr;
-    double uiv[M], uov[M];
-#pragma unroll
-    for (int c = 0; c < M; ++c) {
-      uiv[c] = su[nd * M + c];
-      uov[c] = bd ? __ldg(bcp + c) : suo[idx * M + c];
-    }
-    double* dst = (pass == 0 ? sEin : sEout) + idx * B11;
-    bool ok = true;
-    using D1 = Dual<1>;
-#pragma unroll
-    for (int bcol = 0; bcol < M; ++bcol) {
-      D1 ui[M], uo[M], fh[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        ui[c] = D1(uiv[c]);
-        uo[c] = D1(uov[c]);
-        ui[c].d[0] = (pass == 0 && c == bcol) ? 1.0 : 0.0;
-        uo[c].d[0] = (pass == 1 && c == bcol) ? 1.0 : 0.0;
-        fh[c] = D1(0.0);
-      }
-      if (C::HAS_INV) {
-        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-      }
-      if (C::SECOND) {
-        D1 fv[M];
-        if (bd) {
-          visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
-          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
-#pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
-        } else {
-          if (S > 0) visc_fn<D, C::PH, D1, double, D1>(uo, sqo + idx * MD, n, kp.pp, fv, ok);
-          else visc_fn<D, C::PH, D1, double, D1>(ui, sq + nd * MD, n, kp.pp, fv, ok);
-#pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
-          if (kp.pp.c11 != 0.0) {
-#pragma unroll
-            for (int c = 0; c < M; ++c) fh[c] = fh[c] + (kp.pp.c11 * nn) * (ui[c] - uo[c]);
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < M; ++c) dst[c * M + bcol] = fh[c].d[0];
-    }
-    if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
-  }
   // ---- phase 1c (second-order): viscous flux derivatives, one seed per item
   if (C::SECOND) {
     constexpr int NSU = C::VIS_U ? M : 0, NSEED = NSU + MD;
@@ -811,7 +1197,7 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       TileLines<C>::get(tl, s, dir, line);
       double nv[D], uq[M], qq[MD];
 #pragma unroll
-      for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
+      for (int d = 0; d < D; ++d) nv[d] = mk[((dir * NL + line) * NQ + q) * D + d];
 #pragma unroll
       for (int c = 0; c < M; ++c) uq[c] = 0.0;
 #pragma unroll
@@ -854,37 +1240,12 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       }
       if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
-    // endpoint d/dq of the switch-selected side's viscous flux
-    for (int w = tid; w < NLT * 2 * MD; w += nthr) {
-      const int bq = w % MD, idx = w / MD, tl = idx >> 1, side = idx & 1;
-      int dir, line;
-      TileLines<C>::get(tl, s, dir, line);
-      const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-      const bool out = cn.x >= 0 && conn_sign(cn.y) > 0;
-      const int nd = node_on_line<C>(dir, line, side ? P : 0);
-      double n[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
-      using D1 = Dual<1>;
-      const double* qsrc = out ? sqo + idx * MD : sq + nd * MD;
-      const double* usrc = out ? suo + idx * M : su + nd * M;
-      D1 dqv[MD], fv[M];
-#pragma unroll
-      for (int c = 0; c < MD; ++c) {
-        dqv[c] = D1(qsrc[c]);
-        dqv[c].d[0] = c == bq ? 1.0 : 0.0;
-      }
-      bool ok = true;
-      visc_fn<D, C::PH, double, D1, D1>(usrc, dqv, n, kp.pp, fv, ok);
-      double* dst = sEq + idx * M * MD;
-#pragma unroll
-      for (int c = 0; c < M; ++c) dst[c * MD + bq] = fv[c].d[0];
-      if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
-    }
   }
   __syncthreads();
 
-  // ---- phase 2: K11 line blocks into the staging tile
+  // ---- phase 2: K11 line blocks into the staging tile (after any pending
+  // bulk store of the previous tile has read it out)
+  store_wait(tid);
   // Each item = (tile line, a, b).  Row i of the line (all i for full lines,
   // i = s for 3-D dir-2 lines) gets, for column t on the line,
   //   B(i,t) = sum_q cc[i][t][q] A_q[a][b] + [t == end] mi[i][side] Ein[a][b]
@@ -910,13 +1271,15 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
       av[q] = (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
-    const double ein0 = sEin[(tl * 2 + 0) * B11 + ab], ein1 = sEin[(tl * 2 + 1) * B11 + ab];
-    const double eo0 = sEout[(tl * 2 + 0) * B11 + ab], eo1 = sEout[(tl * 2 + 1) * B11 + ab];
+    const double* e0 = sE + eidx(tl, dir, line, 0) * EJ::SLOT;
+    const double* e1 = sE + eidx(tl, dir, line, 1) * EJ::SLOT;
+    const double ein0 = e0[ab], ein1 = e1[ab];
+    const double eo0 = e0[B11 + ab], eo1 = e1[B11 + ab];
     const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
     const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
-      const double sc = -sinvJ[nd - s * NT];
+      const double sc = -mk[C::MET_NV + C::MET_NE + nd];
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         double v = 0.0;
@@ -950,8 +1313,9 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     stg[(x0 * B11 + ab) * NT + r] = v;
   }
   __syncthreads();
-  store_tile(K11 + static_cast<size_t>(T) * SM::ST11, stg, SM::ST11, tid, nthr);
+  store_issue(K11t, stg, SM::ST11, tid, nthr);
   if (!C::SECOND) return;
+  store_wait(tid);
 
   // ---- phase 3: K12 = dR/dQ (rows a' of the stored block)
   constexpr int B12 = C::B12, R12 = C::R12, A0 = C::PH == PH_NS ? 1 : 0;
@@ -966,8 +1330,8 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     double bv[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) bv[q] = sBq[(tl * NQ + q) * M * MD + a * MD + b];
-    const double eq0 = sEq[(tl * 2 + 0) * M * MD + a * MD + b];
-    const double eq1 = sEq[(tl * 2 + 1) * M * MD + a * MD + b];
+    const double eq0 = sE[eidx(tl, dir, line, 0) * EJ::SLOT + 2 * B11 + a * MD + b];
+    const double eq1 = sE[eidx(tl, dir, line, 1) * EJ::SLOT + 2 * B11 + a * MD + b];
     const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
     const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
     // own-end dependence when boundary or S <= 0; neighbour slot otherwise
@@ -975,7 +1339,7 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
-      const double sc = -sinvJ[nd - s * NT];
+      const double sc = -mk[C::MET_NV + C::MET_NE + nd];
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         double v = 0.0;
@@ -1006,7 +1370,130 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     stg[(x0 * B12 + ab) * NT + r] = v;
   }
   __syncthreads();
-  store_tile(K12 + static_cast<size_t>(T) * SM::ST12, stg, SM::ST12, tid, nthr);
+  store_issue(K12t, stg, SM::ST12, tid, nthr);
+}
+
+template <class C>
+__global__ void __launch_bounds__(128, 3)
+k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+           const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12) {
+  constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
+  using SM = JacSmem<C>;
+  using EJ = EndJac<C>;
+  constexpr int NLT = SM::NLT;
+  extern __shared__ __align__(16) double smem[];
+  double* su = smem;
+  double* sq = su + SM::U;
+  double* sA = sq + SM::Q;
+  double* sAv = sA + SM::A;
+  double* sBq = sAv + SM::AV;
+  double* sE = sBq + SM::BQ;
+  double* stg = sE + SM::SEC;
+  double* sdg = stg + SM::STG;
+  const int T = blockIdx.x;  // tile id
+  const int k = T / C::TPE, s = T - k * C::TPE;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const size_t e = kp.order[k];
+  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+  // ---- phase 0: element state (+ gradient) and the endpoint flux Jacobians
+  // of the tile's line ends (k_endjac scratch), in tile-line order
+  cp_elem<C>(su, U + e * (NPE * M), NPE * M, tid, nthr);
+  if (C::SECOND) cp_elem<C>(sq, Q + e * (NPE * MD), NPE * MD, tid, nthr);
+  {
+    const double* se = SE + static_cast<size_t>(k) * EJ::PER_ELEM;
+    for (int w = tid; w < NLT * 2 * EJ::SLOT; w += nthr) {
+      const int idx = w / EJ::SLOT, o = w - idx * EJ::SLOT;
+      const int tl = idx >> 1, side = idx & 1;
+      int dir, line;
+      TileLines<C>::get(tl, s, dir, line);
+      sE[w] = __ldg(se + ((dir * 2 + side) * NL + line) * EJ::SLOT + o);
+    }
+  }
+  __syncthreads();
+  auto eidx = [](int tl, int, int, int side) { return tl * 2 + side; };
+  jac_tile<C>(kp, k, s, e, su, sq, mk, sE, eidx, sA, sAv, sBq, stg, sdg,
+              K11 + static_cast<size_t>(T) * SM::ST11, C::SECOND ? K12 + static_cast<size_t>(T) * SM::ST12 : nullptr,
+              tid, nthr);
+  store_wait(tid);
+}
+
+// Persistent, TMA-prefetching Jacobian assembly (2-D: one tile = one element).
+// Two input buffers {U, Q, metric, endpoint-Jacobian scratch} of consecutive
+// elements (processing order): the next element's inputs land while the
+// current one is assembled, and the current tile's bulk store drains while the
+// next one computes its flux Jacobians.
+template <class C>
+struct JacP {
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int U = ev(C::NPE * C::M);
+  static constexpr int Q = C::SECOND ? ev(C::NPE * C::MD) : 0;
+  static constexpr int MET = C::METP;
+  static constexpr int SE = ev(EndJac<C>::PER_ELEM);
+  static constexpr int BUF = U + Q + MET + SE;
+  using SM = JacSmem<C>;
+  static constexpr int WORK = SM::A + SM::AV + SM::BQ + SM::STG + SM::DG;
+  static constexpr int TOTAL = 2 + 2 * BUF + WORK;
+  static constexpr bool OK = C::D == 2 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
+                             (EndJac<C>::PER_ELEM % 2 == 0);
+};
+
+template <class C>
+__global__ void __launch_bounds__(128, 3)
+k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+             const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12) {
+  constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
+  using JP = JacP<C>;
+  using SM = JacSmem<C>;
+  using EJ = EndJac<C>;
+  extern __shared__ __align__(16) double smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* const bufs = smem + 2;
+  double* const work = bufs + 2 * JP::BUF;
+  double* sA = work;
+  double* sAv = sA + SM::A;
+  double* sBq = sAv + SM::AV;
+  double* stg = sBq + SM::BQ;
+  double* sdg = stg + SM::STG;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int G = gridDim.x;
+  if (static_cast<int>(blockIdx.x) >= kp.E) return;
+  auto bU = [&](int bi) { return bufs + bi * JP::BUF; };
+  auto bQ = [&](int bi) { return bufs + bi * JP::BUF + JP::U; };
+  auto bMET = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q; };
+  auto bSE = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET; };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k, int bi) {
+    const size_t e = __ldg(kp.order + k);
+    unsigned bytes = NPE * M * 8 + C::METP * 8 + EJ::PER_ELEM * 8;
+    if (C::SECOND) bytes += NPE * MD * 8;
+    mbar_expect_tx(&bar[bi], bytes);
+    tma_load_1d(bU(bi), U + e * (NPE * M), NPE * M * 8, &bar[bi]);
+    if (C::SECOND) tma_load_1d(bQ(bi), Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
+    tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k) * C::METP, C::METP * 8, &bar[bi]);
+    tma_load_1d(bSE(bi), SE + static_cast<size_t>(k) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
+  };
+  const int k0 = blockIdx.x;
+  if (tid == 0) {
+    issue(k0, 0);
+    if (k0 + G < kp.E) issue(k0 + G, 1);
+  }
+  auto eidx = [](int, int dir, int line, int side) { return (dir * 2 + side) * NL + line; };
+  for (int k = k0, it = 0; k < kp.E; k += G, ++it) {
+    const int cur = it & 1;
+    mbar_wait(&bar[cur], (it >> 1) & 1);
+    const size_t e = kp.order[k];
+    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bSE(cur), eidx, sA, sAv, sBq, stg, sdg,
+                K11 + static_cast<size_t>(k) * SM::ST11, C::SECOND ? K12 + static_cast<size_t>(k) * SM::ST12 : nullptr,
+                tid, nthr);
+    __syncthreads();  // all reads of buffer `cur` done
+    if (tid == 0 && k + 2 * G < kp.E) issue(k + 2 * G, cur);
+  }
+  store_wait(tid);
 }
 
 // K21 = dQ/dU (U-independent; D scalars per node pair):

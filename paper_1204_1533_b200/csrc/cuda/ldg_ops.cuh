@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "ldg_kernels.cuh"
@@ -32,9 +33,11 @@ struct DevCtx {
 struct Ops {
   int D, P, PH, RI, M, NP, NQ, NPE, NL, MD, NS11, NS12, B11, B12, R12, NT, TPE, METP, MET_NV, MET_NE;
   size_t jac_smem;
+  size_t endjac_per_elem;  // doubles of endpoint-Jacobian scratch per element
   cudaError_t (*residual)(const DevCtx&, const double* U, const double* Q, double* R);
   cudaError_t (*gradient)(const DevCtx&, const double* U, double* Q);
-  cudaError_t (*jacobian)(const DevCtx&, const double* U, const double* Q, double* K11, double* K12);
+  cudaError_t (*jacobian)(const DevCtx&, const double* U, const double* Q, double* SE, double* K11,
+                          double* K12);
   cudaError_t (*k21)(const DevCtx&, double* K21);
   cudaError_t (*spmv11)(const DevCtx&, const double* V11, const double* x, double* y);
   cudaError_t (*spmv12)(const DevCtx&, const double* V12, const double* w, double* y);
@@ -71,7 +74,30 @@ struct Launch {
   // Residual: thread-per-line kernel (k_residual).  The sub-warp variant
   // (k_residual_sw) is kept for comparison: it measured slower on B200
   // (profiles/ncu_r1_summary.md).
+  // Residual: persistent TMA-prefetching kernel (k_residual_p); the
+  // one-shot kernel k_residual is kept as the LDG_RESIDUAL_SIMPLE fallback.
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
+    static const bool simple = std::getenv("LDG_RESIDUAL_SIMPLE") != nullptr;
+    if (simple) return residual_simple(d, U, Q, R);
+    using RP = ResP<C, EPB>;
+    const size_t smem = sizeof(double) * RP::TOTAL;
+    static int grid_max = 0;
+    if (!grid_max) {
+      cudaFuncSetAttribute(k_residual_p<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_residual_p<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_residual_p<C, EPB>, RP::THREADS, smem);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    const int nbatch = (d.E + EPB - 1) / EPB;
+    const int grid = nbatch < grid_max ? nbatch : grid_max;
+    k_residual_p<C, EPB><<<grid, RP::THREADS, smem, d.stream>>>(params(d), U, Q, R);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t residual_simple(const DevCtx& d, const double* U, const double* Q, double* R) {
     const size_t smem = sizeof(double) *
                         (EPB * C::NPE * C::M + (C::SECOND ? EPB * C::NPE * C::MD : 0) + EPB * C::D * C::NPE * C::M);
     static bool init = false;
@@ -115,7 +141,9 @@ struct Launch {
     return cudaGetLastError();
   }
   static constexpr size_t jac_smem() { return sizeof(double) * JacSmem<C>::TOTAL; }
-  static cudaError_t jacobian(const DevCtx& d, const double* U, const double* Q, double* K11, double* K12) {
+  static constexpr int EJ_SEEDS = C::M;  // seeds per k_endjac thread (primal shared)
+  static cudaError_t jacobian(const DevCtx& d, const double* U, const double* Q, double* SE, double* K11,
+                              double* K12) {
     const size_t smem = jac_smem();
     static bool init = false;
     if (!init) {
@@ -123,7 +151,37 @@ struct Launch {
       cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       init = true;
     }
-    k_jacobian<C><<<d.E * C::TPE, 128, smem, d.stream>>>(params(d), U, Q, K11, K12);
+    constexpr int NSP = (C::M + EJ_SEEDS - 1) / EJ_SEEDS, NSQ = (C::MD + EJ_SEEDS - 1) / EJ_SEEDS;
+    constexpr int IPS = 2 * NSP + (C::SECOND ? NSQ : 0);
+    static const bool one_seed = std::getenv("LDG_ENDJAC_SEEDS1") != nullptr;  // tuning switch
+    if (one_seed) {
+      constexpr int NQ1 = C::SECOND ? C::MD : 0;
+      const long long items = static_cast<long long>(d.E) * 2 * C::D * C::NL * (2 * C::M + NQ1);
+      k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, 0, d.E);
+    } else {
+      const long long items = static_cast<long long>(d.E) * 2 * C::D * C::NL * IPS;
+      k_endjac<C, EJ_SEEDS><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, 0,
+                                                                                       d.E);
+    }
+    count(d);
+    static const bool simple = std::getenv("LDG_JACOBIAN_SIMPLE") != nullptr;
+    if (JacP<C>::OK && !simple) {
+      const size_t psmem = sizeof(double) * JacP<C>::TOTAL;
+      static int grid_max = 0;
+      if (!grid_max) {
+        cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobian_p<C>, 128, psmem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid_max = (per_sm > 0 ? per_sm : 1) * sms;
+      }
+      const int grid = d.E < grid_max ? d.E : grid_max;
+      k_jacobian_p<C><<<grid, 128, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12);
+    } else {
+      k_jacobian<C><<<d.E * C::TPE, 128, smem, d.stream>>>(params(d), U, Q, SE, K11, K12);
+    }
     count(d);
     return cudaGetLastError();
   }
@@ -164,7 +222,7 @@ struct Launch {
   static const Ops* table() {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
-                            C::MET_NV, C::MET_NE, jac_smem(), residual, gradient, jacobian, k21,
+                            C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, residual, gradient, jacobian, k21,
                             spmv11, spmv12, spmv21, split};
     return &ops;
   }
