@@ -1604,63 +1604,54 @@ __device__ __forceinline__ int64_t slot_col(const KParams<C>& kp, int k, size_t 
   return static_cast<int64_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
 }
 
-// y = K11 x  (FUSE: y = v - adt (K11 v + K12 w), used by the split matvec)
+// y = K11 x  (SPLIT: y = v - adt (K11 v + K12 w), the split matvec).
+// One thread per (row, output component a): a warp streams 32 consecutive
+// rows of one block row a, so every value load is contiguous; the x entries
+// of a column are shared by the m threads of a row through L1.
 template <class C, bool SPLIT>
 __global__ void __launch_bounds__(128)
 k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __restrict__ V12,
          const double* __restrict__ x, const double* __restrict__ w, double adt, double* __restrict__ y) {
   constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
+  // thread -> (row group of 32 rows, a, lane)
+  const int lane = static_cast<int>(gid & 31);
+  const int64_t wg = gid >> 5;
+  const int a = static_cast<int>(wg % M);
+  const int64_t row = (wg / M) * 32 + lane;
   if (row >= nrows) return;
   const int64_t T = row / NT;
   const int r = static_cast<int>(row - T * NT);
   const int k = static_cast<int>(T / C::TPE);
   const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
   const int nd = s * NT + r;
-  const size_t e = kp.order[k];
-  double acc[M];
-#pragma unroll
-  for (int a = 0; a < M; ++a) acc[a] = 0.0;
-  const double* vb = V11 + T * (C::NS11 * C::B11 * NT) + r;
+  const size_t e = __ldg(kp.order + k);
+  double acc = 0.0;
+  const double* vb = V11 + T * (C::NS11 * C::B11 * NT) + a * M * NT + r;
 #pragma unroll
   for (int slot = 0; slot < C::NS11; ++slot) {
     const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 0);
-    double xv[M];
-    if (col >= 0) {
+    if (col < 0) continue;
 #pragma unroll
-      for (int b = 0; b < M; ++b) xv[b] = __ldg(x + col * M + b);
-    } else {
-#pragma unroll
-      for (int b = 0; b < M; ++b) xv[b] = 0.0;
-    }
-#pragma unroll
-    for (int a = 0; a < M; ++a)
-#pragma unroll
-      for (int b = 0; b < M; ++b) acc[a] += __ldg(vb + ((slot * C::B11) + a * M + b) * NT) * xv[b];
+    for (int b = 0; b < M; ++b) acc += __ldg(vb + (slot * C::B11 + b) * NT) * __ldg(x + col * M + b);
   }
   if (SPLIT && C::SECOND) {
     constexpr int A0 = C::PH == PH_NS ? 1 : 0;
-    const double* vq = V12 + T * (C::NS12 * C::B12 * NT) + r;
+    if (a >= A0) {
+      const double* vq = V12 + T * (C::NS12 * C::B12 * NT) + (a - A0) * MD * NT + r;
 #pragma unroll
-    for (int slot = 0; slot < C::NS12; ++slot) {
-      const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
-      if (col < 0) continue;
-      double wv[MD];
+      for (int slot = 0; slot < C::NS12; ++slot) {
+        const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
+        if (col < 0) continue;
 #pragma unroll
-      for (int b = 0; b < MD; ++b) wv[b] = __ldg(w + col * MD + b);
-#pragma unroll
-      for (int a = 0; a < C::R12; ++a)
-#pragma unroll
-        for (int b = 0; b < MD; ++b) acc[a + A0] += __ldg(vq + ((slot * C::B12) + a * MD + b) * NT) * wv[b];
+        for (int b = 0; b < MD; ++b) acc += __ldg(vq + (slot * C::B12 + b) * NT) * __ldg(w + col * MD + b);
+      }
     }
   }
-  const size_t yo = (e * NPE + nd) * M;
-#pragma unroll
-  for (int a = 0; a < M; ++a) {
-    if (SPLIT) y[yo + a] = __ldg(x + yo + a) - adt * acc[a];
-    else y[yo + a] = acc[a];
-  }
+  const size_t yo = (e * NPE + nd) * M + a;
+  if (SPLIT) y[yo] = __ldg(x + yo) - adt * acc;
+  else y[yo] = acc;
 }
 
 // y = K12 w  (w: m*D per node)

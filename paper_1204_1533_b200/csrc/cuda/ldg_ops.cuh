@@ -195,8 +195,14 @@ struct Launch {
     const long long rows = static_cast<long long>(d.E) * C::NPE;
     return static_cast<int>((rows + 127) / 128);
   }
+  // one thread per (row, component), rows in groups of 32 per warp
+  static int rgrid_m(const DevCtx& d) {
+    const long long rows = static_cast<long long>(d.E) * C::NPE;
+    const long long threads = (rows + 31) / 32 * 32 * C::M;
+    return static_cast<int>((threads + 127) / 128);
+  }
   static cudaError_t spmv11(const DevCtx& d, const double* V11, const double* x, double* y) {
-    k_spmv11<C, false><<<rgrid(d), 128, 0, d.stream>>>(params(d), V11, nullptr, x, nullptr, 0.0, y);
+    k_spmv11<C, false><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, nullptr, x, nullptr, 0.0, y);
     count(d);
     return cudaGetLastError();
   }
@@ -214,7 +220,7 @@ struct Launch {
   }
   static cudaError_t split(const DevCtx& d, const double* V11, const double* V12, const double* v,
                            const double* w, double adt, double* y) {
-    k_spmv11<C, true><<<rgrid(d), 128, 0, d.stream>>>(params(d), V11, V12, v, w, adt, y);
+    k_spmv11<C, true><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, V12, v, w, adt, y);
     count(d);
     return cudaGetLastError();
   }
