@@ -35,9 +35,12 @@ struct Cfg {
   static constexpr int MET_NE = D * 2 * NL * D;
   static constexpr int MET = MET_NV + MET_NE + NPE;
   static constexpr int METP = (MET + 1) / 2 * 2;
-  // Line-structured Jacobian store: rows tiled by NT = NP^2 rows (2-D: one
-  // element, 3-D: one slab x2 = const).
-  static constexpr int NT = NP * NP;
+  // Line-structured Jacobian store: rows tiled by NT rows.  2-D: one
+  // element (NP^2 rows); 3-D: one slab x2 = const (NP^2 rows), or, for the
+  // 3-D p >= 4 Navier-Stokes operator whose slab tile does not fit shared
+  // memory, one dir-0 coordinate line (NP rows).  Node = tile*NT + row.
+  static constexpr int TD = (D == 3 && PH == PH_NS && P >= 4) ? 1 : 2;
+  static constexpr int NT = TD == 1 ? NP : NP * NP;
   static constexpr int TPE = NPE / NT;                    // tiles per element
   static constexpr int NS11 = D * P + 1 + 2 * D;          // K11 node-columns per row
   static constexpr int NS12 = D * P + 1 + D;              // K12 / K21 node-columns per row

@@ -941,22 +941,49 @@ k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict
 }
 
 // ===================================================================== Jacobian
-// Lines intersecting tile `s` of an element: 2-D: all D*NL lines (full).
-// 3-D: dir-0 and dir-1 lines of slab s (full) and every dir-2 line (row s only).
+// Lines intersecting tile `s` of an element.
+//   2-D: all D*NL lines, all rows on them in the tile ("full").
+//   3-D slab tiles (x2 = s): dir-0 and dir-1 lines of the slab (full) and every
+//     dir-2 line (only its row at position s).
+//   3-D line tiles (dir-0 line s = j + NP k): that dir-0 line (full), the
+//     dir-1 lines (i, k) (row at position j) and dir-2 lines (i, j) (row k).
+// prow(): position on the line of the tile's single row for non-full lines.
 template <class C>
 struct TileLines {
-  static constexpr int NLT = C::D == 2 ? C::D * C::NL : 2 * C::NP + C::NP * C::NP;
+  static constexpr int NLT = C::D == 2 ? C::D * C::NL : (C::TD == 2 ? 2 * C::NP + C::NP * C::NP : 1 + 2 * C::NP);
   __device__ static __forceinline__ void get(int tl, int s, int& dir, int& line) {
+    constexpr int NP = C::NP;
     if (C::D == 2) {
       dir = tl / C::NL;
       line = tl - dir * C::NL;
-    } else if (tl < 2 * C::NP) {
-      dir = tl / C::NP;
-      line = (tl - dir * C::NP) + C::NP * s;
+    } else if (C::TD == 2) {
+      if (tl < 2 * NP) {
+        dir = tl / NP;
+        line = (tl - dir * NP) + NP * s;
+      } else {
+        dir = 2;
+        line = tl - 2 * NP;
+      }
     } else {
-      dir = 2;
-      line = tl - 2 * C::NP;
+      const int j = s % NP, k = s / NP;
+      if (tl == 0) {
+        dir = 0;
+        line = s;
+      } else if (tl <= NP) {
+        dir = 1;
+        line = (tl - 1) + NP * k;
+      } else {
+        dir = 2;
+        line = (tl - 1 - NP) + NP * j;
+      }
     }
+  }
+  __device__ static __forceinline__ bool full(int dir) {
+    return C::D == 2 || (C::TD == 2 ? dir < 2 : dir == 0);
+  }
+  __device__ static __forceinline__ int prow(int dir, int s) {
+    if (C::TD == 2) return s;
+    return dir == 1 ? s % C::NP : s / C::NP;
   }
 };
 
@@ -1127,6 +1154,13 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 // K11 (+ K12 for second-order physics) of one row tile.  Store layout:
 //   K11[((T*NS11 + slot)*B11 + a*M + b)*NT + r]       T = k*TPE + tile, r = row in tile
 //   K12[((T*NS12 + slot)*B12 + a'*MD + b)*NT + r]     a' = stored row (NS: a-1)
+// Jacobian CTA size (128 threads keeps 3 CTAs/SM within the register file).
+template <class C>
+struct JacThreads {
+  static constexpr int value = 128;
+  static constexpr int min_blocks = 3;
+};
+
 template <class C>
 struct JacSmem {
   static constexpr int NLT = TileLines<C>::NLT;
@@ -1266,7 +1300,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const int tl = w / B11, ab = w - tl * B11;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
-    const bool full = C::D == 2 || dir < 2;
+    const bool full = TileLines<C>::full(dir);
     double av[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -1299,7 +1333,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
       for (int i = 0; i < NP; ++i) body(i);
     } else {
-      body(s);
+      body(TileLines<C>::prow(dir, s));
     }
   }
   __syncthreads();
@@ -1326,7 +1360,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const int a = ab / MD + A0, b = ab % MD;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
-    const bool full = C::D == 2 || dir < 2;
+    const bool full = TileLines<C>::full(dir);
     double bv[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) bv[q] = sBq[(tl * NQ + q) * M * MD + a * MD + b];
@@ -1357,7 +1391,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
       for (int i = 0; i < NP; ++i) body(i);
     } else {
-      body(s);
+      body(TileLines<C>::prow(dir, s));
     }
   }
   __syncthreads();
@@ -1374,7 +1408,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 }
 
 template <class C>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(JacThreads<C>::value, JacThreads<C>::min_blocks)
 k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
            const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12) {
   constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
@@ -1438,7 +1472,7 @@ struct JacP {
 };
 
 template <class C>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(JacThreads<C>::value, JacThreads<C>::min_blocks)
 k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
              const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12) {
   constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
@@ -1514,7 +1548,7 @@ __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __rest
     const int tl = w / D, d = w - tl * D;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
-    const bool full = C::D == 2 || dir < 2;
+    const bool full = TileLines<C>::full(dir);
     double nvd[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) nvd[q] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
@@ -1546,7 +1580,7 @@ __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __rest
 #pragma unroll
       for (int i = 0; i < NP; ++i) body(i);
     } else {
-      body(s);
+      body(TileLines<C>::prow(dir, s));
     }
   }
   __syncthreads();

@@ -172,15 +172,15 @@ struct Launch {
         cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
         cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         int per_sm = 0, dev = 0, sms = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobian_p<C>, 128, psmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobian_p<C>, JacThreads<C>::value, psmem);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid_max = (per_sm > 0 ? per_sm : 1) * sms;
       }
       const int grid = d.E < grid_max ? d.E : grid_max;
-      k_jacobian_p<C><<<grid, 128, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12);
+      k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12);
     } else {
-      k_jacobian<C><<<d.E * C::TPE, 128, smem, d.stream>>>(params(d), U, Q, SE, K11, K12);
+      k_jacobian<C><<<d.E * C::TPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11, K12);
     }
     count(d);
     return cudaGetLastError();
