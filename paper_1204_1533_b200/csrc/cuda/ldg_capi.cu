@@ -627,7 +627,7 @@ int ldg_jacobian_assemble(ldg_ctx* c, const double* U, double t) {
         c->k21_valid = true;
       }
     }
-    ensure(c->d_SE, static_cast<size_t>(c->E) * o.endjac_per_elem);
+    ensure(c->d_SE, o.scratch_elems(c->E));
     const int st = finish(c, o.jacobian(c->dc, U, q, c->d_SE, c->d_K11, c->d_K12));
     c->jac_valid = st == LDG_OK;
     return st;
@@ -709,8 +709,11 @@ int ldg_export_blocks_subset(ldg_ctx* c, int which, const int32_t* elems, int32_
             std::fill(blk, blk + br * bc, 0.0);
             for (size_t z = a; z < b; ++z) {
               const int sl = cl[z].second;
+              // store: per (tile, slot) a bsz*NT run laid out [block row][row r][column]
+              const int scol = which == LDG_K11 ? c->m : (which == LDG_K12 ? o.MD : c->D);
               auto at = [&](int ab) {
-                return chunk[((static_cast<size_t>(tile) * NS + sl) * bsz + ab) * NT + r];
+                const int aa = ab / scol, bb = ab % scol;
+                return chunk[(static_cast<size_t>(tile) * NS + sl) * bsz * NT + (static_cast<size_t>(aa) * NT + r) * scol + bb];
               };
               if (which == LDG_K11) {
                 for (int ab = 0; ab < bsz; ++ab) blk[ab] += at(ab);

@@ -1027,7 +1027,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const bool bd = cn.x < 0;
   const int S = conn_sign(cn.y);
   const int nd = node_on_line<C>(dir, line, side ? P : 0);
-  double* slot = SE + static_cast<size_t>(k) * EJ::PER_ELEM + static_cast<size_t>(gs) * EJ::SLOT;
+  double* slot = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM + static_cast<size_t>(gs) * EJ::SLOT;
   int pass, g0;
   if (sub < NSP) {
     pass = 0;
@@ -1155,43 +1155,58 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 //   K11[((T*NS11 + slot)*B11 + a*M + b)*NT + r]       T = k*TPE + tile, r = row in tile
 //   K12[((T*NS12 + slot)*B12 + a'*MD + b)*NT + r]     a' = stored row (NS: a-1)
 // Jacobian CTA size (128 threads keeps 3 CTAs/SM within the register file).
+// Jacobian store (block-contiguous line-structured BSR): row tiles of NT rows,
+// blocks contiguous in row-major order:
+//   K11[(((T*NS11 + slot)*m + a)*NT + r)*m + b]
+//   K12[(((T*NS12 + slot)*R12 + a')*NT + r)*mD + b]      (NS: a' = a-1)
+//   K21[((T*NS12 + slot)*NT + r)*D + d]                   (component-diagonal)
+// i.e. per (slot, block row a) the rows of the tile are consecutive and each
+// row's m entries contiguous.  The assembly writes straight from registers:
+// one thread per (tile line, a, b) forms the line blocks of every row of its
+// line, so each group of m lanes stores one full block row (32 B for m=4:
+// whole sectors); an SpMV warp (32 rows of one block row a) reads one
+// contiguous 1 KB run per slot.  The self (diagonal) block of a row collects the
+// contributions of all D lines through it; the dir-0 thread adds the other
+// directions' terms, so every entry is written exactly once (no atomics, no
+// staging tile, no zero fill).
 template <class C>
 struct JacThreads {
   static constexpr int value = 128;
-  static constexpr int min_blocks = 3;
+  static constexpr int min_blocks = 4;
 };
 
 template <class C>
 struct JacSmem {
   static constexpr int NLT = TileLines<C>::NLT;
-  static constexpr int NDA = C::SECOND ? C::MD : 1;  // q-derivative slots
   static constexpr int U = C::NPE * C::M;
   static constexpr int Q = C::SECOND ? C::NPE * C::MD : 0;
-  static constexpr int UO = 0;  // neighbour traces: consumed by k_endjac only
-  static constexpr int QO = 0;
   static constexpr int A = C::HAS_INV ? NLT * C::NQ * C::B11 : 0;  // dFinv/du . nvec at quad points
   static constexpr int AV = C::VIS_U ? NLT * C::NQ * C::B11 : 0;    // dFvis/du . nvec
   static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
   static constexpr int SEC = NLT * 2 * EndJac<C>::SLOT;       // endpoint flux Jacobians (tile lines)
-  static constexpr int ST11 = C::NS11 * C::B11 * C::NT;
+  static constexpr int TAB = (C::NP * C::NQ + 2 * C::NP + 1) / 2 * 2;  // cc diagonal + M^-1 columns
+  static constexpr int ST11 = C::NS11 * C::B11 * C::NT;       // store doubles per tile
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
-  static constexpr int STG = ST11 > ST12 ? ST11 : ST12;
-  static constexpr int DG = (C::D - 1) * C::NT * (C::B11 > C::B12 ? C::B11 : C::B12);  // diag scratch
-  static constexpr int TOTAL = U + Q + A + AV + BQ + SEC + STG + DG;
+  static constexpr int WORK = A + AV + BQ + TAB;
+  static constexpr int TOTAL = U + Q + SEC + WORK;
 };
 
-// Phases 1-3 of one Jacobian row tile, all operands in shared memory (or
-// read-only global for the metric of the one-shot kernel):
-//   su/sq element state and gradient, mk metric of the element (1/J
-//   included), sE endpoint flux Jacobians indexed by eidx(tl,dir,line,side).
-// K11t / K12t: this tile's destination in the store.  The tile leaves through
-// an asynchronous bulk store; callers wait (store_wait) before the staging
-// buffer is reused or the CTA exits.
+template <class C>
+__device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
+  constexpr int NP = C::NP;
+  if (C::D == 2) return dir * C::NL + line;
+  if (C::TD == 2) return dir < 2 ? dir * NP + line % NP : 2 * NP + line;
+  return dir == 0 ? 0 : (dir == 1 ? 1 + line % NP : 1 + NP + line % NP);
+}
+
+// One Jacobian row tile.  su/sq element state and gradient, mk the element's
+// metric (1/J included), sE the endpoint flux Jacobians of the tile lines
+// indexed by eidx(tl, dir, line, side); stab = {cc[p][p][q], mi[p][s]}.
 template <class C, class EIdx>
 __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, const int s, const size_t e,
                                          const double* su, const double* sq, const double* mk,
                                          const double* sE, EIdx eidx, double* sA, double* sAv, double* sBq,
-                                         double* stg, double* sdg, double* __restrict__ K11t,
+                                         const double* stab, double* __restrict__ K11t,
                                          double* __restrict__ K12t, const int tid, const int nthr) {
   constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, M = C::M, D = C::D, MD = C::MD, NT = C::NT, P = C::P,
                 B11 = C::B11;
@@ -1277,24 +1292,11 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   }
   __syncthreads();
 
-  // ---- phase 2: K11 line blocks into the staging tile (after any pending
-  // bulk store of the previous tile has read it out)
-  store_wait(tid);
-  // Each item = (tile line, a, b).  Row i of the line (all i for full lines,
-  // i = s for 3-D dir-2 lines) gets, for column t on the line,
-  //   B(i,t) = sum_q cc[i][t][q] A_q[a][b] + [t == end] mi[i][side] Ein[a][b]
-  // and for neighbour (side): mi[i][side] Eout[a][b]; scaled by -1/J_row.
-  auto row_slot_store = [&](int dir, int line, int i, int t, double v, double* base, int bsz,
-                            int ab, int nslot_unused) {
-    (void)nslot_unused;
-    const int nd = node_on_line<C>(dir, line, i);
-    const int r = nd - s * NT;
-    if (t == i && dir > 0) {
-      sdg[((dir - 1) * NT + r) * bsz + ab] = v;
-    } else {
-      const int slot = inel_slot<C>(dir, i, t);
-      base[(slot * bsz + ab) * NT + r] = v;
-    }
+  // ---- phase 2: K11 rows of every tile line, stored block row by block row
+  const double* sccd = stab;            // cc[p][p][q]
+  const double* smi = stab + NP * NQ;   // M^-1[p][0], M^-1[p][p]
+  auto avq = [&](int tl, int q, int ab) {
+    return (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
   };
   for (int w = tid; w < NLT * B11; w += nthr) {
     const int tl = w / B11, ab = w - tl * B11;
@@ -1303,8 +1305,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const bool full = TileLines<C>::full(dir);
     double av[NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q)
-      av[q] = (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
+    for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(tl, q, ab) : 0.0;
     const double* e0 = sE + eidx(tl, dir, line, 0) * EJ::SLOT;
     const double* e1 = sE + eidx(tl, dir, line, 1) * EJ::SLOT;
     const double ein0 = e0[ab], ein1 = e1[ab];
@@ -1313,9 +1314,12 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
+      const int r = nd - s * NT;
       const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+      double* rowp = K11t + (static_cast<size_t>(ab / M) * NT + r) * M + ab % M;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
+        if (t == i && dir != 0) continue;  // the dir-0 thread owns the self block
         double v = 0.0;
         if (VOL11) {
 #pragma unroll
@@ -1323,11 +1327,25 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
         }
         if (t == 0) v += kp.bt.mi[i][0] * ein0;
         if (t == P) v += kp.bt.mi[i][1] * ein1;
-        row_slot_store(dir, line, i, t, sc * v, stg, B11, ab, 0);
+        if (t == i) {
+          // self block: add the lines of the other directions through this node
+#pragma unroll
+          for (int d2 = 1; d2 < D; ++d2) {
+            int l2, p2;
+            line_of<C>(d2, nd, l2, p2);
+            const int tl2 = tile_line_of<C>(d2, l2, s);
+            if (VOL11) {
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) v += sccd[p2 * NQ + q] * avq(tl2, q, ab);
+            }
+            if (p2 == 0) v += smi[p2 * 2 + 0] * sE[eidx(tl2, d2, l2, 0) * EJ::SLOT + ab];
+            if (p2 == P) v += smi[p2 * 2 + 1] * sE[eidx(tl2, d2, l2, 1) * EJ::SLOT + ab];
+          }
+        }
+        rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B11] = sc * v;
       }
-      const int r = nd - s * NT;
-      stg[((C::D * P + 1 + 2 * dir + 0) * B11 + ab) * NT + r] = c0.x >= 0 ? sc * (kp.bt.mi[i][0] * eo0) : 0.0;
-      stg[((C::D * P + 1 + 2 * dir + 1) * B11 + ab) * NT + r] = c1.x >= 0 ? sc * (kp.bt.mi[i][1] * eo1) : 0.0;
+      rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 0) * NT * B11] = c0.x >= 0 ? sc * (kp.bt.mi[i][0] * eo0) : 0.0;
+      rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 1) * NT * B11] = c1.x >= 0 ? sc * (kp.bt.mi[i][1] * eo1) : 0.0;
     };
     if (full) {
 #pragma unroll
@@ -1336,25 +1354,10 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       body(TileLines<C>::prow(dir, s));
     }
   }
-  __syncthreads();
-  // diagonal: slot x0 += contributions of the dir >= 1 lines (dir order)
-  for (int w = tid; w < NT * B11; w += nthr) {
-    const int r = w / B11, ab = w - r * B11;
-    const int x0 = r % NP;
-    double v = stg[(x0 * B11 + ab) * NT + r];
-#pragma unroll
-    for (int d = 1; d < D; ++d) v = v + sdg[((d - 1) * NT + r) * B11 + ab];
-    stg[(x0 * B11 + ab) * NT + r] = v;
-  }
-  __syncthreads();
-  store_issue(K11t, stg, SM::ST11, tid, nthr);
   if (!C::SECOND) return;
-  store_wait(tid);
 
-  // ---- phase 3: K12 = dR/dQ (rows a' of the stored block)
-  constexpr int B12 = C::B12, R12 = C::R12, A0 = C::PH == PH_NS ? 1 : 0;
-  for (int i = tid; i < SM::ST12; i += nthr) stg[i] = 0.0;
-  __syncthreads();
+  // ---- phase 3: K12 = dR/dQ (stored rows a' of each block)
+  constexpr int B12 = C::B12, A0 = C::PH == PH_NS ? 1 : 0;
   for (int w = tid; w < NLT * B12; w += nthr) {
     const int tl = w / B12, ab = w - tl * B12;
     const int a = ab / MD + A0, b = ab % MD;
@@ -1373,19 +1376,39 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
+      const int r = nd - s * NT;
       const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+      double* rowp = K12t + (static_cast<size_t>(ab / MD) * NT + r) * MD + ab % MD;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
+        if (t == i && dir != 0) continue;
         double v = 0.0;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * bv[q];
         if (t == 0 && own0) v += kp.bt.mi[i][0] * eq0;
         if (t == P && own1) v += kp.bt.mi[i][1] * eq1;
-        row_slot_store(dir, line, i, t, sc * v, stg, B12, ab, 0);
+        if (t == i) {
+#pragma unroll
+          for (int d2 = 1; d2 < D; ++d2) {
+            int l2, p2;
+            line_of<C>(d2, nd, l2, p2);
+            const int tl2 = tile_line_of<C>(d2, l2, s);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) v += sccd[p2 * NQ + q] * sBq[(tl2 * NQ + q) * M * MD + a * MD + b];
+            if (p2 == 0 || p2 == P) {
+              const int sd2 = p2 == 0 ? 0 : 1;
+              const int2 cx = __ldg(&kp.conn[(static_cast<size_t>(k) * D + d2) * 2 + sd2]);
+              if (cx.x < 0 || conn_sign(cx.y) <= 0)
+                v += smi[p2 * 2 + sd2] * sE[eidx(tl2, d2, l2, sd2) * EJ::SLOT + 2 * B11 + a * MD + b];
+            }
+          }
+        }
+        rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B12] = sc * v;
       }
-      const int r = nd - s * NT;
-      if (!own0) stg[((C::D * P + 1 + dir) * B12 + ab) * NT + r] = sc * (kp.bt.mi[i][0] * eq0);
-      if (!own1) stg[((C::D * P + 1 + dir) * B12 + ab) * NT + r] = sc * (kp.bt.mi[i][1] * eq1);
+      double nbv = 0.0;
+      if (!own0) nbv = sc * (kp.bt.mi[i][0] * eq0);
+      if (!own1) nbv = sc * (kp.bt.mi[i][1] * eq1);
+      rowp[static_cast<size_t>(C::D * P + 1 + dir) * NT * B12] = nbv;
     };
     if (full) {
 #pragma unroll
@@ -1394,23 +1417,22 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       body(TileLines<C>::prow(dir, s));
     }
   }
-  __syncthreads();
-  for (int w = tid; w < NT * B12; w += nthr) {
-    const int r = w / B12, ab = w - r * B12;
-    const int x0 = r % NP;
-    double v = stg[(x0 * B12 + ab) * NT + r];
-#pragma unroll
-    for (int d = 1; d < D; ++d) v = v + sdg[((d - 1) * NT + r) * B12 + ab];
-    stg[(x0 * B12 + ab) * NT + r] = v;
+}
+
+template <class C>
+__device__ __forceinline__ void fill_tab(const KParams<C>& kp, double* stab, int tid, int nthr) {
+  constexpr int NP = C::NP, NQ = C::NQ;
+  for (int i = tid; i < NP * NQ; i += nthr) {
+    const int p = i / NQ, q = i - p * NQ;
+    stab[i] = kp.bt.cc[p][p][q];
   }
-  __syncthreads();
-  store_issue(K12t, stg, SM::ST12, tid, nthr);
+  for (int i = tid; i < 2 * NP; i += nthr) stab[NP * NQ + i] = (&kp.bt.mi[0][0])[i];
 }
 
 template <class C>
 __global__ void __launch_bounds__(JacThreads<C>::value, JacThreads<C>::min_blocks)
 k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-           const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12) {
+           const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12, int k_begin) {
   constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
   using SM = JacSmem<C>;
   using EJ = EndJac<C>;
@@ -1418,23 +1440,22 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   extern __shared__ __align__(16) double smem[];
   double* su = smem;
   double* sq = su + SM::U;
-  double* sA = sq + SM::Q;
+  double* sE = sq + SM::Q;
+  double* sA = sE + SM::SEC;
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
-  double* sE = sBq + SM::BQ;
-  double* stg = sE + SM::SEC;
-  double* sdg = stg + SM::STG;
-  const int T = blockIdx.x;  // tile id
+  double* stab = sBq + SM::BQ;
+  const int T = blockIdx.x + k_begin * C::TPE;  // tile id
   const int k = T / C::TPE, s = T - k * C::TPE;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const size_t e = kp.order[k];
   const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-  // ---- phase 0: element state (+ gradient) and the endpoint flux Jacobians
-  // of the tile's line ends (k_endjac scratch), in tile-line order
+  // element state (+ gradient), endpoint flux Jacobians of the tile's line
+  // ends (k_endjac scratch of this chunk) in tile-line order, tables
   cp_elem<C>(su, U + e * (NPE * M), NPE * M, tid, nthr);
   if (C::SECOND) cp_elem<C>(sq, Q + e * (NPE * MD), NPE * MD, tid, nthr);
   {
-    const double* se = SE + static_cast<size_t>(k) * EJ::PER_ELEM;
+    const double* se = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM;
     for (int w = tid; w < NLT * 2 * EJ::SLOT; w += nthr) {
       const int idx = w / EJ::SLOT, o = w - idx * EJ::SLOT;
       const int tl = idx >> 1, side = idx & 1;
@@ -1443,19 +1464,16 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
       sE[w] = __ldg(se + ((dir * 2 + side) * NL + line) * EJ::SLOT + o);
     }
   }
+  fill_tab<C>(kp, stab, tid, nthr);
   __syncthreads();
   auto eidx = [](int tl, int, int, int side) { return tl * 2 + side; };
-  jac_tile<C>(kp, k, s, e, su, sq, mk, sE, eidx, sA, sAv, sBq, stg, sdg,
-              K11 + static_cast<size_t>(T) * SM::ST11, C::SECOND ? K12 + static_cast<size_t>(T) * SM::ST12 : nullptr,
-              tid, nthr);
-  store_wait(tid);
+  jac_tile<C>(kp, k, s, e, su, sq, mk, sE, eidx, sA, sAv, sBq, stab, K11 + static_cast<size_t>(T) * SM::ST11,
+              C::SECOND ? K12 + static_cast<size_t>(T) * SM::ST12 : nullptr, tid, nthr);
 }
 
-// Persistent, TMA-prefetching Jacobian assembly (2-D: one tile = one element).
-// Two input buffers {U, Q, metric, endpoint-Jacobian scratch} of consecutive
-// elements (processing order): the next element's inputs land while the
-// current one is assembled, and the current tile's bulk store drains while the
-// next one computes its flux Jacobians.
+// Persistent, TMA-prefetching Jacobian assembly (2-D: one tile = one element):
+// two input buffers {U, Q, metric, endpoint-Jacobian scratch} of consecutive
+// elements; the next element's inputs land while the current one assembles.
 template <class C>
 struct JacP {
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
@@ -1465,8 +1483,7 @@ struct JacP {
   static constexpr int SE = ev(EndJac<C>::PER_ELEM);
   static constexpr int BUF = U + Q + MET + SE;
   using SM = JacSmem<C>;
-  static constexpr int WORK = SM::A + SM::AV + SM::BQ + SM::STG + SM::DG;
-  static constexpr int TOTAL = 2 + 2 * BUF + WORK;
+  static constexpr int TOTAL = 2 + 2 * BUF + SM::WORK;
   static constexpr bool OK = C::D == 2 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
                              (EndJac<C>::PER_ELEM % 2 == 0);
 };
@@ -1474,7 +1491,8 @@ struct JacP {
 template <class C>
 __global__ void __launch_bounds__(JacThreads<C>::value, JacThreads<C>::min_blocks)
 k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-             const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12) {
+             const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12, int k_begin,
+             int k_end) {
   constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
   using JP = JacP<C>;
   using SM = JacSmem<C>;
@@ -1486,11 +1504,10 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   double* sA = work;
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
-  double* stg = sBq + SM::BQ;
-  double* sdg = stg + SM::STG;
+  double* stab = sBq + SM::BQ;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = gridDim.x;
-  if (static_cast<int>(blockIdx.x) >= kp.E) return;
+  if (k_begin + static_cast<int>(blockIdx.x) >= k_end) return;
   auto bU = [&](int bi) { return bufs + bi * JP::BUF; };
   auto bQ = [&](int bi) { return bufs + bi * JP::BUF + JP::U; };
   auto bMET = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q; };
@@ -1500,6 +1517,7 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     mbar_init(&bar[1], 1);
     mbar_fence_init();
   }
+  fill_tab<C>(kp, stab, tid, nthr);
   __syncthreads();
   auto issue = [&](int k, int bi) {
     const size_t e = __ldg(kp.order + k);
@@ -1509,72 +1527,84 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     tma_load_1d(bU(bi), U + e * (NPE * M), NPE * M * 8, &bar[bi]);
     if (C::SECOND) tma_load_1d(bQ(bi), Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
     tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k) * C::METP, C::METP * 8, &bar[bi]);
-    tma_load_1d(bSE(bi), SE + static_cast<size_t>(k) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
+    tma_load_1d(bSE(bi), SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
   };
-  const int k0 = blockIdx.x;
+  const int k0 = k_begin + blockIdx.x;
   if (tid == 0) {
     issue(k0, 0);
-    if (k0 + G < kp.E) issue(k0 + G, 1);
+    if (k0 + G < k_end) issue(k0 + G, 1);
   }
   auto eidx = [](int, int dir, int line, int side) { return (dir * 2 + side) * NL + line; };
-  for (int k = k0, it = 0; k < kp.E; k += G, ++it) {
+  for (int k = k0, it = 0; k < k_end; k += G, ++it) {
     const int cur = it & 1;
     mbar_wait(&bar[cur], (it >> 1) & 1);
     const size_t e = kp.order[k];
-    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bSE(cur), eidx, sA, sAv, sBq, stg, sdg,
+    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bSE(cur), eidx, sA, sAv, sBq, stab,
                 K11 + static_cast<size_t>(k) * SM::ST11, C::SECOND ? K12 + static_cast<size_t>(k) * SM::ST12 : nullptr,
                 tid, nthr);
-    __syncthreads();  // all reads of buffer `cur` done
-    if (tid == 0 && k + 2 * G < kp.E) issue(k + 2 * G, cur);
+    __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done
+    if (tid == 0 && k + 2 * G < k_end) issue(k + 2 * G, cur);
   }
-  store_wait(tid);
 }
 
-// K21 = dQ/dU (U-independent; D scalars per node pair):
-//   K21[((T*NS12 + slot)*D + d)*NT + r]
+// K21 = dQ/dU (U-independent; D scalars per node pair), same tiles/rows.
 template <class C>
 __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __restrict__ K21) {
   constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, D = C::D, NT = C::NT, P = C::P;
   constexpr int NLT = TileLines<C>::NLT;
   constexpr int ST = C::NS12 * D * NT;
-  __shared__ double stg[ST];
-  __shared__ double sdg[(D - 1) * NT * D + 1];
   const int T = blockIdx.x;
   const int k = T / C::TPE, s = T - k * C::TPE;
   const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-  for (int i = threadIdx.x; i < ST; i += blockDim.x) stg[i] = 0.0;
-  __syncthreads();
+  double* Kt = K21 + static_cast<size_t>(T) * ST;
+  auto coef = [&](int dir, int line, int p, int t, int d, int2 c0, int2 c1) {
+    // line block entry (row position p, column position t) of direction d
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v += kp.bt.cc[p][t][q] * __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
+    // u_hat = own trace where S = +1, neighbour where S = -1, g_D on boundaries
+    if (t == 0 && c0.x >= 0 && conn_sign(c0.y) > 0)
+      v += kp.bt.mi[p][0] * __ldg(mk + C::MET_NV + ((dir * 2 + 0) * NL + line) * D + d);
+    if (t == P && c1.x >= 0 && conn_sign(c1.y) > 0)
+      v += kp.bt.mi[p][1] * __ldg(mk + C::MET_NV + ((dir * 2 + 1) * NL + line) * D + d);
+    return v;
+  };
   for (int w = threadIdx.x; w < NLT * D; w += blockDim.x) {
     const int tl = w / D, d = w - tl * D;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
     const bool full = TileLines<C>::full(dir);
-    double nvd[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) nvd[q] = __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
     const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
     const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    const bool nbr0 = c0.x >= 0 && conn_sign(c0.y) <= 0;
+    const bool nbr1 = c1.x >= 0 && conn_sign(c1.y) <= 0;
     const double n0 = __ldg(mk + C::MET_NV + ((dir * 2 + 0) * NL + line) * D + d);
     const double n1 = __ldg(mk + C::MET_NV + ((dir * 2 + 1) * NL + line) * D + d);
-    // u_hat = own trace where S = +1, neighbour where S = -1, g_D on boundaries
-    const bool own0 = c0.x >= 0 && conn_sign(c0.y) > 0, nbr0 = c0.x >= 0 && conn_sign(c0.y) <= 0;
-    const bool own1 = c1.x >= 0 && conn_sign(c1.y) > 0, nbr1 = c1.x >= 0 && conn_sign(c1.y) <= 0;
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
       const int r = nd - s * NT;
       const double sc = __ldg(mk + C::MET_NV + C::MET_NE + nd);
+      double* rowp = Kt + static_cast<size_t>(r) * D + d;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
-        double v = 0.0;
+        if (t == i && dir != 0) continue;
+        double v = coef(dir, line, i, t, d, c0, c1);
+        if (t == i) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * nvd[q];
-        if (t == 0 && own0) v += kp.bt.mi[i][0] * n0;
-        if (t == P && own1) v += kp.bt.mi[i][1] * n1;
-        if (t == i && dir > 0) sdg[((dir - 1) * NT + r) * D + d] = sc * v;
-        else stg[(inel_slot<C>(dir, i, t) * D + d) * NT + r] = sc * v;
+          for (int d2 = 1; d2 < D; ++d2) {
+            int l2, p2;
+            line_of<C>(d2, nd, l2, p2);
+            const int2 x0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + d2) * 2 + 0]);
+            const int2 x1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + d2) * 2 + 1]);
+            v += coef(d2, l2, p2, p2, d, x0, x1);
+          }
+        }
+        rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * D] = sc * v;
       }
-      if (nbr0) stg[((C::D * P + 1 + dir) * D + d) * NT + r] = sc * (kp.bt.mi[i][0] * n0);
-      if (nbr1) stg[((C::D * P + 1 + dir) * D + d) * NT + r] = sc * (kp.bt.mi[i][1] * n1);
+      double nbv = 0.0;
+      if (nbr0) nbv = sc * (kp.bt.mi[i][0] * n0);
+      if (nbr1) nbv = sc * (kp.bt.mi[i][1] * n1);
+      rowp[static_cast<size_t>(C::D * P + 1 + dir) * NT * D] = nbv;
     };
     if (full) {
 #pragma unroll
@@ -1583,17 +1613,6 @@ __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __rest
       body(TileLines<C>::prow(dir, s));
     }
   }
-  __syncthreads();
-  for (int w = threadIdx.x; w < NT * D; w += blockDim.x) {
-    const int r = w / D, d = w - r * D;
-    const int x0 = r % NP;
-    double v = stg[(x0 * D + d) * NT + r];
-#pragma unroll
-    for (int dd = 1; dd < C::D; ++dd) v = v + sdg[((dd - 1) * NT + r) * D + d];
-    stg[(x0 * D + d) * NT + r] = v;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < ST; i += blockDim.x) K21[static_cast<size_t>(T) * ST + i] = stg[i];
 }
 
 // ===================================================================== SpMV
@@ -1639,17 +1658,17 @@ __device__ __forceinline__ int64_t slot_col(const KParams<C>& kp, int k, size_t 
 }
 
 // y = K11 x  (SPLIT: y = v - adt (K11 v + K12 w), the split matvec).
-// One thread per (row, output component a): a warp streams 32 consecutive
-// rows of one block row a, so every value load is contiguous; the x entries
-// of a column are shared by the m threads of a row through L1.
+// One thread per (row, output component a); a warp covers 32 consecutive
+// rows of one a.  Block row a of a slot is m contiguous doubles (16-byte
+// loads when m is even); the x entries of a column are shared by the m
+// threads of a row through L1.
 template <class C, bool SPLIT>
 __global__ void __launch_bounds__(128)
 k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __restrict__ V12,
          const double* __restrict__ x, const double* __restrict__ w, double adt, double* __restrict__ y) {
-  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD;
+  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD, B11 = C::B11;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
-  // thread -> (row group of 32 rows, a, lane)
   const int lane = static_cast<int>(gid & 31);
   const int64_t wg = gid >> 5;
   const int a = static_cast<int>(wg % M);
@@ -1662,24 +1681,37 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
   const int nd = s * NT + r;
   const size_t e = __ldg(kp.order + k);
   double acc = 0.0;
-  const double* vb = V11 + T * (C::NS11 * C::B11 * NT) + a * M * NT + r;
+  const double* vb = V11 + T * C::NS11 * NT * B11 + (static_cast<size_t>(a) * NT + r) * M;
 #pragma unroll
   for (int slot = 0; slot < C::NS11; ++slot) {
     const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 0);
     if (col < 0) continue;
+    const double* vp = vb + static_cast<size_t>(slot) * NT * B11;
+    const double* xp = x + col * M;
+    if (M % 2 == 0) {
 #pragma unroll
-    for (int b = 0; b < M; ++b) acc += __ldg(vb + (slot * C::B11 + b) * NT) * __ldg(x + col * M + b);
+      for (int b = 0; b < M; b += 2) {
+        const double2 kv = __ldg(reinterpret_cast<const double2*>(vp + b));
+        const double2 xv = __ldg(reinterpret_cast<const double2*>(xp + b));
+        acc += kv.x * xv.x;
+        acc += kv.y * xv.y;
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < M; ++b) acc += __ldg(vp + b) * __ldg(xp + b);
+    }
   }
   if (SPLIT && C::SECOND) {
     constexpr int A0 = C::PH == PH_NS ? 1 : 0;
     if (a >= A0) {
-      const double* vq = V12 + T * (C::NS12 * C::B12 * NT) + (a - A0) * MD * NT + r;
+      const double* vq = V12 + T * C::NS12 * NT * C::B12 + (static_cast<size_t>(a - A0) * NT + r) * MD;
 #pragma unroll
       for (int slot = 0; slot < C::NS12; ++slot) {
         const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
         if (col < 0) continue;
+        const double* vp = vq + static_cast<size_t>(slot) * NT * C::B12;
 #pragma unroll
-        for (int b = 0; b < MD; ++b) acc += __ldg(vq + (slot * C::B12 + b) * NT) * __ldg(w + col * MD + b);
+        for (int b = 0; b < MD; ++b) acc += __ldg(vp + b) * __ldg(w + col * MD + b);
       }
     }
   }
@@ -1688,44 +1720,43 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
   else y[yo] = acc;
 }
 
-// y = K12 w  (w: m*D per node)
+// y = K12 w  (w: m*D per node); one thread per (row, stored row a')
 template <class C>
 __global__ void __launch_bounds__(128)
 k_spmv12(const KParams<C> kp, const double* __restrict__ V12, const double* __restrict__ w,
          double* __restrict__ y) {
-  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD;
+  constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD, R12 = C::R12;
   constexpr int A0 = C::PH == PH_NS ? 1 : 0;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
+  const int lane = static_cast<int>(gid & 31);
+  const int64_t wg = gid >> 5;
+  const int a = static_cast<int>(wg % M);
+  const int64_t row = (wg / M) * 32 + lane;
   if (row >= nrows) return;
   const int64_t T = row / NT;
   const int r = static_cast<int>(row - T * NT);
   const int k = static_cast<int>(T / C::TPE);
   const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
   const int nd = s * NT + r;
-  const size_t e = kp.order[k];
-  double acc[M];
+  const size_t e = __ldg(kp.order + k);
+  double acc = 0.0;
+  if (a >= A0) {
+    const double* vq = V12 + T * C::NS12 * NT * C::B12 + (static_cast<size_t>(a - A0) * NT + r) * MD;
 #pragma unroll
-  for (int a = 0; a < M; ++a) acc[a] = 0.0;
-  const double* vq = V12 + T * (C::NS12 * C::B12 * NT) + r;
+    for (int slot = 0; slot < C::NS12; ++slot) {
+      const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
+      if (col < 0) continue;
+      const double* vp = vq + static_cast<size_t>(slot) * NT * C::B12;
 #pragma unroll
-  for (int slot = 0; slot < C::NS12; ++slot) {
-    const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 1);
-    if (col < 0) continue;
-    double wv[MD];
-#pragma unroll
-    for (int b = 0; b < MD; ++b) wv[b] = __ldg(w + col * MD + b);
-#pragma unroll
-    for (int a = 0; a < C::R12; ++a)
-#pragma unroll
-      for (int b = 0; b < MD; ++b) acc[a + A0] += __ldg(vq + ((slot * C::B12) + a * MD + b) * NT) * wv[b];
+      for (int b = 0; b < MD; ++b) acc += __ldg(vp + b) * __ldg(w + col * MD + b);
+    }
   }
-  const size_t yo = (e * NPE + nd) * M;
-#pragma unroll
-  for (int a = 0; a < M; ++a) y[yo + a] = acc[a];
+  (void)R12;
+  y[(e * NPE + nd) * M + a] = acc;
 }
 
-// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c])
+// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c]); one thread per row
 template <class C>
 __global__ void __launch_bounds__(128)
 k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __restrict__ v,
@@ -1739,20 +1770,20 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
   const int k = static_cast<int>(T / C::TPE);
   const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
   const int nd = s * NT + r;
-  const size_t e = kp.order[k];
+  const size_t e = __ldg(kp.order + k);
   double acc[M][D];
 #pragma unroll
   for (int c = 0; c < M; ++c)
 #pragma unroll
     for (int d = 0; d < D; ++d) acc[c][d] = 0.0;
-  const double* vb = V21 + T * (C::NS12 * D * NT) + r;
+  const double* vb = V21 + (T * C::NS12 * NT + r) * D;
 #pragma unroll
   for (int slot = 0; slot < C::NS12; ++slot) {
     const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 2);
     if (col < 0) continue;
     double kv[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + (slot * D + d) * NT);
+    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + static_cast<size_t>(slot) * NT * D + d);
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       const double xv = __ldg(v + col * M + c);

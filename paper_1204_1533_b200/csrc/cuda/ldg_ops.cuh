@@ -34,6 +34,7 @@ struct Ops {
   int D, P, PH, RI, M, NP, NQ, NPE, NL, MD, NS11, NS12, B11, B12, R12, NT, TPE, METP, MET_NV, MET_NE;
   size_t jac_smem;
   size_t endjac_per_elem;  // doubles of endpoint-Jacobian scratch per element
+  size_t (*scratch_elems)(int E);  // doubles of scratch for E elements (chunked)
   cudaError_t (*residual)(const DevCtx&, const double* U, const double* Q, double* R);
   cudaError_t (*gradient)(const DevCtx&, const double* U, double* Q);
   cudaError_t (*jacobian)(const DevCtx&, const double* U, const double* Q, double* SE, double* K11,
@@ -142,6 +143,14 @@ struct Launch {
   }
   static constexpr size_t jac_smem() { return sizeof(double) * JacSmem<C>::TOTAL; }
   static constexpr int EJ_SEEDS = C::M;  // seeds per k_endjac thread (primal shared)
+  // Elements per assembly chunk: the endpoint-Jacobian scratch of one chunk
+  // stays within ~48 MB, so it is produced and consumed while L2-resident.
+  static int chunk_elems(int E) {
+    const long long per = static_cast<long long>(EndJac<C>::PER_ELEM) * 8;
+    long long n = (48LL << 20) / (per > 0 ? per : 1);
+    if (n < 1024) n = 1024;
+    return static_cast<int>(n < E ? n : E);
+  }
   static cudaError_t jacobian(const DevCtx& d, const double* U, const double* Q, double* SE, double* K11,
                               double* K12) {
     const size_t smem = jac_smem();
@@ -154,37 +163,44 @@ struct Launch {
     constexpr int NSP = (C::M + EJ_SEEDS - 1) / EJ_SEEDS, NSQ = (C::MD + EJ_SEEDS - 1) / EJ_SEEDS;
     constexpr int IPS = 2 * NSP + (C::SECOND ? NSQ : 0);
     static const bool one_seed = std::getenv("LDG_ENDJAC_SEEDS1") != nullptr;  // tuning switch
-    if (one_seed) {
-      constexpr int NQ1 = C::SECOND ? C::MD : 0;
-      const long long items = static_cast<long long>(d.E) * 2 * C::D * C::NL * (2 * C::M + NQ1);
-      k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, 0, d.E);
-    } else {
-      const long long items = static_cast<long long>(d.E) * 2 * C::D * C::NL * IPS;
-      k_endjac<C, EJ_SEEDS><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, 0,
-                                                                                       d.E);
-    }
-    count(d);
     static const bool simple = std::getenv("LDG_JACOBIAN_SIMPLE") != nullptr;
-    if (JacP<C>::OK && !simple) {
-      const size_t psmem = sizeof(double) * JacP<C>::TOTAL;
-      static int grid_max = 0;
-      if (!grid_max) {
-        cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        int per_sm = 0, dev = 0, sms = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobian_p<C>, JacThreads<C>::value, psmem);
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid_max = (per_sm > 0 ? per_sm : 1) * sms;
-      }
-      const int grid = d.E < grid_max ? d.E : grid_max;
-      k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12);
-    } else {
-      k_jacobian<C><<<d.E * C::TPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11, K12);
+    static int grid_max = 0;
+    const size_t psmem = sizeof(double) * JacP<C>::TOTAL;
+    if (JacP<C>::OK && !grid_max) {
+      cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+      cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobian_p<C>, JacThreads<C>::value, psmem);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
     }
-    count(d);
+    const int chunk = chunk_elems(d.E);
+    for (int kb = 0; kb < d.E; kb += chunk) {
+      const int ke = kb + chunk < d.E ? kb + chunk : d.E;
+      if (one_seed) {
+        constexpr int NQ1 = C::SECOND ? C::MD : 0;
+        const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * (2 * C::M + NQ1);
+        k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, kb, ke);
+      } else {
+        const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * IPS;
+        k_endjac<C, EJ_SEEDS><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE,
+                                                                                         kb, ke);
+      }
+      count(d);
+      if (JacP<C>::OK && !simple) {
+        const int n = ke - kb;
+        const int grid = n < grid_max ? n : grid_max;
+        k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
+      } else {
+        k_jacobian<C><<<(ke - kb) * C::TPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11,
+                                                                                    K12, kb);
+      }
+      count(d);
+    }
     return cudaGetLastError();
   }
+  static size_t scratch_elems(int E) { return static_cast<size_t>(chunk_elems(E)) * EndJac<C>::PER_ELEM; }
   static cudaError_t k21(const DevCtx& d, double* K21) {
     if (!C::SECOND) return cudaSuccess;
     k_k21<C><<<d.E * C::TPE, 128, 0, d.stream>>>(params(d), K21);
@@ -208,7 +224,7 @@ struct Launch {
   }
   static cudaError_t spmv12(const DevCtx& d, const double* V12, const double* w, double* y) {
     if (!C::SECOND) return cudaSuccess;
-    k_spmv12<C><<<rgrid(d), 128, 0, d.stream>>>(params(d), V12, w, y);
+    k_spmv12<C><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V12, w, y);
     count(d);
     return cudaGetLastError();
   }
@@ -228,7 +244,7 @@ struct Launch {
   static const Ops* table() {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
-                            C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, residual, gradient, jacobian, k21,
+                            C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, residual, gradient, jacobian, k21,
                             spmv11, spmv12, spmv21, split};
     return &ops;
   }
