@@ -42,6 +42,18 @@ struct Cfg {
   static constexpr int TD = (D == 3 && PH == PH_NS && P >= 4) ? 1 : 2;
   static constexpr int NT = TD == 1 ? NP : NP * NP;
   static constexpr int TPE = NPE / NT;                    // tiles per element
+  // Assembly work unit of one CTA (independent of the store tile): the whole
+  // element when its flux-Jacobian working set fits shared memory, else one
+  // slab (x2 = const) or one dir-0 line of rows (3-D only).
+  static constexpr long long wu_bytes(int nlt) {
+    return 8LL * (NPE * M + (PH != PH_EULER ? NPE * M * D : 0) + nlt * NQ * M * M * ((PH == PH_NS) ? 2 : 1) +
+                  (PH != PH_EULER ? nlt * NQ * M * M * D : 0) +
+                  nlt * 2 * (2 * M * M + (PH != PH_EULER ? M * M * D : 0)));
+  }
+  static constexpr int WU = D == 2 ? 0
+                            : (wu_bytes(D * NL) <= 100 * 1024 ? 0
+                                                              : (wu_bytes(2 * NP + NP * NP) <= 200 * 1024 ? 1 : 2));
+  static constexpr int UPE = WU == 0 ? 1 : (WU == 1 ? NP : NP * NP);  // work units per element
   static constexpr int NS11 = D * P + 1 + 2 * D;          // K11 node-columns per row
   static constexpr int NS12 = D * P + 1 + D;              // K12 / K21 node-columns per row
   static constexpr int B11 = M * M;

@@ -950,13 +950,14 @@ k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict
 // prow(): position on the line of the tile's single row for non-full lines.
 template <class C>
 struct TileLines {
-  static constexpr int NLT = C::D == 2 ? C::D * C::NL : (C::TD == 2 ? 2 * C::NP + C::NP * C::NP : 1 + 2 * C::NP);
+  // work unit: 0 = element (all D*NL lines, full), 1 = slab, 2 = dir-0 line of rows
+  static constexpr int NLT = C::WU == 0 ? C::D * C::NL : (C::WU == 1 ? 2 * C::NP + C::NP * C::NP : 1 + 2 * C::NP);
   __device__ static __forceinline__ void get(int tl, int s, int& dir, int& line) {
     constexpr int NP = C::NP;
-    if (C::D == 2) {
+    if (C::WU == 0) {
       dir = tl / C::NL;
       line = tl - dir * C::NL;
-    } else if (C::TD == 2) {
+    } else if (C::WU == 1) {
       if (tl < 2 * NP) {
         dir = tl / NP;
         line = (tl - dir * NP) + NP * s;
@@ -979,10 +980,10 @@ struct TileLines {
     }
   }
   __device__ static __forceinline__ bool full(int dir) {
-    return C::D == 2 || (C::TD == 2 ? dir < 2 : dir == 0);
+    return C::WU == 0 || (C::WU == 1 ? dir < 2 : dir == 0);
   }
   __device__ static __forceinline__ int prow(int dir, int s) {
-    if (C::TD == 2) return s;
+    if (C::WU == 1) return s;
     return dir == 1 ? s % C::NP : s / C::NP;
   }
 };
@@ -1171,8 +1172,9 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 // staging tile, no zero fill).
 template <class C>
 struct JacThreads {
-  static constexpr int value = 128;
-  static constexpr int min_blocks = 4;
+  static constexpr bool big = C::D == 3 && C::WU == 0;  // 3-D element work unit: many lines
+  static constexpr int value = big ? 384 : 128;
+  static constexpr int min_blocks = big ? 1 : 4;
 };
 
 template <class C>
@@ -1194,8 +1196,8 @@ struct JacSmem {
 template <class C>
 __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
   constexpr int NP = C::NP;
-  if (C::D == 2) return dir * C::NL + line;
-  if (C::TD == 2) return dir < 2 ? dir * NP + line % NP : 2 * NP + line;
+  if (C::WU == 0) return dir * C::NL + line;
+  if (C::WU == 1) return dir < 2 ? dir * NP + line % NP : 2 * NP + line;
   return dir == 0 ? 0 : (dir == 1 ? 1 + line % NP : 1 + NP + line % NP);
 }
 
@@ -1314,9 +1316,9 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
-      const int r = nd - s * NT;
+      const int r = nd % NT;
       const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-      double* rowp = K11t + (static_cast<size_t>(ab / M) * NT + r) * M + ab % M;
+      double* rowp = K11t + static_cast<size_t>(nd / NT) * SM::ST11 + (static_cast<size_t>(ab / M) * NT + r) * M + ab % M;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         if (t == i && dir != 0) continue;  // the dir-0 thread owns the self block
@@ -1376,9 +1378,9 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
-      const int r = nd - s * NT;
+      const int r = nd % NT;
       const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-      double* rowp = K12t + (static_cast<size_t>(ab / MD) * NT + r) * MD + ab % MD;
+      double* rowp = K12t + static_cast<size_t>(nd / NT) * SM::ST12 + (static_cast<size_t>(ab / MD) * NT + r) * MD + ab % MD;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         if (t == i && dir != 0) continue;
@@ -1445,8 +1447,8 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
   double* stab = sBq + SM::BQ;
-  const int T = blockIdx.x + k_begin * C::TPE;  // tile id
-  const int k = T / C::TPE, s = T - k * C::TPE;
+  const int W = blockIdx.x + k_begin * C::UPE;  // work unit id
+  const int k = W / C::UPE, s = W - k * C::UPE;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const size_t e = kp.order[k];
   const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
@@ -1467,8 +1469,9 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   fill_tab<C>(kp, stab, tid, nthr);
   __syncthreads();
   auto eidx = [](int tl, int, int, int side) { return tl * 2 + side; };
-  jac_tile<C>(kp, k, s, e, su, sq, mk, sE, eidx, sA, sAv, sBq, stab, K11 + static_cast<size_t>(T) * SM::ST11,
-              C::SECOND ? K12 + static_cast<size_t>(T) * SM::ST12 : nullptr, tid, nthr);
+  jac_tile<C>(kp, k, s, e, su, sq, mk, sE, eidx, sA, sAv, sBq, stab,
+              K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
+              C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
 }
 
 // Persistent, TMA-prefetching Jacobian assembly (2-D: one tile = one element):
@@ -1484,8 +1487,8 @@ struct JacP {
   static constexpr int BUF = U + Q + MET + SE;
   using SM = JacSmem<C>;
   static constexpr int TOTAL = 2 + 2 * BUF + SM::WORK;
-  static constexpr bool OK = C::D == 2 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
-                             (EndJac<C>::PER_ELEM % 2 == 0);
+  static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
+                             (EndJac<C>::PER_ELEM % 2 == 0) && 8LL * TOTAL <= 200 * 1024;
 };
 
 template <class C>
@@ -1540,8 +1543,8 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     mbar_wait(&bar[cur], (it >> 1) & 1);
     const size_t e = kp.order[k];
     jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bSE(cur), eidx, sA, sAv, sBq, stab,
-                K11 + static_cast<size_t>(k) * SM::ST11, C::SECOND ? K12 + static_cast<size_t>(k) * SM::ST12 : nullptr,
-                tid, nthr);
+                K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
+                C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
     __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done
     if (tid == 0 && k + 2 * G < k_end) issue(k + 2 * G, cur);
   }
@@ -1553,10 +1556,10 @@ __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __rest
   constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, D = C::D, NT = C::NT, P = C::P;
   constexpr int NLT = TileLines<C>::NLT;
   constexpr int ST = C::NS12 * D * NT;
-  const int T = blockIdx.x;
-  const int k = T / C::TPE, s = T - k * C::TPE;
+  const int W = blockIdx.x;  // work unit
+  const int k = W / C::UPE, s = W - k * C::UPE;
   const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-  double* Kt = K21 + static_cast<size_t>(T) * ST;
+  double* Kt = K21 + static_cast<size_t>(k) * C::TPE * ST;
   auto coef = [&](int dir, int line, int p, int t, int d, int2 c0, int2 c1) {
     // line block entry (row position p, column position t) of direction d
     double v = 0.0;
@@ -1582,9 +1585,9 @@ __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __rest
     const double n1 = __ldg(mk + C::MET_NV + ((dir * 2 + 1) * NL + line) * D + d);
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
-      const int r = nd - s * NT;
+      const int r = nd % NT;
       const double sc = __ldg(mk + C::MET_NV + C::MET_NE + nd);
-      double* rowp = Kt + static_cast<size_t>(r) * D + d;
+      double* rowp = Kt + static_cast<size_t>(nd / NT) * ST + static_cast<size_t>(r) * D + d;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         if (t == i && dir != 0) continue;

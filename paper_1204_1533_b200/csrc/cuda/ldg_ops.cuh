@@ -193,7 +193,7 @@ struct Launch {
         const int grid = n < grid_max ? n : grid_max;
         k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
       } else {
-        k_jacobian<C><<<(ke - kb) * C::TPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11,
+        k_jacobian<C><<<(ke - kb) * C::UPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11,
                                                                                     K12, kb);
       }
       count(d);
@@ -203,7 +203,7 @@ struct Launch {
   static size_t scratch_elems(int E) { return static_cast<size_t>(chunk_elems(E)) * EndJac<C>::PER_ELEM; }
   static cudaError_t k21(const DevCtx& d, double* K21) {
     if (!C::SECOND) return cudaSuccess;
-    k_k21<C><<<d.E * C::TPE, 128, 0, d.stream>>>(params(d), K21);
+    k_k21<C><<<d.E * C::UPE, 128, 0, d.stream>>>(params(d), K21);
     count(d);
     return cudaGetLastError();
   }
