@@ -1206,7 +1206,7 @@ __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
 // indexed by eidx(tl, dir, line, side); stab = {cc[p][p][q], mi[p][s]}.
 template <class C, class EIdx>
 __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, const int s, const size_t e,
-                                         const double* su, const double* sq, const double* mk,
+                                         const double* su, const double* sq, const double* mk, const int2* scon,
                                          const double* sE, EIdx eidx, double* sA, double* sAv, double* sBq,
                                          const double* stab, double* __restrict__ K11t,
                                          double* __restrict__ K12t, const int tid, const int nthr) {
@@ -1312,8 +1312,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     const double* e1 = sE + eidx(tl, dir, line, 1) * EJ::SLOT;
     const double ein0 = e0[ab], ein1 = e1[ab];
     const double eo0 = e0[B11 + ab], eo1 = e1[B11 + ab];
-    const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
-    const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    const int2 c0 = scon[dir * 2 + 0];
+    const int2 c1 = scon[dir * 2 + 1];
     auto body = [&](const int i) {
       const int nd = node_on_line<C>(dir, line, i);
       const int r = nd % NT;
@@ -1371,8 +1371,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     for (int q = 0; q < NQ; ++q) bv[q] = sBq[(tl * NQ + q) * M * MD + a * MD + b];
     const double eq0 = sE[eidx(tl, dir, line, 0) * EJ::SLOT + 2 * B11 + a * MD + b];
     const double eq1 = sE[eidx(tl, dir, line, 1) * EJ::SLOT + 2 * B11 + a * MD + b];
-    const int2 c0 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 0]);
-    const int2 c1 = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + 1]);
+    const int2 c0 = scon[dir * 2 + 0];
+    const int2 c1 = scon[dir * 2 + 1];
     // own-end dependence when boundary or S <= 0; neighbour slot otherwise
     const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
     const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
@@ -1399,7 +1399,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
             for (int q = 0; q < NQ; ++q) v += sccd[p2 * NQ + q] * sBq[(tl2 * NQ + q) * M * MD + a * MD + b];
             if (p2 == 0 || p2 == P) {
               const int sd2 = p2 == 0 ? 0 : 1;
-              const int2 cx = __ldg(&kp.conn[(static_cast<size_t>(k) * D + d2) * 2 + sd2]);
+              const int2 cx = scon[d2 * 2 + sd2];
               if (cx.x < 0 || conn_sign(cx.y) <= 0)
                 v += smi[p2 * 2 + sd2] * sE[eidx(tl2, d2, l2, sd2) * EJ::SLOT + 2 * B11 + a * MD + b];
             }
@@ -1467,9 +1467,11 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
     }
   }
   fill_tab<C>(kp, stab, tid, nthr);
+  __shared__ int2 sconn[2 * C::D];
+  if (tid < 2 * C::D) sconn[tid] = __ldg(&kp.conn[static_cast<size_t>(k) * C::D * 2 + tid]);
   __syncthreads();
   auto eidx = [](int tl, int, int, int side) { return tl * 2 + side; };
-  jac_tile<C>(kp, k, s, e, su, sq, mk, sE, eidx, sA, sAv, sBq, stab,
+  jac_tile<C>(kp, k, s, e, su, sq, mk, sconn, sE, eidx, sA, sAv, sBq, stab,
               K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
               C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
 }
@@ -1483,12 +1485,17 @@ struct JacP {
   static constexpr int U = ev(C::NPE * C::M);
   static constexpr int Q = C::SECOND ? ev(C::NPE * C::MD) : 0;
   static constexpr int MET = C::METP;
+  static constexpr int CONN = ev(2 * C::D);  // int2 entries (8 B each)
   static constexpr int SE = ev(EndJac<C>::PER_ELEM);
-  static constexpr int BUF = U + Q + MET + SE;
+  static constexpr int BUF = U + Q + MET + CONN + SE;
   using SM = JacSmem<C>;
-  static constexpr int TOTAL = 2 + 2 * BUF + SM::WORK;
+  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK); }
+  // prefetch ring depth: 3 for the one-CTA-per-SM 3-D element units (when it
+  // fits), 2 where several CTAs share an SM
+  static constexpr int NBUF = (JacThreads<C>::big && bytes(3) <= 200 * 1024) ? 3 : 2;
+  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK;  // 4 doubles hold up to 3 mbarriers
   static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
-                             (EndJac<C>::PER_ELEM % 2 == 0) && 8LL * TOTAL <= 200 * 1024;
+                             (EndJac<C>::PER_ELEM % 2 == 0) && bytes(2) <= 200 * 1024;
 };
 
 template <class C>
@@ -1496,14 +1503,14 @@ __global__ void __launch_bounds__(JacThreads<C>::value, JacThreads<C>::min_block
 k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
              const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12, int k_begin,
              int k_end) {
-  constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD;
+  constexpr int NPE = C::NPE, NL = C::NL, M = C::M, MD = C::MD, NB = JacP<C>::NBUF;
   using JP = JacP<C>;
   using SM = JacSmem<C>;
   using EJ = EndJac<C>;
   extern __shared__ __align__(16) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  double* const bufs = smem + 2;
-  double* const work = bufs + 2 * JP::BUF;
+  double* const bufs = smem + 4;
+  double* const work = bufs + NB * JP::BUF;
   double* sA = work;
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
@@ -1514,39 +1521,39 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   auto bU = [&](int bi) { return bufs + bi * JP::BUF; };
   auto bQ = [&](int bi) { return bufs + bi * JP::BUF + JP::U; };
   auto bMET = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q; };
-  auto bSE = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET; };
+  auto bCONN = [&](int bi) { return reinterpret_cast<int2*>(bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET); };
+  auto bSE = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET + JP::CONN; };
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
     mbar_fence_init();
   }
   fill_tab<C>(kp, stab, tid, nthr);
   __syncthreads();
   auto issue = [&](int k, int bi) {
     const size_t e = __ldg(kp.order + k);
-    unsigned bytes = NPE * M * 8 + C::METP * 8 + EJ::PER_ELEM * 8;
+    unsigned bytes = NPE * M * 8 + C::METP * 8 + 2 * C::D * 8 + EJ::PER_ELEM * 8;
     if (C::SECOND) bytes += NPE * MD * 8;
     mbar_expect_tx(&bar[bi], bytes);
     tma_load_1d(bU(bi), U + e * (NPE * M), NPE * M * 8, &bar[bi]);
     if (C::SECOND) tma_load_1d(bQ(bi), Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
     tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k) * C::METP, C::METP * 8, &bar[bi]);
+    tma_load_1d(bCONN(bi), kp.conn + static_cast<size_t>(k) * C::D * 2, 2 * C::D * 8, &bar[bi]);
     tma_load_1d(bSE(bi), SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
   };
   const int k0 = k_begin + blockIdx.x;
-  if (tid == 0) {
-    issue(k0, 0);
-    if (k0 + G < k_end) issue(k0 + G, 1);
-  }
+  if (tid == 0)
+    for (int b = 0; b < NB; ++b)
+      if (k0 + b * G < k_end) issue(k0 + b * G, b);
   auto eidx = [](int, int dir, int line, int side) { return (dir * 2 + side) * NL + line; };
   for (int k = k0, it = 0; k < k_end; k += G, ++it) {
-    const int cur = it & 1;
-    mbar_wait(&bar[cur], (it >> 1) & 1);
+    const int cur = it % NB;
+    mbar_wait(&bar[cur], (it / NB) & 1);
     const size_t e = kp.order[k];
-    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bSE(cur), eidx, sA, sAv, sBq, stab,
+    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bCONN(cur), bSE(cur), eidx, sA, sAv, sBq, stab,
                 K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
                 C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
     __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done
-    if (tid == 0 && k + 2 * G < k_end) issue(k + 2 * G, cur);
+    if (tid == 0 && k + NB * G < k_end) issue(k + NB * G, cur);
   }
 }
 
