@@ -35,6 +35,7 @@ struct KParams {
   const double* source;  // reference numbering, may be null
   DevError* err;
   int E;                 // elements
+  int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2 stores
 };
 
 // ---------------------------------------------------------------- helpers
@@ -1173,7 +1174,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 template <class C>
 struct JacThreads {
   static constexpr bool big = C::D == 3 && C::WU == 0;  // 3-D element work unit: many lines
-  static constexpr int value = big ? 384 : 128;
+  static constexpr int value = big ? 640 : 128;
   static constexpr int min_blocks = big ? 1 : 4;
 };
 
@@ -1186,7 +1187,8 @@ struct JacSmem {
   static constexpr int AV = C::VIS_U ? NLT * C::NQ * C::B11 : 0;    // dFvis/du . nvec
   static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
   static constexpr int SEC = NLT * 2 * EndJac<C>::SLOT;       // endpoint flux Jacobians (tile lines)
-  static constexpr int TAB = (C::NP * C::NQ + 2 * C::NP + 1) / 2 * 2;  // cc diagonal + M^-1 columns
+  static constexpr int TABD = (C::NP * C::NQ + 2 * C::NP + 1) / 2 * 2;  // cc diagonal + M^-1 columns
+  static constexpr int TAB = TABD + ((C::D == 3 && C::WU == 0) ? C::NP * C::NP * C::NQ : 0);  // + full cc
   static constexpr int ST11 = C::NS11 * C::B11 * C::NT;       // store doubles per tile
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
   static constexpr int WORK = A + AV + BQ + TAB;
@@ -1199,6 +1201,97 @@ __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
   if (C::WU == 0) return dir * C::NL + line;
   if (C::WU == 1) return dir < 2 ? dir * NP + line % NP : 2 * NP + line;
   return dir == 0 ? 0 : (dir == 1 ? 1 + line % NP : 1 + NP + line % NP);
+}
+
+// 3-D element work unit, output-major K11 stores: one thread per
+// (slab s, slot, row r, column b) computes the m entries (a = 0..m-1) of that
+// block column, so the lanes of a warp run over consecutive (r, b) and every
+// store instruction writes 256 contiguous bytes of one block row a.
+// Line coefficients cc[i][t][q] come from shared memory (lane-dependent i).
+template <class C, class EIdx>
+__device__ __forceinline__ void jac_k11_outmajor(const KParams<C>& kp, const double* mk, const int2* scon,
+                                                 const double* sE, EIdx eidx, const double* sA, const double* sAv,
+                                                 const double* scc, const double* smi, double* __restrict__ K11e,
+                                                 const int tid, const int nthr) {
+  constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, M = C::M, NT = C::NT, P = C::P, B11 = C::B11,
+                NS = C::NS11, TPE = C::TPE;
+  using EJ = EndJac<C>;
+  constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
+  constexpr int ST = JacSmem<C>::ST11;
+  constexpr int RB = NT * M;  // (row, b) entries per (slab, slot)
+  auto aval = [&](int tl, int q, int ab) {
+    return (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
+  };
+  for (int w = tid; w < TPE * NS * RB; w += nthr) {
+    const int rb = w % RB, ss = w / RB;
+    const int slot = ss % NS, s = ss / NS;
+    const int r = rb / M, b = rb - r * M;
+    const int x0 = r % NP, x1 = r / NP, x2 = s;
+    const int nd = r + NT * s;
+    int dir, t, side = -1;
+    if (slot < NP) {
+      dir = 0;
+      t = slot;
+    } else if (slot < NP + 2 * P) {
+      const int z = slot - NP;
+      dir = 1 + z / P;
+      const int tp = z % P, pos = dir == 1 ? x1 : x2;
+      t = tp + (tp >= pos ? 1 : 0);
+    } else {
+      const int z = slot - (3 * P + 1);
+      dir = z >> 1;
+      side = z & 1;
+      t = -1;
+    }
+    const int line = dir == 0 ? x1 + NP * x2 : (dir == 1 ? x0 + NP * x2 : x0 + NP * x1);
+    const int i = dir == 0 ? x0 : (dir == 1 ? x1 : x2);
+    const int tl = dir * NL + line;
+    const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+    double v[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) v[a] = 0.0;
+    if (side >= 0) {
+      const int2 cn = scon[dir * 2 + side];
+      if (cn.x >= 0) {
+        const double mi = smi[i * 2 + side];
+        const double* eo = sE + eidx(tl, dir, line, side) * EJ::SLOT + B11;
+#pragma unroll
+        for (int a = 0; a < M; ++a) v[a] = mi * eo[a * M + b];
+      }
+    } else {
+      // line block (i, t) of direction dir, plus, for the self block, the
+      // other two directions' lines through the node
+      auto add_line = [&](int d, int ln, int ii, int tt) {
+        const int tld = d * NL + ln;
+        if (VOL11) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const double cq = scc[(ii * NP + tt) * NQ + q];
+#pragma unroll
+            for (int a = 0; a < M; ++a) v[a] += cq * aval(tld, q, a * M + b);
+          }
+        }
+        if (tt == 0) {
+          const double* ei = sE + eidx(tld, d, ln, 0) * EJ::SLOT;
+#pragma unroll
+          for (int a = 0; a < M; ++a) v[a] += smi[ii * 2 + 0] * ei[a * M + b];
+        }
+        if (tt == P) {
+          const double* ei = sE + eidx(tld, d, ln, 1) * EJ::SLOT;
+#pragma unroll
+          for (int a = 0; a < M; ++a) v[a] += smi[ii * 2 + 1] * ei[a * M + b];
+        }
+      };
+      add_line(dir, line, i, t);
+      if (dir == 0 && t == x0) {
+        add_line(1, x0 + NP * x2, x1, x1);
+        add_line(2, x0 + NP * x1, x2, x2);
+      }
+    }
+    double* out = K11e + static_cast<size_t>(s) * ST + static_cast<size_t>(slot) * B11 * NT + rb;
+#pragma unroll
+    for (int a = 0; a < M; ++a) out[a * RB] = sc * v[a];
+  }
 }
 
 // One Jacobian row tile.  su/sq element state and gradient, mk the element's
@@ -1217,7 +1310,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   constexpr int NLT = SM::NLT;
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
-  if (C::HAS_INV) {
+  if (C::HAS_INV && !(kp.dbg & 1)) {
     for (int w = tid; w < NLT * NQ; w += nthr) {
       const int tl = w / NQ, q = w - tl * NQ;
       int dir, line;
@@ -1240,7 +1333,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     }
   }
   // ---- phase 1c (second-order): viscous flux derivatives, one seed per item
-  if (C::SECOND) {
+  if (C::SECOND && !(kp.dbg & 1)) {
     constexpr int NSU = C::VIS_U ? M : 0, NSEED = NSU + MD;
     for (int w = tid; w < NLT * NQ * NSEED; w += nthr) {
       const int sd = w % NSEED, tq = w / NSEED, tl = tq / NQ, q = tq - tl * NQ;
@@ -1294,13 +1387,17 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   }
   __syncthreads();
 
+  if (C::D == 3 && C::WU == 0) {
+    jac_k11_outmajor<C>(kp, mk, scon, sE, eidx, sA, sAv, stab + JacSmem<C>::TABD, stab + NP * NQ, K11t, tid,
+                        nthr);
+  }
   // ---- phase 2: K11 rows of every tile line, stored block row by block row
   const double* sccd = stab;            // cc[p][p][q]
   const double* smi = stab + NP * NQ;   // M^-1[p][0], M^-1[p][p]
   auto avq = [&](int tl, int q, int ab) {
     return (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
   };
-  for (int w = tid; w < NLT * B11; w += nthr) {
+  for (int w = ((kp.dbg & 2) || (C::D == 3 && C::WU == 0)) ? NLT * B11 : tid; w < NLT * B11; w += nthr) {
     const int tl = w / B11, ab = w - tl * B11;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
@@ -1429,6 +1526,8 @@ __device__ __forceinline__ void fill_tab(const KParams<C>& kp, double* stab, int
     stab[i] = kp.bt.cc[p][p][q];
   }
   for (int i = tid; i < 2 * NP; i += nthr) stab[NP * NQ + i] = (&kp.bt.mi[0][0])[i];
+  if (C::D == 3 && C::WU == 0)
+    for (int i = tid; i < NP * NP * NQ; i += nthr) stab[JacSmem<C>::TABD + i] = (&kp.bt.cc[0][0][0])[i];
 }
 
 template <class C>

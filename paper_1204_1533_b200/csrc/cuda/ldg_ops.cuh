@@ -66,6 +66,8 @@ struct Launch {
     kp.source = d.source;
     kp.err = d.err;
     kp.E = d.E;
+    static const int dbg = std::getenv("LDG_DEBUG_MASK") ? std::atoi(std::getenv("LDG_DEBUG_MASK")) : 0;
+    kp.dbg = dbg;
     return kp;
   }
   static void count(const DevCtx& d) {
