@@ -341,6 +341,69 @@ __device__ __forceinline__ void llf_fn(const T* uo, const T* ui, const double* n
   for (int c = 0; c < D + 2; ++c) fh[c] = 0.5 * (fl[c] + fr[c]) + hl * (ui[c] - uo[c]);
 }
 
+// Closed-form Jacobian of llf_fn: pass 0 -> dFh/du_in, pass 1 -> dFh/du_out
+// (row-major M x M).  The primal expressions (p, m.nb, lambda) are written
+// exactly as in llf_fn so the |.| and max branch choices are the same as the
+// dual-number evaluation's:
+//   dFh/du_X = 1/2 A(u_X, n) +- 1/2 |n| lam I + 1/2 |n| (u_in - u_out) (x) dlam/du_X,
+// dlam/du_X nonzero only for the side max() selected.
+template <int D>
+__device__ __forceinline__ void llf_jac(const double* uo, const double* ui, const double* n, double gamma,
+                                        const int pass, double* J, bool& ok) {
+  constexpr int M = D + 2;
+  double nn = n[0] * n[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+  nn = sqrt(nn);
+  const double inn = 1.0 / nn;
+  double nb[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) nb[d] = n[d] * inn;
+  double fl[M], fr[M];
+  const double pL = euler_fn<D>(ui, n, gamma, fl, ok);
+  const double pR = euler_fn<D>(uo, n, gamma, fr, ok);
+  double mL = ui[1] * nb[0], mR = uo[1] * nb[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) {
+    mL = mL + ui[1 + d] * nb[d];
+    mR = mR + uo[1 + d] * nb[d];
+  }
+  const double irL = 1.0 / ui[0], irR = 1.0 / uo[0];
+  const double unL = mL * irL, unR = mR * irR;
+  const double cL = sqrt(gamma * pL * irL), cR = sqrt(gamma * pR * irR);
+  const double lamL = dabs(unL) + cL, lamR = dabs(unR) + cR;
+  const bool pickL = lamL >= lamR;
+  const double lam = pickL ? lamL : lamR;
+  const double* u = pass == 0 ? ui : uo;
+  euler_jac_n<D>(u, n, gamma, J, ok);
+  const double hn = 0.5 * nn, dg = pass == 0 ? hn * lam : -hn * lam;
+#pragma unroll
+  for (int c = 0; c < M * M; ++c) J[c] *= 0.5;
+#pragma unroll
+  for (int c = 0; c < M; ++c) J[c * M + c] += dg;
+  if (pickL == (pass == 0)) {
+    // dlam/du of the selected side: s dun/du + dc/du
+    const double ir = pass == 0 ? irL : irR, un = pass == 0 ? unL : unR, c = pass == 0 ? cL : cR;
+    const double p = pass == 0 ? pL : pR;
+    const double s = un >= 0.0 ? 1.0 : -1.0;
+    double mom2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) mom2 += u[1 + d] * u[1 + d];
+    const double g1 = gamma - 1.0, k = 0.5 * gamma * ir / c;
+    double dl[M];
+    dl[0] = -s * un * ir + k * (0.5 * g1 * mom2 * ir * ir - p * ir);
+#pragma unroll
+    for (int d = 0; d < D; ++d) dl[1 + d] = s * nb[d] * ir - k * g1 * u[1 + d] * ir;
+    dl[D + 1] = k * g1;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const double w = hn * (ui[c] - uo[c]);
+#pragma unroll
+      for (int b = 0; b < M; ++b) J[c * M + b] += w * dl[b];
+    }
+  }
+}
+
 // Viscous normal flux F_vis(u, q).n.  Poisson: -q.n.  Navier-Stokes: minus
 // the +tau stress tensor dotted with n.  q layout q[c*D+d].
 template <int D, int PH, class T, class TQ, class TR>

@@ -1002,7 +1002,28 @@ struct EndJac {
   static constexpr int NPASS = C::SECOND ? 3 : 2;
   static constexpr int EQS = C::SECOND ? C::M * C::MD : 0;
   static constexpr int SLOT = 2 * C::B11 + EQS;               // doubles per line end
-  static constexpr int PER_ELEM = 2 * C::D * C::NL * SLOT;    // doubles per element
+  static constexpr int NLE = 2 * C::D * C::NL;                // line ends per element
+  // Scratch block of one element, entry-major: SE[off * LS + le], le =
+  // (dir*2 + side)*NL + line.  k_endjac lanes run over consecutive line ends
+  // (coalesced stores); LS is odd where that keeps PER_ELEM even (16-byte
+  // TMA rows) so shared-memory reads of neighbouring entries spread over banks.
+  static constexpr int LS = SLOT % 2 == 0 ? (NLE | 1) : NLE + (NLE & 1);
+  static constexpr int PER_ELEM = SLOT * LS;                  // doubles per element
+};
+
+// Line-end index functors for jac_tile: whole-element scratch block (k_endjac
+// layout, persistent kernel) and tile-line staging (k_jacobian).
+template <class C>
+struct SeFull {
+  static constexpr int LS = EndJac<C>::LS;
+  __device__ __forceinline__ int operator()(int, int dir, int line, int side) const {
+    return (dir * 2 + side) * C::NL + line;
+  }
+};
+template <class C>
+struct SeTile {
+  static constexpr int LS = (2 * TileLines<C>::NLT) | 1;
+  __device__ __forceinline__ int operator()(int tl, int, int, int side) const { return tl * 2 + side; }
 };
 
 template <class C, int SEEDS>
@@ -1018,10 +1039,11 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nitems = static_cast<int64_t>(k_end - k_begin) * 2 * D * NL * IPS;
   if (item >= nitems) return;
-  const int sub = static_cast<int>(item % IPS);
-  const int64_t gslot = item / IPS;
-  const int k = k_begin + static_cast<int>(gslot / (2 * D * NL));
-  const int gs = static_cast<int>(gslot - static_cast<int64_t>(k - k_begin) * (2 * D * NL));
+  constexpr int NLE = EJ::NLE, LS = EJ::LS;
+  const int gs = static_cast<int>(item % NLE);
+  const int64_t rest = item / NLE;
+  const int sub = static_cast<int>(rest % IPS);
+  const int k = k_begin + static_cast<int>(rest / IPS);
   const int ds = gs / NL, line = gs - ds * NL, dir = ds >> 1, side = ds & 1;
   const size_t e = kp.order[k];
   const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
@@ -1029,7 +1051,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const bool bd = cn.x < 0;
   const int S = conn_sign(cn.y);
   const int nd = node_on_line<C>(dir, line, side ? P : 0);
-  double* slot = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM + static_cast<size_t>(gs) * EJ::SLOT;
+  double* slot = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM + gs;  // entry o at slot[o * LS]
   int pass, g0;
   if (sub < NSP) {
     pass = 0;
@@ -1065,7 +1087,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       for (int j = 0; j < SEEDS; ++j)
         if (g0 + j < M)
 #pragma unroll
-          for (int c = 0; c < M; ++c) slot[B11 + c * M + g0 + j] = 0.0;
+          for (int c = 0; c < M; ++c) slot[(B11 + c * M + g0 + j) * LS] = 0.0;
       return;
     }
     double qiv[C::SECOND ? MD : 1], qov[C::SECOND ? MD : 1];
@@ -1076,9 +1098,18 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         qov[c] = bd ? 0.0 : __ldg(Q + onb * MD + c);
       }
     }
+    // LLF: closed-form inviscid Jacobian (llf_jac); the seeds then carry
+    // only the viscous terms (second-order physics)
+    constexpr bool LLFC = C::HAS_INV && C::RI != LDG_ROE && SEEDS >= M;
+    double Ji[LLFC ? M * M : 1];
+    if (LLFC) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Ji, ok);
+    if (LLFC && !C::SECOND) {
+#pragma unroll
+      for (int c = 0; c < (LLFC ? M * M : 0); ++c) slot[(pass * B11 + c) * LS] = Ji[c];
+    } else
 #pragma unroll
     for (int j = 0; j < SEEDS; ++j) {
-      const int b = g0 + j;
+      const int b = LLFC ? j : g0 + j;
       if (b >= M) break;
       D1 ui[M], uo[M], fh[M];
 #pragma unroll
@@ -1091,7 +1122,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       }
       if (C::HAS_INV) {
         if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        else if (!LLFC) llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
       }
       if (C::SECOND) {
         D1 fv[M];
@@ -1112,7 +1143,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         }
       }
 #pragma unroll
-      for (int c = 0; c < M; ++c) slot[pass * B11 + c * M + b] = fh[c].d[0];
+      for (int c = 0; c < M; ++c) slot[(pass * B11 + c * M + b) * LS] = fh[c].d[0] + (LLFC ? Ji[(c * M + b) % (LLFC ? M * M : 1)] : 0.0);
     }
   } else if (C::SECOND) {
     const bool out = !bd && S > 0;
@@ -1135,7 +1166,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       }
       visc_fn<D, C::PH, double, D1, D1>(usrc, dqv, n, kp.pp, fv, ok);
 #pragma unroll
-      for (int c = 0; c < M; ++c) slot[2 * B11 + c * MD + b] = fv[c].d[0];
+      for (int c = 0; c < M; ++c) slot[(2 * B11 + c * MD + b) * LS] = fv[c].d[0];
     }
   }
   if (!ok) {
@@ -1174,7 +1205,8 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 template <class C>
 struct JacThreads {
   static constexpr bool big = C::D == 3 && C::WU == 0;  // 3-D element work unit: many lines
-  static constexpr int value = big ? 640 : 128;
+  static constexpr int rows = (C::NPE * C::M + 31) / 32 * 32;  // jac_k11_rows3 items
+  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : 128;
   static constexpr int min_blocks = big ? 1 : 4;
 };
 
@@ -1186,7 +1218,7 @@ struct JacSmem {
   static constexpr int A = C::HAS_INV ? NLT * C::NQ * C::B11 : 0;  // dFinv/du . nvec at quad points
   static constexpr int AV = C::VIS_U ? NLT * C::NQ * C::B11 : 0;    // dFvis/du . nvec
   static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
-  static constexpr int SEC = NLT * 2 * EndJac<C>::SLOT;       // endpoint flux Jacobians (tile lines)
+  static constexpr int SEC = ((2 * NLT) | 1) * EndJac<C>::SLOT;  // endpoint flux Jacobians (tile lines)
   static constexpr int TABD = (C::NP * C::NQ + 2 * C::NP + 1) / 2 * 2;  // cc diagonal + M^-1 columns
   static constexpr int TAB = TABD + ((C::D == 3 && C::WU == 0) ? C::NP * C::NP * C::NQ : 0);  // + full cc
   static constexpr int ST11 = C::NS11 * C::B11 * C::NT;       // store doubles per tile
@@ -1203,94 +1235,111 @@ __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
   return dir == 0 ? 0 : (dir == 1 ? 1 + line % NP : 1 + NP + line % NP);
 }
 
-// 3-D element work unit, output-major K11 stores: one thread per
-// (slab s, slot, row r, column b) computes the m entries (a = 0..m-1) of that
-// block column, so the lanes of a warp run over consecutive (r, b) and every
-// store instruction writes 256 contiguous bytes of one block row a.
-// Line coefficients cc[i][t][q] come from shared memory (lane-dependent i).
+// 3-D element work unit, row-major K11 assembly: one thread per (slab s,
+// row r, column b) forms column b of every K11 block of its row.  It walks the
+// three lines through its node (dirs 2, 1, then 0), loading each line's
+// flux-Jacobian column A[q][.][b] into registers once and reusing it for all
+// NP blocks of that line; the self (diagonal) block accumulates in registers
+// across the three lines and is stored with the dir-0 blocks.  For every
+// slot the lanes of a warp run over consecutive (r, b), so each store
+// instruction writes 256 contiguous bytes of one block row a.
 template <class C, class EIdx>
-__device__ __forceinline__ void jac_k11_outmajor(const KParams<C>& kp, const double* mk, const int2* scon,
-                                                 const double* sE, EIdx eidx, const double* sA, const double* sAv,
-                                                 const double* scc, const double* smi, double* __restrict__ K11e,
-                                                 const int tid, const int nthr) {
+__device__ __forceinline__ void jac_k11_rows3(const double* mk, const int2* scon, const double* sE, EIdx eidx,
+                                              const double* sA, const double* sAv, const double* scc,
+                                              const double* smi, double* __restrict__ K11e, const int tid,
+                                              const int nthr) {
   constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, M = C::M, NT = C::NT, P = C::P, B11 = C::B11,
-                NS = C::NS11, TPE = C::TPE;
+                TPE = C::TPE;
   using EJ = EndJac<C>;
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
   constexpr int ST = JacSmem<C>::ST11;
-  constexpr int RB = NT * M;  // (row, b) entries per (slab, slot)
-  auto aval = [&](int tl, int q, int ab) {
-    return (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
-  };
-  for (int w = tid; w < TPE * NS * RB; w += nthr) {
-    const int rb = w % RB, ss = w / RB;
-    const int slot = ss % NS, s = ss / NS;
+  constexpr int RB = NT * M;  // (row, b) entries per (slab, slot, a)
+  constexpr int LS = EIdx::LS;
+  for (int w = tid; w < TPE * RB; w += nthr) {
+    const int s = w / RB, rb = w - s * RB;
     const int r = rb / M, b = rb - r * M;
     const int x0 = r % NP, x1 = r / NP, x2 = s;
     const int nd = r + NT * s;
-    int dir, t, side = -1;
-    if (slot < NP) {
-      dir = 0;
-      t = slot;
-    } else if (slot < NP + 2 * P) {
-      const int z = slot - NP;
-      dir = 1 + z / P;
-      const int tp = z % P, pos = dir == 1 ? x1 : x2;
-      t = tp + (tp >= pos ? 1 : 0);
-    } else {
-      const int z = slot - (3 * P + 1);
-      dir = z >> 1;
-      side = z & 1;
-      t = -1;
-    }
-    const int line = dir == 0 ? x1 + NP * x2 : (dir == 1 ? x0 + NP * x2 : x0 + NP * x1);
-    const int i = dir == 0 ? x0 : (dir == 1 ? x1 : x2);
-    const int tl = dir * NL + line;
     const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-    double v[M];
+    double* out = K11e + static_cast<size_t>(s) * ST + rb;
+    double vs[M];
 #pragma unroll
-    for (int a = 0; a < M; ++a) v[a] = 0.0;
-    if (side >= 0) {
-      const int2 cn = scon[dir * 2 + side];
-      if (cn.x >= 0) {
-        const double mi = smi[i * 2 + side];
-        const double* eo = sE + eidx(tl, dir, line, side) * EJ::SLOT + B11;
+    for (int a = 0; a < M; ++a) vs[a] = 0.0;
 #pragma unroll
-        for (int a = 0; a < M; ++a) v[a] = mi * eo[a * M + b];
+    for (int dd = 0; dd < 3; ++dd) {
+      const int dir = 2 - dd;
+      const int line = dir == 0 ? x1 + NP * x2 : (dir == 1 ? x0 + NP * x2 : x0 + NP * x1);
+      const int i = dir == 0 ? x0 : (dir == 1 ? x1 : x2);
+      const int tl = dir * NL + line;
+      double av[VOL11 ? NQ : 1][M];
+      if (VOL11) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int a = 0; a < M; ++a)
+            av[q][a] = (C::HAS_INV ? sA[(tl * NQ + q) * B11 + a * M + b] : 0.0) +
+                       (C::VIS_U ? sAv[(tl * NQ + q) * B11 + a * M + b] : 0.0);
       }
-    } else {
-      // line block (i, t) of direction dir, plus, for the self block, the
-      // other two directions' lines through the node
-      auto add_line = [&](int d, int ln, int ii, int tt) {
-        const int tld = d * NL + ln;
+      const double* e0 = sE + eidx(tl, dir, line, 0);
+      const double* e1 = sE + eidx(tl, dir, line, 1);
+      const double mi0 = smi[i * 2 + 0], mi1 = smi[i * 2 + 1];
+      // line block (i, t) column b
+      auto blk = [&](const int t, double* v) {
+#pragma unroll
+        for (int a = 0; a < M; ++a) v[a] = 0.0;
         if (VOL11) {
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            const double cq = scc[(ii * NP + tt) * NQ + q];
+            const double cq = scc[(i * NP + t) * NQ + q];
 #pragma unroll
-            for (int a = 0; a < M; ++a) v[a] += cq * aval(tld, q, a * M + b);
+            for (int a = 0; a < M; ++a) v[a] += cq * av[q][a];
           }
         }
-        if (tt == 0) {
-          const double* ei = sE + eidx(tld, d, ln, 0) * EJ::SLOT;
+        if (t == 0) {
 #pragma unroll
-          for (int a = 0; a < M; ++a) v[a] += smi[ii * 2 + 0] * ei[a * M + b];
+          for (int a = 0; a < M; ++a) v[a] += mi0 * e0[(a * M + b) * LS];
         }
-        if (tt == P) {
-          const double* ei = sE + eidx(tld, d, ln, 1) * EJ::SLOT;
+        if (t == P) {
 #pragma unroll
-          for (int a = 0; a < M; ++a) v[a] += smi[ii * 2 + 1] * ei[a * M + b];
+          for (int a = 0; a < M; ++a) v[a] += mi1 * e1[(a * M + b) * LS];
         }
       };
-      add_line(dir, line, i, t);
-      if (dir == 0 && t == x0) {
-        add_line(1, x0 + NP * x2, x1, x1);
-        add_line(2, x0 + NP * x1, x2, x2);
+      double v[M];
+      if (dir != 0) {
+        blk(i, v);
+#pragma unroll
+        for (int a = 0; a < M; ++a) vs[a] += v[a];
+#pragma unroll
+        for (int tp = 0; tp < P; ++tp) {
+          blk(tp + (tp >= i ? 1 : 0), v);
+          double* o = out + static_cast<size_t>(NP + (dir - 1) * P + tp) * B11 * NT;
+#pragma unroll
+          for (int a = 0; a < M; ++a) o[a * RB] = sc * v[a];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+          blk(t, v);
+          if (t == i) {
+#pragma unroll
+            for (int a = 0; a < M; ++a) v[a] += vs[a];
+          }
+          double* o = out + static_cast<size_t>(t) * B11 * NT;
+#pragma unroll
+          for (int a = 0; a < M; ++a) o[a * RB] = sc * v[a];
+        }
+      }
+      // neighbour node-columns 2*dir + side
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const bool nb = scon[dir * 2 + side].x >= 0;
+        const double* eo = (side ? e1 : e0) + B11 * LS;
+        const double mi = side ? mi1 : mi0;
+        double* o = out + static_cast<size_t>(C::D * P + 1 + 2 * dir + side) * B11 * NT;
+#pragma unroll
+        for (int a = 0; a < M; ++a) o[a * RB] = nb ? sc * (mi * eo[(a * M + b) * LS]) : 0.0;
       }
     }
-    double* out = K11e + static_cast<size_t>(s) * ST + static_cast<size_t>(slot) * B11 * NT + rb;
-#pragma unroll
-    for (int a = 0; a < M; ++a) out[a * RB] = sc * v[a];
   }
 }
 
@@ -1306,8 +1355,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, M = C::M, D = C::D, MD = C::MD, NT = C::NT, P = C::P,
                 B11 = C::B11;
   using SM = JacSmem<C>;
-  using EJ = EndJac<C>;
-  constexpr int NLT = SM::NLT;
+  constexpr int NLT = SM::NLT, LS = EIdx::LS;
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
   if (C::HAS_INV && !(kp.dbg & 1)) {
@@ -1387,10 +1435,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   }
   __syncthreads();
 
-  if (C::D == 3 && C::WU == 0) {
-    jac_k11_outmajor<C>(kp, mk, scon, sE, eidx, sA, sAv, stab + JacSmem<C>::TABD, stab + NP * NQ, K11t, tid,
-                        nthr);
-  }
+  if (C::D == 3 && C::WU == 0 && !(kp.dbg & 2))
+    jac_k11_rows3<C>(mk, scon, sE, eidx, sA, sAv, stab + JacSmem<C>::TABD, stab + NP * NQ, K11t, tid, nthr);
   // ---- phase 2: K11 rows of every tile line, stored block row by block row
   const double* sccd = stab;            // cc[p][p][q]
   const double* smi = stab + NP * NQ;   // M^-1[p][0], M^-1[p][p]
@@ -1405,10 +1451,10 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     double av[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(tl, q, ab) : 0.0;
-    const double* e0 = sE + eidx(tl, dir, line, 0) * EJ::SLOT;
-    const double* e1 = sE + eidx(tl, dir, line, 1) * EJ::SLOT;
-    const double ein0 = e0[ab], ein1 = e1[ab];
-    const double eo0 = e0[B11 + ab], eo1 = e1[B11 + ab];
+    const double* e0 = sE + eidx(tl, dir, line, 0);
+    const double* e1 = sE + eidx(tl, dir, line, 1);
+    const double ein0 = e0[ab * LS], ein1 = e1[ab * LS];
+    const double eo0 = e0[(B11 + ab) * LS], eo1 = e1[(B11 + ab) * LS];
     const int2 c0 = scon[dir * 2 + 0];
     const int2 c1 = scon[dir * 2 + 1];
     auto body = [&](const int i) {
@@ -1437,8 +1483,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
               for (int q = 0; q < NQ; ++q) v += sccd[p2 * NQ + q] * avq(tl2, q, ab);
             }
-            if (p2 == 0) v += smi[p2 * 2 + 0] * sE[eidx(tl2, d2, l2, 0) * EJ::SLOT + ab];
-            if (p2 == P) v += smi[p2 * 2 + 1] * sE[eidx(tl2, d2, l2, 1) * EJ::SLOT + ab];
+            if (p2 == 0) v += smi[p2 * 2 + 0] * sE[eidx(tl2, d2, l2, 0) + ab * LS];
+            if (p2 == P) v += smi[p2 * 2 + 1] * sE[eidx(tl2, d2, l2, 1) + ab * LS];
           }
         }
         rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B11] = sc * v;
@@ -1466,8 +1512,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     double bv[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) bv[q] = sBq[(tl * NQ + q) * M * MD + a * MD + b];
-    const double eq0 = sE[eidx(tl, dir, line, 0) * EJ::SLOT + 2 * B11 + a * MD + b];
-    const double eq1 = sE[eidx(tl, dir, line, 1) * EJ::SLOT + 2 * B11 + a * MD + b];
+    const double eq0 = sE[eidx(tl, dir, line, 0) + (2 * B11 + a * MD + b) * LS];
+    const double eq1 = sE[eidx(tl, dir, line, 1) + (2 * B11 + a * MD + b) * LS];
     const int2 c0 = scon[dir * 2 + 0];
     const int2 c1 = scon[dir * 2 + 1];
     // own-end dependence when boundary or S <= 0; neighbour slot otherwise
@@ -1498,7 +1544,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
               const int sd2 = p2 == 0 ? 0 : 1;
               const int2 cx = scon[d2 * 2 + sd2];
               if (cx.x < 0 || conn_sign(cx.y) <= 0)
-                v += smi[p2 * 2 + sd2] * sE[eidx(tl2, d2, l2, sd2) * EJ::SLOT + 2 * B11 + a * MD + b];
+                v += smi[p2 * 2 + sd2] * sE[eidx(tl2, d2, l2, sd2) + (2 * B11 + a * MD + b) * LS];
             }
           }
         }
@@ -1558,19 +1604,18 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   {
     const double* se = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM;
     for (int w = tid; w < NLT * 2 * EJ::SLOT; w += nthr) {
-      const int idx = w / EJ::SLOT, o = w - idx * EJ::SLOT;
+      const int o = w / (2 * NLT), idx = w - o * (2 * NLT);
       const int tl = idx >> 1, side = idx & 1;
       int dir, line;
       TileLines<C>::get(tl, s, dir, line);
-      sE[w] = __ldg(se + ((dir * 2 + side) * NL + line) * EJ::SLOT + o);
+      sE[o * SeTile<C>::LS + idx] = __ldg(se + o * EJ::LS + (dir * 2 + side) * NL + line);
     }
   }
   fill_tab<C>(kp, stab, tid, nthr);
   __shared__ int2 sconn[2 * C::D];
   if (tid < 2 * C::D) sconn[tid] = __ldg(&kp.conn[static_cast<size_t>(k) * C::D * 2 + tid]);
   __syncthreads();
-  auto eidx = [](int tl, int, int, int side) { return tl * 2 + side; };
-  jac_tile<C>(kp, k, s, e, su, sq, mk, sconn, sE, eidx, sA, sAv, sBq, stab,
+  jac_tile<C>(kp, k, s, e, su, sq, mk, sconn, sE, SeTile<C>(), sA, sAv, sBq, stab,
               K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
               C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
 }
@@ -1643,12 +1688,11 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   if (tid == 0)
     for (int b = 0; b < NB; ++b)
       if (k0 + b * G < k_end) issue(k0 + b * G, b);
-  auto eidx = [](int, int dir, int line, int side) { return (dir * 2 + side) * NL + line; };
   for (int k = k0, it = 0; k < k_end; k += G, ++it) {
     const int cur = it % NB;
     mbar_wait(&bar[cur], (it / NB) & 1);
     const size_t e = kp.order[k];
-    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bCONN(cur), bSE(cur), eidx, sA, sAv, sBq, stab,
+    jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bCONN(cur), bSE(cur), SeFull<C>(), sA, sAv, sBq, stab,
                 K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
                 C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
     __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done
