@@ -68,7 +68,14 @@ def sizes(cfg, case, m):
         out["gradient"] = U + 8 * met * E + conn + U * D
         out["residual"] = U + U * D + 8 * met * E + conn + U
     ns11 = D * p + 1 + 2 * D
-    out["jacobian"] = 8 * N * ns11 * m * m + U * (2 if second else 1) + 8 * met * E + conn
+    out["jacobian"] = 8 * N * ns11 * m * m + U + 8 * met * E + conn
+    if second:
+        # K12 = dR/dQ is re-assembled with K11 every step (K21 is U-independent,
+        # assembled once): ns12 node-columns of r12 x m*D blocks per row
+        # (Navier-Stokes drops the density row), plus the gradient Q read.
+        ns12 = D * p + 1 + D
+        r12 = m - 1 if m > 1 else 1
+        out["jacobian"] += 8 * N * ns12 * r12 * m * D + U * D
     out["spmv"] = 8 * N * ns11 * m * m + 2 * U + conn
     return out
 

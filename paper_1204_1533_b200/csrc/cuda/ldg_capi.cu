@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -290,6 +291,74 @@ std::vector<double> spd_inverse(const double* A, int n) {
   return inv;
 }
 
+// Element processing order.  Kernels walk elements in this order and gather
+// face neighbours by reference id, so an order in which face neighbours are
+// processed close together in time turns the neighbour-trace gathers of the
+// residual, the endpoint Jacobians and the SpMV into L2 hits (a renumbered
+// mesh in storage order has none).  Default: Morton (Z-order) of the element
+// centroids on a 2^(60/D)-per-axis grid over the bounding box, ties by id;
+// without node coordinates a breadth-first order over the face graph.
+// LDG_ORDER=identity keeps the storage order.
+std::vector<int32_t> processing_order(const ldg_setup& s, int D, int npe) {
+  const int E = s.n_elems;
+  std::vector<int32_t> ord(E);
+  for (int e = 0; e < E; ++e) ord[e] = e;
+  const char* env = std::getenv("LDG_ORDER");
+  if (env && std::string(env) == "identity") return ord;
+  if (s.node_coords) {
+    std::vector<double> cen(static_cast<size_t>(E) * D, 0.0);
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int e = 0; e < E; ++e)
+      for (int d = 0; d < D; ++d) {
+        double a = 0.0;
+        for (int n = 0; n < npe; ++n) a += s.node_coords[(static_cast<size_t>(e) * npe + n) * D + d];
+        a /= npe;
+        cen[static_cast<size_t>(e) * D + d] = a;
+        lo[d] = std::min(lo[d], a);
+        hi[d] = std::max(hi[d], a);
+      }
+    const int bits = D == 2 ? 30 : 20;
+    const double cells = static_cast<double>((1u << bits) - 1);
+    std::vector<std::pair<uint64_t, int32_t>> key(E);
+    for (int e = 0; e < E; ++e) {
+      uint64_t code = 0;
+      uint32_t q[3] = {0, 0, 0};
+      for (int d = 0; d < D; ++d) {
+        const double w = hi[d] > lo[d] ? (cen[static_cast<size_t>(e) * D + d] - lo[d]) / (hi[d] - lo[d]) : 0.0;
+        q[d] = static_cast<uint32_t>(std::min(cells, std::max(0.0, w * cells)));
+      }
+      for (int b = bits - 1; b >= 0; --b)
+        for (int d = D - 1; d >= 0; --d) code = (code << 1) | ((q[d] >> b) & 1u);
+      key[e] = {code, e};
+    }
+    std::sort(key.begin(), key.end());
+    for (int e = 0; e < E; ++e) ord[e] = key[e].second;
+    return ord;
+  }
+  // breadth-first over face neighbours, restarting at the lowest unvisited id
+  const int F = 2 * D;
+  std::vector<char> seen(E, 0);
+  int head = 0, tail = 0;
+  for (int root = 0; root < E; ++root) {
+    if (seen[root]) continue;
+    seen[root] = 1;
+    ord[tail++] = root;
+    while (head < tail) {
+      const int e = ord[head++];
+      for (int lf = 0; lf < F; ++lf) {
+        const int fid = s.elem_face[static_cast<size_t>(e) * F + lf];
+        if (fid < 0 || fid >= s.n_faces || s.face_elem_r[fid] < 0) continue;
+        const int oe = s.face_elem_l[fid] == e && s.face_face_l[fid] == lf ? s.face_elem_r[fid] : s.face_elem_l[fid];
+        if (oe >= 0 && oe < E && !seen[oe]) {
+          seen[oe] = 1;
+          ord[tail++] = oe;
+        }
+      }
+    }
+  }
+  return ord;
+}
+
 void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   std::map<int, int> tag2bc;
   std::vector<double> bcv;
@@ -476,10 +545,10 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
       for (int t = 0; t < np; ++t)
         for (int q = 0; q < nq; ++q) c->cc[(i * np + t) * nq + q] = c->dq[i * nq + q] * c->phi[t * nq + q];
 
-    // Processing order (identity; the store is laid out in this order).
-    c->order.resize(c->E);
+    // Processing order (the Jacobian store and the metric are laid out in it).
+    c->order = processing_order(*s, c->D, c->npe);
     c->inv_order.resize(c->E);
-    for (int k = 0; k < c->E; ++k) c->order[k] = c->inv_order[k] = k;
+    for (int k = 0; k < c->E; ++k) c->inv_order[c->order[k]] = k;
     ck(cudaMalloc(&c->d_order, c->E * sizeof(int32_t)), "cudaMalloc order");
     ck(cudaMemcpy(c->d_order, c->order.data(), c->E * sizeof(int32_t), cudaMemcpyHostToDevice), "upload order");
 

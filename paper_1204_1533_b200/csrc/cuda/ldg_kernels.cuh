@@ -837,6 +837,445 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   }
 }
 
+// ============================== residual, persistent + TMA, flux-parallel
+// Same prefetch ring as k_residual_p (TMA bulk copies of a batch's element
+// states, metric and connectivity on an mbarrier; neighbour traces by
+// cp.async), but the work of a batch is flattened into short independent
+// items so many more warps are resident:
+//   R1  one item per (element, line, quadrature point): F(u_q).nvec_q (+ the
+//       viscous flux) into shared memory;
+//   R2  one item per (element, line end): the Riemann (+ LDG switch) flux;
+//   R3  one item per (element, node, component): the line projections
+//       r = sum_q dq[i][q] F_q + mi[i][0] Fh_0 + mi[i][1] Fh_1 summed over the
+//       D lines through the node, dU/dt = S - (1/J) sum (coalesced store).
+// Basis tables live in shared memory (lane-dependent indices).
+// Batch input ring shared by the flattened residual and gradient kernels:
+// two buffers of EPB elements {U, (Q), metric, connectivity, neighbour traces
+// (U; Q where the switch selects the neighbour)}; bulk data by TMA on one
+// mbarrier per buffer, neighbour traces by cp.async once the connectivity
+// has landed.
+template <class C, int EPB, bool WQ>
+struct BatchIO {
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int U = ev(EPB * C::NPE * C::M);
+  static constexpr int Q = WQ ? ev(EPB * C::NPE * C::MD) : 0;
+  static constexpr int MET = EPB * C::METP;
+  static constexpr int CONN = ev(EPB * C::D * 2);  // int2 entries, 8 B each
+  static constexpr int NB = ev(EPB * C::LPE * 2 * C::M);
+  static constexpr int NBQ = WQ ? ev(EPB * C::LPE * 2 * C::MD) : 0;
+  static constexpr int BUF = U + Q + MET + CONN + NB + NBQ;
+  static constexpr int SMEM = 2 + 2 * BUF;  // 2 doubles hold the two mbarriers
+  static constexpr bool TMA = (C::NPE * C::M) % 2 == 0 && (!WQ || (C::NPE * C::MD) % 2 == 0);
+  static constexpr long long bytes_per_elem() {
+    return 8LL * 2 * (C::NPE * C::M + (WQ ? C::NPE * C::MD : 0) + C::METP + 2 * C::D + C::LPE * 2 * C::M +
+                      (WQ ? C::LPE * 2 * C::MD : 0));
+  }
+  uint64_t* bar;
+  double* bufs;
+  __device__ BatchIO(double* smem) : bar(reinterpret_cast<uint64_t*>(smem)), bufs(smem + 2) {}
+  __device__ double* bU(int bi) const { return bufs + bi * BUF; }
+  __device__ double* bQ(int bi) const { return bufs + bi * BUF + U; }
+  __device__ double* bMET(int bi) const { return bufs + bi * BUF + U + Q; }
+  __device__ int2* bCONN(int bi) const { return reinterpret_cast<int2*>(bufs + bi * BUF + U + Q + MET); }
+  __device__ double* bNB(int bi) const { return bufs + bi * BUF + U + Q + MET + CONN; }
+  __device__ double* bNBQ(int bi) const { return bufs + bi * BUF + U + Q + MET + CONN + NB; }
+  __device__ void init(int tid) {
+    if (tid == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      mbar_fence_init();
+    }
+  }
+  // bulk loads of one batch into buffer bi (thread 0)
+  __device__ void issue(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int bi) {
+    constexpr int NPE = C::NPE, M = C::M, MD = C::MD, D = C::D;
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    unsigned bytes = nb * (NPE * M * 8) + nb * C::METP * 8 + nb * D * 2 * 8;
+    if (WQ) bytes += nb * (NPE * MD * 8);
+    mbar_expect_tx(&bar[bi], bytes);
+    for (int le = 0; le < nb; ++le) {
+      const size_t e = __ldg(kp.order + k0 + le);
+      tma_load_1d(bU(bi) + le * NPE * M, Ug + e * (NPE * M), NPE * M * 8, &bar[bi]);
+      if (WQ) tma_load_1d(bQ(bi) + le * NPE * MD, Qg + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
+    }
+    tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k0) * C::METP, nb * C::METP * 8, &bar[bi]);
+    tma_load_1d(bCONN(bi), kp.conn + static_cast<size_t>(k0) * D * 2, nb * D * 2 * 8, &bar[bi]);
+  }
+  // synchronous fallback (element chunks not 16-byte aligned)
+  __device__ void load_sync(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int bi, int tid,
+                            int nthr) {
+    constexpr int NPE = C::NPE, M = C::M, MD = C::MD, D = C::D;
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    for (int le = 0; le < nb; ++le) {
+      const size_t e = kp.order[k0 + le];
+      for (int i = tid; i < NPE * M; i += nthr) bU(bi)[le * NPE * M + i] = __ldg(Ug + e * (NPE * M) + i);
+      if (WQ)
+        for (int i = tid; i < NPE * MD; i += nthr) bQ(bi)[le * NPE * MD + i] = __ldg(Qg + e * (NPE * MD) + i);
+    }
+    for (int i = tid; i < nb * C::METP; i += nthr) bMET(bi)[i] = __ldg(kp.metric + static_cast<size_t>(k0) * C::METP + i);
+    for (int i = tid; i < nb * D * 2; i += nthr)
+      bCONN(bi)[i] = __ldg(kp.conn + static_cast<size_t>(k0) * D * 2 + i);
+    __syncthreads();
+  }
+  // neighbour traces of buffer bi (all threads; needs its connectivity)
+  __device__ void gather(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int bi, int tid,
+                         int nthr) {
+    constexpr int NPE = C::NPE, M = C::M, MD = C::MD, D = C::D, NL = C::NL, LPE = C::LPE, NP = C::NP;
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    const int2* sc = bCONN(bi);
+    for (int w = tid; w < nb * LPE * 2; w += nthr) {
+      const int side = w & 1, lw = w >> 1, le = lw / LPE, rem = lw - le * LPE;
+      const int dir = rem / NL, line = rem - dir * NL;
+      const int2 cn = sc[(le * D + dir) * 2 + side];
+      if (cn.x < 0) continue;
+      const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+      double* dst = bNB(bi) + w * M;
+#pragma unroll
+      for (int c = 0; c < M; ++c) cp_async8(dst + c, Ug + nd * M + c);
+      if (WQ && conn_sign(cn.y) > 0) {
+        double* dq = bNBQ(bi) + w * MD;
+#pragma unroll
+        for (int c = 0; c < MD; ++c) cp_async8(dq + c, Qg + nd * MD + c);
+      }
+    }
+    cp_async_commit();
+  }
+  // prologue: batch b0 resident in buffer 0 (traces in flight), b0+G issued
+  __device__ void start(const KParams<C>& kp, const double* Ug, const double* Qg, int b0, int G, int nbatch, int tid,
+                        int nthr) {
+    if (TMA) {
+      if (tid == 0) {
+        issue(kp, Ug, Qg, b0, 0);
+        if (b0 + G < nbatch) issue(kp, Ug, Qg, b0 + G, 1);
+      }
+      mbar_wait(&bar[0], 0);
+    } else {
+      load_sync(kp, Ug, Qg, b0, 0, tid, nthr);
+    }
+    gather(kp, Ug, Qg, b0, 0, tid, nthr);
+  }
+  // epilogue of iteration `it` (batch `batch`): make the next batch resident,
+  // start its gathers, free buffer `cur` and refill it two batches ahead
+  __device__ void advance(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int it, int G,
+                          int nbatch, int tid, int nthr) {
+    const int cur = it & 1, nxt = cur ^ 1;
+    const int nbn = batch + G;
+    if (nbn < nbatch) {
+      if (TMA) mbar_wait(&bar[nxt], ((it + 1) >> 1) & 1);
+      else {
+        __syncthreads();
+        load_sync(kp, Ug, Qg, nbn, nxt, tid, nthr);
+      }
+      gather(kp, Ug, Qg, nbn, nxt, tid, nthr);
+    }
+    __syncthreads();
+    if (TMA && tid == 0 && batch + 2 * G < nbatch) issue(kp, Ug, Qg, batch + 2 * G, cur);
+  }
+};
+
+template <class C, int EPB>
+struct ResF {
+  using IO = BatchIO<C, EPB, C::SECOND>;
+  static constexpr int F = EPB * C::LPE * C::NQ * C::M;
+  static constexpr int FH = EPB * C::LPE * 2 * C::M;
+  static constexpr int TAB = IO::ev(2 * C::NP * C::NQ + 2 * C::NP);
+  static constexpr int TOTAL = IO::SMEM + F + FH + TAB;
+  static constexpr int THREADS = 256;
+  static constexpr long long bytes_per_elem() {
+    return IO::bytes_per_elem() + 8LL * (C::LPE * C::NQ * C::M + C::LPE * 2 * C::M);
+  }
+};
+template <class C>
+struct ResFEpb {
+  static constexpr long long per = ResF<C, 1>::bytes_per_elem();
+  static constexpr int raw = static_cast<int>((110LL * 1024) / per);
+  static constexpr int value = raw < 1 ? 1 : (raw > 8 ? 8 : raw);
+};
+
+template <class C, int EPB>
+__global__ void __launch_bounds__(ResF<C, EPB>::THREADS)
+k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+             double* __restrict__ R) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD,
+                LPE = C::LPE, P = C::P;
+  using RP = ResF<C, EPB>;
+  extern __shared__ __align__(16) double smem[];
+  typename RP::IO io(smem);
+  double* const sF = smem + RP::IO::SMEM;
+  double* const sFH = sF + RP::F;
+  double* const sphi = sFH + RP::FH;     // phi[t][q]
+  double* const sdq = sphi + NP * NQ;    // dq[i][q]
+  double* const smi = sdq + NP * NQ;     // mi[i][side]
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nbatch = (kp.E + EPB - 1) / EPB;
+  const int G = gridDim.x;
+  if (static_cast<int>(blockIdx.x) >= nbatch) return;
+  io.init(tid);
+  for (int i = tid; i < NP * NQ; i += nthr) {
+    sphi[i] = (&kp.bt.phi[0][0])[i];
+    sdq[i] = (&kp.bt.dq[0][0])[i];
+  }
+  for (int i = tid; i < 2 * NP; i += nthr) smi[i] = (&kp.bt.mi[0][0])[i];
+  __syncthreads();
+  io.start(kp, U, Q, blockIdx.x, G, nbatch, tid, nthr);
+  for (int batch = blockIdx.x, it = 0; batch < nbatch; batch += G, ++it) {
+    const int cur = it & 1;
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- R2 (line ends) then R1 (quadrature points)
+    const int n2 = nb * LPE * 2, n1 = nb * LPE * NQ;
+    for (int w = tid; w < n2 + n1; w += nthr) {
+      bool ok = true;
+      int le, dir, line;
+      if (w < n2) {
+        const int side = w & 1, lw = w >> 1;
+        le = lw / LPE;
+        const int rem = lw - le * LPE;
+        dir = rem / NL;
+        line = rem - dir * NL;
+        const double* mk = io.bMET(cur) + le * C::METP;
+        const double* sul = io.bU(cur) + le * NPE * M;
+        const double* sql = io.bQ(cur) + le * NPE * MD;
+        const int2 cn = io.bCONN(cur)[(le * D + dir) * 2 + side];
+        const int S = conn_sign(cn.y);
+        const int nd = node_on_line<C>(dir, line, side ? P : 0);
+        const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
+        double n[D], ui[M], uo[M], fh[M];
+#pragma unroll
+        for (int d = 0; d < D; ++d) n[d] = nep[d];
+        const double* bcp = cn.x < 0 ? kp.bcv + (-1 - cn.x) * M : nullptr;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          ui[c] = sul[nd * M + c];
+          uo[c] = bcp ? __ldg(bcp + c) : io.bNB(cur)[w * M + c];
+          fh[c] = 0.0;
+        }
+        if (C::HAS_INV) {
+          if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+          else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        }
+        if (C::SECOND) {
+          double nn = n[0] * n[0];
+#pragma unroll
+          for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+          nn = sqrt(nn);
+          double fv[M];
+          if (bcp) {
+            visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+            const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - uo[c]);
+          } else {
+            if (S > 0) visc_fn<D, C::PH, double, double, double>(uo, io.bNBQ(cur) + w * MD, n, kp.pp, fv, ok);
+            else visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+#pragma unroll
+            for (int c = 0; c < M; ++c) fh[c] += fv[c];
+            if (kp.pp.c11 != 0.0) {
+#pragma unroll
+              for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) sFH[w * M + c] = fh[c];
+      } else {
+        const int v = w - n2, lw = v / NQ, q = v - lw * NQ;
+        le = lw / LPE;
+        const int rem = lw - le * LPE;
+        dir = rem / NL;
+        line = rem - dir * NL;
+        const double* mk = io.bMET(cur) + le * C::METP;
+        const double* sul = io.bU(cur) + le * NPE * M;
+        const double* sql = io.bQ(cur) + le * NPE * MD;
+        double uq[M], qq[C::SECOND ? MD : 1];
+#pragma unroll
+        for (int c = 0; c < M; ++c) uq[c] = 0.0;
+        if (C::SECOND) {
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+          const int nd = node_on_line<C>(dir, line, t);
+          const double ph = sphi[t * NQ + q];
+#pragma unroll
+          for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
+          if (C::SECOND) {
+#pragma unroll
+            for (int c = 0; c < MD; ++c) qq[c] += ph * sql[nd * MD + c];
+          }
+        }
+        double nv[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) nv[d] = mk[((dir * NL + line) * NQ + q) * D + d];
+        double f[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) f[c] = 0.0;
+        if (C::HAS_INV) euler_fn<D>(uq, nv, kp.pp.gamma, f, ok);
+        if (C::SECOND) {
+          double fv[M];
+          visc_fn<D, C::PH, double, double, double>(uq, qq, nv, kp.pp, fv, ok);
+#pragma unroll
+          for (int c = 0; c < M; ++c) f[c] += fv[c];
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) sF[v * M + c] = f[c];
+      }
+      if (!ok) report_line<C>(kp, kp.order[k0 + le], dir, line, io.bU(cur) + le * NPE * M);
+    }
+    __syncthreads();
+    // ---- R3: dU/dt = S - (1/J) sum_dir r
+    for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
+      const int l = idx / (NPE * M), off = idx - l * NPE * M;
+      const int nd = off / M, c = off - nd * M;
+      const size_t e = kp.order[k0 + l];
+      double sum = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        int ln, i;
+        line_of<C>(d, nd, ln, i);
+        const int lw = l * LPE + d * NL + ln;
+        const double* fq = sF + lw * NQ * M + c;
+        double r = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) r += sdq[i * NQ + q] * fq[q * M];
+        r += smi[i * 2 + 0] * sFH[(lw * 2 + 0) * M + c];
+        r += smi[i * 2 + 1] * sFH[(lw * 2 + 1) * M + c];
+        sum = d == 0 ? r : sum + r;
+      }
+      const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
+      const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
+      R[e * (NPE * M) + off] = src - invJ * sum;
+    }
+    io.advance(kp, U, Q, batch, it, G, nbatch, tid, nthr);
+  }
+}
+
+// ======================================== gradient, persistent + TMA, flattened
+// Q = (1/J) sum_dir M^-1 [u_hat (x) n |ends - sum_q w phi' u_q (x) nvec_q]
+// (PAPER.md:520-573).  Items per batch: G1 one per (element, line, component
+// c) interpolates u_c along the line and accumulates the line's contribution
+//   g[i][d] = sum_q dq[i][q] u_q nvec_q[d] + sum_side mi[i][side] uh n_side[d]
+// in registers (u_hat the switch-selected trace: own where S = +1, neighbour
+// where S = -1, g_D on boundaries), written per direction to shared memory;
+// G2 one per (element, node, c*D+d) sums the directions, scales by 1/J and
+// stores coalesced.
+template <class C, int EPB>
+struct GradF {
+  using IO = BatchIO<C, EPB, false>;
+  static constexpr int ACC = EPB * C::D * C::NPE * C::MD;
+  static constexpr int TAB = IO::ev(2 * C::NP * C::NQ + 2 * C::NP);
+  static constexpr int TOTAL = IO::SMEM + ACC + TAB;
+  static constexpr int THREADS = 256;
+  static constexpr long long bytes_per_elem() { return IO::bytes_per_elem() + 8LL * C::D * C::NPE * C::MD; }
+};
+template <class C>
+struct GradFEpb {
+  static constexpr long long per = GradF<C, 1>::bytes_per_elem();
+  static constexpr int raw = static_cast<int>((110LL * 1024) / per);
+  static constexpr int value = raw < 1 ? 1 : (raw > 8 ? 8 : raw);
+};
+
+template <class C, int EPB>
+__global__ void __launch_bounds__(GradF<C, EPB>::THREADS)
+k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restrict__ Qo) {
+  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD,
+                LPE = C::LPE, P = C::P;
+  using GP = GradF<C, EPB>;
+  extern __shared__ __align__(16) double smem[];
+  typename GP::IO io(smem);
+  double* const sacc = smem + GP::IO::SMEM;  // [EPB][D][NPE][MD]
+  double* const sphi = sacc + GP::ACC;
+  double* const sdq = sphi + NP * NQ;
+  double* const smi = sdq + NP * NQ;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nbatch = (kp.E + EPB - 1) / EPB;
+  const int G = gridDim.x;
+  if (static_cast<int>(blockIdx.x) >= nbatch) return;
+  io.init(tid);
+  for (int i = tid; i < NP * NQ; i += nthr) {
+    sphi[i] = (&kp.bt.phi[0][0])[i];
+    sdq[i] = (&kp.bt.dq[0][0])[i];
+  }
+  for (int i = tid; i < 2 * NP; i += nthr) smi[i] = (&kp.bt.mi[0][0])[i];
+  __syncthreads();
+  io.start(kp, U, nullptr, blockIdx.x, G, nbatch, tid, nthr);
+  for (int batch = blockIdx.x, it = 0; batch < nbatch; batch += G, ++it) {
+    const int cur = it & 1;
+    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- G1: one (line, component) per item
+    for (int v = tid; v < nb * LPE * M; v += nthr) {
+      const int lw = v / M, c = v - lw * M;
+      const int l = lw / LPE, rem = lw - l * LPE;
+      const int dir = rem / NL, line = rem - dir * NL;
+      const double* mk = io.bMET(cur) + l * C::METP;
+      const double* sul = io.bU(cur) + l * NPE * M;
+      const double* nvl = mk + (dir * NL + line) * NQ * D;
+      double ul[NP];
+#pragma unroll
+      for (int t = 0; t < NP; ++t) ul[t] = sul[node_on_line<C>(dir, line, t) * M + c];
+      double g[NP][D];
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int d = 0; d < D; ++d) g[i][d] = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double uq = 0.0;
+#pragma unroll
+        for (int t = 0; t < NP; ++t) uq += sphi[t * NQ + q] * ul[t];
+        double w[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) w[d] = uq * nvl[q * D + d];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const double dqi = sdq[i * NQ + q];
+#pragma unroll
+          for (int d = 0; d < D; ++d) g[i][d] += dqi * w[d];
+        }
+      }
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int2 cn = io.bCONN(cur)[(l * D + dir) * 2 + side];
+        double uh;
+        if (cn.x < 0) uh = __ldg(kp.bcv + (-1 - cn.x) * M + c);  // Dirichlet: u_hat = g_D
+        else if (conn_sign(cn.y) > 0) uh = ul[side ? P : 0];     // S = +1: own trace
+        else uh = io.bNB(cur)[((lw << 1) | side) * M + c];
+        const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const double w = uh * nep[d];
+#pragma unroll
+          for (int i = 0; i < NP; ++i) g[i][d] += smi[i * 2 + side] * w;
+        }
+      }
+      double* acc = sacc + (l * D + dir) * NPE * MD + c * D;
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        const int nd = node_on_line<C>(dir, line, t);
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc[nd * MD + d] = g[t][d];
+      }
+    }
+    __syncthreads();
+    // ---- G2: Q = (1/J) sum_dir d^(dir)
+    for (int idx = tid; idx < nb * NPE * MD; idx += nthr) {
+      const int l = idx / (NPE * MD), off = idx - l * NPE * MD;
+      const int nd = off / MD;
+      const double* a = sacc + l * D * NPE * MD + off;
+      double s = a[0];
+#pragma unroll
+      for (int d = 1; d < D; ++d) s = s + a[d * NPE * MD];
+      const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
+      Qo[kp.order[k0 + l] * static_cast<size_t>(NPE * MD) + off] = invJ * s;
+    }
+    io.advance(kp, U, nullptr, batch, it, G, nbatch, tid, nthr);
+  }
+}
+
 // ===================================================================== gradient
 // Q = (1/J) sum_dir d^(dir),  d = M^-1 [u_hat (x) n |ends - sum_q w phi' u_q (x) nvec_q]
 template <class C, int EPB>

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <string>
 #include <cstring>
 
 #include "ldg_kernels.cuh"
@@ -82,6 +83,13 @@ struct Launch {
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
     static const bool simple = std::getenv("LDG_RESIDUAL_SIMPLE") != nullptr;
     if (simple) return residual_simple(d, U, Q, R);
+    // Kernel choice (measured on B200, bench.py --config N): the flattened
+    // flux-parallel kernel wins where the per-line work is long (second-order
+    // physics: viscous fluxes and the gradient at every point); the
+    // thread-per-line kernel wins for Euler.  LDG_RESIDUAL=line|flux overrides.
+    static const char* sel = std::getenv("LDG_RESIDUAL");
+    const bool flux = sel ? std::string(sel) == "flux" : C::SECOND;
+    if (flux) return residual_f(d, U, Q, R);
     using RP = ResP<C, EPB>;
     const size_t smem = sizeof(double) * RP::TOTAL;
     static int grid_max = 0;
@@ -97,6 +105,46 @@ struct Launch {
     const int nbatch = (d.E + EPB - 1) / EPB;
     const int grid = nbatch < grid_max ? nbatch : grid_max;
     k_residual_p<C, EPB><<<grid, RP::THREADS, smem, d.stream>>>(params(d), U, Q, R);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t residual_f(const DevCtx& d, const double* U, const double* Q, double* R) {
+    constexpr int EF = ResFEpb<C>::value;
+    using RP = ResF<C, EF>;
+    const size_t smem = sizeof(double) * RP::TOTAL;
+    static int grid_max = 0;
+    if (!grid_max) {
+      cudaFuncSetAttribute(k_residual_f<C, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_residual_f<C, EF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_residual_f<C, EF>, RP::THREADS, smem);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    const int nbatch = (d.E + EF - 1) / EF;
+    const int grid = nbatch < grid_max ? nbatch : grid_max;
+    k_residual_f<C, EF><<<grid, RP::THREADS, smem, d.stream>>>(params(d), U, Q, R);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t gradient_f(const DevCtx& d, const double* U, double* Q) {
+    constexpr int EF = GradFEpb<C>::value;
+    using GP = GradF<C, EF>;
+    const size_t smem = sizeof(double) * GP::TOTAL;
+    static int grid_max = 0;
+    if (!grid_max) {
+      cudaFuncSetAttribute(k_gradient_f<C, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_gradient_f<C, EF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gradient_f<C, EF>, GP::THREADS, smem);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    const int nbatch = (d.E + EF - 1) / EF;
+    const int grid = nbatch < grid_max ? nbatch : grid_max;
+    k_gradient_f<C, EF><<<grid, GP::THREADS, smem, d.stream>>>(params(d), U, Q);
     count(d);
     return cudaGetLastError();
   }
@@ -131,6 +179,8 @@ struct Launch {
   }
   static cudaError_t gradient(const DevCtx& d, const double* U, double* Q) {
     if (!C::SECOND) return cudaSuccess;
+    static const char* gsel = std::getenv("LDG_GRADIENT");
+    if (!(gsel && std::string(gsel) == "line")) return gradient_f(d, U, Q);
     const size_t smem = sizeof(double) * (EPB * C::NPE * C::M + EPB * C::D * C::NPE * C::MD);
     static bool init = false;
     if (!init) {
