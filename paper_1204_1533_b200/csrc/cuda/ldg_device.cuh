@@ -461,4 +461,58 @@ __device__ __forceinline__ void visc_fn(const T* u, const TQ* q, const double* n
   }
 }
 
+// Closed-form d(F_vis.n)/dq (row-major M x MD, column c'*D + d).  The viscous
+// flux of visc_fn is linear in q, F_vis = L(u) q; L's columns follow from
+// the responses of the flux to unit velocity-gradient and energy-gradient
+// entries (gv = (q_m - v q_rho)/rho, gE = (q_E - E q_rho)/rho):
+//   q_{1+k,d}: (1/rho) R(gv[k][d]),   q_{D+1,d}: (1/rho) R(gE[d]),
+//   q_{0,d}:   -(sum_k v_k col(q_{1+k,d}) + E col(q_{D+1,d})).
+template <int D, int PH>
+__device__ __forceinline__ void visc_dq(const double* u, const double* n, const PhysParams& pp, double* L,
+                                        bool& ok) {
+  constexpr int M = PH == PH_POISSON ? 1 : D + 2, MD = M * D;
+#pragma unroll
+  for (int i = 0; i < M * MD; ++i) L[i] = 0.0;
+  if (PH == PH_POISSON) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) L[d] = -n[d];
+    return;
+  }
+  const double rho = u[0];
+  ok = ok && (rho > 0.0);
+  const double irho = 1.0 / rho;
+  double v[D], vn = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    v[i] = u[1 + i] * irho;
+    vn += v[i] * n[i];
+  }
+  const double E = u[D + 1] * irho;
+  const double mu = pp.mu, kap = pp.kap, c23 = 2.0 / 3.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int col = (1 + k) * D + d;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double t = (i == k ? n[d] : 0.0) + (i == d ? n[k] : 0.0) - (k == d ? c23 * n[i] : 0.0);
+        L[(1 + i) * MD + col] = -irho * (mu * t);
+      }
+      const double en = mu * (v[k] * n[d] + v[d] * n[k]) - (k == d ? c23 * mu * vn : 0.0);
+      L[(D + 1) * MD + col] = irho * (kap * v[k] * n[d] - en);
+    }
+#pragma unroll
+  for (int d = 0; d < D; ++d) L[(D + 1) * MD + (D + 1) * D + d] = -irho * kap * n[d];
+#pragma unroll
+  for (int c = 1; c < M; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double s = E * L[c * MD + (D + 1) * D + d];
+#pragma unroll
+      for (int k = 0; k < D; ++k) s += v[k] * L[c * MD + (1 + k) * D + d];
+      L[c * MD + d] = -s;
+    }
+}
+
 }  // namespace ldg

@@ -1448,6 +1448,9 @@ struct EndJac {
   // TMA rows) so shared-memory reads of neighbouring entries spread over banks.
   static constexpr int LS = SLOT % 2 == 0 ? (NLE | 1) : NLE + (NLE & 1);
   static constexpr int PER_ELEM = SLOT * LS;                  // doubles per element
+  // k_endjac items per line end with `seeds` u-seeds per thread: the in and
+  // out passes, plus one closed-form dF_vis/dq item (second order)
+  static constexpr int items(int seeds) { return 2 * ((C::M + seeds - 1) / seeds) + (C::SECOND ? 1 : 0); }
 };
 
 // Line-end index functors for jac_tile: whole-element scratch block (k_endjac
@@ -1473,8 +1476,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
                 B11 = C::B11;
   using EJ = EndJac<C>;
   constexpr int NSP = (M + SEEDS - 1) / SEEDS;         // u-seed groups per pass
-  constexpr int NSQ = (MD + SEEDS - 1) / SEEDS;        // q-seed groups
-  constexpr int IPS = 2 * NSP + (C::SECOND ? NSQ : 0);  // items per line end
+  constexpr int IPS = EJ::items(SEEDS);                 // items per line end
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nitems = static_cast<int64_t>(k_end - k_begin) * 2 * D * NL * IPS;
   if (item >= nitems) return;
@@ -1585,28 +1587,15 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       for (int c = 0; c < M; ++c) slot[(pass * B11 + c * M + b) * LS] = fh[c].d[0] + (LLFC ? Ji[(c * M + b) % (LLFC ? M * M : 1)] : 0.0);
     }
   } else if (C::SECOND) {
+    // dF_vis/dq of the switch-selected side, closed form (visc_dq)
     const bool out = !bd && S > 0;
-    const size_t src = out ? onb : own;
     double usrc[M];
 #pragma unroll
     for (int c = 0; c < M; ++c) usrc[c] = out ? uov[c] : uiv[c];
-    double qv[MD];
+    double L[M * MD];
+    visc_dq<D, C::PH>(usrc, n, kp.pp, L, ok);
 #pragma unroll
-    for (int c = 0; c < MD; ++c) qv[c] = __ldg(Q + src * MD + c);
-#pragma unroll
-    for (int j = 0; j < SEEDS; ++j) {
-      const int b = g0 + j;
-      if (b >= MD) break;
-      D1 dqv[MD], fv[M];
-#pragma unroll
-      for (int c = 0; c < MD; ++c) {
-        dqv[c] = D1(qv[c]);
-        dqv[c].d[0] = c == b ? 1.0 : 0.0;
-      }
-      visc_fn<D, C::PH, double, D1, D1>(usrc, dqv, n, kp.pp, fv, ok);
-#pragma unroll
-      for (int c = 0; c < M; ++c) slot[(2 * B11 + c * MD + b) * LS] = fv[c].d[0];
-    }
+    for (int c = 0; c < M * MD; ++c) slot[(2 * B11 + c) * LS] = L[c];
   }
   if (!ok) {
     // a non-physical state at this line end: report the offending nodal state
@@ -1819,9 +1808,10 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
   }
-  // ---- phase 1c (second-order): viscous flux derivatives, one seed per item
+  // ---- phase 1c (second-order): viscous flux derivatives at the quadrature
+  // points: one item per u-seed (dual numbers) plus one closed-form dF/dq item
   if (C::SECOND && !(kp.dbg & 1)) {
-    constexpr int NSU = C::VIS_U ? M : 0, NSEED = NSU + MD;
+    constexpr int NSU = C::VIS_U ? M : 0, NSEED = NSU + 1;
     for (int w = tid; w < NLT * NQ * NSEED; w += nthr) {
       const int sd = w % NSEED, tq = w / NSEED, tl = tq / NQ, q = tq - tl * NQ;
       int dir, line;
@@ -1857,17 +1847,11 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
         for (int c = 0; c < M; ++c) a[c * M + sd] = fv[c].d[0];
       } else {
-        const int bq = sd - NSU;
-        D1 dq[MD];
-#pragma unroll
-        for (int c = 0; c < MD; ++c) {
-          dq[c] = D1(qq[c]);
-          dq[c].d[0] = c == bq ? 1.0 : 0.0;
-        }
-        visc_fn<D, C::PH, double, D1, D1>(uq, dq, nv, kp.pp, fv, ok);
+        double L[M * MD];
+        visc_dq<D, C::PH>(uq, nv, kp.pp, L, ok);
         double* bqp = sBq + (tl * NQ + q) * M * MD;
 #pragma unroll
-        for (int c = 0; c < M; ++c) bqp[c * MD + bq] = fv[c].d[0];
+        for (int c = 0; c < M * MD; ++c) bqp[c] = L[c];
       }
       if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }

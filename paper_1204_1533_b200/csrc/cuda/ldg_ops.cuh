@@ -212,8 +212,7 @@ struct Launch {
       cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       init = true;
     }
-    constexpr int NSP = (C::M + EJ_SEEDS - 1) / EJ_SEEDS, NSQ = (C::MD + EJ_SEEDS - 1) / EJ_SEEDS;
-    constexpr int IPS = 2 * NSP + (C::SECOND ? NSQ : 0);
+    constexpr int IPS = EndJac<C>::items(EJ_SEEDS);
     static const bool one_seed = std::getenv("LDG_ENDJAC_SEEDS1") != nullptr;  // tuning switch
     static const bool simple = std::getenv("LDG_JACOBIAN_SIMPLE") != nullptr;
     static int grid_max = 0;
@@ -231,8 +230,7 @@ struct Launch {
     for (int kb = 0; kb < d.E; kb += chunk) {
       const int ke = kb + chunk < d.E ? kb + chunk : d.E;
       if (one_seed) {
-        constexpr int NQ1 = C::SECOND ? C::MD : 0;
-        const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * (2 * C::M + NQ1);
+        const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * EndJac<C>::items(1);
         k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, kb, ke);
       } else {
         const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * IPS;
