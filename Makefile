@@ -43,3 +43,10 @@ clean:
 	rm -rf build $(PKG)/*.so oracle/*.so
 
 .PHONY: all clean ref
+
+# Variant build for A/B timing (bench.py with LDG_B200_LIB=build/var/$(VAR)/liblinedg_b200.so):
+#   make variant VAR=name VFLAGS="-DLDG_JT_SMALL=128 -DLDG_JT_MINB=6"
+variant:
+	@mkdir -p build/var/$(VAR)/obj
+	for f in $(CU_SRCS); do $(NVCC) $(NVFLAGS) $(VFLAGS) -c $$f -o build/var/$(VAR)/obj/$$(basename $$f .cu).o & done; wait
+	$(NVCC) $(ARCH) -shared -o build/var/$(VAR)/liblinedg_b200.so build/var/$(VAR)/obj/*.o -lcudart

@@ -97,6 +97,8 @@ class LhLatticeParams(C.Structure):
 
 def _load(name: str) -> C.CDLL:
     path = os.path.join(_HERE, name)
+    if name == "liblinedg_b200.so" and os.environ.get("LDG_B200_LIB"):
+        path = os.environ["LDG_B200_LIB"]  # A/B experiments with a variant build
     if not os.path.exists(path):
         raise RuntimeError(
             f"{name} is not built ({path}); run `make -j` or __graft_entry__.build() first")

@@ -67,7 +67,11 @@ struct ldg_ctx {
   std::vector<double> phi, dq, mi, cc;
   std::vector<int32_t> order, inv_order;
   std::vector<int2> conn;
+  std::vector<int2> fpart;       // [k][2D] face partner {k', 2 dir' + side'} or {-1, 0}
+  std::vector<int64_t> owned_off;  // per Jacobian chunk, into d_owned
   // device
+  int2* d_fpart = nullptr;
+  int32_t* d_owned = nullptr;
   int32_t* d_order = nullptr;
   double* d_metric = nullptr;
   int2* d_conn = nullptr;
@@ -101,6 +105,8 @@ struct ldg_ctx {
     cudaFree(d_order);
     cudaFree(d_metric);
     cudaFree(d_conn);
+    cudaFree(d_fpart);
+    cudaFree(d_owned);
     cudaFree(d_bcv);
     cudaFree(d_source);
     cudaFree(d_Q);
@@ -223,6 +229,47 @@ namespace {
 int face_of(int D, int dir, int side) {
   if (D == 2) return dir == 0 ? (side ? 1 : 3) : (side ? 2 : 0);
   return 2 * dir + side;
+}
+
+// Inverse of face_of: reference local face -> 2 dir + side.
+int local_face_ds(int D, int lf) {
+  for (int ds = 0; ds < 2 * D; ++ds)
+    if (face_of(D, ds >> 1, ds & 1) == lf) return ds;
+  return -1;
+}
+
+// Face sharing of the endpoint flux Jacobians: keep a partner link only where
+// it is mutual and (second-order physics) the LDG switch flips across the
+// face; then list, chunk by chunk, the faces whose Jacobians the chunk
+// computes: every face whose partner lies outside the chunk, and of an
+// in-chunk pair the one with the lower (k, ds).
+void build_face_sharing(ldg_ctx& c, int chunk) {
+  const int F = 2 * c.D;
+  for (int k = 0; k < c.E; ++k)
+    for (int ds = 0; ds < F; ++ds) {
+      int2& p = c.fpart[static_cast<size_t>(k) * F + ds];
+      if (p.x < 0) continue;
+      const int2 q = c.fpart[static_cast<size_t>(p.x) * F + p.y];
+      const int s0 = (c.conn[static_cast<size_t>(k) * F + ds].y >> 24) & 1;
+      const int s1 = (c.conn[static_cast<size_t>(p.x) * F + p.y].y >> 24) & 1;
+      if (p.y < 0 || q.x != k || q.y != ds || (c.second && s0 == s1)) p = int2{-1, 0};
+    }
+  std::vector<int32_t> owned;
+  c.owned_off.assign(1, 0);
+  for (int kb = 0; kb < c.E; kb += chunk) {
+    const int ke = std::min(c.E, kb + chunk);
+    for (int k = kb; k < ke; ++k)
+      for (int ds = 0; ds < F; ++ds) {
+        const int2 p = c.fpart[static_cast<size_t>(k) * F + ds];
+        const bool mine = p.x < kb || p.x >= ke || static_cast<int64_t>(k) * F + ds < static_cast<int64_t>(p.x) * F + p.y;
+        if (mine) owned.push_back(k * F + ds);
+      }
+    c.owned_off.push_back(static_cast<int64_t>(owned.size()));
+  }
+  ck(cudaMalloc(&c.d_fpart, c.fpart.size() * sizeof(int2)), "cudaMalloc fpart");
+  ck(cudaMemcpy(c.d_fpart, c.fpart.data(), c.fpart.size() * sizeof(int2), cudaMemcpyHostToDevice), "upload fpart");
+  ck(cudaMalloc(&c.d_owned, std::max<size_t>(1, owned.size()) * sizeof(int32_t)), "cudaMalloc owned");
+  ck(cudaMemcpy(c.d_owned, owned.data(), owned.size() * sizeof(int32_t), cudaMemcpyHostToDevice), "upload owned");
 }
 
 // 2-D reference face parameterisation (mesh.cpp:51-65).
@@ -371,6 +418,7 @@ void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   if (bcv.empty()) bcv.push_back(0.0);
   const int F = 2 * c.D, P = c.p;
   c.conn.assign(static_cast<size_t>(c.E) * c.D * 2, int2{0, 0});
+  c.fpart.assign(static_cast<size_t>(c.E) * c.D * 2, int2{-1, 0});
   for (int k = 0; k < c.E; ++k) {
     const int e = c.order[k];
     for (int dir = 0; dir < c.D; ++dir) {
@@ -432,6 +480,7 @@ void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
           throw ldg_error(LDG_ERR_CONFIG, "face node map out of packing range");
         out.x = oe;
         out.y = (f00 & 0xff) | ((c1 & 0xff) << 8) | ((c2 & 0xff) << 16) | flag;
+        c.fpart[(static_cast<size_t>(k) * c.D + dir) * 2 + side] = int2{c.inv_order[oe], local_face_ds(c.D, olf)};
       }
     }
   }
@@ -593,6 +642,15 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     d.source = nullptr;
     d.err = c->d_err;
     d.E = c->E;
+    {
+      const char* fs = std::getenv("LDG_FACE_SHARE");
+      if (!(fs && std::string(fs) == "0")) {
+        build_face_sharing(*c, o.chunk_elems(c->E));
+        d.fpart = c->d_fpart;
+        d.owned = c->d_owned;
+        d.owned_off = c->owned_off.data();
+      }
+    }
     d.launches = &c->launches;
     *out = c.release();
     return LDG_OK;

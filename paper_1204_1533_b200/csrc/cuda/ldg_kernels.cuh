@@ -34,6 +34,8 @@ struct KParams {
   const double* bcv;     // [nbc][M]
   const double* source;  // reference numbering, may be null
   DevError* err;
+  const int2* fpart;     // [k][2D] face partner {k', 2 dir' + side'} ({-1, 0}: none)
+  const int32_t* owned;  // owned faces (k*2D + ds) of the Jacobian chunks, or null
   int E;                 // elements
   int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2 stores
 };
@@ -1471,21 +1473,28 @@ struct SeTile {
 template <class C, int SEEDS>
 __global__ void __launch_bounds__(128)
 k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-         double* __restrict__ SE, int k_begin, int k_end) {
+         double* __restrict__ SE, int k_begin, int k_end, long long o_begin, long long o_end) {
   constexpr int NP = C::NP, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD, P = C::P,
                 B11 = C::B11;
   using EJ = EndJac<C>;
   constexpr int NSP = (M + SEEDS - 1) / SEEDS;         // u-seed groups per pass
   constexpr int IPS = EJ::items(SEEDS);                 // items per line end
+  // Items: (face, pass item, line), lines fastest.  A face is an element's
+  // local face ds = 2 dir + side; with face sharing (kp.owned) only the faces
+  // this chunk owns are visited and the result is also written, negated with
+  // in/out swapped, into the partner's line end: the numerical flux is
+  // conservative, Fh(u_o, u_i, -n) = -Fh(u_i, u_o, n) (Riemann, LDG switch
+  // (S flips across a face) and penalty terms alike).
+  constexpr int LS = EJ::LS;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nitems = static_cast<int64_t>(k_end - k_begin) * 2 * D * NL * IPS;
-  if (item >= nitems) return;
-  constexpr int NLE = EJ::NLE, LS = EJ::LS;
-  const int gs = static_cast<int>(item % NLE);
-  const int64_t rest = item / NLE;
+  if (item >= (o_end - o_begin) * NL * IPS) return;
+  const int line = static_cast<int>(item % NL);
+  const int64_t rest = item / NL;
   const int sub = static_cast<int>(rest % IPS);
-  const int k = k_begin + static_cast<int>(rest / IPS);
-  const int ds = gs / NL, line = gs - ds * NL, dir = ds >> 1, side = ds & 1;
+  const int64_t fi = rest / IPS;
+  const int fc = kp.owned ? __ldg(kp.owned + o_begin + fi) : static_cast<int>(k_begin * 2 * D + fi);
+  const int k = fc / (2 * D), ds = fc - k * 2 * D, dir = ds >> 1, side = ds & 1;
+  const int gs = ds * NL + line;
   const size_t e = kp.order[k];
   const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
   const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
@@ -1493,6 +1502,20 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const int S = conn_sign(cn.y);
   const int nd = node_on_line<C>(dir, line, side ? P : 0);
   double* slot = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM + gs;  // entry o at slot[o * LS]
+  // partner line end (same chunk only): pass 0 <-> pass 1, all entries negated
+  double* pslot = nullptr;
+  if (kp.owned && !bd) {
+    const int2 fp = __ldg(&kp.fpart[static_cast<size_t>(k) * 2 * D + ds]);
+    if (fp.x >= k_begin && fp.x < k_end) {
+      int pl, ppos;
+      line_of<C>(fp.y >> 1, conn_node(cn.y, line, NP), pl, ppos);
+      pslot = SE + static_cast<size_t>(fp.x - k_begin) * EJ::PER_ELEM + fp.y * NL + pl;
+    }
+  }
+  auto put = [&](int ps, int o, double v) {
+    slot[(ps * B11 + o) * LS] = v;
+    if (pslot) pslot[((ps == 2 ? 2 : 1 - ps) * B11 + o) * LS] = -v;
+  };
   int pass, g0;
   if (sub < NSP) {
     pass = 0;
@@ -1528,7 +1551,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       for (int j = 0; j < SEEDS; ++j)
         if (g0 + j < M)
 #pragma unroll
-          for (int c = 0; c < M; ++c) slot[(B11 + c * M + g0 + j) * LS] = 0.0;
+          for (int c = 0; c < M; ++c) slot[(B11 + c * M + g0 + j) * LS] = 0.0;  // boundary: no partner
       return;
     }
     double qiv[C::SECOND ? MD : 1], qov[C::SECOND ? MD : 1];
@@ -1546,7 +1569,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     if (LLFC) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Ji, ok);
     if (LLFC && !C::SECOND) {
 #pragma unroll
-      for (int c = 0; c < (LLFC ? M * M : 0); ++c) slot[(pass * B11 + c) * LS] = Ji[c];
+      for (int c = 0; c < (LLFC ? M * M : 0); ++c) put(pass, c, Ji[c]);
     } else
 #pragma unroll
     for (int j = 0; j < SEEDS; ++j) {
@@ -1584,7 +1607,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         }
       }
 #pragma unroll
-      for (int c = 0; c < M; ++c) slot[(pass * B11 + c * M + b) * LS] = fh[c].d[0] + (LLFC ? Ji[(c * M + b) % (LLFC ? M * M : 1)] : 0.0);
+      for (int c = 0; c < M; ++c) put(pass, c * M + b, fh[c].d[0] + (LLFC ? Ji[(c * M + b) % (LLFC ? M * M : 1)] : 0.0));
     }
   } else if (C::SECOND) {
     // dF_vis/dq of the switch-selected side, closed form (visc_dq)
@@ -1595,7 +1618,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     double L[M * MD];
     visc_dq<D, C::PH>(usrc, n, kp.pp, L, ok);
 #pragma unroll
-    for (int c = 0; c < M * MD; ++c) slot[(2 * B11 + c) * LS] = L[c];
+    for (int c = 0; c < M * MD; ++c) put(2, c, L[c]);
   }
   if (!ok) {
     // a non-physical state at this line end: report the offending nodal state
@@ -1634,8 +1657,21 @@ template <class C>
 struct JacThreads {
   static constexpr bool big = C::D == 3 && C::WU == 0;  // 3-D element work unit: many lines
   static constexpr int rows = (C::NPE * C::M + 31) / 32 * 32;  // jac_k11_rows3 items
-  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : 128;
-  static constexpr int min_blocks = big ? 1 : 4;
+  // other work units: one phase-2 item (tile line, a, b) per thread when that
+  // is 129..256 threads (no tail round behind the barrier), else 128
+  static constexpr int p2 = (TileLines<C>::NLT * C::B11 + 31) / 32 * 32;
+#ifndef LDG_JT_SMALL  // tuning knobs (variant builds): CTA size / min CTAs per SM
+  // (measured: second-order tiles gain from it, the Euler tile does not)
+  static constexpr int small = C::SECOND && p2 > 128 && p2 <= 256 ? p2 : 128;
+#else
+  static constexpr int small = LDG_JT_SMALL;
+#endif
+  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : small;
+#ifndef LDG_JT_MINB
+  static constexpr int min_blocks = big ? 1 : (small > 128 ? 65536 / (small * 128) : 4);
+#else
+  static constexpr int min_blocks = big ? 1 : LDG_JT_MINB;
+#endif
 };
 
 template <class C>

@@ -27,6 +27,10 @@ struct DevCtx {
   const double* bcv = nullptr;
   const double* source = nullptr;
   DevError* err = nullptr;
+  // face sharing of the endpoint flux Jacobians (null = every line end computes its own)
+  const int2* fpart = nullptr;        // [k][2D]: partner {k', 2 dir' + side'} or {-1, 0}
+  const int32_t* owned = nullptr;     // owned faces k*2D + ds, chunk by chunk
+  const int64_t* owned_off = nullptr; // host: chunk c owns owned[owned_off[c] .. owned_off[c+1])
   int E = 0;
   long long* launches = nullptr;
 };
@@ -36,6 +40,7 @@ struct Ops {
   size_t jac_smem;
   size_t endjac_per_elem;  // doubles of endpoint-Jacobian scratch per element
   size_t (*scratch_elems)(int E);  // doubles of scratch for E elements (chunked)
+  int (*chunk_elems)(int E);       // elements per Jacobian assembly chunk
   cudaError_t (*residual)(const DevCtx&, const double* U, const double* Q, double* R);
   cudaError_t (*gradient)(const DevCtx&, const double* U, double* Q);
   cudaError_t (*jacobian)(const DevCtx&, const double* U, const double* Q, double* SE, double* K11,
@@ -66,6 +71,8 @@ struct Launch {
     kp.bcv = d.bcv;
     kp.source = d.source;
     kp.err = d.err;
+    kp.fpart = d.fpart;
+    kp.owned = d.owned;
     kp.E = d.E;
     static const int dbg = std::getenv("LDG_DEBUG_MASK") ? std::atoi(std::getenv("LDG_DEBUG_MASK")) : 0;
     kp.dbg = dbg;
@@ -194,7 +201,11 @@ struct Launch {
     return cudaGetLastError();
   }
   static constexpr size_t jac_smem() { return sizeof(double) * JacSmem<C>::TOTAL; }
+#ifndef LDG_EJ_SEEDS
   static constexpr int EJ_SEEDS = C::M;  // seeds per k_endjac thread (primal shared)
+#else
+  static constexpr int EJ_SEEDS = LDG_EJ_SEEDS < C::M ? LDG_EJ_SEEDS : C::M;  // tuning knob
+#endif
   // Elements per assembly chunk: the endpoint-Jacobian scratch of one chunk
   // stays within ~48 MB, so it is produced and consumed while L2-resident.
   static int chunk_elems(int E) {
@@ -227,15 +238,20 @@ struct Launch {
       grid_max = (per_sm > 0 ? per_sm : 1) * sms;
     }
     const int chunk = chunk_elems(d.E);
-    for (int kb = 0; kb < d.E; kb += chunk) {
+    for (int kb = 0, ci = 0; kb < d.E; kb += chunk, ++ci) {
       const int ke = kb + chunk < d.E ? kb + chunk : d.E;
+      // faces whose endpoint Jacobians this chunk computes
+      const long long ob = d.owned ? d.owned_off[ci] : 0;
+      const long long oe = d.owned ? d.owned_off[ci + 1] : static_cast<long long>(ke - kb) * 2 * C::D;
+      const long long nf = oe - ob;
       if (one_seed) {
-        const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * EndJac<C>::items(1);
-        k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, kb, ke);
+        const long long items = nf * C::NL * EndJac<C>::items(1);
+        k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, kb, ke,
+                                                                                  ob, oe);
       } else {
-        const long long items = static_cast<long long>(ke - kb) * 2 * C::D * C::NL * IPS;
+        const long long items = nf * C::NL * IPS;
         k_endjac<C, EJ_SEEDS><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE,
-                                                                                         kb, ke);
+                                                                                         kb, ke, ob, oe);
       }
       count(d);
       if (JacP<C>::OK && !simple) {
@@ -294,7 +310,7 @@ struct Launch {
   static const Ops* table() {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
-                            C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, residual, gradient, jacobian, k21,
+                            C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, chunk_elems, residual, gradient, jacobian, k21,
                             spmv11, spmv12, spmv21, split};
     return &ops;
   }
