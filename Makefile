@@ -50,3 +50,4 @@ variant:
 	@mkdir -p build/var/$(VAR)/obj
 	for f in $(CU_SRCS); do $(NVCC) $(NVFLAGS) $(VFLAGS) -c $$f -o build/var/$(VAR)/obj/$$(basename $$f .cu).o & done; wait
 	$(NVCC) $(ARCH) -shared -o build/var/$(VAR)/liblinedg_b200.so build/var/$(VAR)/obj/*.o -lcudart
+	rm -rf build/var/$(VAR)/obj

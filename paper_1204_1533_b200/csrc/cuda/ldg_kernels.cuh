@@ -639,9 +639,14 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
     unsigned bytes = nb * (NPE * M * 8) + nb * C::METP * 8 + nb * D * 2 * 8;
     if (C::SECOND) bytes += nb * (NPE * MD * 8);
+    int ev_[EPB];
+#pragma unroll
+    for (int le = 0; le < EPB; ++le) ev_[le] = le < nb ? __ldg(kp.order + k0 + le) : 0;
     mbar_expect_tx(&bar[bi], bytes);
-    for (int le = 0; le < nb; ++le) {
-      const size_t e = __ldg(kp.order + k0 + le);
+#pragma unroll
+    for (int le = 0; le < EPB; ++le) {
+      if (le >= nb) break;
+      const size_t e = static_cast<size_t>(ev_[le]);
       tma_load_1d(bU(bi) + le * NPE * M, U + e * (NPE * M), NPE * M * 8, &bar[bi]);
       if (C::SECOND) tma_load_1d(bQ(bi) + le * NPE * MD, Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
     }
@@ -894,9 +899,16 @@ struct BatchIO {
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
     unsigned bytes = nb * (NPE * M * 8) + nb * C::METP * 8 + nb * D * 2 * 8;
     if (WQ) bytes += nb * (NPE * MD * 8);
+    // element ids first: the bulk copies are asm volatile with a memory
+    // clobber, so a load between them would wait out its full latency
+    int ev_[EPB];
+#pragma unroll
+    for (int le = 0; le < EPB; ++le) ev_[le] = le < nb ? __ldg(kp.order + k0 + le) : 0;
     mbar_expect_tx(&bar[bi], bytes);
-    for (int le = 0; le < nb; ++le) {
-      const size_t e = __ldg(kp.order + k0 + le);
+#pragma unroll
+    for (int le = 0; le < EPB; ++le) {
+      if (le >= nb) break;
+      const size_t e = static_cast<size_t>(ev_[le]);
       tma_load_1d(bU(bi) + le * NPE * M, Ug + e * (NPE * M), NPE * M * 8, &bar[bi]);
       if (WQ) tma_load_1d(bQ(bi) + le * NPE * MD, Qg + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
     }
@@ -1691,6 +1703,11 @@ struct JacSmem {
   static constexpr int TOTAL = U + Q + SEC + WORK;
 };
 
+#ifndef LDG_P2_UNROLL  // tuning knob: unroll of the phase-2 row loop (0 = full)
+#define LDG_P2_UNROLL 0
+#endif
+constexpr int P2_UNROLL_K = LDG_P2_UNROLL;
+
 template <class C>
 __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
   constexpr int NP = C::NP;
@@ -1820,6 +1837,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
                 B11 = C::B11;
   using SM = JacSmem<C>;
   constexpr int NLT = SM::NLT, LS = EIdx::LS;
+  constexpr int P2_UNROLL = P2_UNROLL_K > 0 ? P2_UNROLL_K : NP;
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
   if (C::HAS_INV && !(kp.dbg & 1)) {
@@ -1952,7 +1970,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 1) * NT * B11] = c1.x >= 0 ? sc * (kp.bt.mi[i][1] * eo1) : 0.0;
     };
     if (full) {
-#pragma unroll
+#pragma unroll P2_UNROLL
       for (int i = 0; i < NP; ++i) body(i);
     } else {
       body(TileLines<C>::prow(dir, s));
