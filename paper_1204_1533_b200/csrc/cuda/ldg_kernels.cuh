@@ -37,7 +37,7 @@ struct KParams {
   const int2* fpart;     // [k][2D] face partner {k', 2 dir' + side'} ({-1, 0}: none)
   const int32_t* owned;  // owned faces (k*2D + ds) of the Jacobian chunks, or null
   int E;                 // elements
-  int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2 stores
+  int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2, bit2 skip the staged bulk store
 };
 
 // ---------------------------------------------------------------- helpers
@@ -1696,7 +1696,10 @@ struct JacSmem {
   static constexpr int BQ = C::SECOND ? NLT * C::NQ * C::M * C::MD : 0;  // dFvis/dq . nvec
   static constexpr int SEC = ((2 * NLT) | 1) * EndJac<C>::SLOT;  // endpoint flux Jacobians (tile lines)
   static constexpr int TABD = (C::NP * C::NQ + 2 * C::NP + 1) / 2 * 2;  // cc diagonal + M^-1 columns
-  static constexpr int TAB = TABD + ((C::D == 3 && C::WU == 0) ? C::NP * C::NP * C::NQ : 0);  // + full cc
+  // + full cc[i][t][q] + phi[t][q]: the assembly reads its basis coefficients
+  // from shared memory (constant-bank operands are hoisted into registers by
+  // the compiler and spill)
+  static constexpr int TAB = TABD + C::NP * C::NP * C::NQ + C::NP * C::NQ;
   static constexpr int ST11 = C::NS11 * C::B11 * C::NT;       // store doubles per tile
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
   static constexpr int WORK = A + AV + BQ + TAB;
@@ -1707,6 +1710,14 @@ struct JacSmem {
 #define LDG_P2_UNROLL 0
 #endif
 constexpr int P2_UNROLL_K = LDG_P2_UNROLL;
+#ifndef LDG_P2_ROWS  // tuning knob: 2-D phase 2 with one row per item (1) or one line per item (0);
+#define LDG_P2_ROWS 0  // measured: per-line items are faster (C2 0.264 vs 0.297 ms)
+#endif
+constexpr bool P2_ROWS = LDG_P2_ROWS != 0;
+#ifndef LDG_JAC_SMEMTAB  // tuning knob: assembly basis coefficients from shared memory (1) or the constant
+#define LDG_JAC_SMEMTAB 0  // bank (0); measured: the constant bank wins (C2 0.266 vs 0.311 ms) despite its spills
+#endif
+constexpr bool JAC_SMEMTAB = LDG_JAC_SMEMTAB != 0;
 
 template <class C>
 __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
@@ -1837,7 +1848,15 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
                 B11 = C::B11;
   using SM = JacSmem<C>;
   constexpr int NLT = SM::NLT, LS = EIdx::LS;
-  constexpr int P2_UNROLL = P2_UNROLL_K > 0 ? P2_UNROLL_K : NP;
+  // measured: second-order tiles (phase 3 follows, more live state) prefer
+  // the rolled row loop, the Euler tile the unrolled one
+  constexpr int P2_UNROLL = P2_UNROLL_K > 0 ? P2_UNROLL_K : (C::SECOND ? 1 : NP);
+  const double* const tcc = stab + SM::TABD;                  // cc[i][t][q]
+  const double* const tphi = tcc + NP * NP * NQ;               // phi[t][q]
+  const double* const tmi = stab + NP * NQ;                    // mi[i][side]
+  auto CC = [&](int i, int t, int q) { return JAC_SMEMTAB ? tcc[(i * NP + t) * NQ + q] : kp.bt.cc[i][t][q]; };
+  auto MI = [&](int i, int sd) { return JAC_SMEMTAB ? tmi[i * 2 + sd] : kp.bt.mi[i][sd]; };
+  auto PHI = [&](int t, int q) { return JAC_SMEMTAB ? tphi[t * NQ + q] : kp.bt.phi[t][q]; };
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
   if (C::HAS_INV && !(kp.dbg & 1)) {
@@ -1853,7 +1872,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         const int nd = node_on_line<C>(dir, line, t);
-        const double ph = kp.bt.phi[t][q];
+        const double ph = PHI(t, q);
 #pragma unroll
         for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
       }
@@ -1880,7 +1899,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         const int nd = node_on_line<C>(dir, line, t);
-        const double ph = kp.bt.phi[t][q];
+        const double ph = PHI(t, q);
 #pragma unroll
         for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
 #pragma unroll
@@ -1920,11 +1939,11 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   auto avq = [&](int tl, int q, int ab) {
     return (C::HAS_INV ? sA[(tl * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? sAv[(tl * NQ + q) * B11 + ab] : 0.0);
   };
-  for (int w = ((kp.dbg & 2) || (C::D == 3 && C::WU == 0)) ? NLT * B11 : tid; w < NLT * B11; w += nthr) {
-    const int tl = w / B11, ab = w - tl * B11;
+  // one (tile line, block entry ab): setup shared by the rows of the line,
+  // then rows(body, full) runs body(i) for the rows this item owns
+  auto line_item = [&](const int tl, const int ab, auto&& rows) {
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
-    const bool full = TileLines<C>::full(dir);
     double av[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(tl, q, ab) : 0.0;
@@ -1945,10 +1964,10 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
         double v = 0.0;
         if (VOL11) {
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * av[q];
+          for (int q = 0; q < NQ; ++q) v += CC(i, t, q) * av[q];
         }
-        if (t == 0) v += kp.bt.mi[i][0] * ein0;
-        if (t == P) v += kp.bt.mi[i][1] * ein1;
+        if (t == 0) v += MI(i, 0) * ein0;
+        if (t == P) v += MI(i, 1) * ein1;
         if (t == i) {
           // self block: add the lines of the other directions through this node
 #pragma unroll
@@ -1966,14 +1985,32 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
         }
         rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B11] = sc * v;
       }
-      rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 0) * NT * B11] = c0.x >= 0 ? sc * (kp.bt.mi[i][0] * eo0) : 0.0;
-      rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 1) * NT * B11] = c1.x >= 0 ? sc * (kp.bt.mi[i][1] * eo1) : 0.0;
+      rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 0) * NT * B11] = c0.x >= 0 ? sc * (MI(i, 0) * eo0) : 0.0;
+      rowp[static_cast<size_t>(C::D * P + 1 + 2 * dir + 1) * NT * B11] = c1.x >= 0 ? sc * (MI(i, 1) * eo1) : 0.0;
     };
-    if (full) {
+    rows(body, TileLines<C>::full(dir), dir);
+  };
+  if (C::D == 2 && P2_ROWS) {
+    // 2-D (every line full): one item per (row position i, tile line, ab),
+    // i outermost -- NP * NLT * B11 items balance over the CTA (the per-line
+    // items leave a tail round), and i is warp-uniform when NLT * B11 is a
+    // multiple of 32, so cc[i][t][q] stays a uniform constant-bank operand
+    constexpr int NI = NLT * B11;
+    for (int w = (kp.dbg & 2) ? NP * NI : tid; w < NP * NI; w += nthr) {
+      const int i = w / NI, rest = w - i * NI, tl = rest / B11, ab = rest - tl * B11;
+      line_item(tl, ab, [&](auto& body, bool, int) { body(i); });
+    }
+  } else {
+    for (int w = ((kp.dbg & 2) || (C::D == 3 && C::WU == 0)) ? NLT * B11 : tid; w < NLT * B11; w += nthr) {
+      const int tl = w / B11, ab = w - tl * B11;
+      line_item(tl, ab, [&](auto& body, bool full, int dir) {
+        if (full) {
 #pragma unroll P2_UNROLL
-      for (int i = 0; i < NP; ++i) body(i);
-    } else {
-      body(TileLines<C>::prow(dir, s));
+          for (int i = 0; i < NP; ++i) body(i);
+        } else {
+          body(TileLines<C>::prow(dir, s));
+        }
+      });
     }
   }
   if (!C::SECOND) return;
@@ -2006,9 +2043,9 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
         if (t == i && dir != 0) continue;
         double v = 0.0;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) v += kp.bt.cc[i][t][q] * bv[q];
-        if (t == 0 && own0) v += kp.bt.mi[i][0] * eq0;
-        if (t == P && own1) v += kp.bt.mi[i][1] * eq1;
+        for (int q = 0; q < NQ; ++q) v += CC(i, t, q) * bv[q];
+        if (t == 0 && own0) v += MI(i, 0) * eq0;
+        if (t == P && own1) v += MI(i, 1) * eq1;
         if (t == i) {
 #pragma unroll
           for (int d2 = 1; d2 < D; ++d2) {
@@ -2028,8 +2065,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
         rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B12] = sc * v;
       }
       double nbv = 0.0;
-      if (!own0) nbv = sc * (kp.bt.mi[i][0] * eq0);
-      if (!own1) nbv = sc * (kp.bt.mi[i][1] * eq1);
+      if (!own0) nbv = sc * (MI(i, 0) * eq0);
+      if (!own1) nbv = sc * (MI(i, 1) * eq1);
       rowp[static_cast<size_t>(C::D * P + 1 + dir) * NT * B12] = nbv;
     };
     if (full) {
@@ -2049,8 +2086,8 @@ __device__ __forceinline__ void fill_tab(const KParams<C>& kp, double* stab, int
     stab[i] = kp.bt.cc[p][p][q];
   }
   for (int i = tid; i < 2 * NP; i += nthr) stab[NP * NQ + i] = (&kp.bt.mi[0][0])[i];
-  if (C::D == 3 && C::WU == 0)
-    for (int i = tid; i < NP * NP * NQ; i += nthr) stab[JacSmem<C>::TABD + i] = (&kp.bt.cc[0][0][0])[i];
+  for (int i = tid; i < NP * NP * NQ; i += nthr) stab[JacSmem<C>::TABD + i] = (&kp.bt.cc[0][0][0])[i];
+  for (int i = tid; i < NP * NQ; i += nthr) stab[JacSmem<C>::TABD + NP * NP * NQ + i] = (&kp.bt.phi[0][0])[i];
 }
 
 template <class C>
@@ -2110,11 +2147,21 @@ struct JacP {
   static constexpr int SE = ev(EndJac<C>::PER_ELEM);
   static constexpr int BUF = U + Q + MET + CONN + SE;
   using SM = JacSmem<C>;
-  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK); }
+  // 2-D: the element's K11 tile is formed in shared memory and leaves with one
+  // TMA bulk store (sequential write stream, no per-entry global stores)
+#ifndef LDG_JAC_STAGE
+#define LDG_JAC_STAGE 1
+#endif
+  // (measured: a small gain for the Euler tile, a loss for second-order
+  // tiles whose larger footprint costs occupancy)
+  static constexpr bool STAGE = LDG_JAC_STAGE && C::D == 2 && !C::SECOND && (SM::ST11 % 2 == 0) &&
+                                8LL * SM::ST11 <= 64 * 1024;
+  static constexpr int STG = STAGE ? SM::ST11 : 0;
+  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + STG); }
   // prefetch ring depth: 3 for the one-CTA-per-SM 3-D element units (when it
   // fits), 2 where several CTAs share an SM
   static constexpr int NBUF = (JacThreads<C>::big && bytes(3) <= 200 * 1024) ? 3 : 2;
-  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK;  // 4 doubles hold up to 3 mbarriers
+  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + STG;  // 4 doubles hold up to 3 mbarriers
   static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
                              (EndJac<C>::PER_ELEM % 2 == 0) && bytes(2) <= 200 * 1024;
 };
@@ -2136,6 +2183,7 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
   double* stab = sBq + SM::BQ;
+  double* sstage = work + SM::WORK;  // K11 tile staging (JP::STAGE)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = gridDim.x;
   if (k_begin + static_cast<int>(blockIdx.x) >= k_end) return;
@@ -2168,13 +2216,25 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   for (int k = k0, it = 0; k < k_end; k += G, ++it) {
     const int cur = it % NB;
     mbar_wait(&bar[cur], (it / NB) & 1);
+    // staging free again: the previous tile's bulk store has read it (waited
+    // here by its issuer; jac_tile's barrier before phase 2 publishes it)
+    if (JP::STAGE && tid == 0 && it > 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     const size_t e = kp.order[k];
+    double* const K11g = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11;
     jac_tile<C>(kp, k, 0, e, bU(cur), bQ(cur), bMET(cur), bCONN(cur), bSE(cur), SeFull<C>(), sA, sAv, sBq, stab,
-                K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
+                JP::STAGE ? sstage : K11g,
                 C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
-    __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done
+    if (JP::STAGE) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done; tile staged
+    if (JP::STAGE && tid == 0 && !(kp.dbg & 4)) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(K11g),
+                   "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
     if (tid == 0 && k + NB * G < k_end) issue(k + NB * G, cur);
   }
+  if (JP::STAGE && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // K21 = dQ/dU (U-independent; D scalars per node pair), same tiles/rows.
