@@ -329,6 +329,8 @@ def main():
     # ---- end to end through the host-buffer C-ABI (pinned host memory)
     Uh = torch.from_numpy(U).pin_memory().numpy()
     xh = torch.from_numpy(x).pin_memory().numpy()
+    Rh = torch.empty(U.size, dtype=torch.float64).pin_memory().numpy()  # pinned result buffers
+    yh = torch.empty(x.size, dtype=torch.float64).pin_memory().numpy()
     ctx.set_sync_errors(True)
     e2e_times = []
     torch.cuda.set_stream(stream)
@@ -339,9 +341,9 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        ctx.residual(Uh)
+        ctx.residual(Uh, out=Rh)
         ctx.assemble_jacobians(Uh)
-        ctx.spmv(LDG_K11, xh)
+        ctx.spmv(LDG_K11, xh, out=yh)
         t1.record(stream)
         torch.cuda.synchronize()
         if k >= args.warmup:

@@ -153,12 +153,22 @@ class LineDG:
         self._check(self.lib.ldg_set_source(self._h, dptr(a)))
 
     # ------------------------------------------------------------ residuals
-    def residual(self, U, t: float = 0.0, Q_out=None):
+    @staticmethod
+    def _host_out(out, n):
+        """Result array of a host-path call: `out` (e.g. pinned memory, so the
+        device-to-host copy runs at full PCIe speed) or a new array."""
+        if out is None:
+            return np.empty(n)
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous and out.size == n):
+            raise ValueError(f"out must be a contiguous float64 array of {n} entries")
+        return out
+
+    def residual(self, U, t: float = 0.0, Q_out=None, out=None):
         """dU/dt = R(U, D(U)) (first-order physics: R(U)).  Device tensors in,
-        device tensor out; numpy in -> numpy out (host path)."""
+        device tensor out; numpy in -> numpy out (host path, into `out` if given)."""
         if not _is_torch(U):
             Uh = np.ascontiguousarray(U, dtype=np.float64)
-            R = np.empty(self.n_dofs)
+            R = self._host_out(out, self.n_dofs)
             Qh = np.empty(self.n_dofs * self.dim) if (Q_out is not None and self.second_order) else None
             self._check(self.lib.ldg_residual_host(self._h, dptr(Uh), t, dptr(R), dptr(Qh)))
             if Qh is not None:
@@ -222,11 +232,11 @@ class LineDG:
             vals = vals.reshape(nnzb, info.block_rows, info.block_cols)
         return rows, cols, vals
 
-    def spmv(self, which: int, x):
+    def spmv(self, which: int, x, out=None):
         if not _is_torch(x):
             xh = np.ascontiguousarray(x, dtype=np.float64)
             ny = self.n_dofs * (self.dim if which == _abi.LDG_K21 else 1)
-            y = np.empty(ny)
+            y = self._host_out(out, ny)
             self._check(self.lib.ldg_bsr_spmv_host(self._h, which, dptr(xh), dptr(y)))
             return y
         x = self._as_dev(x)
@@ -235,11 +245,11 @@ class LineDG:
         self._check(self.lib.ldg_bsr_spmv(self._h, which, self._ptr(x), self._ptr(y)))
         return y
 
-    def split_matvec(self, alpha_dt: float, v):
+    def split_matvec(self, alpha_dt: float, v, out=None):
         """(I - alpha_dt (K11 + K12 K21)) v without forming the product."""
         if not _is_torch(v):
             vh = np.ascontiguousarray(v, dtype=np.float64)
-            y = np.empty(self.n_dofs)
+            y = self._host_out(out, self.n_dofs)
             self._check(self.lib.ldg_split_matvec_host(self._h, alpha_dt, dptr(vh), dptr(y)))
             return y
         v = self._as_dev(v)

@@ -72,6 +72,20 @@ def test_residual_host_path(setup):
     R_ref = ora.residual(U)
     R = gpu.residual(U)  # numpy in -> host path through the C-ABI
     assert rel(R, R_ref) <= TOL
+    # into a caller-provided pinned buffer (bench.py's end-to-end leg)
+    Rp = torch.empty(R.size, dtype=torch.float64).pin_memory().numpy()
+    assert gpu.residual(U, out=Rp) is Rp
+    assert np.array_equal(Rp, R)
+    # host-path Jacobian + SpMV / split matvec into pinned buffers
+    gpu.assemble_jacobians(U)
+    ora.assemble(U)
+    x = case.normal_vector(gpu.m, cfg.vector_seed)
+    yp = torch.empty(x.size, dtype=torch.float64).pin_memory().numpy()
+    assert gpu.spmv(LDG_K11, x, out=yp) is yp
+    assert rel(yp, ora.spmv(LDG_K11, x)) <= TOL
+    assert rel(gpu.split_matvec(0.37, x, out=yp), ora.split_matvec(0.37, x)) <= TOL
+    with pytest.raises(ValueError):
+        gpu.residual(U, out=np.empty(3))
 
 
 def test_gradient_and_second_order(setup):
