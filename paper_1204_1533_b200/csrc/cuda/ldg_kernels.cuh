@@ -1440,6 +1440,21 @@ struct TileLines {
     if (C::WU == 1) return s;
     return dir == 1 ? s % C::NP : s / C::NP;
   }
+  // Row items of a slab / line unit: the full lines come first (NFULL of
+  // them, every row), then one row of each transverse line; rr -> (tl, i).
+  static constexpr int NFULL = C::WU == 1 ? 2 * C::NP : 1;
+  static constexpr int NROWS = NFULL * C::NP + (NLT - NFULL);
+  __device__ static __forceinline__ void row_item(int rr, int s, int& tl, int& i) {
+    if (rr < NFULL * C::NP) {
+      tl = rr / C::NP;
+      i = rr - tl * C::NP;
+    } else {
+      tl = NFULL + rr - NFULL * C::NP;
+      int dir, line;
+      get(tl, s, dir, line);
+      i = prow(dir, s);
+    }
+  }
 };
 
 // Endpoint flux Jacobians of every element line end, into a per-element
@@ -1678,9 +1693,15 @@ struct JacThreads {
 #else
   static constexpr int small = LDG_JT_SMALL;
 #endif
-  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : small;
+  // 3-D slab / line work units (one CTA per unit, shared memory for one CTA
+  // per SM): as many warps as the 128-register cap allows
+#ifndef LDG_JT_UNIT3
+#define LDG_JT_UNIT3 512
+#endif
+  static constexpr bool unit3 = C::D == 3 && C::WU != 0;
+  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : (unit3 ? LDG_JT_UNIT3 : small);
 #ifndef LDG_JT_MINB
-  static constexpr int min_blocks = big ? 1 : (small > 128 ? 65536 / (small * 128) : 4);
+  static constexpr int min_blocks = big || unit3 ? 1 : (small > 128 ? 65536 / (small * 128) : 4);
 #else
   static constexpr int min_blocks = big ? 1 : LDG_JT_MINB;
 #endif
@@ -1703,7 +1724,8 @@ struct JacSmem {
   static constexpr int ST11 = C::NS11 * C::B11 * C::NT;       // store doubles per tile
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
   static constexpr int WORK = A + AV + BQ + TAB;
-  static constexpr int TOTAL = U + Q + SEC + WORK;
+  static constexpr int MET = (C::METP + 1) / 2 * 2;  // k_jacobian stages the element's metric
+  static constexpr int TOTAL = U + Q + SEC + WORK + MET;
 };
 
 #ifndef LDG_P2_UNROLL  // tuning knob: unroll of the phase-2 row loop (0 = full)
@@ -2000,6 +2022,16 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       const int i = w / NI, rest = w - i * NI, tl = rest / B11, ab = rest - tl * B11;
       line_item(tl, ab, [&](auto& body, bool, int) { body(i); });
     }
+  } else if (C::D == 3 && C::WU != 0) {
+    // slab / line units: one row per item (the full lines' items would carry
+    // NP rows against one for the transverse lines')
+    using TL = TileLines<C>;
+    for (int w = (kp.dbg & 2) ? TL::NROWS * B11 : tid; w < TL::NROWS * B11; w += nthr) {
+      const int rr = w / B11, ab = w - rr * B11;
+      int tl, i;
+      TL::row_item(rr, s, tl, i);
+      line_item(tl, ab, [&](auto& body, bool, int) { body(i); });
+    }
   } else {
     for (int w = ((kp.dbg & 2) || (C::D == 3 && C::WU == 0)) ? NLT * B11 : tid; w < NLT * B11; w += nthr) {
       const int tl = w / B11, ab = w - tl * B11;
@@ -2017,8 +2049,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 
   // ---- phase 3: K12 = dR/dQ (stored rows a' of each block)
   constexpr int B12 = C::B12, A0 = C::PH == PH_NS ? 1 : 0;
-  for (int w = tid; w < NLT * B12; w += nthr) {
-    const int tl = w / B12, ab = w - tl * B12;
+  auto k12_item = [&](const int tl, const int ab, auto&& rows) {
     const int a = ab / MD + A0, b = ab % MD;
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
@@ -2069,11 +2100,27 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       if (!own1) nbv = sc * (MI(i, 1) * eq1);
       rowp[static_cast<size_t>(C::D * P + 1 + dir) * NT * B12] = nbv;
     };
-    if (full) {
+    rows(body, full, dir);
+  };
+  if (C::D == 3 && C::WU != 0) {
+    using TL = TileLines<C>;
+    for (int w = tid; w < TL::NROWS * B12; w += nthr) {
+      const int rr = w / B12, ab = w - rr * B12;
+      int tl, i;
+      TL::row_item(rr, s, tl, i);
+      k12_item(tl, ab, [&](auto& body, bool, int) { body(i); });
+    }
+  } else {
+    for (int w = tid; w < NLT * B12; w += nthr) {
+      const int tl = w / B12, ab = w - tl * B12;
+      k12_item(tl, ab, [&](auto& body, bool full, int dir) {
+        if (full) {
 #pragma unroll
-      for (int i = 0; i < NP; ++i) body(i);
-    } else {
-      body(TileLines<C>::prow(dir, s));
+          for (int i = 0; i < NP; ++i) body(i);
+        } else {
+          body(TileLines<C>::prow(dir, s));
+        }
+      });
     }
   }
 }
@@ -2106,26 +2153,36 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
   double* stab = sBq + SM::BQ;
+  double* smet = stab + SM::TAB;
   const int W = blockIdx.x + k_begin * C::UPE;  // work unit id
   const int k = W / C::UPE, s = W - k * C::UPE;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const size_t e = kp.order[k];
-  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-  // element state (+ gradient), endpoint flux Jacobians of the tile's line
-  // ends (k_endjac scratch of this chunk) in tile-line order, tables
-  cp_elem<C>(su, U + e * (NPE * M), NPE * M, tid, nthr);
-  if (C::SECOND) cp_elem<C>(sq, Q + e * (NPE * MD), NPE * MD, tid, nthr);
+  const double* mk = smet;
+  // element state (+ gradient), metric, endpoint flux Jacobians of the
+  // tile's line ends (k_endjac scratch of this chunk) in tile-line order:
+  // all as asynchronous 8-byte copies, so their latencies overlap
   {
+    const double* ug = U + e * (NPE * M);
+    for (int i = tid; i < NPE * M; i += nthr) cp_async8(su + i, ug + i);
+    if (C::SECOND) {
+      const double* qg = Q + e * (NPE * MD);
+      for (int i = tid; i < NPE * MD; i += nthr) cp_async8(sq + i, qg + i);
+    }
+    const double* mg = kp.metric + static_cast<size_t>(k) * C::METP;
+    for (int i = tid; i < C::METP; i += nthr) cp_async8(smet + i, mg + i);
     const double* se = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM;
     for (int w = tid; w < NLT * 2 * EJ::SLOT; w += nthr) {
       const int o = w / (2 * NLT), idx = w - o * (2 * NLT);
       const int tl = idx >> 1, side = idx & 1;
       int dir, line;
       TileLines<C>::get(tl, s, dir, line);
-      sE[o * SeTile<C>::LS + idx] = __ldg(se + o * EJ::LS + (dir * 2 + side) * NL + line);
+      cp_async8(sE + o * SeTile<C>::LS + idx, se + o * EJ::LS + (dir * 2 + side) * NL + line);
     }
+    cp_async_commit();
   }
   fill_tab<C>(kp, stab, tid, nthr);
+  cp_async_wait_all();
   __shared__ int2 sconn[2 * C::D];
   if (tid < 2 * C::D) sconn[tid] = __ldg(&kp.conn[static_cast<size_t>(k) * C::D * 2 + tid]);
   __syncthreads();
