@@ -515,4 +515,82 @@ __device__ __forceinline__ void visc_dq(const double* u, const double* n, const 
     }
 }
 
+// Closed-form d(F_vis.n)/du at fixed q (row-major M x M), Navier-Stokes.
+// visc_fn is linear in the velocity / energy gradients
+//   gv[i][d] = (q_{1+i,d} - v_i q_{0,d}) / rho,  gE[d] = (q_{D+1,d} - E q_{0,d}) / rho,
+// with T_i(G) = mu sum_j (G_ij + G_ji) n_j - 2/3 mu tr(G) n_i:
+//   F[1+i] = -T_i(gv),  F[D+1] = -(sum_i v_i T_i(gv) + kap sum_j (gE_j - sum_i v_i gv_ij) n_j),
+// so column c follows from (dv, dG, dgE) = d(v, gv, gE)/du_c:
+//   rho:  dv_i = -v_i/rho, dG_ij = (v_i q_0j/rho - gv_ij)/rho, dgE_j = (E q_0j/rho - gE_j)/rho
+//   m_k:  dv_i = delta_ik/rho, dG_ij = -delta_ik q_0j/rho^2, dgE = 0
+//   e:    dv = 0, dG = 0, dgE_j = -q_0j/rho^2.
+// Poisson: F_vis does not depend on u (zero).
+template <int D, int PH>
+__device__ __forceinline__ void visc_du(const double* u, const double* q, const double* n, const PhysParams& pp,
+                                        double* J, bool& ok) {
+  constexpr int M = PH == PH_POISSON ? 1 : D + 2;
+#pragma unroll
+  for (int i = 0; i < M * M; ++i) J[i] = 0.0;
+  if (PH == PH_POISSON) return;
+  const double rho = u[0];
+  ok = ok && (rho > 0.0);
+  const double irho = 1.0 / rho;
+  double v[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) v[i] = u[1 + i] * irho;
+  const double E = u[D + 1] * irho;
+  double gv[D][D], gE[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) gv[i][d] = (q[(1 + i) * D + d] - v[i] * q[d]) * irho;
+    gE[d] = (q[(D + 1) * D + d] - E * q[d]) * irho;
+  }
+  const double mu = pp.mu, kap = pp.kap, c23 = 2.0 / 3.0;
+  auto T = [&](const double (&G)[D][D], double* t) {
+    double tr = G[0][0];
+#pragma unroll
+    for (int k = 1; k < D; ++k) tr += G[k][k];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s += mu * (G[i][j] + G[j][i]) * n[j];
+      t[i] = s - c23 * mu * tr * n[i];
+    }
+  };
+  double tn[D];
+  T(gv, tn);
+  const double ir2 = irho * irho;
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    double dv[D], dG[D][D], dgE[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      dv[i] = c == 0 ? -v[i] * irho : (c == 1 + i ? irho : 0.0);
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        dG[i][j] = c == 0 ? (v[i] * q[j] * irho - gv[i][j]) * irho : (c == 1 + i ? -q[j] * ir2 : 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) dgE[j] = c == 0 ? (E * q[j] * irho - gE[j]) * irho : (c == D + 1 ? -q[j] * ir2 : 0.0);
+    double dtn[D];
+    T(dG, dtn);
+    double den = 0.0, dhn = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      J[(1 + i) * M + c] = -dtn[i];
+      den += dv[i] * tn[i] + v[i] * dtn[i];
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = dgE[j];
+#pragma unroll
+      for (int i = 0; i < D; ++i) s -= dv[i] * gv[i][j] + v[i] * dG[i][j];
+      dhn += s * n[j];
+    }
+    J[(D + 1) * M + c] = -(den + kap * dhn);
+  }
+}
+
 }  // namespace ldg

@@ -40,6 +40,11 @@ struct KParams {
   int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2, bit2 skip the staged bulk store
 };
 
+#ifndef LDG_VISC_DU  // closed-form viscous dF/du (1) or dual numbers (0)
+#define LDG_VISC_DU 1
+#endif
+constexpr bool VISC_DU_CLOSED = LDG_VISC_DU != 0;
+
 // ---------------------------------------------------------------- helpers
 
 template <class C>
@@ -1589,18 +1594,38 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         qov[c] = bd ? 0.0 : __ldg(Q + onb * MD + c);
       }
     }
-    // LLF: closed-form inviscid Jacobian (llf_jac); the seeds then carry
-    // only the viscous terms (second-order physics)
+    // Closed-form parts (all seeds at once): the LLF inviscid Jacobian
+    // (llf_jac) and, second order, the viscous flux of the switch-selected
+    // side (visc_du) plus the C11 penalty; dual-number seeds carry the rest
+    // (the Roe flux).
     constexpr bool LLFC = C::HAS_INV && C::RI != LDG_ROE && SEEDS >= M;
-    double Ji[LLFC ? M * M : 1];
-    if (LLFC) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Ji, ok);
-    if (LLFC && !C::SECOND) {
+    constexpr bool VCF = C::SECOND && VISC_DU_CLOSED && SEEDS >= M;
+    constexpr bool ALLC = (!C::HAS_INV || LLFC) && (!C::SECOND || VCF);
+    double Jx[(LLFC || VCF) ? M * M : 1];
 #pragma unroll
-      for (int c = 0; c < (LLFC ? M * M : 0); ++c) put(pass, c, Ji[c]);
+    for (int c = 0; c < ((LLFC || VCF) ? M * M : 1); ++c) Jx[c] = 0.0;
+    if (LLFC) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Jx, ok);
+    if (VCF) {
+      const bool sel_in = bd || S <= 0;  // the viscous flux is taken from u_in (else u_out)
+      if ((pass == 0) == sel_in) {
+        double Jv[M * M];
+        visc_du<D, C::PH>(sel_in ? uiv : uov, sel_in ? qiv : qov, n, kp.pp, Jv, ok);
+#pragma unroll
+        for (int c = 0; c < M * M; ++c) Jx[c] += Jv[c];
+      }
+      double pen = 0.0;
+      if (bd) pen = pass == 0 ? (kp.pp.c11bd / (D == 2 ? nn : sqrt(nn))) * nn : 0.0;
+      else if (kp.pp.c11 != 0.0) pen = pass == 0 ? kp.pp.c11 * nn : -(kp.pp.c11 * nn);
+#pragma unroll
+      for (int c = 0; c < M; ++c) Jx[c * M + c] += pen;
+    }
+    if (ALLC) {
+#pragma unroll
+      for (int c = 0; c < ((LLFC || VCF) ? M * M : 0); ++c) put(pass, c, Jx[c]);
     } else
 #pragma unroll
     for (int j = 0; j < SEEDS; ++j) {
-      const int b = LLFC ? j : g0 + j;
+      const int b = (LLFC || VCF) ? j : g0 + j;
       if (b >= M) break;
       D1 ui[M], uo[M], fh[M];
 #pragma unroll
@@ -1615,7 +1640,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
         else if (!LLFC) llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
       }
-      if (C::SECOND) {
+      if (C::SECOND && !VCF) {
         D1 fv[M];
         if (bd) {
           visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
@@ -1634,7 +1659,8 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         }
       }
 #pragma unroll
-      for (int c = 0; c < M; ++c) put(pass, c * M + b, fh[c].d[0] + (LLFC ? Ji[(c * M + b) % (LLFC ? M * M : 1)] : 0.0));
+      for (int c = 0; c < M; ++c)
+        put(pass, c * M + b, fh[c].d[0] + ((LLFC || VCF) ? Jx[(c * M + b) % ((LLFC || VCF) ? M * M : 1)] : 0.0));
     }
   } else if (C::SECOND) {
     // dF_vis/dq of the switch-selected side, closed form (visc_dq)
@@ -1906,7 +1932,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   // ---- phase 1c (second-order): viscous flux derivatives at the quadrature
   // points: one item per u-seed (dual numbers) plus one closed-form dF/dq item
   if (C::SECOND && !(kp.dbg & 1)) {
-    constexpr int NSU = C::VIS_U ? M : 0, NSEED = NSU + 1;
+    constexpr int NSU = C::VIS_U ? (VISC_DU_CLOSED ? 1 : M) : 0, NSEED = NSU + 1;
     for (int w = tid; w < NLT * NQ * NSEED; w += nthr) {
       const int sd = w % NSEED, tq = w / NSEED, tl = tq / NQ, q = tq - tl * NQ;
       int dir, line;
@@ -1930,7 +1956,13 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       bool ok = true;
       using D1 = Dual<1>;
       D1 fv[M];
-      if (sd < NSU) {
+      if (sd < NSU && VISC_DU_CLOSED) {
+        double Jv[M * M];
+        visc_du<D, C::PH>(uq, qq, nv, kp.pp, Jv, ok);
+        double* a = sAv + (tl * NQ + q) * B11;
+#pragma unroll
+        for (int c = 0; c < M * M; ++c) a[c] = Jv[c];
+      } else if (sd < NSU) {
         D1 du[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) {
