@@ -596,12 +596,16 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
 // one mbarrier); the scattered neighbour traces of batch i+1 are gathered with
 // cp.async as soon as its connectivity has landed.  Compute is the
 // thread-per-line scheme of k_residual with every operand in shared memory.
+#ifndef LDG_RES_MET_SMEM  // residual: stage the metric in the ring (1) or read it from global (0)
+#define LDG_RES_MET_SMEM 1
+#endif
 template <class C, int EPB>
 struct ResP {
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr bool METS = LDG_RES_MET_SMEM != 0;
   static constexpr int U = ev(EPB * C::NPE * C::M);
   static constexpr int Q = C::SECOND ? ev(EPB * C::NPE * C::MD) : 0;
-  static constexpr int MET = EPB * C::METP;
+  static constexpr int MET = METS ? EPB * C::METP : 0;
   static constexpr int CONN = ev(EPB * C::D * 2);  // int2 entries, 8 B each
   static constexpr int NB = ev(EPB * C::LPE * 2 * C::M);
   static constexpr int NBQ = C::SECOND ? ev(EPB * C::LPE * 2 * C::MD) : 0;
@@ -642,7 +646,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   // bulk loads of one batch into buffer bi (thread 0 issues; TMA path)
   auto issue = [&](int batch, int bi) {
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
-    unsigned bytes = nb * (NPE * M * 8) + nb * C::METP * 8 + nb * D * 2 * 8;
+    unsigned bytes = nb * (NPE * M * 8) + (RP::METS ? nb * C::METP * 8 : 0) + nb * D * 2 * 8;
     if (C::SECOND) bytes += nb * (NPE * MD * 8);
     int ev_[EPB];
 #pragma unroll
@@ -655,7 +659,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
       tma_load_1d(bU(bi) + le * NPE * M, U + e * (NPE * M), NPE * M * 8, &bar[bi]);
       if (C::SECOND) tma_load_1d(bQ(bi) + le * NPE * MD, Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
     }
-    tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k0) * C::METP, nb * C::METP * 8, &bar[bi]);
+    if (RP::METS) tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k0) * C::METP, nb * C::METP * 8, &bar[bi]);
     tma_load_1d(bCONN(bi), kp.conn + static_cast<size_t>(k0) * D * 2, nb * D * 2 * 8, &bar[bi]);
   };
   // synchronous fallback (element chunks not 16-byte aligned)
@@ -667,7 +671,8 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
       if (C::SECOND)
         for (int i = tid; i < NPE * MD; i += nthr) bQ(bi)[le * NPE * MD + i] = __ldg(Q + e * (NPE * MD) + i);
     }
-    for (int i = tid; i < nb * C::METP; i += nthr) bMET(bi)[i] = __ldg(kp.metric + static_cast<size_t>(k0) * C::METP + i);
+    if (RP::METS)
+      for (int i = tid; i < nb * C::METP; i += nthr) bMET(bi)[i] = __ldg(kp.metric + static_cast<size_t>(k0) * C::METP + i);
     for (int i = tid; i < nb * D * 2; i += nthr) bCONN(bi)[i] = __ldg(kp.conn + static_cast<size_t>(k0) * D * 2 + i);
     __syncthreads();
   };
@@ -704,17 +709,19 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     load_sync(b0, 0);
   }
   gather(b0, 0);
+  __shared__ int sord[EPB];  // element ids of the batch (epilogue addresses)
   for (int batch = b0, it = 0; batch < nbatch; batch += G, ++it) {
     const int cur = it & 1, nxt = cur ^ 1;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
     cp_async_wait_all();
     __syncthreads();
+    if (tid < nb) sord[tid] = __ldg(kp.order + k0 + tid);  // lands during the line work
     // ---- lines
     const int le = tid / LPE;
     if (le < nb) {
       const int rem = tid - le * LPE;
       const int dir = rem / NL, line = rem - dir * NL;
-      const double* mk = bMET(cur) + le * C::METP;
+      const double* mk = RP::METS ? bMET(cur) + le * C::METP : kp.metric + static_cast<size_t>(k0 + le) * C::METP;
       const double* nvl = mk + (dir * NL + line) * NQ * D;
       const double* sul = bU(cur) + le * NPE * M;
       const double* sql = bQ(cur) + le * NPE * MD;
@@ -825,12 +832,13 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
       const int l = idx / (NPE * M), off = idx - l * NPE * M;
       const int nd = off / M;
-      const size_t e = kp.order[k0 + l];
+      const size_t e = static_cast<size_t>(sord[l]);
       const double* a = sacc + l * D * NPE * M + off;
       double sum = a[0];
 #pragma unroll
       for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
-      const double invJ = bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
+      const double invJ = RP::METS ? bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd]
+                                   : __ldg(kp.metric + static_cast<size_t>(k0 + l) * C::METP + C::MET_NV + C::MET_NE + nd);
       const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
       R[e * (NPE * M) + off] = src - invJ * sum;
     }
@@ -1037,11 +1045,13 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
   for (int i = tid; i < 2 * NP; i += nthr) smi[i] = (&kp.bt.mi[0][0])[i];
   __syncthreads();
   io.start(kp, U, Q, blockIdx.x, G, nbatch, tid, nthr);
+  __shared__ int sord[EPB];  // element ids of the batch (epilogue addresses)
   for (int batch = blockIdx.x, it = 0; batch < nbatch; batch += G, ++it) {
     const int cur = it & 1;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
     cp_async_wait_all();
     __syncthreads();
+    if (tid < nb) sord[tid] = __ldg(kp.order + k0 + tid);
     // ---- R2 (line ends) then R1 (quadrature points)
     const int n2 = nb * LPE * 2, n1 = nb * LPE * NQ;
     for (int w = tid; w < n2 + n1; w += nthr) {
@@ -1148,7 +1158,7 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
     for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
       const int l = idx / (NPE * M), off = idx - l * NPE * M;
       const int nd = off / M, c = off - nd * M;
-      const size_t e = kp.order[k0 + l];
+      const size_t e = static_cast<size_t>(sord[l]);
       double sum = 0.0;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
@@ -1220,11 +1230,13 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
   for (int i = tid; i < 2 * NP; i += nthr) smi[i] = (&kp.bt.mi[0][0])[i];
   __syncthreads();
   io.start(kp, U, nullptr, blockIdx.x, G, nbatch, tid, nthr);
+  __shared__ int sord[EPB];  // element ids of the batch (epilogue addresses)
   for (int batch = blockIdx.x, it = 0; batch < nbatch; batch += G, ++it) {
     const int cur = it & 1;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
     cp_async_wait_all();
     __syncthreads();
+    if (tid < nb) sord[tid] = __ldg(kp.order + k0 + tid);
     // ---- G1: one (line, component) per item
     for (int v = tid; v < nb * LPE * M; v += nthr) {
       const int lw = v / M, c = v - lw * M;
@@ -1289,7 +1301,7 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
 #pragma unroll
       for (int d = 1; d < D; ++d) s = s + a[d * NPE * MD];
       const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
-      Qo[kp.order[k0 + l] * static_cast<size_t>(NPE * MD) + off] = invJ * s;
+      Qo[static_cast<size_t>(sord[l]) * (NPE * MD) + off] = invJ * s;
     }
     io.advance(kp, U, nullptr, batch, it, G, nbatch, tid, nthr);
   }
