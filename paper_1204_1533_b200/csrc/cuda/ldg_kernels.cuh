@@ -2338,6 +2338,257 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   if (JP::STAGE && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// ============================================ 3-D line-streaming assembly
+// For 3-D operators whose element flux-Jacobian working set does not fit
+// shared memory (p = 4 Navier-Stokes, p = 4 Euler): one persistent CTA per
+// element at a time.  The element's lines are streamed in groups of NP lines
+// of one direction (dirs 2, 1, then 0; NL/NP groups per direction):
+//   phase P  the group's quadrature-point flux Jacobians (A = dF_inv/du closed
+//            form, Av = dF_vis/du closed form, Bq = dF_vis/dq closed form)
+//   phase X  one item per (line, row, block entry) expands them into the line
+//            blocks of that row (+ lifted endpoint blocks) and stores K11/K12
+// with phase P of group g+1 (and its endpoint-scratch gather) running in the
+// same barrier interval as phase X of group g (double-buffered).  No line is
+// evaluated twice.  The self (diagonal) blocks accumulate in shared memory
+// over the dir-2 and dir-1 passes; the dir-0 pass completes and stores them.
+template <class C>
+struct JacS3 {
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int NP = C::NP, NQ = C::NQ, M = C::M, MD = C::MD, B11 = C::B11;
+  static constexpr int GL = NP;                        // lines per group
+  static constexpr int NG = C::NL / GL;                // groups per direction
+  static constexpr int NPT = GL * NQ;                  // quadrature points per group
+  static constexpr int A = C::HAS_INV ? NPT * B11 : 0;
+  static constexpr int AV = C::VIS_U ? NPT * B11 : 0;
+  static constexpr int BQ = C::SECOND ? NPT * M * MD : 0;
+  static constexpr int PTS = ev(A + AV + BQ);          // one buffer
+  static constexpr int SLS = 2 * GL + 1;               // line-end stride of the group scratch
+  static constexpr int SEG = ev(SLS * EndJac<C>::SLOT); // one buffer
+  static constexpr int U = ev(C::NPE * M);
+  static constexpr int Q = C::SECOND ? ev(C::NPE * MD) : 0;
+  static constexpr int MET = ev(C::METP);
+  static constexpr int S11 = C::NPE * B11;
+  static constexpr int S12 = C::SECOND ? C::NPE * C::B12 : 0;
+  static constexpr int TAB = JacSmem<C>::TAB;
+  static constexpr int TOTAL = U + Q + MET + S11 + S12 + 2 * PTS + 2 * SEG + TAB;
+  static constexpr int THREADS = 512;
+  static constexpr bool OK = C::D == 3 && 8LL * TOTAL <= 220 * 1024;
+};
+
+template <class C>
+__global__ void __launch_bounds__(JacS3<C>::THREADS, 1)
+k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
+         const double* __restrict__ SE, double* __restrict__ K11, double* __restrict__ K12, int k_begin,
+         int k_end) {
+  using S3 = JacS3<C>;
+  using EJ = EndJac<C>;
+  using SM = JacSmem<C>;
+  constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, NPE = C::NPE, M = C::M, MD = C::MD, D = C::D, P = C::P,
+                NT = C::NT, B11 = C::B11, B12 = C::B12, GL = S3::GL, NG = S3::NG, SLS = S3::SLS;
+  constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+  constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
+  extern __shared__ __align__(16) double smem[];
+  double* const su = smem;
+  double* const sq = su + S3::U;
+  double* const mk = sq + S3::Q;
+  double* const self11 = mk + S3::MET;
+  double* const self12 = self11 + S3::S11;
+  double* const pts0 = self12 + S3::S12;
+  double* const seg0 = pts0 + 2 * S3::PTS;
+  double* const stab = seg0 + 2 * S3::SEG;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const double* tcc = stab + SM::TABD;  // cc[i][t][q]
+  const double* sccd = stab;            // cc[p][p][q]
+  const double* smi = stab + NP * NQ;   // mi[p][side]
+  fill_tab<C>(kp, stab, tid, nthr);
+  __shared__ int2 scon[2 * D];
+  // group gi = (pass dd, group g): direction 2 - dd, lines g*GL + j
+  auto gdir = [](int gi) { return 2 - gi / NG; };
+  auto gline = [](int gi, int j) { return (gi % NG) * GL + j; };
+  for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x) {
+    const size_t e = kp.order[k];
+    // ---- element inputs (asynchronous 8-byte copies)
+    {
+      const double* ug = U + e * (NPE * M);
+      for (int i = tid; i < NPE * M; i += nthr) cp_async8(su + i, ug + i);
+      if (C::SECOND) {
+        const double* qg = Q + e * (NPE * MD);
+        for (int i = tid; i < NPE * MD; i += nthr) cp_async8(sq + i, qg + i);
+      }
+      const double* mg = kp.metric + static_cast<size_t>(k) * C::METP;
+      for (int i = tid; i < C::METP; i += nthr) cp_async8(mk + i, mg + i);
+      if (tid < 2 * D) scon[tid] = __ldg(&kp.conn[static_cast<size_t>(k) * D * 2 + tid]);
+      cp_async_commit();
+    }
+    const double* seel = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM;
+    // endpoint scratch of group gi -> buffer: [off][side*GL + j] (stride SLS)
+    auto gather = [&](int gi, double* dst) {
+      const int dir = gdir(gi);
+      for (int w = tid; w < EJ::SLOT * 2 * GL; w += nthr) {
+        const int o = w / (2 * GL), sj = w - o * (2 * GL), side = sj / GL, j = sj - side * GL;
+        cp_async8(dst + o * SLS + sj, seel + o * EJ::LS + (dir * 2 + side) * NL + gline(gi, j));
+      }
+      cp_async_commit();
+    };
+    // phase P of group gi -> buffer
+    auto phaseP = [&](int gi, double* pb) {
+      const int dir = gdir(gi);
+      double* pA = pb;
+      double* pAv = pA + S3::A;
+      double* pBq = pAv + S3::AV;
+      // item kinds present: A (inviscid), Av (viscous d/du), Bq (viscous d/dq)
+      constexpr int KA = C::HAS_INV ? 1 : 0, KV = C::VIS_U ? 1 : 0, KB = C::SECOND ? 1 : 0;
+      constexpr int KINDS = KA + KV + KB;
+      for (int w = tid; w < GL * NQ * KINDS; w += nthr) {
+        const int kind = w / (GL * NQ), pt = w - kind * (GL * NQ), j = pt / NQ, q = pt - j * NQ;
+        const bool isA = KA && kind == 0, isV = KV && kind == KA;
+        const int line = gline(gi, j);
+        double nv[D], uq[M], qq[C::SECOND ? MD : 1];
+#pragma unroll
+        for (int d = 0; d < D; ++d) nv[d] = mk[((dir * NL + line) * NQ + q) * D + d];
+#pragma unroll
+        for (int c = 0; c < M; ++c) uq[c] = 0.0;
+        if (C::SECOND) {
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qq[c] = 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+          const int nd = node_on_line<C>(dir, line, t);
+          const double ph = kp.bt.phi[t][q];
+#pragma unroll
+          for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
+          if (C::SECOND && isV) {
+#pragma unroll
+            for (int c = 0; c < MD; ++c) qq[c] += ph * sq[nd * MD + c];
+          }
+        }
+        bool ok = true;
+        if (isA) {
+          if (C::HAS_INV) euler_jac_n<D>(uq, nv, kp.pp.gamma, pA + pt * B11, ok);
+        } else if (isV) {
+          double Jv[M * M];
+          visc_du<D, C::PH>(uq, qq, nv, kp.pp, Jv, ok);
+#pragma unroll
+          for (int c = 0; c < M * M; ++c) pAv[pt * B11 + c] = Jv[c];
+        } else if (C::SECOND) {
+          double L[M * MD];
+          visc_dq<D, C::PH>(uq, nv, kp.pp, L, ok);
+#pragma unroll
+          for (int c = 0; c < M * MD; ++c) pBq[pt * M * MD + c] = L[c];
+        }
+        if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
+      }
+    };
+    // phase X of group gi from buffers pb (quadrature points) and sg (scratch)
+    auto phaseX = [&](int gi, const double* pb, const double* sg) {
+      const int dir = gdir(gi);
+      const double* pA = pb;
+      const double* pAv = pA + S3::A;
+      const double* pBq = pAv + S3::AV;
+      const int2 c0 = scon[dir * 2 + 0], c1 = scon[dir * 2 + 1];
+      auto avq = [&](int j, int q, int ab) {
+        return (C::HAS_INV ? pA[(j * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? pAv[(j * NQ + q) * B11 + ab] : 0.0);
+      };
+      constexpr int N11 = GL * NP * B11;
+      constexpr int N12 = C::SECOND ? GL * NP * B12 : 0;
+      for (int w = tid; w < N11 + N12; w += nthr) {
+        if (w < N11) {
+          // ---- K11: (line j, row i, entry ab)
+          const int ab = w % B11, ji = w / B11, i = ji % NP, j = ji / NP;
+          const int line = gline(gi, j);
+          const int nd = node_on_line<C>(dir, line, i);
+          const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+          const double* e0 = sg + 0 * GL + j;
+          const double* e1 = sg + 1 * GL + j;
+          double av[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(j, q, ab) : 0.0;
+          double* rowp = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11 + static_cast<size_t>(nd / NT) * SM::ST11 +
+                         (static_cast<size_t>(ab / M) * NT + nd % NT) * M + ab % M;
+#pragma unroll
+          for (int t = 0; t < NP; ++t) {
+            double v = 0.0;
+            if (VOL11) {
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) v += tcc[(i * NP + t) * NQ + q] * av[q];
+            }
+            if (t == 0) v += smi[i * 2 + 0] * e0[ab * SLS];
+            if (t == P) v += smi[i * 2 + 1] * e1[ab * SLS];
+            if (t == i) {
+              // self block: dir 2 starts it, dir 1 adds, dir 0 completes and stores
+              double* sp = self11 + nd * B11 + ab;
+              if (dir == 2) *sp = v;
+              else if (dir == 1) *sp += v;
+              else rowp[static_cast<size_t>(t) * NT * B11] = sc * (v + *sp);
+              continue;
+            }
+            rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B11] = sc * v;
+          }
+          rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] =
+              c0.x >= 0 ? sc * (smi[i * 2 + 0] * e0[(B11 + ab) * SLS]) : 0.0;
+          rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] =
+              c1.x >= 0 ? sc * (smi[i * 2 + 1] * e1[(B11 + ab) * SLS]) : 0.0;
+        } else if (C::SECOND) {
+          // ---- K12: (line j, row i, stored entry ab = a' * MD + b)
+          const int v12 = w - N11;
+          const int ab = v12 % B12, ji = v12 / B12, i = ji % NP, j = ji / NP;
+          const int a = ab / MD + A0, b = ab % MD;
+          const int line = gline(gi, j);
+          const int nd = node_on_line<C>(dir, line, i);
+          const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+          double bv[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) bv[q] = pBq[(j * NQ + q) * M * MD + a * MD + b];
+          const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + 0 * GL + j];
+          const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + 1 * GL + j];
+          const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
+          const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
+          double* rowp = K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 + static_cast<size_t>(nd / NT) * SM::ST12 +
+                         (static_cast<size_t>(ab / MD) * NT + nd % NT) * MD + ab % MD;
+#pragma unroll
+          for (int t = 0; t < NP; ++t) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) v += tcc[(i * NP + t) * NQ + q] * bv[q];
+            if (t == 0 && own0) v += smi[i * 2 + 0] * eq0;
+            if (t == P && own1) v += smi[i * 2 + 1] * eq1;
+            if (t == i) {
+              double* sp = self12 + nd * B12 + ab;
+              if (dir == 2) *sp = v;
+              else if (dir == 1) *sp += v;
+              else rowp[static_cast<size_t>(t) * NT * B12] = sc * (v + *sp);
+              continue;
+            }
+            rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B12] = sc * v;
+          }
+          double nbv = 0.0;
+          if (!own0) nbv = sc * (smi[i * 2 + 0] * eq0);
+          if (!own1) nbv = sc * (smi[i * 2 + 1] * eq1);
+          rowp[static_cast<size_t>(D * P + 1 + dir) * NT * B12] = nbv;
+        }
+      }
+    };
+    (void)sccd;
+    // ---- pipeline over the 3*NG groups
+    cp_async_wait_all();
+    __syncthreads();  // element inputs + tables
+    gather(0, seg0);
+    phaseP(0, pts0);
+    cp_async_wait_all();
+    __syncthreads();
+    constexpr int NGT = 3 * NG;
+    for (int gi = 0; gi < NGT; ++gi) {
+      const int cb = gi & 1, nb = cb ^ 1;
+      if (gi + 1 < NGT) gather(gi + 1, seg0 + nb * S3::SEG);
+      phaseX(gi, pts0 + cb * S3::PTS, seg0 + cb * S3::SEG);
+      if (gi + 1 < NGT) phaseP(gi + 1, pts0 + nb * S3::PTS);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+  }
+}
+
 // K21 = dQ/dU (U-independent; D scalars per node pair), same tiles/rows.
 template <class C>
 __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __restrict__ K21) {

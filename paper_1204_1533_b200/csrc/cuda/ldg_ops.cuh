@@ -237,6 +237,17 @@ struct Launch {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       grid_max = (per_sm > 0 ? per_sm : 1) * sms;
     }
+    static const bool units = std::getenv("LDG_JAC_UNITS") != nullptr;  // 3-D: slab/line work units instead
+    const size_t s3smem = sizeof(double) * JacS3<C>::TOTAL;
+    static int s3_grid = 0;
+    if (C::D == 3 && C::WU != 0 && JacS3<C>::OK && !s3_grid) {
+      cudaFuncSetAttribute(k_jac_s3<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3smem);
+      cudaFuncSetAttribute(k_jac_s3<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      s3_grid = sms;
+    }
     const int chunk = chunk_elems(d.E);
     for (int kb = 0, ci = 0; kb < d.E; kb += chunk, ++ci) {
       const int ke = kb + chunk < d.E ? kb + chunk : d.E;
@@ -258,6 +269,11 @@ struct Launch {
         const int n = ke - kb;
         const int grid = n < grid_max ? n : grid_max;
         k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
+      } else if (C::D == 3 && C::WU != 0 && JacS3<C>::OK && !units) {
+        // 3-D line-streaming assembly (one persistent CTA per element)
+        const int n = ke - kb;
+        const int grid = n < s3_grid ? n : s3_grid;
+        k_jac_s3<C><<<grid, JacS3<C>::THREADS, s3smem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
       } else {
         k_jacobian<C><<<(ke - kb) * C::UPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11,
                                                                                     K12, kb);
