@@ -2367,10 +2367,12 @@ struct JacS3 {
   static constexpr int U = ev(C::NPE * M);
   static constexpr int Q = C::SECOND ? ev(C::NPE * MD) : 0;
   static constexpr int MET = ev(C::METP);
-  static constexpr int S11 = C::NPE * B11;
-  static constexpr int S12 = C::SECOND ? C::NPE * C::B12 : 0;
-  static constexpr int TAB = JacSmem<C>::TAB;
-  static constexpr int TOTAL = U + Q + MET + S11 + S12 + 2 * PTS + 2 * SEG + TAB;
+  static constexpr int S11 = ev(C::NPE * B11);  // even sizes keep every buffer 16-byte aligned
+  static constexpr int S12 = C::SECOND ? ev(C::NPE * C::B12) : 0;
+  static constexpr int TAB = JacSmem<C>::TABD;         // cc[p][p][q], mi[p][side]
+  static constexpr int NQ8 = (NQ + 1) / 2 * 2;          // cc rows padded to pairs (16-byte loads)
+  static constexpr int CC8 = NP * NP * NQ8;
+  static constexpr int TOTAL = U + Q + MET + S11 + S12 + 2 * PTS + 2 * SEG + TAB + CC8;
   static constexpr int THREADS = 512;
   static constexpr bool OK = C::D == 3 && 8LL * TOTAL <= 220 * 1024;
 };
@@ -2396,11 +2398,29 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   double* const pts0 = self12 + S3::S12;
   double* const seg0 = pts0 + 2 * S3::PTS;
   double* const stab = seg0 + 2 * S3::SEG;
+  double* const cc8 = stab + S3::TAB;   // cc[i][t][q], rows padded to NQ8 (zeros)
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const double* tcc = stab + SM::TABD;  // cc[i][t][q]
   const double* sccd = stab;            // cc[p][p][q]
   const double* smi = stab + NP * NQ;   // mi[p][side]
-  fill_tab<C>(kp, stab, tid, nthr);
+  constexpr int NQ8 = S3::NQ8;
+  for (int x = tid; x < NP * NQ; x += nthr) stab[x] = kp.bt.cc[x / NQ][x / NQ][x % NQ];
+  for (int x = tid; x < 2 * NP; x += nthr) stab[NP * NQ + x] = (&kp.bt.mi[0][0])[x];
+  for (int x = tid; x < S3::CC8; x += nthr) {
+    const int it = x / NQ8, q = x - it * NQ8;
+    cc8[x] = q < NQ ? (&kp.bt.cc[0][0][0])[it * NQ + q] : 0.0;
+  }
+  // sum_q cc[i][t][q] f[q] with 16-byte coefficient loads
+  auto ccdot = [&](int i, int t, const double* f) {
+    const double2* c2 = reinterpret_cast<const double2*>(cc8 + (i * NP + t) * NQ8);
+    double v = 0.0;
+#pragma unroll
+    for (int h = 0; h < NQ8 / 2; ++h) {
+      const double2 cv = c2[h];
+      v += cv.x * f[2 * h];
+      if (2 * h + 1 < NQ) v += cv.y * f[2 * h + 1];
+    }
+    return v;
+  };
   __shared__ int2 scon[2 * D];
   // group gi = (pass dd, group g): direction 2 - dd, lines g*GL + j
   auto gdir = [](int gi) { return 2 - gi / NG; };
@@ -2439,7 +2459,8 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       // item kinds present: A (inviscid), Av (viscous d/du), Bq (viscous d/dq)
       constexpr int KA = C::HAS_INV ? 1 : 0, KV = C::VIS_U ? 1 : 0, KB = C::SECOND ? 1 : 0;
       constexpr int KINDS = KA + KV + KB;
-      for (int w = tid; w < GL * NQ * KINDS; w += nthr) {
+      // on the highest thread ids: phase X leaves them one item fewer
+      for (int w = nthr - 1 - tid; w < GL * NQ * KINDS; w += nthr) {
         const int kind = w / (GL * NQ), pt = w - kind * (GL * NQ), j = pt / NQ, q = pt - j * NQ;
         const bool isA = KA && kind == 0, isV = KV && kind == KA;
         const int line = gline(gi, j);
@@ -2501,18 +2522,14 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const double sc = -mk[C::MET_NV + C::MET_NE + nd];
           const double* e0 = sg + 0 * GL + j;
           const double* e1 = sg + 1 * GL + j;
-          double av[NQ];
+          double av[NQ8];
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(j, q, ab) : 0.0;
+          for (int q = 0; q < NQ8; ++q) av[q] = (VOL11 && q < NQ) ? avq(j, q, ab) : 0.0;
           double* rowp = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11 + static_cast<size_t>(nd / NT) * SM::ST11 +
                          (static_cast<size_t>(ab / M) * NT + nd % NT) * M + ab % M;
 #pragma unroll
           for (int t = 0; t < NP; ++t) {
-            double v = 0.0;
-            if (VOL11) {
-#pragma unroll
-              for (int q = 0; q < NQ; ++q) v += tcc[(i * NP + t) * NQ + q] * av[q];
-            }
+            double v = VOL11 ? ccdot(i, t, av) : 0.0;
             if (t == 0) v += smi[i * 2 + 0] * e0[ab * SLS];
             if (t == P) v += smi[i * 2 + 1] * e1[ab * SLS];
             if (t == i) {
@@ -2537,9 +2554,9 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const int line = gline(gi, j);
           const int nd = node_on_line<C>(dir, line, i);
           const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-          double bv[NQ];
+          double bv[NQ8];
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) bv[q] = pBq[(j * NQ + q) * M * MD + a * MD + b];
+          for (int q = 0; q < NQ8; ++q) bv[q] = q < NQ ? pBq[(j * NQ + q) * M * MD + a * MD + b] : 0.0;
           const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + 0 * GL + j];
           const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + 1 * GL + j];
           const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
@@ -2548,9 +2565,7 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
                          (static_cast<size_t>(ab / MD) * NT + nd % NT) * MD + ab % MD;
 #pragma unroll
           for (int t = 0; t < NP; ++t) {
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) v += tcc[(i * NP + t) * NQ + q] * bv[q];
+            double v = ccdot(i, t, bv);
             if (t == 0 && own0) v += smi[i * 2 + 0] * eq0;
             if (t == P && own1) v += smi[i * 2 + 1] * eq1;
             if (t == i) {
