@@ -2355,7 +2355,9 @@ template <class C>
 struct JacS3 {
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
   static constexpr int NP = C::NP, NQ = C::NQ, M = C::M, MD = C::MD, B11 = C::B11;
-  static constexpr int GL = NP;                        // lines per group
+  // lines per group: NP (one slab of a direction) for second-order physics,
+  // a whole direction otherwise (no K12, small per-point footprint)
+  static constexpr int GL = C::SECOND ? NP : C::NL;
   static constexpr int NG = C::NL / GL;                // groups per direction
   static constexpr int NPT = GL * NQ;                  // quadrature points per group
   static constexpr int A = C::HAS_INV ? NPT * B11 : 0;

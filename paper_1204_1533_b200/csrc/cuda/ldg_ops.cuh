@@ -238,9 +238,10 @@ struct Launch {
       grid_max = (per_sm > 0 ? per_sm : 1) * sms;
     }
     static const bool units = std::getenv("LDG_JAC_UNITS") != nullptr;  // 3-D: slab/line work units instead
+    static const bool force_s3 = std::getenv("LDG_JAC_S3") != nullptr;  // 3-D: line streaming for element units too
     const size_t s3smem = sizeof(double) * JacS3<C>::TOTAL;
     static int s3_grid = 0;
-    if (C::D == 3 && C::WU != 0 && JacS3<C>::OK && !s3_grid) {
+    if (C::D == 3 && (C::WU != 0 || force_s3) && JacS3<C>::OK && !s3_grid) {
       cudaFuncSetAttribute(k_jac_s3<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3smem);
       cudaFuncSetAttribute(k_jac_s3<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       int dev = 0, sms = 0;
@@ -265,11 +266,11 @@ struct Launch {
                                                                                          kb, ke, ob, oe);
       }
       count(d);
-      if (JacP<C>::OK && !simple) {
+      if (JacP<C>::OK && !simple && !(C::D == 3 && force_s3)) {
         const int n = ke - kb;
         const int grid = n < grid_max ? n : grid_max;
         k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
-      } else if (C::D == 3 && C::WU != 0 && JacS3<C>::OK && !units) {
+      } else if (C::D == 3 && (C::WU != 0 || force_s3) && JacS3<C>::OK && !units) {
         // 3-D line-streaming assembly (one persistent CTA per element)
         const int n = ke - kb;
         const int grid = n < s3_grid ? n : s3_grid;
