@@ -1007,7 +1007,12 @@ struct ResF {
   static constexpr int FH = EPB * C::LPE * 2 * C::M;
   static constexpr int TAB = IO::ev(2 * C::NP * C::NQ + 2 * C::NP);
   static constexpr int TOTAL = IO::SMEM + F + FH + TAB;
-  static constexpr int THREADS = 256;
+  // one element per batch (the ring fills shared memory): as many warps as
+  // the register file allows
+#ifndef LDG_RESF_THREADS1
+#define LDG_RESF_THREADS1 512
+#endif
+  static constexpr int THREADS = EPB == 1 ? LDG_RESF_THREADS1 : 256;
   static constexpr long long bytes_per_elem() {
     return IO::bytes_per_elem() + 8LL * (C::LPE * C::NQ * C::M + C::LPE * 2 * C::M);
   }
