@@ -45,6 +45,14 @@ struct KParams {
 #endif
 constexpr bool VISC_DU_CLOSED = LDG_VISC_DU != 0;
 
+#ifndef LDG_JAC_SMEMTAB  // tuning knob: assembly basis coefficients from shared memory (1) or the constant
+#define LDG_JAC_SMEMTAB 0  // bank (0); measured: the constant bank wins (C2 0.266 vs 0.311 ms) despite its spills
+#endif
+constexpr int JAC_SMEMTAB = LDG_JAC_SMEMTAB;
+#ifndef LDG_JAC_CHAINS  // assembly: line-block sums as one (1) or two (2) dependent DFMA chains
+#define LDG_JAC_CHAINS 1
+#endif
+constexpr int JAC_CHAINS = LDG_JAC_CHAINS;  // 0 constant bank, 1 shared (scalar), 2 shared (pairs)
 // ---------------------------------------------------------------- helpers
 
 template <class C>
@@ -1763,7 +1771,9 @@ struct JacSmem {
   // + full cc[i][t][q] + phi[t][q]: the assembly reads its basis coefficients
   // from shared memory (constant-bank operands are hoisted into registers by
   // the compiler and spill)
-  static constexpr int TAB = TABD + C::NP * C::NP * C::NQ + C::NP * C::NQ;
+  static constexpr int NQ8 = (C::NQ + 1) / 2 * 2;
+  static constexpr int CC8 = LDG_JAC_SMEMTAB == 2 ? C::NP * C::NP * NQ8 : 0;  // pair-padded cc (16-byte loads)
+  static constexpr int TAB = TABD + (C::NP * C::NP * C::NQ + C::NP * C::NQ + 1) / 2 * 2 + CC8;
   static constexpr int ST11 = C::NS11 * C::B11 * C::NT;       // store doubles per tile
   static constexpr int ST12 = C::SECOND ? C::NS12 * C::B12 * C::NT : 0;
   static constexpr int WORK = A + AV + BQ + TAB;
@@ -1779,10 +1789,7 @@ constexpr int P2_UNROLL_K = LDG_P2_UNROLL;
 #define LDG_P2_ROWS 0  // measured: per-line items are faster (C2 0.264 vs 0.297 ms)
 #endif
 constexpr bool P2_ROWS = LDG_P2_ROWS != 0;
-#ifndef LDG_JAC_SMEMTAB  // tuning knob: assembly basis coefficients from shared memory (1) or the constant
-#define LDG_JAC_SMEMTAB 0  // bank (0); measured: the constant bank wins (C2 0.266 vs 0.311 ms) despite its spills
-#endif
-constexpr bool JAC_SMEMTAB = LDG_JAC_SMEMTAB != 0;
+
 
 template <class C>
 __device__ __forceinline__ int tile_line_of(int dir, int line, int s) {
@@ -1919,7 +1926,35 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   const double* const tcc = stab + SM::TABD;                  // cc[i][t][q]
   const double* const tphi = tcc + NP * NP * NQ;               // phi[t][q]
   const double* const tmi = stab + NP * NQ;                    // mi[i][side]
-  auto CC = [&](int i, int t, int q) { return JAC_SMEMTAB ? tcc[(i * NP + t) * NQ + q] : kp.bt.cc[i][t][q]; };
+  auto CC = [&](int i, int t, int q) { return JAC_SMEMTAB == 1 ? tcc[(i * NP + t) * NQ + q] : kp.bt.cc[i][t][q]; };
+  // sum_q cc[i][t][q] f[q]: constant bank, or (JAC_SMEMTAB == 2) 16-byte
+  // loads from the pair-padded shared table (f padded with zeros)
+  constexpr int NQ8 = SM::NQ8;
+  const double* const tcc8 = stab + SM::TAB - SM::CC8;
+  auto ccdot = [&](int i, int t, const double* f) {
+    double v = 0.0;
+    if (JAC_SMEMTAB == 2) {
+      const double2* c2 = reinterpret_cast<const double2*>(tcc8 + (i * NP + t) * NQ8);
+#pragma unroll
+      for (int h = 0; h < NQ8 / 2; ++h) {
+        const double2 cv = c2[h];
+        v += cv.x * f[2 * h];
+        if (2 * h + 1 < NQ) v += cv.y * f[2 * h + 1];
+      }
+    } else if (JAC_CHAINS == 2) {
+      // two independent partial sums (half the dependent DFMA chain)
+      double v1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; q += 2) v += CC(i, t, q) * f[q];
+#pragma unroll
+      for (int q = 1; q < NQ; q += 2) v1 += CC(i, t, q) * f[q];
+      v += v1;
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v += CC(i, t, q) * f[q];
+    }
+    return v;
+  };
   auto MI = [&](int i, int sd) { return JAC_SMEMTAB ? tmi[i * 2 + sd] : kp.bt.mi[i][sd]; };
   auto PHI = [&](int t, int q) { return JAC_SMEMTAB ? tphi[t * NQ + q] : kp.bt.phi[t][q]; };
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
@@ -2015,9 +2050,9 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   auto line_item = [&](const int tl, const int ab, auto&& rows) {
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
-    double av[NQ];
+    double av[NQ8];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(tl, q, ab) : 0.0;
+    for (int q = 0; q < NQ8; ++q) av[q] = (VOL11 && q < NQ) ? avq(tl, q, ab) : 0.0;
     const double* e0 = sE + eidx(tl, dir, line, 0);
     const double* e1 = sE + eidx(tl, dir, line, 1);
     const double ein0 = e0[ab * LS], ein1 = e1[ab * LS];
@@ -2032,11 +2067,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         if (t == i && dir != 0) continue;  // the dir-0 thread owns the self block
-        double v = 0.0;
-        if (VOL11) {
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) v += CC(i, t, q) * av[q];
-        }
+        double v = VOL11 ? ccdot(i, t, av) : 0.0;
         if (t == 0) v += MI(i, 0) * ein0;
         if (t == P) v += MI(i, 1) * ein1;
         if (t == i) {
@@ -2103,9 +2134,9 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     int dir, line;
     TileLines<C>::get(tl, s, dir, line);
     const bool full = TileLines<C>::full(dir);
-    double bv[NQ];
+    double bv[NQ8];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) bv[q] = sBq[(tl * NQ + q) * M * MD + a * MD + b];
+    for (int q = 0; q < NQ8; ++q) bv[q] = q < NQ ? sBq[(tl * NQ + q) * M * MD + a * MD + b] : 0.0;
     const double eq0 = sE[eidx(tl, dir, line, 0) + (2 * B11 + a * MD + b) * LS];
     const double eq1 = sE[eidx(tl, dir, line, 1) + (2 * B11 + a * MD + b) * LS];
     const int2 c0 = scon[dir * 2 + 0];
@@ -2121,9 +2152,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         if (t == i && dir != 0) continue;
-        double v = 0.0;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) v += CC(i, t, q) * bv[q];
+        double v = ccdot(i, t, bv);
         if (t == 0 && own0) v += MI(i, 0) * eq0;
         if (t == P && own1) v += MI(i, 1) * eq1;
         if (t == i) {
@@ -2184,6 +2213,14 @@ __device__ __forceinline__ void fill_tab(const KParams<C>& kp, double* stab, int
   for (int i = tid; i < 2 * NP; i += nthr) stab[NP * NQ + i] = (&kp.bt.mi[0][0])[i];
   for (int i = tid; i < NP * NP * NQ; i += nthr) stab[JacSmem<C>::TABD + i] = (&kp.bt.cc[0][0][0])[i];
   for (int i = tid; i < NP * NQ; i += nthr) stab[JacSmem<C>::TABD + NP * NP * NQ + i] = (&kp.bt.phi[0][0])[i];
+  if (JacSmem<C>::CC8) {
+    constexpr int NQ8 = JacSmem<C>::NQ8;
+    double* cc8 = stab + JacSmem<C>::TAB - JacSmem<C>::CC8;
+    for (int x = tid; x < NP * NP * NQ8; x += nthr) {
+      const int it = x / NQ8, q = x - it * NQ8;
+      cc8[x] = q < NQ ? (&kp.bt.cc[0][0][0])[it * NQ + q] : 0.0;
+    }
+  }
 }
 
 template <class C>
