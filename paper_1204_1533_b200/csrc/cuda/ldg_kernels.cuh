@@ -1910,7 +1910,9 @@ __device__ __forceinline__ void jac_k11_rows3(const double* mk, const int2* scon
 // One Jacobian row tile.  su/sq element state and gradient, mk the element's
 // metric (1/J included), sE the endpoint flux Jacobians of the tile lines
 // indexed by eidx(tl, dir, line, side); stab = {cc[p][p][q], mi[p][s]}.
-template <class C, class EIdx>
+// PHS: bit 0 runs phase 1 (quadrature-point flux Jacobians into sA/sAv/sBq),
+// bit 1 phases 2-3 (expansion and stores); 3 = both, with a barrier between.
+template <class C, class EIdx, int PHS = 3>
 __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, const int s, const size_t e,
                                          const double* su, const double* sq, const double* mk, const int2* scon,
                                          const double* sE, EIdx eidx, double* sA, double* sAv, double* sBq,
@@ -1959,7 +1961,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   auto PHI = [&](int t, int q) { return JAC_SMEMTAB ? tphi[t * NQ + q] : kp.bt.phi[t][q]; };
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
-  if (C::HAS_INV && !(kp.dbg & 1)) {
+  if ((PHS & 1) && C::HAS_INV && !(kp.dbg & 1)) {
     for (int w = tid; w < NLT * NQ; w += nthr) {
       const int tl = w / NQ, q = w - tl * NQ;
       int dir, line;
@@ -1983,7 +1985,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   }
   // ---- phase 1c (second-order): viscous flux derivatives at the quadrature
   // points: one item per u-seed (dual numbers) plus one closed-form dF/dq item
-  if (C::SECOND && !(kp.dbg & 1)) {
+  if ((PHS & 1) && C::SECOND && !(kp.dbg & 1)) {
     constexpr int NSU = C::VIS_U ? (VISC_DU_CLOSED ? 1 : M) : 0, NSEED = NSU + 1;
     for (int w = tid; w < NLT * NQ * NSEED; w += nthr) {
       const int sd = w % NSEED, tq = w / NSEED, tl = tq / NQ, q = tq - tl * NQ;
@@ -2035,7 +2037,8 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
       if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
     }
   }
-  __syncthreads();
+  if (PHS == 3) __syncthreads();
+  if (!(PHS & 2)) return;
 
   if (C::D == 3 && C::WU == 0 && !(kp.dbg & 2))
     jac_k11_rows3<C>(mk, scon, sE, eidx, sA, sAv, stab + JacSmem<C>::TABD, stab + NP * NQ, K11t, tid, nthr);
@@ -2297,14 +2300,22 @@ struct JacP {
 #endif
   // (measured: a small gain for the Euler tile, a loss for second-order
   // tiles whose larger footprint costs occupancy)
-  static constexpr bool STAGE = LDG_JAC_STAGE && C::D == 2 && !C::SECOND && (SM::ST11 % 2 == 0) &&
+  // 2-D: software pipeline -- phases 2-3 of element k and phase 1 of element
+  // k+1 share one barrier interval (double quadrature-point tables, 3-deep
+  // input ring)
+#ifndef LDG_JAC_PIPE  // measured: no gain for C2 (0.267 vs 0.265 ms), a loss for C3 (occupancy): off
+#define LDG_JAC_PIPE 0
+#endif
+  static constexpr bool PIPE = LDG_JAC_PIPE && C::D == 2;
+  static constexpr int WORK2 = PIPE ? SM::A + SM::AV + SM::BQ : 0;  // second quadrature-point set
+  static constexpr bool STAGE = !PIPE && LDG_JAC_STAGE && C::D == 2 && !C::SECOND && (SM::ST11 % 2 == 0) &&
                                 8LL * SM::ST11 <= 64 * 1024;
   static constexpr int STG = STAGE ? SM::ST11 : 0;
-  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + STG); }
-  // prefetch ring depth: 3 for the one-CTA-per-SM 3-D element units (when it
-  // fits), 2 where several CTAs share an SM
-  static constexpr int NBUF = (JacThreads<C>::big && bytes(3) <= 200 * 1024) ? 3 : 2;
-  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + STG;  // 4 doubles hold up to 3 mbarriers
+  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + WORK2 + STG); }
+  // prefetch ring depth: 3 for the pipelined 2-D tile and the one-CTA-per-SM
+  // 3-D element units (when it fits), 2 where several CTAs share an SM
+  static constexpr int NBUF = ((PIPE || JacThreads<C>::big) && bytes(3) <= 200 * 1024) ? 3 : 2;
+  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + WORK2 + STG;  // 4 doubles hold up to 3 mbarriers
   static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
                              (EndJac<C>::PER_ELEM % 2 == 0) && bytes(2) <= 200 * 1024;
 };
@@ -2326,7 +2337,10 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
   double* stab = sBq + SM::BQ;
-  double* sstage = work + SM::WORK;  // K11 tile staging (JP::STAGE)
+  double* sstage = work + SM::WORK + JP::WORK2;  // K11 tile staging (JP::STAGE)
+  double* sA2 = work + SM::WORK;                  // second quadrature-point set (JP::PIPE)
+  double* sAv2 = sA2 + SM::A;
+  double* sBq2 = sAv2 + SM::AV;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = gridDim.x;
   if (k_begin + static_cast<int>(blockIdx.x) >= k_end) return;
@@ -2356,6 +2370,34 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   if (tid == 0)
     for (int b = 0; b < NB; ++b)
       if (k0 + b * G < k_end) issue(k0 + b * G, b);
+  if (JP::PIPE) {
+    // phase 1 of the first element, then per interval: phases 2-3 of element
+    // k (set it&1) and phase 1 of element k+G (set (it+1)&1), one barrier
+    if (k0 < k_end) {
+      mbar_wait(&bar[0], 0);
+      jac_tile<C, SeFull<C>, 1>(kp, k0, 0, kp.order[k0], bU(0), bQ(0), bMET(0), bCONN(0), bSE(0), SeFull<C>(), sA, sAv,
+                                sBq, stab, nullptr, nullptr, tid, nthr);
+    }
+    __syncthreads();
+    for (int k = k0, it = 0; k < k_end; k += G, ++it) {
+      const int cur = it % NB, nx = (it + 1) % NB;
+      const int kn = k + G;
+      if (kn < k_end) mbar_wait(&bar[nx], ((it + 1) / NB) & 1);
+      double* a0 = (it & 1) ? sA2 : sA;
+      double* av0 = (it & 1) ? sAv2 : sAv;
+      double* bq0 = (it & 1) ? sBq2 : sBq;
+      jac_tile<C, SeFull<C>, 2>(kp, k, 0, kp.order[k], bU(cur), bQ(cur), bMET(cur), bCONN(cur), bSE(cur), SeFull<C>(),
+                                a0, av0, bq0, stab, K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
+                                C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
+      if (kn < k_end)
+        jac_tile<C, SeFull<C>, 1>(kp, kn, 0, kp.order[kn], bU(nx), bQ(nx), bMET(nx), bCONN(nx), bSE(nx), SeFull<C>(),
+                                  (it & 1) ? sA : sA2, (it & 1) ? sAv : sAv2, (it & 1) ? sBq : sBq2, stab, nullptr,
+                                  nullptr, tid, nthr);
+      __syncthreads();  // buffer `cur` and quadrature-point set it&1 are free
+      if (tid == 0 && k + NB * G < k_end) issue(k + NB * G, cur);
+    }
+    return;
+  }
   for (int k = k0, it = 0; k < k_end; k += G, ++it) {
     const int cur = it % NB;
     mbar_wait(&bar[cur], (it / NB) & 1);
