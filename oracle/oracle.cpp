@@ -8,6 +8,7 @@
 //   residual_second_order / residual_primal
 //   assemble_jacobians (Analytic + FD)
 //   CscMatrix, split_matvec
+//   build_preconditioner, gmres
 // It follows the reference's numerics literally where they are specified:
 // r = M^-1 b through the Cholesky factor of M column by column
 // (basis.cpp:81-88, 185-189), fluxes at the quadrature points of the
@@ -69,6 +70,11 @@ struct Ctx {
   std::vector<int32_t> ep_elem, ep_node, ep_bc;  // ep_bc: -1 interior, else index in bcv
   std::vector<std::vector<double>> bcv;          // Dirichlet states
   BlockMat K[3];
+  // block-Jacobi preconditioner: per element LU (partial pivoting) of
+  // I - alpha_dt A~ restricted to the element (dense n_e x n_e, row-major)
+  std::vector<double> pcLU;
+  std::vector<int32_t> pcPiv;
+  bool pc_built = false;
   std::string err;
   std::vector<double> err_state;
   int err_elem = -1, err_node = -1;
@@ -1120,6 +1126,233 @@ int lo_split_matvec(const lo_ctx* x, double adt, const double* v, double* y) {
       for (size_t i = 0; i < n; ++i) a[i] = a[i] + b[i];
     }
     for (size_t i = 0; i < n; ++i) y[i] = v[i] - adt * a[i];
+  });
+}
+
+// ---- block-Jacobi preconditioner
+// A~ equals A = K11 + K12 K21 on the block-diagonal Line-DG pattern -- row
+// and column node in the same element and on a common coordinate line -- and
+// is zero elsewhere: fill of the product and inter-element couplings are
+// dropped, while the product's entries that land on the pattern are exact
+// (summed over every middle node, neighbour elements included).  Each element
+// block of I - alpha_dt A~ is LU-factorised with partial pivoting.
+namespace {
+bool on_line_pattern(const Ctx& c, int r, int col) {
+  int same = 0;
+  int a = r, b = col;
+  for (int d = 0; d < c.D; ++d) {
+    same += (a % c.np) == (b % c.np);
+    a /= c.np;
+    b /= c.np;
+  }
+  return same >= c.D - 1;
+}
+}  // namespace
+
+int lo_precond_build(lo_ctx* x, double adt) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    const BlockMat& K11 = c.K[LDG_K11];
+    if (!K11.built) throw std::runtime_error("oracle: Jacobian not assembled");
+    const int m = c.m, npe = c.npe, ne = npe * m;
+    c.pcLU.assign(static_cast<size_t>(c.E) * ne * ne, 0.0);
+    c.pcPiv.assign(static_cast<size_t>(c.E) * ne, 0);
+    std::atomic<int> bad{-1};
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int e = 0; e < c.E; ++e) {
+      double* Me = &c.pcLU[static_cast<size_t>(e) * ne * ne];
+      const int64_t base = static_cast<int64_t>(e) * npe;
+      for (int r = 0; r < npe; ++r) {
+        const int64_t R = base + r;
+        for (int64_t k = K11.rowptr[R]; k < K11.rowptr[R + 1]; ++k) {
+          const int64_t cn = K11.col[k];
+          if (cn < base || cn >= base + npe || !on_line_pattern(c, r, static_cast<int>(cn - base))) continue;
+          const int cl = static_cast<int>(cn - base);
+          for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) Me[(r * m + a) * ne + cl * m + b] += K11.val[(k * m + a) * m + b];
+        }
+        if (c.second) {
+          const BlockMat& K12 = c.K[LDG_K12];
+          const BlockMat& K21 = c.K[LDG_K21];
+          const int mD = m * c.D;
+          for (int64_t k = K12.rowptr[R]; k < K12.rowptr[R + 1]; ++k) {
+            const int64_t mid = K12.col[k];
+            const double* b12 = &K12.val[k * m * mD];  // m x mD
+            for (int64_t j = K21.rowptr[mid]; j < K21.rowptr[mid + 1]; ++j) {
+              const int64_t cn = K21.col[j];
+              if (cn < base || cn >= base + npe || !on_line_pattern(c, r, static_cast<int>(cn - base))) continue;
+              const int cl = static_cast<int>(cn - base);
+              const double* b21 = &K21.val[j * mD * m];  // mD x m
+              for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) {
+                  double s = 0.0;
+                  for (int q = 0; q < mD; ++q) s += b12[a * mD + q] * b21[q * m + b];
+                  Me[(r * m + a) * ne + cl * m + b] += s;
+                }
+            }
+          }
+        }
+      }
+      for (int i = 0; i < ne * ne; ++i) Me[i] *= -adt;
+      for (int i = 0; i < ne; ++i) Me[i * ne + i] += 1.0;
+      // LU with partial pivoting (row interchanges recorded in piv)
+      int32_t* piv = &c.pcPiv[static_cast<size_t>(e) * ne];
+      for (int kk = 0; kk < ne; ++kk) {
+        int pr = kk;
+        double best = std::fabs(Me[kk * ne + kk]);
+        for (int i = kk + 1; i < ne; ++i)
+          if (std::fabs(Me[i * ne + kk]) > best) {
+            best = std::fabs(Me[i * ne + kk]);
+            pr = i;
+          }
+        piv[kk] = pr;
+        if (!(best > 0.0)) {
+          int expect = -1;
+          bad.compare_exchange_strong(expect, e);
+          break;
+        }
+        if (pr != kk)
+          for (int j = 0; j < ne; ++j) std::swap(Me[kk * ne + j], Me[pr * ne + j]);
+        const double ip = 1.0 / Me[kk * ne + kk];
+        for (int i = kk + 1; i < ne; ++i) {
+          const double l = Me[i * ne + kk] * ip;
+          Me[i * ne + kk] = l;
+          for (int j = kk + 1; j < ne; ++j) Me[i * ne + j] -= l * Me[kk * ne + j];
+        }
+      }
+    }
+    if (bad.load() >= 0)
+      throw std::runtime_error("oracle: singular preconditioner block at element " + std::to_string(bad.load()));
+    c.pc_built = true;
+  });
+}
+
+namespace {
+void pc_apply(const Ctx& c, const double* r, double* z) {
+  const int ne = c.npe * c.m;
+#pragma omp parallel for schedule(static)
+  for (int e = 0; e < c.E; ++e) {
+    const double* LU = &c.pcLU[static_cast<size_t>(e) * ne * ne];
+    const int32_t* piv = &c.pcPiv[static_cast<size_t>(e) * ne];
+    double* ze = z + static_cast<size_t>(e) * ne;
+    const double* re = r + static_cast<size_t>(e) * ne;
+    for (int i = 0; i < ne; ++i) ze[i] = re[i];
+    for (int i = 0; i < ne; ++i) std::swap(ze[i], ze[piv[i]]);
+    for (int i = 0; i < ne; ++i) {
+      double s = ze[i];
+      for (int j = 0; j < i; ++j) s -= LU[i * ne + j] * ze[j];
+      ze[i] = s;
+    }
+    for (int i = ne - 1; i >= 0; --i) {
+      double s = ze[i];
+      for (int j = i + 1; j < ne; ++j) s -= LU[i * ne + j] * ze[j];
+      ze[i] = s / LU[i * ne + i];
+    }
+  }
+}
+double dotv(const double* a, const double* b, size_t n) {
+  double s = 0.0;
+#pragma omp parallel for reduction(+ : s) schedule(static)
+  for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) s += a[i] * b[i];
+  return s;
+}
+}  // namespace
+
+int lo_precond_apply(const lo_ctx* x, const double* r, double* z) {
+  return guarded([&] {
+    if (!x->c.pc_built) throw std::runtime_error("oracle: preconditioner not built");
+    pc_apply(x->c, r, z);
+  });
+}
+
+// Right-preconditioned restarted GMRES with modified Gram-Schmidt and Givens
+// rotations, operator = split_matvec(alpha_dt), preconditioner
+// = block-Jacobi (use_pc) or identity; x0 = 0.  Stops when the true residual
+// ||b - A x|| <= rtol ||b|| (checked at every restart and at the end) or the
+// Givens estimate says so, or after maxit iterations.
+int lo_gmres(const lo_ctx* x, double adt, const double* b, double rtol, int32_t maxit, int32_t restart,
+             int32_t use_pc, double* xout, int32_t* iters, int32_t* converged, double* resnorm) {
+  return guarded([&] {
+    const Ctx& c = x->c;
+    if (!(rtol > 0.0) || maxit < 1 || restart < 1) throw std::invalid_argument("oracle: gmres arguments");
+    if (use_pc && !c.pc_built) throw std::runtime_error("oracle: preconditioner not built");
+    const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
+    auto op = [&](const double* v, double* y) {
+      if (lo_split_matvec(x, adt, v, y) != LDG_OK) throw std::runtime_error(g_err);
+    };
+    std::fill(xout, xout + n, 0.0);
+    const double bn = std::sqrt(dotv(b, b, n));
+    *iters = 0;
+    *converged = 0;
+    *resnorm = bn;
+    if (bn == 0.0) {
+      *converged = 1;
+      return;
+    }
+    std::vector<double> r(b, b + n), w(n), t(n);
+    const int mr = restart;
+    std::vector<std::vector<double>> V(mr + 1, std::vector<double>(n)), Z(mr, std::vector<double>(n));
+    std::vector<double> H((mr + 1) * mr), cs(mr), sn(mr), g(mr + 1);
+    double beta = bn;
+    int it = 0;
+    while (true) {
+      for (size_t i = 0; i < n; ++i) V[0][i] = r[i] / beta;
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int j = 0;
+      for (; j < mr && it < maxit; ++j) {
+        if (use_pc) pc_apply(c, V[j].data(), Z[j].data());
+        else std::copy(V[j].begin(), V[j].end(), Z[j].begin());
+        op(Z[j].data(), w.data());
+        for (int i = 0; i <= j; ++i) {
+          const double h = dotv(w.data(), V[i].data(), n);
+          H[i * mr + j] = h;
+          for (size_t q = 0; q < n; ++q) w[q] -= h * V[i][q];
+        }
+        const double hn = std::sqrt(dotv(w.data(), w.data(), n));
+        if (!std::isfinite(hn)) throw std::runtime_error("oracle: gmres numerical breakdown");
+        H[(j + 1) * mr + j] = hn;
+        if (hn > 0.0)
+          for (size_t q = 0; q < n; ++q) V[j + 1][q] = w[q] / hn;
+        for (int i = 0; i < j; ++i) {
+          const double a0 = H[i * mr + j], a1 = H[(i + 1) * mr + j];
+          H[i * mr + j] = cs[i] * a0 + sn[i] * a1;
+          H[(i + 1) * mr + j] = -sn[i] * a0 + cs[i] * a1;
+        }
+        const double a0 = H[j * mr + j], a1 = H[(j + 1) * mr + j];
+        const double den = std::hypot(a0, a1);
+        cs[j] = den > 0.0 ? a0 / den : 1.0;
+        sn[j] = den > 0.0 ? a1 / den : 0.0;
+        H[j * mr + j] = den;
+        H[(j + 1) * mr + j] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        ++it;
+        if (std::fabs(g[j + 1]) <= rtol * bn || hn == 0.0) {
+          ++j;
+          break;
+        }
+      }
+      // x += Z y,  H(0:j,0:j) y = g(0:j)
+      std::vector<double> y(j, 0.0);
+      for (int i = j - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int q = i + 1; q < j; ++q) s -= H[i * mr + q] * y[q];
+        y[i] = s / H[i * mr + i];
+      }
+      for (int i = 0; i < j; ++i)
+        for (size_t q = 0; q < n; ++q) xout[q] += y[i] * Z[i][q];
+      op(xout, t.data());
+      for (size_t q = 0; q < n; ++q) r[q] = b[q] - t[q];
+      beta = std::sqrt(dotv(r.data(), r.data(), n));
+      *resnorm = beta;
+      if (beta <= rtol * bn) {
+        *converged = 1;
+        break;
+      }
+      if (it >= maxit) break;
+    }
+    *iters = it;
   });
 }
 

@@ -55,6 +55,10 @@ def lib():
         L.lo_spmv.argtypes = [vp, C.c_int32, _dp, _dp]
         L.lo_split_matvec.argtypes = [vp, C.c_double, _dp, _dp]
         L.lo_fd_dense.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
+        L.lo_precond_build.argtypes = [vp, C.c_double]
+        L.lo_precond_apply.argtypes = [vp, _dp, _dp]
+        L.lo_gmres.argtypes = [vp, C.c_double, _dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, _dp,
+                               C.POINTER(C.c_int32), C.POINTER(C.c_int32), _dp]
         L.lo_euler_flux.argtypes = [C.c_int32, _dp, C.c_double, _dp]
         L.lo_riemann.argtypes = [C.c_int32, C.c_int32, _dp, _dp, _dp, C.c_double, _dp]
         L.lo_ns_viscous_flux.argtypes = [C.c_int32, _dp, _dp, C.c_double, C.c_double, C.c_double, _dp]
@@ -189,6 +193,26 @@ class Oracle:
         y = np.zeros(self.n_dofs)
         self._check(self.L.lo_split_matvec(self.h, adt, _d(v), _d(y)))
         return y
+
+    def precond_build(self, adt):
+        self._check(self.L.lo_precond_build(self.h, adt))
+
+    def precond_apply(self, r):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.zeros(self.n_dofs)
+        self._check(self.L.lo_precond_apply(self.h, _d(r), _d(z)))
+        return z
+
+    def gmres(self, adt, b, rtol=1e-8, maxit=50, restart=30, precond=True):
+        """(x, iterations, converged, ||b - A x||) of right-preconditioned GMRES."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(self.n_dofs)
+        it = C.c_int32()
+        cv = C.c_int32()
+        rn = C.c_double()
+        self._check(self.L.lo_gmres(self.h, adt, _d(b), rtol, maxit, restart, 1 if precond else 0, _d(x),
+                                    C.byref(it), C.byref(cv), C.byref(rn)))
+        return x, it.value, bool(cv.value), rn.value
 
     def fd_dense(self, which, U, Q=None):
         U = np.ascontiguousarray(U, dtype=np.float64)
