@@ -172,6 +172,31 @@ int ldg_pattern_info_get(const ldg_ctx* ctx, int which, ldg_pattern_info* info);
 int ldg_bsr_spmv(ldg_ctx* ctx, int which, const double* x, double* y);
 /* y = v - alpha_dt (K11 v + K12 (K21 v)); first-order: y = v - alpha_dt K11 v */
 int ldg_split_matvec(ldg_ctx* ctx, double alpha_dt, const double* v, double* y);
+
+/* Block-Jacobi preconditioner: per element,
+   the LU factors (partial pivoting) of I - alpha_dt A~, A~ = K11 + K12 K21 kept
+   only on the block-diagonal Line-DG pattern (row and column node in the same
+   element and on a common coordinate line; the product's entries landing there
+   are exact, all other fill and inter-element couplings dropped).  Requires an
+   assembled Jacobian.  Element blocks of up to 128 unknowns (2-D p <= 4,
+   3-D p = 1); LDG_ERR_CONFIG beyond, LDG_ERR_SOLVER for a singular block.
+   Replaces build_preconditioner(blocks, alpha_dt). */
+int ldg_precond_build(ldg_ctx* ctx, double alpha_dt);
+/* z = (I - alpha_dt A~)^-1 r, device vectors (reference numbering). */
+int ldg_precond_apply(ldg_ctx* ctx, const double* r, double* z);
+int ldg_precond_apply_host(ldg_ctx* ctx, const double* r, double* z);
+/* Right-preconditioned restarted GMRES with modified Gram-Schmidt
+   (SPEC.md:429-437): solves (I - alpha_dt (K11 + K12 K21)) x = b with the split
+   matvec as operator and, if use_precond, the block-Jacobi preconditioner;
+   x0 = 0.  Returns when ||b - A x|| <= rtol ||b|| or after maxit iterations
+   (never an error on stagnation); LDG_ERR_SOLVER on non-finite Krylov vectors.
+   iters/converged/resnorm (true residual norm) are outputs.  Replaces
+   gmres(operator, precond, b, rtol, maxit, restart). */
+int ldg_gmres(ldg_ctx* ctx, double alpha_dt, const double* b, double* x, double rtol, int32_t maxit,
+               int32_t restart, int32_t use_precond, int32_t* iters, int32_t* converged, double* resnorm);
+int ldg_gmres_host(ldg_ctx* ctx, double alpha_dt, const double* b, double* x, double rtol, int32_t maxit,
+                           int32_t restart, int32_t use_precond, int32_t* iters, int32_t* converged,
+                           double* resnorm);
 /* Export of the node pattern (host arrays of nnzb int64) and block values
  * (host array nnzb*block_rows*block_cols, row-major blocks), reference numbering.
  * Any pointer may be NULL. */

@@ -145,6 +145,7 @@ GPU_SYMBOLS = [
     "ldg_export_blocks", "ldg_export_blocks_subset", "ldg_set_sync_errors", "ldg_synchronize",
     "ldg_residual_host", "ldg_jacobian_assemble_host", "ldg_bsr_spmv_host", "ldg_split_matvec_host",
     "ldg_kernel_launches", "ldg_jacobian_bytes",
+    "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
 ]
 
 
@@ -180,6 +181,13 @@ def gpu_lib() -> C.CDLL:
         L.ldg_jacobian_assemble_host.argtypes = [vp, _dp, C.c_double]
         L.ldg_bsr_spmv_host.argtypes = [vp, C.c_int, _dp, _dp]
         L.ldg_split_matvec_host.argtypes = [vp, C.c_double, _dp, _dp]
+        L.ldg_precond_build.argtypes = [vp, C.c_double]
+        L.ldg_precond_apply.argtypes = [vp, vp, vp]
+        L.ldg_precond_apply_host.argtypes = [vp, _dp, _dp]
+        _g = [vp, C.c_double, vp, vp, C.c_double, C.c_int32, C.c_int32, C.c_int32,
+              C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        L.ldg_gmres.argtypes = _g
+        L.ldg_gmres_host.argtypes = [vp, C.c_double, _dp, _dp] + _g[4:]
         L.ldg_kernel_launches.argtypes = [vp]
         L.ldg_kernel_launches.restype = C.c_int64
         L.ldg_jacobian_bytes.argtypes = [vp]

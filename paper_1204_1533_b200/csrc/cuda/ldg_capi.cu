@@ -72,6 +72,16 @@ struct ldg_ctx {
   // device
   int2* d_fpart = nullptr;
   int32_t* d_owned = nullptr;
+  int32_t* d_inv_order = nullptr;
+  // block-Jacobi preconditioner (per element LU, column-major) and GMRES workspace
+  double* d_pcLU = nullptr;
+  int32_t* d_pcPiv = nullptr;
+  int* d_pcbad = nullptr;
+  bool pc_valid = false;
+  double* d_kv = nullptr;  // Krylov vectors V[0..restart] then Z[0..restart-1]
+  int kv_restart = 0;
+  double* d_kw = nullptr;  // w, t, r
+  double* d_kred = nullptr;  // reduction partials + Hessenberg (column-major) + scalars
   int32_t* d_order = nullptr;
   double* d_metric = nullptr;
   int2* d_conn = nullptr;
@@ -107,6 +117,13 @@ struct ldg_ctx {
     cudaFree(d_conn);
     cudaFree(d_fpart);
     cudaFree(d_owned);
+    cudaFree(d_inv_order);
+    cudaFree(d_pcLU);
+    cudaFree(d_pcPiv);
+    cudaFree(d_pcbad);
+    cudaFree(d_kv);
+    cudaFree(d_kw);
+    cudaFree(d_kred);
     cudaFree(d_bcv);
     cudaFree(d_source);
     cudaFree(d_Q);
@@ -530,6 +547,67 @@ double* ensure(double*& p, size_t n) {
   return p;
 }
 
+// ---- Krylov vector kernels.  Reductions are deterministic: fixed-grid block
+// partial sums, then one block sums the partials in a fixed tree order.
+constexpr int KR_THREADS = 256, KR_BLOCKS = 592;
+
+__global__ void __launch_bounds__(KR_THREADS) k_dot_part(const double* __restrict__ a, const double* __restrict__ b,
+                                                         size_t n, double* __restrict__ part) {
+  __shared__ double sh[KR_THREADS];
+  double s = 0.0;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * KR_THREADS + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * KR_THREADS)
+    s += a[i] * b[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = KR_THREADS / 2; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void __launch_bounds__(KR_THREADS) k_dot_fin(const double* __restrict__ part, int np, double* out,
+                                                        int root) {
+  __shared__ double sh[KR_THREADS];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += KR_THREADS) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = KR_THREADS / 2; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = root ? sqrt(sh[0]) : sh[0];
+}
+// y -= (*coef) x
+__global__ void k_axpy_dev(double* __restrict__ y, const double* __restrict__ x, size_t n,
+                           const double* __restrict__ coef) {
+  const double a = *coef;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] -= a * x[i];
+}
+// y += a x
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, size_t n, double a) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] += a * x[i];
+}
+// y = x / (*den)  (den > 0), or y = x / den_h when den == nullptr
+__global__ void k_div(double* __restrict__ y, const double* __restrict__ x, size_t n, const double* den,
+                      double den_h) {
+  const double d = den ? *den : den_h;
+  if (!(d > 0.0)) return;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] = x[i] / d;
+}
+__global__ void k_sub(double* __restrict__ r, const double* __restrict__ b, const double* __restrict__ t, size_t n) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    r[i] = b[i] - t[i];
+}
+
 }  // namespace
 
 extern "C" {
@@ -600,6 +678,9 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     for (int k = 0; k < c->E; ++k) c->inv_order[c->order[k]] = k;
     ck(cudaMalloc(&c->d_order, c->E * sizeof(int32_t)), "cudaMalloc order");
     ck(cudaMemcpy(c->d_order, c->order.data(), c->E * sizeof(int32_t), cudaMemcpyHostToDevice), "upload order");
+    ck(cudaMalloc(&c->d_inv_order, c->E * sizeof(int32_t)), "cudaMalloc inv_order");
+    ck(cudaMemcpy(c->d_inv_order, c->inv_order.data(), c->E * sizeof(int32_t), cudaMemcpyHostToDevice),
+       "upload inv_order");
 
     build_connectivity(*c, *s, *ph);
 
@@ -642,6 +723,7 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     d.source = nullptr;
     d.err = c->d_err;
     d.E = c->E;
+    d.inv_order = c->d_inv_order;
     {
       const char* fs = std::getenv("LDG_FACE_SHARE");
       if (!(fs && std::string(fs) == "0")) {
@@ -891,6 +973,207 @@ int ldg_split_matvec(ldg_ctx* c, double adt, const double* v, double* y) {
       w = c->d_w;
     }
     return finish(c, o.split(c->dc, c->d_K11, c->d_K12, v, w, adt, y));
+  });
+}
+
+// ----------------------------------------- block-Jacobi preconditioner + GMRES
+//
+int ldg_precond_build(ldg_ctx* c, double alpha_dt) {
+  return guarded(c, [&]() -> int {
+    if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+    const ldg::Ops& o = *c->ops;
+    if (o.pc_ne <= 0)
+      throw ldg_error(LDG_ERR_CONFIG, "block-Jacobi preconditioner: element blocks above 128 unknowns "
+                                      "(3-D p >= 2) are not supported");
+    const size_t ne = static_cast<size_t>(o.pc_ne);
+    if (!c->d_pcLU) ck(cudaMalloc(&c->d_pcLU, static_cast<size_t>(c->E) * ne * ne * sizeof(double)), "cudaMalloc LU");
+    if (!c->d_pcPiv) ck(cudaMalloc(&c->d_pcPiv, static_cast<size_t>(c->E) * ne * sizeof(int32_t)), "cudaMalloc piv");
+    if (!c->d_pcbad) ck(cudaMalloc(&c->d_pcbad, sizeof(int)), "cudaMalloc flag");
+    ck(cudaMemsetAsync(c->d_pcbad, 0xff, sizeof(int), c->stream), "reset flag");
+    c->pc_valid = false;
+    ck(o.pc_build(c->dc, c->d_K11, c->d_K12, c->d_K21, alpha_dt, c->d_pcLU, c->d_pcPiv, c->d_pcbad), "pc build");
+    int bad = -1;
+    ck(cudaMemcpyAsync(&bad, c->d_pcbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "read flag");
+    ck(cudaStreamSynchronize(c->stream), "stream synchronize");
+    if (bad >= 0)
+      throw ldg_error(LDG_ERR_SOLVER, "singular block-Jacobi block at element " + std::to_string(bad));
+    c->pc_valid = true;
+    return LDG_OK;
+  });
+}
+
+int ldg_precond_apply(ldg_ctx* c, const double* r, double* z) {
+  return guarded(c, [&]() -> int {
+    if (!c->pc_valid) throw ldg_error(LDG_ERR_SOLVER, "preconditioner not built");
+    const ldg::Ops& o = *c->ops;
+    return finish(c, o.pc_apply(c->dc, c->d_pcLU, c->d_pcPiv, r, z));
+  });
+}
+
+int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rtol, int32_t maxit, int32_t restart,
+              int32_t use_precond, int32_t* iters, int32_t* converged, double* resnorm) {
+  return guarded(c, [&]() -> int {
+    if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+    if (!(rtol > 0.0) || maxit < 1 || restart < 1 || !b || !x)
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "gmres: rtol > 0, maxit >= 1, restart >= 1 and vectors required");
+    if (use_precond && !c->pc_valid) throw ldg_error(LDG_ERR_SOLVER, "preconditioner not built");
+    const ldg::Ops& o = *c->ops;
+    const size_t n = c->nU();
+    const int mr = restart;
+    if (c->kv_restart < mr) {
+      cudaFree(c->d_kv);
+      c->d_kv = nullptr;
+      ck(cudaMalloc(&c->d_kv, (2 * static_cast<size_t>(mr) + 1) * n * sizeof(double)), "cudaMalloc Krylov");
+      cudaFree(c->d_kred);
+      c->d_kred = nullptr;
+      c->kv_restart = mr;
+    }
+    ensure(c->d_kw, 3 * n);
+    ensure(c->d_kred, KR_BLOCKS + (static_cast<size_t>(mr) + 1) * mr + 8);
+    double* V = c->d_kv;                 // (mr+1) x n
+    double* Zs = c->d_kv + (mr + 1) * n;  // mr x n
+    double* w = c->d_kw;
+    double* t = w + n;
+    double* r = t + n;
+    double* part = c->d_kred;
+    double* Hd = part + KR_BLOCKS;       // column-major (mr+1) x mr
+    double* sc = Hd + (mr + 1) * mr;     // scalars
+    cudaStream_t st = c->stream;
+    const int vb = 592, vt = 256;
+    auto dot = [&](const double* a, const double* bb, double* out, int root) {
+      c->launches += 2;
+      k_dot_part<<<KR_BLOCKS, KR_THREADS, 0, st>>>(a, bb, n, part);
+      k_dot_fin<<<1, KR_THREADS, 0, st>>>(part, KR_BLOCKS, out, root);
+    };
+    auto op = [&](const double* v, double* y) {
+      const double* ww = nullptr;
+      if (c->second) {
+        ensure(c->d_w, c->nQ());
+        ck(o.spmv21(c->dc, c->d_K21, v, c->d_w), "K21 launch");
+        ww = c->d_w;
+      }
+      ck(o.split(c->dc, c->d_K11, c->d_K12, v, ww, alpha_dt, y), "split launch");
+    };
+    auto host_scalar = [&](const double* dptr_) {
+      double h = 0.0;
+      ck(cudaMemcpyAsync(&h, dptr_, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H scalar");
+      ck(cudaStreamSynchronize(st), "stream synchronize");
+      return h;
+    };
+    ck(cudaMemsetAsync(x, 0, n * sizeof(double), st), "zero x");
+    dot(b, b, sc, 1);
+    const double bn = host_scalar(sc);
+    *iters = 0;
+    *converged = 0;
+    *resnorm = bn;
+    if (bn == 0.0) {
+      *converged = 1;
+      return LDG_OK;
+    }
+    ck(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy b");
+    std::vector<double> H(static_cast<size_t>(mr + 1) * mr), cs(mr), sn(mr), g(mr + 1), col(mr + 1);
+    double beta = bn;
+    int it = 0;
+    while (true) {
+      k_div<<<vb, vt, 0, st>>>(V, r, n, nullptr, beta);
+      ++c->launches;
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int j = 0;
+      for (; j < mr && it < maxit; ++j) {
+        double* Vj = V + static_cast<size_t>(j) * n;
+        double* Zj = use_precond ? Zs + static_cast<size_t>(j) * n : Vj;
+        if (use_precond) ck(o.pc_apply(c->dc, c->d_pcLU, c->d_pcPiv, Vj, Zj), "pc apply");
+        op(Zj, w);
+        for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+          double* hij = Hd + static_cast<size_t>(j) * (mr + 1) + i;
+          dot(w, V + static_cast<size_t>(i) * n, hij, 0);
+          k_axpy_dev<<<vb, vt, 0, st>>>(w, V + static_cast<size_t>(i) * n, n, hij);
+          ++c->launches;
+        }
+        double* hn_d = Hd + static_cast<size_t>(j) * (mr + 1) + j + 1;
+        dot(w, w, hn_d, 1);
+        k_div<<<vb, vt, 0, st>>>(V + static_cast<size_t>(j + 1) * n, w, n, hn_d, 0.0);
+        ++c->launches;
+        ck(cudaMemcpyAsync(col.data(), Hd + static_cast<size_t>(j) * (mr + 1), (j + 2) * sizeof(double),
+                           cudaMemcpyDeviceToHost, st), "D2H Hessenberg column");
+        ck(cudaStreamSynchronize(st), "stream synchronize");
+        const double hn = col[j + 1];
+        if (!std::isfinite(hn)) throw ldg_error(LDG_ERR_SOLVER, "gmres: numerical breakdown (non-finite Krylov vector)");
+        for (int i = 0; i <= j + 1; ++i) H[i * mr + j] = col[i];
+        for (int i = 0; i < j; ++i) {
+          const double a0 = H[i * mr + j], a1 = H[(i + 1) * mr + j];
+          H[i * mr + j] = cs[i] * a0 + sn[i] * a1;
+          H[(i + 1) * mr + j] = -sn[i] * a0 + cs[i] * a1;
+        }
+        const double a0 = H[j * mr + j], a1 = H[(j + 1) * mr + j];
+        const double den = std::hypot(a0, a1);
+        cs[j] = den > 0.0 ? a0 / den : 1.0;
+        sn[j] = den > 0.0 ? a1 / den : 0.0;
+        H[j * mr + j] = den;
+        H[(j + 1) * mr + j] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        ++it;
+        if (std::fabs(g[j + 1]) <= rtol * bn || hn == 0.0) {
+          ++j;
+          break;
+        }
+      }
+      std::vector<double> y(j, 0.0);
+      for (int i = j - 1; i >= 0; --i) {
+        double s_ = g[i];
+        for (int q = i + 1; q < j; ++q) s_ -= H[i * mr + q] * y[q];
+        y[i] = s_ / H[i * mr + i];
+      }
+      for (int i = 0; i < j; ++i)
+      {
+        k_axpy<<<vb, vt, 0, st>>>(x, use_precond ? Zs + static_cast<size_t>(i) * n : V + static_cast<size_t>(i) * n,
+                                  n, y[i]);
+        ++c->launches;
+      }
+      op(x, t);
+      k_sub<<<vb, vt, 0, st>>>(r, b, t, n);
+      ++c->launches;
+      dot(r, r, sc, 1);
+      beta = host_scalar(sc);
+      *resnorm = beta;
+      if (beta <= rtol * bn) {
+        *converged = 1;
+        break;
+      }
+      if (it >= maxit) break;
+    }
+    *iters = it;
+    return finish(c, cudaGetLastError());
+  });
+}
+
+int ldg_gmres_host(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rtol, int32_t maxit,
+                   int32_t restart, int32_t use_precond, int32_t* iters, int32_t* converged, double* resnorm) {
+  return guarded(c, [&]() -> int {
+    ensure(c->d_hx, c->nU());
+    ensure(c->d_hy, c->nU());
+    ck(cudaMemcpyAsync(c->d_hx, b, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D b");
+    const int st = ldg_gmres(c, alpha_dt, c->d_hx, c->d_hy, rtol, maxit, restart, use_precond, iters, converged,
+                             resnorm);
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(x, c->d_hy, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H x");
+    return finish(c, cudaSuccess) == LDG_OK && cudaStreamSynchronize(c->stream) == cudaSuccess ? LDG_OK
+                                                                                               : LDG_ERR_CUDA;
+  });
+}
+
+int ldg_precond_apply_host(ldg_ctx* c, const double* r, double* z) {
+  return guarded(c, [&]() -> int {
+    ensure(c->d_hx, c->nU());
+    ensure(c->d_hy, c->nU());
+    ck(cudaMemcpyAsync(c->d_hx, r, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D r");
+    const int st = ldg_precond_apply(c, c->d_hx, c->d_hy);
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(z, c->d_hy, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H z");
+    ck(cudaStreamSynchronize(c->stream), "stream synchronize");
+    return LDG_OK;
   });
 }
 

@@ -35,6 +35,7 @@ struct KParams {
   const double* source;  // reference numbering, may be null
   DevError* err;
   const int2* fpart;     // [k][2D] face partner {k', 2 dir' + side'} ({-1, 0}: none)
+  const int32_t* inv_order;  // reference element e -> processing index k
   const int32_t* owned;  // owned faces (k*2D + ds) of the Jacobian chunks, or null
   int E;                 // elements
   int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2, bit2 skip the staged bulk store
@@ -2939,6 +2940,197 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
   for (int c = 0; c < M; ++c)
 #pragma unroll
     for (int d = 0; d < D; ++d) w[wo + c * D + d] = acc[c][d];
+}
+
+// ===================================================== block-Jacobi preconditioner
+// (PAPER.md:725-740).  A~ equals A = K11 + K12 K21
+// on the block-diagonal Line-DG pattern (row and column node in the same
+// element and on a common coordinate line), zero elsewhere; the product's
+// entries that land on the pattern are summed over every middle node,
+// neighbour elements included.  One CTA per element: the element block of
+// I - alpha_dt A~ is gathered from the block-row store into shared memory,
+// LU-factorised with partial pivoting (the oracle's pivot rule: the first
+// largest |a_ik|), and written column-major with its pivots.
+template <class C>
+struct PcCfg {
+  static constexpr int NE = C::NPE * C::M;  // unknowns per element
+  static constexpr int LDM = NE | 1;        // odd row stride (shared-memory banks)
+  static constexpr bool OK = NE <= 128;
+  static constexpr int THREADS = 256;
+  static constexpr size_t smem() { return sizeof(double) * NE * LDM; }
+};
+
+template <class C>
+__device__ __forceinline__ bool pc_on_line(int a, int b) {
+  int same = 0;
+#pragma unroll
+  for (int d = 0; d < C::D; ++d) {
+    same += (a % C::NP) == (b % C::NP);
+    a /= C::NP;
+    b /= C::NP;
+  }
+  return same >= C::D - 1;
+}
+
+template <class C>
+__global__ void __launch_bounds__(PcCfg<C>::THREADS)
+k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __restrict__ K12,
+           const double* __restrict__ K21, double adt, double* __restrict__ LUc, int32_t* __restrict__ piv,
+           int* __restrict__ bad) {
+  using PC = PcCfg<C>;
+  constexpr int NE = PC::NE, LDM = PC::LDM, M = C::M, NPE = C::NPE, NT = C::NT, D = C::D, MD = C::MD,
+                NS11 = C::NS11, NS12 = C::NS12, R12 = C::R12, NSIN = C::D * C::P + 1;
+  constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+  extern __shared__ __align__(16) double Ms[];
+  __shared__ int spiv;
+  __shared__ int sbad;
+  const int k = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  const size_t e = kp.order[k];
+  for (int x = tid; x < NE * LDM; x += nthr) Ms[x] = 0.0;
+  if (tid == 0) sbad = 0;
+  __syncthreads();
+  // K11: the in-element line slots (each (row, column) node pair once)
+  for (int w = tid; w < NPE * NSIN * M * M; w += nthr) {
+    const int b = w % M, a = (w / M) % M, rest = w / (M * M), slot = rest % NSIN, nd = rest / NSIN;
+    const int64_t col = slot_col<C, NSIN>(kp, k, e, nd, slot, 0);
+    const int cl = static_cast<int>(col - static_cast<int64_t>(e) * NPE);
+    const size_t T = static_cast<size_t>(k) * C::TPE + nd / NT;
+    const double v = K11[(((T * NS11 + slot) * M + a) * NT + nd % NT) * M + b];
+    Ms[(nd * M + a) * LDM + cl * M + b] = v;
+  }
+  __syncthreads();
+  if (C::SECOND) {
+    // K12 K21 on the pattern: every (row, K12 slot) path through its middle node
+    for (int w = tid; w < NPE * NS12; w += nthr) {
+      const int nd = w / NS12, s12 = w - nd * NS12;
+      const int64_t mid = slot_col<C, NSIN>(kp, k, e, nd, s12, 1);
+      if (mid < 0) continue;
+      const int em = static_cast<int>(mid / NPE), ndm = static_cast<int>(mid - static_cast<int64_t>(em) * NPE);
+      const int km = __ldg(kp.inv_order + em);
+      const size_t T12 = static_cast<size_t>(k) * C::TPE + nd / NT;
+      const size_t T21 = static_cast<size_t>(km) * C::TPE + ndm / NT;
+      for (int s21 = 0; s21 < NS12; ++s21) {
+        const int64_t col = slot_col<C, NSIN>(kp, km, static_cast<size_t>(em), ndm, s21, 2);
+        if (col < 0 || col / NPE != static_cast<int64_t>(e)) continue;
+        const int cl = static_cast<int>(col - static_cast<int64_t>(e) * NPE);
+        if (!pc_on_line<C>(nd, cl)) continue;
+        double k21[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) k21[d] = __ldg(K21 + ((T21 * NS12 + s21) * NT + ndm % NT) * D + d);
+        for (int ap = 0; ap < R12; ++ap)
+          for (int b = 0; b < M; ++b) {
+            double sum = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              sum += __ldg(K12 + (((T12 * NS12 + s12) * R12 + ap) * NT + nd % NT) * MD + b * D + d) * k21[d];
+            atomicAdd(&Ms[(nd * M + ap + A0) * LDM + cl * M + b], sum);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  for (int x = tid; x < NE * NE; x += nthr) {
+    const int i = x / NE, j = x - i * NE;
+    Ms[i * LDM + j] = (i == j ? 1.0 : 0.0) - adt * Ms[i * LDM + j];
+  }
+  __syncthreads();
+  // LU with partial pivoting
+  for (int kk = 0; kk < NE; ++kk) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = kk;
+      for (int i = kk + tid; i < NE; i += 32) {
+        const double v = fabs(Ms[i * LDM + kk]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, off);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (tid == 0) {
+        spiv = bi;
+        piv[static_cast<size_t>(k) * NE + kk] = bi;
+        if (!(best > 0.0)) sbad = 1;
+      }
+    }
+    __syncthreads();
+    const int pr = spiv;
+    if (pr != kk)
+      for (int j = tid; j < NE; j += nthr) {
+        const double t = Ms[kk * LDM + j];
+        Ms[kk * LDM + j] = Ms[pr * LDM + j];
+        Ms[pr * LDM + j] = t;
+      }
+    __syncthreads();
+    const double ip = 1.0 / Ms[kk * LDM + kk];
+    for (int i = kk + 1 + tid; i < NE; i += nthr) Ms[i * LDM + kk] *= ip;
+    __syncthreads();
+    const int rem = NE - kk - 1;
+    for (int x = tid; x < rem * rem; x += nthr) {
+      const int i = kk + 1 + x / rem, j = kk + 1 + x % rem;
+      Ms[i * LDM + j] -= Ms[i * LDM + kk] * Ms[kk * LDM + j];
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && sbad) atomicCAS(bad, -1, static_cast<int>(e));
+  double* out = LUc + static_cast<size_t>(k) * NE * NE;
+  for (int x = tid; x < NE * NE; x += nthr) {
+    const int j = x / NE, i = x - j * NE;
+    out[x] = Ms[i * LDM + j];  // column-major
+  }
+}
+
+// z = (I - alpha_dt A~)^-1 r, one warp per element: row interchanges, then
+// column-oriented unit-lower and upper triangular solves on coalesced column
+// loads of the element's LU factors.
+template <class C>
+__global__ void __launch_bounds__(128)
+k_pc_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* __restrict__ piv,
+           const double* __restrict__ r, double* __restrict__ z) {
+  using PC = PcCfg<C>;
+  constexpr int NE = PC::NE;
+  __shared__ double zs[4][NE];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + wl;
+  if (k >= kp.E) return;
+  const size_t e = __ldg(kp.order + k);
+  double* zw = zs[wl];
+  const double* re = r + e * NE;
+  for (int i = lane; i < NE; i += 32) zw[i] = re[i];
+  __syncwarp();
+  if (lane == 0) {
+    const int32_t* pv = piv + static_cast<size_t>(k) * NE;
+    for (int i = 0; i < NE; ++i) {
+      const int p = pv[i];
+      const double t = zw[i];
+      zw[i] = zw[p];
+      zw[p] = t;
+    }
+  }
+  __syncwarp();
+  const double* L = LUc + static_cast<size_t>(k) * NE * NE;
+  for (int j = 0; j < NE - 1; ++j) {
+    const double zj = zw[j];
+    for (int i = j + 1 + lane; i < NE; i += 32) zw[i] -= L[j * NE + i] * zj;
+    __syncwarp();
+  }
+  for (int j = NE - 1; j >= 0; --j) {
+    if (lane == 0) zw[j] /= L[j * NE + j];
+    __syncwarp();
+    const double zj = zw[j];
+    for (int i = lane; i < j; i += 32) zw[i] -= L[j * NE + i] * zj;
+    __syncwarp();
+  }
+  double* ze = z + e * NE;
+  for (int i = lane; i < NE; i += 32) ze[i] = zw[i];
 }
 
 }  // namespace ldg

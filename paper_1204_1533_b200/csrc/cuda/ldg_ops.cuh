@@ -30,6 +30,7 @@ struct DevCtx {
   // face sharing of the endpoint flux Jacobians (null = every line end computes its own)
   const int2* fpart = nullptr;        // [k][2D]: partner {k', 2 dir' + side'} or {-1, 0}
   const int32_t* owned = nullptr;     // owned faces k*2D + ds, chunk by chunk
+  const int32_t* inv_order = nullptr; // reference element -> processing index
   const int64_t* owned_off = nullptr; // host: chunk c owns owned[owned_off[c] .. owned_off[c+1])
   int E = 0;
   long long* launches = nullptr;
@@ -51,6 +52,10 @@ struct Ops {
   cudaError_t (*spmv21)(const DevCtx&, const double* V21, const double* v, double* w);
   cudaError_t (*split)(const DevCtx&, const double* V11, const double* V12, const double* v,
                        const double* w, double adt, double* y);
+  int pc_ne;  // unknowns per element of the block-Jacobi blocks (0: not supported)
+  cudaError_t (*pc_build)(const DevCtx&, const double* V11, const double* V12, const double* V21, double adt,
+                          double* LUc, int32_t* piv, int* bad);
+  cudaError_t (*pc_apply)(const DevCtx&, const double* LUc, const int32_t* piv, const double* r, double* z);
 };
 
 template <class C>
@@ -73,6 +78,7 @@ struct Launch {
     kp.err = d.err;
     kp.fpart = d.fpart;
     kp.owned = d.owned;
+    kp.inv_order = d.inv_order;
     kp.E = d.E;
     static const int dbg = std::getenv("LDG_DEBUG_MASK") ? std::atoi(std::getenv("LDG_DEBUG_MASK")) : 0;
     kp.dbg = dbg;
@@ -324,11 +330,30 @@ struct Launch {
     return cudaGetLastError();
   }
 
+  static cudaError_t pc_build(const DevCtx& d, const double* V11, const double* V12, const double* V21, double adt,
+                              double* LUc, int32_t* piv, int* bad) {
+    if (!PcCfg<C>::OK) return cudaErrorNotSupported;
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_pc_build<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PcCfg<C>::smem());
+      init = true;
+    }
+    k_pc_build<C><<<d.E, PcCfg<C>::THREADS, PcCfg<C>::smem(), d.stream>>>(params(d), V11, V12, V21, adt, LUc, piv,
+                                                                         bad);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t pc_apply(const DevCtx& d, const double* LUc, const int32_t* piv, const double* r, double* z) {
+    if (!PcCfg<C>::OK) return cudaErrorNotSupported;
+    k_pc_apply<C><<<(d.E + 3) / 4, 128, 0, d.stream>>>(params(d), LUc, piv, r, z);
+    count(d);
+    return cudaGetLastError();
+  }
   static const Ops* table() {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
                             C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, chunk_elems, residual, gradient, jacobian, k21,
-                            spmv11, spmv12, spmv21, split};
+                            spmv11, spmv12, spmv21, split, PcCfg<C>::OK ? PcCfg<C>::NE : 0, pc_build, pc_apply};
     return &ops;
   }
 };

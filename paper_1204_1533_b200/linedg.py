@@ -245,6 +245,41 @@ class LineDG:
         self._check(self.lib.ldg_bsr_spmv(self._h, which, self._ptr(x), self._ptr(y)))
         return y
 
+    # ------------------------------------------------- preconditioned GMRES
+    def precond_build(self, alpha_dt: float):
+        """Block-Jacobi preconditioner of I - alpha_dt A~."""
+        self._check(self.lib.ldg_precond_build(self._h, alpha_dt))
+
+    def precond_apply(self, r, out=None):
+        if not _is_torch(r):
+            rh = np.ascontiguousarray(r, dtype=np.float64)
+            z = self._host_out(out, self.n_dofs)
+            self._check(self.lib.ldg_precond_apply_host(self._h, dptr(rh), dptr(z)))
+            return z
+        r = self._as_dev(r)
+        z = self._dev(self.n_dofs)
+        self._check(self.lib.ldg_precond_apply(self._h, self._ptr(r), self._ptr(z)))
+        return z
+
+    def gmres(self, alpha_dt: float, b, rtol: float = 1e-8, maxit: int = 50, restart: int = 30,
+              precond: bool = True, out=None):
+        """Right-preconditioned GMRES on (I - alpha_dt (K11 + K12 K21)) x = b:
+        (x, iterations, converged, ||b - A x||)."""
+        it = C.c_int32()
+        cv = C.c_int32()
+        rn = C.c_double()
+        if not _is_torch(b):
+            bh = np.ascontiguousarray(b, dtype=np.float64)
+            x = self._host_out(out, self.n_dofs)
+            self._check(self.lib.ldg_gmres_host(self._h, alpha_dt, dptr(bh), dptr(x), rtol, maxit, restart,
+                                                1 if precond else 0, C.byref(it), C.byref(cv), C.byref(rn)))
+            return x, it.value, bool(cv.value), rn.value
+        b = self._as_dev(b)
+        x = self._dev(self.n_dofs)
+        self._check(self.lib.ldg_gmres(self._h, alpha_dt, self._ptr(b), self._ptr(x), rtol, maxit, restart,
+                                       1 if precond else 0, C.byref(it), C.byref(cv), C.byref(rn)))
+        return x, it.value, bool(cv.value), rn.value
+
     def split_matvec(self, alpha_dt: float, v, out=None):
         """(I - alpha_dt (K11 + K12 K21)) v without forming the product."""
         if not _is_torch(v):
