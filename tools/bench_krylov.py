@@ -1,0 +1,68 @@
+"""Timing of the §8f row-1 solver pieces on one configuration (not the bench.py
+contract line): block-Jacobi build, one preconditioner application, one
+split matvec, and a fixed-iteration preconditioned GMRES solve.
+
+    python tools/bench_krylov.py [--config 1] [--iters 20] [--adt 0.05]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1204_1533_b200 import CONFIGS  # noqa: E402
+from paper_1204_1533_b200.linedg import LineDG  # noqa: E402
+
+
+def ev_time(fn, reps):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--adt", type=float, default=0.05)
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    case, U = cfg.build()
+    g = LineDG(case, cfg.physics)
+    src = cfg.source_for(case)
+    if src is not None:
+        g.set_source(src)
+    Ud = torch.from_numpy(U).cuda()
+    g.assemble_jacobians(Ud)
+    b = torch.from_numpy(case.normal_vector(g.m, cfg.vector_seed)).cuda()
+    t_build = ev_time(lambda: g.precond_build(a.adt), 3)
+    t_apply = ev_time(lambda: g.precond_apply(b), 10)
+    t_mv = ev_time(lambda: g.split_matvec(a.adt, b), 10)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x, it, cv, rn = g.gmres(a.adt, b, rtol=1e-30, maxit=a.iters, restart=a.iters, precond=True)
+    torch.cuda.synchronize()
+    t_gm = (time.perf_counter() - t0) * 1e3
+    ne = case.npe * g.m
+    lu_bytes = case.E * ne * ne * 8
+    print(json.dumps({"config": cfg.name, "dofs": g.n_dofs, "adt": a.adt,
+                      "precond_build_ms": t_build, "precond_apply_ms": t_apply,
+                      "precond_apply_GBs": lu_bytes / (t_apply * 1e-3) / 1e9, "lu_bytes": lu_bytes,
+                      "split_matvec_ms": t_mv, "gmres_iters": it, "gmres_ms": t_gm,
+                      "gmres_ms_per_iter": t_gm / max(it, 1), "resnorm": rn}))
+
+
+if __name__ == "__main__":
+    main()
