@@ -152,6 +152,31 @@ class Context {
     return y;
   }
 
+  // build_preconditioner(blocks, alpha_dt): block-Jacobi factors
+  // of I - alpha_dt A~ on the device (after assemble_jacobians).
+  void build_preconditioner(double alpha_dt) { check(ldg_precond_build(ctx_, alpha_dt), ctx_); }
+
+  // gmres(split_matvec, precond, b, rtol, maxit, restart):
+  // right-preconditioned GMRES on (I - alpha_dt (K11 + K12 K21)) x = b, x0 = 0.
+  struct GmresResult {
+    std::vector<double> x;
+    int iterations = 0;
+    bool converged = false;
+    double residual_norm = 0.0;
+  };
+  GmresResult gmres(double alpha_dt, const std::vector<double>& b, double rtol, int maxit, int restart,
+                    bool precond = true) {
+    GmresResult out;
+    out.x.assign(b.size(), 0.0);
+    int32_t it = 0, conv = 0;
+    check(ldg_gmres_host(ctx_, alpha_dt, b.data(), out.x.data(), rtol, maxit, restart, precond ? 1 : 0, &it, &conv,
+                         &out.residual_norm),
+          ctx_);
+    out.iterations = it;
+    out.converged = conv != 0;
+    return out;
+  }
+
   // Triplet export `i j value` of one matrix, scalar indices.
   struct Triplets {
     std::vector<long long> i, j;

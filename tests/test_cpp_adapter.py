@@ -35,7 +35,12 @@ int main() {
     GridFunction R = ctx.residual_first_order(U, 0.0);
     double mx = 0; for (double v : R.data) mx = v > mx ? v : (-v > mx ? -v : mx);
     std::printf("gpu residual max %g\n", mx);
-    return mx < 1e-11 ? 0 : 3;
+    ctx.assemble_jacobians(U, 0.0);
+    ctx.build_preconditioner(0.1);
+    std::vector<double> rhs(U.data.size(), 1.0);
+    auto sol = ctx.gmres(0.1, rhs, 1e-10, 50, 50, true);
+    std::printf("gmres %d iterations, residual %g\n", sol.iterations, sol.residual_norm);
+    return (mx < 1e-11 && sol.converged) ? 0 : 3;
   } catch (const std::exception& e) {
     std::printf("threw: %s\n", e.what());
     return 2;
