@@ -197,6 +197,36 @@ int ldg_gmres(ldg_ctx* ctx, double alpha_dt, const double* b, double* x, double 
 int ldg_gmres_host(ldg_ctx* ctx, double alpha_dt, const double* b, double* x, double rtol, int32_t maxit,
                            int32_t restart, int32_t use_precond, int32_t* iters, int32_t* converged,
                            double* resnorm);
+/* Time integration.
+   rk4_step: classical explicit RK4 on dU/dt = R(U).  dirk3_step: the paper's
+   L-stable three-stage third-order DIRK (alpha = 0.435866521508459), stage
+   slopes K_i solved by Newton on K - R(U_n + dt (sum_{j<i} a_ij K_j + alpha K))
+   with the shift form (I - alpha dt A) dK = -(K - R); each linear solve is
+   gmres_iters iterations of (block-Jacobi preconditioned) GMRES.  Jacobian
+   reuse: the context's assembled Jacobian is kept across
+   stages and steps and reassembled (at the current stage state) only when a
+   stage's Newton count reaches recompute_threshold, or when none exists; the
+   preconditioner is rebuilt when the Jacobian or alpha dt changes.  U is a
+   device vector updated in place.  Step failure (max_newton reached) ->
+   LDG_ERR_SOLVER; non-finite stages -> LDG_ERR_PHYSICAL_STATE / LDG_ERR_SOLVER. */
+typedef struct ldg_newton_cfg {
+  int32_t gmres_iters;         /* GMRES iterations per Newton update (paper: 5) */
+  int32_t recompute_threshold; /* Newton iterations of one stage solve before reassembly (paper: 15) */
+  int32_t max_newton;          /* cap per stage solve */
+  int32_t use_precond;         /* block-Jacobi (1) or none (0) */
+  double newton_tol;           /* stage converged when ||K - R(U_stage)||_inf <= newton_tol */
+} ldg_newton_cfg;
+typedef struct ldg_solver_stats {
+  int32_t newton_iters;        /* Newton updates over the step, all stages */
+  int32_t gmres_iters;         /* GMRES iterations over the step */
+  int32_t jacobian_assemblies; /* Jacobian (re)assemblies during the step */
+  int32_t residual_evals;      /* residual evaluations during the step */
+  double residual_norm;        /* final ||K - R||_inf of the last stage */
+} ldg_solver_stats;
+int ldg_rk4_step(ldg_ctx* ctx, double* U, double t, double dt);
+int ldg_dirk3_step(ldg_ctx* ctx, double* U, double t, double dt, const ldg_newton_cfg* cfg,
+                   ldg_solver_stats* stats);
+
 /* Export of the node pattern (host arrays of nnzb int64) and block values
  * (host array nnzb*block_rows*block_cols, row-major blocks), reference numbering.
  * Any pointer may be NULL. */

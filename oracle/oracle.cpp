@@ -9,6 +9,7 @@
 //   assemble_jacobians (Analytic + FD)
 //   CscMatrix, split_matvec
 //   build_preconditioner, gmres
+//   rk4_step, dirk3_step (Newton, reuse)
 // It follows the reference's numerics literally where they are specified:
 // r = M^-1 b through the Cholesky factor of M column by column
 // (basis.cpp:81-88, 185-189), fluxes at the quadrature points of the
@@ -75,6 +76,7 @@ struct Ctx {
   std::vector<double> pcLU;
   std::vector<int32_t> pcPiv;
   bool pc_built = false;
+  double pc_adt = 0.0;
   std::string err;
   std::vector<double> err_state;
   int err_elem = -1, err_node = -1;
@@ -1224,6 +1226,7 @@ int lo_precond_build(lo_ctx* x, double adt) {
     if (bad.load() >= 0)
       throw std::runtime_error("oracle: singular preconditioner block at element " + std::to_string(bad.load()));
     c.pc_built = true;
+    c.pc_adt = adt;
   });
 }
 
@@ -1353,6 +1356,104 @@ int lo_gmres(const lo_ctx* x, double adt, const double* b, double rtol, int32_t 
       if (it >= maxit) break;
     }
     *iters = it;
+  });
+}
+
+// ---- time integration
+namespace {
+double inf_norm(const double* a, size_t n) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i) m = std::max(m, std::fabs(a[i]));
+  return m;
+}
+}  // namespace
+
+int lo_rk4_step(lo_ctx* x, double* U, double t, double dt) {
+  return guarded([&] {
+    const Ctx& c = x->c;
+    const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
+    std::vector<double> k1(n), k2(n), k3(n), k4(n), us(n);
+    auto F = [&](const double* u, double* k, int stage) {
+      if (lo_residual(x, u, t, k, nullptr, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+      for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(k[i])) throw std::runtime_error("oracle: rk4 blow-up at stage " + std::to_string(stage));
+    };
+    F(U, k1.data(), 1);
+    for (size_t i = 0; i < n; ++i) us[i] = U[i] + 0.5 * dt * k1[i];
+    F(us.data(), k2.data(), 2);
+    for (size_t i = 0; i < n; ++i) us[i] = U[i] + 0.5 * dt * k2[i];
+    F(us.data(), k3.data(), 3);
+    for (size_t i = 0; i < n; ++i) us[i] = U[i] + dt * k3[i];
+    F(us.data(), k4.data(), 4);
+    for (size_t i = 0; i < n; ++i) U[i] += dt / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+  });
+}
+
+// DIRK3: a = [[al,0,0],[tau2-al,al,0],[b1,b2,al]], b = (b1, b2, al).
+int lo_dirk3_step(lo_ctx* x, double* U, double t, double dt, const ldg_newton_cfg* cfg, ldg_solver_stats* st) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    if (!(dt > 0.0) || !cfg || cfg->gmres_iters < 1 || cfg->recompute_threshold < 1 || cfg->max_newton < 1)
+      throw std::invalid_argument("oracle: dirk3 arguments");
+    const double al = 0.435866521508459, tau2 = (1.0 + al) / 2.0;
+    const double b1 = -(6.0 * al * al - 16.0 * al + 1.0) / 4.0, b2 = (6.0 * al * al - 20.0 * al + 5.0) / 4.0;
+    const double A[3][3] = {{al, 0.0, 0.0}, {tau2 - al, al, 0.0}, {b1, b2, al}};
+    const double B[3] = {b1, b2, al};
+    const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
+    const double adt = al * dt;
+    ldg_solver_stats s{};
+    auto assemble = [&](const double* u) {
+      if (lo_assemble(x, u, t, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+      ++s.jacobian_assemblies;
+      c.pc_built = false;
+    };
+    auto ensure_pc = [&]() {
+      if (cfg->use_precond && (!c.pc_built || c.pc_adt != adt))
+        if (lo_precond_build(x, adt) != LDG_OK) throw std::runtime_error(g_err);
+    };
+    auto F = [&](const double* u, double* k) {
+      if (lo_residual(x, u, t, k, nullptr, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+      ++s.residual_evals;
+    };
+    if (!c.K[LDG_K11].built) assemble(U);
+    ensure_pc();
+    std::vector<std::vector<double>> K(3, std::vector<double>(n));
+    std::vector<double> Kc(n), us(n), Fv(n), G(n), dK(n);
+    F(U, Kc.data());  // initial slope guess of stage 1: R(U_n)
+    for (int i = 0; i < 3; ++i) {
+      int it = 0;
+      while (true) {
+        for (size_t q = 0; q < n; ++q) {
+          double sacc = 0.0;
+          for (int j = 0; j < i; ++j) sacc += A[i][j] * K[j][q];
+          us[q] = U[q] + dt * (sacc + al * Kc[q]);
+        }
+        F(us.data(), Fv.data());
+        for (size_t q = 0; q < n; ++q) G[q] = Kc[q] - Fv[q];
+        const double gn = inf_norm(G.data(), n);
+        if (!std::isfinite(gn)) throw std::runtime_error("oracle: dirk3 non-finite stage");
+        s.residual_norm = gn;
+        if (gn <= cfg->newton_tol) break;
+        if (it >= cfg->max_newton) throw std::runtime_error("oracle: dirk3 step failure (Newton did not converge)");
+        if (it > 0 && it % cfg->recompute_threshold == 0) {
+          assemble(us.data());
+          ensure_pc();
+        }
+        for (size_t q = 0; q < n; ++q) G[q] = -G[q];
+        int32_t gi = 0, gc = 0;
+        double gr = 0.0;
+        if (lo_gmres(x, adt, G.data(), 1e-300, cfg->gmres_iters, cfg->gmres_iters, cfg->use_precond, dK.data(), &gi,
+                     &gc, &gr) != LDG_OK)
+          throw std::runtime_error(g_err);
+        s.gmres_iters += gi;
+        for (size_t q = 0; q < n; ++q) Kc[q] += dK[q];
+        ++it;
+        ++s.newton_iters;
+      }
+      K[i] = Kc;
+    }
+    for (size_t q = 0; q < n; ++q) U[q] += dt * (B[0] * K[0][q] + B[1] * K[1][q] + B[2] * K[2][q]);
+    if (st) *st = s;
   });
 }
 

@@ -55,6 +55,10 @@ def lib():
         L.lo_spmv.argtypes = [vp, C.c_int32, _dp, _dp]
         L.lo_split_matvec.argtypes = [vp, C.c_double, _dp, _dp]
         L.lo_fd_dense.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
+        from paper_1204_1533_b200._abi import LdgNewtonCfg, LdgSolverStats
+        L.lo_rk4_step.argtypes = [vp, _dp, C.c_double, C.c_double]
+        L.lo_dirk3_step.argtypes = [vp, _dp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
+                                    C.POINTER(LdgSolverStats)]
         L.lo_precond_build.argtypes = [vp, C.c_double]
         L.lo_precond_apply.argtypes = [vp, _dp, _dp]
         L.lo_gmres.argtypes = [vp, C.c_double, _dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, _dp,
@@ -213,6 +217,19 @@ class Oracle:
         self._check(self.L.lo_gmres(self.h, adt, _d(b), rtol, maxit, restart, 1 if precond else 0, _d(x),
                                     C.byref(it), C.byref(cv), C.byref(rn)))
         return x, it.value, bool(cv.value), rn.value
+
+    def rk4_step(self, U, dt, t=0.0):
+        U = np.array(U, dtype=np.float64)
+        self._check(self.L.lo_rk4_step(self.h, _d(U), t, dt))
+        return U
+
+    def dirk3_step(self, U, dt, cfg, t=0.0):
+        """(U_next, stats dict); cfg = paper_1204_1533_b200._abi.newton_cfg(...)."""
+        from paper_1204_1533_b200._abi import LdgSolverStats
+        U = np.array(U, dtype=np.float64)
+        st = LdgSolverStats()
+        self._check(self.L.lo_dirk3_step(self.h, _d(U), t, dt, C.byref(cfg), C.byref(st)))
+        return U, st.as_dict()
 
     def fd_dense(self, which, U, Q=None):
         U = np.ascontiguousarray(U, dtype=np.float64)

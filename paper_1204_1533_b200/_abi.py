@@ -138,6 +138,26 @@ def host_lib() -> C.CDLL:
     return _host
 
 
+class LdgNewtonCfg(C.Structure):
+    """ldg_newton_cfg (include/linedg_b200.h)."""
+    _fields_ = [("gmres_iters", C.c_int32), ("recompute_threshold", C.c_int32), ("max_newton", C.c_int32),
+                ("use_precond", C.c_int32), ("newton_tol", C.c_double)]
+
+
+class LdgSolverStats(C.Structure):
+    """ldg_solver_stats (include/linedg_b200.h)."""
+    _fields_ = [("newton_iters", C.c_int32), ("gmres_iters", C.c_int32), ("jacobian_assemblies", C.c_int32),
+                ("residual_evals", C.c_int32), ("residual_norm", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def newton_cfg(gmres_iters=5, recompute_threshold=15, max_newton=50, use_precond=True, newton_tol=1e-8):
+    """The paper's Newton/GMRES policy."""
+    return LdgNewtonCfg(gmres_iters, recompute_threshold, max_newton, 1 if use_precond else 0, newton_tol)
+
+
 GPU_SYMBOLS = [
     "ldg_create", "ldg_destroy", "ldg_last_error", "ldg_last_error_state", "ldg_components",
     "ldg_num_dofs", "ldg_set_source", "ldg_residual", "ldg_residual_uq", "ldg_gradient",
@@ -146,6 +166,7 @@ GPU_SYMBOLS = [
     "ldg_residual_host", "ldg_jacobian_assemble_host", "ldg_bsr_spmv_host", "ldg_split_matvec_host",
     "ldg_kernel_launches", "ldg_jacobian_bytes",
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
+    "ldg_rk4_step", "ldg_dirk3_step",
 ]
 
 
@@ -188,6 +209,9 @@ def gpu_lib() -> C.CDLL:
               C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         L.ldg_gmres.argtypes = _g
         L.ldg_gmres_host.argtypes = [vp, C.c_double, _dp, _dp] + _g[4:]
+        L.ldg_rk4_step.argtypes = [vp, vp, C.c_double, C.c_double]
+        L.ldg_dirk3_step.argtypes = [vp, vp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
+                                     C.POINTER(LdgSolverStats)]
         L.ldg_kernel_launches.argtypes = [vp]
         L.ldg_kernel_launches.restype = C.c_int64
         L.ldg_jacobian_bytes.argtypes = [vp]

@@ -78,6 +78,8 @@ struct ldg_ctx {
   int32_t* d_pcPiv = nullptr;
   int* d_pcbad = nullptr;
   bool pc_valid = false;
+  double pc_adt = 0.0;
+  double* d_ti = nullptr;  // time-integration workspace (8 vectors)
   double* d_kv = nullptr;  // Krylov vectors V[0..restart] then Z[0..restart-1]
   int kv_restart = 0;
   double* d_kw = nullptr;  // w, t, r
@@ -124,6 +126,7 @@ struct ldg_ctx {
     cudaFree(d_kv);
     cudaFree(d_kw);
     cudaFree(d_kred);
+    cudaFree(d_ti);
     cudaFree(d_bcv);
     cudaFree(d_source);
     cudaFree(d_Q);
@@ -602,6 +605,80 @@ __global__ void k_div(double* __restrict__ y, const double* __restrict__ x, size
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     y[i] = x[i] / d;
 }
+// max |a_i|: block partials, then one block (deterministic)
+__global__ void __launch_bounds__(KR_THREADS) k_amax_part(const double* __restrict__ a, size_t n,
+                                                          double* __restrict__ part) {
+  __shared__ double sh[KR_THREADS];
+  double s = 0.0;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * KR_THREADS + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * KR_THREADS) {
+    const double v = fabs(a[i]);
+    s = (v > s || v != v) ? v : s;  // NaN propagates
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = KR_THREADS / 2; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) {
+      const double v = sh[threadIdx.x + o];
+      if (v > sh[threadIdx.x] || v != v) sh[threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void __launch_bounds__(KR_THREADS) k_amax_fin(const double* __restrict__ part, int np, double* out) {
+  __shared__ double sh[KR_THREADS];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += KR_THREADS) s = (part[i] > s || part[i] != part[i]) ? part[i] : s;
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = KR_THREADS / 2; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) {
+      const double v = sh[threadIdx.x + o];
+      if (v > sh[threadIdx.x] || v != v) sh[threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+// us = U + dt (a0 K0 + a1 K1 + al Kc)   (stage state; nprev previous slopes)
+__global__ void k_stage_state(double* __restrict__ us, const double* __restrict__ U, const double* __restrict__ K0,
+                              const double* __restrict__ K1, const double* __restrict__ Kc, size_t n, double dt,
+                              double a0, double a1, double al, int nprev) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    double sacc = 0.0;
+    if (nprev > 0) sacc += a0 * K0[i];
+    if (nprev > 1) sacc += a1 * K1[i];
+    us[i] = U[i] + dt * (sacc + al * Kc[i]);
+  }
+}
+// G = Fv - Kc (the Newton right-hand side -(K - F))
+__global__ void k_rhs(double* __restrict__ g, const double* __restrict__ Kc, const double* __restrict__ Fv, size_t n) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    g[i] = -(Kc[i] - Fv[i]);
+}
+// U += dt (b0 K0 + b1 K1 + b2 K2)
+__global__ void k_dirk_update(double* __restrict__ U, const double* __restrict__ K0, const double* __restrict__ K1,
+                              const double* __restrict__ K2, size_t n, double dt, double b0, double b1, double b2) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    U[i] += dt * (b0 * K0[i] + b1 * K1[i] + b2 * K2[i]);
+}
+// RK4: us = U + f k ; final U += dt/6 (k1 + 2 k2 + 2 k3 + k4)
+__global__ void k_rk_state(double* __restrict__ us, const double* __restrict__ U, const double* __restrict__ k,
+                           size_t n, double f) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    us[i] = U[i] + f * k[i];
+}
+__global__ void k_rk4_update(double* __restrict__ U, const double* __restrict__ k1, const double* __restrict__ k2,
+                             const double* __restrict__ k3, const double* __restrict__ k4, size_t n, double dt) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    U[i] += dt / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+}
 __global__ void k_sub(double* __restrict__ r, const double* __restrict__ b, const double* __restrict__ t, size_t n) {
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -998,6 +1075,7 @@ int ldg_precond_build(ldg_ctx* c, double alpha_dt) {
     if (bad >= 0)
       throw ldg_error(LDG_ERR_SOLVER, "singular block-Jacobi block at element " + std::to_string(bad));
     c->pc_valid = true;
+    c->pc_adt = alpha_dt;
     return LDG_OK;
   });
 }
@@ -1174,6 +1252,137 @@ int ldg_precond_apply_host(ldg_ctx* c, const double* r, double* z) {
     ck(cudaMemcpyAsync(z, c->d_hy, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H z");
     ck(cudaStreamSynchronize(c->stream), "stream synchronize");
     return LDG_OK;
+  });
+}
+
+// ---------------------------------------------------------- time integration
+// (PAPER.md:641-685, 755-775), mirroring the oracle's
+// lo_rk4_step / lo_dirk3_step operation by operation.
+int ldg_rk4_step(ldg_ctx* c, double* U, double t, double dt) {
+  return guarded(c, [&]() -> int {
+    if (!(dt > 0.0) || !U) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "rk4_step: dt > 0 and U required");
+    const size_t n = c->nU();
+    double* w = ensure(c->d_ti, 8 * n);
+    double *k1 = w, *k2 = w + n, *k3 = w + 2 * n, *k4 = w + 3 * n, *us = w + 4 * n;
+    double* red = ensure(c->d_kred, KR_BLOCKS + 8);
+    cudaStream_t st = c->stream;
+    const bool was = c->sync_errors;
+    c->sync_errors = true;
+    auto F = [&](const double* u, double* k, int stage) {
+      int s_ = ldg_residual(c, u, t, k, nullptr);
+      if (s_ != LDG_OK) {
+        c->sync_errors = was;
+        throw ldg_error(s_, c->err);
+      }
+      k_amax_part<<<KR_BLOCKS, KR_THREADS, 0, st>>>(k, n, red);
+      k_amax_fin<<<1, KR_THREADS, 0, st>>>(red, KR_BLOCKS, red + KR_BLOCKS);
+      c->launches += 2;
+      double m = 0.0;
+      ck(cudaMemcpyAsync(&m, red + KR_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "stream synchronize");
+      if (!std::isfinite(m)) {
+        c->sync_errors = was;
+        throw ldg_error(LDG_ERR_SOLVER, "rk4 blow-up at stage " + std::to_string(stage));
+      }
+    };
+    const int vb = 592, vt = 256;
+    F(U, k1, 1);
+    k_rk_state<<<vb, vt, 0, st>>>(us, U, k1, n, 0.5 * dt);
+    F(us, k2, 2);
+    k_rk_state<<<vb, vt, 0, st>>>(us, U, k2, n, 0.5 * dt);
+    F(us, k3, 3);
+    k_rk_state<<<vb, vt, 0, st>>>(us, U, k3, n, dt);
+    F(us, k4, 4);
+    k_rk4_update<<<vb, vt, 0, st>>>(U, k1, k2, k3, k4, n, dt);
+    c->launches += 4;
+    c->sync_errors = was;
+    return finish(c, cudaGetLastError());
+  });
+}
+
+int ldg_dirk3_step(ldg_ctx* c, double* U, double t, double dt, const ldg_newton_cfg* cfg, ldg_solver_stats* stats) {
+  return guarded(c, [&]() -> int {
+    if (!(dt > 0.0) || !U || !cfg || cfg->gmres_iters < 1 || cfg->recompute_threshold < 1 || cfg->max_newton < 1)
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "dirk3_step: dt > 0, U and a valid ldg_newton_cfg required");
+    const double al = 0.435866521508459, tau2 = (1.0 + al) / 2.0;
+    const double b1 = -(6.0 * al * al - 16.0 * al + 1.0) / 4.0, b2 = (6.0 * al * al - 20.0 * al + 5.0) / 4.0;
+    const double A[3][3] = {{al, 0.0, 0.0}, {tau2 - al, al, 0.0}, {b1, b2, al}};
+    const double B[3] = {b1, b2, al};
+    const size_t n = c->nU();
+    const double adt = al * dt;
+    double* w = ensure(c->d_ti, 8 * n);
+    double* K[3] = {w, w + n, w + 2 * n};
+    double *Kc = w + 3 * n, *us = w + 4 * n, *Fv = w + 5 * n, *G = w + 6 * n, *dK = w + 7 * n;
+    double* red = ensure(c->d_kred, KR_BLOCKS + 8);
+    cudaStream_t st = c->stream;
+    const int vb = 592, vt = 256;
+    ldg_solver_stats s{};
+    const bool was = c->sync_errors;
+    c->sync_errors = true;
+    auto chk = [&](int code) {
+      if (code != LDG_OK) {
+        c->sync_errors = was;
+        throw ldg_error(code, c->err);
+      }
+    };
+    auto assemble = [&](const double* u) {
+      chk(ldg_jacobian_assemble(c, u, t));
+      ++s.jacobian_assemblies;
+      c->pc_valid = false;
+    };
+    auto ensure_pc = [&]() {
+      if (cfg->use_precond && (!c->pc_valid || c->pc_adt != adt)) chk(ldg_precond_build(c, adt));
+    };
+    auto F = [&](const double* u, double* k) {
+      chk(ldg_residual(c, u, t, k, nullptr));
+      ++s.residual_evals;
+    };
+    if (!c->jac_valid) assemble(U);
+    ensure_pc();
+    F(U, Kc);
+    for (int i = 0; i < 3; ++i) {
+      int it = 0;
+      while (true) {
+        k_stage_state<<<vb, vt, 0, st>>>(us, U, K[0], K[1], Kc, n, dt, A[i][0], A[i][1], al, i);
+        ++c->launches;
+        F(us, Fv);
+        k_rhs<<<vb, vt, 0, st>>>(G, Kc, Fv, n);
+        k_amax_part<<<KR_BLOCKS, KR_THREADS, 0, st>>>(G, n, red);
+        k_amax_fin<<<1, KR_THREADS, 0, st>>>(red, KR_BLOCKS, red + KR_BLOCKS);
+        c->launches += 3;
+        double gn = 0.0;
+        ck(cudaMemcpyAsync(&gn, red + KR_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "stream synchronize");
+        if (!std::isfinite(gn)) {
+          c->sync_errors = was;
+          throw ldg_error(LDG_ERR_SOLVER, "dirk3: non-finite stage");
+        }
+        s.residual_norm = gn;
+        if (gn <= cfg->newton_tol) break;
+        if (it >= cfg->max_newton) {
+          c->sync_errors = was;
+          throw ldg_error(LDG_ERR_SOLVER, "dirk3: step failure (Newton did not converge)");
+        }
+        if (it > 0 && it % cfg->recompute_threshold == 0) {
+          assemble(us);
+          ensure_pc();
+        }
+        int32_t gi = 0, gc = 0;
+        double gr = 0.0;
+        chk(ldg_gmres(c, adt, G, dK, 1e-300, cfg->gmres_iters, cfg->gmres_iters, cfg->use_precond, &gi, &gc, &gr));
+        s.gmres_iters += gi;
+        k_axpy<<<vb, vt, 0, st>>>(Kc, dK, n, 1.0);
+        ++c->launches;
+        ++it;
+        ++s.newton_iters;
+      }
+      ck(cudaMemcpyAsync(K[i], Kc, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy stage slope");
+    }
+    k_dirk_update<<<vb, vt, 0, st>>>(U, K[0], K[1], K[2], n, dt, B[0], B[1], B[2]);
+    ++c->launches;
+    c->sync_errors = was;
+    if (stats) *stats = s;
+    return finish(c, cudaGetLastError());
   });
 }
 

@@ -1528,8 +1528,11 @@ struct SeTile {
   __device__ __forceinline__ int operator()(int tl, int, int, int side) const { return tl * 2 + side; }
 };
 
+#ifndef LDG_EJ_MINB  // k_endjac min CTAs per SM (register cap 65536 / (128 * minb))
+#define LDG_EJ_MINB 1
+#endif
 template <class C, int SEEDS>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, LDG_EJ_MINB)
 k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
          double* __restrict__ SE, int k_begin, int k_end, long long o_begin, long long o_end) {
   constexpr int NP = C::NP, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD, P = C::P,

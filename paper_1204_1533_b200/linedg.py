@@ -280,6 +280,30 @@ class LineDG:
                                        1 if precond else 0, C.byref(it), C.byref(cv), C.byref(rn)))
         return x, it.value, bool(cv.value), rn.value
 
+    # ---------------------------------------------------- time integration
+    def _state_on_device(self, U):
+        """(device copy of U, came_from_host)."""
+        if _is_torch(U):
+            return self._as_dev(U).clone(), False
+        import torch
+
+        return torch.from_numpy(np.array(U, dtype=np.float64)).cuda(), True
+
+    def rk4_step(self, U, dt: float, t: float = 0.0):
+        """Classical RK4 step of dU/dt = R(U)."""
+        Ud, host = self._state_on_device(U)
+        self._check(self.lib.ldg_rk4_step(self._h, self._ptr(Ud), t, dt))
+        return Ud.cpu().numpy() if host else Ud
+
+    def dirk3_step(self, U, dt: float, cfg=None, t: float = 0.0):
+        """L-stable DIRK3 step with Newton + (preconditioned) GMRES and Jacobian reuse
+        (SPEC.md:501-523): (U_next, stats dict).  cfg: _abi.newton_cfg(...)."""
+        cfg = cfg if cfg is not None else _abi.newton_cfg()
+        Ud, host = self._state_on_device(U)
+        st = _abi.LdgSolverStats()
+        self._check(self.lib.ldg_dirk3_step(self._h, self._ptr(Ud), t, dt, C.byref(cfg), C.byref(st)))
+        return (Ud.cpu().numpy() if host else Ud), st.as_dict()
+
     def split_matvec(self, alpha_dt: float, v, out=None):
         """(I - alpha_dt (K11 + K12 K21)) v without forming the product."""
         if not _is_torch(v):
