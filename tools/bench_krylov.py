@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--adt", type=float, default=0.05)
+    ap.add_argument("--dirk-dt", type=float, default=0.01)
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     case, U = cfg.build()
@@ -55,13 +56,31 @@ def main():
     x, it, cv, rn = g.gmres(a.adt, b, rtol=1e-30, maxit=a.iters, restart=a.iters, precond=True)
     torch.cuda.synchronize()
     t_gm = (time.perf_counter() - t0) * 1e3
+    # one implicit DIRK3 step with the paper's Newton policy (5 GMRES / 15 Newton)
+    from paper_1204_1533_b200._abi import newton_cfg
+    pol = newton_cfg(gmres_iters=5, recompute_threshold=15, max_newton=100, newton_tol=1e-8)
+    from paper_1204_1533_b200.linedg import SolverError
+    try:
+        g.dirk3_step(Ud, a.dirk_dt, pol)  # warm (Jacobian assembled, preconditioner built)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, dstats = g.dirk3_step(Ud, a.dirk_dt, pol)
+        torch.cuda.synchronize()
+        t_dirk = (time.perf_counter() - t0) * 1e3
+    except SolverError as ex:
+        t_dirk, dstats = None, {"failure": str(ex)}
+    t0 = time.perf_counter()
+    g.rk4_step(Ud, 1e-4)
+    torch.cuda.synchronize()
+    t_rk4 = (time.perf_counter() - t0) * 1e3
     ne = case.npe * g.m
     lu_bytes = case.E * ne * ne * 8
     print(json.dumps({"config": cfg.name, "dofs": g.n_dofs, "adt": a.adt,
                       "precond_build_ms": t_build, "precond_apply_ms": t_apply,
                       "precond_apply_GBs": lu_bytes / (t_apply * 1e-3) / 1e9, "lu_bytes": lu_bytes,
                       "split_matvec_ms": t_mv, "gmres_iters": it, "gmres_ms": t_gm,
-                      "gmres_ms_per_iter": t_gm / max(it, 1), "resnorm": rn}))
+                      "gmres_ms_per_iter": t_gm / max(it, 1), "resnorm": rn,
+                      "dirk3_dt": a.dirk_dt, "dirk3_step_ms": t_dirk, "dirk3_stats": dstats, "rk4_step_ms": t_rk4}))
 
 
 if __name__ == "__main__":
