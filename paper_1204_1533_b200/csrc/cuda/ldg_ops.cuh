@@ -213,10 +213,13 @@ struct Launch {
   static constexpr int EJ_SEEDS = LDG_EJ_SEEDS < C::M ? LDG_EJ_SEEDS : C::M;  // tuning knob
 #endif
   // Elements per assembly chunk: the endpoint-Jacobian scratch of one chunk
-  // stays within ~48 MB, so it is produced and consumed while L2-resident.
+  // stays within LDG_CHUNK_MB (default 512 MB).  Measured: fewer, larger chunks
+  // beat L2-sized ones (kernel ramps and tails per chunk outweigh the scratch
+  // re-read; C2 one chunk 0.252 vs 0.262 ms, C4 17.1 vs 18.3 ms).
   static int chunk_elems(int E) {
     const long long per = static_cast<long long>(EndJac<C>::PER_ELEM) * 8;
-    long long n = (48LL << 20) / (per > 0 ? per : 1);
+    static const long long budget = (std::getenv("LDG_CHUNK_MB") ? std::atoll(std::getenv("LDG_CHUNK_MB")) : 512LL) << 20;
+    long long n = budget / (per > 0 ? per : 1);
     if (n < 1024) n = 1024;
     return static_cast<int>(n < E ? n : E);
   }
