@@ -53,7 +53,8 @@ constexpr int JAC_SMEMTAB = LDG_JAC_SMEMTAB;
 #ifndef LDG_JAC_CHAINS  // assembly: line-block sums as one (1) or two (2) dependent DFMA chains
 #define LDG_JAC_CHAINS 1
 #endif
-constexpr int JAC_CHAINS = LDG_JAC_CHAINS;  // 0 constant bank, 1 shared (scalar), 2 shared (pairs)
+constexpr int JAC_CHAINS = LDG_JAC_CHAINS;
+  // 0 constant bank, 1 shared (scalar), 2 shared (pairs)
 // ---------------------------------------------------------------- helpers
 
 template <class C>
@@ -2812,9 +2813,14 @@ __device__ __forceinline__ int64_t slot_col(const KParams<C>& kp, int k, size_t 
 template <class C, bool SPLIT>
 __global__ void __launch_bounds__(128)
 k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __restrict__ V12,
-         const double* __restrict__ x, const double* __restrict__ w, double adt, double* __restrict__ y) {
+         const double* __restrict__ x, const double* __restrict__ w, double adt, double* __restrict__ y, int rev) {
   constexpr int M = C::M, NT = C::NT, NPE = C::NPE, MD = C::MD, B11 = C::B11;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // rev: blocks walk the rows from the end -- the Jacobian assembly writes the
+  // store in increasing tile order, so its last ~L2-size of tiles is still
+  // cached when the first matvec after an assembly starts (a gain where that
+  // is a noticeable share of the store: the launcher sets rev for stores <= 1 GB)
+  const int64_t gid = static_cast<int64_t>(rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * blockDim.x +
+                      threadIdx.x;
   const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
   const int lane = static_cast<int>(gid & 31);
   const int64_t wg = gid >> 5;

@@ -309,8 +309,15 @@ struct Launch {
     const long long threads = (rows + 31) / 32 * 32 * C::M;
     return static_cast<int>((threads + 127) / 128);
   }
+  // reverse row order for small stores (see k_spmv11); LDG_SPMV_REVERSE=0/1 forces it
+  static int spmv_rev(const DevCtx& d) {
+    static const char* env = std::getenv("LDG_SPMV_REVERSE");
+    if (env) return std::atoi(env) != 0;
+    const double store = 8.0 * d.E * C::NPE * C::NS11 * C::B11;
+    return store <= static_cast<double>(1LL << 30) ? 1 : 0;
+  }
   static cudaError_t spmv11(const DevCtx& d, const double* V11, const double* x, double* y) {
-    k_spmv11<C, false><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, nullptr, x, nullptr, 0.0, y);
+    k_spmv11<C, false><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, nullptr, x, nullptr, 0.0, y, spmv_rev(d));
     count(d);
     return cudaGetLastError();
   }
@@ -328,7 +335,7 @@ struct Launch {
   }
   static cudaError_t split(const DevCtx& d, const double* V11, const double* V12, const double* v,
                            const double* w, double adt, double* y) {
-    k_spmv11<C, true><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, V12, v, w, adt, y);
+    k_spmv11<C, true><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, V12, v, w, adt, y, spmv_rev(d));
     count(d);
     return cudaGetLastError();
   }
