@@ -620,10 +620,18 @@ struct ResP {
   static constexpr int NB = ev(EPB * C::LPE * 2 * C::M);
   static constexpr int NBQ = C::SECOND ? ev(EPB * C::LPE * 2 * C::MD) : 0;
   static constexpr int BUF = U + Q + MET + CONN + NB + NBQ;
-  static constexpr int ACC = EPB * C::D * C::NPE * C::M;
+  // SPLIT threads per line (warp-uniform halves: the first half of the CTA
+  // takes the first quadrature points and the left end of every line, the
+  // second half the rest and the right end; per-half partial sums in ACC)
+#ifndef LDG_RES_SPLIT  // measured slower for C2/C4 (more warps, same latency chains): off
+#define LDG_RES_SPLIT 1
+#endif
+  static constexpr int SPLIT = LDG_RES_SPLIT;
+  static constexpr int LT = (EPB * C::LPE + 31) / 32 * 32;  // line threads of one half
+  static constexpr int ACC = SPLIT * EPB * C::D * C::NPE * C::M;
   static constexpr int TOTAL = 2 + 2 * BUF + ACC;  // 2 doubles hold the two mbarriers
   static constexpr bool TMA = (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0);
-  static constexpr int THREADS = (EPB * C::LPE + 31) / 32 * 32;
+  static constexpr int THREADS = SPLIT * LT;
 };
 
 template <class C, int EPB>
@@ -726,10 +734,14 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     cp_async_wait_all();
     __syncthreads();
     if (tid < nb) sord[tid] = __ldg(kp.order + k0 + tid);  // lands during the line work
-    // ---- lines
-    const int le = tid / LPE;
-    if (le < nb) {
-      const int rem = tid - le * LPE;
+    // ---- lines (RP::SPLIT threads per line, warp-uniform halves; the body is
+    // instantiated per half so each thread issues only its own points)
+    const int half_rt = RP::SPLIT > 1 ? tid / RP::LT : 0, lt = tid - half_rt * RP::LT;
+    constexpr int QH = RP::SPLIT > 1 ? (NQ + 1) / 2 : NQ;
+    const int le = lt / LPE;
+    auto line_work = [&](auto HC) {
+      constexpr int half = decltype(HC)::value;
+      const int rem = lt - le * LPE;
       const int dir = rem / NL, line = rem - dir * NL;
       const double* mk = RP::METS ? bMET(cur) + le * C::METP : kp.metric + static_cast<size_t>(k0 + le) * C::METP;
       const double* nvl = mk + (dir * NL + line) * NQ * D;
@@ -743,6 +755,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
         for (int c = 0; c < M; ++c) r[i][c] = 0.0;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
+        if (RP::SPLIT > 1 && ((q < QH) != (half == 0))) continue;  // compile-time
         double uq[M], qq[C::SECOND ? MD : 1];
 #pragma unroll
         for (int c = 0; c < M; ++c) uq[c] = 0.0;
@@ -781,6 +794,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
       }
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
+        if (RP::SPLIT > 1 && side != half) continue;  // compile-time
         const int2 cn = bCONN(cur)[(le * D + dir) * 2 + side];
         const int S = conn_sign(cn.y);
         const int ie = side ? P : 0;
@@ -829,13 +843,17 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
           for (int c = 0; c < M; ++c) r[i][c] += kp.bt.mi[i][side] * fh[c];
       }
       if (!ok) report_line<C>(kp, kp.order[k0 + le], dir, line, sul);
-      double* acc = sacc + (le * D + dir) * NPE * M;
+      double* acc = sacc + ((half * EPB + le) * D + dir) * NPE * M;
 #pragma unroll
       for (int t = 0; t < NP; ++t) {
         const int nd = node_on_line<C>(dir, line, t);
 #pragma unroll
         for (int c = 0; c < M; ++c) acc[nd * M + c] = r[t][c];
       }
+    };
+    if (le < nb) {
+      if (RP::SPLIT > 1 && half_rt == 1) line_work(std::integral_constant<int, 1>{});
+      else line_work(std::integral_constant<int, 0>{});
     }
     __syncthreads();
     // ---- dU/dt = S - (1/J) sum_dir r
@@ -847,6 +865,10 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
       double sum = a[0];
 #pragma unroll
       for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
+#pragma unroll
+      for (int h = 1; h < RP::SPLIT; ++h)
+#pragma unroll
+        for (int d = 0; d < D; ++d) sum = sum + a[(h * EPB * D + d) * NPE * M];
       const double invJ = RP::METS ? bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd]
                                    : __ldg(kp.metric + static_cast<size_t>(k0 + l) * C::METP + C::MET_NV + C::MET_NE + nd);
       const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
