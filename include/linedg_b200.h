@@ -12,7 +12,8 @@
  *   residual_primal(ctx, U, t)                 SPEC.md:248-256   -> ldg_residual (second-order physics)
  *   assemble_jacobians(ctx, U, t, Analytic)    SPEC.md:409-417   -> ldg_jacobian_assemble
  *   split_matvec(blocks, alpha_dt, v)          SPEC.md:419-427   -> ldg_split_matvec
- *   CscMatrix export / triplet export          SPEC.md:391-394, 465 -> ldg_export_triplets
+ *   CscMatrix export                           SPEC.md:391-394      -> ldg_export_blocks
+ *   triplet export / sparsity CSV              SPEC.md:465, 633     -> ldg_write_triplets, ldg_write_sparsity_csv
  *
  * Inputs are the reference's own setup objects, flattened (no Eigen, no C++
  * types): NodalBasis1D (reference basis.hpp:17-43), QuadMesh/Face/elem_face
@@ -236,6 +237,19 @@ int ldg_export_blocks(ldg_ctx* ctx, int which, int64_t* rows, int64_t* cols, dou
  * elems == NULL); *nnzb_out receives the number of blocks written.         */
 int ldg_export_blocks_subset(ldg_ctx* ctx, int which, const int32_t* elems, int32_t n_elems,
                              int64_t* rows, int64_t* cols, double* vals, int64_t* nnzb_out);
+
+/* Wire formats: matrix export as text triplets `i j value`, one
+ * structural scalar entry per line (K11: every entry of every node block; K12:
+ * all but the Navier-Stokes density row; K21: the component diagonal), 0-based
+ * indices in the reference numbering (rows: DOF (e*npe+node)*m+c, or the Q
+ * index for K21), ascending rows, %.17g values.  Replaces the reference's
+ * triplet dump of a CscMatrix. */
+int ldg_write_triplets(ldg_ctx* ctx, int which, const char* path);
+/* Sparsity summary CSV `p,avg_cols_per_block_row,nnz`:
+ * node-columns per node row (the Table-1 quantity) and the
+ * structural scalar nonzeros of one matrix; append != 0 adds a row (header
+ * only when the file is empty). */
+int ldg_write_sparsity_csv(ldg_ctx* ctx, int which, const char* path, int append);
 
 /* Error synchronisation.  By default every device entry point waits for its
  * kernels and reports a physical-state failure synchronously, like the

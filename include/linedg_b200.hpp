@@ -198,6 +198,14 @@ class Context {
         }
     return out;
   }
+  // Text wire formats: `i j value` triplet file and the
+  // `p,avg_cols_per_block_row,nnz` sparsity summary.
+  void write_triplets(int which, const std::string& path) {
+    check(ldg_write_triplets(ctx_, which, path.c_str()), ctx_);
+  }
+  void write_sparsity_csv(int which, const std::string& path, bool append = false) {
+    check(ldg_write_sparsity_csv(ctx_, which, path.c_str(), append ? 1 : 0), ctx_);
+  }
 
  private:
   static void check(int status, const ldg_ctx* c) {

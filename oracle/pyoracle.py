@@ -170,6 +170,41 @@ class Oracle:
                                             _d(vals)))
         return rows, cols, vals.reshape(nnzb.value, br.value, bc.value)
 
+    def structural_mask(self, which):
+        """Structural scalar entries of a node block (the wire-format rule of
+        ldg_write_triplets): K11 all; K12 all but the Navier-Stokes density
+        row; K21 the component diagonal."""
+        br = self.m * self.dim if which == 2 else self.m
+        bc = self.m * self.dim if which == 1 else self.m
+        mask = np.ones((br, bc), dtype=bool)
+        if which == 1 and self._ph.kind == 2:
+            mask[0, :] = False
+        if which == 2:
+            mask[:] = False
+            for c in range(self.m):
+                mask[c * self.dim:(c + 1) * self.dim, c] = True
+        return mask
+
+    def triplets(self, which):
+        """(i, j, v) scalar triplets in the order ldg_write_triplets emits them
+        (rows ascending; within a row, columns ascending) -- checker for the
+        `i j value` export."""
+        rows, cols, vals = self.export_blocks(which)
+        mask = self.structural_mask(which)
+        br, bc = mask.shape
+        a, b = np.nonzero(mask)
+        i = (rows[:, None] * br + a[None, :]).ravel()
+        j = (cols[:, None] * bc + b[None, :]).ravel()
+        v = vals[:, a, b].ravel()
+        o = np.lexsort((j, i))
+        return i[o], j[o], v[o]
+
+    def sparsity_row(self, which):
+        """(p, avg node-cols per node row, structural scalar nnz)."""
+        rows, _, _ = self.export_blocks(which)
+        n_rows = self.case.E * self.case.npe
+        return self.case.p, len(rows) / n_rows, len(rows) * int(self.structural_mask(which).sum())
+
     def export_csc(self, which):
         nnz = C.c_int64()
         self._check(self.L.lo_export_csc(self.h, which, None, None, None, C.byref(nnz)))

@@ -77,6 +77,34 @@ void* ref_case_create(int p, int nv, const double* verts, int ne, const int* ele
   }
 }
 
+// The reference's own load_mesh (mesh.cpp:115-146) + optional periodic pairs.
+void* ref_case_load(int p, const char* path, int nper, const int* ptags, const double* ptr) {
+  try {
+    auto* c = new RefCase;
+    c->b = make_basis(p);
+    c->m = load_mesh(std::string(path));
+    for (int k = 0; k < nper; ++k)
+      make_periodic(c->m, ptags[2 * k], ptags[2 * k + 1], Eigen::Vector2d(ptr[3 * k], ptr[3 * k + 1]));
+    c->sw = assign_switches(c->m);
+    c->maps = compute_mapping(c->m, c->b);
+    return c;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// The reference's own save_mesh (mesh.cpp:148-160).
+int ref_case_save(void* h, const char* path) {
+  try {
+    save_mesh(static_cast<RefCase*>(h)->m, std::string(path));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 void ref_case_free(void* h) { delete static_cast<RefCase*>(h); }
 int ref_case_num_faces(void* h) { return static_cast<RefCase*>(h)->m.num_faces(); }
 

@@ -119,6 +119,9 @@ def host_lib() -> C.CDLL:
         L.lh_case_custom.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _dp, C.c_int32, _ip,
                                      C.c_int32, _ip, C.c_int32, _ip, _dp, C.POINTER(C.c_void_p)]
         L.lh_case_free.argtypes = [C.c_void_p]
+        L.lh_case_load_mesh.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _ip, _dp,
+                                        C.POINTER(C.c_void_p)]
+        L.lh_case_save_mesh.argtypes = [C.c_void_p, C.c_char_p]
         L.lh_case_setup.argtypes = [C.c_void_p]
         L.lh_case_setup.restype = C.POINTER(LdgSetup)
         L.lh_case_num_vertices.argtypes = [C.c_void_p]
@@ -166,7 +169,7 @@ GPU_SYMBOLS = [
     "ldg_residual_host", "ldg_jacobian_assemble_host", "ldg_bsr_spmv_host", "ldg_split_matvec_host",
     "ldg_kernel_launches", "ldg_jacobian_bytes",
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
-    "ldg_rk4_step", "ldg_dirk3_step",
+    "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv",
 ]
 
 
@@ -212,6 +215,8 @@ def gpu_lib() -> C.CDLL:
         L.ldg_rk4_step.argtypes = [vp, vp, C.c_double, C.c_double]
         L.ldg_dirk3_step.argtypes = [vp, vp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                      C.POINTER(LdgSolverStats)]
+        L.ldg_write_triplets.argtypes = [vp, C.c_int, C.c_char_p]
+        L.ldg_write_sparsity_csv.argtypes = [vp, C.c_int, C.c_char_p, C.c_int]
         L.ldg_kernel_launches.argtypes = [vp]
         L.ldg_kernel_launches.restype = C.c_int64
         L.ldg_jacobian_bytes.argtypes = [vp]

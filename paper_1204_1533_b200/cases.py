@@ -11,6 +11,7 @@ DESIGN.md ("Config choices"), following SURVEY.md Appendix C.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
@@ -104,6 +105,27 @@ class Case:
         if st != 0:
             raise _setup_error(st)
         return cls(h.value)
+
+    @classmethod
+    def load_mesh(cls, path: str, p: int, periodic=(), gll=True) -> "Case":
+        """Case from a reference mesh text file (load_mesh, mesh.cpp:115-146),
+        then optional periodic pairs ((tag_a, tag_b), translation)."""
+        pt = np.ascontiguousarray(np.asarray([t for t, _ in periodic], dtype=np.int32).reshape(-1, 2))
+        ptr = np.zeros((len(periodic), 3))
+        for i, (_, tr) in enumerate(periodic):
+            ptr[i, :len(tr)] = tr
+        h = C.c_void_p()
+        st = host_lib().lh_case_load_mesh(os.fsencode(path), p, 1 if gll else 0, len(periodic),
+                                          _abi.iptr(pt), dptr(ptr), C.byref(h))
+        if st != 0:
+            raise _setup_error(st)
+        return cls(h.value)
+
+    def save_mesh(self, path: str):
+        """Write the mesh in the reference text format (save_mesh, mesh.cpp:148-160)."""
+        st = self._lib.lh_case_save_mesh(self._h, os.fsencode(path))
+        if st != 0:
+            raise _setup_error(st)
 
     def __del__(self):
         try:

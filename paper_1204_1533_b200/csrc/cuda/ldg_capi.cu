@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -1025,6 +1026,81 @@ int ldg_export_blocks_subset(ldg_ctx* c, int which, const int32_t* elems, int32_
 
 int ldg_export_blocks(ldg_ctx* c, int which, int64_t* rows, int64_t* cols, double* vals) {
   return ldg_export_blocks_subset(c, which, nullptr, 0, rows, cols, vals, nullptr);
+}
+
+// Structural scalar entries of a node block (a, b): K11 all m x m; K12 all
+// but the Navier-Stokes density row (its flux has no viscous part); K21 the
+// component diagonal (c, d) <- c.  Shared by the triplet and CSV writers.
+static bool scalar_structural(const ldg_ctx* c, int which, int a, int b) {
+  if (which == LDG_K12) return !(c->ph == ldg::PH_NS && a == 0);
+  if (which == LDG_K21) return a / c->D == b;
+  return true;
+}
+
+// Matrix export as text triplets `i j value`, one structural
+// scalar entry per line, 0-based indices in the reference numbering (rows:
+// DOF (e*npe+node)*m+c, or the Q index for K21; columns likewise), rows in
+// ascending order, values printed with 17 significant digits.  Streams the
+// store element by element (no full host copy).
+int ldg_write_triplets(ldg_ctx* c, int which, const char* path) {
+  return guarded(c, [&]() -> int {
+    if (!path) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "path is NULL");
+    if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+    if (which < 0 || which > 2 || (which != LDG_K11 && !c->second))
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "matrix not available for this physics");
+    FILE* f = std::fopen(path, "w");
+    if (!f) throw ldg_error(LDG_ERR_CONFIG, std::string("cannot write '") + path + "'");
+    const int br = which == LDG_K21 ? c->m * c->D : c->m;
+    const int bc = which == LDG_K12 ? c->m * c->D : c->m;
+    const size_t cap = static_cast<size_t>(c->npe) * c->nslots(which);
+    std::vector<int64_t> rows(cap), cols(cap);
+    std::vector<double> vals(cap * br * bc);
+    std::vector<char> buf(1 << 20);
+    std::setvbuf(f, buf.data(), _IOFBF, buf.size());
+    int st = LDG_OK;
+    for (int32_t e = 0; e < c->E && st == LDG_OK; ++e) {
+      int64_t nb = 0;
+      st = ldg_export_blocks_subset(c, which, &e, 1, rows.data(), cols.data(), vals.data(), &nb);
+      if (st != LDG_OK) break;
+      // the export is sorted by (row node, col node); emit scalar rows in order
+      for (int64_t z0 = 0; z0 < nb;) {
+        int64_t z1 = z0;
+        while (z1 < nb && rows[z1] == rows[z0]) ++z1;
+        for (int a = 0; a < br; ++a)
+          for (int64_t z = z0; z < z1; ++z)
+            for (int b = 0; b < bc; ++b)
+              if (scalar_structural(c, which, a, b))
+                std::fprintf(f, "%lld %lld %.17g\n", static_cast<long long>(rows[z] * br + a),
+                             static_cast<long long>(cols[z] * bc + b), vals[(z * br + a) * bc + b]);
+        z0 = z1;
+      }
+    }
+    if (std::fclose(f) != 0 && st == LDG_OK) throw ldg_error(LDG_ERR_CONFIG, std::string("write failed: ") + path);
+    return st;
+  });
+}
+
+// Sparsity summary CSV `p,avg_cols_per_block_row,nnz` (the
+// `linedg sparsity` Table-1 oracle): node-columns per node row
+// (the Table-1 quantity) and structural scalar nonzeros.
+// append != 0 adds a row to an existing file (header only when it is empty).
+int ldg_write_sparsity_csv(ldg_ctx* c, int which, const char* path, int append) {
+  return guarded(c, [&]() -> int {
+    if (!path) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "path is NULL");
+    ldg_pattern_info info;
+    int st = ldg_pattern_info_get(c, which, &info);
+    if (st != LDG_OK) return st;
+    int per = 0;
+    for (int a = 0; a < info.block_rows; ++a)
+      for (int b = 0; b < info.block_cols; ++b) per += scalar_structural(c, which, a, b);
+    FILE* f = std::fopen(path, append ? "a" : "w");
+    if (!f) throw ldg_error(LDG_ERR_CONFIG, std::string("cannot write '") + path + "'");
+    if (std::ftell(f) == 0) std::fprintf(f, "p,avg_cols_per_block_row,nnz\n");
+    std::fprintf(f, "%d,%.6f,%lld\n", c->p, static_cast<double>(info.nnzb) / static_cast<double>(info.n_rows),
+                 static_cast<long long>(info.nnzb * per));
+    if (std::fclose(f) != 0) throw ldg_error(LDG_ERR_CONFIG, std::string("write failed: ") + path);
+    return LDG_OK;
+  });
 }
 
 int ldg_bsr_spmv(ldg_ctx* c, int which, const double* x, double* y) {

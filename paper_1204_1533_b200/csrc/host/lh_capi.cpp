@@ -152,6 +152,39 @@ int lh_case_custom(int32_t dim, int32_t p, int32_t gll, int32_t nv, const double
   }
 }
 
+// Reference mesh file (mesh.cpp:115-146) + optional periodic pairs, then the
+// same switch / mapping setup as every case.  tag_lines records the boundary
+// faces as loaded (before pairing).
+int lh_case_load_mesh(const char* path, int32_t p, int32_t gll, int32_t nper, const int32_t* per_tags,
+                      const double* per_tr, lh_case** out) {
+  try {
+    if (!path) throw std::invalid_argument("path is NULL");
+    auto c = std::make_unique<lh_case>();
+    c->basis = make_basis(p, gll != 0);
+    c->mesh = load_mesh(std::string(path));
+    for (const Face& f : c->mesh.faces)
+      if (f.boundary()) c->tag_lines.insert(c->tag_lines.end(), {f.elem_l, f.face_l, f.tag});
+    for (int k = 0; k < nper; ++k)
+      make_periodic(c->mesh, per_tags[2 * k], per_tags[2 * k + 1], per_tr + 3 * k);
+    finish_case(c.get());
+    *out = c.release();
+    return LDG_OK;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
+// save_mesh (mesh.cpp:148-160) of a case's mesh (2-D).
+int lh_case_save_mesh(const lh_case* c, const char* path) {
+  try {
+    if (!path) throw std::invalid_argument("path is NULL");
+    save_mesh(c->mesh, std::string(path));
+    return LDG_OK;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
 void lh_case_free(lh_case* c) { delete c; }
 int32_t lh_case_num_tag_lines(const lh_case* c) { return static_cast<int32_t>(c->tag_lines.size() / 3); }
 void lh_case_tag_lines(const lh_case* c, int32_t* out) {

@@ -1,5 +1,9 @@
 // linedg_host.cpp -- setup restatement (see linedg_host.hpp for the map to
 // the reference sources).  No Eigen: small dense operations are written out.
+#include <fstream>
+#include <istream>
+#include <ostream>
+
 #include "linedg_host.hpp"
 
 #include <algorithm>
@@ -975,6 +979,74 @@ Mesh make_lattice_mesh(const LatticeSpec& s, std::vector<int>* tag_lines) {
     }
   }
   return m;
+}
+
+// ------------------------------------------------------------- mesh text I/O
+// The reference mesh file (SPEC.md "External Interfaces"; mesh.cpp:115-166):
+// `nv ne nb`, nv lines `x y`, ne lines `v0 v1 v2 v3` (0-based, CCW), nb lines
+// `elem local_face tag`.  Same parse order, checks and config_error messages
+// as load_mesh (mesh.cpp:115-146); faces are built before the tag lines are
+// applied, every untagged boundary face keeps tag 0 (mesh.cpp:94).  2-D only,
+// like the format.
+Mesh load_mesh(std::istream& in) {
+  Mesh mesh;
+  mesh.dim = 2;
+  int nv = 0, ne = 0, nb = 0;
+  if (!(in >> nv >> ne >> nb)) throw config_error("mesh: failed to read header `nv ne nb`");
+  if (nv < 0 || ne < 0 || nb < 0) throw config_error("mesh: failed to read header `nv ne nb`");
+  mesh.verts.resize(static_cast<size_t>(nv) * 2);
+  for (int i = 0; i < nv; ++i)
+    if (!(in >> mesh.verts[2 * i] >> mesh.verts[2 * i + 1]))
+      throw config_error("mesh: failed to read vertex " + std::to_string(i));
+  mesh.elems.resize(static_cast<size_t>(ne) * 4);
+  for (int e = 0; e < ne; ++e)
+    for (int c = 0; c < 4; ++c) {
+      int& v = mesh.elems[4 * e + c];
+      if (!(in >> v)) throw config_error("mesh: failed to read element " + std::to_string(e));
+      if (v < 0 || v >= nv)
+        throw config_error("mesh: element " + std::to_string(e) + " has vertex index out of range");
+    }
+  build_faces(mesh);
+  for (int b = 0; b < nb; ++b) {
+    int e = 0, lf = 0, tag = 0;
+    if (!(in >> e >> lf >> tag)) throw config_error("mesh: failed to read boundary tag line " + std::to_string(b));
+    if (e < 0 || e >= ne || lf < 0 || lf > 3)
+      throw config_error("mesh: boundary tag line " + std::to_string(b) + " out of range");
+    Face& f = mesh.faces[mesh.elem_face[4 * e + lf]];
+    if (!f.boundary())
+      throw config_error("mesh: tagged face (" + std::to_string(e) + "," + std::to_string(lf) +
+                         ") is not a boundary face");
+    f.tag = tag;
+  }
+  return mesh;
+}
+
+Mesh load_mesh(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw config_error("mesh: cannot open '" + path + "'");
+  return load_mesh(in);
+}
+
+// save_mesh (mesh.cpp:148-160): 17 significant digits, the faces still on the
+// boundary (after any periodic pairing) in face order as `elem_l face_l tag`.
+void save_mesh(const Mesh& mesh, std::ostream& out) {
+  if (mesh.dim != 2) throw config_error("mesh: the text format is 2-D only");
+  out.precision(17);
+  std::vector<const Face*> bf;
+  for (const Face& f : mesh.faces)
+    if (f.boundary()) bf.push_back(&f);
+  out << mesh.nv() << " " << mesh.ne() << " " << bf.size() << "\n";
+  for (int i = 0; i < mesh.nv(); ++i) out << mesh.verts[2 * i] << " " << mesh.verts[2 * i + 1] << "\n";
+  for (int e = 0; e < mesh.ne(); ++e)
+    out << mesh.elems[4 * e] << " " << mesh.elems[4 * e + 1] << " " << mesh.elems[4 * e + 2] << " "
+        << mesh.elems[4 * e + 3] << "\n";
+  for (const Face* f : bf) out << f->elem_l << " " << f->face_l << " " << f->tag << "\n";
+}
+
+void save_mesh(const Mesh& mesh, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw config_error("mesh: cannot write '" + path + "'");
+  save_mesh(mesh, out);
 }
 
 }  // namespace ldgh

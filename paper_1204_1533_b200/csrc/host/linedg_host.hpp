@@ -15,6 +15,7 @@
 
 #include <array>
 #include <cstdint>
+#include <iosfwd>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -118,5 +119,11 @@ struct LatticeSpec {
 // tag_lines (optional): the boundary tag lines (elem, local_face, tag) as a
 // reference mesh file would carry them, recorded before periodic pairing.
 Mesh make_lattice_mesh(const LatticeSpec& s, std::vector<int>* tag_lines = nullptr);
+
+// Reference mesh text format (mesh.cpp:115-166), 2-D.
+Mesh load_mesh(std::istream& in);
+Mesh load_mesh(const std::string& path);
+void save_mesh(const Mesh& mesh, std::ostream& out);
+void save_mesh(const Mesh& mesh, const std::string& path);
 
 }  // namespace ldgh

@@ -18,6 +18,7 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -231,6 +232,14 @@ class LineDG:
         if values:
             vals = vals.reshape(nnzb, info.block_rows, info.block_cols)
         return rows, cols, vals
+
+    def write_triplets(self, which: int, path: str):
+        """Text triplets `i j value` of one matrix."""
+        self._check(self.lib.ldg_write_triplets(self._h, which, os.fsencode(path)))
+
+    def write_sparsity_csv(self, which: int, path: str, append: bool = False):
+        """Sparsity summary CSV `p,avg_cols_per_block_row,nnz`."""
+        self._check(self.lib.ldg_write_sparsity_csv(self._h, which, os.fsencode(path), 1 if append else 0))
 
     def spmv(self, which: int, x, out=None):
         if not _is_torch(x):
