@@ -64,14 +64,26 @@ typedef enum ldg_riemann_kind {
   LDG_LLF = 1   /* local Lax-Friedrichs (extension; not in the reference)                      */
 } ldg_riemann_kind;
 
+/* Boundary conditions (BcKind, physics.hpp:16; SPEC.md:266,
+ * 366-368).  value[] holds constant data per component (the reference's
+ * std::function data cannot cross to the device).                          */
 typedef enum ldg_bc_kind {
-  LDG_BC_DIRICHLET = 0     /* constant state g_D; Euler: Riemann flux vs g_D */
+  LDG_BC_DIRICHLET = 0,        /* g_D = value: Riemann flux vs g_D (inviscid), F(u,q).n + C11_bd|n|(u - g_D)
+                                  (viscous), u_hat = g_D                            */
+  LDG_BC_NEUMANN = 1,          /* g_N = value: F_hat.n = g_N |n| (whole flux), u_hat = u (C22 = 0;
+                                  PAPER.md:577-581)                                                   */
+  LDG_BC_CHARACTERISTIC = 2,   /* far-field state = value: Riemann flux vs the free-stream ghost state
+                                  (SPEC.md:266, 366); viscous terms as Dirichlet with the far state    */
+  LDG_BC_SLIP_WALL = 3,        /* Riemann flux vs the interior state with mirrored normal momentum
+                                  (SPEC.md:367); viscous F(u,q).n, u_hat = u; Euler / Navier-Stokes   */
+  LDG_BC_NO_SLIP_ADIABATIC = 4 /* not supported: ldg_create returns LDG_ERR_CONFIG (SPEC.md:368 needs a
+                                  component-dependent u_hat; the K21 store is component-uniform)     */
 } ldg_bc_kind;
 
 typedef struct ldg_bc {
   int32_t tag;             /* mesh boundary tag (Face::tag, mesh.hpp:24) */
   int32_t kind;            /* ldg_bc_kind */
-  double value[8];         /* g_D per component (first m used) */
+  double value[8];         /* g_D / g_N / far-field state per component (first m used) */
 } ldg_bc;
 
 typedef struct ldg_physics {

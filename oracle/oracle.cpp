@@ -69,7 +69,8 @@ struct Ctx {
   std::vector<double> jac, invJ, nvec, nend, source;
   // Endpoint table [E][D][2][NL]: neighbour element / node, or boundary.
   std::vector<int32_t> ep_elem, ep_node, ep_bc;  // ep_bc: -1 interior, else index in bcv
-  std::vector<std::vector<double>> bcv;          // Dirichlet states
+  std::vector<std::vector<double>> bcv;          // boundary data (g_D / g_N / far-field state)
+  std::vector<int> bck;                          // boundary kind per bcv entry (ldg_bc_kind)
   BlockMat K[3];
   // block-Jacobi preconditioner: per element LU (partial pivoting) of
   // I - alpha_dt A~ restricted to the element (dense n_e x n_e, row-major)
@@ -157,8 +158,14 @@ void build_endpoints(Ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   c.ep_bc.assign(n, -1);
   std::map<int, int> tag2bc;
   for (int i = 0; i < ph.n_bc; ++i) {
+    const int kind = ph.bcs[i].kind;
+    if (kind < LDG_BC_DIRICHLET || kind > LDG_BC_SLIP_WALL)
+      throw std::runtime_error("oracle: unsupported boundary-condition kind");
+    if (kind == LDG_BC_SLIP_WALL && !c.has_inv)
+      throw std::runtime_error("oracle: slip-wall boundaries need Euler or Navier-Stokes physics");
     tag2bc[ph.bcs[i].tag] = static_cast<int>(c.bcv.size());
     c.bcv.emplace_back(ph.bcs[i].value, ph.bcs[i].value + c.m);
+    c.bck.push_back(kind);
   }
   const int F = 2 * c.D;
   for (int e = 0; e < c.E; ++e)
@@ -263,20 +270,42 @@ double norm_of(const double* n, int D) {
   return std::sqrt(s);
 }
 
+// u_hat of a boundary end is the interior trace (Neumann-type with C22 = 0,
+// PAPER.md:580; slip wall), else the prescribed state.
+inline bool uhat_inner(int bkind) { return bkind == LDG_BC_NEUMANN || bkind == LDG_BC_SLIP_WALL; }
+
 // Endpoint numerical flux F_hat . n (inviscid Riemann + LDG viscous switch
-// flux; Dirichlet: PAPER.md:569-574).
+// flux; boundaries PAPER.md:566-582).
 //   interior: uo/qo are the neighbour's node values; bc == nullptr
-//   boundary: bc = g_D, uo/qo ignored
+//   boundary: bc = the boundary data, bkind its ldg_bc_kind, uo/qo ignored:
+//     Dirichlet / characteristic: Riemann vs g, + F(u,q).n + C11_bd|n|(u - g)
+//     slip wall: Riemann vs the interior state with mirrored normal momentum
+//                (a function of u_in, so Dual seeds carry through), + F(u,q).n
+//     Neumann:   the prescribed normal flux g_N |n|
 template <class T>
 void endpoint_flux(const Ctx& c, const T* ui, const T* qi, const T* uo, const T* qo,
-                   const double* bc, const double* n, int S, T* out) {
+                   const double* bc, int bkind, const double* n, int S, T* out) {
   const int m = c.m, D = c.D;
   for (int k = 0; k < m; ++k) out[k] = 0.0;
   const double nn = norm_of(n, D);
+  if (bc && bkind == LDG_BC_NEUMANN) {
+    for (int k = 0; k < m; ++k) out[k] = bc[k] * nn;
+    return;
+  }
   if (c.has_inv) {
     T g[MAXM];
     const T* other = uo;
-    if (bc) {
+    if (bc && bkind == LDG_BC_SLIP_WALL) {
+      double n2 = 0.0;
+      for (int d = 0; d < D; ++d) n2 += n[d] * n[d];
+      T mn = ui[1] * n[0];
+      for (int d = 1; d < D; ++d) mn = mn + ui[1 + d] * n[d];
+      const T f = mn * (2.0 / n2);
+      g[0] = ui[0];
+      for (int d = 0; d < D; ++d) g[1 + d] = ui[1 + d] - f * n[d];
+      g[m - 1] = ui[m - 1];
+      other = g;
+    } else if (bc) {
       for (int k = 0; k < m; ++k) g[k] = bc[k];
       other = g;
     }
@@ -287,8 +316,12 @@ void endpoint_flux(const Ctx& c, const T* ui, const T* qi, const T* uo, const T*
     T fv[MAXM];
     if (bc) {
       vflux_dot(c, ui, qi, n, fv);
-      const double c11 = c.c11_bd * c.p * c.p / std::pow(nn, 1.0 / (D - 1));
-      for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k] + c11 * nn * (ui[k] - bc[k]);
+      if (bkind == LDG_BC_SLIP_WALL) {
+        for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k];
+      } else {
+        const double c11 = c.c11_bd * c.p * c.p / std::pow(nn, 1.0 / (D - 1));
+        for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k] + c11 * nn * (ui[k] - bc[k]);
+      }
     } else {
       if (S > 0) vflux_dot(c, uo, qo, n, fv);
       else vflux_dot(c, ui, qi, n, fv);
@@ -306,6 +339,7 @@ struct LineData {
   double q[MAXNP][MAXM * MAXD];
   double uo[2][MAXM], qo[2][MAXM * MAXD];
   const double* bc[2];
+  int bk[2];  // boundary kind of each end (-1 interior)
 };
 
 void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const double* Q,
@@ -320,8 +354,10 @@ void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const 
   for (int side = 0; side < 2; ++side) {
     const size_t k = c.epi(e, dir, side, line);
     L.bc[side] = nullptr;
+    L.bk[side] = -1;
     if (c.ep_bc[k] >= 0) {
       L.bc[side] = c.bcv[c.ep_bc[k]].data();
+      L.bk[side] = c.bck[c.ep_bc[k]];
       continue;
     }
     const size_t nd = static_cast<size_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
@@ -356,7 +392,7 @@ void line_residual(const Ctx& c, int e, int dir, int line, const LineData& L, do
   for (int side = 0; side < 2; ++side) {
     const int ie = side ? c.p : 0;
     double fh[MAXM];
-    endpoint_flux<double>(c, L.u[ie], L.q[ie], L.uo[side], L.qo[side], L.bc[side],
+    endpoint_flux<double>(c, L.u[ie], L.q[ie], L.uo[side], L.qo[side], L.bc[side], L.bk[side],
                           c.ne(e, dir, side, line), c.sign(e, dir, side), fh);
     for (int k = 0; k < m; ++k) r[ie][k] += fh[k];
   }
@@ -407,7 +443,8 @@ void line_gradient(const Ctx& c, int e, int dir, int line, const LineData& L,
     const int ie = side ? c.p : 0;
     const double* n = c.ne(e, dir, side, line);
     const double* uh;
-    if (L.bc[side]) uh = L.bc[side];  // u_hat = g_D
+    if (L.bc[side] && !uhat_inner(L.bk[side])) uh = L.bc[side];  // u_hat = g_D
+    else if (L.bc[side]) uh = L.u[ie];                        // Neumann-type / slip wall
     else uh = c.sign(e, dir, side) > 0 ? L.u[ie] : L.uo[side];
     for (int k = 0; k < m; ++k)
       for (int dd = 0; dd < D; ++dd) d[ie][k * D + dd] += uh[k] * n[dd];
@@ -485,17 +522,19 @@ void pattern_line(const Ctx& c, int e, int dir, int line, int which, std::vector
       const size_t k = c.epi(e, dir, side, line);
       const int ie = side ? c.p : 0;
       const bool bd = c.ep_bc[k] >= 0;
+      const int bkind = bd ? c.bck[c.ep_bc[k]] : -1;
+      const bool neu = bkind == LDG_BC_NEUMANN;  // prescribed flux: no u or q dependence
       const int64_t nbr = bd ? -1 : static_cast<int64_t>(c.ep_elem[k]) * c.npe + c.ep_node[k];
       const int S = c.sign(e, dir, side);
       if (which == LDG_K11) {
         bool in = false, outn = false;
         if (c.has_inv) {
-          in = true;
+          in = !neu;
           outn = !bd;
         }
         if (c.second) {
           if (bd) {
-            in = in || c.vis_u || c.c11_bd != 0.0;
+            in = in || (!neu && (c.vis_u || (bkind != LDG_BC_SLIP_WALL && c.c11_bd != 0.0)));
           } else {
             if (c.vis_u) {
               if (S > 0) outn = true;
@@ -507,10 +546,15 @@ void pattern_line(const Ctx& c, int e, int dir, int line, int which, std::vector
         if (in) out.push_back({own(i), own(ie)});
         if (outn) out.push_back({own(i), nbr});
       } else if (which == LDG_K12) {
-        if (bd || S <= 0) out.push_back({own(i), own(ie)});
+        if (bd) {
+          if (!neu) out.push_back({own(i), own(ie)});
+        } else if (S <= 0) out.push_back({own(i), own(ie)});
         else out.push_back({own(i), nbr});
       } else {  // K21: u_hat
-        if (bd) continue;
+        if (bd) {
+          if (uhat_inner(bkind)) out.push_back({own(i), own(ie)});
+          continue;
+        }
         if (S > 0) out.push_back({own(i), own(ie)});
         else out.push_back({own(i), nbr});
       }
@@ -664,7 +708,7 @@ void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
             qi[k] = DU(c.second ? L.q[ie][k] : 0.0);
             qo[k] = DU(c.second && !bd ? L.qo[side][k] : 0.0);
           }
-          endpoint_flux<DU>(c, ui, qi, uo, qo, L.bc[side], n, S, f);
+          endpoint_flux<DU>(c, ui, qi, uo, qo, L.bc[side], L.bk[side], n, S, f);
           for (int a = 0; a < m; ++a)
             for (int b = 0; b < m; ++b) e11[side][pass][a * m + b] = f[a].d[b];
           has11[side][pass] = true;
@@ -682,7 +726,7 @@ void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
             if (pass == 0) qi[k].d[k] = 1.0;
             else qo[k].d[k] = 1.0;
           }
-          endpoint_flux<DQ>(c, ui, qi, uo, qo, L.bc[side], n, S, f);
+          endpoint_flux<DQ>(c, ui, qi, uo, qo, L.bc[side], L.bk[side], n, S, f);
           for (int a = 0; a < m; ++a)
             for (int b = 0; b < mD; ++b) e12[side][pass][a * mD + b] = f[a].d[b];
           has12[side][pass] = true;
@@ -778,7 +822,8 @@ void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
             }
             for (int side = 0; side < 2; ++side) {
               const int ie = side ? c.p : 0;
-              if (ie == cidx && !L.bc[side] && c.sign(e, dir, side) > 0) {
+              if (ie == cidx && ((!L.bc[side] && c.sign(e, dir, side) > 0) ||
+                                 (L.bc[side] && uhat_inner(L.bk[side])))) {
                 const double* n = c.ne(e, dir, side, line);
                 for (int dd = 0; dd < D; ++dd) col[ie][dd] += n[dd];
               }

@@ -105,6 +105,24 @@ int ref_case_save(void* h, const char* path) {
   }
 }
 
+// The reference's compute_mapping with a CurveProjector (mapping.cpp:30-65).
+int ref_case_remap(void* h, void (*fn)(void*, const double*, int, double*), void* user) {
+  try {
+    auto* c = static_cast<RefCase*>(h);
+    CurveProjector cp = [fn, user](const Eigen::Vector2d& x, int tag) {
+      const double xin[2] = {x.x(), x.y()};
+      double out[2];
+      fn(user, xin, tag, out);
+      return Eigen::Vector2d(out[0], out[1]);
+    };
+    c->maps = compute_mapping(c->m, c->b, &cp);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 void ref_case_free(void* h) { delete static_cast<RefCase*>(h); }
 int ref_case_num_faces(void* h) { return static_cast<RefCase*>(h)->m.num_faces(); }
 

@@ -18,6 +18,10 @@ LDG_ERR_INVALID_ARGUMENT = 5
 LDG_POISSON, LDG_EULER, LDG_NAVIER_STOKES = 0, 1, 2
 LDG_ROE, LDG_LLF = 0, 1
 LDG_BC_DIRICHLET = 0
+LDG_BC_NEUMANN = 1
+LDG_BC_CHARACTERISTIC = 2
+LDG_BC_SLIP_WALL = 3
+LDG_BC_NO_SLIP_ADIABATIC = 4
 LDG_K11, LDG_K12, LDG_K21 = 0, 1, 2
 
 _dp = C.POINTER(C.c_double)
@@ -95,6 +99,10 @@ class LhLatticeParams(C.Structure):
     ]
 
 
+# CurveProjector callback: fn(user, x[2], tag, out[2]) (mapping.hpp:13-15)
+CURVE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double))
+
+
 def _load(name: str) -> C.CDLL:
     path = os.path.join(_HERE, name)
     if name == "liblinedg_b200.so" and os.environ.get("LDG_B200_LIB"):
@@ -122,6 +130,8 @@ def host_lib() -> C.CDLL:
         L.lh_case_load_mesh.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _ip, _dp,
                                         C.POINTER(C.c_void_p)]
         L.lh_case_save_mesh.argtypes = [C.c_void_p, C.c_char_p]
+        L.lh_case_remap.argtypes = [C.c_void_p, CURVE_FN, C.c_void_p]
+        L.lh_case_remap_circles.argtypes = [C.c_void_p, C.c_int32, _ip, _dp, _dp, _dp]
         L.lh_case_setup.argtypes = [C.c_void_p]
         L.lh_case_setup.restype = C.POINTER(LdgSetup)
         L.lh_case_num_vertices.argtypes = [C.c_void_p]

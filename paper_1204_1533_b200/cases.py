@@ -27,7 +27,10 @@ GAMMA = 1.4
 @dataclass
 class Physics:
     """Mirror of GasModel / LdgParams / BoundaryTable (physics.hpp:10-35,
-    SPEC.md:197-205).  bcs: list of (tag, values) Dirichlet conditions."""
+    SPEC.md:197-205).  bcs: list of (tag, values) Dirichlet conditions or
+    (tag, values, kind) with kind an ldg_bc_kind (LDG_BC_NEUMANN: values =
+    g_N; LDG_BC_CHARACTERISTIC: values = far-field state; LDG_BC_SLIP_WALL:
+    values unused)."""
 
     kind: int = _abi.LDG_EULER
     riemann: int = _abi.LDG_ROE
@@ -47,9 +50,10 @@ class Physics:
 
     def to_c(self):
         arr = (LdgBc * max(1, len(self.bcs)))()
-        for i, (tag, vals) in enumerate(self.bcs):
+        for i, bc in enumerate(self.bcs):
+            tag, vals = bc[0], bc[1]
             arr[i].tag = tag
-            arr[i].kind = _abi.LDG_BC_DIRICHLET
+            arr[i].kind = bc[2] if len(bc) > 2 else _abi.LDG_BC_DIRICHLET
             for k, v in enumerate(vals):
                 arr[i].value[k] = v
         ph = LdgPhysics(self.kind, self.riemann, self.gamma, self.mu, self.prandtl, self.c11,
@@ -124,6 +128,31 @@ class Case:
     def save_mesh(self, path: str):
         """Write the mesh in the reference text format (save_mesh, mesh.cpp:148-160)."""
         st = self._lib.lh_case_save_mesh(self._h, os.fsencode(path))
+        if st != 0:
+            raise _setup_error(st)
+
+    # ------------------------------------------------------ curved geometry
+    def remap(self, projector):
+        """Recompute the mapping with a boundary projection (the reference
+        CurveProjector, mapping.hpp:13-15; mapping.cpp:30-65):
+        projector(x, y, tag) -> (x', y') for every boundary-face node."""
+        def _fn(_user, x, tag, out):
+            px, py = projector(x[0], x[1], tag)
+            out[0] = px
+            out[1] = py
+
+        cb = _abi.CURVE_FN(_fn)
+        st = self._lib.lh_case_remap(self._h, cb, None)
+        if st != 0:
+            raise _setup_error(st)
+
+    def remap_circles(self, circles):
+        """Built-in projector: circles = [(tag, cx, cy, r), ...]; boundary faces
+        with that tag are projected radially onto the circle."""
+        n = len(circles)
+        tags = np.array([c[0] for c in circles], dtype=np.int32)
+        cx, cy, r = (np.array([c[k] for c in circles], dtype=np.float64) for k in (1, 2, 3))
+        st = self._lib.lh_case_remap_circles(self._h, n, _abi.iptr(tags), dptr(cx), dptr(cy), dptr(r))
         if st != 0:
             raise _setup_error(st)
 
@@ -306,3 +335,30 @@ def _configs() -> List[Config]:
 
 
 CONFIGS = _configs()
+
+
+def annulus_mesh(nr: int, nt: int, r0: float, r1: float, stretch: float = 1.0):
+    """Straight-sided quadrilaterals of the ring r0 <= r <= r1 around the origin
+    (the paper's cylinder geometry): nr elements radially
+    (geometric spacing ratio `stretch`), nt around, closed by vertex reuse.
+    Returns (verts, elems, btags) with tag 1 on the cylinder (local face 3)
+    and tag 2 on the far field (local face 1); elements CCW (v0 at (r_i,
+    theta_j), v1 at (r_i+1, theta_j))."""
+    if stretch == 1.0:
+        radii = np.linspace(r0, r1, nr + 1)
+    else:
+        w = stretch ** np.arange(nr)
+        radii = r0 + (r1 - r0) * np.concatenate([[0.0], np.cumsum(w) / w.sum()])
+    th = 2 * np.pi * np.arange(nt) / nt
+    verts = np.array([[r * np.cos(t), r * np.sin(t)] for t in th for r in radii])
+    vid = lambda i, j: (j % nt) * (nr + 1) + i  # noqa: E731
+    elems, btags = [], []
+    for j in range(nt):
+        for i in range(nr):
+            e = len(elems)
+            elems.append([vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)])
+            if i == 0:
+                btags.append([e, 3, 1])
+            if i == nr - 1:
+                btags.append([e, 1, 2])
+    return verts, np.array(elems, dtype=np.int32), np.array(btags, dtype=np.int32)

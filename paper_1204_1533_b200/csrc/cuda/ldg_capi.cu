@@ -89,6 +89,8 @@ struct ldg_ctx {
   double* d_metric = nullptr;
   int2* d_conn = nullptr;
   double* d_bcv = nullptr;
+  int32_t* d_bck = nullptr;     // boundary kind per boundary index
+  std::vector<int32_t> bck;
   double* d_source = nullptr;
   ldg::DevError* h_err = nullptr;
   ldg::DevError* d_err = nullptr;
@@ -129,6 +131,7 @@ struct ldg_ctx {
     cudaFree(d_kred);
     cudaFree(d_ti);
     cudaFree(d_bcv);
+    cudaFree(d_bck);
     cudaFree(d_source);
     cudaFree(d_Q);
     cudaFree(d_w);
@@ -181,9 +184,11 @@ struct ldg_ctx {
   bool in_dep(int k, int dir, int side) const {
     const int2& c = cn(k, dir, side);
     const bool bd = c.x < 0;
+    const int bkind = bd ? bck[-1 - c.x] : -1;
+    if (bkind == LDG_BC_NEUMANN) return false;  // prescribed flux: no u dependence
     if (has_inv) return true;
     if (!second) return false;
-    if (bd) return vis_u || c11bd != 0.0;
+    if (bd) return vis_u || (bkind != LDG_BC_SLIP_WALL && c11bd != 0.0);
     return (vis_u && csign(c) <= 0) || c11 != 0.0;
   }
   bool out_dep(int k, int dir, int side) const {
@@ -430,13 +435,23 @@ std::vector<int32_t> processing_order(const ldg_setup& s, int D, int npe) {
 void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   std::map<int, int> tag2bc;
   std::vector<double> bcv;
+  c.bck.clear();
   for (int i = 0; i < ph.n_bc; ++i) {
-    if (ph.bcs[i].kind != LDG_BC_DIRICHLET)
+    const int kind = ph.bcs[i].kind;
+    if (kind == LDG_BC_NO_SLIP_ADIABATIC)
+      throw ldg_error(LDG_ERR_CONFIG,
+                      "no-slip adiabatic walls are not supported (their gradient trace u_hat is component-dependent; "
+                      "the K21 store is component-uniform)");
+    if (kind < LDG_BC_DIRICHLET || kind > LDG_BC_SLIP_WALL)
       throw ldg_error(LDG_ERR_CONFIG, "unsupported boundary-condition kind");
+    if (kind == LDG_BC_SLIP_WALL && !c.has_inv)
+      throw ldg_error(LDG_ERR_CONFIG, "slip-wall boundaries need Euler or Navier-Stokes physics");
     tag2bc[ph.bcs[i].tag] = i;
+    c.bck.push_back(kind);
     for (int k = 0; k < c.m; ++k) bcv.push_back(ph.bcs[i].value[k]);
   }
   if (bcv.empty()) bcv.push_back(0.0);
+  if (c.bck.empty()) c.bck.push_back(0);
   const int F = 2 * c.D, P = c.p;
   c.conn.assign(static_cast<size_t>(c.E) * c.D * 2, int2{0, 0});
   c.fpart.assign(static_cast<size_t>(c.E) * c.D * 2, int2{-1, 0});
@@ -507,6 +522,8 @@ void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   }
   ck(cudaMalloc(&c.d_bcv, bcv.size() * sizeof(double)), "cudaMalloc bcv");
   ck(cudaMemcpy(c.d_bcv, bcv.data(), bcv.size() * sizeof(double), cudaMemcpyHostToDevice), "upload bcv");
+  ck(cudaMalloc(&c.d_bck, c.bck.size() * sizeof(int32_t)), "cudaMalloc bck");
+  ck(cudaMemcpy(c.d_bck, c.bck.data(), c.bck.size() * sizeof(int32_t), cudaMemcpyHostToDevice), "upload bck");
   ck(cudaMalloc(&c.d_conn, c.conn.size() * sizeof(int2)), "cudaMalloc conn");
   ck(cudaMemcpy(c.d_conn, c.conn.data(), c.conn.size() * sizeof(int2), cudaMemcpyHostToDevice),
      "upload conn");
@@ -798,6 +815,7 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     d.metric = c->d_metric;
     d.conn = c->d_conn;
     d.bcv = c->d_bcv;
+    d.bck = c->d_bck;
     d.source = nullptr;
     d.err = c->d_err;
     d.E = c->E;

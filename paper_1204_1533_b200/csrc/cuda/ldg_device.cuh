@@ -87,6 +87,10 @@ struct PhysParams {
   double c11, c11bd;      // interior C11; boundary coefficient c11_bd * p^2
 };
 
+// Boundary condition kinds (reference BcKind, physics.hpp:16; the values of
+// ldg_bc_kind in include/linedg_b200.h).
+enum BcKindDev : int { BC_DIRICHLET = 0, BC_NEUMANN = 1, BC_CHARACTERISTIC = 2, BC_SLIP_WALL = 3 };
+
 // ------------------------------------------------------------ Dual<N>
 template <int N>
 struct Dual {
@@ -245,6 +249,31 @@ __device__ __forceinline__ void euler_jac_n(const double* u, const double* n, do
 #pragma unroll
   for (int j = 0; j < D; ++j) r[1 + j] = H * n[j] - g1 * un * v[j];
   r[D + 1] = gamma * un;
+}
+
+// Exterior state of a boundary line end for the Riemann flux
+// (SPEC.md:266, 366-368): Dirichlet / characteristic far field -> g (the
+// prescribed / free-stream state); slip wall -> the interior state with its
+// normal momentum mirrored, m - 2 (m.n) n / |n|^2.  T = double or Dual<N>
+// (the ghost is a function of u_in, so its derivative carries through).
+template <int D, int M, class T>
+__device__ __forceinline__ void bc_ghost(int kind, const double* g, const T* ui, const double* n, T* uo) {
+  if (M == D + 2 && kind == BC_SLIP_WALL) {
+    double n2 = n[0] * n[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) n2 += n[d] * n[d];
+    T mn = ui[1] * n[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) mn = mn + ui[1 + d] * n[d];
+    const T f = mn * (2.0 / n2);
+    uo[0] = ui[0];
+#pragma unroll
+    for (int d = 0; d < D; ++d) uo[1 + d] = ui[1 + d] - f * n[d];
+    uo[M - 1] = ui[M - 1];
+  } else {
+#pragma unroll
+    for (int c = 0; c < M; ++c) uo[c] = T(__ldg(g + c));
+  }
 }
 
 // Roe flux (u_out = R, u_in = L), outward normal n.

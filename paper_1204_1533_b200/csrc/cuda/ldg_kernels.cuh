@@ -31,7 +31,8 @@ struct KParams {
   const int32_t* order;  // processing index k -> reference element e
   const double* metric;  // [k][METP]
   const int2* conn;      // [k][D][2]
-  const double* bcv;     // [nbc][M]
+  const double* bcv;     // [nbc][M] boundary data (Dirichlet / far-field state, Neumann flux)
+  const int32_t* bck;    // [nbc] boundary kind (BcKindDev)
   const double* source;  // reference numbering, may be null
   DevError* err;
   const int2* fpart;     // [k][2D] face partner {k', 2 dir' + side'} ({-1, 0}: none)
@@ -40,6 +41,55 @@ struct KParams {
   int E;                 // elements
   int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2, bit2 skip the staged bulk store
 };
+
+// Numerical flux F_hat.n at a boundary line end (SPEC.md:266,
+// 366-368), bc = boundary index, n the non-normalised outward normal, nn = |n|:
+//   Dirichlet / characteristic: Riemann flux against g (the prescribed /
+//     free-stream state) + viscous F(u_in, q_in).n + C11_bd |n| (u_in - g);
+//   slip wall: Riemann flux against the mirrored-normal-momentum ghost of
+//     u_in + viscous F(u_in, q_in).n (no penalty);
+//   Neumann: the prescribed normal flux g_N |n| (no other term).
+// T = double or Dual<N> in u_in; TQ the type of q_in.
+template <class C, class T, class TQ>
+__device__ __forceinline__ void bnd_flux(const KParams<C>& kp, int bc, const T* ui, const TQ* qi, const double* n,
+                                         double nn, T* fh, bool& ok) {
+  constexpr int M = C::M, D = C::D;
+  const int kind = __ldg(kp.bck + bc);
+  const double* g = kp.bcv + bc * M;
+#pragma unroll
+  for (int c = 0; c < M; ++c) fh[c] = T(0.0);
+  if (kind == BC_NEUMANN) {
+#pragma unroll
+    for (int c = 0; c < M; ++c) fh[c] = T(__ldg(g + c) * nn);
+    return;
+  }
+  if (C::HAS_INV) {
+    T uo[M];
+    bc_ghost<D, M>(kind, g, ui, n, uo);
+    if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+    else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+  }
+  if (C::SECOND) {
+    T fv[M];
+    visc_fn<D, C::PH, T, TQ, T>(ui, qi, n, kp.pp, fv, ok);
+    if (kind == BC_SLIP_WALL) {
+#pragma unroll
+      for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
+    } else {
+      const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+#pragma unroll
+      for (int c = 0; c < M; ++c) fh[c] = fh[c] + (fv[c] + (c11 * nn) * (ui[c] - __ldg(g + c)));
+    }
+  }
+}
+// u_hat of the auxiliary gradient at a boundary end: g (Dirichlet-type,
+// PAPER.md:573) or the interior trace (Neumann-type with C22 = 0,
+// PAPER.md:580; slip wall)
+template <class C>
+__device__ __forceinline__ bool bnd_uhat_inner(const KParams<C>& kp, int bc) {
+  const int kind = __ldg(kp.bck + bc);
+  return kind == BC_NEUMANN || kind == BC_SLIP_WALL;
+}
 
 #ifndef LDG_VISC_DU  // closed-form viscous dF/du (1) or dual numbers (0)
 #define LDG_VISC_DU 1
@@ -344,12 +394,21 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
         ui[c] = sul[nd * M + c];
         fh[c] = 0.0;
       }
-      if (C::HAS_INV) {
-        double g[M];
+      if (bcp[side]) {
+        double nn = n[0] * n[0];
 #pragma unroll
-        for (int c = 0; c < M; ++c) g[c] = bcp[side] ? __ldg(bcp[side] + c) : uo[side][c];
-        if (C::RI == LDG_ROE) roe_fn<D>(g, ui, n, kp.pp.gamma, fh, ok);
-        else llf_fn<D>(g, ui, n, kp.pp.gamma, fh, ok);
+        for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+        nn = sqrt(nn);
+        double qi[C::SECOND ? MD : 1];
+        if (C::SECOND) {
+#pragma unroll
+          for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
+        }
+        bnd_flux<C>(kp, static_cast<int>(bcp[side] - kp.bcv) / M, ui, qi, n, nn, fh, ok);
+      } else {
+      if (C::HAS_INV) {
+        if (C::RI == LDG_ROE) roe_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
+        else llf_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
       }
       if (C::SECOND) {
         double nn = n[0] * n[0];
@@ -357,15 +416,7 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
         for (int d = 1; d < D; ++d) nn += n[d] * n[d];
         nn = sqrt(nn);
         double fv[M];
-        if (bcp[side]) {
-          double qi[MD];
-#pragma unroll
-          for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
-          visc_fn<D, C::PH, double, double, double>(ui, qi, n, kp.pp, fv, ok);
-          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
-#pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - __ldg(bcp[side] + c));
-        } else {
+        {
           if (sg[side] > 0) {
             visc_fn<D, C::PH, double, double, double>(uo[side], qo[side], n, kp.pp, fv, ok);
           } else {
@@ -381,6 +432,7 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
             for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[side][c]);
           }
         }
+      }
       }
 #pragma unroll
       for (int i = 0; i < NP; ++i)
@@ -524,6 +576,13 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
       ui[c] = sul[nd * M + c];
       uo[c] = bcp ? __ldg(bcp + c) : __ldg(U + ond * M + c);
     }
+    if (bcp) {
+      double nn = n[0] * n[0];
+#pragma unroll
+      for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+      nn = sqrt(nn);
+      bnd_flux<C>(kp, -1 - cn.x, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
+    } else {
     if (C::HAS_INV) {
       if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
       else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
@@ -555,6 +614,7 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
           for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
         }
       }
+    }
     }
   }
   // lane transpose: lane i < NP forms r_i
@@ -811,6 +871,13 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
           uo[c] = bcp ? __ldg(bcp + c) : bNB(cur)[w * M + c];
           fh[c] = 0.0;
         }
+        if (bcp) {
+          double nn = n[0] * n[0];
+#pragma unroll
+          for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+          nn = sqrt(nn);
+          bnd_flux<C>(kp, -1 - cn.x, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
+        } else {
         if (C::HAS_INV) {
           if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
           else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
@@ -836,6 +903,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
               for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
             }
           }
+        }
         }
 #pragma unroll
         for (int i = 0; i < NP; ++i)
@@ -1117,7 +1185,14 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
           uo[c] = bcp ? __ldg(bcp + c) : io.bNB(cur)[w * M + c];
           fh[c] = 0.0;
         }
-        if (C::HAS_INV) {
+        if (bcp) {
+            double nn = n[0] * n[0];
+#pragma unroll
+            for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+            nn = sqrt(nn);
+            bnd_flux<C>(kp, -1 - cn.x, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
+          } else {
+          if (C::HAS_INV) {
           if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
           else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
         }
@@ -1143,6 +1218,7 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
             }
           }
         }
+          }
 #pragma unroll
         for (int c = 0; c < M; ++c) sFH[w * M + c] = fh[c];
       } else {
@@ -1309,8 +1385,10 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
       for (int side = 0; side < 2; ++side) {
         const int2 cn = io.bCONN(cur)[(l * D + dir) * 2 + side];
         double uh;
-        if (cn.x < 0) uh = __ldg(kp.bcv + (-1 - cn.x) * M + c);  // Dirichlet: u_hat = g_D
-        else if (conn_sign(cn.y) > 0) uh = ul[side ? P : 0];     // S = +1: own trace
+        if (cn.x < 0 && !bnd_uhat_inner(kp, -1 - cn.x))
+          uh = __ldg(kp.bcv + (-1 - cn.x) * M + c);  // Dirichlet-type: u_hat = g_D
+        else if (cn.x < 0 || conn_sign(cn.y) > 0)
+          uh = ul[side ? P : 0];  // S = +1; Neumann-type / slip-wall boundary
         else uh = io.bNB(cur)[((lw << 1) | side) * M + c];
         const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
 #pragma unroll
@@ -1403,10 +1481,10 @@ k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict
       const int ie = side ? C::P : 0;
       const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
       double uh[M];
-      if (cn.x < 0) {  // Dirichlet: u_hat = g_D
+      if (cn.x < 0 && !bnd_uhat_inner(kp, -1 - cn.x)) {  // Dirichlet-type: u_hat = g_D
 #pragma unroll
         for (int c = 0; c < M; ++c) uh[c] = __ldg(kp.bcv + (-1 - cn.x) * M + c);
-      } else if (conn_sign(cn.y) > 0) {  // S = +1: own trace
+      } else if (cn.x < 0 || conn_sign(cn.y) > 0) {  // S = +1; Neumann-type / slip wall
         const int nd = node_on_line<C>(dir, line, ie);
 #pragma unroll
         for (int c = 0; c < M; ++c) uh[c] = sul[nd * M + c];
@@ -1622,11 +1700,16 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const size_t own = e * NPE + nd;
   const size_t onb = bd ? 0 : static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
   double uiv[M], uov[M];
+  // boundary kind: Dirichlet / characteristic (ghost = g), slip wall (ghost =
+  // mirrored u_in), Neumann (constant flux: no u dependence), see bnd_flux
+  const int bkind = bd ? __ldg(kp.bck + (-1 - cn.x)) : -1;
+  const bool bneu = bkind == BC_NEUMANN, bslip = bkind == BC_SLIP_WALL;
 #pragma unroll
   for (int c = 0; c < M; ++c) {
     uiv[c] = __ldg(U + own * M + c);
-    uov[c] = bd ? __ldg(bcp + c) : __ldg(U + onb * M + c);
+    if (!bd) uov[c] = __ldg(U + onb * M + c);
   }
+  if (bd) bc_ghost<D, M>(bkind, bcp, uiv, n, uov);
   bool ok = true;
   using D1 = Dual<1>;
   if (pass < 2) {
@@ -1656,17 +1739,37 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     double Jx[(LLFC || VCF) ? M * M : 1];
 #pragma unroll
     for (int c = 0; c < ((LLFC || VCF) ? M * M : 1); ++c) Jx[c] = 0.0;
-    if (LLFC) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Jx, ok);
+    if (LLFC && !bneu) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Jx, ok);
+    if (LLFC && bslip) {
+      // chain rule through the ghost: dFh/du_in += dFh/du_out * dghost/du_in,
+      // dghost/du_in = diag(1, I - 2 n n^T / |n|^2, 1)
+      double J1[LLFC ? M * M : 1], n2 = 0.0;
+      llf_jac<D>(uov, uiv, n, kp.pp.gamma, 1, J1, ok);
+#pragma unroll
+      for (int d = 0; d < D; ++d) n2 += n[d] * n[d];
+#pragma unroll
+      for (int c = 0; c < (LLFC ? M : 0); ++c) {
+        Jx[c * M] += J1[c * M];
+        Jx[c * M + M - 1] += J1[c * M + M - 1];
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double v = J1[c * M + 1 + b];
+#pragma unroll
+          for (int k2 = 0; k2 < D; ++k2) v -= J1[c * M + 1 + k2] * (2.0 * n[k2] * n[b] / n2);
+          Jx[c * M + 1 + b] += v;
+        }
+      }
+    }
     if (VCF) {
       const bool sel_in = bd || S <= 0;  // the viscous flux is taken from u_in (else u_out)
-      if ((pass == 0) == sel_in) {
+      if ((pass == 0) == sel_in && !bneu) {
         double Jv[M * M];
         visc_du<D, C::PH>(sel_in ? uiv : uov, sel_in ? qiv : qov, n, kp.pp, Jv, ok);
 #pragma unroll
         for (int c = 0; c < M * M; ++c) Jx[c] += Jv[c];
       }
       double pen = 0.0;
-      if (bd) pen = pass == 0 ? (kp.pp.c11bd / (D == 2 ? nn : sqrt(nn))) * nn : 0.0;
+      if (bd) pen = (pass == 0 && !bneu && !bslip) ? (kp.pp.c11bd / (D == 2 ? nn : sqrt(nn))) * nn : 0.0;
       else if (kp.pp.c11 != 0.0) pen = pass == 0 ? kp.pp.c11 * nn : -(kp.pp.c11 * nn);
 #pragma unroll
       for (int c = 0; c < M; ++c) Jx[c * M + c] += pen;
@@ -1688,17 +1791,20 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         uo[c].d[0] = (pass == 1 && c == b) ? 1.0 : 0.0;
         fh[c] = D1(0.0);
       }
-      if (C::HAS_INV) {
+      if (bslip) bc_ghost<D, M>(bkind, bcp, ui, n, uo);  // the ghost follows u_in
+      if (C::HAS_INV && !bneu) {
         if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
         else if (!LLFC) llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
       }
       if (C::SECOND && !VCF) {
         D1 fv[M];
         if (bd) {
-          visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
-          const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+          if (!bneu) {
+            visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
+            const double c11 = bslip ? 0.0 : kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
 #pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
+            for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * (ui[c] - __ldg(bcp + c));
+          }
         } else {
           if (S > 0) visc_fn<D, C::PH, D1, double, D1>(uo, qov, n, kp.pp, fv, ok);
           else visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
@@ -1723,7 +1829,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     double L[M * MD];
     visc_dq<D, C::PH>(usrc, n, kp.pp, L, ok);
 #pragma unroll
-    for (int c = 0; c < M * MD; ++c) put(2, c, L[c]);
+    for (int c = 0; c < M * MD; ++c) put(2, c, bneu ? 0.0 : L[c]);
   }
   if (!ok) {
     // a non-physical state at this line end: report the offending nodal state
@@ -1766,8 +1872,9 @@ struct JacThreads {
   // is 129..256 threads (no tail round behind the barrier), else 128
   static constexpr int p2 = (TileLines<C>::NLT * C::B11 + 31) / 32 * 32;
 #ifndef LDG_JT_SMALL  // tuning knobs (variant builds): CTA size / min CTAs per SM
-  // (measured: second-order tiles gain from it, the Euler tile does not)
-  static constexpr int small = C::SECOND && p2 > 128 && p2 <= 256 ? p2 : 128;
+  // (measured: second-order tiles gain from it; the C2 Euler tile too since
+  // the single-chunk endpoint scratch: 0.242 vs 0.252 ms at 160 vs 128 threads)
+  static constexpr int small = p2 > 128 && p2 <= 256 ? p2 : 128;
 #else
   static constexpr int small = LDG_JT_SMALL;
 #endif
@@ -2732,10 +2839,12 @@ __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __rest
     double v = 0.0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) v += kp.bt.cc[p][t][q] * __ldg(mk + ((dir * NL + line) * NQ + q) * D + d);
-    // u_hat = own trace where S = +1, neighbour where S = -1, g_D on boundaries
-    if (t == 0 && c0.x >= 0 && conn_sign(c0.y) > 0)
+    // u_hat = own trace where S = +1, neighbour where S = -1; on boundaries
+    // g_D (Dirichlet-type: no u dependence) or the own trace (Neumann / slip wall)
+    auto own_uh = [&](int2 cx) { return cx.x >= 0 ? conn_sign(cx.y) > 0 : bnd_uhat_inner(kp, -1 - cx.x); };
+    if (t == 0 && own_uh(c0))
       v += kp.bt.mi[p][0] * __ldg(mk + C::MET_NV + ((dir * 2 + 0) * NL + line) * D + d);
-    if (t == P && c1.x >= 0 && conn_sign(c1.y) > 0)
+    if (t == P && own_uh(c1))
       v += kp.bt.mi[p][1] * __ldg(mk + C::MET_NV + ((dir * 2 + 1) * NL + line) * D + d);
     return v;
   };

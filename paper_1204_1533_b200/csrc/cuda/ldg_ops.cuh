@@ -25,6 +25,7 @@ struct DevCtx {
   const double* metric = nullptr;
   const int2* conn = nullptr;
   const double* bcv = nullptr;
+  const int32_t* bck = nullptr;
   const double* source = nullptr;
   DevError* err = nullptr;
   // face sharing of the endpoint flux Jacobians (null = every line end computes its own)
@@ -74,6 +75,7 @@ struct Launch {
     kp.metric = d.metric;
     kp.conn = d.conn;
     kp.bcv = d.bcv;
+    kp.bck = d.bck;
     kp.source = d.source;
     kp.err = d.err;
     kp.fpart = d.fpart;

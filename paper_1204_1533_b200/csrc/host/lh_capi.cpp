@@ -185,6 +185,56 @@ int lh_case_save_mesh(const lh_case* c, const char* path) {
   }
 }
 
+// Curved boundaries: recompute the mapping with a boundary projection
+// (CurveProjector, mapping.hpp:13-15; mapping.cpp:30-65).  fn(user, x, tag,
+// out) returns the projected position of a straight-sided boundary node.
+int lh_case_remap(lh_case* c, void (*fn)(void*, const double*, int, double*), void* user) {
+  try {
+    if (c->mesh.dim != 2) throw config_error("mapping: curved boundaries are 2-D only (reference mapping.cpp)");
+    CurveProjector cp;
+    cp.fn = fn;
+    cp.user = user;
+    c->map = compute_mapping(c->mesh, c->basis, fn ? &cp : nullptr);
+    c->flatten();
+    return LDG_OK;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
+namespace {
+struct Circles {
+  std::vector<int> tags;
+  std::vector<double> cx, cy, r;
+};
+// radial projection onto the circle of the face's tag (identity for other tags)
+void circle_proj(void* user, const double* x, int tag, double* out) {
+  const Circles& cs = *static_cast<const Circles*>(user);
+  out[0] = x[0];
+  out[1] = x[1];
+  for (size_t i = 0; i < cs.tags.size(); ++i)
+    if (cs.tags[i] == tag) {
+      const double dx = x[0] - cs.cx[i], dy = x[1] - cs.cy[i];
+      const double s = cs.r[i] / std::sqrt(dx * dx + dy * dy);
+      out[0] = cs.cx[i] + s * dx;
+      out[1] = cs.cy[i] + s * dy;
+      return;
+    }
+}
+}  // namespace
+
+// Built-in projector: boundary faces tagged tags[k] lie on the circle of
+// centre (cx[k], cy[k]) and radius r[k] (the paper's cylinder geometry).
+int lh_case_remap_circles(lh_case* c, int32_t n, const int32_t* tags, const double* cx, const double* cy,
+                          const double* r) {
+  Circles cs;
+  cs.tags.assign(tags, tags + n);
+  cs.cx.assign(cx, cx + n);
+  cs.cy.assign(cy, cy + n);
+  cs.r.assign(r, r + n);
+  return lh_case_remap(c, circle_proj, &cs);
+}
+
 void lh_case_free(lh_case* c) { delete c; }
 int32_t lh_case_num_tag_lines(const lh_case* c) { return static_cast<int32_t>(c->tag_lines.size() / 3); }
 void lh_case_tag_lines(const lh_case* c, int32_t* out) {

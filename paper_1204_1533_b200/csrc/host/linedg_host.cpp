@@ -635,7 +635,7 @@ int count_switch_violations(const Mesh& m, const std::vector<int8_t>& sw) {
 
 // ================================================================= mapping
 
-Mapping compute_mapping(const Mesh& m, const Basis1D& b) {
+Mapping compute_mapping(const Mesh& m, const Basis1D& b, const CurveProjector* curve) {
   const int D = m.dim, p = b.p, n = p + 1, nq = b.nq(), ne = m.ne();
   const int npe = D == 2 ? n * n : n * n * n;
   const int NL = D == 2 ? n : n * n;
@@ -655,8 +655,7 @@ Mapping compute_mapping(const Mesh& m, const Basis1D& b) {
   for (int e = 0; e < ne; ++e) {
     double* X = &mp.coords[static_cast<size_t>(e) * npe * D];
     const int* ev = &m.elems[static_cast<size_t>(e) * m.vpe()];
-    // Straight-sided isoparametric placement (mapping.cpp:12-29, bilinear;
-    // trilinear in 3-D).  Curved projection (mapping.cpp:30-65) is out of scope.
+    // Isoparametric placement (mapping.cpp:12-29, bilinear; trilinear in 3-D).
     if (D == 2) {
       const double* v0 = &m.verts[2 * ev[0]];
       const double* v1 = &m.verts[2 * ev[1]];
@@ -669,6 +668,49 @@ Mapping compute_mapping(const Mesh& m, const Basis1D& b) {
           for (int k = 0; k < 2; ++k)
             X[(i + n * j) * 2 + k] = w0 * v0[k] + w1 * v1[k] + w2 * v2[k] + w3 * v3[k];
         }
+      // Curved boundary (mapping.cpp:30-65): project the nodes of every
+      // boundary face, in local-face order, and blend each face's
+      // displacement linearly into the interior (weight 1 on the face, 0 on
+      // the opposite one).  Faces are processed in sequence on the updated
+      // positions, so a corner moved by face lf is re-projected by face lf+1.
+      if (curve && curve->fn) {
+        for (int lf = 0; lf < 4; ++lf) {
+          const Face& f = m.faces[m.elem_face[4 * e + lf]];
+          if (!f.boundary()) continue;
+          std::vector<double> delta(2 * n);
+          bool moved = false;
+          for (int k = 0; k < n; ++k) {
+            int i = 0, j = 0;  // face node k in face-parameter order (mesh.cpp:51-63)
+            switch (lf) {
+              case 0: i = k; j = 0; break;
+              case 1: i = p; j = k; break;
+              case 2: i = p - k; j = p; break;
+              default: i = 0; j = p - k; break;
+            }
+            const double* x0 = &X[(i + n * j) * 2];
+            double xp[2];
+            curve->fn(curve->user, x0, f.tag, xp);
+            delta[2 * k] = xp[0] - x0[0];
+            delta[2 * k + 1] = xp[1] - x0[1];
+            if (std::sqrt(delta[2 * k] * delta[2 * k] + delta[2 * k + 1] * delta[2 * k + 1]) > 0.0) moved = true;
+          }
+          if (!moved) continue;
+          for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+              const double si = b.nodes[i], sj = b.nodes[j];
+              double blend;
+              int k;
+              switch (lf) {
+                case 0: blend = 1 - sj; k = i; break;
+                case 1: blend = si; k = j; break;
+                case 2: blend = sj; k = p - i; break;
+                default: blend = 1 - si; k = p - j; break;
+              }
+              X[(i + n * j) * 2] += blend * delta[2 * k];
+              X[(i + n * j) * 2 + 1] += blend * delta[2 * k + 1];
+            }
+        }
+      }
     } else {
       for (int kk = 0; kk < n; ++kk)
         for (int j = 0; j < n; ++j)

@@ -7,7 +7,7 @@
 // 3-D hexahedra (the paper's formulation):
 //   * NodalBasis1D / make_basis / gauss_legendre   basis.cpp:11-193
 //   * build_faces / make_periodic / assign_switches mesh.cpp:51-364
-//   * compute_mapping (straight-sided)              mapping.cpp:12-153
+//   * compute_mapping (+ curved boundary projection) mapping.cpp:12-153
 //   * lattice mesh generators + seeded states for the BASELINE.json configs
 // Everything here is setup, run once per case; the hot path lives in the
 // CUDA library (csrc/cuda) behind include/linedg_b200.h.
@@ -89,7 +89,15 @@ struct Mapping {
   std::vector<double> nvec;    // [E][D][NL][nq][D]
   std::vector<double> nend;    // [E][D][2][NL][D]
 };
-Mapping compute_mapping(const Mesh& m, const Basis1D& b);
+// Boundary projection of high-order nodes (the reference CurveProjector,
+// mapping.hpp:13-15): out = projection of the straight-sided position x of a
+// node on a boundary face with the given tag.
+struct CurveProjector {
+  void (*fn)(void* user, const double* x, int tag, double* out) = nullptr;
+  void* user = nullptr;
+};
+// curve (optional, 2-D): boundary projection + transfinite blend (mapping.cpp:30-65).
+Mapping compute_mapping(const Mesh& m, const Basis1D& b, const CurveProjector* curve = nullptr);
 
 // ---------------------------------------------------------------- RNG
 // splitmix64; uniform from the top 53 bits; normal by Box-Muller.
