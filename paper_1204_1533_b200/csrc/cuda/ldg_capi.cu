@@ -70,9 +70,11 @@ struct ldg_ctx {
   std::vector<int2> conn;
   std::vector<int2> fpart;       // [k][2D] face partner {k', 2 dir' + side'} or {-1, 0}
   std::vector<int64_t> owned_off;  // per Jacobian chunk, into d_owned
+  std::vector<int64_t> bspec_off;  // per Jacobian chunk, into d_bspec (slip-wall / Neumann ends)
   // device
   int2* d_fpart = nullptr;
   int32_t* d_owned = nullptr;
+  int32_t* d_bspec = nullptr;
   int32_t* d_inv_order = nullptr;
   // block-Jacobi preconditioner (per element LU, column-major) and GMRES workspace
   double* d_pcLU = nullptr;
@@ -122,6 +124,7 @@ struct ldg_ctx {
     cudaFree(d_conn);
     cudaFree(d_fpart);
     cudaFree(d_owned);
+    cudaFree(d_bspec);
     cudaFree(d_inv_order);
     cudaFree(d_pcLU);
     cudaFree(d_pcPiv);
@@ -269,8 +272,12 @@ int local_face_ds(int D, int lf) {
 // face; then list, chunk by chunk, the faces whose Jacobians the chunk
 // computes: every face whose partner lies outside the chunk, and of an
 // in-chunk pair the one with the lower (k, ds).
-void build_face_sharing(ldg_ctx& c, int chunk) {
+// Boundary ends with a slip-wall or Neumann condition are listed apart
+// (bspec): k_endjac<..., BND = true> handles them, so the main instantiation
+// keeps a seed-independent exterior state.
+void build_face_sharing(ldg_ctx& c, int chunk, bool share) {
   const int F = 2 * c.D;
+  if (!share) std::fill(c.fpart.begin(), c.fpart.end(), int2{-1, 0});
   for (int k = 0; k < c.E; ++k)
     for (int ds = 0; ds < F; ++ds) {
       int2& p = c.fpart[static_cast<size_t>(k) * F + ds];
@@ -280,18 +287,30 @@ void build_face_sharing(ldg_ctx& c, int chunk) {
       const int s1 = (c.conn[static_cast<size_t>(p.x) * F + p.y].y >> 24) & 1;
       if (p.y < 0 || q.x != k || q.y != ds || (c.second && s0 == s1)) p = int2{-1, 0};
     }
-  std::vector<int32_t> owned;
+  std::vector<int32_t> owned, bspec;
   c.owned_off.assign(1, 0);
+  c.bspec_off.assign(1, 0);
   for (int kb = 0; kb < c.E; kb += chunk) {
     const int ke = std::min(c.E, kb + chunk);
     for (int k = kb; k < ke; ++k)
       for (int ds = 0; ds < F; ++ds) {
+        const int2 cx = c.conn[static_cast<size_t>(k) * F + ds];
+        if (cx.x < 0) {
+          const int kind = c.bck[-1 - cx.x];
+          if (kind == LDG_BC_SLIP_WALL || kind == LDG_BC_NEUMANN) {
+            bspec.push_back(k * F + ds);
+            continue;
+          }
+        }
         const int2 p = c.fpart[static_cast<size_t>(k) * F + ds];
         const bool mine = p.x < kb || p.x >= ke || static_cast<int64_t>(k) * F + ds < static_cast<int64_t>(p.x) * F + p.y;
         if (mine) owned.push_back(k * F + ds);
       }
     c.owned_off.push_back(static_cast<int64_t>(owned.size()));
+    c.bspec_off.push_back(static_cast<int64_t>(bspec.size()));
   }
+  ck(cudaMalloc(&c.d_bspec, std::max<size_t>(1, bspec.size()) * sizeof(int32_t)), "cudaMalloc bspec");
+  ck(cudaMemcpy(c.d_bspec, bspec.data(), bspec.size() * sizeof(int32_t), cudaMemcpyHostToDevice), "upload bspec");
   ck(cudaMalloc(&c.d_fpart, c.fpart.size() * sizeof(int2)), "cudaMalloc fpart");
   ck(cudaMemcpy(c.d_fpart, c.fpart.data(), c.fpart.size() * sizeof(int2), cudaMemcpyHostToDevice), "upload fpart");
   ck(cudaMalloc(&c.d_owned, std::max<size_t>(1, owned.size()) * sizeof(int32_t)), "cudaMalloc owned");
@@ -822,12 +841,12 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     d.inv_order = c->d_inv_order;
     {
       const char* fs = std::getenv("LDG_FACE_SHARE");
-      if (!(fs && std::string(fs) == "0")) {
-        build_face_sharing(*c, o.chunk_elems(c->E));
-        d.fpart = c->d_fpart;
-        d.owned = c->d_owned;
-        d.owned_off = c->owned_off.data();
-      }
+      build_face_sharing(*c, o.chunk_elems(c->E), !(fs && std::string(fs) == "0"));
+      d.fpart = c->d_fpart;
+      d.owned = c->d_owned;
+      d.owned_off = c->owned_off.data();
+      d.bspec = c->d_bspec;
+      d.bspec_off = c->bspec_off.data();
     }
     d.launches = &c->launches;
     *out = c.release();

@@ -1632,10 +1632,14 @@ struct SeTile {
 #ifndef LDG_EJ_MINB  // k_endjac min CTAs per SM (register cap 65536 / (128 * minb))
 #define LDG_EJ_MINB 1
 #endif
-template <class C, int SEEDS>
+// BND = false: the chunk's owned faces (flist = kp.owned, or every face of
+// the chunk when null) except slip-wall / Neumann boundary ends; BND = true:
+// exactly those ends (flist = their list), with the general boundary kinds.
+template <class C, int SEEDS, bool BND>
 __global__ void __launch_bounds__(128, LDG_EJ_MINB)
 k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-         double* __restrict__ SE, int k_begin, int k_end, long long o_begin, long long o_end) {
+         double* __restrict__ SE, int k_begin, int k_end, long long o_begin, long long o_end,
+         const int32_t* __restrict__ flist) {
   constexpr int NP = C::NP, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD, P = C::P,
                 B11 = C::B11;
   using EJ = EndJac<C>;
@@ -1654,7 +1658,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const int64_t rest = item / NL;
   const int sub = static_cast<int>(rest % IPS);
   const int64_t fi = rest / IPS;
-  const int fc = kp.owned ? __ldg(kp.owned + o_begin + fi) : static_cast<int>(k_begin * 2 * D + fi);
+  const int fc = flist ? __ldg(flist + o_begin + fi) : static_cast<int>(k_begin * 2 * D + fi);
   const int k = fc / (2 * D), ds = fc - k * 2 * D, dir = ds >> 1, side = ds & 1;
   const int gs = ds * NL + line;
   const size_t e = kp.order[k];
@@ -1702,8 +1706,8 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   double uiv[M], uov[M];
   // boundary kind: Dirichlet / characteristic (ghost = g), slip wall (ghost =
   // mirrored u_in), Neumann (constant flux: no u dependence), see bnd_flux
-  const int bkind = bd ? __ldg(kp.bck + (-1 - cn.x)) : -1;
-  const bool bneu = bkind == BC_NEUMANN, bslip = bkind == BC_SLIP_WALL;
+  const int bkind = (BND && bd) ? __ldg(kp.bck + (-1 - cn.x)) : -1;
+  const bool bneu = BND && bkind == BC_NEUMANN, bslip = BND && bkind == BC_SLIP_WALL;
 #pragma unroll
   for (int c = 0; c < M; ++c) {
     uiv[c] = __ldg(U + own * M + c);
@@ -1739,27 +1743,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     double Jx[(LLFC || VCF) ? M * M : 1];
 #pragma unroll
     for (int c = 0; c < ((LLFC || VCF) ? M * M : 1); ++c) Jx[c] = 0.0;
-    if (LLFC && !bneu) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Jx, ok);
-    if (LLFC && bslip) {
-      // chain rule through the ghost: dFh/du_in += dFh/du_out * dghost/du_in,
-      // dghost/du_in = diag(1, I - 2 n n^T / |n|^2, 1)
-      double J1[LLFC ? M * M : 1], n2 = 0.0;
-      llf_jac<D>(uov, uiv, n, kp.pp.gamma, 1, J1, ok);
-#pragma unroll
-      for (int d = 0; d < D; ++d) n2 += n[d] * n[d];
-#pragma unroll
-      for (int c = 0; c < (LLFC ? M : 0); ++c) {
-        Jx[c * M] += J1[c * M];
-        Jx[c * M + M - 1] += J1[c * M + M - 1];
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          double v = J1[c * M + 1 + b];
-#pragma unroll
-          for (int k2 = 0; k2 < D; ++k2) v -= J1[c * M + 1 + k2] * (2.0 * n[k2] * n[b] / n2);
-          Jx[c * M + 1 + b] += v;
-        }
-      }
-    }
+    if (LLFC) llf_jac<D>(uov, uiv, n, kp.pp.gamma, pass, Jx, ok);  // (LLFC: never a BND instantiation)
     if (VCF) {
       const bool sel_in = bd || S <= 0;  // the viscous flux is taken from u_in (else u_out)
       if ((pass == 0) == sel_in && !bneu) {
@@ -1791,7 +1775,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         uo[c].d[0] = (pass == 1 && c == b) ? 1.0 : 0.0;
         fh[c] = D1(0.0);
       }
-      if (bslip) bc_ghost<D, M>(bkind, bcp, ui, n, uo);  // the ghost follows u_in
+      if (bslip) bc_ghost<D, M>(bkind, bcp, ui, n, uo);  // the ghost follows u_in (BND only)
       if (C::HAS_INV && !bneu) {
         if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
         else if (!LLFC) llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);

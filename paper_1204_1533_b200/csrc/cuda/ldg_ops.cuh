@@ -33,6 +33,8 @@ struct DevCtx {
   const int32_t* owned = nullptr;     // owned faces k*2D + ds, chunk by chunk
   const int32_t* inv_order = nullptr; // reference element -> processing index
   const int64_t* owned_off = nullptr; // host: chunk c owns owned[owned_off[c] .. owned_off[c+1])
+  const int32_t* bspec = nullptr;     // slip-wall / Neumann boundary faces, chunk by chunk
+  const int64_t* bspec_off = nullptr; // host offsets into bspec
   int E = 0;
   long long* launches = nullptr;
 };
@@ -269,14 +271,22 @@ struct Launch {
       const long long nf = oe - ob;
       if (one_seed) {
         const long long items = nf * C::NL * EndJac<C>::items(1);
-        k_endjac<C, 1><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE, kb, ke,
-                                                                                  ob, oe);
+        k_endjac<C, 1, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
+            params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
       } else {
         const long long items = nf * C::NL * IPS;
-        k_endjac<C, EJ_SEEDS><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(params(d), U, Q, SE,
-                                                                                         kb, ke, ob, oe);
+        k_endjac<C, EJ_SEEDS, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
+            params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
       }
       count(d);
+      // slip-wall / Neumann boundary ends of the chunk (general kinds)
+      if (d.bspec && d.bspec_off[ci + 1] > d.bspec_off[ci]) {
+        const long long sb = d.bspec_off[ci], se = d.bspec_off[ci + 1];
+        const long long items = (se - sb) * C::NL * EndJac<C>::items(1);
+        k_endjac<C, 1, true><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
+            params(d), U, Q, SE, kb, ke, sb, se, d.bspec);
+        count(d);
+      }
       if (JacP<C>::OK && !simple && !(C::D == 3 && force_s3)) {
         const int n = ke - kb;
         const int grid = n < grid_max ? n : grid_max;
