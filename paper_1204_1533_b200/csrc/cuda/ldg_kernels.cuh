@@ -694,8 +694,11 @@ struct ResP {
   static constexpr int THREADS = SPLIT * LT;
 };
 
+#ifndef LDG_RES_MINB  // k_residual_p min CTAs per SM (register cap)
+#define LDG_RES_MINB 1
+#endif
 template <class C, int EPB>
-__global__ void __launch_bounds__(ResP<C, EPB>::THREADS)
+__global__ void __launch_bounds__(ResP<C, EPB>::THREADS, LDG_RES_MINB)
 k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
              double* __restrict__ R) {
   constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD,
@@ -1630,7 +1633,7 @@ struct SeTile {
 };
 
 #ifndef LDG_EJ_MINB  // k_endjac min CTAs per SM (register cap 65536 / (128 * minb))
-#define LDG_EJ_MINB 1
+#define LDG_EJ_MINB 3  // measured: C2 Jacobian 0.244 -> 0.239 ms, C3 -1.3 %, C4 neutral
 #endif
 // BND = false: the chunk's owned faces (flist = kp.owned, or every face of
 // the chunk when null) except slip-wall / Neumann boundary ends; BND = true:
