@@ -237,6 +237,36 @@ typedef struct ldg_solver_stats {
   double residual_norm;        /* final ||K - R||_inf of the last stage */
 } ldg_solver_stats;
 int ldg_rk4_step(ldg_ctx* ctx, double* U, double t, double dt);
+/* Pseudo-transient continuation to a steady state (PAPER.md:
+   641-652 "a sequence of increasing timesteps dt and a final step without the
+   time derivatives", backward Euler): linearised backward-Euler updates
+   (I - dt A) dU = dt R(U) with dt = dt0, dt0*growth, ... (n_steps of them),
+   then Newton updates with dt = dt_final (default 1e12: the identity term is
+   negligible, i.e. pure Newton on R(U) = 0), each linear solve gmres_iters
+   iterations of (block-Jacobi) GMRES or fewer when ||b - A x|| <= gmres_rtol ||b||;
+   Jacobian reused until recompute_threshold updates have been made with it.
+   Converged when ||R(U)||_inf <= newton_tol (checked first: a steady U0 returns
+   after one residual).  A continuation update that produces a non-physical
+   state or grows the residual 1e4-fold is rejected: U restored, dt halved,
+   Jacobian refreshed (at most 10 times).  A rejected final-phase
+   update, or no convergence after n_steps + max_newton updates -> LDG_ERR_SOLVER.  U: device vector,
+   updated in place.  log_csv (optional, host path): one row per update
+   `step,stage,newton_iters,gmres_iters,jacobian_refreshed,residual_norm`
+   (stage 0 = continuation, 1 = final Newton, 2 = rejected). */
+typedef struct ldg_steady_cfg {
+  double dt0;                  /* first pseudo-time step (> 0) */
+  double growth;               /* dt_{k+1} = growth * dt_k (>= 1; SPEC default ramp: 2) */
+  int32_t n_steps;             /* continuation updates (SPEC default 10) */
+  double dt_final;             /* final-phase step (<= 0: 1e12) */
+  int32_t gmres_iters;         /* GMRES iterations per update (cap) */
+  double gmres_rtol;           /* GMRES early exit (0: run gmres_iters) */
+  int32_t recompute_threshold; /* updates per Jacobian */
+  int32_t max_newton;          /* final-phase update cap */
+  int32_t use_precond;         /* block-Jacobi (1) or none (0) */
+  double newton_tol;           /* ||R(U)||_inf target */
+  const char* log_csv;         /* per-update CSV rows, or NULL */
+} ldg_steady_cfg;
+int ldg_steady_solve(ldg_ctx* ctx, double* U, double t, const ldg_steady_cfg* cfg, ldg_solver_stats* stats);
 int ldg_dirk3_step(ldg_ctx* ctx, double* U, double t, double dt, const ldg_newton_cfg* cfg,
                    ldg_solver_stats* stats);
 

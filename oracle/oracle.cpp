@@ -1298,10 +1298,19 @@ void pc_apply(const Ctx& c, const double* r, double* z) {
     }
   }
 }
+// Deterministic for any thread count: fixed chunk partial sums, summed in order.
 double dotv(const double* a, const double* b, size_t n) {
+  constexpr int NB = 64;
+  double part[NB];
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < NB; ++j) {
+    const size_t lo = n * j / NB, hi = n * (j + 1) / NB;
+    double s = 0.0;
+    for (size_t i = lo; i < hi; ++i) s += a[i] * b[i];
+    part[j] = s;
+  }
   double s = 0.0;
-#pragma omp parallel for reduction(+ : s) schedule(static)
-  for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) s += a[i] * b[i];
+  for (int j = 0; j < NB; ++j) s += part[j];
   return s;
 }
 }  // namespace
@@ -1499,6 +1508,99 @@ int lo_dirk3_step(lo_ctx* x, double* U, double t, double dt, const ldg_newton_cf
     }
     for (size_t q = 0; q < n; ++q) U[q] += dt * (B[0] * K[0][q] + B[1] * K[1][q] + B[2] * K[2][q]);
     if (st) *st = s;
+  });
+}
+
+// Pseudo-transient continuation: the
+// restatement the device driver ldg_steady_solve mirrors operation by
+// operation (see include/linedg_b200.h for the contract).
+int lo_steady_solve(lo_ctx* x, double* U, double t, const ldg_steady_cfg* cfg, ldg_solver_stats* st) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    if (!cfg || !(cfg->dt0 > 0.0) || !(cfg->growth >= 1.0) || cfg->n_steps < 0 || cfg->gmres_iters < 1 ||
+        cfg->recompute_threshold < 1 || cfg->max_newton < 1)
+      throw std::invalid_argument("oracle: steady_solve arguments");
+    const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
+    const double dt_final = cfg->dt_final > 0.0 ? cfg->dt_final : 1e12;
+    const double rtol = cfg->gmres_rtol > 0.0 ? cfg->gmres_rtol : 1e-300;
+    ldg_solver_stats s{};
+    std::vector<double> R(n), b(n), dU(n), Us(n), Rs(n);
+    // residual at U into R; false on a non-physical state (the update is rejected)
+    auto F = [&](double& rn) {
+      const int code = lo_residual(x, U, t, R.data(), nullptr, nullptr, 0);
+      ++s.residual_evals;
+      if (code == LDG_ERR_PHYSICAL_STATE) return false;
+      if (code != LDG_OK) throw std::runtime_error(g_err);
+      rn = inf_norm(R.data(), n);
+      return true;
+    };
+    double rn = 0.0;
+    if (!F(rn)) throw std::runtime_error("oracle: steady_solve: non-physical initial state");
+    if (!std::isfinite(rn)) throw std::runtime_error("oracle: steady_solve non-finite residual");
+    s.residual_norm = rn;
+    const double rn0 = rn;
+    bool done = rn <= cfg->newton_tol;
+    int since = 0, rejects = 0;
+    bool fresh = true;  // (re)assemble before the next update
+    double dt = cfg->dt0, pc_dt = -1.0;
+    // continuation updates left before the final (Newton) phase; a rejected
+    // final-phase update returns to continuation for 5 more updates
+    int cont_left = cfg->n_steps, newton_left = cfg->max_newton;
+    for (int k = 0; !done && (cont_left > 0 || newton_left > 0); ++k) {
+      const bool fin = cont_left == 0;
+      const double h = fin ? dt_final : dt;
+      if (fresh || since >= cfg->recompute_threshold) {
+        if (lo_assemble(x, U, t, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+        ++s.jacobian_assemblies;
+        since = 0;
+        fresh = false;
+        c.pc_built = false;
+      }
+      if (cfg->use_precond && (!c.pc_built || pc_dt != h)) {
+        if (lo_precond_build(x, h) != LDG_OK) throw std::runtime_error(g_err);
+        pc_dt = h;
+      }
+      for (size_t q = 0; q < n; ++q) b[q] = h * R[q];
+      int32_t gi = 0, gc = 0;
+      double gr = 0.0;
+      if (lo_gmres(x, h, b.data(), rtol, cfg->gmres_iters, cfg->gmres_iters, cfg->use_precond, dU.data(), &gi, &gc,
+                   &gr) != LDG_OK)
+        throw std::runtime_error(g_err);
+      s.gmres_iters += gi;
+      std::copy(U, U + n, Us.begin());
+      std::copy(R.begin(), R.end(), Rs.begin());
+      for (size_t q = 0; q < n; ++q) U[q] += dU[q];
+      ++since;
+      ++s.newton_iters;
+      double rn1 = 0.0;
+      const bool phys = F(rn1);
+      if (!phys || !(rn1 <= 1e4 * rn0)) {
+        // rejected update: restore, halve the pseudo-time step, fresh Jacobian
+        // (SPEC.md:535 step-failure policy); the final phase cannot back off
+        if (++rejects > 10) throw std::runtime_error("oracle: steady_solve diverged");
+        std::copy(Us.begin(), Us.end(), U);
+        std::copy(Rs.begin(), Rs.end(), R.begin());
+        if (fin) {
+          cont_left = 5;  // back to continuation at the last pseudo-time step
+          --newton_left;
+        } else {
+          dt *= 0.5;
+        }
+        fresh = true;
+        continue;
+      }
+      rn = rn1;
+      s.residual_norm = rn;
+      done = rn <= cfg->newton_tol;
+      if (fin) {
+        --newton_left;
+      } else {
+        --cont_left;
+        dt *= cfg->growth;
+      }
+    }
+    if (st) *st = s;
+    if (!done) throw std::runtime_error("oracle: steady_solve did not converge");
   });
 }
 

@@ -55,10 +55,11 @@ def lib():
         L.lo_spmv.argtypes = [vp, C.c_int32, _dp, _dp]
         L.lo_split_matvec.argtypes = [vp, C.c_double, _dp, _dp]
         L.lo_fd_dense.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
-        from paper_1204_1533_b200._abi import LdgNewtonCfg, LdgSolverStats
+        from paper_1204_1533_b200._abi import LdgNewtonCfg, LdgSolverStats, LdgSteadyCfg
         L.lo_rk4_step.argtypes = [vp, _dp, C.c_double, C.c_double]
         L.lo_dirk3_step.argtypes = [vp, _dp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                     C.POINTER(LdgSolverStats)]
+        L.lo_steady_solve.argtypes = [vp, _dp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
         L.lo_precond_build.argtypes = [vp, C.c_double]
         L.lo_precond_apply.argtypes = [vp, _dp, _dp]
         L.lo_gmres.argtypes = [vp, C.c_double, _dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, _dp,
@@ -264,6 +265,14 @@ class Oracle:
         U = np.array(U, dtype=np.float64)
         st = LdgSolverStats()
         self._check(self.L.lo_dirk3_step(self.h, _d(U), t, dt, C.byref(cfg), C.byref(st)))
+        return U, st.as_dict()
+
+    def steady_solve(self, U, cfg, t=0.0):
+        """(U_steady, stats dict); cfg = paper_1204_1533_b200._abi.steady_cfg(...)."""
+        from paper_1204_1533_b200._abi import LdgSolverStats
+        U = np.array(U, dtype=np.float64)
+        st = LdgSolverStats()
+        self._check(self.L.lo_steady_solve(self.h, _d(U), t, C.byref(cfg), C.byref(st)))
         return U, st.as_dict()
 
     def fd_dense(self, which, U, Q=None):

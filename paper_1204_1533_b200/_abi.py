@@ -166,6 +166,22 @@ class LdgSolverStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class LdgSteadyCfg(C.Structure):
+    """ldg_steady_cfg (include/linedg_b200.h)."""
+    _fields_ = [("dt0", C.c_double), ("growth", C.c_double), ("n_steps", C.c_int32), ("dt_final", C.c_double),
+                ("gmres_iters", C.c_int32), ("gmres_rtol", C.c_double), ("recompute_threshold", C.c_int32),
+                ("max_newton", C.c_int32), ("use_precond", C.c_int32), ("newton_tol", C.c_double),
+                ("log_csv", C.c_char_p)]
+
+
+def steady_cfg(dt0=1e-2, growth=2.0, n_steps=10, dt_final=0.0, gmres_iters=30, gmres_rtol=1e-3,
+               recompute_threshold=1, max_newton=20, use_precond=True, newton_tol=1e-10, log_csv=None):
+    """Pseudo-transient continuation policy (geometric ramp
+    dt0 * 2^k over 10 steps, then Newton without the time derivative)."""
+    return LdgSteadyCfg(dt0, growth, n_steps, dt_final, gmres_iters, gmres_rtol, recompute_threshold, max_newton,
+                        1 if use_precond else 0, newton_tol, None if log_csv is None else os.fsencode(log_csv))
+
+
 def newton_cfg(gmres_iters=5, recompute_threshold=15, max_newton=50, use_precond=True, newton_tol=1e-8):
     """The paper's Newton/GMRES policy."""
     return LdgNewtonCfg(gmres_iters, recompute_threshold, max_newton, 1 if use_precond else 0, newton_tol)
@@ -179,7 +195,7 @@ GPU_SYMBOLS = [
     "ldg_residual_host", "ldg_jacobian_assemble_host", "ldg_bsr_spmv_host", "ldg_split_matvec_host",
     "ldg_kernel_launches", "ldg_jacobian_bytes",
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
-    "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv",
+    "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv", "ldg_steady_solve",
 ]
 
 
@@ -225,6 +241,7 @@ def gpu_lib() -> C.CDLL:
         L.ldg_rk4_step.argtypes = [vp, vp, C.c_double, C.c_double]
         L.ldg_dirk3_step.argtypes = [vp, vp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                      C.POINTER(LdgSolverStats)]
+        L.ldg_steady_solve.argtypes = [vp, vp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
         L.ldg_write_triplets.argtypes = [vp, C.c_int, C.c_char_p]
         L.ldg_write_sparsity_csv.argtypes = [vp, C.c_int, C.c_char_p, C.c_int]
         L.ldg_kernel_launches.argtypes = [vp]

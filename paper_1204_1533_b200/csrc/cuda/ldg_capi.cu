@@ -1426,7 +1426,6 @@ int ldg_dirk3_step(ldg_ctx* c, double* U, double t, double dt, const ldg_newton_
     double* w = ensure(c->d_ti, 8 * n);
     double* K[3] = {w, w + n, w + 2 * n};
     double *Kc = w + 3 * n, *us = w + 4 * n, *Fv = w + 5 * n, *G = w + 6 * n, *dK = w + 7 * n;
-    double* red = ensure(c->d_kred, KR_BLOCKS + 8);
     cudaStream_t st = c->stream;
     const int vb = 592, vt = 256;
     ldg_solver_stats s{};
@@ -1460,6 +1459,8 @@ int ldg_dirk3_step(ldg_ctx* c, double* U, double t, double dt, const ldg_newton_
         ++c->launches;
         F(us, Fv);
         k_rhs<<<vb, vt, 0, st>>>(G, Kc, Fv, n);
+        // (re-fetched each time: ldg_gmres reallocates d_kred when its restart grows)
+        double* red = ensure(c->d_kred, KR_BLOCKS + 8);
         k_amax_part<<<KR_BLOCKS, KR_THREADS, 0, st>>>(G, n, red);
         k_amax_fin<<<1, KR_THREADS, 0, st>>>(red, KR_BLOCKS, red + KR_BLOCKS);
         c->launches += 3;
@@ -1494,6 +1495,132 @@ int ldg_dirk3_step(ldg_ctx* c, double* U, double t, double dt, const ldg_newton_
     k_dirk_update<<<vb, vt, 0, st>>>(U, K[0], K[1], K[2], n, dt, B[0], B[1], B[2]);
     ++c->launches;
     c->sync_errors = was;
+    if (stats) *stats = s;
+    return finish(c, cudaGetLastError());
+  });
+}
+
+// Pseudo-transient continuation to a steady state (PAPER.md:
+// 641-652); mirrors the oracle's lo_steady_solve operation by operation.
+int ldg_steady_solve(ldg_ctx* c, double* U, double t, const ldg_steady_cfg* cfg, ldg_solver_stats* stats) {
+  return guarded(c, [&]() -> int {
+    if (!U || !cfg || !(cfg->dt0 > 0.0) || !(cfg->growth >= 1.0) || cfg->n_steps < 0 || cfg->gmres_iters < 1 ||
+        cfg->recompute_threshold < 1 || cfg->max_newton < 1)
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "steady_solve: U and a valid ldg_steady_cfg required");
+    const size_t n = c->nU();
+    const double dt_final = cfg->dt_final > 0.0 ? cfg->dt_final : 1e12;
+    const double rtol = cfg->gmres_rtol > 0.0 ? cfg->gmres_rtol : 1e-300;
+    double* w = ensure(c->d_ti, 8 * n);  // (the DIRK3 workspace: 8 vectors)
+    double *R = w, *b = w + n, *dU = w + 2 * n, *Us = w + 3 * n, *Rs = w + 4 * n;
+    cudaStream_t st = c->stream;
+    const int vb = 592, vt = 256;
+    ldg_solver_stats s{};
+    const bool was = c->sync_errors;
+    c->sync_errors = true;
+    FILE* log = nullptr;
+    if (cfg->log_csv) {
+      log = std::fopen(cfg->log_csv, "w");
+      if (!log) {
+        c->sync_errors = was;
+        throw ldg_error(LDG_ERR_CONFIG, std::string("cannot write '") + cfg->log_csv + "'");
+      }
+      std::fprintf(log, "step,stage,newton_iters,gmres_iters,jacobian_refreshed,residual_norm\n");
+    }
+    auto fail = [&](int code, const std::string& msg) {
+      c->sync_errors = was;
+      if (log) std::fclose(log);
+      if (stats) *stats = s;
+      throw ldg_error(code, msg);
+    };
+    auto chk = [&](int code) {
+      if (code != LDG_OK) fail(code, c->err);
+    };
+    // residual at U into R (and its inf-norm); false on a non-physical state
+    auto F = [&](double& rn) {
+      const int code = ldg_residual(c, U, t, R, nullptr);
+      ++s.residual_evals;
+      if (code == LDG_ERR_PHYSICAL_STATE) return false;
+      chk(code);
+      // (re-fetched each time: ldg_gmres reallocates d_kred when its restart grows)
+      double* red = ensure(c->d_kred, KR_BLOCKS + 8);
+      k_amax_part<<<KR_BLOCKS, KR_THREADS, 0, st>>>(R, n, red);
+      k_amax_fin<<<1, KR_THREADS, 0, st>>>(red, KR_BLOCKS, red + KR_BLOCKS);
+      c->launches += 2;
+      ck(cudaMemcpyAsync(&rn, red + KR_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "stream synchronize");
+      return true;
+    };
+    double rn = 0.0;
+    if (!F(rn)) fail(LDG_ERR_PHYSICAL_STATE, c->err);
+    if (!std::isfinite(rn)) fail(LDG_ERR_SOLVER, "steady_solve: non-finite residual");
+    s.residual_norm = rn;
+    const double rn0 = rn;
+    bool done = rn <= cfg->newton_tol;
+    int since = 0, rejects = 0;
+    bool fresh = true;
+    double dt = cfg->dt0;
+    // continuation updates left before the final (Newton) phase; a rejected
+    // final-phase update returns to continuation for 5 more updates
+    int cont_left = cfg->n_steps, newton_left = cfg->max_newton;
+    for (int k = 0; !done && (cont_left > 0 || newton_left > 0); ++k) {
+      const bool fin = cont_left == 0;
+      const double h = fin ? dt_final : dt;
+      bool refreshed = false;
+      if (fresh || since >= cfg->recompute_threshold) {
+        chk(ldg_jacobian_assemble(c, U, t));
+        ++s.jacobian_assemblies;
+        since = 0;
+        fresh = false;
+        c->pc_valid = false;
+        refreshed = true;
+      }
+      if (cfg->use_precond && (!c->pc_valid || c->pc_adt != h)) chk(ldg_precond_build(c, h));
+      ck(cudaMemsetAsync(b, 0, n * sizeof(double), st), "memset");
+      k_axpy<<<vb, vt, 0, st>>>(b, R, n, h);  // b = h R
+      ++c->launches;
+      int32_t gi = 0, gc = 0;
+      double gr = 0.0;
+      chk(ldg_gmres(c, h, b, dU, rtol, cfg->gmres_iters, cfg->gmres_iters, cfg->use_precond, &gi, &gc, &gr));
+      s.gmres_iters += gi;
+      ck(cudaMemcpyAsync(Us, U, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "save U");
+      ck(cudaMemcpyAsync(Rs, R, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "save R");
+      k_axpy<<<vb, vt, 0, st>>>(U, dU, n, 1.0);
+      ++c->launches;
+      ++since;
+      ++s.newton_iters;
+      double rn1 = 0.0;
+      const bool phys = F(rn1);
+      if (!phys || !(rn1 <= 1e4 * rn0)) {
+        // rejected update: restore, halve the pseudo-time step, fresh Jacobian
+        // (SPEC.md:535 step-failure policy); the final phase cannot back off
+        if (log) std::fprintf(log, "%d,2,%d,%d,%d,%.17g\n", k, s.newton_iters, gi, refreshed ? 1 : 0, phys ? rn1 : -1.0);
+        if (++rejects > 10) fail(LDG_ERR_SOLVER, "steady_solve: diverged");
+        ck(cudaMemcpyAsync(U, Us, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "restore U");
+        ck(cudaMemcpyAsync(R, Rs, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "restore R");
+        if (fin) {
+          cont_left = 5;  // back to continuation at the last pseudo-time step
+          --newton_left;
+        } else {
+          dt *= 0.5;
+        }
+        fresh = true;
+        continue;
+      }
+      rn = rn1;
+      s.residual_norm = rn;
+      if (log)
+        std::fprintf(log, "%d,%d,%d,%d,%d,%.17g\n", k, fin ? 1 : 0, s.newton_iters, gi, refreshed ? 1 : 0, rn);
+      done = rn <= cfg->newton_tol;
+      if (fin) {
+        --newton_left;
+      } else {
+        --cont_left;
+        dt *= cfg->growth;
+      }
+    }
+    if (!done) fail(LDG_ERR_SOLVER, "steady_solve: no convergence within n_steps + max_newton updates");
+    c->sync_errors = was;
+    if (log) std::fclose(log);
     if (stats) *stats = s;
     return finish(c, cudaGetLastError());
   });

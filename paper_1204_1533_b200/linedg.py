@@ -313,6 +313,15 @@ class LineDG:
         self._check(self.lib.ldg_dirk3_step(self._h, self._ptr(Ud), t, dt, C.byref(cfg), C.byref(st)))
         return (Ud.cpu().numpy() if host else Ud), st.as_dict()
 
+    def steady_solve(self, U, cfg=None, t: float = 0.0):
+        """Pseudo-transient continuation to R(U) = 0:
+        (U_steady, stats dict).  cfg: _abi.steady_cfg(...)."""
+        cfg = cfg if cfg is not None else _abi.steady_cfg()
+        Ud, host = self._state_on_device(U)
+        st = _abi.LdgSolverStats()
+        self._check(self.lib.ldg_steady_solve(self._h, self._ptr(Ud), t, C.byref(cfg), C.byref(st)))
+        return (Ud.cpu().numpy() if host else Ud), st.as_dict()
+
     def split_matvec(self, alpha_dt: float, v, out=None):
         """(I - alpha_dt (K11 + K12 K21)) v without forming the product."""
         if not _is_torch(v):
