@@ -301,7 +301,13 @@ int ldg_write_sparsity_csv(ldg_ctx* ctx, int which, const char* path, int append
 int ldg_set_sync_errors(ldg_ctx* ctx, int on);
 int ldg_synchronize(ldg_ctx* ctx);
 
-/* Host-buffer variants (end-to-end path: H2D, kernels, D2H, synchronise). */
+/* Host-buffer variants (end-to-end path: H2D, kernels, D2H).  With error
+ * synchronisation on (default) each call synchronises before returning.  With
+ * ldg_set_sync_errors(ctx, 0), ldg_residual_host / ldg_jacobian_assemble_host /
+ * ldg_bsr_spmv_host are asynchronous: uploads run on a copy stream, downloads
+ * on another, ordered against the kernels by events (transfers of consecutive
+ * calls overlap the kernels in both PCIe directions); the host buffers must
+ * stay valid (pinned for overlap) and results are ready after ldg_synchronize. */
 int ldg_residual_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
 int ldg_jacobian_assemble_host(ldg_ctx* ctx, const double* U, double t);
 int ldg_bsr_spmv_host(ldg_ctx* ctx, int which, const double* x, double* y);

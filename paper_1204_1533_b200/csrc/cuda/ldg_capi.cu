@@ -105,7 +105,13 @@ struct ldg_ctx {
   size_t n11 = 0, n12 = 0, n21 = 0;
   bool jac_valid = false, k21_valid = false;
   double* d_hu = nullptr;  // staging for host variants
+  double* d_hu2 = nullptr;  // (assembly input: a separate buffer so its upload overlaps the residual)
   double* d_hr = nullptr;
+  // asynchronous host variants (sync_errors off): uploads on cs_in, downloads
+  // on cs_out, kernels on `stream`; events order buffer reuse
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_k = nullptr, ev_free_hu = nullptr, ev_free_hu2 = nullptr, ev_free_hx = nullptr,
+              ev_out_r = nullptr, ev_out_y = nullptr, ev_join = nullptr;
   double* d_hx = nullptr;
   double* d_hy = nullptr;
   cudaStream_t stream = nullptr;
@@ -143,7 +149,12 @@ struct ldg_ctx {
     cudaFree(d_K21);
     cudaFree(d_SE);
     cudaFree(d_hu);
+    cudaFree(d_hu2);
     cudaFree(d_hr);
+    for (cudaEvent_t ev : {ev_in, ev_k, ev_free_hu, ev_free_hu2, ev_free_hx, ev_out_r, ev_out_y, ev_join})
+      if (ev) cudaEventDestroy(ev);
+    if (cs_in) cudaStreamDestroy(cs_in);
+    if (cs_out) cudaStreamDestroy(cs_out);
     cudaFree(d_hx);
     cudaFree(d_hy);
     if (h_err) cudaFreeHost(h_err);
@@ -821,6 +832,13 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
 
     ldg::DevCtx& d = c->dc;
     d.stream = c->stream;
+    ck(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking), "create upload stream");
+    ck(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking), "create download stream");
+    for (cudaEvent_t* ev : {&c->ev_in, &c->ev_k, &c->ev_free_hu, &c->ev_free_hu2, &c->ev_free_hx, &c->ev_out_r,
+                            &c->ev_out_y, &c->ev_join}) {
+      ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "create event");
+      ck(cudaEventRecord(*ev, c->stream), "record event");  // completed: nothing to wait for yet
+    }
     d.phi = c->phi.data();
     d.dq = c->dq.data();
     d.mi = c->mi.data();
@@ -875,6 +893,11 @@ int ldg_set_sync_errors(ldg_ctx* c, int on) {
 }
 int ldg_synchronize(ldg_ctx* c) {
   return guarded(c, [&]() -> int {
+    // join the asynchronous host variants' copy streams into the context stream
+    ck(cudaEventRecord(c->ev_join, c->cs_in), "record join");
+    ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join uploads");
+    ck(cudaEventRecord(c->ev_join, c->cs_out), "record join");
+    ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join downloads");
     const bool was = c->sync_errors;
     c->sync_errors = true;
     const int st = finish(c, cudaSuccess);
@@ -1343,8 +1366,8 @@ int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rt
 int ldg_gmres_host(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rtol, int32_t maxit,
                    int32_t restart, int32_t use_precond, int32_t* iters, int32_t* converged, double* resnorm) {
   return guarded(c, [&]() -> int {
-    ensure(c->d_hx, c->nU());
-    ensure(c->d_hy, c->nU());
+    ensure(c->d_hx, c->nQ());  // (shared with ldg_bsr_spmv_host: sized for K12 / K21 vectors)
+    ensure(c->d_hy, c->nQ());
     ck(cudaMemcpyAsync(c->d_hx, b, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D b");
     const int st = ldg_gmres(c, alpha_dt, c->d_hx, c->d_hy, rtol, maxit, restart, use_precond, iters, converged,
                              resnorm);
@@ -1357,8 +1380,8 @@ int ldg_gmres_host(ldg_ctx* c, double alpha_dt, const double* b, double* x, doub
 
 int ldg_precond_apply_host(ldg_ctx* c, const double* r, double* z) {
   return guarded(c, [&]() -> int {
-    ensure(c->d_hx, c->nU());
-    ensure(c->d_hy, c->nU());
+    ensure(c->d_hx, c->nQ());
+    ensure(c->d_hy, c->nQ());
     ck(cudaMemcpyAsync(c->d_hx, r, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D r");
     const int st = ldg_precond_apply(c, c->d_hx, c->d_hy);
     if (st != LDG_OK) return st;
@@ -1627,12 +1650,52 @@ int ldg_steady_solve(ldg_ctx* c, double* U, double t, const ldg_steady_cfg* cfg,
 }
 
 // ------------------------------------------------------------ host variants
+// Host-buffer variants.  With error synchronisation on (the default) each
+// call uploads on the context stream, runs, downloads and synchronises.  With
+// it off (ldg_set_sync_errors(ctx, 0)) the calls are asynchronous like the
+// device entry points: uploads run on a copy stream (cs_in) and downloads on
+// another (cs_out), ordered against the kernels by events, so the transfers
+// of consecutive calls overlap each other and the kernels in both PCIe
+// directions; host buffers must stay valid (pinned for true overlap) and
+// results are ready after ldg_synchronize().
+namespace {
+// upload n doubles to dbuf once `free_ev` (the last reader of dbuf) completed;
+// the context stream then waits for the upload
+void upload_async(ldg_ctx* c, double* dbuf, const double* h, size_t n, cudaEvent_t free_ev) {
+  ck(cudaStreamWaitEvent(c->cs_in, free_ev, 0), "wait buffer");
+  ck(cudaMemcpyAsync(dbuf, h, n * sizeof(double), cudaMemcpyHostToDevice, c->cs_in), "H2D");
+  ck(cudaEventRecord(c->ev_in, c->cs_in), "record upload");
+  ck(cudaStreamWaitEvent(c->stream, c->ev_in, 0), "wait upload");
+}
+// download n doubles from dbuf after the context stream's work so far
+void download_async(ldg_ctx* c, double* h, const double* dbuf, size_t n, cudaEvent_t done_ev) {
+  ck(cudaEventRecord(c->ev_k, c->stream), "record kernels");
+  ck(cudaStreamWaitEvent(c->cs_out, c->ev_k, 0), "wait kernels");
+  ck(cudaMemcpyAsync(h, dbuf, n * sizeof(double), cudaMemcpyDeviceToHost, c->cs_out), "D2H");
+  ck(cudaEventRecord(done_ev, c->cs_out), "record download");
+}
+}  // namespace
+
 int ldg_residual_host(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
   return guarded(c, [&]() -> int {
     ensure(c->d_hu, c->nU());
     ensure(c->d_hr, c->nU());
-    ck(cudaMemcpyAsync(c->d_hu, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
     double* dq = c->second ? ensure(c->d_Q, c->nQ()) : nullptr;
+    if (!c->sync_errors) {
+      upload_async(c, c->d_hu, U, c->nU(), c->ev_free_hu);
+      ck(cudaStreamWaitEvent(c->stream, c->ev_out_r, 0), "wait R/Q download");  // d_hr, d_Q reuse
+      int st = ldg_residual(c, c->d_hu, t, c->d_hr, dq);
+      if (st != LDG_OK) return st;
+      ck(cudaEventRecord(c->ev_free_hu, c->stream), "record");
+      ck(cudaEventRecord(c->ev_k, c->stream), "record kernels");
+      ck(cudaStreamWaitEvent(c->cs_out, c->ev_k, 0), "wait kernels");
+      ck(cudaMemcpyAsync(R, c->d_hr, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->cs_out), "D2H R");
+      if (Q && dq)
+        ck(cudaMemcpyAsync(Q, dq, c->nQ() * sizeof(double), cudaMemcpyDeviceToHost, c->cs_out), "D2H Q");
+      ck(cudaEventRecord(c->ev_out_r, c->cs_out), "record download");
+      return LDG_OK;
+    }
+    ck(cudaMemcpyAsync(c->d_hu, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
     const bool was = c->sync_errors;
     c->sync_errors = false;
     int st = ldg_residual(c, c->d_hu, t, c->d_hr, dq);
@@ -1651,11 +1714,19 @@ int ldg_residual_host(ldg_ctx* c, const double* U, double t, double* R, double* 
 
 int ldg_jacobian_assemble_host(ldg_ctx* c, const double* U, double t) {
   return guarded(c, [&]() -> int {
-    ensure(c->d_hu, c->nU());
-    ck(cudaMemcpyAsync(c->d_hu, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
+    ensure(c->d_hu2, c->nU());
+    if (!c->sync_errors) {
+      upload_async(c, c->d_hu2, U, c->nU(), c->ev_free_hu2);
+      if (c->second) ck(cudaStreamWaitEvent(c->stream, c->ev_out_r, 0), "wait Q download");  // d_Q reuse
+      const int st = ldg_jacobian_assemble(c, c->d_hu2, t);
+      if (st != LDG_OK) return st;
+      ck(cudaEventRecord(c->ev_free_hu2, c->stream), "record");
+      return LDG_OK;
+    }
+    ck(cudaMemcpyAsync(c->d_hu2, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
     const bool was = c->sync_errors;
     c->sync_errors = true;
-    const int st = ldg_jacobian_assemble(c, c->d_hu, t);
+    const int st = ldg_jacobian_assemble(c, c->d_hu2, t);
     c->sync_errors = was;
     return st;
   });
@@ -1667,6 +1738,15 @@ int ldg_bsr_spmv_host(ldg_ctx* c, int which, const double* x, double* y) {
     const size_t ny = which == LDG_K21 ? c->nQ() : c->nU();
     double* dx = ensure(c->d_hx, c->nQ());
     double* dy = ensure(c->d_hy, c->nQ());
+    if (!c->sync_errors) {
+      upload_async(c, dx, x, nx, c->ev_free_hx);
+      ck(cudaStreamWaitEvent(c->stream, c->ev_out_y, 0), "wait y download");
+      const int st = ldg_bsr_spmv(c, which, dx, dy);
+      if (st != LDG_OK) return st;
+      ck(cudaEventRecord(c->ev_free_hx, c->stream), "record");
+      download_async(c, y, dy, ny, c->ev_out_y);
+      return LDG_OK;
+    }
     ck(cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D x");
     const bool was = c->sync_errors;
     c->sync_errors = false;

@@ -213,3 +213,31 @@ def test_large_mesh_assembly_rows_match_oracle(ci):
             first = v1
     gpu.assemble_jacobians(dev(U))
     assert np.array_equal(gpu.export_blocks(LDG_K11, elems=elems)[2], first)
+
+
+def test_async_host_path_matches_sync():
+    """ldg_set_sync_errors(ctx, 0): host-buffer calls run on the copy streams
+    and return early; after synchronize() the results equal the synchronous
+    ones bitwise (C2 scaled and C3 scaled: second-order Q download too)."""
+    for ci in (1, 2):
+        cfg = CONFIGS[ci]
+        case, U = cfg.build(n=8)
+        gpu = LineDG(case, cfg.physics)
+        x = case.normal_vector(gpu.m, cfg.vector_seed)
+        R0 = gpu.residual(U)
+        gpu.assemble_jacobians(U)
+        y0 = gpu.spmv(LDG_K11, x)
+        Rp = torch.empty(R0.size, dtype=torch.float64).pin_memory().numpy()
+        yp = torch.empty(y0.size, dtype=torch.float64).pin_memory().numpy()
+        Up = torch.from_numpy(U).pin_memory().numpy()
+        xp = torch.from_numpy(x).pin_memory().numpy()
+        gpu.set_sync_errors(False)
+        for _ in range(3):  # repeated calls reuse the staging buffers (event-ordered)
+            Rp[:] = 0.0
+            yp[:] = 0.0
+            gpu.residual(Up, out=Rp)
+            gpu.assemble_jacobians(Up)
+            gpu.spmv(LDG_K11, xp, out=yp)
+            gpu.synchronize()
+            assert np.array_equal(Rp, R0) and np.array_equal(yp, y0)
+        gpu.set_sync_errors(True)
