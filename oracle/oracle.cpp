@@ -942,6 +942,7 @@ int lo_create(const ldg_setup* s, const ldg_physics* ph, lo_ctx** out) {
     c.npe = c.D == 2 ? c.np * c.np : c.np * c.np * c.np;
     c.NL = c.D == 2 ? c.np : c.np * c.np;
     c.E = s->n_elems;
+    if (c.E < 1) throw std::runtime_error("oracle: mesh has no elements");
     if (c.np > MAXNP || c.nq > MAXNQ) throw std::invalid_argument("oracle: p too large");
     c.kind = ph->kind;
     c.riemann = ph->riemann;

@@ -752,6 +752,7 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     c->nq = s->n_quad;
     c->E = s->n_elems;
     if (c->D != 2 && c->D != 3) throw ldg_error(LDG_ERR_CONFIG, "dim must be 2 or 3");
+    if (c->E < 1) throw ldg_error(LDG_ERR_CONFIG, "mesh has no elements");
     if (c->nq != (3 * c->p + 2) / 2) throw ldg_error(LDG_ERR_CONFIG, "n_quad must be (3p+2)/2");
     if (ph->c22 != 0.0)
       throw ldg_error(LDG_ERR_CONFIG, "residual_primal requires C22 = 0 (SPEC.md:250-252)");
