@@ -2533,9 +2533,23 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     if (JP::STAGE) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done; tile staged
     if (JP::STAGE && tid == 0 && !(kp.dbg & 4)) {
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(K11g),
-                   "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8))
-                   : "memory");
+#ifndef LDG_JAC_STORE_HINT  // L2 policy of the tile store: 0 none, 1 evict_first, 2 evict_last
+#define LDG_JAC_STORE_HINT 2  // measured (C2): evict_last 0.3944 vs 0.3979 ms per step (SpMV reads more of K11 from L2)
+#endif
+      if (LDG_JAC_STORE_HINT == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(K11g),
+                     "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8))
+                     : "memory");
+      } else {
+        uint64_t pol;
+        if (LDG_JAC_STORE_HINT == 1)
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+        else
+          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(K11g),
+                     "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8)), "l"(pol)
+                     : "memory");
+      }
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
     if (tid == 0 && k + NB * G < k_end) issue(k + NB * G, cur);
