@@ -2942,6 +2942,21 @@ __device__ __forceinline__ int64_t slot_col(const KParams<C>& kp, int k, size_t 
 // rows of one a.  Block row a of a slot is m contiguous doubles (16-byte
 // loads when m is even); the x entries of a column are shared by the m
 // threads of a row through L1.
+// Jacobian value stream of the SpMV (read once): 0 ld.global.nc, 1 streaming
+// (ld.global.cs), 2 ld.global.nc.L1::no_allocate
+#ifndef LDG_SPMV_STREAM
+#define LDG_SPMV_STREAM 1  // measured: C2 SpMV 120.3 -> 115.4 us (ld.global.cs), C4 neutral
+#endif
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  if (LDG_SPMV_STREAM == 1) return __ldcs(reinterpret_cast<const double2*>(p));
+  if (LDG_SPMV_STREAM == 2) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+  }
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double ld_stream1(const double* p) { return LDG_SPMV_STREAM == 1 ? __ldcs(p) : __ldg(p); }
 template <class C, bool SPLIT>
 __global__ void __launch_bounds__(128)
 k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __restrict__ V12,
@@ -2976,14 +2991,16 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
     if (M % 2 == 0) {
 #pragma unroll
       for (int b = 0; b < M; b += 2) {
-        const double2 kv = __ldg(reinterpret_cast<const double2*>(vp + b));
+        // (streaming loads where the store is small enough that its tail is
+        // still in L2 -- the same condition as rev; measured C2 -5 us, C3 +6 us)
+        const double2 kv = rev ? ld_stream2(vp + b) : __ldg(reinterpret_cast<const double2*>(vp + b));
         const double2 xv = __ldg(reinterpret_cast<const double2*>(xp + b));
         acc += kv.x * xv.x;
         acc += kv.y * xv.y;
       }
     } else {
 #pragma unroll
-      for (int b = 0; b < M; ++b) acc += __ldg(vp + b) * __ldg(xp + b);
+      for (int b = 0; b < M; ++b) acc += ld_stream1(vp + b) * __ldg(xp + b);
     }
   }
   if (SPLIT && C::SECOND) {
@@ -2996,7 +3013,7 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
         if (col < 0) continue;
         const double* vp = vq + static_cast<size_t>(slot) * NT * C::B12;
 #pragma unroll
-        for (int b = 0; b < MD; ++b) acc += __ldg(vp + b) * __ldg(w + col * MD + b);
+        for (int b = 0; b < MD; ++b) acc += ld_stream1(vp + b) * __ldg(w + col * MD + b);
       }
     }
   }
@@ -3034,7 +3051,7 @@ k_spmv12(const KParams<C> kp, const double* __restrict__ V12, const double* __re
       if (col < 0) continue;
       const double* vp = vq + static_cast<size_t>(slot) * NT * C::B12;
 #pragma unroll
-      for (int b = 0; b < MD; ++b) acc += __ldg(vp + b) * __ldg(w + col * MD + b);
+      for (int b = 0; b < MD; ++b) acc += ld_stream1(vp + b) * __ldg(w + col * MD + b);
     }
   }
   (void)R12;
@@ -3068,7 +3085,7 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
     if (col < 0) continue;
     double kv[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + static_cast<size_t>(slot) * NT * D + d);
+    for (int d = 0; d < D; ++d) kv[d] = ld_stream1(vb + static_cast<size_t>(slot) * NT * D + d);
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       const double xv = __ldg(v + col * M + c);
