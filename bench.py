@@ -52,6 +52,27 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def fp64_peak():
+    """Measured FP64 FMA peak (tools/fp64_peak.cu on this pool's B200, written to
+    profiles/fp64_peak.json), else the B200 datasheet figure."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["fp64_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return 40.0, "nominal (B200 datasheet 40 TFLOP/s FP64)"
+
+
+def flops(index, case):
+    """Algorithmic FP64 flops per launch (profiles/flops.json, tools/flop_model.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "flops.json")) as f:
+            fm = json.load(f)[f"config{index}"]
+    except Exception:
+        return None
+    return {k: fm[k] * case.E for k in ("residual", "jacobian", "spmv")}
+
+
 def sizes(cfg, case, m):
     """Algorithmic bytes per launch (adapted to this store:
     no column-index stream)."""
@@ -368,6 +389,14 @@ def main():
         gbs = b / (tms * 1e-3) / 1e9
         breakdown[name] = {"ms": tms, "GB/s": gbs, "frac_hbm": gbs / hbm, "alg_bytes": b}
     breakdown["residual"]["GDOF/s"] = dofs / (t_res * 1e-3) / 1e9
+    # FP64 side of the roofline (fraction = max(bytes/BW, flops/P_fp64))
+    p64, p64_src = fp64_peak()
+    fl = flops(args.config, case)
+    if fl is not None:
+        for name, tms in kern.items():
+            tf = fl[name] / (tms * 1e-3) / 1e12
+            breakdown[name].update({"alg_flops": fl[name], "TFLOP/s": tf, "frac_fp64": tf / p64,
+                                    "frac_roofline": max(breakdown[name]["frac_hbm"], tf / p64)})
     bdom = by[dom] if dom != "residual" else by["residual"] + by.get("gradient", 0)
     achieved = bdom / (kern[dom] * 1e-3) / 1e9
     traffic = None
@@ -384,7 +413,11 @@ def main():
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json config shapes)", "config": workload,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src},
+                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                         "fp64": None if fl is None else {
+                             "flops": fl[dom], "achieved_tflops": fl[dom] / (kern[dom] * 1e-3) / 1e12,
+                             "peak_tflops": p64, "frac": fl[dom] / (kern[dom] * 1e-3) / 1e12 / p64,
+                             "peak_source": p64_src}},
             "breakdown": breakdown,
             "e2e": {"value": world * dofs / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 3 * 8 * dofs, "d2h_bytes_per_step": 2 * 8 * dofs},

@@ -871,6 +871,51 @@ void gradient(const Ctx& c, const double* U, double* Q, const std::vector<int>* 
   for_elems(c, subset, [&](int e) { elem_gradient(c, e, U, Q); });
 }
 
+// ------------------------------------------------------------ flop counting
+// Algorithmic FP64 operation counts: the oracle's own
+// templated flux functions run on a counting scalar; +, -, *, /, sqrt count 1
+// each (negation, |.|, max and comparisons 0).  Forward-mode Jacobians are
+// costed from the primal counts: with N seeds an add costs 1+N, a multiply
+// 1+3N, a divide 2+2N, a sqrt 2+N.
+struct FlCount {
+  double add = 0, mul = 0, div = 0, sqrt = 0;
+  double total() const { return add + mul + div + sqrt; }
+  double dual(int N) const { return add * (1 + N) + mul * (1 + 3 * N) + div * (2 + 2 * N) + sqrt * (2 + N); }
+};
+inline thread_local FlCount g_fl;
+struct Fl {
+  double v = 0.0;
+  Fl() = default;
+  Fl(double x) : v(x) {}  // NOLINT: constants promote implicitly
+};
+inline Fl operator+(Fl a, Fl b) { g_fl.add += 1; return Fl(a.v + b.v); }
+inline Fl operator-(Fl a, Fl b) { g_fl.add += 1; return Fl(a.v - b.v); }
+inline Fl operator*(Fl a, Fl b) { g_fl.mul += 1; return Fl(a.v * b.v); }
+inline Fl operator/(Fl a, Fl b) { g_fl.div += 1; return Fl(a.v / b.v); }
+inline Fl operator+(Fl a, double b) { return a + Fl(b); }
+inline Fl operator+(double a, Fl b) { return Fl(a) + b; }
+inline Fl operator-(Fl a, double b) { return a - Fl(b); }
+inline Fl operator-(double a, Fl b) { return Fl(a) - b; }
+inline Fl operator*(Fl a, double b) { return a * Fl(b); }
+inline Fl operator*(double a, Fl b) { return Fl(a) * b; }
+inline Fl operator/(Fl a, double b) { return a / Fl(b); }
+inline Fl operator/(double a, Fl b) { return Fl(a) / b; }
+inline Fl operator-(Fl a) { return Fl(-a.v); }
+inline bool operator<(Fl a, Fl b) { return a.v < b.v; }
+inline bool operator<(Fl a, double b) { return a.v < b; }
+inline bool operator<=(Fl a, double b) { return a.v <= b; }
+inline Fl sqrt(Fl a) { g_fl.sqrt += 1; return Fl(std::sqrt(a.v)); }
+inline Fl abs(Fl a) { return Fl(a.v >= 0.0 ? a.v : -a.v); }
+inline Fl max(Fl a, Fl b) { return a.v >= b.v ? a : b; }
+inline double value_of(Fl x) { return x.v; }
+
+template <class F>
+FlCount count_ops(F&& f) {
+  g_fl = FlCount{};
+  f();
+  return g_fl;
+}
+
 }  // namespace ora
 
 // ===================================================================== C-ABI
@@ -1602,6 +1647,81 @@ int lo_steady_solve(lo_ctx* x, double* U, double t, const ldg_steady_cfg* cfg, l
     }
     if (st) *st = s;
     if (!done) throw std::runtime_error("oracle: steady_solve did not converge");
+  });
+}
+
+// Algorithmic FP64 flops per ELEMENT of the hot-path kernels,
+// from the oracle's templated flux functions on a counting scalar plus the
+// line algebra of the algorithm (interpolation, projection, lifting,
+// block expansion, 1/J scaling):
+//   out[0] residual (first order) or gradient + residual (second order)
+//   out[1] Jacobian assembly (K11, + K12 for second order; K21 is U-independent)
+//   out[2] K11 SpMV (2 flops per stored value)
+//   out[3..6] per evaluation: inviscid normal flux, Riemann flux, viscous
+//             normal flux, and (dual-cost) Riemann Jacobian with m seeds
+// The Riemann flux is counted once per line end (residual) and its Jacobian
+// once per face side pair (face-shared, as the assembly computes it).
+int lo_flop_model(const lo_ctx* x, double* out) {
+  return guarded([&] {
+    const Ctx& c = x->c;
+    const int D = c.D, m = c.m, NP = c.np, NQ = c.nq, NL = c.NL, NPE = c.npe, MD = m * D;
+    // a physical sample state (free stream + gradient) for the counting runs
+    Fl u[MAXM], uo[MAXM], q[MAXM * MAXD], f[MAXM];
+    if (c.kind == LDG_POISSON) {
+      u[0] = 0.3;
+      uo[0] = 0.2;
+    } else {
+      u[0] = 1.0;
+      uo[0] = 1.05;
+      for (int d = 0; d < D; ++d) {
+        u[1 + d] = 0.3 - 0.1 * d;
+        uo[1 + d] = 0.25 + 0.05 * d;
+      }
+      u[m - 1] = 2.5;
+      uo[m - 1] = 2.6;
+    }
+    for (int k = 0; k < MD; ++k) q[k] = 0.01 * (k + 1);
+    const double n[3] = {0.6, 0.8, 0.1};
+    const FlCount fn = c.has_inv ? count_ops([&] {
+      Ctx cc = c;
+      cc.second = false;
+      flux_dot(cc, u, q, n, f);
+    }) : FlCount{};
+    const FlCount fv = c.second ? count_ops([&] { vflux_dot(c, u, q, n, f); }) : FlCount{};
+    const FlCount fr = c.has_inv ? count_ops([&] {
+      if (c.riemann == LDG_ROE) roe_flux(D, uo, u, n, c.gas, f);
+      else llf_flux(D, uo, u, n, c.gas, f);
+    }) : FlCount{};
+    const double L = D * NL;
+    const double interp = 2.0 * NP * m, proj = 2.0 * NP * m, lift = 2.0 * NP * m;
+    double res = 0.0, jac = 0.0;
+    if (!c.second) {
+      res = L * (NQ * (interp + fn.total() + proj) + 2 * (fr.total() + lift)) + NPE * m * (D + 1.0);
+    } else {
+      // gradient pass: per (line, component): interpolation, u_q nvec_q, projection, lifting
+      const double grad = L * m * (NQ * (2.0 * NP + D + 2.0 * NP * D) + 2 * (D + 2.0 * NP * D)) + NPE * MD * D;
+      const double resid = L * (NQ * (interp + 2.0 * NP * MD + fn.total() + fv.total() + m + proj) +
+                                2 * (fr.total() + fv.total() + m + lift)) + NPE * m * (D + 1.0);
+      res = grad + resid;
+    }
+    const double ns11 = D * c.p + 1 + 2 * D, ns12 = D * c.p + 1 + D;
+    // K11: quadrature-point flux Jacobians (forward mode, m seeds), the line
+    // block expansion sum_q cc[i][t][q] A_q, endpoint lifting, 1/J scaling
+    const double Aq = (c.has_inv ? fn.dual(m) : 0.0) + (c.second && c.vis_u ? fv.dual(m) : 0.0);
+    jac = L * (NQ * (interp + Aq) + 2.0 * NP * NP * NQ * m * m + 2 * (fr.dual(m) + 2.0 * NP * m * m)) +
+          NPE * ns11 * m * m;
+    if (c.second) {
+      // K12: dF_vis/dq at the quadrature points (m*D seeds) and its expansion; endpoint viscous Jacobians
+      jac += L * (NQ * (2.0 * NP * MD + fv.dual(MD)) + 2.0 * NP * NP * NQ * m * MD + 2 * (fv.dual(MD) + 2.0 * NP * m * MD)) +
+             NPE * ns12 * m * MD;
+    }
+    out[0] = res;
+    out[1] = jac;
+    out[2] = 2.0 * NPE * ns11 * m * m;
+    out[3] = fn.total();
+    out[4] = fr.total();
+    out[5] = fv.total();
+    out[6] = fr.dual(m);
   });
 }
 

@@ -60,6 +60,7 @@ def lib():
         L.lo_dirk3_step.argtypes = [vp, _dp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                     C.POINTER(LdgSolverStats)]
         L.lo_steady_solve.argtypes = [vp, _dp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
+        L.lo_flop_model.argtypes = [vp, _dp]
         L.lo_precond_build.argtypes = [vp, C.c_double]
         L.lo_precond_apply.argtypes = [vp, _dp, _dp]
         L.lo_gmres.argtypes = [vp, C.c_double, _dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, _dp,
@@ -274,6 +275,14 @@ class Oracle:
         st = LdgSolverStats()
         self._check(self.L.lo_steady_solve(self.h, _d(U), t, C.byref(cfg), C.byref(st)))
         return U, st.as_dict()
+
+    def flop_model(self):
+        """Algorithmic FP64 flops per element: {'residual', 'jacobian', 'spmv'}
+        plus the per-evaluation flux counts (oracle lo_flop_model)."""
+        out = np.zeros(7)
+        self._check(self.L.lo_flop_model(self.h, _d(out)))
+        keys = ("residual", "jacobian", "spmv", "flux", "riemann", "viscous_flux", "riemann_jacobian")
+        return dict(zip(keys, out.tolist()))
 
     def fd_dense(self, which, U, Q=None):
         U = np.ascontiguousarray(U, dtype=np.float64)
