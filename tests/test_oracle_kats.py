@@ -455,3 +455,29 @@ def test_poisson_k11_dirichlet_rows_only():
     bdry_elems = {e for e in range(c.E) if any(f[ef[e, k], 2] < 0 for k in range(4))}
     assert set((rows // c.npe).tolist()) <= bdry_elems  # "Dirichlet rows only"
     assert len(rows) > 0
+
+
+def test_flop_model_counts():
+    """Algorithmic flop model: the counting scalar sees the
+    oracle's own fluxes; SpMV = 2 flops per stored K11 value; the committed
+    profiles/flops.json matches a fresh count."""
+    import json
+    import os
+
+    from oracle.pyoracle import Oracle
+    from paper_1204_1533_b200 import CONFIGS
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    committed = json.load(open(os.path.join(root, "profiles", "flops.json")))
+    for i, cfg in enumerate(CONFIGS):
+        case, _ = cfg.build(n=2)
+        fm = Oracle(case, cfg.physics).flop_model()
+        D, p, m = case.dim, case.p, cfg.physics.components(case.dim)
+        assert fm["spmv"] == 2 * case.npe * (D * p + 1 + 2 * D) * m * m
+        assert fm["residual"] > 0 and fm["jacobian"] > fm["residual"]
+        if cfg.physics.kind == 0:  # Poisson: no Riemann flux
+            assert fm["riemann"] == 0 and fm["flux"] == 0
+        else:
+            assert fm["riemann"] > 2 * fm["flux"] and fm["riemann_jacobian"] > fm["riemann"]
+        for k in ("residual", "jacobian", "spmv"):
+            assert committed[f"config{i}"][k] == fm[k]
