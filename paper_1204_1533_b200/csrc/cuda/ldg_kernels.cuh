@@ -3016,7 +3016,7 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
       }
     } else {
 #pragma unroll
-      for (int b = 0; b < M; ++b) acc += ld_stream1(vp + b) * __ldg(xp + b);
+      for (int b = 0; b < M; ++b) acc += (rev ? ld_stream1(vp + b) : __ldg(vp + b)) * __ldg(xp + b);
     }
   }
   if (SPLIT && C::SECOND) {
@@ -3029,7 +3029,7 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
         if (col < 0) continue;
         const double* vp = vq + static_cast<size_t>(slot) * NT * C::B12;
 #pragma unroll
-        for (int b = 0; b < MD; ++b) acc += ld_stream1(vp + b) * __ldg(w + col * MD + b);
+        for (int b = 0; b < MD; ++b) acc += __ldg(vp + b) * __ldg(w + col * MD + b);
       }
     }
   }
@@ -3067,7 +3067,7 @@ k_spmv12(const KParams<C> kp, const double* __restrict__ V12, const double* __re
       if (col < 0) continue;
       const double* vp = vq + static_cast<size_t>(slot) * NT * C::B12;
 #pragma unroll
-      for (int b = 0; b < MD; ++b) acc += ld_stream1(vp + b) * __ldg(w + col * MD + b);
+      for (int b = 0; b < MD; ++b) acc += __ldg(vp + b) * __ldg(w + col * MD + b);
     }
   }
   (void)R12;
@@ -3101,7 +3101,7 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
     if (col < 0) continue;
     double kv[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) kv[d] = ld_stream1(vb + static_cast<size_t>(slot) * NT * D + d);
+    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + static_cast<size_t>(slot) * NT * D + d);
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       const double xv = __ldg(v + col * M + c);
