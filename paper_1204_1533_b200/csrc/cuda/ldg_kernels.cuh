@@ -1771,7 +1771,31 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 #pragma unroll
       for (int c = 0; c < M; ++c) Jx[c * M + c] += pen;
     }
-    if (ALLC) {
+#ifndef LDG_EJ_DUALN  // all M seeds in one Dual<M> evaluation of the Riemann flux (first-order, not BND)
+#define LDG_EJ_DUALN 0  // measured slower: +18 us at 168 regs (spills), +6 us at 255
+#endif
+    constexpr bool DN = LDG_EJ_DUALN && !BND && !C::SECOND && C::HAS_INV && !LLFC && SEEDS == M;
+    if (DN) {
+      using DM = Dual<(DN ? M : 1)>;
+      DM ui[M], uo[M], fh[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        ui[c] = DM(uiv[c]);
+        uo[c] = DM(uov[c]);
+#pragma unroll
+        for (int b = 0; b < (DN ? M : 1); ++b) {
+          ui[c].d[b] = (pass == 0 && c == b) ? 1.0 : 0.0;
+          uo[c].d[b] = (pass == 1 && c == b) ? 1.0 : 0.0;
+        }
+        fh[c] = DM(0.0);
+      }
+      if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+#pragma unroll
+        for (int b = 0; b < (DN ? M : 1); ++b) put(pass, c * M + b, fh[c].d[b]);
+    } else if (ALLC) {
 #pragma unroll
       for (int c = 0; c < ((LLFC || VCF) ? M * M : 0); ++c) put(pass, c, Jx[c]);
     } else
