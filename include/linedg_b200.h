@@ -76,8 +76,10 @@ typedef enum ldg_bc_kind {
                                   (SPEC.md:266, 366); viscous terms as Dirichlet with the far state    */
   LDG_BC_SLIP_WALL = 3,        /* Riemann flux vs the interior state with mirrored normal momentum
                                   (SPEC.md:367); viscous F(u,q).n, u_hat = u; Euler / Navier-Stokes   */
-  LDG_BC_NO_SLIP_ADIABATIC = 4 /* not supported: ldg_create returns LDG_ERR_CONFIG (SPEC.md:368 needs a
-                                  component-dependent u_hat; the K21 store is component-uniform)     */
+  LDG_BC_NO_SLIP_ADIABATIC = 4 /* mixed wall: Riemann flux vs the interior state with its
+                                  momentum reversed; viscous: momentum F(u,q).n + C11_bd|n| m (Dirichlet
+                                  zero velocity), zero energy flux (adiabatic); u_hat = (rho, 0, E) of u;
+                                  Euler / Navier-Stokes                                                */
 } ldg_bc_kind;
 
 typedef struct ldg_bc {

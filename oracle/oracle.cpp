@@ -159,9 +159,9 @@ void build_endpoints(Ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   std::map<int, int> tag2bc;
   for (int i = 0; i < ph.n_bc; ++i) {
     const int kind = ph.bcs[i].kind;
-    if (kind < LDG_BC_DIRICHLET || kind > LDG_BC_SLIP_WALL)
+    if (kind < LDG_BC_DIRICHLET || kind > LDG_BC_NO_SLIP_ADIABATIC)
       throw std::runtime_error("oracle: unsupported boundary-condition kind");
-    if (kind == LDG_BC_SLIP_WALL && !c.has_inv)
+    if ((kind == LDG_BC_SLIP_WALL || kind == LDG_BC_NO_SLIP_ADIABATIC) && !c.has_inv)
       throw std::runtime_error("oracle: slip-wall boundaries need Euler or Navier-Stokes physics");
     tag2bc[ph.bcs[i].tag] = static_cast<int>(c.bcv.size());
     c.bcv.emplace_back(ph.bcs[i].value, ph.bcs[i].value + c.m);
@@ -272,7 +272,15 @@ double norm_of(const double* n, int D) {
 
 // u_hat of a boundary end is the interior trace (Neumann-type with C22 = 0,
 // PAPER.md:580; slip wall), else the prescribed state.
-inline bool uhat_inner(int bkind) { return bkind == LDG_BC_NEUMANN || bkind == LDG_BC_SLIP_WALL; }
+inline bool uhat_inner(int bkind) {
+  return bkind == LDG_BC_NEUMANN || bkind == LDG_BC_SLIP_WALL || bkind == LDG_BC_NO_SLIP_ADIABATIC;
+}
+// per component: the no-slip adiabatic wall is mixed -- Dirichlet
+// zero momentum (u_hat = 0), Neumann density and energy (u_hat = u_in)
+inline bool uhat_inner_c(int bkind, int comp, int m) {
+  if (bkind == LDG_BC_NO_SLIP_ADIABATIC) return comp == 0 || comp == m - 1;
+  return uhat_inner(bkind);
+}
 
 // Endpoint numerical flux F_hat . n (inviscid Riemann + LDG viscous switch
 // flux; boundaries PAPER.md:566-582).
@@ -295,7 +303,13 @@ void endpoint_flux(const Ctx& c, const T* ui, const T* qi, const T* uo, const T*
   if (c.has_inv) {
     T g[MAXM];
     const T* other = uo;
-    if (bc && bkind == LDG_BC_SLIP_WALL) {
+    if (bc && bkind == LDG_BC_NO_SLIP_ADIABATIC) {
+      // no-slip wall: the interior state with its full momentum reversed
+      g[0] = ui[0];
+      for (int d = 0; d < D; ++d) g[1 + d] = -ui[1 + d];
+      g[m - 1] = ui[m - 1];
+      other = g;
+    } else if (bc && bkind == LDG_BC_SLIP_WALL) {
       double n2 = 0.0;
       for (int d = 0; d < D; ++d) n2 += n[d] * n[d];
       T mn = ui[1] * n[0];
@@ -318,6 +332,12 @@ void endpoint_flux(const Ctx& c, const T* ui, const T* qi, const T* uo, const T*
       vflux_dot(c, ui, qi, n, fv);
       if (bkind == LDG_BC_SLIP_WALL) {
         for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k];
+      } else if (bkind == LDG_BC_NO_SLIP_ADIABATIC) {
+        // momentum: Dirichlet zero velocity, F(u,q).n + C11_bd |n| (m - 0);
+        // density: F(u,q).n (zero row); energy: zero normal flux (adiabatic, no wall work)
+        const double c11 = c.c11_bd * c.p * c.p / std::pow(nn, 1.0 / (D - 1));
+        out[0] = out[0] + fv[0];
+        for (int k = 1; k < m - 1; ++k) out[k] = out[k] + fv[k] + c11 * nn * ui[k];
       } else {
         const double c11 = c.c11_bd * c.p * c.p / std::pow(nn, 1.0 / (D - 1));
         for (int k = 0; k < m; ++k) out[k] = out[k] + fv[k] + c11 * nn * (ui[k] - bc[k]);
@@ -443,8 +463,15 @@ void line_gradient(const Ctx& c, int e, int dir, int line, const LineData& L,
     const int ie = side ? c.p : 0;
     const double* n = c.ne(e, dir, side, line);
     const double* uh;
-    if (L.bc[side] && !uhat_inner(L.bk[side])) uh = L.bc[side];  // u_hat = g_D
-    else if (L.bc[side]) uh = L.u[ie];                        // Neumann-type / slip wall
+    double uhw[MAXM];
+    if (L.bc[side] && L.bk[side] == LDG_BC_NO_SLIP_ADIABATIC) {  // mixed: momentum 0, rho and E interior
+      for (int k = 0; k < m; ++k) uhw[k] = uhat_inner_c(L.bk[side], k, m) ? L.u[ie][k] : 0.0;
+      uh = uhw;
+    } else if (L.bc[side] && !uhat_inner(L.bk[side])) {
+      uh = L.bc[side];  // u_hat = g_D
+    } else if (L.bc[side]) {
+      uh = L.u[ie];  // Neumann-type / slip wall
+    }
     else uh = c.sign(e, dir, side) > 0 ? L.u[ie] : L.uo[side];
     for (int k = 0; k < m; ++k)
       for (int dd = 0; dd < D; ++dd) d[ie][k * D + dd] += uh[k] * n[dd];
@@ -808,7 +835,7 @@ void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
         std::vector<Contrib> p21;
         pattern_line(c, e, dir, line, LDG_K21, p21);
         for (int cidx = 0; cidx < np + 2; ++cidx) {
-          double col[MAXNP][MAXD] = {};
+          double col[MAXNP][MAXD] = {}, colw[MAXNP][MAXD] = {};  // colw: no-slip ends (rho, E only)
           int64_t gcol;
           if (cidx < np) {
             gcol = own(cidx);
@@ -822,8 +849,11 @@ void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
             }
             for (int side = 0; side < 2; ++side) {
               const int ie = side ? c.p : 0;
-              if (ie == cidx && ((!L.bc[side] && c.sign(e, dir, side) > 0) ||
-                                 (L.bc[side] && uhat_inner(L.bk[side])))) {
+              if (ie == cidx && L.bc[side] && L.bk[side] == LDG_BC_NO_SLIP_ADIABATIC) {
+                const double* n = c.ne(e, dir, side, line);
+                for (int dd = 0; dd < D; ++dd) colw[ie][dd] += n[dd];
+              } else if (ie == cidx && ((!L.bc[side] && c.sign(e, dir, side) > 0) ||
+                                        (L.bc[side] && uhat_inner(L.bk[side])))) {
                 const double* n = c.ne(e, dir, side, line);
                 for (int dd = 0; dd < D; ++dd) col[ie][dd] += n[dd];
               }
@@ -838,11 +868,13 @@ void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
             for (int dd = 0; dd < D; ++dd) col[ie][dd] = n[dd];
           }
           for (int dd = 0; dd < D; ++dd) c.mass_solve(&col[0][dd], MAXD);
+          for (int dd = 0; dd < D; ++dd) c.mass_solve(&colw[0][dd], MAXD);
           for (int i = 0; i < np; ++i) {
             if (!has_pat(p21, own(i), gcol)) continue;
             double blk[MAXM * MAXD * MAXM] = {};
             for (int k = 0; k < m; ++k)
-              for (int dd = 0; dd < D; ++dd) blk[(k * D + dd) * m + k] = col[i][dd];
+              for (int dd = 0; dd < D; ++dd)
+                blk[(k * D + dd) * m + k] = col[i][dd] + ((k == 0 || k == m - 1) ? colw[i][dd] : 0.0);
             addblk(LDG_K21, own(i), gcol, blk, c.invJ[own(i)]);
           }
         }

@@ -308,7 +308,7 @@ void build_face_sharing(ldg_ctx& c, int chunk, bool share) {
         const int2 cx = c.conn[static_cast<size_t>(k) * F + ds];
         if (cx.x < 0) {
           const int kind = c.bck[-1 - cx.x];
-          if (kind == LDG_BC_SLIP_WALL || kind == LDG_BC_NEUMANN) {
+          if (kind == LDG_BC_SLIP_WALL || kind == LDG_BC_NEUMANN || kind == LDG_BC_NO_SLIP_ADIABATIC) {
             bspec.push_back(k * F + ds);
             continue;
           }
@@ -468,14 +468,11 @@ void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
   c.bck.clear();
   for (int i = 0; i < ph.n_bc; ++i) {
     const int kind = ph.bcs[i].kind;
-    if (kind == LDG_BC_NO_SLIP_ADIABATIC)
-      throw ldg_error(LDG_ERR_CONFIG,
-                      "no-slip adiabatic walls are not supported (their gradient trace u_hat is component-dependent; "
-                      "the K21 store is component-uniform)");
-    if (kind < LDG_BC_DIRICHLET || kind > LDG_BC_SLIP_WALL)
+    if (kind < LDG_BC_DIRICHLET || kind > LDG_BC_NO_SLIP_ADIABATIC)
       throw ldg_error(LDG_ERR_CONFIG, "unsupported boundary-condition kind");
-    if (kind == LDG_BC_SLIP_WALL && !c.has_inv)
-      throw ldg_error(LDG_ERR_CONFIG, "slip-wall boundaries need Euler or Navier-Stokes physics");
+    if ((kind == LDG_BC_SLIP_WALL || kind == LDG_BC_NO_SLIP_ADIABATIC) && !c.has_inv)
+      throw ldg_error(LDG_ERR_CONFIG, "slip-wall and no-slip-wall boundaries need Euler or Navier-Stokes physics");
+    if (kind == LDG_BC_NO_SLIP_ADIABATIC) ++c.dc.noslip;
     tag2bc[ph.bcs[i].tag] = i;
     c.bck.push_back(kind);
     for (int k = 0; k < c.m; ++k) bcv.push_back(ph.bcs[i].value[k]);
@@ -1028,7 +1025,7 @@ int ldg_export_blocks_subset(ldg_ctx* c, int which, const int32_t* elems, int32_
       list.resize(c->E);
       for (int e = 0; e < c->E; ++e) list[e] = e;
     }
-    std::vector<double> chunk(per_elem);
+    std::vector<double> chunk(per_elem), metk(o.METP);
     int64_t pos = 0;
     std::vector<std::pair<int64_t, int>> cl;
     for (const int32_t e : list) {
@@ -1038,6 +1035,10 @@ int ldg_export_blocks_subset(ldg_ctx* c, int which, const int32_t* elems, int32_
         ck(cudaMemcpy(chunk.data(), dsrc + static_cast<size_t>(k) * per_elem, per_elem * sizeof(double),
                       cudaMemcpyDeviceToHost),
            "download Jacobian");
+      if (vals && which == LDG_K21 && c->dc.noslip)
+        ck(cudaMemcpy(metk.data(), c->d_metric + static_cast<size_t>(k) * o.METP, o.METP * sizeof(double),
+                      cudaMemcpyDeviceToHost),
+           "download metric");
       for (int nd = 0; nd < c->npe; ++nd) {
         const int tile = nd / NT, r = nd % NT;
         cl.clear();
@@ -1073,6 +1074,27 @@ int ldg_export_blocks_subset(ldg_ctx* c, int which, const int32_t* elems, int32_
                 for (int cc2 = 0; cc2 < c->m; ++cc2)
                   for (int d = 0; d < c->D; ++d) blk[(cc2 * c->D + d) * bc + cc2] += at(d);
               }
+            }
+            if (which == LDG_K21 && c->dc.noslip) {
+              // wall terms (k21_wall_terms): density and energy rows of no-slip ends
+              for (int dir = 0; dir < c->D; ++dir)
+                for (int side = 0; side < 2; ++side) {
+                  const int2& cx = c->cn(k, dir, side);
+                  if (cx.x >= 0 || c->bck[-1 - cx.x] != LDG_BC_NO_SLIP_ADIABATIC) continue;
+                  int line, lp;
+                  c->line_of(dir, nd, line, lp);
+                  const int xs[3] = {nd % c->np, (nd / c->np) % c->np, nd / (c->np * c->np)};
+                  const int st[3] = {1, c->np, c->np * c->np};
+                  const int endn = nd + ((side ? c->p : 0) - xs[dir]) * st[dir];
+                  if (static_cast<int64_t>(e) * c->npe + endn != cl[a].first) continue;
+                  const double invJ = metk[o.MET_NV + o.MET_NE + nd];
+                  const double mi = c->mi[lp * 2 + side];
+                  for (int d = 0; d < c->D; ++d) {
+                    const double cf = invJ * (mi * metk[o.MET_NV + ((dir * 2 + side) * c->NL + line) * c->D + d]);
+                    blk[(0 * c->D + d) * bc + 0] += cf;
+                    blk[((c->m - 1) * c->D + d) * bc + c->m - 1] += cf;
+                  }
+                }
             }
           }
           ++pos;

@@ -89,7 +89,7 @@ struct PhysParams {
 
 // Boundary condition kinds (reference BcKind, physics.hpp:16; the values of
 // ldg_bc_kind in include/linedg_b200.h).
-enum BcKindDev : int { BC_DIRICHLET = 0, BC_NEUMANN = 1, BC_CHARACTERISTIC = 2, BC_SLIP_WALL = 3 };
+enum BcKindDev : int { BC_DIRICHLET = 0, BC_NEUMANN = 1, BC_CHARACTERISTIC = 2, BC_SLIP_WALL = 3, BC_NO_SLIP = 4 };
 
 // ------------------------------------------------------------ Dual<N>
 template <int N>
@@ -258,7 +258,13 @@ __device__ __forceinline__ void euler_jac_n(const double* u, const double* n, do
 // (the ghost is a function of u_in, so its derivative carries through).
 template <int D, int M, class T>
 __device__ __forceinline__ void bc_ghost(int kind, const double* g, const T* ui, const double* n, T* uo) {
-  if (M == D + 2 && kind == BC_SLIP_WALL) {
+  if (M == D + 2 && kind == BC_NO_SLIP) {
+    // no-slip wall: the interior state with its full momentum reversed
+    uo[0] = ui[0];
+#pragma unroll
+    for (int d = 0; d < D; ++d) uo[1 + d] = -ui[1 + d];
+    uo[M - 1] = ui[M - 1];
+  } else if (M == D + 2 && kind == BC_SLIP_WALL) {
     double n2 = n[0] * n[0];
 #pragma unroll
     for (int d = 1; d < D; ++d) n2 += n[d] * n[d];

@@ -33,6 +33,7 @@ struct KParams {
   const int2* conn;      // [k][D][2]
   const double* bcv;     // [nbc][M] boundary data (Dirichlet / far-field state, Neumann flux)
   const int32_t* bck;    // [nbc] boundary kind (BcKindDev)
+  int noslip;            // number of no-slip-wall boundary conditions (K21 wall terms)
   const double* source;  // reference numbering, may be null
   DevError* err;
   const int2* fpart;     // [k][2D] face partner {k', 2 dir' + side'} ({-1, 0}: none)
@@ -75,6 +76,13 @@ __device__ __forceinline__ void bnd_flux(const KParams<C>& kp, int bc, const T* 
     if (kind == BC_SLIP_WALL) {
 #pragma unroll
       for (int c = 0; c < M; ++c) fh[c] = fh[c] + fv[c];
+    } else if (kind == BC_NO_SLIP) {
+      // momentum: Dirichlet zero velocity (penalty on m - 0); density row of F
+      // is zero; energy: zero normal flux (adiabatic, no wall work)
+      const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+      fh[0] = fh[0] + fv[0];
+#pragma unroll
+      for (int c = 1; c < M - 1; ++c) fh[c] = fh[c] + (fv[c] + (c11 * nn) * ui[c]);
     } else {
       const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
 #pragma unroll
@@ -89,6 +97,16 @@ template <class C>
 __device__ __forceinline__ bool bnd_uhat_inner(const KParams<C>& kp, int bc) {
   const int kind = __ldg(kp.bck + bc);
   return kind == BC_NEUMANN || kind == BC_SLIP_WALL;
+}
+// u_hat of component c at a boundary end with interior trace uin: the
+// no-slip adiabatic wall is mixed -- zero momentum (Dirichlet
+// velocity), interior density and energy (Neumann-type, C22 = 0)
+template <class C>
+__device__ __forceinline__ double bnd_uhat(const KParams<C>& kp, int bc, int c, double uin) {
+  const int kind = __ldg(kp.bck + bc);
+  if (kind == BC_NO_SLIP) return (c == 0 || c == C::M - 1) ? uin : 0.0;
+  if (kind == BC_NEUMANN || kind == BC_SLIP_WALL) return uin;
+  return __ldg(kp.bcv + bc * C::M + c);
 }
 
 #ifndef LDG_VISC_DU  // closed-form viscous dF/du (1) or dual numbers (0)
@@ -1398,10 +1416,10 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
       for (int side = 0; side < 2; ++side) {
         const int2 cn = io.bCONN(cur)[(l * D + dir) * 2 + side];
         double uh;
-        if (cn.x < 0 && !bnd_uhat_inner(kp, -1 - cn.x))
-          uh = __ldg(kp.bcv + (-1 - cn.x) * M + c);  // Dirichlet-type: u_hat = g_D
-        else if (cn.x < 0 || conn_sign(cn.y) > 0)
-          uh = ul[side ? P : 0];  // S = +1; Neumann-type / slip-wall boundary
+        if (cn.x < 0)  // boundary: g_D, the interior trace, or mixed (no-slip wall)
+          uh = bnd_uhat(kp, -1 - cn.x, c, ul[side ? P : 0]);
+        else if (conn_sign(cn.y) > 0)
+          uh = ul[side ? P : 0];  // S = +1
         else uh = io.bNB(cur)[((lw << 1) | side) * M + c];
         const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
 #pragma unroll
@@ -1494,10 +1512,11 @@ k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict
       const int ie = side ? C::P : 0;
       const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
       double uh[M];
-      if (cn.x < 0 && !bnd_uhat_inner(kp, -1 - cn.x)) {  // Dirichlet-type: u_hat = g_D
+      if (cn.x < 0) {  // boundary: g_D, the interior trace, or mixed (no-slip wall)
+        const int nd = node_on_line<C>(dir, line, ie);
 #pragma unroll
-        for (int c = 0; c < M; ++c) uh[c] = __ldg(kp.bcv + (-1 - cn.x) * M + c);
-      } else if (cn.x < 0 || conn_sign(cn.y) > 0) {  // S = +1; Neumann-type / slip wall
+        for (int c = 0; c < M; ++c) uh[c] = bnd_uhat(kp, -1 - cn.x, c, sul[nd * M + c]);
+      } else if (conn_sign(cn.y) > 0) {  // S = +1
         const int nd = node_on_line<C>(dir, line, ie);
 #pragma unroll
         for (int c = 0; c < M; ++c) uh[c] = sul[nd * M + c];
@@ -1720,7 +1739,8 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   // boundary kind: Dirichlet / characteristic (ghost = g), slip wall (ghost =
   // mirrored u_in), Neumann (constant flux: no u dependence), see bnd_flux
   const int bkind = (BND && bd) ? __ldg(kp.bck + (-1 - cn.x)) : -1;
-  const bool bneu = BND && bkind == BC_NEUMANN, bslip = BND && bkind == BC_SLIP_WALL;
+  const bool bneu = BND && bkind == BC_NEUMANN, bslip = BND && bkind == BC_SLIP_WALL,
+             bnos = BND && bkind == BC_NO_SLIP;
 #pragma unroll
   for (int c = 0; c < M; ++c) {
     uiv[c] = __ldg(U + own * M + c);
@@ -1812,7 +1832,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         uo[c].d[0] = (pass == 1 && c == b) ? 1.0 : 0.0;
         fh[c] = D1(0.0);
       }
-      if (bslip) bc_ghost<D, M>(bkind, bcp, ui, n, uo);  // the ghost follows u_in (BND only)
+      if (bslip || bnos) bc_ghost<D, M>(bkind, bcp, ui, n, uo);  // the ghost follows u_in (BND only)
       if (C::HAS_INV && !bneu) {
         if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
         else if (!LLFC) llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
@@ -1820,7 +1840,13 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       if (C::SECOND && !VCF) {
         D1 fv[M];
         if (bd) {
-          if (!bneu) {
+          if (bnos) {  // mixed wall: momentum penalty on m - 0, zero energy flux
+            visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
+            const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
+            fh[0] = fh[0] + fv[0];
+#pragma unroll
+            for (int c = 1; c < M - 1; ++c) fh[c] = fh[c] + fv[c] + (c11 * nn) * ui[c];
+          } else if (!bneu) {
             visc_fn<D, C::PH, D1, double, D1>(ui, qiv, n, kp.pp, fv, ok);
             const double c11 = bslip ? 0.0 : kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
 #pragma unroll
@@ -1850,7 +1876,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     double L[M * MD];
     visc_dq<D, C::PH>(usrc, n, kp.pp, L, ok);
 #pragma unroll
-    for (int c = 0; c < M * MD; ++c) put(2, c, bneu ? 0.0 : L[c]);
+    for (int c = 0; c < M * MD; ++c) put(2, c, (bneu || (bnos && c / MD == M - 1)) ? 0.0 : L[c]);
   }
   if (!ok) {
     // a non-physical state at this line end: report the offending nodal state
@@ -2866,6 +2892,32 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 }
 
 // K21 = dQ/dU (U-independent; D scalars per node pair), same tiles/rows.
+// K21 wall terms of row node nd of element k (processing index): at a
+// no-slip-wall end the gradient trace of density and energy is the own trace
+// (zero momentum), so K21 gains (1/J) M^-1[pos][side] n_d for those two
+// components only -- kept out of the component-uniform K21 store and applied
+// by its consumers (k_spmv21, k_pc_build, the export).  f(end_node, coef[D]).
+template <class C, class F>
+__device__ __forceinline__ void k21_wall_terms(const KParams<C>& kp, int k, int nd, F&& f) {
+  constexpr int D = C::D, NL = C::NL, P = C::P;
+  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
+  const double invJ = __ldg(mk + C::MET_NV + C::MET_NE + nd);
+#pragma unroll
+  for (int dir = 0; dir < D; ++dir)
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int2 cx = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+      if (cx.x >= 0 || __ldg(kp.bck + (-1 - cx.x)) != BC_NO_SLIP) continue;
+      int line, pos;
+      line_of<C>(dir, nd, line, pos);
+      const double mi = kp.bt.mi[pos][side];
+      double cf[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cf[d] = invJ * (mi * __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d));
+      f(node_on_line<C>(dir, line, side ? P : 0), cf);
+    }
+}
+
 template <class C>
 __global__ void __launch_bounds__(128) k_k21(const KParams<C> kp, double* __restrict__ K21) {
   constexpr int NP = C::NP, NQ = C::NQ, NL = C::NL, D = C::D, NT = C::NT, P = C::P;
@@ -3133,6 +3185,15 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
       for (int d = 0; d < D; ++d) acc[c][d] += kv[d] * xv;
     }
   }
+  if (C::HAS_INV && kp.noslip)
+    k21_wall_terms<C>(kp, k, nd, [&](int end, const double* cf) {
+      const double x0 = __ldg(v + (e * NPE + end) * M), x1 = __ldg(v + (e * NPE + end) * M + M - 1);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        acc[0][d] += cf[d] * x0;
+        acc[M - 1][d] += cf[d] * x1;
+      }
+    });
   const size_t wo = (e * NPE + nd) * M * D;
 #pragma unroll
   for (int c = 0; c < M; ++c)
@@ -3224,6 +3285,19 @@ k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __
             atomicAdd(&Ms[(nd * M + ap + A0) * LDM + cl * M + b], sum);
           }
       }
+      if (C::HAS_INV && kp.noslip && em == static_cast<int>(e))
+        k21_wall_terms<C>(kp, km, ndm, [&](int end, const double* cf) {
+          if (!pc_on_line<C>(nd, end)) return;
+          for (int ap = 0; ap < R12; ++ap)
+            for (int bi = 0; bi < 2; ++bi) {  // density and energy columns
+              const int b = bi ? M - 1 : 0;
+              double sum = 0.0;
+#pragma unroll
+              for (int d = 0; d < D; ++d)
+                sum += __ldg(K12 + (((T12 * NS12 + s12) * R12 + ap) * NT + nd % NT) * MD + b * D + d) * cf[d];
+              atomicAdd(&Ms[(nd * M + ap + A0) * LDM + end * M + b], sum);
+            }
+        });
     }
     __syncthreads();
   }

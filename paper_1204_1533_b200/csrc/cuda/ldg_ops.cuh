@@ -26,6 +26,7 @@ struct DevCtx {
   const int2* conn = nullptr;
   const double* bcv = nullptr;
   const int32_t* bck = nullptr;
+  int noslip = 0;
   const double* source = nullptr;
   DevError* err = nullptr;
   // face sharing of the endpoint flux Jacobians (null = every line end computes its own)
@@ -78,6 +79,7 @@ struct Launch {
     kp.conn = d.conn;
     kp.bcv = d.bcv;
     kp.bck = d.bck;
+    kp.noslip = d.noslip;
     kp.source = d.source;
     kp.err = d.err;
     kp.fpart = d.fpart;

@@ -1,5 +1,5 @@
 """Boundary conditions beyond Dirichlet: Neumann,
-characteristic far field, slip wall (reference BcKind, physics.hpp:16-31;
+characteristic far field, slip wall, no-slip adiabatic wall (reference BcKind, physics.hpp:16-31;
 PAPER.md:566-582), and curved boundaries
 (mapping.cpp:30-65, tests/test_curved_mapping.py).
 
@@ -7,9 +7,11 @@ CPU: known answers and properties of the oracle restatement -- linear fields
 are steady with exact Neumann data, slip walls conserve mass and energy
 (zero normal mass flux through the mirrored-state Roe/LLF flux),
 characteristic == Dirichlet against the far state, analytic Jacobians equal
-finite differences (chain rule through the slip-wall ghost state), no-slip
-walls are refused.  GPU (-m gpu): residual, gradient, K11/K12/K21 patterns
-(bit-exact) and values, SpMV and split matvec vs the oracle (<= 1e-12).
+finite differences (chain rule through the slip- and no-slip-wall ghost
+states, the no-slip wall's component-dependent gradient trace), slip and
+no-slip walls conserve mass and energy.  GPU (-m gpu): residual, gradient,
+K11/K12/K21 patterns (bit-exact) and values, K11/K21 SpMV, split matvec and
+the block-Jacobi preconditioner vs the oracle (<= 1e-12 / 1e-11).
 """
 import numpy as np
 import pytest
@@ -21,8 +23,8 @@ from oracle.pyoracle import Oracle
 
 G = 1.4
 EU, NS, PO = _abi.LDG_EULER, _abi.LDG_NAVIER_STOKES, _abi.LDG_POISSON
-DIR, NEU, CHAR, SLIP = (_abi.LDG_BC_DIRICHLET, _abi.LDG_BC_NEUMANN, _abi.LDG_BC_CHARACTERISTIC,
-                        _abi.LDG_BC_SLIP_WALL)
+DIR, NEU, CHAR, SLIP, NOSLIP = (_abi.LDG_BC_DIRICHLET, _abi.LDG_BC_NEUMANN, _abi.LDG_BC_CHARACTERISTIC,
+                                _abi.LDG_BC_SLIP_WALL, _abi.LDG_BC_NO_SLIP_ADIABATIC)
 
 
 def rel(a, b):
@@ -196,9 +198,48 @@ def test_poisson_neumann_jacobian_vs_fd_and_pattern():
 def test_unsupported_boundary_kinds_are_refused():
     case = box(2, 2, 2)
     with pytest.raises(RuntimeError):
-        Oracle(case, Physics(EU, bcs=[(t, [1, 0, 0, 2.5], _abi.LDG_BC_NO_SLIP_ADIABATIC) for t in (1, 2, 3, 4)]))
-    with pytest.raises(RuntimeError):
         Oracle(case, Physics(PO, bcs=[(t, [0.0], SLIP) for t in (1, 2, 3, 4)]))
+    with pytest.raises(RuntimeError):
+        Oracle(case, Physics(PO, bcs=[(t, [0.0], NOSLIP) for t in (1, 2, 3, 4)]))
+    with pytest.raises(RuntimeError):
+        Oracle(case, Physics(EU, bcs=[(t, [0.0] * 4, 7) for t in (1, 2, 3, 4)]))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_no_slip_walls_conserve_mass_and_energy(dim):
+    """A closed box of no-slip adiabatic walls: the reversed-
+    momentum ghost carries no mass or energy through the wall, the adiabatic
+    condition no viscous energy flux."""
+    case = box(dim, 3, 3 if dim == 2 else 2)
+    U = flow_state(case, seed=6)
+    bcs = [(t, [0.0] * (dim + 2), NOSLIP) for t in range(1, 2 * dim + 1)]
+    ora = Oracle(case, Physics(NS, mu=0.02, bcs=bcs))
+    R = ora.residual(U).reshape(case.E, case.npe, dim + 2)
+    w = node_weights(case)
+    for comp in (0, dim + 1):
+        tot = (w * R[..., comp]).sum()
+        scale = (w * np.abs(R[..., comp])).sum()
+        assert abs(tot) < 1e-12 * scale, (comp, tot, scale)
+    # the gradient sees zero velocity at the wall: Q of momentum uses u_hat = 0
+    Q = ora.gradient(U)
+    assert np.isfinite(Q).all()
+
+
+def test_no_slip_jacobians_vs_fd():
+    """Mixed no-slip wall: component-dependent gradient trace (K21 rows of
+    density and energy only) and the momentum penalty -- analytic = FD."""
+    far = list(conservative(np.array(1.0), [np.array(0.3), np.array(-0.2)], np.array(1 / G)))
+    case = box(2, 2, 2)
+    U = flow_state(case, seed=4)
+    bcs = [(1, [0] * 4, NOSLIP), (2, far, CHAR), (3, [0] * 4, NOSLIP), (4, far, DIR)]
+    _fd_check(case, Physics(NS, mu=0.05, bcs=bcs), U, True)
+    _fd_check(case, Physics(EU, bcs=bcs), U, False)
+    case3 = box(3, 2, 1)
+    U3 = flow_state(case3, seed=2)
+    far3 = list(conservative(np.array(1.0), [np.array(0.2), np.array(0.1), np.array(-0.1)], np.array(1 / G)))
+    bcs3 = [(1, far3, CHAR), (2, far3, CHAR), (3, [0] * 5, NOSLIP), (4, [0] * 5, NOSLIP), (5, [0] * 5, SLIP),
+            (6, [0] * 5, NOSLIP)]
+    _fd_check(case3, Physics(NS, mu=0.05, bcs=bcs3), U3, True)
 
 
 # ------------------------------------------------------------- GPU parity
@@ -240,7 +281,21 @@ def _gpu_cases():
             return case, Physics(kind, riemann=riemann, mu=mu, bcs=bcs), flow_state(case, seed=13), kind == NS
         return b
 
-    return [("cyl-p3-roe", cyl(3, _abi.LDG_ROE)), ("cyl-p4-roe", cyl(4, _abi.LDG_ROE)),
+    def ns_noslip(p, dim=2):
+        def b():
+            case = box(dim, 3 if dim == 2 else 2, p)
+            if dim == 2:
+                bcs = [(1, [0] * 4, NOSLIP), (2, far2, CHAR), (3, [0] * 4, NOSLIP), (4, far2, DIR)]
+            else:
+                far3 = list(conservative(np.array(1.0), [np.array(0.2), np.array(0.1), np.array(-0.1)],
+                                         np.array(1 / G)))
+                bcs = [(1, far3, CHAR), (2, far3, CHAR), (3, [0] * 5, NOSLIP), (4, [0] * 5, NOSLIP),
+                       (5, [0] * 5, SLIP), (6, [0] * 5, NOSLIP)]
+            return case, Physics(NS, mu=0.02, bcs=bcs), flow_state(case, seed=17), True
+        return b
+
+    return [("ns-noslip-p3", ns_noslip(3)), ("ns-noslip-p4", ns_noslip(4)), ("ns3-noslip-p2", ns_noslip(2, 3)),
+            ("cyl-p3-roe", cyl(3, _abi.LDG_ROE)), ("cyl-p4-roe", cyl(4, _abi.LDG_ROE)),
             ("cyl-p4-llf", cyl(4, _abi.LDG_LLF)), ("ns-box-p3", ns_box(3)), ("ns-box-p4", ns_box(4)),
             ("poisson-p3", poisson(3)), ("euler3-p3-llf", box3(EU, 3, _abi.LDG_LLF)),
             ("euler3-p2-roe", box3(EU, 2)), ("ns3-p2", box3(NS, 2)), ("ns3-p4", box3(NS, 4))]
@@ -275,19 +330,26 @@ def test_gpu_boundary_parity(name, builder):
         assert rel(v1, v0) <= 1e-12, (w, rel(v1, v0))
     x = case.normal_vector(gpu.m, 77)
     assert rel(host(gpu.spmv(LDG_K11, dev(x))), ora.spmv(LDG_K11, x)) <= 1e-12
+    if second:
+        assert rel(host(gpu.spmv(LDG_K21, dev(x))), ora.spmv(LDG_K21, x)) <= 1e-12
     for adt in (1e-3, 0.37):
         assert rel(host(gpu.split_matvec(adt, dev(x))), ora.split_matvec(adt, x)) <= 1e-12
+    if case.dim == 2 and case.npe * gpu.m <= 128:
+        # block-Jacobi preconditioner (K12 K21 on the element pattern, wall terms included)
+        gpu.precond_build(0.05)
+        ora.precond_build(0.05)
+        assert rel(host(gpu.precond_apply(dev(x))), ora.precond_apply(x)) <= 1e-11
 
 
 @pytest.mark.gpu
-def test_gpu_refuses_no_slip_and_poisson_slip():
+def test_gpu_refuses_poisson_walls():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_1204_1533_b200.linedg import ConfigError, LineDG
 
     case = box(2, 2, 2)
-    with pytest.raises(ConfigError, match="no-slip"):
-        LineDG(case, Physics(EU, bcs=[(t, [1, 0, 0, 2.5], _abi.LDG_BC_NO_SLIP_ADIABATIC) for t in (1, 2, 3, 4)]))
     with pytest.raises(ConfigError, match="slip-wall"):
         LineDG(case, Physics(PO, bcs=[(t, [0.0], SLIP) for t in (1, 2, 3, 4)]))
+    with pytest.raises(ConfigError, match="no-slip"):
+        LineDG(case, Physics(PO, bcs=[(t, [0.0], NOSLIP) for t in (1, 2, 3, 4)]))
