@@ -166,6 +166,16 @@ int ldg_last_error_state(const ldg_ctx* ctx, int32_t* elem, int32_t* node, doubl
 int ldg_components(const ldg_ctx* ctx);               /* m */
 int64_t ldg_num_dofs(const ldg_ctx* ctx);             /* E * npe * m */
 
+/* Space- and time-dependent boundary data (the reference's std::function
+ * g_D / g_N data, physics.hpp:20-31): fn(user, x[dim], t, out[m]) is evaluated
+ * on the host at the end node of every boundary line end tagged `tag` (node
+ * coordinates from ldg_setup.node_coords, required) and uploaded; it replaces
+ * that condition's constant value[] (Dirichlet g_D, Neumann g_N, far-field
+ * state).  Re-evaluated when a device call passes a different t.  fn = NULL
+ * restores the constant data.  The callback runs on the calling host thread. */
+typedef void (*ldg_bc_fn)(void* user, const double* x, double t, double* out);
+int ldg_set_boundary_function(ldg_ctx* ctx, int32_t tag, ldg_bc_fn fn, void* user);
+
 /* Optional nodal source S (E*npe*m doubles, host pointer), added to R
  * (PoissonModel::source_fn evaluated at the nodes, physics.hpp:102). */
 int ldg_set_source(ldg_ctx* ctx, const double* source_host);

@@ -71,6 +71,13 @@ struct Ctx {
   std::vector<int32_t> ep_elem, ep_node, ep_bc;  // ep_bc: -1 interior, else index in bcv
   std::vector<std::vector<double>> bcv;          // boundary data (g_D / g_N / far-field state)
   std::vector<int> bck;                          // boundary kind per bcv entry (ldg_bc_kind)
+  std::vector<int> bctag;                        // mesh tag per bcv entry
+  // boundary functions: end-node coordinates per line end [E][D][2][NL][D],
+  // per-line-end data ep_g [E][D][2][NL][m] when any function is registered
+  std::vector<double> ep_x, ep_g;
+  std::map<int, std::pair<ldg_bc_fn, void*>> bfun;
+  double bfun_t = 0.0;
+  bool bfun_dirty = false;
   BlockMat K[3];
   // block-Jacobi preconditioner: per element LU (partial pivoting) of
   // I - alpha_dt A~ restricted to the element (dense n_e x n_e, row-major)
@@ -166,6 +173,7 @@ void build_endpoints(Ctx& c, const ldg_setup& s, const ldg_physics& ph) {
     tag2bc[ph.bcs[i].tag] = static_cast<int>(c.bcv.size());
     c.bcv.emplace_back(ph.bcs[i].value, ph.bcs[i].value + c.m);
     c.bck.push_back(kind);
+    c.bctag.push_back(ph.bcs[i].tag);
   }
   const int F = 2 * c.D;
   for (int e = 0; e < c.E; ++e)
@@ -376,7 +384,7 @@ void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const 
     L.bc[side] = nullptr;
     L.bk[side] = -1;
     if (c.ep_bc[k] >= 0) {
-      L.bc[side] = c.bcv[c.ep_bc[k]].data();
+      L.bc[side] = c.ep_g.empty() ? c.bcv[c.ep_bc[k]].data() : &c.ep_g[k * c.m];
       L.bk[side] = c.bck[c.ep_bc[k]];
       continue;
     }
@@ -1062,6 +1070,18 @@ int lo_create(const ldg_setup* s, const ldg_physics* ph, lo_ctx** out) {
       c.sw.assign(s->switch_plus, s->switch_plus + static_cast<size_t>(c.E) * c.D);
     }
     build_endpoints(c, *s, *ph);
+    if (s->node_coords) {  // own end-node coordinates of every line end (boundary functions)
+      c.ep_x.assign(c.ep_bc.size() * c.D, 0.0);
+      for (int e = 0; e < c.E; ++e)
+        for (int dir = 0; dir < c.D; ++dir)
+          for (int side = 0; side < 2; ++side)
+            for (int line = 0; line < c.NL; ++line) {
+              const int nd = c.node_on_line(dir, line, side ? c.p : 0);
+              const size_t k = c.epi(e, dir, side, line);
+              for (int d = 0; d < c.D; ++d)
+                c.ep_x[k * c.D + d] = s->node_coords[(static_cast<size_t>(e) * c.npe + nd) * c.D + d];
+            }
+    }
     *out = x.release();
   });
 }
@@ -1077,14 +1097,54 @@ int lo_set_source(lo_ctx* x, const double* S) {
   });
 }
 
+}  // extern "C"
+namespace {
+// boundary functions: evaluate at every boundary line end's own end node
+void refresh_boundary(Ctx& c, double t) {
+  if (c.bfun.empty()) {
+    c.ep_g.clear();
+    return;
+  }
+  if (!c.bfun_dirty && t == c.bfun_t && !c.ep_g.empty()) return;
+  const size_t n = c.ep_bc.size();
+  c.ep_g.assign(n * c.m, 0.0);
+  for (size_t k = 0; k < n; ++k) {
+    const int bc = c.ep_bc[k];
+    if (bc < 0) continue;
+    auto it = c.bfun.find(c.bctag[bc]);
+    if (it == c.bfun.end()) std::copy(c.bcv[bc].begin(), c.bcv[bc].end(), c.ep_g.begin() + k * c.m);
+    else it->second.first(it->second.second, &c.ep_x[k * c.D], t, &c.ep_g[k * c.m]);
+  }
+  c.bfun_t = t;
+  c.bfun_dirty = false;
+}
+}  // namespace
+extern "C" {
+
+int lo_set_boundary_function(lo_ctx* x, int32_t tag, ldg_bc_fn fn, void* user) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    if (std::find(c.bctag.begin(), c.bctag.end(), tag) == c.bctag.end())
+      throw std::runtime_error("oracle: no boundary condition with tag " + std::to_string(tag));
+    if (fn && c.ep_x.empty()) throw std::runtime_error("oracle: boundary functions need node coordinates");
+    if (fn) c.bfun[tag] = {fn, user};
+    else c.bfun.erase(tag);
+    c.bfun_dirty = true;
+  });
+}
+
 int lo_gradient(lo_ctx* x, const double* U, double t, double* Q) {
-  (void)t;
-  return guarded([&] { gradient(x->c, U, Q); });
+  return guarded([&] {
+    refresh_boundary(x->c, t);
+    gradient(x->c, U, Q);
+  });
 }
 
 int lo_residual_uq(lo_ctx* x, const double* U, const double* Q, double t, double* R) {
-  (void)t;
-  return guarded([&] { residual(x->c, U, Q, R); });
+  return guarded([&] {
+    refresh_boundary(x->c, t);
+    residual(x->c, U, Q, R);
+  });
 }
 
 // Residual, optionally restricted to a subset of elements (rows of other
@@ -1092,9 +1152,9 @@ int lo_residual_uq(lo_ctx* x, const double* U, const double* Q, double t, double
 // first (on the needed elements plus their neighbours: here, all).
 int lo_residual(lo_ctx* x, const double* U, double t, double* R, double* Qout,
                 const int32_t* elems, int32_t n_sub) {
-  (void)t;
   return guarded([&] {
     Ctx& c = x->c;
+    refresh_boundary(c, t);
     std::vector<int> sub;
     const std::vector<int>* sp = nullptr;
     if (elems) {
@@ -1119,9 +1179,9 @@ int lo_residual(lo_ctx* x, const double* U, double t, double* R, double* Qout,
 // Analytic assembly (mode 0) of K11 (+K12, K21 for second-order physics),
 // optionally only for the rows of a subset of elements.
 int lo_assemble(lo_ctx* x, const double* U, double t, const int32_t* elems, int32_t n_sub) {
-  (void)t;
   return guarded([&] {
     Ctx& c = x->c;
+    refresh_boundary(c, t);
     std::vector<int> sub;
     const std::vector<int>* sp = nullptr;
     if (elems) {

@@ -61,6 +61,8 @@ def lib():
                                     C.POINTER(LdgSolverStats)]
         L.lo_steady_solve.argtypes = [vp, _dp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
         L.lo_flop_model.argtypes = [vp, _dp]
+        from paper_1204_1533_b200._abi import BC_FN
+        L.lo_set_boundary_function.argtypes = [vp, C.c_int32, BC_FN, vp]
         L.lo_precond_build.argtypes = [vp, C.c_double]
         L.lo_precond_apply.argtypes = [vp, _dp, _dp]
         L.lo_gmres.argtypes = [vp, C.c_double, _dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, _dp,
@@ -275,6 +277,19 @@ class Oracle:
         st = LdgSolverStats()
         self._check(self.L.lo_steady_solve(self.h, _d(U), t, C.byref(cfg), C.byref(st)))
         return U, st.as_dict()
+
+    def set_boundary_function(self, tag, fn):
+        """fn(x, t) -> m values; None restores the constant data."""
+        from paper_1204_1533_b200._abi import BC_FN, make_bc_fn
+        if not hasattr(self, "_bc_cbs"):
+            self._bc_cbs = {}
+        if fn is None:
+            self._bc_cbs.pop(tag, None)
+            self._check(self.L.lo_set_boundary_function(self.h, tag, BC_FN(), None))
+            return
+        cb = make_bc_fn(fn, self.dim, self.m)
+        self._bc_cbs[tag] = cb
+        self._check(self.L.lo_set_boundary_function(self.h, tag, cb, None))
 
     def flop_model(self):
         """Algorithmic FP64 flops per element: {'residual', 'jacobian', 'spmv'}

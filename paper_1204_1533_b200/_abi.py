@@ -103,6 +103,19 @@ class LhLatticeParams(C.Structure):
 CURVE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double))
 
 
+# Boundary-data callback: fn(user, x[dim], t, out[m]) (ldg_bc_fn; physics.hpp:20-31)
+BC_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_double, C.POINTER(C.c_double))
+
+
+def make_bc_fn(fn, dim: int, m: int):
+    """ctypes callback from fn(x: tuple of dim floats, t) -> sequence of m values."""
+    def _cb(_user, x, t, out):
+        v = fn(tuple(x[d] for d in range(dim)), t)
+        for k in range(m):
+            out[k] = float(v[k])
+    return BC_FN(_cb)
+
+
 def _load(name: str) -> C.CDLL:
     path = os.path.join(_HERE, name)
     if name == "liblinedg_b200.so" and os.environ.get("LDG_B200_LIB"):
@@ -196,6 +209,7 @@ GPU_SYMBOLS = [
     "ldg_kernel_launches", "ldg_jacobian_bytes",
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
     "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv", "ldg_steady_solve",
+    "ldg_set_boundary_function",
 ]
 
 
@@ -241,6 +255,7 @@ def gpu_lib() -> C.CDLL:
         L.ldg_rk4_step.argtypes = [vp, vp, C.c_double, C.c_double]
         L.ldg_dirk3_step.argtypes = [vp, vp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                      C.POINTER(LdgSolverStats)]
+        L.ldg_set_boundary_function.argtypes = [vp, C.c_int32, BC_FN, vp]
         L.ldg_steady_solve.argtypes = [vp, vp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
         L.ldg_write_triplets.argtypes = [vp, C.c_int, C.c_char_p]
         L.ldg_write_sparsity_csv.argtypes = [vp, C.c_int, C.c_char_p, C.c_int]

@@ -93,6 +93,15 @@ struct ldg_ctx {
   double* d_bcv = nullptr;
   int32_t* d_bck = nullptr;     // boundary kind per boundary index
   std::vector<int32_t> bck;
+  // boundary functions (ldg_set_boundary_function): boundary faces (k, ds) in
+  // processing order, their tags, end-node coordinates [face][NL][D]
+  std::vector<int32_t> bface_of, bface_tag, bc_tag;
+  std::vector<double> bface_x, bcv_host;
+  std::map<int, std::pair<ldg_bc_fn, void*>> bfun;
+  double bfun_t = 0.0;
+  bool bfun_dirty = false, has_coords = false;
+  int32_t* d_bface = nullptr;
+  double* d_bvals = nullptr;
   double* d_source = nullptr;
   ldg::DevError* h_err = nullptr;
   ldg::DevError* d_err = nullptr;
@@ -141,6 +150,8 @@ struct ldg_ctx {
     cudaFree(d_ti);
     cudaFree(d_bcv);
     cudaFree(d_bck);
+    cudaFree(d_bface);
+    cudaFree(d_bvals);
     cudaFree(d_source);
     cudaFree(d_Q);
     cudaFree(d_w);
@@ -806,6 +817,38 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
        "upload inv_order");
 
     build_connectivity(*c, *s, *ph);
+    // boundary faces (processing order) for boundary functions
+    {
+      const int F = 2 * c->D;
+      c->bface_of.assign(static_cast<size_t>(c->E) * F, -1);
+      c->has_coords = s->node_coords != nullptr;
+      for (int i = 0; i < ph->n_bc; ++i) c->bc_tag.push_back(ph->bcs[i].tag);
+      for (int i = 0; i < ph->n_bc; ++i)
+        for (int k2 = 0; k2 < c->m; ++k2) c->bcv_host.push_back(ph->bcs[i].value[k2]);
+      for (int k = 0; k < c->E; ++k)
+        for (int ds = 0; ds < F; ++ds) {
+          const int2 cx = c->conn[static_cast<size_t>(k) * F + ds];
+          if (cx.x >= 0) continue;
+          c->bface_of[static_cast<size_t>(k) * F + ds] = static_cast<int32_t>(c->bface_tag.size());
+          c->bface_tag.push_back(-1 - cx.x);  // boundary index
+          const int dir = ds >> 1, side = ds & 1, e = c->order[k];
+          for (int line = 0; line < c->NL; ++line) {
+            // own end node of the line (node_on_line): position 0 or p along dir
+            int base;
+            if (c->D == 2) base = dir == 0 ? c->np * line : line;
+            else {
+              const int t1 = dir == 0 ? 1 : 0, t2 = dir == 2 ? 1 : 2;
+              const int st[3] = {1, c->np, c->np * c->np};
+              base = (line % c->np) * st[t1] + (line / c->np) * st[t2];
+            }
+            const int stride = dir == 0 ? 1 : (dir == 1 ? c->np : c->np * c->np);
+            const int nd = base + (side ? c->p : 0) * stride;
+            for (int d = 0; d < c->D; ++d)
+              c->bface_x.push_back(c->has_coords ? s->node_coords[(static_cast<size_t>(e) * c->npe + nd) * c->D + d]
+                                                 : 0.0);
+          }
+        }
+    }
 
     // Metric in processing order, 1/J precomputed.
     const ldg::Ops& o = *c->ops;
@@ -918,25 +961,81 @@ int ldg_set_source(ldg_ctx* c, const double* S) {
   });
 }
 
-int ldg_gradient(ldg_ctx* c, const double* U, double t, double* Q) {
-  (void)t;
+namespace {
+// Boundary functions: (re)evaluate at the boundary end nodes when registered
+// data changed or t differs from the last evaluation, upload, point the
+// kernels at it (DevCtx::bface / bvals); none registered -> constant data.
+void refresh_boundary(ldg_ctx* c, double t) {
+  if (c->bfun.empty()) {
+    c->dc.bface = nullptr;
+    c->dc.bvals = nullptr;
+    return;
+  }
+  if (!c->bfun_dirty && t == c->bfun_t && c->dc.bface) return;
+  const size_t nf = c->bface_tag.size();
+  const int NL = c->NL, m = c->m, D = c->D;
+  std::vector<double> h(std::max<size_t>(1, nf * NL * m));
+  for (size_t f = 0; f < nf; ++f) {
+    const int bc = c->bface_tag[f];
+    auto it = c->bfun.find(c->bc_tag[bc]);
+    for (int line = 0; line < NL; ++line) {
+      double* out = &h[(f * NL + line) * m];
+      if (it == c->bfun.end()) {
+        for (int k = 0; k < m; ++k) out[k] = c->bcv_host[static_cast<size_t>(bc) * m + k];
+      } else {
+        it->second.first(it->second.second, &c->bface_x[(f * NL + line) * D], t, out);
+      }
+    }
+  }
+  if (!c->d_bface) {
+    ck(cudaMalloc(&c->d_bface, c->bface_of.size() * sizeof(int32_t)), "cudaMalloc bface");
+    ck(cudaMemcpy(c->d_bface, c->bface_of.data(), c->bface_of.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+       "upload bface");
+    ck(cudaMalloc(&c->d_bvals, h.size() * sizeof(double)), "cudaMalloc bvals");
+  }
+  // (stream-ordered: kernels already queued read the previous values first)
+  ck(cudaMemcpyAsync(c->d_bvals, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+     "upload boundary data");
+  ck(cudaStreamSynchronize(c->stream), "stream synchronize");  // h is a local buffer
+  c->dc.bface = c->d_bface;
+  c->dc.bvals = c->d_bvals;
+  c->bfun_t = t;
+  c->bfun_dirty = false;
+}
+}  // namespace
+
+int ldg_set_boundary_function(ldg_ctx* c, int32_t tag, ldg_bc_fn fn, void* user) {
   return guarded(c, [&]() -> int {
+    if (std::find(c->bc_tag.begin(), c->bc_tag.end(), tag) == c->bc_tag.end())
+      throw ldg_error(LDG_ERR_CONFIG, "no boundary condition with tag " + std::to_string(tag));
+    if (fn && !c->has_coords)
+      throw ldg_error(LDG_ERR_CONFIG, "boundary functions need ldg_setup.node_coords");
+    if (fn) c->bfun[tag] = {fn, user};
+    else c->bfun.erase(tag);
+    c->bfun_dirty = true;
+    return LDG_OK;
+  });
+}
+
+int ldg_gradient(ldg_ctx* c, const double* U, double t, double* Q) {
+  return guarded(c, [&]() -> int {
+    refresh_boundary(c, t);
     if (!c->second) throw ldg_error(LDG_ERR_CONFIG, "gradient_residual needs second-order physics");
     return finish(c, c->ops->gradient(c->dc, U, Q));
   });
 }
 
 int ldg_residual_uq(ldg_ctx* c, const double* U, const double* Q, double t, double* R) {
-  (void)t;
   return guarded(c, [&]() -> int {
+    refresh_boundary(c, t);
     if (!c->second) return finish(c, c->ops->residual(c->dc, U, nullptr, R));
     return finish(c, c->ops->residual(c->dc, U, Q, R));
   });
 }
 
 int ldg_residual(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
-  (void)t;
   return guarded(c, [&]() -> int {
+    refresh_boundary(c, t);
     if (!c->second) return finish(c, c->ops->residual(c->dc, U, nullptr, R));
     double* q = Q ? Q : ensure(c->d_Q, c->nQ());
     ck(c->ops->gradient(c->dc, U, q), "gradient launch");
@@ -945,8 +1044,8 @@ int ldg_residual(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
 }
 
 int ldg_jacobian_assemble(ldg_ctx* c, const double* U, double t) {
-  (void)t;
   return guarded(c, [&]() -> int {
+    refresh_boundary(c, t);
     const ldg::Ops& o = *c->ops;
     if (o.jac_smem > 227 * 1024)
       throw ldg_error(LDG_ERR_CONFIG, "Jacobian tile of this configuration exceeds shared memory (" +

@@ -34,6 +34,8 @@ struct KParams {
   const double* bcv;     // [nbc][M] boundary data (Dirichlet / far-field state, Neumann flux)
   const int32_t* bck;    // [nbc] boundary kind (BcKindDev)
   int noslip;            // number of no-slip-wall boundary conditions (K21 wall terms)
+  const int32_t* bface;  // [k][2D] boundary-face index into bvals, -1: constant data (null: none)
+  const double* bvals;   // [bface][NL][M] boundary data per line end (ldg_set_boundary_function)
   const double* source;  // reference numbering, may be null
   DevError* err;
   const int2* fpart;     // [k][2D] face partner {k', 2 dir' + side'} ({-1, 0}: none)
@@ -51,12 +53,23 @@ struct KParams {
 //     u_in + viscous F(u_in, q_in).n (no penalty);
 //   Neumann: the prescribed normal flux g_N |n| (no other term).
 // T = double or Dual<N> in u_in; TQ the type of q_in.
+// Boundary data of one line end: per-node values from a boundary function
+// (ldg_set_boundary_function: the reference's std::function g_D / g_N / far
+// state evaluated at the end node) or the boundary condition's constants.
+template <class C>
+__device__ __forceinline__ const double* bnd_g(const KParams<C>& kp, int bc, int k, int ds, int line) {
+  if (kp.bface) {
+    const int f = __ldg(kp.bface + static_cast<size_t>(k) * 2 * C::D + ds);
+    if (f >= 0) return kp.bvals + (static_cast<size_t>(f) * C::NL + line) * C::M;
+  }
+  return kp.bcv + bc * C::M;
+}
+
 template <class C, class T, class TQ>
-__device__ __forceinline__ void bnd_flux(const KParams<C>& kp, int bc, const T* ui, const TQ* qi, const double* n,
-                                         double nn, T* fh, bool& ok) {
+__device__ __forceinline__ void bnd_flux(const KParams<C>& kp, int bc, const double* g, const T* ui, const TQ* qi,
+                                         const double* n, double nn, T* fh, bool& ok) {
   constexpr int M = C::M, D = C::D;
   const int kind = __ldg(kp.bck + bc);
-  const double* g = kp.bcv + bc * M;
 #pragma unroll
   for (int c = 0; c < M; ++c) fh[c] = T(0.0);
   if (kind == BC_NEUMANN) {
@@ -102,11 +115,11 @@ __device__ __forceinline__ bool bnd_uhat_inner(const KParams<C>& kp, int bc) {
 // no-slip adiabatic wall is mixed -- zero momentum (Dirichlet
 // velocity), interior density and energy (Neumann-type, C22 = 0)
 template <class C>
-__device__ __forceinline__ double bnd_uhat(const KParams<C>& kp, int bc, int c, double uin) {
+__device__ __forceinline__ double bnd_uhat(const KParams<C>& kp, int bc, const double* g, int c, double uin) {
   const int kind = __ldg(kp.bck + bc);
   if (kind == BC_NO_SLIP) return (c == 0 || c == C::M - 1) ? uin : 0.0;
   if (kind == BC_NEUMANN || kind == BC_SLIP_WALL) return uin;
-  return __ldg(kp.bcv + bc * C::M + c);
+  return __ldg(g + c);
 }
 
 #ifndef LDG_VISC_DU  // closed-form viscous dF/du (1) or dual numbers (0)
@@ -361,7 +374,7 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
           for (int c = 0; c < MD; ++c) qo[side][c] = __ldg(Q + nd * MD + c);
         }
       } else {
-        bcp[side] = kp.bcv + (-1 - cn.x) * M;
+        bcp[side] = bnd_g(kp, -1 - cn.x, k, dir * 2 + side, line);
       }
     }
     double r[NP][M];
@@ -432,7 +445,8 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
 #pragma unroll
           for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
         }
-        bnd_flux<C>(kp, static_cast<int>(bcp[side] - kp.bcv) / M, ui, qi, n, nn, fh, ok);
+        const int2 cb = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
+        bnd_flux<C>(kp, -1 - cb.x, bcp[side], ui, qi, n, nn, fh, ok);
       } else {
       if (C::HAS_INV) {
         if (C::RI == LDG_ROE) roe_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
@@ -596,7 +610,7 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
     double n[D], ui[M], uo[M];
 #pragma unroll
     for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
-    const double* bcp = cn.x < 0 ? kp.bcv + (-1 - cn.x) * M : nullptr;
+    const double* bcp = cn.x < 0 ? bnd_g(kp, -1 - cn.x, k, dir * 2 + side, line) : nullptr;
     size_t ond = 0;
     if (!bcp) ond = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
 #pragma unroll
@@ -609,7 +623,7 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
 #pragma unroll
       for (int d = 1; d < D; ++d) nn += n[d] * n[d];
       nn = sqrt(nn);
-      bnd_flux<C>(kp, -1 - cn.x, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
+      bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
     } else {
     if (C::HAS_INV) {
       if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
@@ -895,7 +909,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
         double n[D], ui[M], uo[M], fh[M];
 #pragma unroll
         for (int d = 0; d < D; ++d) n[d] = nep[d];
-        const double* bcp = cn.x < 0 ? kp.bcv + (-1 - cn.x) * M : nullptr;
+        const double* bcp = cn.x < 0 ? bnd_g(kp, -1 - cn.x, k0 + le, dir * 2 + side, line) : nullptr;
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           ui[c] = sul[nd * M + c];
@@ -907,7 +921,7 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
 #pragma unroll
           for (int d = 1; d < D; ++d) nn += n[d] * n[d];
           nn = sqrt(nn);
-          bnd_flux<C>(kp, -1 - cn.x, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
+          bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
         } else {
         if (C::HAS_INV) {
           if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
@@ -1209,7 +1223,7 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
         double n[D], ui[M], uo[M], fh[M];
 #pragma unroll
         for (int d = 0; d < D; ++d) n[d] = nep[d];
-        const double* bcp = cn.x < 0 ? kp.bcv + (-1 - cn.x) * M : nullptr;
+        const double* bcp = cn.x < 0 ? bnd_g(kp, -1 - cn.x, k0 + le, dir * 2 + side, line) : nullptr;
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           ui[c] = sul[nd * M + c];
@@ -1221,7 +1235,7 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
 #pragma unroll
             for (int d = 1; d < D; ++d) nn += n[d] * n[d];
             nn = sqrt(nn);
-            bnd_flux<C>(kp, -1 - cn.x, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
+            bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
           } else {
           if (C::HAS_INV) {
           if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
@@ -1417,7 +1431,7 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
         const int2 cn = io.bCONN(cur)[(l * D + dir) * 2 + side];
         double uh;
         if (cn.x < 0)  // boundary: g_D, the interior trace, or mixed (no-slip wall)
-          uh = bnd_uhat(kp, -1 - cn.x, c, ul[side ? P : 0]);
+          uh = bnd_uhat(kp, -1 - cn.x, bnd_g(kp, -1 - cn.x, k0 + l, dir * 2 + side, line), c, ul[side ? P : 0]);
         else if (conn_sign(cn.y) > 0)
           uh = ul[side ? P : 0];  // S = +1
         else uh = io.bNB(cur)[((lw << 1) | side) * M + c];
@@ -1515,7 +1529,8 @@ k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict
       if (cn.x < 0) {  // boundary: g_D, the interior trace, or mixed (no-slip wall)
         const int nd = node_on_line<C>(dir, line, ie);
 #pragma unroll
-        for (int c = 0; c < M; ++c) uh[c] = bnd_uhat(kp, -1 - cn.x, c, sul[nd * M + c]);
+        for (int c = 0; c < M; ++c)
+          uh[c] = bnd_uhat(kp, -1 - cn.x, bnd_g(kp, -1 - cn.x, k, dir * 2 + side, line), c, sul[nd * M + c]);
       } else if (conn_sign(cn.y) > 0) {  // S = +1
         const int nd = node_on_line<C>(dir, line, ie);
 #pragma unroll
@@ -1732,7 +1747,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 #pragma unroll
   for (int d = 1; d < D; ++d) nn += n[d] * n[d];
   nn = sqrt(nn);
-  const double* bcp = bd ? kp.bcv + (-1 - cn.x) * M : nullptr;
+  const double* bcp = bd ? bnd_g(kp, -1 - cn.x, k, ds, line) : nullptr;
   const size_t own = e * NPE + nd;
   const size_t onb = bd ? 0 : static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
   double uiv[M], uov[M];

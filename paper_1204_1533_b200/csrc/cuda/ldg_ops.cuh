@@ -27,6 +27,8 @@ struct DevCtx {
   const double* bcv = nullptr;
   const int32_t* bck = nullptr;
   int noslip = 0;
+  const int32_t* bface = nullptr;  // per-line-end boundary data (ldg_set_boundary_function)
+  const double* bvals = nullptr;
   const double* source = nullptr;
   DevError* err = nullptr;
   // face sharing of the endpoint flux Jacobians (null = every line end computes its own)
@@ -80,6 +82,8 @@ struct Launch {
     kp.bcv = d.bcv;
     kp.bck = d.bck;
     kp.noslip = d.noslip;
+    kp.bface = d.bface;
+    kp.bvals = d.bvals;
     kp.source = d.source;
     kp.err = d.err;
     kp.fpart = d.fpart;

@@ -149,6 +149,21 @@ class LineDG:
     def jacobian_bytes(self) -> int:
         return int(self.lib.ldg_jacobian_bytes(self._h))
 
+    def set_boundary_function(self, tag: int, fn):
+        """Space/time-dependent boundary data for the condition on `tag`
+        (the reference's std::function data, physics.hpp:20-31):
+        fn(x, t) -> m values at the boundary end node x; None restores the
+        constant ldg_bc values."""
+        if not hasattr(self, "_bc_cbs"):
+            self._bc_cbs = {}
+        if fn is None:
+            self._bc_cbs.pop(tag, None)
+            self._check(self.lib.ldg_set_boundary_function(self._h, tag, _abi.BC_FN(), None))
+            return
+        cb = _abi.make_bc_fn(fn, self.dim, self.m)
+        self._bc_cbs[tag] = cb  # keep the ctypes callback alive
+        self._check(self.lib.ldg_set_boundary_function(self._h, tag, cb, None))
+
     def set_source(self, S: Optional[np.ndarray]):
         a = None if S is None else np.ascontiguousarray(S, dtype=np.float64)
         self._check(self.lib.ldg_set_source(self._h, dptr(a)))
