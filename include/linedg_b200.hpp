@@ -11,10 +11,15 @@
 //
 // Errors are rethrown as the reference's exception types (errors.hpp:10-28).
 // Physics crosses as a descriptor (ldg_physics), not a PhysicsModel&:
-// virtual per-point callbacks and std::function boundary data cannot run on
-// the device; constant Dirichlet states per tag are supported.
+// virtual per-point callbacks cannot run on the device.  Boundary data: the
+// constant ldg_bc values per tag, or a BoundaryCondition-style
+// std::function(x, t, out) per tag (set_boundary_function), evaluated on the
+// host at the boundary end nodes.
 #pragma once
 
+#include <functional>
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -156,6 +161,20 @@ class Context {
   // of I - alpha_dt A~ on the device (after assemble_jacobians).
   void build_preconditioner(double alpha_dt) { check(ldg_precond_build(ctx_, alpha_dt), ctx_); }
 
+  // Position/time-dependent boundary data for the condition on `tag`, with the
+  // signature of BoundaryCondition::dirichlet / ::neumann (physics.hpp:22-23).
+  using BoundaryFn = std::function<void(const Eigen::Vector2d&, double, double*)>;
+  void set_boundary_function(int tag, BoundaryFn g) {
+    if (!g) {
+      check(ldg_set_boundary_function(ctx_, tag, nullptr, nullptr), ctx_);
+      bfns_.erase(tag);
+      return;
+    }
+    auto holder = std::make_unique<BoundaryFn>(std::move(g));
+    check(ldg_set_boundary_function(ctx_, tag, &Context::boundary_trampoline, holder.get()), ctx_);
+    bfns_[tag] = std::move(holder);
+  }
+
   // gmres(split_matvec, precond, b, rtol, maxit, restart):
   // right-preconditioned GMRES on (I - alpha_dt (K11 + K12 K21)) x = b, x0 = 0.
   struct GmresResult {
@@ -208,6 +227,10 @@ class Context {
   }
 
  private:
+  static void boundary_trampoline(void* user, const double* x, double t, double* out) {
+    (*static_cast<BoundaryFn*>(user))(Eigen::Vector2d(x[0], x[1]), t, out);
+  }
+  std::map<int, std::unique_ptr<BoundaryFn>> bfns_;
   static void check(int status, const ldg_ctx* c) {
     if (status == LDG_OK) return;
     const std::string msg = ldg_last_error(c);
