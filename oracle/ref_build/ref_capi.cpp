@@ -123,6 +123,35 @@ int ref_case_remap(void* h, void (*fn)(void*, const double*, int, double*), void
   }
 }
 
+// The reference's own refine_uniform (mesh.cpp:168-213) of a case's mesh.
+void* ref_case_refine(void* h) {
+  try {
+    auto* src = static_cast<RefCase*>(h);
+    auto* c = new RefCase;
+    c->b = src->b;
+    c->m = refine_uniform(src->m);
+    c->sw = assign_switches(c->m);
+    c->maps = compute_mapping(c->m, c->b);
+    return c;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+int ref_case_num_vertices(void* h) { return static_cast<int>(static_cast<RefCase*>(h)->m.vertices.size()); }
+void ref_case_vertices(void* h, double* out) {
+  const auto& v = static_cast<RefCase*>(h)->m.vertices;
+  for (size_t i = 0; i < v.size(); ++i) {
+    out[2 * i] = v[i].x();
+    out[2 * i + 1] = v[i].y();
+  }
+}
+void ref_case_elements(void* h, int* out) {
+  const auto& q = static_cast<RefCase*>(h)->m.elems;
+  for (size_t e = 0; e < q.size(); ++e)
+    for (int k = 0; k < 4; ++k) out[4 * e + k] = q[e][k];
+}
+
 void ref_case_free(void* h) { delete static_cast<RefCase*>(h); }
 int ref_case_num_faces(void* h) { return static_cast<RefCase*>(h)->m.num_faces(); }
 

@@ -143,6 +143,7 @@ def host_lib() -> C.CDLL:
         L.lh_case_load_mesh.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _ip, _dp,
                                         C.POINTER(C.c_void_p)]
         L.lh_case_save_mesh.argtypes = [C.c_void_p, C.c_char_p]
+        L.lh_case_refine.argtypes = [C.c_void_p, C.c_int32, _ip, _dp, C.POINTER(C.c_void_p)]
         L.lh_case_remap.argtypes = [C.c_void_p, CURVE_FN, C.c_void_p]
         L.lh_case_remap_circles.argtypes = [C.c_void_p, C.c_int32, _ip, _dp, _dp, _dp]
         L.lh_case_setup.argtypes = [C.c_void_p]

@@ -125,6 +125,19 @@ class Case:
             raise _setup_error(st)
         return cls(h.value)
 
+    def refine(self, periodic=()) -> "Case":
+        """Uniformly refined case (refine_uniform, mesh.cpp:168-213: each quad
+        split into four), same basis, then optional periodic pairs."""
+        pt = np.ascontiguousarray(np.asarray([t for t, _ in periodic], dtype=np.int32).reshape(-1, 2))
+        ptr = np.zeros((len(periodic), 3))
+        for i, (_, tr) in enumerate(periodic):
+            ptr[i, :len(tr)] = tr
+        h = C.c_void_p()
+        st = self._lib.lh_case_refine(self._h, len(periodic), _abi.iptr(pt), dptr(ptr), C.byref(h))
+        if st != 0:
+            raise _setup_error(st)
+        return Case(h.value)
+
     def save_mesh(self, path: str):
         """Write the mesh in the reference text format (save_mesh, mesh.cpp:148-160)."""
         st = self._lib.lh_case_save_mesh(self._h, os.fsencode(path))

@@ -235,6 +235,26 @@ int lh_case_remap_circles(lh_case* c, int32_t n, const int32_t* tags, const doub
   return lh_case_remap(c, circle_proj, &cs);
 }
 
+// Uniformly refined copy of a case's mesh (refine_uniform, mesh.cpp:168-213),
+// same basis, then optional periodic pairs.  tag_lines: the refined boundary.
+int lh_case_refine(const lh_case* src, int32_t nper, const int32_t* per_tags, const double* per_tr,
+                   lh_case** out) {
+  try {
+    auto c = std::make_unique<lh_case>();
+    c->basis = src->basis;
+    c->mesh = refine_uniform(src->mesh);
+    for (const Face& f : c->mesh.faces)
+      if (f.boundary()) c->tag_lines.insert(c->tag_lines.end(), {f.elem_l, f.face_l, f.tag});
+    for (int k = 0; k < nper; ++k)
+      make_periodic(c->mesh, per_tags[2 * k], per_tags[2 * k + 1], per_tr + 3 * k);
+    finish_case(c.get());
+    *out = c.release();
+    return LDG_OK;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
 void lh_case_free(lh_case* c) { delete c; }
 int32_t lh_case_num_tag_lines(const lh_case* c) { return static_cast<int32_t>(c->tag_lines.size() / 3); }
 void lh_case_tag_lines(const lh_case* c, int32_t* out) {

@@ -7,6 +7,7 @@
 #include "linedg_host.hpp"
 
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <numeric>
 #include <unordered_map>
@@ -1021,6 +1022,59 @@ Mesh make_lattice_mesh(const LatticeSpec& s, std::vector<int>* tag_lines) {
     }
   }
   return m;
+}
+
+// ------------------------------------------------------------ refinement
+// refine_uniform (mesh.cpp:168-213): every quad split into four at its edge
+// midpoints and centroid; boundary-edge midpoints are created first (face
+// order), then per element m01, m12, m23, m30 (shared through an edge map) and
+// the centroid; children keep their parent edge's boundary tag.  2-D.
+Mesh refine_uniform(const Mesh& mesh) {
+  if (mesh.dim != 2) throw config_error("mesh: uniform refinement is 2-D only");
+  Mesh out;
+  out.dim = 2;
+  out.verts = mesh.verts;
+  std::map<std::pair<int, int>, int> edge_mid;
+  auto midpoint = [&](int a, int b) {
+    const auto key = std::make_pair(std::min(a, b), std::max(a, b));
+    auto it = edge_mid.find(key);
+    if (it != edge_mid.end()) return it->second;
+    const int id = out.nv();
+    for (int k = 0; k < 2; ++k) out.verts.push_back(0.5 * (mesh.verts[2 * a + k] + mesh.verts[2 * b + k]));
+    edge_mid.emplace(key, id);
+    return id;
+  };
+  std::map<std::pair<int, int>, int> child_edge_tag;
+  for (const Face& f : mesh.faces) {
+    if (!f.boundary()) continue;
+    const int va = mesh.elems[4 * f.elem_l + f.face_l];
+    const int vb = mesh.elems[4 * f.elem_l + (f.face_l + 1) % 4];
+    const int m = midpoint(va, vb);
+    child_edge_tag[{std::min(va, m), std::max(va, m)}] = f.tag;
+    child_edge_tag[{std::min(m, vb), std::max(m, vb)}] = f.tag;
+  }
+  for (int e = 0; e < mesh.ne(); ++e) {
+    const int* q = &mesh.elems[4 * e];
+    const int m01 = midpoint(q[0], q[1]);
+    const int m12 = midpoint(q[1], q[2]);
+    const int m23 = midpoint(q[2], q[3]);
+    const int m30 = midpoint(q[3], q[0]);
+    const int c = out.nv();
+    for (int k = 0; k < 2; ++k)
+      out.verts.push_back(0.25 * (mesh.verts[2 * q[0] + k] + mesh.verts[2 * q[1] + k] + mesh.verts[2 * q[2] + k] +
+                                  mesh.verts[2 * q[3] + k]));
+    const int kids[4][4] = {{q[0], m01, c, m30}, {m01, q[1], m12, c}, {c, m12, q[2], m23}, {m30, c, m23, q[3]}};
+    for (const auto& kq : kids) out.elems.insert(out.elems.end(), kq, kq + 4);
+  }
+  build_faces(out);
+  for (Face& f : out.faces) {
+    if (!f.boundary()) continue;
+    const int va = out.elems[4 * f.elem_l + f.face_l];
+    const int vb = out.elems[4 * f.elem_l + (f.face_l + 1) % 4];
+    auto it = child_edge_tag.find({std::min(va, vb), std::max(va, vb)});
+    if (it != child_edge_tag.end()) f.tag = it->second;
+  }
+  return out;
 }
 
 // ------------------------------------------------------------- mesh text I/O

@@ -128,6 +128,9 @@ struct LatticeSpec {
 // reference mesh file would carry them, recorded before periodic pairing.
 Mesh make_lattice_mesh(const LatticeSpec& s, std::vector<int>* tag_lines = nullptr);
 
+// refine_uniform (mesh.cpp:168-213), 2-D.
+Mesh refine_uniform(const Mesh& mesh);
+
 // Reference mesh text format (mesh.cpp:115-166), 2-D.
 Mesh load_mesh(std::istream& in);
 Mesh load_mesh(const std::string& path);

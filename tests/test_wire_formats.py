@@ -219,3 +219,54 @@ def test_gpu_triplets_need_an_assembled_jacobian(tmp_path):
         gpu.write_triplets(LDG_K11, str(tmp_path / "x.txt"))
     with pytest.raises(ValueError):
         gpu.write_sparsity_csv(LDG_K12, str(tmp_path / "x.csv"))
+
+
+@pytest.mark.parametrize("spec", MESHES[:2], ids=["n5p3", "n6p4"])
+def test_refine_uniform_matches_reference(tmp_path, spec):
+    """refine_uniform (mesh.cpp:168-213; element count x4 per
+    refinement, tags inherited): vertices bitwise, elements, faces, switches
+    and mapping equal to the reference's own implementation; twice -> x16."""
+    ref = _ref()
+    if not hasattr(ref, "ref_case_refine"):
+        pytest.skip("oracle/_ref predates the refinement wrapper")
+    vp, ip, dp = C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_double)
+    ref.ref_case_refine.argtypes = [vp]
+    ref.ref_case_refine.restype = vp
+    ref.ref_case_num_vertices.argtypes = [vp]
+    ref.ref_case_vertices.argtypes = [vp, dp]
+    ref.ref_case_elements.argtypes = [vp, ip]
+    n, p, _, jit, perm, rot, length = spec
+    src = Case.lattice(2, n, p, (*length, 1.0), jit, False, False, perm, rot, seeds=(31, 32, 33))
+    path = tmp_path / "in.mesh"
+    src.save_mesh(str(path))
+    ours0 = Case.load_mesh(str(path), p)
+    h0 = _ref_load(ref, p, str(path))
+    assert h0, ref.ref_last_error()
+    try:
+        ours, h = ours0, h0
+        for level in (1, 2):
+            ours = ours.refine()
+            h2 = ref.ref_case_refine(h)
+            assert h2, ref.ref_last_error()
+            if h is not h0:
+                ref.ref_case_free(h)
+            h = h2
+            assert ours.E == src.E * 4 ** level
+            nv = ref.ref_case_num_vertices(h)
+            rv = np.zeros(2 * nv)
+            ref.ref_case_vertices(h, rv.ctypes.data_as(dp))
+            assert np.array_equal(rv.reshape(nv, 2), ours.vertices())
+            re_ = np.zeros(4 * ours.E, dtype=np.int32)
+            ref.ref_case_elements(h, re_.ctypes.data_as(ip))
+            assert np.array_equal(re_.reshape(-1, 4), ours.elements())
+            nf = ref.ref_case_num_faces(h)
+            rf = np.zeros(nf * 6, dtype=np.int32)
+            ref.ref_case_faces(h, rf.ctypes.data_as(ip))
+            assert np.array_equal(rf.reshape(nf, 6), ours.faces())
+            sw = np.zeros(ours.E * 2, dtype=np.int8)
+            ref.ref_case_switches(h, sw.ctypes.data_as(C.POINTER(C.c_int8)))
+            assert np.array_equal(sw.reshape(ours.E, 2), ours.switches())
+        if h is not h0:
+            ref.ref_case_free(h)
+    finally:
+        ref.ref_case_free(h0)
