@@ -66,7 +66,14 @@ struct Ops {
 
 template <class C>
 struct Launch {
-  static constexpr int EPB = 128 / C::LPE > 0 ? 128 / C::LPE : 1;
+#ifndef LDG_RES_LINES  // line threads per residual CTA (EPB = elements per batch)
+  // measured: 64 for 2-D (C2 residual 35.9 -> 34.5 us: smaller batches, more
+  // CTAs per SM), 128 for 3-D (C4: 64 is 1.6 % slower)
+  static constexpr int RES_LINES = C::D == 2 ? 64 : 128;
+#else
+  static constexpr int RES_LINES = LDG_RES_LINES;
+#endif
+  static constexpr int EPB = RES_LINES / C::LPE > 0 ? RES_LINES / C::LPE : 1;
   static constexpr int RTHREADS = (EPB * C::LPE + 31) / 32 * 32;
 
   static KParams<C> params(const DevCtx& d) {
