@@ -1162,10 +1162,13 @@ struct ResF {
     return IO::bytes_per_elem() + 8LL * (C::LPE * C::NQ * C::M + C::LPE * 2 * C::M);
   }
 };
+#ifndef LDG_RESF_BUDGET_KB  // shared-memory budget per CTA of the flux-parallel residual / gradient
+#define LDG_RESF_BUDGET_KB 110  // measured (C3): 72 KB +40 us, 55 KB +96 us
+#endif
 template <class C>
 struct ResFEpb {
   static constexpr long long per = ResF<C, 1>::bytes_per_elem();
-  static constexpr int raw = static_cast<int>((110LL * 1024) / per);
+  static constexpr int raw = static_cast<int>((LDG_RESF_BUDGET_KB * 1024LL) / per);
   static constexpr int value = raw < 1 ? 1 : (raw > 8 ? 8 : raw);
 };
 
@@ -1360,7 +1363,7 @@ struct GradF {
 template <class C>
 struct GradFEpb {
   static constexpr long long per = GradF<C, 1>::bytes_per_elem();
-  static constexpr int raw = static_cast<int>((110LL * 1024) / per);
+  static constexpr int raw = static_cast<int>((LDG_RESF_BUDGET_KB * 1024LL) / per);
   static constexpr int value = raw < 1 ? 1 : (raw > 8 ? 8 : raw);
 };
 
@@ -2510,7 +2513,10 @@ struct JacP {
   static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + WORK2 + STG); }
   // prefetch ring depth: 3 for the pipelined 2-D tile and the one-CTA-per-SM
   // 3-D element units (when it fits), 2 where several CTAs share an SM
-  static constexpr int NBUF = ((PIPE || JacThreads<C>::big) && bytes(3) <= 200 * 1024) ? 3 : 2;
+#ifndef LDG_JAC_NBUF3  // 3-deep input ring for every persistent assembly that fits (knob)
+#define LDG_JAC_NBUF3 0  // measured (C2): -0.9 us, within noise: off
+#endif
+  static constexpr int NBUF = ((PIPE || JacThreads<C>::big || LDG_JAC_NBUF3) && bytes(3) <= 200 * 1024) ? 3 : 2;
   static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + WORK2 + STG;  // 4 doubles hold up to 3 mbarriers
   static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
                              (EndJac<C>::PER_ELEM % 2 == 0) && bytes(2) <= 200 * 1024;
