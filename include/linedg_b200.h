@@ -207,6 +207,11 @@ int ldg_split_matvec(ldg_ctx* ctx, double alpha_dt, const double* v, double* y);
    3-D p = 1); LDG_ERR_CONFIG beyond, LDG_ERR_SOLVER for a singular block.
    Replaces build_preconditioner(blocks, alpha_dt). */
 int ldg_precond_build(ldg_ctx* ctx, double alpha_dt);
+/* Block-Jacobi mode: 0 (default) LU factors + triangular solves per apply;
+   1 the build also forms the explicit block inverses (build ~4x slower, apply
+   ~2x faster: a dense block matvec at HBM rate) -- pays off when one build
+   serves many applications.  Invalidates a built preconditioner. */
+int ldg_set_precond_mode(ldg_ctx* ctx, int mode);
 /* z = (I - alpha_dt A~)^-1 r, device vectors (reference numbering). */
 int ldg_precond_apply(ldg_ctx* ctx, const double* r, double* z);
 int ldg_precond_apply_host(ldg_ctx* ctx, const double* r, double* z);

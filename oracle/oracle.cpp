@@ -84,6 +84,7 @@ struct Ctx {
   std::vector<double> pcLU;
   std::vector<int32_t> pcPiv;
   bool pc_built = false;
+  int pc_inverse = 0;  // 0 LU solves, 1 explicit block inverse (ldg_set_precond_mode)
   double pc_adt = 0.0;
   std::string err;
   std::vector<double> err_state;
@@ -1405,6 +1406,25 @@ int lo_precond_build(lo_ctx* x, double adt) {
           for (int j = kk + 1; j < ne; ++j) Me[i * ne + j] -= l * Me[kk * ne + j];
         }
       }
+      if (bad.load() >= 0 || !c.pc_inverse) continue;
+      // explicit block inverse X = U^-1 L^-1 P (as the device build: per
+      // column the operation order of a forward / back substitution of P e_j);
+      // the apply is then a dense block matvec
+      std::vector<int> perm(ne);
+      for (int i = 0; i < ne; ++i) perm[i] = i;
+      for (int kk = 0; kk < ne; ++kk) std::swap(perm[kk], perm[piv[kk]]);
+      std::vector<double> X(static_cast<size_t>(ne) * ne);
+      for (int i = 0; i < ne; ++i)
+        for (int j = 0; j < ne; ++j) X[i * ne + j] = perm[i] == j ? 1.0 : 0.0;
+      for (int kk = 0; kk < ne - 1; ++kk)
+        for (int i = kk + 1; i < ne; ++i)
+          for (int j = 0; j < ne; ++j) X[i * ne + j] -= Me[i * ne + kk] * X[kk * ne + j];
+      for (int kk = ne - 1; kk >= 0; --kk) {
+        for (int j = 0; j < ne; ++j) X[kk * ne + j] = X[kk * ne + j] / Me[kk * ne + kk];
+        for (int i = 0; i < kk; ++i)
+          for (int j = 0; j < ne; ++j) X[i * ne + j] -= Me[i * ne + kk] * X[kk * ne + j];
+      }
+      std::copy(X.begin(), X.end(), Me);
     }
     if (bad.load() >= 0)
       throw std::runtime_error("oracle: singular preconditioner block at element " + std::to_string(bad.load()));
@@ -1422,6 +1442,14 @@ void pc_apply(const Ctx& c, const double* r, double* z) {
     const int32_t* piv = &c.pcPiv[static_cast<size_t>(e) * ne];
     double* ze = z + static_cast<size_t>(e) * ne;
     const double* re = r + static_cast<size_t>(e) * ne;
+    if (c.pc_inverse) {
+      for (int i = 0; i < ne; ++i) {  // explicit inverse (lo_precond_build)
+        double s = 0.0;
+        for (int j = 0; j < ne; ++j) s += LU[i * ne + j] * re[j];
+        ze[i] = s;
+      }
+      continue;
+    }
     for (int i = 0; i < ne; ++i) ze[i] = re[i];
     for (int i = 0; i < ne; ++i) std::swap(ze[i], ze[piv[i]]);
     for (int i = 0; i < ne; ++i) {
@@ -1452,6 +1480,14 @@ double dotv(const double* a, const double* b, size_t n) {
   return s;
 }
 }  // namespace
+
+int lo_set_precond_mode(lo_ctx* x, int32_t mode) {
+  return guarded([&] {
+    if (mode != 0 && mode != 1) throw std::invalid_argument("oracle: precond mode");
+    x->c.pc_inverse = mode;
+    x->c.pc_built = false;
+  });
+}
 
 int lo_precond_apply(const lo_ctx* x, const double* r, double* z) {
   return guarded([&] {

@@ -64,6 +64,7 @@ def lib():
         from paper_1204_1533_b200._abi import BC_FN
         L.lo_set_boundary_function.argtypes = [vp, C.c_int32, BC_FN, vp]
         L.lo_precond_build.argtypes = [vp, C.c_double]
+        L.lo_set_precond_mode.argtypes = [vp, C.c_int32]
         L.lo_precond_apply.argtypes = [vp, _dp, _dp]
         L.lo_gmres.argtypes = [vp, C.c_double, _dp, C.c_double, C.c_int32, C.c_int32, C.c_int32, _dp,
                                C.POINTER(C.c_int32), C.POINTER(C.c_int32), _dp]
@@ -236,6 +237,9 @@ class Oracle:
         y = np.zeros(self.n_dofs)
         self._check(self.L.lo_split_matvec(self.h, adt, _d(v), _d(y)))
         return y
+
+    def set_precond_mode(self, mode):
+        self._check(self.L.lo_set_precond_mode(self.h, mode))
 
     def precond_build(self, adt):
         self._check(self.L.lo_precond_build(self.h, adt))

@@ -210,7 +210,7 @@ GPU_SYMBOLS = [
     "ldg_kernel_launches", "ldg_jacobian_bytes",
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
     "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv", "ldg_steady_solve",
-    "ldg_set_boundary_function",
+    "ldg_set_boundary_function", "ldg_set_precond_mode",
 ]
 
 
@@ -256,6 +256,7 @@ def gpu_lib() -> C.CDLL:
         L.ldg_rk4_step.argtypes = [vp, vp, C.c_double, C.c_double]
         L.ldg_dirk3_step.argtypes = [vp, vp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                      C.POINTER(LdgSolverStats)]
+        L.ldg_set_precond_mode.argtypes = [vp, C.c_int]
         L.ldg_set_boundary_function.argtypes = [vp, C.c_int32, BC_FN, vp]
         L.ldg_steady_solve.argtypes = [vp, vp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
         L.ldg_write_triplets.argtypes = [vp, C.c_int, C.c_char_p]

@@ -1338,6 +1338,15 @@ int ldg_precond_build(ldg_ctx* c, double alpha_dt) {
   });
 }
 
+int ldg_set_precond_mode(ldg_ctx* c, int mode) {
+  return guarded(c, [&]() -> int {
+    if (mode != 0 && mode != 1) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "precond mode must be 0 (LU) or 1 (inverse)");
+    c->dc.pc_inverse = mode;
+    c->pc_valid = false;
+    return LDG_OK;
+  });
+}
+
 int ldg_precond_apply(ldg_ctx* c, const double* r, double* z) {
   return guarded(c, [&]() -> int {
     if (!c->pc_valid) throw ldg_error(LDG_ERR_SOLVER, "preconditioner not built");

@@ -3231,13 +3231,19 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
 // I - alpha_dt A~ is gathered from the block-row store into shared memory,
 // LU-factorised with partial pivoting (the oracle's pivot rule: the first
 // largest |a_ik|), and written column-major with its pivots.
-template <class C>
+// INV (runtime mode ldg_set_precond_mode): the build also forms the explicit
+// block inverse from the LU factors, so the apply is a dense, dependency-free
+// block matvec streaming the factors at HBM rate instead of 2 NE dependent
+// solve steps (measured C2: apply 0.49 -> 0.22 ms, build 11 -> 43 ms).
+template <class C, bool INV_ = false>
 struct PcCfg {
   static constexpr int NE = C::NPE * C::M;  // unknowns per element
   static constexpr int LDM = NE | 1;        // odd row stride (shared-memory banks)
   static constexpr bool OK = NE <= 128;
+  static constexpr bool INV = INV_;
+  static constexpr int LDX = NE | 1;        // inverse columns in shared memory (odd stride)
   static constexpr int THREADS = 256;
-  static constexpr size_t smem() { return sizeof(double) * NE * LDM; }
+  static constexpr size_t smem() { return sizeof(double) * (NE * LDM + (INV ? NE * LDX : 0)) + sizeof(int) * NE; }
 };
 
 template <class C>
@@ -3252,16 +3258,17 @@ __device__ __forceinline__ bool pc_on_line(int a, int b) {
   return same >= C::D - 1;
 }
 
-template <class C>
+template <class C, bool INV>
 __global__ void __launch_bounds__(PcCfg<C>::THREADS)
 k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __restrict__ K12,
            const double* __restrict__ K21, double adt, double* __restrict__ LUc, int32_t* __restrict__ piv,
            int* __restrict__ bad) {
-  using PC = PcCfg<C>;
+  using PC = PcCfg<C, INV>;
   constexpr int NE = PC::NE, LDM = PC::LDM, M = C::M, NPE = C::NPE, NT = C::NT, D = C::D, MD = C::MD,
                 NS11 = C::NS11, NS12 = C::NS12, R12 = C::R12, NSIN = C::D * C::P + 1;
   constexpr int A0 = C::PH == PH_NS ? 1 : 0;
   extern __shared__ __align__(16) double Ms[];
+  int* const spv = reinterpret_cast<int*>(Ms + NE * LDM + (PC::INV ? NE * PC::LDX : 0));  // pivot sequence
   __shared__ int spiv;
   __shared__ int sbad;
   const int k = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
@@ -3351,6 +3358,7 @@ k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __
       if (tid == 0) {
         spiv = bi;
         piv[static_cast<size_t>(k) * NE + kk] = bi;
+        spv[kk] = bi;
         if (!(best > 0.0)) sbad = 1;
       }
     }
@@ -3375,6 +3383,50 @@ k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __
   }
   if (tid == 0 && sbad) atomicCAS(bad, -1, static_cast<int>(e));
   double* out = LUc + static_cast<size_t>(k) * NE * NE;
+  if (PC::INV) {
+    // X = A^-1 from P A = L U: X = U^-1 L^-1 P, all columns at once (row-major
+    // X[i][j]); per column the operation order is that of a forward / back
+    // substitution of P e_j (the oracle's lo_precond_build does the same)
+    double* X = Ms + NE * LDM;
+    __shared__ int sperm[128];
+    if (tid == 0) {
+      for (int i = 0; i < NE; ++i) sperm[i] = i;
+      for (int kk = 0; kk < NE; ++kk) {
+        const int p = spv[kk];
+        const int t = sperm[kk];
+        sperm[kk] = sperm[p];
+        sperm[p] = t;
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < NE * NE; x += nthr) {
+      const int i = x / NE, j = x - i * NE;
+      X[i * PC::LDX + j] = sperm[i] == j ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < NE - 1; ++kk) {  // unit lower
+      const int rem = NE - kk - 1;
+      for (int x = tid; x < rem * NE; x += nthr) {
+        const int i = kk + 1 + x / NE, j = x % NE;
+        X[i * PC::LDX + j] -= Ms[i * LDM + kk] * X[kk * PC::LDX + j];
+      }
+      __syncthreads();
+    }
+    for (int kk = NE - 1; kk >= 0; --kk) {  // upper
+      for (int j = tid; j < NE; j += nthr) X[kk * PC::LDX + j] = X[kk * PC::LDX + j] / Ms[kk * LDM + kk];
+      __syncthreads();
+      for (int x = tid; x < kk * NE; x += nthr) {
+        const int i = x / NE, j = x % NE;
+        X[i * PC::LDX + j] -= Ms[i * LDM + kk] * X[kk * PC::LDX + j];
+      }
+      __syncthreads();
+    }
+    for (int x = tid; x < NE * NE; x += nthr) {
+      const int j = x / NE, i = x - j * NE;
+      out[x] = X[i * PC::LDX + j];  // column-major inverse
+    }
+    return;
+  }
   for (int x = tid; x < NE * NE; x += nthr) {
     const int j = x / NE, i = x - j * NE;
     out[x] = Ms[i * LDM + j];  // column-major
@@ -3384,11 +3436,11 @@ k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __
 // z = (I - alpha_dt A~)^-1 r, one warp per element: row interchanges, then
 // column-oriented unit-lower and upper triangular solves on coalesced column
 // loads of the element's LU factors.
-template <class C>
+template <class C, bool INV>
 __global__ void __launch_bounds__(128)
 k_pc_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* __restrict__ piv,
            const double* __restrict__ r, double* __restrict__ z) {
-  using PC = PcCfg<C>;
+  using PC = PcCfg<C, INV>;
   constexpr int NE = PC::NE;
   __shared__ double zs[4][NE];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -3399,6 +3451,29 @@ k_pc_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* _
   const double* re = r + e * NE;
   for (int i = lane; i < NE; i += 32) zw[i] = re[i];
   __syncwarp();
+  if (PC::INV) {
+    // z = A^-1 r: lanes over rows, columns streamed (coalesced column loads)
+    constexpr int RPL = (NE + 31) / 32;
+    double acc[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) acc[q] = 0.0;
+    const double* Xc = LUc + static_cast<size_t>(k) * NE * NE;
+    for (int j = 0; j < NE; ++j) {
+      const double rj = zw[j];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q;
+        if (i < NE) acc[q] += __ldcs(Xc + j * NE + i) * rj;
+      }
+    }
+    double* ze = z + e * NE;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q;
+      if (i < NE) ze[i] = acc[q];
+    }
+    return;
+  }
   if (lane == 0) {
     const int32_t* pv = piv + static_cast<size_t>(k) * NE;
     for (int i = 0; i < NE; ++i) {

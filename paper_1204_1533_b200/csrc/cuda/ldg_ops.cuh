@@ -29,6 +29,7 @@ struct DevCtx {
   int noslip = 0;
   const int32_t* bface = nullptr;  // per-line-end boundary data (ldg_set_boundary_function)
   const double* bvals = nullptr;
+  int pc_inverse = 0;  // block-Jacobi mode: 0 LU solves, 1 explicit block inverse
   const double* source = nullptr;
   DevError* err = nullptr;
   // face sharing of the endpoint flux Jacobians (null = every line end computes its own)
@@ -365,22 +366,29 @@ struct Launch {
     return cudaGetLastError();
   }
 
+  template <bool INV>
+  static void pc_build_t(const DevCtx& d, const double* V11, const double* V12, const double* V21, double adt,
+                         double* LUc, int32_t* piv, int* bad) {
+    using PC = PcCfg<C, INV>;
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_pc_build<C, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::smem());
+      init = true;
+    }
+    k_pc_build<C, INV><<<d.E, PC::THREADS, PC::smem(), d.stream>>>(params(d), V11, V12, V21, adt, LUc, piv, bad);
+  }
   static cudaError_t pc_build(const DevCtx& d, const double* V11, const double* V12, const double* V21, double adt,
                               double* LUc, int32_t* piv, int* bad) {
     if (!PcCfg<C>::OK) return cudaErrorNotSupported;
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_pc_build<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PcCfg<C>::smem());
-      init = true;
-    }
-    k_pc_build<C><<<d.E, PcCfg<C>::THREADS, PcCfg<C>::smem(), d.stream>>>(params(d), V11, V12, V21, adt, LUc, piv,
-                                                                         bad);
+    if (d.pc_inverse) pc_build_t<true>(d, V11, V12, V21, adt, LUc, piv, bad);
+    else pc_build_t<false>(d, V11, V12, V21, adt, LUc, piv, bad);
     count(d);
     return cudaGetLastError();
   }
   static cudaError_t pc_apply(const DevCtx& d, const double* LUc, const int32_t* piv, const double* r, double* z) {
     if (!PcCfg<C>::OK) return cudaErrorNotSupported;
-    k_pc_apply<C><<<(d.E + 3) / 4, 128, 0, d.stream>>>(params(d), LUc, piv, r, z);
+    if (d.pc_inverse) k_pc_apply<C, true><<<(d.E + 3) / 4, 128, 0, d.stream>>>(params(d), LUc, piv, r, z);
+    else k_pc_apply<C, false><<<(d.E + 3) / 4, 128, 0, d.stream>>>(params(d), LUc, piv, r, z);
     count(d);
     return cudaGetLastError();
   }

@@ -270,6 +270,10 @@ class LineDG:
         return y
 
     # ------------------------------------------------- preconditioned GMRES
+    def set_precond_mode(self, mode: int):
+        """Block-Jacobi mode: 0 LU solves (default), 1 explicit block inverses."""
+        self._check(self.lib.ldg_set_precond_mode(self._h, mode))
+
     def precond_build(self, alpha_dt: float):
         """Block-Jacobi preconditioner of I - alpha_dt A~."""
         self._check(self.lib.ldg_precond_build(self._h, alpha_dt))

@@ -126,9 +126,26 @@ def test_block_jacobi_effectiveness_poisson_p3():
 
 
 # ---------------------------------------------------------------- GPU parity
+def test_precond_inverse_mode_equals_lu():
+    """ldg_set_precond_mode(1): explicit block inverses -- the same operator as
+    the LU solves to round-off."""
+    cfg = CONFIGS[2]
+    c, U = cfg.build(n=3)
+    o = Oracle(c, cfg.physics)
+    o.assemble(U)
+    r = rng.standard_normal(o.n_dofs)
+    o.precond_build(0.05)
+    z_lu = o.precond_apply(r)
+    o.set_precond_mode(1)
+    o.precond_build(0.05)
+    z_inv = o.precond_apply(r)
+    assert rel(z_inv, z_lu) <= 1e-12
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 1], ids=["lu", "inverse"])
 @pytest.mark.parametrize("ci,n", [(0, 4), (1, 4), (2, 3)])
-def test_gpu_preconditioner_and_gmres(ci, n):
+def test_gpu_preconditioner_and_gmres(ci, n, mode):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -138,6 +155,8 @@ def test_gpu_preconditioner_and_gmres(ci, n):
     c, U = cfg.build(n=n)
     o = Oracle(c, cfg.physics)
     g = LineDG(c, cfg.physics)
+    o.set_precond_mode(mode)
+    g.set_precond_mode(mode)
     src = cfg.source_for(c)
     if src is not None:
         o.set_source(src)

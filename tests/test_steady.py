@@ -115,9 +115,9 @@ def test_gpu_steady_solve_matches_oracle(which, tmp_path):
             assert s1[k] == s2[k], (k, s1, s2)
         assert np.abs(U2 - U1).max() <= 1e-9 * np.abs(U1).max()
     else:
-        # nonlinear continuation: round-off may move the last 1e-10 crossing by
-        # one update; both end at the same steady state
-        assert abs(s1["newton_iters"] - s2["newton_iters"]) <= 1, (s1, s2)
+        # nonlinear continuation with fixed-length GMRES: round-off moves the
+        # path by a few updates; both end at the same steady state
+        assert abs(s1["newton_iters"] - s2["newton_iters"]) <= 3, (s1, s2)
         assert s2["residual_norm"] <= 1e-10
         assert np.abs(U2 - U1).max() <= 1e-8 * np.abs(U1).max()
     rows = log.read_text().splitlines()
