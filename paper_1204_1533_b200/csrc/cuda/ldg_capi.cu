@@ -907,6 +907,7 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
       d.bspec = c->d_bspec;
       d.bspec_off = c->bspec_off.data();
     }
+
     d.launches = &c->launches;
     *out = c.release();
     return LDG_OK;

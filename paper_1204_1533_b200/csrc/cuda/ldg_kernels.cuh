@@ -2479,6 +2479,83 @@ k_jacobian(const KParams<C> kp, const double* __restrict__ U, const double* __re
               C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
 }
 
+// Fused endpoint phase (JacP::FE): gather the neighbour traces of the
+// element's line ends (cp.async), then one item per (line end, pass) forms
+// the closed-form LLF endpoint Jacobian dFh/du_in (pass 0) or dFh/du_out
+// (pass 1) straight into the shared endpoint block in the k_endjac scratch
+// layout (entry-major, stride LS).  Boundary ends (Dirichlet-type only: the
+// host enables the fused path when no slip / Neumann / no-slip wall exists):
+// ghost = the boundary data, no out-block.
+template <class C>
+__device__ __forceinline__ void endpoint_gather(const double* __restrict__ U, const int2* sc, double* snb, int tid,
+                                                int nthr) {
+  constexpr int D = C::D, NL = C::NL, M = C::M, NP = C::NP, NPE = C::NPE;
+  for (int w = tid; w < 2 * D * NL; w += nthr) {
+    const int ds = w / NL, line = w - ds * NL;
+    const int2 cn = sc[ds];
+    if (cn.x < 0) continue;
+    const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
+#pragma unroll
+    for (int c = 0; c < M; ++c) cp_async8(snb + w * M + c, U + nd * M + c);
+  }
+  cp_async_commit();
+}
+// (the traces of this element were gathered by endpoint_gather one element
+// ahead; wait for them, then form the blocks)
+template <class C>
+__device__ __forceinline__ void endpoint_phase(const KParams<C>& kp, int k, const double* su, const double* mk,
+                                               const int2* sc, double* sE, const double* snb,
+                                               const double* __restrict__ SEg, int tid, int nthr) {
+  constexpr int D = C::D, NL = C::NL, M = C::M, NP = C::NP, P = C::P, B11 = C::B11;
+  constexpr int NLE = 2 * D * NL, LS = EndJac<C>::LS;
+  cp_async_wait_all();
+  __syncthreads();
+  for (int w = tid; w < 2 * NLE; w += nthr) {
+    const int pass = w / NLE, le = w - pass * NLE;
+    const int ds = le / NL, line = le - ds * NL, dir = ds >> 1, side = ds & 1;
+    const int2 cn = sc[ds];
+    const bool bd = cn.x < 0;
+    double J[M * M];
+    if (bd) {
+      const int kind = __ldg(kp.bck + (-1 - cn.x));
+      if (kind == BC_SLIP_WALL || kind == BC_NEUMANN || kind == BC_NO_SLIP) {
+        // general boundary kinds: blocks from k_endjac<..., BND> (global scratch of the chunk)
+#pragma unroll
+        for (int o = 0; o < M * M; ++o) sE[(pass * B11 + o) * LS + le] = __ldg(SEg + (pass * B11 + o) * LS + le);
+        continue;
+      }
+    }
+    if (bd && pass == 1) {
+#pragma unroll
+      for (int o = 0; o < M * M; ++o) sE[(B11 + o) * LS + le] = 0.0;
+      continue;
+    }
+    const int nd = node_on_line<C>(dir, line, side ? P : 0);
+    double n[D], ui[M], uo[M];
+#pragma unroll
+    for (int d = 0; d < D; ++d) n[d] = mk[C::MET_NV + (ds * NL + line) * D + d];
+    const double* g = bd ? bnd_g(kp, -1 - cn.x, k, ds, line) : nullptr;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      ui[c] = su[nd * M + c];
+      uo[c] = bd ? __ldg(g + c) : snb[le * M + c];
+    }
+    bool ok = true;
+    llf_jac<D>(uo, ui, n, kp.pp.gamma, pass, J, ok);
+#pragma unroll
+    for (int o = 0; o < M * M; ++o) sE[(pass * B11 + o) * LS + le] = J[o];
+    if (!ok) {
+      double m2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) m2 += ui[1 + d] * ui[1 + d];
+      const bool own_bad = !(ui[0] > 0.0) || !((kp.pp.gamma - 1.0) * (ui[D + 1] - 0.5 * m2 / ui[0]) > 0.0);
+      report_bad_state<double, M>(kp.err, own_bad || bd ? static_cast<int>(kp.order[k]) : cn.x,
+                                  own_bad || bd ? nd : conn_node(cn.y, line, NP), own_bad || bd ? ui : uo);
+    }
+  }
+  __syncthreads();
+}
+
 // Persistent, TMA-prefetching Jacobian assembly (2-D: one tile = one element):
 // two input buffers {U, Q, metric, endpoint-Jacobian scratch} of consecutive
 // elements; the next element's inputs land while the current one assembles.
@@ -2490,7 +2567,20 @@ struct JacP {
   static constexpr int MET = C::METP;
   static constexpr int CONN = ev(2 * C::D);  // int2 entries (8 B each)
   static constexpr int SE = ev(EndJac<C>::PER_ELEM);
-  static constexpr int BUF = U + Q + MET + CONN + SE;
+  // fused endpoint phase (3-D element units, first order, LLF: closed-form
+  // endpoint Jacobians computed in the assembly from gathered neighbour
+  // traces; no k_endjac launch and no scratch round trip through HBM)
+#ifndef LDG_JAC_FUSED_EJ
+#define LDG_JAC_FUSED_EJ 1
+#endif
+  static constexpr bool FE = LDG_JAC_FUSED_EJ && C::D == 3 && C::WU == 0 && !C::SECOND && C::HAS_INV &&
+                             C::RI != LDG_ROE;
+  static constexpr int NBV = FE ? ev(2 * C::D * C::NL * C::M) : 0;  // neighbour traces per line end
+  // fused: the endpoint block is computed per element (one copy outside the
+  // ring), only the neighbour traces ride the ring
+  static constexpr int SER = FE ? 0 : SE;   // endpoint block per ring buffer
+  static constexpr int SE1 = FE ? SE : 0;   // single endpoint block (fused)
+  static constexpr int BUF = U + Q + MET + CONN + SER + NBV;
   using SM = JacSmem<C>;
   // 2-D: the element's K11 tile is formed in shared memory and leaves with one
   // TMA bulk store (sequential write stream, no per-entry global stores)
@@ -2510,14 +2600,14 @@ struct JacP {
   static constexpr bool STAGE = !PIPE && LDG_JAC_STAGE && C::D == 2 && !C::SECOND && (SM::ST11 % 2 == 0) &&
                                 8LL * SM::ST11 <= 64 * 1024;
   static constexpr int STG = STAGE ? SM::ST11 : 0;
-  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + WORK2 + STG); }
+  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + WORK2 + STG + SE1); }
   // prefetch ring depth: 3 for the pipelined 2-D tile and the one-CTA-per-SM
   // 3-D element units (when it fits), 2 where several CTAs share an SM
 #ifndef LDG_JAC_NBUF3  // 3-deep input ring for every persistent assembly that fits (knob)
 #define LDG_JAC_NBUF3 0  // measured (C2): -0.9 us, within noise: off
 #endif
   static constexpr int NBUF = ((PIPE || JacThreads<C>::big || LDG_JAC_NBUF3) && bytes(3) <= 200 * 1024) ? 3 : 2;
-  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + WORK2 + STG;  // 4 doubles hold up to 3 mbarriers
+  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + WORK2 + STG + SE1;  // 4 doubles hold up to 3 mbarriers
   static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
                              (EndJac<C>::PER_ELEM % 2 == 0) && bytes(2) <= 200 * 1024;
 };
@@ -2550,7 +2640,12 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   auto bQ = [&](int bi) { return bufs + bi * JP::BUF + JP::U; };
   auto bMET = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q; };
   auto bCONN = [&](int bi) { return reinterpret_cast<int2*>(bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET); };
-  auto bSE = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET + JP::CONN; };
+  double* const se1 = work + SM::WORK + JP::WORK2 + JP::STG;  // fused: the element's endpoint block
+  auto bSE = [&](int bi) {
+    return JP::FE ? se1 : bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET + JP::CONN;
+  };
+  auto bNBV = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET + JP::CONN + JP::SER; };
+  constexpr bool fe = JP::FE;
   if (tid == 0) {
     for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
     mbar_fence_init();
@@ -2559,7 +2654,7 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   __syncthreads();
   auto issue = [&](int k, int bi) {
     const size_t e = __ldg(kp.order + k);
-    unsigned bytes = NPE * M * 8 + C::METP * 8 + 2 * C::D * 8 + EJ::PER_ELEM * 8;
+    unsigned bytes = NPE * M * 8 + C::METP * 8 + 2 * C::D * 8 + (fe ? 0 : EJ::PER_ELEM * 8);
     if (C::SECOND) bytes += NPE * MD * 8;
     mbar_expect_tx(&bar[bi], bytes);
     tma_load_1d(bU(bi), U + e * (NPE * M), NPE * M * 8, &bar[bi]);
@@ -2569,7 +2664,9 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
 #ifndef LDG_SE_ONCE  // endpoint scratch read with an L2 evict-first policy
 #define LDG_SE_ONCE 0  // measured: no gain (C2 +0.7 us, C3 +8 us)
 #endif
-    if (LDG_SE_ONCE)
+    if (fe) {
+      // (endpoint Jacobians computed in the element loop)
+    } else if (LDG_SE_ONCE)
       tma_load_1d_once(bSE(bi), SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
     else
       tma_load_1d(bSE(bi), SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
@@ -2609,6 +2706,17 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   for (int k = k0, it = 0; k < k_end; k += G, ++it) {
     const int cur = it % NB;
     mbar_wait(&bar[cur], (it / NB) & 1);
+    if (JP::FE && fe) {
+      if (it == 0) endpoint_gather<C>(U, bCONN(cur), bNBV(cur), tid, nthr);
+      endpoint_phase<C>(kp, k, bU(cur), bMET(cur), bCONN(cur), bSE(cur), bNBV(cur),
+                        SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, tid, nthr);
+      // prefetch: the next element's neighbour traces land during this assembly
+      if (k + G < k_end) {
+        const int nx = (it + 1) % NB;
+        mbar_wait(&bar[nx], ((it + 1) / NB) & 1);
+        endpoint_gather<C>(U, bCONN(nx), bNBV(nx), tid, nthr);
+      }
+    }
     // staging free again: the previous tile's bulk store has read it (waited
     // here by its issuer; jac_tile's barrier before phase 2 publishes it)
     if (JP::STAGE && tid == 0 && it > 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");

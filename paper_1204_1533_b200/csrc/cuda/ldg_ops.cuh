@@ -283,7 +283,11 @@ struct Launch {
       const long long ob = d.owned ? d.owned_off[ci] : 0;
       const long long oe = d.owned ? d.owned_off[ci + 1] : static_cast<long long>(ke - kb) * 2 * C::D;
       const long long nf = oe - ob;
-      if (one_seed) {
+      // (fused configurations: the persistent assembly computes the endpoint
+      // Jacobians itself -- only when that kernel runs)
+      const bool fused = JacP<C>::FE && JacP<C>::OK && !simple && !(C::D == 3 && force_s3);
+      if (fused) {
+      } else if (one_seed) {
         const long long items = nf * C::NL * EndJac<C>::items(1);
         k_endjac<C, 1, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
             params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
@@ -292,7 +296,7 @@ struct Launch {
         k_endjac<C, EJ_SEEDS, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
             params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
       }
-      count(d);
+      if (!fused) count(d);
       // slip-wall / Neumann boundary ends of the chunk (general kinds)
       if (d.bspec && d.bspec_off[ci + 1] > d.bspec_off[ci]) {
         const long long sb = d.bspec_off[ci], se = d.bspec_off[ci + 1];
