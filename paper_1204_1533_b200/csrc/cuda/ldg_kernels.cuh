@@ -448,17 +448,16 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
         const int2 cb = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
         bnd_flux<C>(kp, -1 - cb.x, bcp[side], ui, qi, n, nn, fh, ok);
       } else {
-      if (C::HAS_INV) {
-        if (C::RI == LDG_ROE) roe_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
-        else llf_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
-      }
-      if (C::SECOND) {
-        double nn = n[0] * n[0];
+        if (C::HAS_INV) {
+          if (C::RI == LDG_ROE) roe_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
+          else llf_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
+        }
+        if (C::SECOND) {
+          double nn = n[0] * n[0];
 #pragma unroll
-        for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-        nn = sqrt(nn);
-        double fv[M];
-        {
+          for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+          nn = sqrt(nn);
+          double fv[M];
           if (sg[side] > 0) {
             visc_fn<D, C::PH, double, double, double>(uo[side], qo[side], n, kp.pp, fv, ok);
           } else {
@@ -474,7 +473,6 @@ k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __re
             for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[side][c]);
           }
         }
-      }
       }
 #pragma unroll
       for (int i = 0; i < NP; ++i)
@@ -625,22 +623,16 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
       nn = sqrt(nn);
       bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
     } else {
-    if (C::HAS_INV) {
-      if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-      else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-    }
-    if (C::SECOND) {
-      double nn = n[0] * n[0];
+      if (C::HAS_INV) {
+        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+      }
+      if (C::SECOND) {
+        double nn = n[0] * n[0];
 #pragma unroll
-      for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-      nn = sqrt(nn);
-      double fv[M];
-      if (bcp) {
-        visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
-        const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
-#pragma unroll
-        for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - uo[c]);
-      } else {
+        for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+        nn = sqrt(nn);
+        double fv[M];
         if (S > 0) {
           double qo[MD];
 #pragma unroll
@@ -656,7 +648,6 @@ k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* _
           for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
         }
       }
-    }
     }
   }
   // lane transpose: lane i < NP forms r_i
@@ -923,22 +914,16 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
           nn = sqrt(nn);
           bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
         } else {
-        if (C::HAS_INV) {
-          if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-          else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-        }
-        if (C::SECOND) {
-          double nn = n[0] * n[0];
+          if (C::HAS_INV) {
+            if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+            else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+          }
+          if (C::SECOND) {
+            double nn = n[0] * n[0];
 #pragma unroll
-          for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-          nn = sqrt(nn);
-          double fv[M];
-          if (bcp) {
-            visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
-            const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
-#pragma unroll
-            for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - uo[c]);
-          } else {
+            for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+            nn = sqrt(nn);
+            double fv[M];
             if (S > 0) visc_fn<D, C::PH, double, double, double>(uo, bNBQ(cur) + w * MD, n, kp.pp, fv, ok);
             else visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
 #pragma unroll
@@ -948,7 +933,6 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
               for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
             }
           }
-        }
         }
 #pragma unroll
         for (int i = 0; i < NP; ++i)
@@ -1234,38 +1218,31 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
           fh[c] = 0.0;
         }
         if (bcp) {
-            double nn = n[0] * n[0];
-#pragma unroll
-            for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-            nn = sqrt(nn);
-            bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
-          } else {
-          if (C::HAS_INV) {
-          if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-          else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-        }
-        if (C::SECOND) {
           double nn = n[0] * n[0];
 #pragma unroll
           for (int d = 1; d < D; ++d) nn += n[d] * n[d];
           nn = sqrt(nn);
-          double fv[M];
-          if (bcp) {
-            visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
-            const double c11 = kp.pp.c11bd / (D == 2 ? nn : sqrt(nn));
-#pragma unroll
-            for (int c = 0; c < M; ++c) fh[c] += fv[c] + c11 * nn * (ui[c] - uo[c]);
+          bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
           } else {
-            if (S > 0) visc_fn<D, C::PH, double, double, double>(uo, io.bNBQ(cur) + w * MD, n, kp.pp, fv, ok);
-            else visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
-#pragma unroll
-            for (int c = 0; c < M; ++c) fh[c] += fv[c];
-            if (kp.pp.c11 != 0.0) {
-#pragma unroll
-              for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
+              if (C::HAS_INV) {
+              if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
+              else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
             }
-          }
-        }
+            if (C::SECOND) {
+              double nn = n[0] * n[0];
+#pragma unroll
+              for (int d = 1; d < D; ++d) nn += n[d] * n[d];
+              nn = sqrt(nn);
+              double fv[M];
+              if (S > 0) visc_fn<D, C::PH, double, double, double>(uo, io.bNBQ(cur) + w * MD, n, kp.pp, fv, ok);
+              else visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
+#pragma unroll
+              for (int c = 0; c < M; ++c) fh[c] += fv[c];
+              if (kp.pp.c11 != 0.0) {
+#pragma unroll
+                for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
+              }
+            }
           }
 #pragma unroll
         for (int c = 0; c < M; ++c) sFH[w * M + c] = fh[c];
