@@ -128,10 +128,12 @@ def test_projected_nodes_on_circles_and_area_converges():
     assert errs[2] < errs[0]
 
 
-def test_free_stream_preserved_on_curved_mesh():
+@pytest.mark.parametrize("p", [2, 4])
+def test_free_stream_preserved_on_curved_mesh(p):
+    """SPEC acceptance 7 (p in {2, 4})."""
     from oracle.pyoracle import Oracle
 
-    _, _, _, case = annulus(4)
+    _, _, _, case = annulus(p)
     case.remap_circles([(1, 0.0, 0.0, R0), (2, 0.0, 0.0, R1)])
     g = 1.4
     st = [1.0, 0.5, 0.1, 1 / (g - 1) / g + 0.5 * (0.25 + 0.01)]
