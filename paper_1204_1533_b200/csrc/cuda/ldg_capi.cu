@@ -1791,6 +1791,19 @@ int ldg_steady_solve(ldg_ctx* c, double* U, double t, const ldg_steady_cfg* cfg,
 // directions; host buffers must stay valid (pinned for true overlap) and
 // results are ready after ldg_synchronize().
 namespace {
+// device address of a mapped pinned host buffer (cudaHostAlloc / registered
+// memory under unified addressing), else nullptr
+double* mapped_host(double* h) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  static const char* env = std::getenv("LDG_ZERO_COPY");  // 0 disables (A/B)
+  if (env && std::atoi(env) == 0) return nullptr;
+  return static_cast<double*>(a.devicePointer);
+}
 // upload n doubles to dbuf once `free_ev` (the last reader of dbuf) completed;
 // the context stream then waits for the upload
 void upload_async(ldg_ctx* c, double* dbuf, const double* h, size_t n, cudaEvent_t free_ev) {
@@ -1870,14 +1883,33 @@ int ldg_bsr_spmv_host(ldg_ctx* c, int which, const double* x, double* y) {
     const size_t ny = which == LDG_K21 ? c->nQ() : c->nU();
     double* dx = ensure(c->d_hx, c->nQ());
     double* dy = ensure(c->d_hy, c->nQ());
+    // zero-copy output: a K11 product into mapped pinned host memory is
+    // written by the kernel itself (whole node rows per warp store, see
+    // k_spmv11), so the PCIe transfer of y overlaps the product instead of
+    // following it; pageable buffers take the staged copy
+    double* yz = which == LDG_K11 && c->ops->M == 4 ? mapped_host(y) : nullptr;
+    auto product = [&](double* dst) -> int {
+      if (!yz) return ldg_bsr_spmv(c, which, dx, dst);
+      if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
+      return finish(c, c->ops->spmv11_zc(c->dc, c->d_K11, dx, dst));
+    };
     if (!c->sync_errors) {
       upload_async(c, dx, x, nx, c->ev_free_hx);
       ck(cudaStreamWaitEvent(c->stream, c->ev_out_y, 0), "wait y download");
-      const int st = ldg_bsr_spmv(c, which, dx, dy);
+      const int st = product(yz ? yz : dy);
       if (st != LDG_OK) return st;
       ck(cudaEventRecord(c->ev_free_hx, c->stream), "record");
-      download_async(c, y, dy, ny, c->ev_out_y);
+      if (yz) ck(cudaEventRecord(c->ev_out_y, c->stream), "record product");
+      else download_async(c, y, dy, ny, c->ev_out_y);
       return LDG_OK;
+    }
+    if (yz) {
+      ck(cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D x");
+      const bool was = c->sync_errors;
+      c->sync_errors = true;
+      const int st = product(yz);
+      c->sync_errors = was;
+      return st;
     }
     ck(cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D x");
     const bool was = c->sync_errors;

@@ -55,6 +55,7 @@ struct Ops {
                           double* K12);
   cudaError_t (*k21)(const DevCtx&, double* K21);
   cudaError_t (*spmv11)(const DevCtx&, const double* V11, const double* x, double* y);
+  cudaError_t (*spmv11_zc)(const DevCtx&, const double* V11, const double* x, double* y);  // y mapped host
   cudaError_t (*spmv12)(const DevCtx&, const double* V12, const double* w, double* y);
   cudaError_t (*spmv21)(const DevCtx&, const double* V21, const double* v, double* w);
   cudaError_t (*split)(const DevCtx&, const double* V11, const double* V12, const double* v,
@@ -351,6 +352,12 @@ struct Launch {
     count(d);
     return cudaGetLastError();
   }
+  static cudaError_t spmv11_zc(const DevCtx& d, const double* V11, const double* x, double* y) {
+    k_spmv11<C, false, true><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, nullptr, x, nullptr, 0.0, y,
+                                                               spmv_rev(d));
+    count(d);
+    return cudaGetLastError();
+  }
   static cudaError_t spmv12(const DevCtx& d, const double* V12, const double* w, double* y) {
     if (!C::SECOND) return cudaSuccess;
     k_spmv12<C><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V12, w, y);
@@ -400,7 +407,7 @@ struct Launch {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
                             C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, chunk_elems, residual, gradient, jacobian, k21,
-                            spmv11, spmv12, spmv21, split, PcCfg<C>::OK ? PcCfg<C>::NE : 0, pc_build, pc_apply};
+                            spmv11, spmv11_zc, spmv12, spmv21, split, PcCfg<C>::OK ? PcCfg<C>::NE : 0, pc_build, pc_apply};
     return &ops;
   }
 };

@@ -241,6 +241,13 @@ def test_async_host_path_matches_sync():
             gpu.synchronize()
             assert np.array_equal(Rp, R0) and np.array_equal(yp, y0)
         gpu.set_sync_errors(True)
+        # synchronous call into pinned memory: the zero-copy product (M = 4)
+        yp[:] = 0.0
+        gpu.spmv(LDG_K11, xp, out=yp)
+        assert np.array_equal(yp, y0)
+        ora = Oracle(case, cfg.physics)
+        ora.assemble(U)
+        assert rel(y0, ora.spmv(LDG_K11, x)) <= TOL
 
 
 @pytest.mark.slow
