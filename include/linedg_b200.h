@@ -324,7 +324,10 @@ int ldg_synchronize(ldg_ctx* ctx);
  * ldg_bsr_spmv_host are asynchronous: uploads run on a copy stream, downloads
  * on another, ordered against the kernels by events (transfers of consecutive
  * calls overlap the kernels in both PCIe directions); the host buffers must
- * stay valid (pinned for overlap) and results are ready after ldg_synchronize. */
+ * stay valid (pinned for overlap) and results are ready after ldg_synchronize.
+ * ldg_bsr_spmv_host(K11) with y in mapped pinned memory (cudaHostAlloc /
+ * cudaHostRegister under unified addressing) and m = 4 is zero-copy: the
+ * product kernel writes y over PCIe while it runs (LDG_ZERO_COPY=0 disables). */
 int ldg_residual_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
 int ldg_jacobian_assemble_host(ldg_ctx* ctx, const double* U, double t);
 int ldg_bsr_spmv_host(ldg_ctx* ctx, int which, const double* x, double* y);
