@@ -3585,7 +3585,36 @@ k_pc_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* _
     }
     return;
   }
-  if (lane == 0) {
+  (void)zw;
+  (void)re;
+  (void)e;
+}
+
+// LU apply: EPW elements per warp (32 / EPW lanes each), so every dependent
+// column-load step of the substitutions serves EPW independent chains -- the
+// solve is bound by that load latency, not by bandwidth.  Same operations in
+// the same order per element as the single-element form.
+#ifndef LDG_PC_EPW
+#define LDG_PC_EPW 2  // measured (C2 apply): 1 -> 0.486 ms, 2 -> 0.407 ms
+#endif
+template <class C>
+__global__ void __launch_bounds__(128)
+k_pc_apply_lu2(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* __restrict__ piv,
+               const double* __restrict__ r, double* __restrict__ z) {
+  using PC = PcCfg<C, false>;
+  constexpr int NE = PC::NE, EPW = LDG_PC_EPW, LW = 32 / EPW;
+  __shared__ double zs[4 * EPW][PC::OK ? NE : 1];  // (unused instantiations stay small)
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, hl = lane / LW, sl = lane % LW;
+  const int kk = (blockIdx.x * 4 + wl) * EPW + hl;
+  if ((blockIdx.x * 4 + wl) * EPW >= kp.E) return;  // (whole warp)
+  const bool valid = kk < kp.E;
+  const int k = valid ? kk : kp.E - 1;  // an idle group shadows the last element (no store)
+  const size_t e = __ldg(kp.order + k);
+  double* zw = zs[wl * EPW + hl];
+  const double* re = r + e * NE;
+  for (int i = sl; i < NE; i += LW) zw[i] = re[i];
+  __syncwarp();
+  if (sl == 0) {
     const int32_t* pv = piv + static_cast<size_t>(k) * NE;
     for (int i = 0; i < NE; ++i) {
       const int p = pv[i];
@@ -3598,18 +3627,20 @@ k_pc_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* _
   const double* L = LUc + static_cast<size_t>(k) * NE * NE;
   for (int j = 0; j < NE - 1; ++j) {
     const double zj = zw[j];
-    for (int i = j + 1 + lane; i < NE; i += 32) zw[i] -= L[j * NE + i] * zj;
+    for (int i = j + 1 + sl; i < NE; i += LW) zw[i] -= L[j * NE + i] * zj;
     __syncwarp();
   }
   for (int j = NE - 1; j >= 0; --j) {
-    if (lane == 0) zw[j] /= L[j * NE + j];
+    if (sl == 0) zw[j] /= L[j * NE + j];
     __syncwarp();
     const double zj = zw[j];
-    for (int i = lane; i < j; i += 32) zw[i] -= L[j * NE + i] * zj;
+    for (int i = sl; i < j; i += LW) zw[i] -= L[j * NE + i] * zj;
     __syncwarp();
   }
-  double* ze = z + e * NE;
-  for (int i = lane; i < NE; i += 32) ze[i] = zw[i];
+  if (valid) {
+    double* ze = z + e * NE;
+    for (int i = sl; i < NE; i += LW) ze[i] = zw[i];
+  }
 }
 
 }  // namespace ldg

@@ -399,7 +399,8 @@ struct Launch {
   static cudaError_t pc_apply(const DevCtx& d, const double* LUc, const int32_t* piv, const double* r, double* z) {
     if (!PcCfg<C>::OK) return cudaErrorNotSupported;
     if (d.pc_inverse) k_pc_apply<C, true><<<(d.E + 3) / 4, 128, 0, d.stream>>>(params(d), LUc, piv, r, z);
-    else k_pc_apply<C, false><<<(d.E + 3) / 4, 128, 0, d.stream>>>(params(d), LUc, piv, r, z);
+    else k_pc_apply_lu2<C><<<(d.E + 4 * LDG_PC_EPW - 1) / (4 * LDG_PC_EPW), 128, 0, d.stream>>>(params(d), LUc, piv,
+                                                                                              r, z);
     count(d);
     return cudaGetLastError();
   }
