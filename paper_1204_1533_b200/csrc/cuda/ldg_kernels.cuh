@@ -3485,10 +3485,14 @@ k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __
     const double ip = 1.0 / Ms[kk * LDM + kk];
     for (int i = kk + 1 + tid; i < NE; i += nthr) Ms[i * LDM + kk] *= ip;
     __syncthreads();
-    const int rem = NE - kk - 1;
-    for (int x = tid; x < rem * rem; x += nthr) {
-      const int i = kk + 1 + x / rem, j = kk + 1 + x % rem;
-      Ms[i * LDM + j] -= Ms[i * LDM + kk] * Ms[kk * LDM + j];
+    // trailing update: warps over rows, lanes over columns (no per-entry
+    // integer division; the row multiplier stays in a register)
+    {
+      const int ty = tid >> 5, tx = tid & 31, TY = nthr >> 5;
+      for (int i = kk + 1 + ty; i < NE; i += TY) {
+        const double lik = Ms[i * LDM + kk];
+        for (int j = kk + 1 + tx; j < NE; j += 32) Ms[i * LDM + j] -= lik * Ms[kk * LDM + j];
+      }
     }
     __syncthreads();
   }
