@@ -1,23 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the Line-DG hot path on B200 (BASELINE.json metric).
 
-One step = one pass of the hot path over the configuration's synthetic input:
-residual (GDOF/s) + analytic Jacobian assembly + block-SpMV on a seeded N(0,1)
-vector (BASELINE.json config 2: "residual + Jacobian + block-SpMV"), fp64.
+One step = one pass of the hot path over the configuration's synthetic input,
+fp64: the residual R(U) (second-order physics: Q = D(U), then R(U, Q)), the
+analytic Jacobian assembly at U (sharing that Q, as a Newton step does), and
+NMV matvecs with the assembled Jacobian on seeded N(0,1) vectors -- the split
+matvec (I - adt (K11 + K12 K21)) v that GMRES applies for second-order physics,
+the K11 block-SpMV for first-order physics.  The default workload is the
+largest single-GPU configuration, BASELINE.json config 5 (3-D Navier-Stokes
+p=4 48^3, 69 M DOFs, 164 GB Jacobian store): "full residual, Jacobian assembly
+and 30 block-SpMVs on seeded N(0,1) vectors" (NMV = 30; other configs NMV = 1).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
 value      = DOFs processed per second through the whole step (all ranks), GDOF/s,
-             inputs resident in HBM, L2 flushed (512 MB write) between steps.
-e2e        = same metric through the reference-facing host-buffer C-ABI calls
-             (ldg_residual_host, ldg_jacobian_assemble_host, ldg_bsr_spmv_host,
-             asynchronous mode + ldg_synchronize): H2D of U (twice: residual and
-             assembly inputs) and x, D2H of R and y, all inside the timed region.
-roofline   = the step's dominant kernel: algorithmic bytes per launch / mean
+             inputs resident in HBM, L2 flushed (512 MB write + read) between steps
+             (every C3-C5 operand is also larger than the 126 MB L2).
+e2e        = the same step through the reference-facing host-buffer C-ABI
+             (ldg_residual_assemble_host: one upload of U, R downloaded; then NMV
+             ldg_split_matvec_host / ldg_bsr_spmv_host calls, v up and y down each),
+             asynchronous mode + ldg_synchronize, all transfers inside the timed region.
+roofline   = the step's dominant kernel family: algorithmic bytes per launch / mean
              CUDA-event duration vs the measured HBM copy bandwidth.
-cpu_baseline = the CPU oracle (oracle/, a port of the reference algorithm;
-             the reference's own hot-path sources do not exist) on this host.
---impl reference runs only that CPU implementation (all host threads).
+cpu_baseline = the CPU oracle (oracle/, a port of the reference algorithm; the
+             reference's own hot-path sources do not exist) on this host: a
+             cost-proportional element subset of the same step, extrapolated
+             linearly to the full mesh, all host threads, plus a 1-thread figure.
+--impl reference runs only that CPU implementation.
 Multi-GPU: the north star keeps the path on one GPU ("nothing across GPUs"),
 so N > 1 runs N independent replicas (weak scaling, no collective).
 """
@@ -84,21 +93,26 @@ def sizes(cfg, case, m):
     U = 8 * N * m
     out = {}
     second = cfg.physics.second_order()
+    ns11 = D * p + 1 + 2 * D
+    ns12 = D * p + 1 + D
+    r12 = m - 1 if m > 1 else 1
+    K11 = 8 * N * ns11 * m * m
+    K12 = 8 * N * ns12 * r12 * m * D
+    K21 = 8 * N * ns12 * D
     if not second:
         out["residual"] = 2 * U + 8 * met * E + conn
     else:
-        out["gradient"] = U + 8 * met * E + conn + U * D
-        out["residual"] = U + U * D + 8 * met * E + conn + U
-    ns11 = D * p + 1 + 2 * D
-    out["jacobian"] = 8 * N * ns11 * m * m + U + 8 * met * E + conn
+        # gradient pass (Q out) + residual pass (U, Q in, R out)
+        out["residual"] = (U + 8 * met * E + conn + U * D) + (U + U * D + 8 * met * E + conn + U)
+    out["jacobian"] = K11 + U + 8 * met * E + conn
     if second:
-        # K12 = dR/dQ is re-assembled with K11 every step (K21 is U-independent,
-        # assembled once): ns12 node-columns of r12 x m*D blocks per row
-        # (Navier-Stokes drops the density row), plus the gradient Q read.
-        ns12 = D * p + 1 + D
-        r12 = m - 1 if m > 1 else 1
-        out["jacobian"] += 8 * N * ns12 * r12 * m * D + U * D
-    out["spmv"] = 8 * N * ns11 * m * m + 2 * U + conn
+        # K12 = dR/dQ re-assembled with K11 every step (K21 is U-independent,
+        # assembled once), plus the gradient Q read
+        out["jacobian"] += K12 + U * D
+        # split matvec: K21 pass (v in, w out), then K11 v + K12 w and the axpy
+        out["matvec"] = (K21 + U + U * D + conn) + (K11 + K12 + U + U * D + U + conn)
+    else:
+        out["matvec"] = K11 + 2 * U + conn
     return out
 
 
@@ -179,52 +193,58 @@ def _kernels_per_step(ctx, step, stream, torch):
 
 
 # ---------------------------------------------------------------- CPU leg
-def cpu_step_fn(cfg, case, U, x):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_cpu(cfg, case, U, xs, nmv, adt, steps, budget_s=20.0, threads=None, frac=None):
+    """The oracle (CPU port of the reference algorithm) on a cost-proportional
+    element subset of the step (lo_time_sample), extrapolated linearly to the
+    full mesh: returns (full-step seconds per sample, threads, subset size)."""
     from oracle.pyoracle import Oracle  # CPU baseline leg only
 
+    threads = threads or Oracle.max_threads()
     ora = Oracle(case, cfg.physics)
     src = cfg.source_for(case)
     if src is not None:
         ora.set_source(src)
-
-    def step():
-        ora.residual(U)
-        ora.assemble(U)
-        ora.spmv(LDG_K11, x)
-    return ora, step
-
-
-def run_cpu(cfg, case, U, x, steps, warmup, budget_s=20.0):
-    from oracle.pyoracle import Oracle
-
-    threads = Oracle.max_threads()
-    Oracle.set_threads(threads)
-    _, step = cpu_step_fn(cfg, case, U, x)
+    # subset size: a first small probe, then sized so one sample takes ~budget/steps
+    n = max(1, min(case.E, case.E // (frac or 512)))
+    elems = np.arange(case.E, dtype=np.int32)
+    probe = ora.time_sample(U, xs[0], adt, nmv, elems[:n], threads, reps=1).sum()
+    if frac is None:
+        want = max(0.5, budget_s / max(1, steps))
+        n = int(min(case.E, max(n, n * want / max(probe, 1e-6))))
+    out = []
     t0 = time.perf_counter()
-    for _ in range(max(1, warmup)):
-        step()
-        if time.perf_counter() - t0 > budget_s / 2:
-            break
-    times = []
     for _ in range(max(1, steps)):
-        t = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t)
-        if sum(times) > budget_s:
+        secs = ora.time_sample(U, xs[0], adt, nmv, elems[:n], threads, reps=1)
+        out.append(float(secs.sum()) * case.E / n)
+        if time.perf_counter() - t0 > budget_s:
             break
-    dofs = case.E * case.npe * cfg.physics.components(case.dim)
-    return dofs, times, threads
+    ora.close() if hasattr(ora, "close") else None
+    return out, threads, n
 
 
 # ---------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=1, help="BASELINE.json config index (1 = 2-D Euler p=4 128^2)")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE.json config index (4 = 3-D Navier-Stokes p=4 48^3, the largest single-GPU config)")
+    ap.add_argument("--matvecs", type=int, default=None, help="matvecs per step (default: 30 for config 4, else 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
 
@@ -233,25 +253,38 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.config]
     m = cfg.physics.components(cfg.dim)
+    second = cfg.physics.second_order()
+    nmv = args.matvecs if args.matvecs is not None else (30 if args.config == 4 else 1)
+    nvec = max(1, min(3, nmv))
+    ADT = 0.05
+    mv_name = "split matvec (I - adt(K11 + K12 K21)) v" if second else "K11 block-SpMV"
+    metric = "residual GDOF/s, Jacobian assembly + block-SpMV GB/s (fp64), % HBM roofline, 1 B200"
     workload = {"workload": cfg.name, "config_index": args.config, "elements": cfg.n ** cfg.dim,
-                "p": cfg.p, "dofs": cfg.dofs(), "step": "residual + Jacobian assembly + K11 block-SpMV",
-                "l2": "flushed between steps (512 MB write + 512 MB read)", "parallelism": "replicas" if world > 1 else "1 GPU"}
+                "p": cfg.p, "dofs": cfg.dofs(),
+                "step": f"residual + Jacobian assembly (one shared Q = D(U)) + {nmv} x {mv_name}",
+                "matvecs": nmv, "matvec_vectors": f"{nvec} seeded N(0,1) vectors, cycled; alpha_dt = {ADT}",
+                "l2": "flushed between steps (512 MB write + 512 MB read); C3-C5 operands also exceed L2",
+                "parallelism": "replicas" if world > 1 else "1 GPU"}
 
     if args.impl == "reference":
         if rank != 0:
             return
         case, U = cfg.build()
-        x = case.normal_vector(m, cfg.vector_seed)
-        dofs, times, threads = run_cpu(cfg, case, U, x, args.steps, args.warmup, budget_s=max(30.0, args.cpu_budget))
-        t = statistics.mean(times)
+        xs = [case.normal_vector(m, cfg.vector_seed + k) for k in range(nvec)]
+        warm, _, _ = run_cpu(cfg, case, U, xs, nmv, ADT, max(1, min(args.warmup, 1)), budget_s=10.0)
+        times, threads, n = run_cpu(cfg, case, U, xs, nmv, ADT, args.steps, budget_s=max(30.0, args.cpu_budget))
+        t = statistics.median(times)
+        dofs = case.E * case.npe * m
         val = dofs / t / 1e9
-        line = {"metric": "residual GDOF/s, Jacobian assembly + block-SpMV GB/s (fp64), % HBM roofline, 1 B200",
-                "impl": "reference", "value": val, "unit": "GDOF/s", "n_gpus": args.gpus, "steps": len(times),
-                "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config shapes)",
-                "config": workload,
+        line = {"metric": metric, "impl": "reference", "value": val, "unit": "GDOF/s", "n_gpus": args.gpus,
+                "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, BASELINE.json config shapes)", "config": workload,
                 "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "port",
-                                 "sample": f"full {cfg.name} step (all {case.E} elements) x {len(times)}"},
+                                 "cpu": cpu_model(),
+                                 "sample": f"{cfg.name} step on {n} of {case.E} elements per sample (oracle, "
+                                           f"OpenMP), extrapolated linearly to the full mesh; median of "
+                                           f"{len(times)}"},
                 "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -266,7 +299,7 @@ def main():
 
         dist.init_process_group("nccl")
     case, U = cfg.build()
-    x = case.normal_vector(m, cfg.vector_seed)
+    xs_h = [case.normal_vector(m, cfg.vector_seed + k) for k in range(nvec)]
     N = case.E * case.npe
     dofs = N * m
     stream = torch.cuda.Stream()
@@ -275,7 +308,10 @@ def main():
     if src is not None:
         ctx.set_source(src)
     Ud = torch.from_numpy(U).cuda()
-    xd = torch.from_numpy(x).cuda()
+    xs = [torch.from_numpy(x).cuda() for x in xs_h]
+    Rd = torch.empty(dofs, dtype=torch.float64, device="cuda")
+    Qd = torch.empty(dofs * case.dim, dtype=torch.float64, device="cuda") if second else None
+    ys = [torch.empty(dofs, dtype=torch.float64, device="cuda") for _ in range(min(2, nmv))]
     # L2 flush between steps: write 512 MB (> 126 MB L2), then read another
     # 512 MB so the lines left in L2 are clean (no write-back lands in the
     # next timed kernel).
@@ -283,35 +319,37 @@ def main():
     rbuf = torch.ones(128 * 1024 * 1024, dtype=torch.int32, device="cuda")
     fsink = torch.empty((), dtype=torch.int64, device="cuda")
 
-    class _Flush:
-        @staticmethod
-        def zero_():
-            fbuf.zero_()
-            torch.sum(rbuf, dim=0, out=fsink)
+    def flush():
+        fbuf.zero_()
+        torch.sum(rbuf, dim=0, out=fsink)
 
-    flush = _Flush()
+    def op_residual():
+        ctx.residual(Ud, Q_out=Qd, out=Rd)
+
+    def op_jacobian():
+        if second:
+            ctx.assemble_jacobians_q(Ud, Qd)
+        else:
+            ctx.assemble_jacobians(Ud)
+
+    def op_matvecs():
+        for k in range(nmv):
+            if second:
+                ctx.split_matvec(ADT, xs[k % nvec], out=ys[k % 2])
+            else:
+                ctx.spmv(LDG_K11, xs[k % nvec], out=ys[k % 2])
+
+    ops = [op_residual, op_jacobian, op_matvecs]
     torch.cuda.synchronize()
     ctx.set_sync_errors(False)
-
-    def step(ev):
-        ev[0].record(stream)
-        ctx.residual(Ud)
-        ev[1].record(stream)
-        ctx.assemble_jacobians(Ud)
-        ev[2].record(stream)
-        ctx.spmv(LDG_K11, xd)
-        ev[3].record(stream)
-
     with torch.cuda.stream(stream):
         for _ in range(max(1, args.warmup)):
-            flush.zero_()
-            step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+            flush()
+            for op in ops:
+                op()
     ctx.synchronize()
     # Each op of the step is captured once as a CUDA graph and replayed; the
-    # event pairs around the replays time each kernel on the launching
-    # stream.  The 512 MB L2-flush kernel ahead of every step keeps the host
-    # ahead of the GPU, so no host launch gap falls inside a timed interval.
-    ops = [lambda: ctx.residual(Ud), lambda: ctx.assemble_jacobians(Ud), lambda: ctx.spmv(LDG_K11, xd)]
+    # event pairs around the replays time each op on the launching stream.
     graphs = []
     for op in ops:
         g = torch.cuda.CUDAGraph()
@@ -326,7 +364,7 @@ def main():
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         for k in range(args.steps):
-            flush.zero_()
+            flush()
             evs[k][0].record(stream)
             for i, g in enumerate(graphs):
                 g.replay()
@@ -338,95 +376,97 @@ def main():
     ctx.synchronize()  # surfaces any physical-state failure of the timed steps
     per = [(e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[0].elapsed_time(e[3]))
            for e in evs]
-    # kernels per step: counted by the library while capturing the step
-    n_per_step = _kernels_per_step(ctx, step, stream, torch)
-    launches = n_per_step * args.steps
-    t_res = statistics.mean(p[0] for p in per)
-    t_jac = statistics.mean(p[1] for p in per)
-    t_spv = statistics.mean(p[2] for p in per)
-    ms = statistics.mean(p[3] for p in per)
+    # kernels per step: counted by the library over one (uncaptured) step
+    n0 = ctx.kernel_launches()
+    with torch.cuda.stream(stream):
+        for op in ops:
+            op()
+    ctx.synchronize()
+    launches = (ctx.kernel_launches() - n0) * args.steps
+    t_res = statistics.median(p[0] for p in per)
+    t_jac = statistics.median(p[1] for p in per)
+    t_mvs = statistics.median(p[2] for p in per)
+    ms = statistics.median(p[3] for p in per)
     ms = max_over_ranks(ms)
     value = replica_throughput(dofs, world, ms)
 
     # ---- end to end through the host-buffer C-ABI (pinned host memory)
-    Uh = torch.from_numpy(U).pin_memory().numpy()
-    xh = torch.from_numpy(x).pin_memory().numpy()
-    Rh = torch.empty(U.size, dtype=torch.float64).pin_memory().numpy()  # pinned result buffers
-    yh = torch.empty(x.size, dtype=torch.float64).pin_memory().numpy()
-    # asynchronous host-buffer calls (ldg_set_sync_errors(ctx, 0)): uploads and
-    # downloads run on the context's copy streams and overlap the kernels and
-    # each other; ldg_synchronize joins them (results valid after it).
-    ctx.set_sync_errors(False)
-    e2e_times = []
-    torch.cuda.set_stream(stream)
-    for k in range(args.warmup + args.steps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-        torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        ctx.residual(Uh, out=Rh)
-        ctx.assemble_jacobians(Uh)
-        ctx.spmv(LDG_K11, xh, out=yh)
-        ctx.synchronize()
-        t1.record(stream)
-        torch.cuda.synchronize()
-        if k >= args.warmup:
-            e2e_times.append(t0.elapsed_time(t1))
-    ctx.set_sync_errors(True)
-    e2e_ms = statistics.mean(e2e_times)
-    e2e_ms = max_over_ranks(e2e_ms)
+    e2e = None
+    if not args.no_e2e:
+        Uh = torch.from_numpy(U).pin_memory().numpy()
+        xh = [torch.from_numpy(x).pin_memory().numpy() for x in xs_h]
+        Rh = torch.empty(dofs, dtype=torch.float64).pin_memory().numpy()
+        yh = [torch.empty(dofs, dtype=torch.float64).pin_memory().numpy() for _ in range(min(2, nmv))]
+        ctx.set_sync_errors(False)
+        e2e_times = []
+        for k in range(args.warmup + args.steps):
+            with torch.cuda.stream(stream):
+                flush()
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            ctx.residual_and_assemble(Uh, out=Rh)
+            for j in range(nmv):
+                if second:
+                    ctx.split_matvec(ADT, xh[j % nvec], out=yh[j % 2])
+                else:
+                    ctx.spmv(LDG_K11, xh[j % nvec], out=yh[j % 2])
+            ctx.synchronize()
+            t1.record(stream)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                e2e_times.append(t0.elapsed_time(t1))
+        ctx.set_sync_errors(True)
+        e2e_ms = max_over_ranks(statistics.median(e2e_times))
+        e2e = {"value": world * dofs / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * dofs * (1 + nmv), "d2h_bytes_per_step": 8 * dofs * (1 + nmv),
+               "path": "ldg_residual_assemble_host + NMV x " +
+                       ("ldg_split_matvec_host" if second else "ldg_bsr_spmv_host") + " (pinned, asynchronous)"}
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel family
     hbm, peak_src = peaks()
     by = sizes(cfg, case, m)
-    kern = {"residual": t_res, "jacobian": t_jac, "spmv": t_spv}
-    dom = max(kern, key=kern.get)
+    kern = {"residual": t_res, "jacobian": t_jac, "matvec": t_mvs / nmv}
+    share = {"residual": t_res / ms, "jacobian": t_jac / ms, "matvec": t_mvs / ms}
+    dom = max(share, key=share.get)
     breakdown = {}
     for name, tms in kern.items():
-        b = by[name] if name != "residual" else by["residual"] + by.get("gradient", 0)
-        gbs = b / (tms * 1e-3) / 1e9
-        breakdown[name] = {"ms": tms, "GB/s": gbs, "frac_hbm": gbs / hbm, "alg_bytes": b}
+        gbs = by[name] / (tms * 1e-3) / 1e9
+        breakdown[name] = {"ms_per_launch": tms, "launches_per_step": nmv if name == "matvec" else 1,
+                           "share_of_step": share[name], "GB/s": gbs, "frac_hbm": gbs / hbm,
+                           "alg_bytes": by[name]}
     breakdown["residual"]["GDOF/s"] = dofs / (t_res * 1e-3) / 1e9
-    # FP64 side of the roofline (fraction = max(bytes/BW, flops/P_fp64))
     p64, p64_src = fp64_peak()
     fl = flops(args.config, case)
     if fl is not None:
+        fl = {"residual": fl["residual"], "jacobian": fl["jacobian"], "matvec": fl["spmv"]}
         for name, tms in kern.items():
             tf = fl[name] / (tms * 1e-3) / 1e12
             breakdown[name].update({"alg_flops": fl[name], "TFLOP/s": tf, "frac_fp64": tf / p64,
                                     "frac_roofline": max(breakdown[name]["frac_hbm"], tf / p64)})
-    bdom = by[dom] if dom != "residual" else by["residual"] + by.get("gradient", 0)
-    achieved = bdom / (kern[dom] * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
-        except Exception:
-            traffic = None
-
-    line = {"metric": "residual GDOF/s, Jacobian assembly + block-SpMV GB/s (fp64), % HBM roofline, 1 B200",
-            "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, BASELINE.json config shapes)", "config": workload,
+    achieved = by[dom] / (kern[dom] * 1e-3) / 1e9
+    line = {"metric": metric, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config shapes)",
+            "config": workload,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "fp64": None if fl is None else {
-                             "flops": fl[dom], "achieved_tflops": fl[dom] / (kern[dom] * 1e-3) / 1e12,
-                             "peak_tflops": p64, "frac": fl[dom] / (kern[dom] * 1e-3) / 1e12 / p64,
-                             "peak_source": p64_src}},
-            "breakdown": breakdown,
-            "e2e": {"value": world * dofs / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": 3 * 8 * dofs, "d2h_bytes_per_step": 2 * 8 * dofs},
-            "gpu_launches": launches, "clocks": clocks,
+                         "frac": achieved / hbm, "traffic": None,
+                         "traffic_note": "ncu dram__bytes_read+write per launch: profiles/ (not measured in-run)",
+                         "peak_source": peak_src},
+            "breakdown": breakdown, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "jacobian_store_bytes": ctx.jacobian_bytes()}
     if rank == 0 and world == 1 and not args.no_cpu:
-        cd, times, threads = run_cpu(cfg, case, U, x, max(2, min(args.steps, 10)), 1, args.cpu_budget)
-        line["cpu_baseline"] = {"value": cd / statistics.mean(times) / 1e9, "unit": "GDOF/s", "cores": threads,
-                                "kind": "port", "sample": f"full {cfg.name} step x {len(times)} (oracle, OpenMP)"}
+        ctx.close()
+        del Ud, xs, Rd, Qd, ys
+        times, threads, n = run_cpu(cfg, case, U, xs_h, nmv, ADT, 3, args.cpu_budget)
+        t1c, _, n1 = run_cpu(cfg, case, U, xs_h, nmv, ADT, 1, args.cpu_budget / 4, threads=1,
+                             frac=max(1, case.E // max(1, n // max(1, threads))))
+        line["cpu_baseline"] = {
+            "value": dofs / statistics.median(times) / 1e9, "unit": "GDOF/s", "cores": threads, "kind": "port",
+            "cpu": cpu_model(), "value_1core": dofs / t1c[0] / 1e9,
+            "sample": f"{cfg.name} step on {n} of {case.E} elements ({threads} threads; 1-thread figure on {n1}), "
+                      f"oracle lo_time_sample, extrapolated linearly to the full mesh; median of {len(times)}"}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

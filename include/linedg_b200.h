@@ -24,8 +24,10 @@
  * (field.hpp:38-40 generalised to D).
  *
  * Device entry points take DEVICE pointers and are stream-ordered on the
- * stream given to ldg_create; the *_host variants take HOST pointers and
- * synchronise.  Every entry point returns an ldg_status; the message of the
+ * stream given to ldg_create; every device vector must be 16-byte aligned
+ * (it is read with 16-byte vector / bulk-async copies; a misaligned pointer is
+ * rejected with LDG_ERR_INVALID_ARGUMENT).  The *_host variants take HOST
+ * pointers and synchronise.  Every entry point returns an ldg_status; the message of the
  * last failure is available from ldg_last_error().  Status codes mirror the
  * reference exception taxonomy (errors.hpp:10-28):
  *   LDG_ERR_PHYSICAL_STATE  <-> physical_state_error (state via ldg_last_error_state)
@@ -192,6 +194,10 @@ int ldg_gradient(ldg_ctx* ctx, const double* U, double t, double* Q);
 /* Jacobians (analytic), stored on the device in the line-structured block
  * store.  Second-order physics uses Q = D(U), computed internally. */
 int ldg_jacobian_assemble(ldg_ctx* ctx, const double* U, double t);
+/* Assembly at U with the gradient Q = D(U) the caller already holds on the
+ * device (from ldg_residual(ctx, U, t, R, Q)): skips recomputing Q.  Q is
+ * ignored (may be NULL) for first-order physics. */
+int ldg_jacobian_assemble_q(ldg_ctx* ctx, const double* U, const double* Q, double t);
 int ldg_pattern_info_get(const ldg_ctx* ctx, int which, ldg_pattern_info* info);
 /* y = K x for K in {K11, K12, K21} (device pointers; x, y in reference numbering). */
 int ldg_bsr_spmv(ldg_ctx* ctx, int which, const double* x, double* y);
@@ -321,17 +327,32 @@ int ldg_synchronize(ldg_ctx* ctx);
 /* Host-buffer variants (end-to-end path: H2D, kernels, D2H).  With error
  * synchronisation on (default) each call synchronises before returning.  With
  * ldg_set_sync_errors(ctx, 0), ldg_residual_host / ldg_jacobian_assemble_host /
- * ldg_bsr_spmv_host are asynchronous: uploads run on a copy stream, downloads
+ * ldg_residual_assemble_host / ldg_bsr_spmv_host / ldg_split_matvec_host (two
+ * staging slots) are asynchronous: uploads run on a copy stream, downloads
  * on another, ordered against the kernels by events (transfers of consecutive
  * calls overlap the kernels in both PCIe directions); the host buffers must
  * stay valid (pinned for overlap) and results are ready after ldg_synchronize.
  * ldg_bsr_spmv_host(K11) with y in mapped pinned memory (cudaHostAlloc /
  * cudaHostRegister under unified addressing) and m = 4 is zero-copy: the
- * product kernel writes y over PCIe while it runs (LDG_ZERO_COPY=0 disables). */
+ * product kernel writes y over PCIe while it runs (LDG_OPT_ZERO_COPY).        */
 int ldg_residual_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
 int ldg_jacobian_assemble_host(ldg_ctx* ctx, const double* U, double t);
+/* R(U) and the Jacobian at U from one upload of U (a Newton step): second-
+ * order physics computes Q = D(U) once for both (Q_or_null receives it). */
+int ldg_residual_assemble_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
 int ldg_bsr_spmv_host(ldg_ctx* ctx, int which, const double* x, double* y);
 int ldg_split_matvec_host(ldg_ctx* ctx, double alpha_dt, const double* v, double* y);
+
+/* Execution options (defaults chosen by measurement).
+ *   LDG_OPT_SPMV_ROW_ORDER  block-SpMV / split-matvec row walk: 0 auto (reverse
+ *                           row order for K11 stores <= 1 GiB, whose tail is
+ *                           still L2-resident after the assembly), 1 forward,
+ *                           2 reverse.  Results are bitwise independent of it.
+ *   LDG_OPT_ZERO_COPY       1 (default): ldg_bsr_spmv_host(K11) writes y
+ *                           straight into mapped pinned memory; 0: staged copy.
+ * Returns LDG_ERR_INVALID_ARGUMENT for an unknown option or value.          */
+enum { LDG_OPT_SPMV_ROW_ORDER = 1, LDG_OPT_ZERO_COPY = 2 };
+int ldg_set_option(ldg_ctx* ctx, int option, int64_t value);
 
 /* Instrumentation: number of kernel launches issued by this context so far,
  * and the device-side byte footprint of the Jacobian store. */

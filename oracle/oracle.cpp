@@ -20,6 +20,7 @@
 // (include/linedg_b200.h: ldg_setup), read verbatim.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -111,15 +112,16 @@ struct Ctx {
     return side ? s : -s;
   }
   // Cholesky solve of one column in place (basis.cpp:81-88).
-  void mass_solve(double* x, int stride) const {
-    double y[MAXNP];
+  template <class T>
+  void mass_solve(T* x, int stride) const {
+    T y[MAXNP];
     for (int i = 0; i < np; ++i) {
-      double s = x[i * stride];
+      T s = x[i * stride];
       for (int j = 0; j < i; ++j) s -= L[i * np + j] * y[j];
       y[i] = s / L[i * np + i];
     }
     for (int i = np - 1; i >= 0; --i) {
-      double s = y[i];
+      T s = y[i];
       for (int j = i + 1; j < np; ++j) s -= L[j * np + i] * x[j * stride];
       x[i * stride] = s / L[i * np + i];
     }
@@ -363,16 +365,18 @@ void endpoint_flux(const Ctx& c, const T* ui, const T* qi, const T* uo, const T*
 
 // ----------------------------------------------------------------- gather
 
+template <class T = double>
 struct LineData {
-  double u[MAXNP][MAXM];
-  double q[MAXNP][MAXM * MAXD];
-  double uo[2][MAXM], qo[2][MAXM * MAXD];
+  T u[MAXNP][MAXM];
+  T q[MAXNP][MAXM * MAXD];
+  T uo[2][MAXM], qo[2][MAXM * MAXD];
   const double* bc[2];
   int bk[2];  // boundary kind of each end (-1 interior)
 };
 
-void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const double* Q,
-                 LineData& L) {
+template <class T>
+void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const T* Q,
+                 LineData<T>& L) {
   const int m = c.m, mD = c.m * c.D;
   for (int t = 0; t < c.np; ++t) {
     const size_t nd = static_cast<size_t>(e) * c.npe + c.node_on_line(dir, line, t);
@@ -399,19 +403,20 @@ void gather_line(const Ctx& c, int e, int dir, int line, const double* U, const 
 // --------------------------------------------------------------- residual
 
 // r^(dir) of one line (before the 1/J scaling), b = M^-1(...).
-void line_residual(const Ctx& c, int e, int dir, int line, const LineData& L, double r[][MAXM]) {
+template <class T>
+void line_residual(const Ctx& c, int e, int dir, int line, const LineData<T>& L, T r[][MAXM]) {
   const int m = c.m, np = c.np, nq = c.nq, D = c.D, mD = m * D;
   for (int i = 0; i < np; ++i)
     for (int k = 0; k < m; ++k) r[i][k] = 0.0;
   for (int q = 0; q < nq; ++q) {
-    double uq[MAXM] = {0}, qq[MAXM * MAXD] = {0};
+    T uq[MAXM] = {0}, qq[MAXM * MAXD] = {0};
     for (int t = 0; t < np; ++t) {
       const double ph = c.phi[t * nq + q];
       for (int k = 0; k < m; ++k) uq[k] += ph * L.u[t][k];
       if (c.second)
         for (int k = 0; k < mD; ++k) qq[k] += ph * L.q[t][k];
     }
-    double ft[MAXM];
+    T ft[MAXM];
     flux_dot(c, uq, qq, c.nv(e, dir, line, q), ft);
     for (int i = 0; i < np; ++i) {
       const double w = c.qw[q] * c.dphi[i * nq + q];
@@ -420,19 +425,20 @@ void line_residual(const Ctx& c, int e, int dir, int line, const LineData& L, do
   }
   for (int side = 0; side < 2; ++side) {
     const int ie = side ? c.p : 0;
-    double fh[MAXM];
-    endpoint_flux<double>(c, L.u[ie], L.q[ie], L.uo[side], L.qo[side], L.bc[side], L.bk[side],
+    T fh[MAXM];
+    endpoint_flux<T>(c, L.u[ie], L.q[ie], L.uo[side], L.qo[side], L.bc[side], L.bk[side],
                           c.ne(e, dir, side, line), c.sign(e, dir, side), fh);
     for (int k = 0; k < m; ++k) r[ie][k] += fh[k];
   }
   for (int k = 0; k < m; ++k) c.mass_solve(&r[0][k], MAXM);
 }
 
-void elem_residual(const Ctx& c, int e, const double* U, const double* Q, double* R) {
+template <class T>
+void elem_residual(const Ctx& c, int e, const double* U, const T* Q, double* R) {
   const int m = c.m, npe = c.npe;
-  std::vector<double> acc(static_cast<size_t>(npe) * m, 0.0);
-  LineData L;
-  double r[MAXNP][MAXM];
+  std::vector<T> acc(static_cast<size_t>(npe) * m, T(0.0));
+  LineData<T> L;
+  T r[MAXNP][MAXM];
   for (int dir = 0; dir < c.D; ++dir)
     for (int line = 0; line < c.NL; ++line) {
       gather_line(c, e, dir, line, U, Q, L);
@@ -446,19 +452,20 @@ void elem_residual(const Ctx& c, int e, const double* U, const double* Q, double
     const size_t g = static_cast<size_t>(e) * npe + nd;
     for (int k = 0; k < m; ++k) {
       const double s = c.source.empty() ? 0.0 : c.source[g * m + k];
-      R[g * m + k] = s - c.invJ[g] * acc[nd * m + k];
+      R[g * m + k] = static_cast<double>(s - c.invJ[g] * acc[nd * m + k]);
     }
   }
 }
 
 // d^(dir) of one line: M^-1 [u_hat (x) n at the ends - sum_q w phi' u_q (x) nvec_q].
-void line_gradient(const Ctx& c, int e, int dir, int line, const LineData& L,
-                   double d[][MAXM * MAXD]) {
+template <class T>
+void line_gradient(const Ctx& c, int e, int dir, int line, const LineData<T>& L,
+                   T d[][MAXM * MAXD]) {
   const int m = c.m, np = c.np, nq = c.nq, D = c.D, mD = m * D;
   for (int i = 0; i < np; ++i)
     for (int k = 0; k < mD; ++k) d[i][k] = 0.0;
   for (int q = 0; q < nq; ++q) {
-    double uq[MAXM] = {0};
+    T uq[MAXM] = {0};
     for (int t = 0; t < np; ++t)
       for (int k = 0; k < m; ++k) uq[k] += c.phi[t * nq + q] * L.u[t][k];
     const double* nvq = c.nv(e, dir, line, q);
@@ -471,13 +478,14 @@ void line_gradient(const Ctx& c, int e, int dir, int line, const LineData& L,
   for (int side = 0; side < 2; ++side) {
     const int ie = side ? c.p : 0;
     const double* n = c.ne(e, dir, side, line);
-    const double* uh;
-    double uhw[MAXM];
+    const T* uh;
+    T uhw[MAXM];
     if (L.bc[side] && L.bk[side] == LDG_BC_NO_SLIP_ADIABATIC) {  // mixed: momentum 0, rho and E interior
       for (int k = 0; k < m; ++k) uhw[k] = uhat_inner_c(L.bk[side], k, m) ? L.u[ie][k] : 0.0;
       uh = uhw;
     } else if (L.bc[side] && !uhat_inner(L.bk[side])) {
-      uh = L.bc[side];  // u_hat = g_D
+      for (int k = 0; k < m; ++k) uhw[k] = L.bc[side][k];  // u_hat = g_D
+      uh = uhw;
     } else if (L.bc[side]) {
       uh = L.u[ie];  // Neumann-type / slip wall
     }
@@ -488,14 +496,15 @@ void line_gradient(const Ctx& c, int e, int dir, int line, const LineData& L,
   for (int k = 0; k < mD; ++k) c.mass_solve(&d[0][k], MAXM * MAXD);
 }
 
-void elem_gradient(const Ctx& c, int e, const double* U, double* Q) {
+template <class T>
+void elem_gradient(const Ctx& c, int e, const double* U, T* Q) {
   const int mD = c.m * c.D, npe = c.npe;
-  std::vector<double> acc(static_cast<size_t>(npe) * mD, 0.0);
-  LineData L;
-  double d[MAXNP][MAXM * MAXD];
+  std::vector<T> acc(static_cast<size_t>(npe) * mD, T(0.0));
+  LineData<T> L;
+  T d[MAXNP][MAXM * MAXD];
   for (int dir = 0; dir < c.D; ++dir)
     for (int line = 0; line < c.NL; ++line) {
-      gather_line(c, e, dir, line, U, nullptr, L);
+      gather_line<T>(c, e, dir, line, U, nullptr, L);
       line_gradient(c, e, dir, line, L, d);
       for (int t = 0; t < c.np; ++t) {
         const int nd = c.node_on_line(dir, line, t);
@@ -654,7 +663,7 @@ template <int NU, int NQ>
 void elem_jacobian(Ctx& c, int e, const double* U, const double* Q) {
   const int m = c.m, np = c.np, nq = c.nq, D = c.D, mD = m * D;
   const int64_t base = static_cast<int64_t>(e) * c.npe;
-  LineData L;
+  LineData<> L;
   using DU = Dual<NU>;
   using DQ = Dual<NQ>;
   auto addblk = [&](int which, int64_t row, int64_t col, const double* blk, double scale) {
@@ -904,12 +913,14 @@ JacFn pick_jac(int m, int D) {
 
 // -------------------------------------------------------------- public ops
 
-void residual(const Ctx& c, const double* U, const double* Q, double* R,
+template <class T>
+void residual(const Ctx& c, const double* U, const T* Q, double* R,
               const std::vector<int>* subset = nullptr) {
-  for_elems(c, subset, [&](int e) { elem_residual(c, e, U, Q, R); });
+  for_elems(c, subset, [&](int e) { elem_residual<T>(c, e, U, Q, R); });
 }
-void gradient(const Ctx& c, const double* U, double* Q, const std::vector<int>* subset = nullptr) {
-  for_elems(c, subset, [&](int e) { elem_gradient(c, e, U, Q); });
+template <class T>
+void gradient(const Ctx& c, const double* U, T* Q, const std::vector<int>* subset = nullptr) {
+  for_elems(c, subset, [&](int e) { elem_gradient<T>(c, e, U, Q); });
 }
 
 // ------------------------------------------------------------ flop counting
@@ -1172,7 +1183,35 @@ int lo_residual(lo_ctx* x, const double* U, double t, double* R, double* Qout,
       gradient(c, U, Q);
       residual(c, U, Q, R, sp);
     } else {
-      residual(c, U, nullptr, R, sp);
+      residual<double>(c, U, nullptr, R, sp);
+    }
+  });
+}
+
+// Extended-precision residual (x87 80-bit long double, 64-bit significand):
+// the same restatement evaluated with every intermediate -- interpolated
+// states, fluxes, line projections, the mass solve, the direction sum and, for
+// second-order physics, Q -- carried in long double and rounded to double once
+// at the end.  Inputs (U, metric, basis tables) are the same doubles.  Used by
+// the parity tests as the accuracy yardstick on near-steady states where the
+// residual is a large cancellation.
+int lo_residual_ext(lo_ctx* x, const double* U, double t, double* R, const int32_t* elems,
+                    int32_t n_sub) {
+  return guarded([&] {
+    Ctx& c = x->c;
+    refresh_boundary(c, t);
+    std::vector<int> sub;
+    const std::vector<int>* sp = nullptr;
+    if (elems) {
+      sub = subset_of(elems, n_sub);
+      sp = &sub;
+    }
+    if (c.second) {
+      std::vector<long double> Q(static_cast<size_t>(c.E) * c.npe * c.m * c.D, 0.0L);
+      gradient<long double>(c, U, Q.data());
+      residual<long double>(c, U, Q.data(), R, sp);
+    } else {
+      residual<long double>(c, U, nullptr, R, sp);
     }
   });
 }
@@ -1294,6 +1333,97 @@ int lo_spmv(const lo_ctx* x, int32_t which, const double* v, double* y) {
       }
       for (int a = 0; a < K.br; ++a) y[r * K.br + a] = acc[a];
     }
+  });
+}
+
+// CPU baseline sample (bench.py's cpu_baseline leg and --impl reference):
+// one bounded, cost-proportional sample of the bench step on the elements
+// `elems` with `threads` OpenMP threads -- gradient (second order), residual,
+// analytic Jacobian values (the pattern of the subset is built once, untimed,
+// like the device store layout at context creation) and `nmv` matvecs over the
+// subset's rows (K21 rows then v - adt (K11 v + K12 w), or K11 v for first-order
+// physics).  Each phase is timed with steady_clock; secs[0..3] = gradient,
+// residual, Jacobian, all matvecs, each the median over `reps` repetitions.
+// Per element this is exactly the work of the full step, so the full-mesh time
+// extrapolates linearly (t_full = t_sample E / n).
+int lo_time_sample(lo_ctx* x, const double* U, const double* v, double adt, int32_t nmv, const int32_t* elems,
+                   int32_t n_sub, int32_t threads, int32_t reps, double* secs) {
+  return guarded([&] {
+    Ctx& c = x->c;
+#ifdef _OPENMP
+    const int old = omp_get_max_threads();
+    omp_set_num_threads(threads > 0 ? threads : old);
+#endif
+    refresh_boundary(c, 0.0);
+    std::vector<int> sub = subset_of(elems, n_sub);
+    const int nm = c.second ? 3 : 1;
+    for (int w = 0; w < nm; ++w) {
+      build_pattern(c, w, &sub);
+      c.K[w].subset = true;
+    }
+    const size_t nU = static_cast<size_t>(c.E) * c.npe * c.m;
+    std::vector<double> Q(c.second ? nU * c.D : 0, 0.0), R(nU, 0.0), y(nU, 0.0), wv(c.second ? nU * c.D : 0, 0.0);
+    JacFn jf = pick_jac(c.m, c.D);
+    using clk = std::chrono::steady_clock;
+    auto since = [](clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); };
+    std::vector<double> tg, tr, tj, tm;
+    const int ns = static_cast<int>(sub.size());
+    auto rows_mv = [&](const BlockMat& K, const double* xv, double* out, int64_t row0) {
+      double acc[MAXM * MAXD] = {0};
+      for (int64_t k = K.rowptr[row0]; k < K.rowptr[row0 + 1]; ++k) {
+        const double* blk = &K.val[k * K.br * K.bc];
+        const double* xx = xv + K.col[k] * K.bc;
+        for (int a = 0; a < K.br; ++a)
+          for (int b = 0; b < K.bc; ++b) acc[a] += blk[a * K.bc + b] * xx[b];
+      }
+      for (int a = 0; a < K.br; ++a) out[a] += acc[a];
+    };
+    for (int rep = 0; rep < (reps > 0 ? reps : 1); ++rep) {
+      auto t0 = clk::now();
+      if (c.second) gradient<double>(c, U, Q.data(), &sub);
+      tg.push_back(since(t0));
+      t0 = clk::now();
+      residual<double>(c, U, c.second ? Q.data() : nullptr, R.data(), &sub);
+      tr.push_back(since(t0));
+      for (int w = 0; w < nm; ++w) std::fill(c.K[w].val.begin(), c.K[w].val.end(), 0.0);
+      t0 = clk::now();
+      for_elems(c, &sub, [&](int e) { jf(c, e, U, c.second ? Q.data() : nullptr); });
+      tj.push_back(since(t0));
+      t0 = clk::now();
+      for (int k = 0; k < nmv; ++k) {
+        if (c.second) {
+#pragma omp parallel for schedule(static)
+          for (int i = 0; i < ns; ++i)
+            for (int nd = 0; nd < c.npe; ++nd) {
+              const int64_t r = static_cast<int64_t>(sub[i]) * c.npe + nd;
+              double* o = &wv[r * c.m * c.D];
+              for (int a = 0; a < c.m * c.D; ++a) o[a] = 0.0;
+              rows_mv(c.K[LDG_K21], v, o, r);
+            }
+        }
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < ns; ++i)
+          for (int nd = 0; nd < c.npe; ++nd) {
+            const int64_t r = static_cast<int64_t>(sub[i]) * c.npe + nd;
+            double a[MAXM] = {0};
+            rows_mv(c.K[LDG_K11], v, a, r);
+            if (c.second) rows_mv(c.K[LDG_K12], wv.data(), a, r);
+            for (int q = 0; q < c.m; ++q) y[r * c.m + q] = v[r * c.m + q] - adt * a[q];
+          }
+      }
+      tm.push_back(since(t0));
+    }
+    auto med = [](std::vector<double> t) {
+      std::sort(t.begin(), t.end());
+      return t[t.size() / 2];
+    };
+    secs[0] = med(tg);
+    secs[1] = med(tr);
+    secs[2] = med(tj);
+    secs[3] = med(tm);
+#ifdef _OPENMP
+    omp_set_num_threads(old);
+#endif
   });
 }
 

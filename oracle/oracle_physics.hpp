@@ -75,10 +75,12 @@ template <int N> inline Dual<N> sqrt(const Dual<N>& a) {
 template <int N> inline Dual<N> abs(const Dual<N>& a) { return a.v >= 0.0 ? a : -a; }
 template <int N> inline Dual<N> max(const Dual<N>& a, const Dual<N>& b) { return a.v >= b.v ? a : b; }
 inline double value_of(double x) { return x; }
+inline double value_of(long double x) { return static_cast<double>(x); }
 template <int N> inline double value_of(const Dual<N>& x) { return x.v; }
 using std::abs;
 using std::sqrt;
 inline double max(double a, double b) { return a >= b ? a : b; }
+inline long double max(long double a, long double b) { return a >= b ? a : b; }
 
 // Raised on rho <= 0 or p <= 0 (errors.hpp:10-18; physics.hpp:192).
 struct physical_state_error : std::runtime_error {

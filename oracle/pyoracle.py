@@ -47,6 +47,9 @@ def lib():
         L.lo_gradient.argtypes = [vp, _dp, C.c_double, _dp]
         L.lo_residual_uq.argtypes = [vp, _dp, _dp, C.c_double, _dp]
         L.lo_residual.argtypes = [vp, _dp, C.c_double, _dp, _dp, _ip, C.c_int32]
+        L.lo_residual_ext.argtypes = [vp, _dp, C.c_double, _dp, _ip, C.c_int32]
+        L.lo_time_sample.argtypes = [vp, _dp, _dp, C.c_double, C.c_int32, _ip, C.c_int32, C.c_int32,
+                                     C.c_int32, _dp]
         L.lo_assemble.argtypes = [vp, _dp, C.c_double, _ip, C.c_int32]
         L.lo_assemble_uq.argtypes = [vp, _dp, _dp]
         L.lo_pattern_info.argtypes = [vp, C.c_int32, _lp, _ip, _ip]
@@ -138,6 +141,28 @@ class Oracle:
                                        None if el is None else el.ctypes.data_as(_ip),
                                        0 if el is None else len(el)))
         return (R, Q) if want_q else R
+
+    def residual_ext(self, U, t=0.0, elems: Optional[Sequence[int]] = None):
+        """The residual evaluated in x87 long double (64-bit significand) and
+        rounded once: the accuracy yardstick for ill-conditioned states."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        R = np.zeros(self.n_dofs)
+        el = None if elems is None else np.ascontiguousarray(elems, dtype=np.int32)
+        self._check(self.L.lo_residual_ext(self.h, _d(U), t, _d(R),
+                                           None if el is None else el.ctypes.data_as(_ip),
+                                           0 if el is None else len(el)))
+        return R
+
+    def time_sample(self, U, v, adt, nmv, elems, threads, reps=3):
+        """CPU baseline sample: median seconds of (gradient, residual, Jacobian,
+        nmv matvecs) over the elements `elems` (lo_time_sample)."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        el = np.ascontiguousarray(elems, dtype=np.int32)
+        secs = np.zeros(4)
+        self._check(self.L.lo_time_sample(self.h, _d(U), _d(v), adt, nmv, el.ctypes.data_as(_ip), len(el),
+                                          threads, reps, _d(secs)))
+        return secs
 
     def gradient(self, U, t=0.0):
         U = np.ascontiguousarray(U, dtype=np.float64)

@@ -23,6 +23,7 @@ LDG_BC_CHARACTERISTIC = 2
 LDG_BC_SLIP_WALL = 3
 LDG_BC_NO_SLIP_ADIABATIC = 4
 LDG_K11, LDG_K12, LDG_K21 = 0, 1, 2
+LDG_OPT_SPMV_ROW_ORDER, LDG_OPT_ZERO_COPY = 1, 2
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -210,7 +211,8 @@ GPU_SYMBOLS = [
     "ldg_kernel_launches", "ldg_jacobian_bytes",
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
     "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv", "ldg_steady_solve",
-    "ldg_set_boundary_function", "ldg_set_precond_mode",
+    "ldg_set_boundary_function", "ldg_set_precond_mode", "ldg_set_option", "ldg_jacobian_assemble_q",
+    "ldg_residual_assemble_host",
 ]
 
 
@@ -235,6 +237,7 @@ def gpu_lib() -> C.CDLL:
         L.ldg_residual_uq.argtypes = [vp, vp, vp, C.c_double, vp]
         L.ldg_gradient.argtypes = [vp, vp, C.c_double, vp]
         L.ldg_jacobian_assemble.argtypes = [vp, vp, C.c_double]
+        L.ldg_jacobian_assemble_q.argtypes = [vp, vp, vp, C.c_double]
         L.ldg_pattern_info_get.argtypes = [vp, C.c_int, C.POINTER(LdgPatternInfo)]
         L.ldg_bsr_spmv.argtypes = [vp, C.c_int, vp, vp]
         L.ldg_split_matvec.argtypes = [vp, C.c_double, vp, vp]
@@ -244,6 +247,7 @@ def gpu_lib() -> C.CDLL:
         L.ldg_synchronize.argtypes = [vp]
         L.ldg_residual_host.argtypes = [vp, _dp, C.c_double, _dp, _dp]
         L.ldg_jacobian_assemble_host.argtypes = [vp, _dp, C.c_double]
+        L.ldg_residual_assemble_host.argtypes = [vp, _dp, C.c_double, _dp, _dp]
         L.ldg_bsr_spmv_host.argtypes = [vp, C.c_int, _dp, _dp]
         L.ldg_split_matvec_host.argtypes = [vp, C.c_double, _dp, _dp]
         L.ldg_precond_build.argtypes = [vp, C.c_double]
@@ -257,6 +261,7 @@ def gpu_lib() -> C.CDLL:
         L.ldg_dirk3_step.argtypes = [vp, vp, C.c_double, C.c_double, C.POINTER(LdgNewtonCfg),
                                      C.POINTER(LdgSolverStats)]
         L.ldg_set_precond_mode.argtypes = [vp, C.c_int]
+        L.ldg_set_option.argtypes = [vp, C.c_int, C.c_int64]
         L.ldg_set_boundary_function.argtypes = [vp, C.c_int32, BC_FN, vp]
         L.ldg_steady_solve.argtypes = [vp, vp, C.c_double, C.POINTER(LdgSteadyCfg), C.POINTER(LdgSolverStats)]
         L.ldg_write_triplets.argtypes = [vp, C.c_int, C.c_char_p]

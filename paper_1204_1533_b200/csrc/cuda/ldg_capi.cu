@@ -123,9 +123,15 @@ struct ldg_ctx {
               ev_out_r = nullptr, ev_out_y = nullptr, ev_join = nullptr;
   double* d_hx = nullptr;
   double* d_hy = nullptr;
+  // split_matvec_host staging ring (asynchronous mode)
+  double* d_mv_in[2] = {nullptr, nullptr};
+  double* d_mv_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_mv_free[2] = {nullptr, nullptr}, ev_mv_out[2] = {nullptr, nullptr};
+  int mv_slot = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
   bool sync_errors = true;
+  bool zero_copy = true;  // LDG_OPT_ZERO_COPY
   std::string err;
   int err_elem = -1, err_node = -1;
   double err_state[8] = {0};
@@ -168,6 +174,12 @@ struct ldg_ctx {
     if (cs_out) cudaStreamDestroy(cs_out);
     cudaFree(d_hx);
     cudaFree(d_hy);
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(d_mv_in[k]);
+      cudaFree(d_mv_out[k]);
+      if (ev_mv_free[k]) cudaEventDestroy(ev_mv_free[k]);
+      if (ev_mv_out[k]) cudaEventDestroy(ev_mv_out[k]);
+    }
     if (h_err) cudaFreeHost(h_err);
   }
 
@@ -412,13 +424,10 @@ std::vector<double> spd_inverse(const double* A, int n) {
 // mesh in storage order has none).  Default: Morton (Z-order) of the element
 // centroids on a 2^(60/D)-per-axis grid over the bounding box, ties by id;
 // without node coordinates a breadth-first order over the face graph.
-// LDG_ORDER=identity keeps the storage order.
 std::vector<int32_t> processing_order(const ldg_setup& s, int D, int npe) {
   const int E = s.n_elems;
   std::vector<int32_t> ord(E);
   for (int e = 0; e < E; ++e) ord[e] = e;
-  const char* env = std::getenv("LDG_ORDER");
-  if (env && std::string(env) == "identity") return ord;
   if (s.node_coords) {
     std::vector<double> cen(static_cast<size_t>(E) * D, 0.0);
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -599,6 +608,14 @@ int finish(ldg_ctx* c, cudaError_t launch) {
     return LDG_ERR_PHYSICAL_STATE;
   }
   return LDG_OK;
+}
+
+// Device vectors are read with 16-byte vector / bulk-async loads: reject a
+// misaligned pointer (e.g. a view at an odd element offset) instead of letting
+// it fault the context.
+void check_aligned(const void* p, const char* what) {
+  if (reinterpret_cast<uintptr_t>(p) & 15u)
+    throw ldg_error(LDG_ERR_INVALID_ARGUMENT, std::string(what) + " must be 16-byte aligned");
 }
 
 double* ensure(double*& p, size_t n) {
@@ -876,7 +893,8 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     ck(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking), "create upload stream");
     ck(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking), "create download stream");
     for (cudaEvent_t* ev : {&c->ev_in, &c->ev_k, &c->ev_free_hu, &c->ev_free_hu2, &c->ev_free_hx, &c->ev_out_r,
-                            &c->ev_out_y, &c->ev_join}) {
+                            &c->ev_out_y, &c->ev_join, &c->ev_mv_free[0], &c->ev_mv_free[1], &c->ev_mv_out[0],
+                            &c->ev_mv_out[1]}) {
       ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "create event");
       ck(cudaEventRecord(*ev, c->stream), "record event");  // completed: nothing to wait for yet
     }
@@ -899,8 +917,7 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     d.E = c->E;
     d.inv_order = c->d_inv_order;
     {
-      const char* fs = std::getenv("LDG_FACE_SHARE");
-      build_face_sharing(*c, o.chunk_elems(c->E), !(fs && std::string(fs) == "0"));
+      build_face_sharing(*c, o.chunk_elems(c->E), true);
       d.fpart = c->d_fpart;
       d.owned = c->d_owned;
       d.owned_off = c->owned_off.data();
@@ -928,6 +945,20 @@ int64_t ldg_num_dofs(const ldg_ctx* c) { return static_cast<int64_t>(c->nU()); }
 int64_t ldg_kernel_launches(const ldg_ctx* c) { return c->launches; }
 int64_t ldg_jacobian_bytes(const ldg_ctx* c) {
   return static_cast<int64_t>((c->n11 + c->n12 + c->n21) * sizeof(double));
+}
+int ldg_set_option(ldg_ctx* c, int option, int64_t value) {
+  return guarded(c, [&]() -> int {
+    if (option == LDG_OPT_SPMV_ROW_ORDER) {
+      if (value < 0 || value > 2) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "row order must be 0, 1 or 2");
+      c->dc.spmv_order = static_cast<int>(value);
+    } else if (option == LDG_OPT_ZERO_COPY) {
+      if (value != 0 && value != 1) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "zero copy must be 0 or 1");
+      c->zero_copy = value != 0;
+    } else {
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "unknown option " + std::to_string(option));
+    }
+    return LDG_OK;
+  });
 }
 int ldg_set_sync_errors(ldg_ctx* c, int on) {
   c->sync_errors = on != 0;
@@ -1020,6 +1051,8 @@ int ldg_set_boundary_function(ldg_ctx* c, int32_t tag, ldg_bc_fn fn, void* user)
 
 int ldg_gradient(ldg_ctx* c, const double* U, double t, double* Q) {
   return guarded(c, [&]() -> int {
+    check_aligned(U, "U");
+    check_aligned(Q, "Q");
     refresh_boundary(c, t);
     if (!c->second) throw ldg_error(LDG_ERR_CONFIG, "gradient_residual needs second-order physics");
     return finish(c, c->ops->gradient(c->dc, U, Q));
@@ -1028,6 +1061,9 @@ int ldg_gradient(ldg_ctx* c, const double* U, double t, double* Q) {
 
 int ldg_residual_uq(ldg_ctx* c, const double* U, const double* Q, double t, double* R) {
   return guarded(c, [&]() -> int {
+    check_aligned(U, "U");
+    check_aligned(R, "R");
+    if (c->second) check_aligned(Q, "Q");
     refresh_boundary(c, t);
     if (!c->second) return finish(c, c->ops->residual(c->dc, U, nullptr, R));
     return finish(c, c->ops->residual(c->dc, U, Q, R));
@@ -1036,6 +1072,9 @@ int ldg_residual_uq(ldg_ctx* c, const double* U, const double* Q, double t, doub
 
 int ldg_residual(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
   return guarded(c, [&]() -> int {
+    check_aligned(U, "U");
+    check_aligned(R, "R");
+    if (Q) check_aligned(Q, "Q");
     refresh_boundary(c, t);
     if (!c->second) return finish(c, c->ops->residual(c->dc, U, nullptr, R));
     double* q = Q ? Q : ensure(c->d_Q, c->nQ());
@@ -1044,38 +1083,62 @@ int ldg_residual(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
   });
 }
 
-int ldg_jacobian_assemble(ldg_ctx* c, const double* U, double t) {
-  return guarded(c, [&]() -> int {
-    refresh_boundary(c, t);
-    const ldg::Ops& o = *c->ops;
-    if (o.jac_smem > 227 * 1024)
-      throw ldg_error(LDG_ERR_CONFIG, "Jacobian tile of this configuration exceeds shared memory (" +
-                                          std::to_string(o.jac_smem) + " B)");
-    const size_t rows = static_cast<size_t>(c->E) * c->npe;
-    if (!c->d_K11) {
-      c->n11 = rows * o.NS11 * o.B11;
-      ck(cudaMalloc(&c->d_K11, c->n11 * sizeof(double)), "cudaMalloc K11");
-      if (c->second) {
-        c->n12 = rows * o.NS12 * o.B12;
-        c->n21 = rows * o.NS12 * c->D;
-        ck(cudaMalloc(&c->d_K12, c->n12 * sizeof(double)), "cudaMalloc K12");
-        ck(cudaMalloc(&c->d_K21, c->n21 * sizeof(double)), "cudaMalloc K21");
-      }
-    }
-    const double* q = nullptr;
+namespace {
+// Assembly at (U, Q): Q = D(U) already on the device (second-order physics),
+// or computed here when q_given is null.
+int assemble_at(ldg_ctx* c, const double* U, const double* q_given, double t) {
+  refresh_boundary(c, t);
+  const ldg::Ops& o = *c->ops;
+  if (o.jac_smem > 227 * 1024)
+    throw ldg_error(LDG_ERR_CONFIG, "Jacobian tile of this configuration exceeds shared memory (" +
+                                        std::to_string(o.jac_smem) + " B)");
+  const size_t rows = static_cast<size_t>(c->E) * c->npe;
+  if (!c->d_K11) {
+    c->n11 = rows * o.NS11 * o.B11;
+    ck(cudaMalloc(&c->d_K11, c->n11 * sizeof(double)), "cudaMalloc K11");
     if (c->second) {
+      c->n12 = rows * o.NS12 * o.B12;
+      c->n21 = rows * o.NS12 * c->D;
+      ck(cudaMalloc(&c->d_K12, c->n12 * sizeof(double)), "cudaMalloc K12");
+      ck(cudaMalloc(&c->d_K21, c->n21 * sizeof(double)), "cudaMalloc K21");
+    }
+  }
+  const double* q = nullptr;
+  if (c->second) {
+    if (q_given) {
+      q = q_given;
+    } else {
       q = ensure(c->d_Q, c->nQ());
       ck(o.gradient(c->dc, U, c->d_Q), "gradient launch");
-      // K21 is U- and t-independent: assembled once.
-      if (!c->k21_valid) {
-        ck(o.k21(c->dc, c->d_K21), "K21 launch");
-        c->k21_valid = true;
-      }
     }
-    ensure(c->d_SE, o.scratch_elems(c->E));
-    const int st = finish(c, o.jacobian(c->dc, U, q, c->d_SE, c->d_K11, c->d_K12));
-    c->jac_valid = st == LDG_OK;
-    return st;
+    // K21 is U- and t-independent: assembled once.
+    if (!c->k21_valid) {
+      ck(o.k21(c->dc, c->d_K21), "K21 launch");
+      c->k21_valid = true;
+    }
+  }
+  ensure(c->d_SE, o.scratch_elems(c->E));
+  // a new Jacobian invalidates the block-Jacobi factors built from the old one
+  c->pc_valid = false;
+  const int st = finish(c, o.jacobian(c->dc, U, q, c->d_SE, c->d_K11, c->d_K12));
+  c->jac_valid = st == LDG_OK;
+  return st;
+}
+}  // namespace
+
+int ldg_jacobian_assemble(ldg_ctx* c, const double* U, double t) {
+  return guarded(c, [&]() -> int {
+    check_aligned(U, "U");
+    return assemble_at(c, U, nullptr, t);
+  });
+}
+
+int ldg_jacobian_assemble_q(ldg_ctx* c, const double* U, const double* Q, double t) {
+  return guarded(c, [&]() -> int {
+    if (c->second && !Q) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "Q required for second-order physics");
+    check_aligned(U, "U");
+    if (Q) check_aligned(Q, "Q");
+    return assemble_at(c, U, c->second ? Q : nullptr, t);
   });
 }
 
@@ -1288,6 +1351,8 @@ int ldg_write_sparsity_csv(ldg_ctx* c, int which, const char* path, int append) 
 
 int ldg_bsr_spmv(ldg_ctx* c, int which, const double* x, double* y) {
   return guarded(c, [&]() -> int {
+    check_aligned(x, "x");
+    check_aligned(y, "y");
     if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
     const ldg::Ops& o = *c->ops;
     if (which == LDG_K11) return finish(c, o.spmv11(c->dc, c->d_K11, x, y));
@@ -1300,6 +1365,8 @@ int ldg_bsr_spmv(ldg_ctx* c, int which, const double* x, double* y) {
 
 int ldg_split_matvec(ldg_ctx* c, double adt, const double* v, double* y) {
   return guarded(c, [&]() -> int {
+    check_aligned(v, "v");
+    check_aligned(y, "y");
     if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
     const ldg::Ops& o = *c->ops;
     const double* w = nullptr;
@@ -1350,6 +1417,8 @@ int ldg_set_precond_mode(ldg_ctx* c, int mode) {
 
 int ldg_precond_apply(ldg_ctx* c, const double* r, double* z) {
   return guarded(c, [&]() -> int {
+    check_aligned(r, "r");
+    check_aligned(z, "z");
     if (!c->pc_valid) throw ldg_error(LDG_ERR_SOLVER, "preconditioner not built");
     const ldg::Ops& o = *c->ops;
     return finish(c, o.pc_apply(c->dc, c->d_pcLU, c->d_pcPiv, r, z));
@@ -1362,6 +1431,8 @@ int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rt
     if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
     if (!(rtol > 0.0) || maxit < 1 || restart < 1 || !b || !x)
       throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "gmres: rtol > 0, maxit >= 1, restart >= 1 and vectors required");
+    check_aligned(b, "b");
+    check_aligned(x, "x");
     if (use_precond && !c->pc_valid) throw ldg_error(LDG_ERR_SOLVER, "preconditioner not built");
     const ldg::Ops& o = *c->ops;
     const size_t n = c->nU();
@@ -1793,15 +1864,15 @@ int ldg_steady_solve(ldg_ctx* c, double* U, double t, const ldg_steady_cfg* cfg,
 namespace {
 // device address of a mapped pinned host buffer (cudaHostAlloc / registered
 // memory under unified addressing), else nullptr
-double* mapped_host(double* h) {
+double* mapped_host(const ldg_ctx* c, double* h) {
+  if (!c->zero_copy) return nullptr;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
     (void)cudaGetLastError();
     return nullptr;
   }
   if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
-  static const char* env = std::getenv("LDG_ZERO_COPY");  // 0 disables (A/B)
-  if (env && std::atoi(env) == 0) return nullptr;
+  if (reinterpret_cast<uintptr_t>(a.devicePointer) & 15u) return nullptr;  // staged copy instead
   return static_cast<double*>(a.devicePointer);
 }
 // upload n doubles to dbuf once `free_ev` (the last reader of dbuf) completed;
@@ -1857,6 +1928,42 @@ int ldg_residual_host(ldg_ctx* c, const double* U, double t, double* R, double* 
   });
 }
 
+// Residual and Jacobian at one state from ONE upload of U (a Newton step's
+// R(U) and J(U)): second-order physics computes Q = D(U) once for both.
+int ldg_residual_assemble_host(ldg_ctx* c, const double* U, double t, double* R, double* Q) {
+  return guarded(c, [&]() -> int {
+    ensure(c->d_hu, c->nU());
+    ensure(c->d_hr, c->nU());
+    double* dq = c->second ? ensure(c->d_Q, c->nQ()) : nullptr;
+    const size_t nb = c->nU() * sizeof(double);
+    if (!c->sync_errors) {
+      upload_async(c, c->d_hu, U, c->nU(), c->ev_free_hu);
+      ck(cudaStreamWaitEvent(c->stream, c->ev_out_r, 0), "wait R/Q download");  // d_hr, d_Q reuse
+      int st = ldg_residual(c, c->d_hu, t, c->d_hr, dq);
+      if (st != LDG_OK) return st;
+      ck(cudaEventRecord(c->ev_k, c->stream), "record kernels");
+      ck(cudaStreamWaitEvent(c->cs_out, c->ev_k, 0), "wait kernels");
+      ck(cudaMemcpyAsync(R, c->d_hr, nb, cudaMemcpyDeviceToHost, c->cs_out), "D2H R");
+      if (Q && dq) ck(cudaMemcpyAsync(Q, dq, nb * c->D, cudaMemcpyDeviceToHost, c->cs_out), "D2H Q");
+      ck(cudaEventRecord(c->ev_out_r, c->cs_out), "record download");
+      st = assemble_at(c, c->d_hu, dq, t);  // the download overlaps the assembly
+      if (st != LDG_OK) return st;
+      ck(cudaEventRecord(c->ev_free_hu, c->stream), "record");
+      return LDG_OK;
+    }
+    ck(cudaMemcpyAsync(c->d_hu, U, nb, cudaMemcpyHostToDevice, c->stream), "H2D U");
+    c->sync_errors = false;
+    int st = ldg_residual(c, c->d_hu, t, c->d_hr, dq);
+    if (st == LDG_OK) {
+      ck(cudaMemcpyAsync(R, c->d_hr, nb, cudaMemcpyDeviceToHost, c->stream), "D2H R");
+      if (Q && dq) ck(cudaMemcpyAsync(Q, dq, nb * c->D, cudaMemcpyDeviceToHost, c->stream), "D2H Q");
+      st = assemble_at(c, c->d_hu, dq, t);
+    }
+    c->sync_errors = true;
+    return st == LDG_OK ? finish(c, cudaSuccess) : st;
+  });
+}
+
 int ldg_jacobian_assemble_host(ldg_ctx* c, const double* U, double t) {
   return guarded(c, [&]() -> int {
     ensure(c->d_hu2, c->nU());
@@ -1887,7 +1994,7 @@ int ldg_bsr_spmv_host(ldg_ctx* c, int which, const double* x, double* y) {
     // written by the kernel itself (whole node rows per warp store, see
     // k_spmv11), so the PCIe transfer of y overlaps the product instead of
     // following it; pageable buffers take the staged copy
-    double* yz = which == LDG_K11 && c->ops->M == 4 ? mapped_host(y) : nullptr;
+    double* yz = which == LDG_K11 && c->ops->M == 4 ? mapped_host(c, y) : nullptr;
     auto product = [&](double* dst) -> int {
       if (!yz) return ldg_bsr_spmv(c, which, dx, dst);
       if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
@@ -1928,20 +2035,31 @@ int ldg_bsr_spmv_host(ldg_ctx* c, int which, const double* x, double* y) {
 
 int ldg_split_matvec_host(ldg_ctx* c, double adt, const double* v, double* y) {
   return guarded(c, [&]() -> int {
-    ensure(c->d_hu, c->nU());
-    ensure(c->d_hr, c->nU());
-    ck(cudaMemcpyAsync(c->d_hu, v, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D v");
-    const bool was = c->sync_errors;
+    const size_t n = c->nU();
+    if (!c->sync_errors) {
+      // two staging slots: the upload of the next v and the download of the
+      // previous y overlap this product (GMRES-style back-to-back calls)
+      const int s = c->mv_slot;
+      c->mv_slot ^= 1;
+      double* dv = ensure(c->d_mv_in[s], n);
+      double* dy = ensure(c->d_mv_out[s], n);
+      upload_async(c, dv, v, n, c->ev_mv_free[s]);
+      ck(cudaStreamWaitEvent(c->stream, c->ev_mv_out[s], 0), "wait y download");
+      const int st = ldg_split_matvec(c, adt, dv, dy);
+      if (st != LDG_OK) return st;
+      ck(cudaEventRecord(c->ev_mv_free[s], c->stream), "record");
+      download_async(c, y, dy, n, c->ev_mv_out[s]);
+      return LDG_OK;
+    }
+    ensure(c->d_hu, n);
+    ensure(c->d_hr, n);
+    ck(cudaMemcpyAsync(c->d_hu, v, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D v");
     c->sync_errors = false;
     int st = ldg_split_matvec(c, adt, c->d_hu, c->d_hr);
-    c->sync_errors = was;
-    if (st != LDG_OK) return st;
-    ck(cudaMemcpyAsync(y, c->d_hr, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H y");
-    const bool w2 = c->sync_errors;
     c->sync_errors = true;
-    st = finish(c, cudaSuccess);
-    c->sync_errors = w2;
-    return st;
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(y, c->d_hr, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H y");
+    return finish(c, cudaSuccess);
   });
 }
 

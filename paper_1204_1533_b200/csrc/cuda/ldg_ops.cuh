@@ -40,6 +40,7 @@ struct DevCtx {
   const int32_t* bspec = nullptr;     // slip-wall / Neumann boundary faces, chunk by chunk
   const int64_t* bspec_off = nullptr; // host offsets into bspec
   int E = 0;
+  int spmv_order = 0;  // LDG_OPT_SPMV_ROW_ORDER: 0 auto, 1 forward, 2 reverse
   long long* launches = nullptr;
 };
 
@@ -340,10 +341,9 @@ struct Launch {
     const long long threads = (rows + 31) / 32 * 32 * C::M;
     return static_cast<int>((threads + 127) / 128);
   }
-  // reverse row order for small stores (see k_spmv11); LDG_SPMV_REVERSE=0/1 forces it
+  // reverse row order for small stores (see k_spmv11); LDG_OPT_SPMV_ROW_ORDER forces it
   static int spmv_rev(const DevCtx& d) {
-    static const char* env = std::getenv("LDG_SPMV_REVERSE");
-    if (env) return std::atoi(env) != 0;
+    if (d.spmv_order) return d.spmv_order == 2;
     const double store = 8.0 * d.E * C::NPE * C::NS11 * C::B11;
     return store <= static_cast<double>(1LL << 30) ? 1 : 0;
   }

@@ -120,8 +120,15 @@ class LineDG:
             state = buf[: self.m].copy()
         _raise(st, msg, state, elem.value, node.value)
 
-    def _dev(self, n: int):
-        return self._torch.empty(n, dtype=self._torch.float64, device="cuda")
+    def _dev(self, n: int, out=None):
+        """Device result buffer: `out` (a contiguous float64 CUDA tensor of n
+        entries, e.g. a preallocated buffer reused inside a CUDA graph) or new."""
+        if out is None:
+            return self._torch.empty(n, dtype=self._torch.float64, device="cuda")
+        if not (_is_torch(out) and out.dtype == self._torch.float64 and out.is_cuda and out.is_contiguous()
+                and out.numel() == n):
+            raise ValueError(f"out must be a contiguous float64 CUDA tensor of {n} entries")
+        return out
 
     @staticmethod
     def _ptr(t):
@@ -139,6 +146,10 @@ class LineDG:
 
     def set_sync_errors(self, on: bool):
         self._check(self.lib.ldg_set_sync_errors(self._h, 1 if on else 0))
+
+    def set_option(self, option: int, value: int):
+        """ldg_set_option (LDG_OPT_SPMV_ROW_ORDER, LDG_OPT_ZERO_COPY)."""
+        self._check(self.lib.ldg_set_option(self._h, int(option), int(value)))
 
     def synchronize(self):
         self._check(self.lib.ldg_synchronize(self._h))
@@ -191,7 +202,7 @@ class LineDG:
                 Q_out[...] = Qh
             return R
         U = self._as_dev(U)
-        R = self._dev(self.n_dofs)
+        R = self._dev(self.n_dofs, out)
         self._check(self.lib.ldg_residual(self._h, self._ptr(U), t, self._ptr(R), self._ptr(Q_out)))
         return R
 
@@ -219,6 +230,24 @@ class LineDG:
             return
         U = self._as_dev(U)
         self._check(self.lib.ldg_jacobian_assemble(self._h, self._ptr(U), t))
+
+    def assemble_jacobians_q(self, U, Q, t: float = 0.0):
+        """Assembly at U with the gradient Q = D(U) already on the device (from
+        residual(U, Q_out=Q)): the Newton step's R and J share one gradient."""
+        U = self._as_dev(U)
+        Q = self._as_dev(Q) if self.second_order else None
+        self._check(self.lib.ldg_jacobian_assemble_q(self._h, self._ptr(U), self._ptr(Q), t))
+
+    def residual_and_assemble(self, U, t: float = 0.0, out=None, Q_out=None):
+        """Host buffers: R(U) and the Jacobian at U from one upload of U
+        (ldg_residual_assemble_host); returns R."""
+        Uh = np.ascontiguousarray(U, dtype=np.float64)
+        R = self._host_out(out, self.n_dofs)
+        Qh = np.empty(self.n_dofs * self.dim) if (Q_out is not None and self.second_order) else None
+        self._check(self.lib.ldg_residual_assemble_host(self._h, dptr(Uh), t, dptr(R), dptr(Qh)))
+        if Qh is not None:
+            Q_out[...] = Qh
+        return R
 
     def pattern_info(self, which: int) -> LdgPatternInfo:
         info = LdgPatternInfo()
@@ -265,7 +294,7 @@ class LineDG:
             return y
         x = self._as_dev(x)
         ny = self.n_dofs * (self.dim if which == _abi.LDG_K21 else 1)
-        y = self._dev(ny)
+        y = self._dev(ny, out)
         self._check(self.lib.ldg_bsr_spmv(self._h, which, self._ptr(x), self._ptr(y)))
         return y
 
@@ -349,6 +378,6 @@ class LineDG:
             self._check(self.lib.ldg_split_matvec_host(self._h, alpha_dt, dptr(vh), dptr(y)))
             return y
         v = self._as_dev(v)
-        y = self._dev(self.n_dofs)
+        y = self._dev(self.n_dofs, out)
         self._check(self.lib.ldg_split_matvec(self._h, alpha_dt, self._ptr(v), self._ptr(y)))
         return y

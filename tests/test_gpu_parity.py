@@ -250,21 +250,35 @@ def test_async_host_path_matches_sync():
         assert rel(y0, ora.spmv(LDG_K11, x)) <= TOL
 
 
+def _with_neighbours(ora, case, elems):
+    """elems plus the elements their K12 (switch-side) columns reach: the K21
+    rows a split matvec over the rows of `elems` consumes."""
+    r, c, _ = ora.export_blocks(LDG_K12)
+    keep = np.isin(r // case.npe, elems)
+    return np.unique(np.concatenate([elems, (c[keep] // case.npe).astype(np.int32)])).astype(np.int32)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("ci", [2, 3, 4], ids=["C3-full", "C4-full", "C5-full"])
 def test_full_size_rows_match_oracle(ci):
     """Full BASELINE.json sizes (C3 6.6 M, C4 84 M, C5 69 M DOFs; C5's store is
-    164 GB): the residual on the DOFs of 32 random elements and their K11
-    (+ K12, K21) rows against the oracle evaluated on those elements only,
-    and the Table-1 node-column counts of the whole K11 pattern (2p+5 in 2-D,
-    3p+7 in 3-D, periodic)."""
+    164 GB) on the configs' OWN states (no perturbation): on the DOFs of 32
+    random elements, the residual, the K11 (+ K12, K21) rows, the K11 product
+    and the split matvec against the oracle evaluated on those elements only,
+    and the Table-1 node-column counts of the whole K11 pattern.
+
+    Residual tolerance.  C3 and C5 are near-steady: their residual is a 1e4-fold
+    cancellation of O(p^2/h) line terms, so ANY fp64 evaluation carries a
+    normwise error far above 1e-12 -- the oracle itself moves by 3e-10 (C3) /
+    4e-11 (C5) between an FMA-contracted and an uncontracted build, and lies
+    2e-10 / 6e-11 from the same restatement evaluated in long double
+    (DESIGN.md section 3).  The bar on the own state is therefore accuracy:
+    the GPU residual must be at least as close to the extended-precision
+    evaluation as the fp64 oracle is (or within 1e-12 of it).  The 1e-12
+    GPU-vs-oracle bar itself is checked on a seeded 2 % perturbation of the
+    same state (an O(n) residual on the same code paths)."""
     cfg = CONFIGS[ci]
     case, U = cfg.build()
-    # The configs' states are near-steady (smooth small perturbations): at full
-    # resolution their residual is a ~1e4-fold cancellation of O(n) line terms,
-    # so summation order alone moves it by ~1e-10 relative.  A seeded 2 %
-    # multiplicative perturbation gives an O(n) residual on the same code paths.
-    U = U * (1.0 + 0.02 * np.random.default_rng(12).standard_normal(U.shape))
     gpu = LineDG(case, cfg.physics)
     try:
         ora = Oracle(case, cfg.physics)
@@ -272,9 +286,20 @@ def test_full_size_rows_match_oracle(ci):
         elems = np.sort(rng.choice(case.E, 32, replace=False)).astype(np.int32)
         m = gpu.m
         dofs = (elems[:, None] * case.npe * m + np.arange(case.npe * m)[None, :]).ravel()
-        R = host(gpu.residual(dev(U)))
-        R0 = ora.residual(U, elems=elems)
-        assert rel(R[dofs], R0[dofs]) <= TOL
+        # residual on the config's own state: accuracy against long double
+        R = host(gpu.residual(dev(U)))[dofs]
+        R64 = ora.residual(U, elems=elems)[dofs]
+        Rx = ora.residual_ext(U, elems=elems)[dofs]
+        e_gpu, e_ora = rel(R, Rx), rel(R64, Rx)
+        print(f"C{ci + 1} residual: gpu-vs-ext {e_gpu:.3e}  oracle64-vs-ext {e_ora:.3e}  "
+              f"gpu-vs-oracle64 {rel(R, R64):.3e}")
+        assert e_gpu <= max(TOL, e_ora), (e_gpu, e_ora)
+        # the 1e-12 bar against the fp64 oracle on an O(n) residual
+        Up = U * (1.0 + 0.02 * np.random.default_rng(12).standard_normal(U.shape))
+        Rp = host(gpu.residual(dev(Up)))
+        assert rel(Rp[dofs], ora.residual(Up, elems=elems)[dofs]) <= TOL
+        del Rp, Up
+        # Jacobian rows, K11 product and split matvec on the config's own state
         gpu.assemble_jacobians(dev(U))
         ora.assemble(U, elems=elems)
         for w in _matrices(cfg):
@@ -285,5 +310,41 @@ def test_full_size_rows_match_oracle(ci):
             assert rel(v1, v0[keep]) <= TOL, (w, rel(v1, v0[keep]))
         per_row = 2 * cfg.p + 5 if case.dim == 2 else 3 * cfg.p + 7
         assert gpu.pattern_info(LDG_K11).nnzb == per_row * case.E * case.npe
+        x = case.normal_vector(m, cfg.vector_seed)
+        xd = dev(x)
+        y = host(gpu.spmv(LDG_K11, xd))[dofs]
+        assert rel(y, ora.spmv(LDG_K11, x)[dofs]) <= TOL
+        if cfg.physics.second_order():  # K21 rows of the neighbours the K12 columns reach
+            ora.assemble(U, elems=_with_neighbours(ora, case, elems))
+        for adt in (1e-3, 0.37):
+            s = host(gpu.split_matvec(adt, xd))[dofs]
+            assert rel(s, ora.split_matvec(adt, x)[dofs]) <= TOL, adt
     finally:
         gpu.close()
+
+
+@pytest.mark.parametrize("ci", [1, 2, 3, 4], ids=["C2", "C3", "C4", "C5"])
+def test_spmv_row_orders(ci):
+    """Both row walks of the block SpMV / split matvec (LDG_OPT_SPMV_ROW_ORDER:
+    forward, taken by every store above 1 GiB -- C3, C4, C5 at full size -- and
+    reverse, taken by small stores) against the oracle, and bitwise equal to
+    each other."""
+    cfg = CONFIGS[ci]
+    case, U = cfg.build(n=4 if cfg.dim == 2 else 3)
+    gpu = LineDG(case, cfg.physics)
+    ora = Oracle(case, cfg.physics)
+    ora.assemble(U)
+    gpu.assemble_jacobians(dev(U))
+    x = case.normal_vector(gpu.m, cfg.vector_seed)
+    y_ref = ora.spmv(LDG_K11, x)
+    s_ref = ora.split_matvec(0.37, x)
+    out = []
+    for order in (1, 2):
+        gpu.set_option(_abi.LDG_OPT_SPMV_ROW_ORDER, order)
+        y = host(gpu.spmv(LDG_K11, dev(x)))
+        s = host(gpu.split_matvec(0.37, dev(x)))
+        assert rel(y, y_ref) <= TOL and rel(s, s_ref) <= TOL, order
+        out.append((y, s))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    with pytest.raises(Exception):
+        gpu.set_option(_abi.LDG_OPT_SPMV_ROW_ORDER, 3)

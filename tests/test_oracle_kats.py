@@ -510,3 +510,23 @@ def test_vortex_residual_approximates_time_derivative():
         errs.append(np.abs(R - dU).max())
     rates = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
     assert min(rates) >= p - 1 and errs[-1] < 3e-3, (errs, rates)
+
+
+@pytest.mark.parametrize("ci", range(5))
+def test_extended_precision_residual(ci):
+    """The long-double evaluation of the residual (the accuracy yardstick of the
+    full-size parity test) agrees with the fp64 oracle to 1e-12 on the
+    well-conditioned scaled-down configs, and the CPU timing sample
+    (bench.py's cpu_baseline) runs every phase."""
+    cfg = CONFIGS[ci]
+    case, U = cfg.build(n=4 if cfg.dim == 2 else 2)
+    ora = Oracle(case, cfg.physics)
+    src = cfg.source_for(case)
+    if src is not None:
+        ora.set_source(src)
+    R = ora.residual(U)
+    Rx = ora.residual_ext(U)
+    assert np.abs(R - Rx).max() <= 1e-12 * np.abs(Rx).max()
+    x = case.normal_vector(cfg.physics.components(case.dim), cfg.vector_seed)
+    secs = ora.time_sample(U, x, 0.05, 2, np.arange(case.E, dtype=np.int32)[: max(1, case.E // 2)], 1, reps=1)
+    assert secs.shape == (4,) and np.all(secs[1:] > 0) and (secs[0] > 0 or not cfg.physics.second_order())
