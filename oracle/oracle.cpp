@@ -1248,6 +1248,7 @@ int lo_assemble(lo_ctx* x, const double* U, double t, const int32_t* elems, int3
     }
     JacFn f = pick_jac(c.m, c.D);
     for_elems(c, sp, [&](int e) { f(c, e, U, Q); });
+    c.pc_built = false;  // factors of the old Jacobian are stale
   });
 }
 
@@ -1731,8 +1732,10 @@ int lo_rk4_step(lo_ctx* x, double* U, double t, double dt) {
     const Ctx& c = x->c;
     const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
     std::vector<double> k1(n), k2(n), k3(n), k4(n), us(n);
+    // stage times t, t + dt/2, t + dt/2, t + dt
     auto F = [&](const double* u, double* k, int stage) {
-      if (lo_residual(x, u, t, k, nullptr, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+      const double ts = t + (stage == 1 ? 0.0 : stage == 4 ? dt : 0.5 * dt);
+      if (lo_residual(x, u, ts, k, nullptr, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
       for (size_t i = 0; i < n; ++i)
         if (!std::isfinite(k[i])) throw std::runtime_error("oracle: rk4 blow-up at stage " + std::to_string(stage));
     };
@@ -1760,8 +1763,10 @@ int lo_dirk3_step(lo_ctx* x, double* U, double t, double dt, const ldg_newton_cf
     const size_t n = static_cast<size_t>(c.E) * c.npe * c.m;
     const double adt = al * dt;
     ldg_solver_stats s{};
-    auto assemble = [&](const double* u) {
-      if (lo_assemble(x, u, t, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+    // stage times t + c_i dt, c = (alpha, tau2, 1)
+    const double cst[3] = {al, tau2, 1.0};
+    auto assemble = [&](const double* u, double ta) {
+      if (lo_assemble(x, u, ta, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
       ++s.jacobian_assemblies;
       c.pc_built = false;
     };
@@ -1769,15 +1774,15 @@ int lo_dirk3_step(lo_ctx* x, double* U, double t, double dt, const ldg_newton_cf
       if (cfg->use_precond && (!c.pc_built || c.pc_adt != adt))
         if (lo_precond_build(x, adt) != LDG_OK) throw std::runtime_error(g_err);
     };
-    auto F = [&](const double* u, double* k) {
-      if (lo_residual(x, u, t, k, nullptr, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
+    auto F = [&](const double* u, double* k, double ta) {
+      if (lo_residual(x, u, ta, k, nullptr, nullptr, 0) != LDG_OK) throw std::runtime_error(g_err);
       ++s.residual_evals;
     };
-    if (!c.K[LDG_K11].built) assemble(U);
+    if (!c.K[LDG_K11].built) assemble(U, t);
     ensure_pc();
     std::vector<std::vector<double>> K(3, std::vector<double>(n));
     std::vector<double> Kc(n), us(n), Fv(n), G(n), dK(n);
-    F(U, Kc.data());  // initial slope guess of stage 1: R(U_n)
+    F(U, Kc.data(), t);  // initial slope guess of stage 1: R(U_n)
     for (int i = 0; i < 3; ++i) {
       int it = 0;
       while (true) {
@@ -1786,7 +1791,7 @@ int lo_dirk3_step(lo_ctx* x, double* U, double t, double dt, const ldg_newton_cf
           for (int j = 0; j < i; ++j) sacc += A[i][j] * K[j][q];
           us[q] = U[q] + dt * (sacc + al * Kc[q]);
         }
-        F(us.data(), Fv.data());
+        F(us.data(), Fv.data(), t + cst[i] * dt);
         for (size_t q = 0; q < n; ++q) G[q] = Kc[q] - Fv[q];
         const double gn = inf_norm(G.data(), n);
         if (!std::isfinite(gn)) throw std::runtime_error("oracle: dirk3 non-finite stage");
@@ -1794,7 +1799,7 @@ int lo_dirk3_step(lo_ctx* x, double* U, double t, double dt, const ldg_newton_cf
         if (gn <= cfg->newton_tol) break;
         if (it >= cfg->max_newton) throw std::runtime_error("oracle: dirk3 step failure (Newton did not converge)");
         if (it > 0 && it % cfg->recompute_threshold == 0) {
-          assemble(us.data());
+          assemble(us.data(), t + cst[i] * dt);
           ensure_pc();
         }
         for (size_t q = 0; q < n; ++q) G[q] = -G[q];

@@ -132,6 +132,7 @@ struct ldg_ctx {
   long long launches = 0;
   bool sync_errors = true;
   bool zero_copy = true;  // LDG_OPT_ZERO_COPY
+  int device = -1;       // CUDA device of the context (current at ldg_create)
   std::string err;
   int err_elem = -1, err_node = -1;
   double err_state[8] = {0};
@@ -576,8 +577,24 @@ void build_connectivity(ldg_ctx& c, const ldg_setup& s, const ldg_physics& ph) {
      "upload conn");
 }
 
+// Makes the context's device current for the duration of an entry point
+// (launch configuration, allocations and streams all belong to it) and
+// restores the caller's device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const ldg_ctx* c) {
+    if (!c || c->device < 0) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 int guarded(ldg_ctx* c, F&& f) {
+  DeviceGuard dg(c);
   try {
     return f();
   } catch (const ldg_error& ex) {
@@ -771,6 +788,7 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw ldg_error(LDG_ERR_CUDA, "no CUDA device: the B200 hot path has no CPU fallback");
     auto c = std::make_unique<ldg_ctx>();
+    ck(cudaGetDevice(&c->device), "cudaGetDevice");
     c->D = s->dim;
     c->p = s->p;
     c->np = c->p + 1;
@@ -931,7 +949,10 @@ int ldg_create(const ldg_setup* s, const ldg_physics* ph, void* stream, ldg_ctx*
   });
 }
 
-void ldg_destroy(ldg_ctx* c) { delete c; }
+void ldg_destroy(ldg_ctx* c) {
+  DeviceGuard dg(c);  // frees on the context's device
+  delete c;
+}
 
 int ldg_last_error_state(const ldg_ctx* c, int32_t* elem, int32_t* node, double* state) {
   if (!c) return LDG_ERR_INVALID_ARGUMENT;
@@ -1095,12 +1116,12 @@ int assemble_at(ldg_ctx* c, const double* U, const double* q_given, double t) {
   const size_t rows = static_cast<size_t>(c->E) * c->npe;
   if (!c->d_K11) {
     c->n11 = rows * o.NS11 * o.B11;
-    ck(cudaMalloc(&c->d_K11, c->n11 * sizeof(double)), "cudaMalloc K11");
+    ck(cudaMalloc(&c->d_K11, c->n11 * sizeof(double) + 64), "cudaMalloc K11");  // +64: tile loads round to 16 B
     if (c->second) {
       c->n12 = rows * o.NS12 * o.B12;
       c->n21 = rows * o.NS12 * c->D;
-      ck(cudaMalloc(&c->d_K12, c->n12 * sizeof(double)), "cudaMalloc K12");
-      ck(cudaMalloc(&c->d_K21, c->n21 * sizeof(double)), "cudaMalloc K21");
+      ck(cudaMalloc(&c->d_K12, c->n12 * sizeof(double) + 64), "cudaMalloc K12");  // +64: tile loads round to 16 B
+      ck(cudaMalloc(&c->d_K21, c->n21 * sizeof(double) + 64), "cudaMalloc K21");  // +64: tile loads round to 16 B
     }
   }
   const double* q = nullptr;
@@ -1607,8 +1628,11 @@ int ldg_rk4_step(ldg_ctx* c, double* U, double t, double dt) {
     cudaStream_t st = c->stream;
     const bool was = c->sync_errors;
     c->sync_errors = true;
+    // classical RK4 stage times t, t + dt/2, t + dt/2, t + dt (time-dependent
+    // boundary data is evaluated at each stage's own time)
     auto F = [&](const double* u, double* k, int stage) {
-      int s_ = ldg_residual(c, u, t, k, nullptr);
+      const double ts = t + (stage == 1 ? 0.0 : stage == 4 ? dt : 0.5 * dt);
+      int s_ = ldg_residual(c, u, ts, k, nullptr);
       if (s_ != LDG_OK) {
         c->sync_errors = was;
         throw ldg_error(s_, c->err);
@@ -1663,27 +1687,29 @@ int ldg_dirk3_step(ldg_ctx* c, double* U, double t, double dt, const ldg_newton_
         throw ldg_error(code, c->err);
       }
     };
-    auto assemble = [&](const double* u) {
-      chk(ldg_jacobian_assemble(c, u, t));
+    // stage times t + c_i dt, c = (alpha, tau2, 1) (row sums of the tableau)
+    const double cst[3] = {al, tau2, 1.0};
+    auto assemble = [&](const double* u, double ta) {
+      chk(ldg_jacobian_assemble(c, u, ta));
       ++s.jacobian_assemblies;
       c->pc_valid = false;
     };
     auto ensure_pc = [&]() {
       if (cfg->use_precond && (!c->pc_valid || c->pc_adt != adt)) chk(ldg_precond_build(c, adt));
     };
-    auto F = [&](const double* u, double* k) {
-      chk(ldg_residual(c, u, t, k, nullptr));
+    auto F = [&](const double* u, double* k, double ta) {
+      chk(ldg_residual(c, u, ta, k, nullptr));
       ++s.residual_evals;
     };
-    if (!c->jac_valid) assemble(U);
+    if (!c->jac_valid) assemble(U, t);
     ensure_pc();
-    F(U, Kc);
+    F(U, Kc, t);
     for (int i = 0; i < 3; ++i) {
       int it = 0;
       while (true) {
         k_stage_state<<<vb, vt, 0, st>>>(us, U, K[0], K[1], Kc, n, dt, A[i][0], A[i][1], al, i);
         ++c->launches;
-        F(us, Fv);
+        F(us, Fv, t + cst[i] * dt);
         k_rhs<<<vb, vt, 0, st>>>(G, Kc, Fv, n);
         // (re-fetched each time: ldg_gmres reallocates d_kred when its restart grows)
         double* red = ensure(c->d_kred, KR_BLOCKS + 8);
@@ -1704,7 +1730,7 @@ int ldg_dirk3_step(ldg_ctx* c, double* U, double t, double dt, const ldg_newton_
           throw ldg_error(LDG_ERR_SOLVER, "dirk3: step failure (Newton did not converge)");
         }
         if (it > 0 && it % cfg->recompute_threshold == 0) {
-          assemble(us);
+          assemble(us, t + cst[i] * dt);
           ensure_pc();
         }
         int32_t gi = 0, gc = 0;

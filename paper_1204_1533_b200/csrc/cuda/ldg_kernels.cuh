@@ -42,7 +42,6 @@ struct KParams {
   const int32_t* inv_order;  // reference element e -> processing index k
   const int32_t* owned;  // owned faces (k*2D + ds) of the Jacobian chunks, or null
   int E;                 // elements
-  int dbg;               // diagnostics: bit0 skip assembly phase 1, bit1 skip phase 2, bit2 skip the staged bulk store
 };
 
 // Numerical flux F_hat.n at a boundary line end (SPEC.md:266,
@@ -325,380 +324,14 @@ __device__ __forceinline__ void store_tile(double* __restrict__ gdst, const doub
   }
 }
 
-// ===================================================================== residual
-// FIRST: first-order physics (Q absent).  Otherwise R(U, Q).
-template <class C, int EPB>
-__global__ void __launch_bounds__((EPB * C::LPE + 31) / 32 * 32)
-k_residual(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-           double* __restrict__ R) {
-  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
-                MD = C::MD, LPE = C::LPE;
-  extern __shared__ double smem[];
-  double* su = smem;                                   // [EPB][NPE*M]
-  double* sq = su + EPB * NPE * M;                     // [EPB][NPE*MD]
-  double* sacc = sq + (C::SECOND ? EPB * NPE * MD : 0);  // [EPB][D][NPE*M]
-  const int k0 = blockIdx.x * EPB;
-  const int nb = min(EPB, kp.E - k0);
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  for (int le = 0; le < nb; ++le) {
-    const size_t e = kp.order[k0 + le];
-    cp_elem<C>(su + le * NPE * M, U + e * (NPE * M), NPE * M, tid, nthr);
-    if (C::SECOND) cp_elem<C>(sq + le * NPE * MD, Q + e * (NPE * MD), NPE * MD, tid, nthr);
-  }
-  __syncthreads();
-  const int le = tid / LPE;
-  if (le < nb) {
-    const int rem = tid - le * LPE;
-    const int dir = rem / NL, line = rem - dir * NL;
-    const int k = k0 + le;
-    const int e = kp.order[k];
-    const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-    const double* nvl = mk + (dir * NL + line) * NQ * D;
-    const double* sul = su + le * NPE * M;
-    const double* sql = sq + le * NPE * MD;
-    bool ok = true;
-    // Neighbour traces at both line ends.
-    double uo[2][M], qo[2][MD];
-    const double* bcp[2] = {nullptr, nullptr};
-    int sg[2];
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-      sg[side] = conn_sign(cn.y);
-      if (cn.x >= 0) {
-        const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
-#pragma unroll
-        for (int c = 0; c < M; ++c) uo[side][c] = __ldg(U + nd * M + c);
-        if (C::SECOND && sg[side] > 0) {
-#pragma unroll
-          for (int c = 0; c < MD; ++c) qo[side][c] = __ldg(Q + nd * MD + c);
-        }
-      } else {
-        bcp[side] = bnd_g(kp, -1 - cn.x, k, dir * 2 + side, line);
-      }
-    }
-    double r[NP][M];
-#pragma unroll
-    for (int i = 0; i < NP; ++i)
-#pragma unroll
-      for (int c = 0; c < M; ++c) r[i][c] = 0.0;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      double uq[M], qq[C::SECOND ? MD : 1];
-#pragma unroll
-      for (int c = 0; c < M; ++c) uq[c] = 0.0;
-      if (C::SECOND) {
-#pragma unroll
-        for (int c = 0; c < MD; ++c) qq[c] = 0.0;
-      }
-#pragma unroll
-      for (int t = 0; t < NP; ++t) {
-        const int nd = node_on_line<C>(dir, line, t);
-        const double ph = kp.bt.phi[t][q];
-#pragma unroll
-        for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
-        if (C::SECOND) {
-#pragma unroll
-          for (int c = 0; c < MD; ++c) qq[c] += ph * sql[nd * MD + c];
-        }
-      }
-      double nv[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) nv[d] = __ldg(nvl + q * D + d);
-      double f[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) f[c] = 0.0;
-      if (C::HAS_INV) euler_fn<D>(uq, nv, kp.pp.gamma, f, ok);
-      if (C::SECOND) {
-        double fv[M];
-        visc_fn<D, C::PH, double, double, double>(uq, qq, nv, kp.pp, fv, ok);
-#pragma unroll
-        for (int c = 0; c < M; ++c) f[c] += fv[c];
-      }
-#pragma unroll
-      for (int i = 0; i < NP; ++i)
-#pragma unroll
-        for (int c = 0; c < M; ++c) r[i][c] += kp.bt.dq[i][q] * f[c];
-    }
-    // Endpoint numerical fluxes, lifted by the M^-1 columns 0 and p.
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int ie = side ? C::P : 0;
-      const int nd = node_on_line<C>(dir, line, ie);
-      const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
-      double n[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) n[d] = __ldg(nep + d);
-      double ui[M], fh[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        ui[c] = sul[nd * M + c];
-        fh[c] = 0.0;
-      }
-      if (bcp[side]) {
-        double nn = n[0] * n[0];
-#pragma unroll
-        for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-        nn = sqrt(nn);
-        double qi[C::SECOND ? MD : 1];
-        if (C::SECOND) {
-#pragma unroll
-          for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
-        }
-        const int2 cb = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-        bnd_flux<C>(kp, -1 - cb.x, bcp[side], ui, qi, n, nn, fh, ok);
-      } else {
-        if (C::HAS_INV) {
-          if (C::RI == LDG_ROE) roe_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
-          else llf_fn<D>(uo[side], ui, n, kp.pp.gamma, fh, ok);
-        }
-        if (C::SECOND) {
-          double nn = n[0] * n[0];
-#pragma unroll
-          for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-          nn = sqrt(nn);
-          double fv[M];
-          if (sg[side] > 0) {
-            visc_fn<D, C::PH, double, double, double>(uo[side], qo[side], n, kp.pp, fv, ok);
-          } else {
-            double qi[MD];
-#pragma unroll
-            for (int c = 0; c < MD; ++c) qi[c] = sql[nd * MD + c];
-            visc_fn<D, C::PH, double, double, double>(ui, qi, n, kp.pp, fv, ok);
-          }
-#pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] += fv[c];
-          if (kp.pp.c11 != 0.0) {
-#pragma unroll
-            for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[side][c]);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NP; ++i)
-#pragma unroll
-        for (int c = 0; c < M; ++c) r[i][c] += kp.bt.mi[i][side] * fh[c];
-    }
-    if (!ok) report_line<C>(kp, e, dir, line, sul);
-    double* acc = sacc + (le * D + dir) * NPE * M;
-#pragma unroll
-    for (int t = 0; t < NP; ++t) {
-      const int nd = node_on_line<C>(dir, line, t);
-#pragma unroll
-      for (int c = 0; c < M; ++c) acc[nd * M + c] = r[t][c];
-    }
-  }
-  __syncthreads();
-  // dU/dt = S - (1/J) sum_dir r^(dir)
-  for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
-    const int l = idx / (NPE * M), off = idx - l * NPE * M;
-    const int nd = off / M;
-    const int k = k0 + l;
-    const size_t e = kp.order[k];
-    const double* a = sacc + l * D * NPE * M + off;
-    double s = a[0];
-#pragma unroll
-    for (int d = 1; d < D; ++d) s = s + a[d * NPE * M];
-    const double invJ = __ldg(kp.metric + static_cast<size_t>(k) * C::METP + C::MET_NV + C::MET_NE + nd);
-    const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
-    R[e * (NPE * M) + off] = src - invJ * s;
-  }
-}
-
-// Sub-warp residual: a group of G = n_q lanes per line (one lane per
-// quadrature point), GPW = 32 / G groups per warp.  Lane j interpolates the
-// state to its quadrature point and evaluates the flux there; the projection
-// r_i = sum_q dq[i][q] f_q is a lane transpose through warp shuffles (lane i
-// gathers f_q from lanes q); lanes 0 and 1 evaluate the endpoint numerical
-// fluxes of sides 0 and 1 and broadcast them for the M^-1 lifting.
-template <class C>
-struct SubWarp {
-  static constexpr int G = C::NQ;
-  static constexpr int GPW = 32 / G;
-  static constexpr int EPB_RAW = (6 * GPW + C::LPE - 1) / C::LPE;
-  static constexpr int EPB = EPB_RAW < 1 ? 1 : EPB_RAW;
-  static constexpr int LINES = EPB * C::LPE;
-  static constexpr int WARPS = (LINES + GPW - 1) / GPW;
-  static constexpr int THREADS = WARPS * 32;
-};
-
-template <class C>
-__global__ void __launch_bounds__(SubWarp<C>::THREADS, 2)
-k_residual_sw(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
-              double* __restrict__ R) {
-  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D, MD = C::MD,
-                LPE = C::LPE, P = C::P;
-  using SW = SubWarp<C>;
-  constexpr int EPB = SW::EPB, G = SW::G, GPW = SW::GPW;
-  extern __shared__ double smem[];
-  double* su = smem;                                      // [EPB][NPE*M]
-  double* sq = su + EPB * NPE * M;                        // [EPB][NPE*MD]
-  double* sacc = sq + (C::SECOND ? EPB * NPE * MD : 0);   // [EPB][D][NPE*M]
-  double* sphi = sacc + EPB * D * NPE * M;                // [NP][NQ]
-  double* sdq = sphi + NP * NQ;                           // [NP][NQ]
-  const int k0 = blockIdx.x * EPB;
-  const int nb = min(EPB, kp.E - k0);
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  for (int i = tid; i < NP * NQ; i += nthr) {
-    sphi[i] = (&kp.bt.phi[0][0])[i];
-    sdq[i] = (&kp.bt.dq[0][0])[i];
-  }
-  for (int i = tid; i < NP * 2; i += nthr) sdq[NP * NQ + i] = (&kp.bt.mi[0][0])[i];
-  for (int le = 0; le < nb; ++le) {
-    const size_t e = kp.order[k0 + le];
-    cp_elem<C>(su + le * NPE * M, U + e * (NPE * M), NPE * M, tid, nthr);
-    if (C::SECOND) cp_elem<C>(sq + le * NPE * MD, Q + e * (NPE * MD), NPE * MD, tid, nthr);
-  }
-  __syncthreads();
-  const int lane = tid & 31, warp = tid >> 5;
-  const int g = lane / G, j = lane - g * G;
-  const int gl = warp * GPW + g;  // line within the CTA
-  const int le = gl / LPE;
-  const bool act = g < GPW && le < nb;
-  const int rem = gl - le * LPE;
-  const int dir = rem / NL, line = rem - dir * NL;
-  const int k = k0 + (act ? le : 0);
-  const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-  const double* sul = su + (act ? le : 0) * NPE * M;
-  const double* sql = sq + (act ? le : 0) * NPE * MD;
-  bool ok = true;
-  // quadrature-point flux (lane j < NQ)
-  double f[M];
-#pragma unroll
-  for (int c = 0; c < M; ++c) f[c] = 0.0;
-  if (act) {
-    double uq[M], qq[C::SECOND ? MD : 1];
-#pragma unroll
-    for (int c = 0; c < M; ++c) uq[c] = 0.0;
-    if (C::SECOND) {
-#pragma unroll
-      for (int c = 0; c < MD; ++c) qq[c] = 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < NP; ++t) {
-      const int nd = node_on_line<C>(dir, line, t);
-      const double ph = sphi[t * NQ + j];
-#pragma unroll
-      for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
-      if (C::SECOND) {
-#pragma unroll
-        for (int c = 0; c < MD; ++c) qq[c] += ph * sql[nd * MD + c];
-      }
-    }
-    double nv[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) nv[d] = __ldg(mk + ((dir * NL + line) * NQ + j) * D + d);
-    if (C::HAS_INV) euler_fn<D>(uq, nv, kp.pp.gamma, f, ok);
-    if (C::SECOND) {
-      double fv[M];
-      visc_fn<D, C::PH, double, double, double>(uq, qq, nv, kp.pp, fv, ok);
-#pragma unroll
-      for (int c = 0; c < M; ++c) f[c] += fv[c];
-    }
-  }
-  // endpoint numerical flux: lane 0 -> side 0, lane 1 -> side 1
-  double fh[M];
-#pragma unroll
-  for (int c = 0; c < M; ++c) fh[c] = 0.0;
-  if (act && j < 2) {
-    const int side = j;
-    const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-    const int S = conn_sign(cn.y);
-    const int nd = node_on_line<C>(dir, line, side ? P : 0);
-    double n[D], ui[M], uo[M];
-#pragma unroll
-    for (int d = 0; d < D; ++d) n[d] = __ldg(mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D + d);
-    const double* bcp = cn.x < 0 ? bnd_g(kp, -1 - cn.x, k, dir * 2 + side, line) : nullptr;
-    size_t ond = 0;
-    if (!bcp) ond = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
-#pragma unroll
-    for (int c = 0; c < M; ++c) {
-      ui[c] = sul[nd * M + c];
-      uo[c] = bcp ? __ldg(bcp + c) : __ldg(U + ond * M + c);
-    }
-    if (bcp) {
-      double nn = n[0] * n[0];
-#pragma unroll
-      for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-      nn = sqrt(nn);
-      bnd_flux<C>(kp, -1 - cn.x, bcp, ui, (C::SECOND ? sql + nd * MD : sul), n, nn, fh, ok);
-    } else {
-      if (C::HAS_INV) {
-        if (C::RI == LDG_ROE) roe_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-        else llf_fn<D>(uo, ui, n, kp.pp.gamma, fh, ok);
-      }
-      if (C::SECOND) {
-        double nn = n[0] * n[0];
-#pragma unroll
-        for (int d = 1; d < D; ++d) nn += n[d] * n[d];
-        nn = sqrt(nn);
-        double fv[M];
-        if (S > 0) {
-          double qo[MD];
-#pragma unroll
-          for (int c = 0; c < MD; ++c) qo[c] = __ldg(Q + ond * MD + c);
-          visc_fn<D, C::PH, double, double, double>(uo, qo, n, kp.pp, fv, ok);
-        } else {
-          visc_fn<D, C::PH, double, double, double>(ui, sql + nd * MD, n, kp.pp, fv, ok);
-        }
-#pragma unroll
-        for (int c = 0; c < M; ++c) fh[c] += fv[c];
-        if (kp.pp.c11 != 0.0) {
-#pragma unroll
-          for (int c = 0; c < M; ++c) fh[c] += kp.pp.c11 * nn * (ui[c] - uo[c]);
-        }
-      }
-    }
-  }
-  // lane transpose: lane i < NP forms r_i
-  const int base = g * G;
-  double r[M];
-#pragma unroll
-  for (int c = 0; c < M; ++c) r[c] = 0.0;
-  const int i = j < NP ? j : 0;
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const double w = sdq[i * NQ + q];
-#pragma unroll
-    for (int c = 0; c < M; ++c) r[c] += w * __shfl_sync(0xffffffffu, f[c], base + q);
-  }
-#pragma unroll
-  for (int c = 0; c < M; ++c) {
-    const double fm = __shfl_sync(0xffffffffu, fh[c], base + 0);
-    const double fp = __shfl_sync(0xffffffffu, fh[c], base + 1);
-    r[c] += sdq[NP * NQ + i * 2 + 0] * fm + sdq[NP * NQ + i * 2 + 1] * fp;
-  }
-  if (act && j < NP) {
-    double* acc = sacc + (le * D + dir) * NPE * M;
-    const int nd = node_on_line<C>(dir, line, j);
-#pragma unroll
-    for (int c = 0; c < M; ++c) acc[nd * M + c] = r[c];
-  }
-  if (!ok) report_line<C>(kp, kp.order[k], dir, line, sul);
-  __syncthreads();
-  for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
-    const int l = idx / (NPE * M), off = idx - l * NPE * M;
-    const int nd = off / M;
-    const int kk = k0 + l;
-    const size_t e = kp.order[kk];
-    const double* a = sacc + l * D * NPE * M + off;
-    double sum = a[0];
-#pragma unroll
-    for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
-    const double invJ = __ldg(kp.metric + static_cast<size_t>(kk) * C::METP + C::MET_NV + C::MET_NE + nd);
-    const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
-    R[e * (NPE * M) + off] = src - invJ * sum;
-  }
-}
-
 // ================================================= residual, persistent + TMA
 // Persistent CTAs walk batches of EPB elements (grid-stride).  Two smem
 // buffers: while batch i is computed from buffer i%2, the TMA engine fills the
 // other buffer with batch i+1 (element states -- one bulk copy per element,
 // the batch's metric and connectivity -- one bulk copy each, all completing on
 // one mbarrier); the scattered neighbour traces of batch i+1 are gathered with
-// cp.async as soon as its connectivity has landed.  Compute is the
-// thread-per-line scheme of k_residual with every operand in shared memory.
+// cp.async as soon as its connectivity has landed.  Compute is
+// thread-per-line with every operand in shared memory.
 #ifndef LDG_RES_MET_SMEM  // residual: stage the metric in the ring (1) or read it from global (0)
 #define LDG_RES_MET_SMEM 1
 #endif
@@ -1447,112 +1080,6 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
   }
 }
 
-// ===================================================================== gradient
-// Q = (1/J) sum_dir d^(dir),  d = M^-1 [u_hat (x) n |ends - sum_q w phi' u_q (x) nvec_q]
-template <class C, int EPB>
-__global__ void __launch_bounds__((EPB * C::LPE + 31) / 32 * 32)
-k_gradient(const KParams<C> kp, const double* __restrict__ U, double* __restrict__ Q) {
-  constexpr int NP = C::NP, NQ = C::NQ, NPE = C::NPE, NL = C::NL, M = C::M, D = C::D,
-                MD = C::MD, LPE = C::LPE;
-  extern __shared__ double smem[];
-  double* su = smem;                   // [EPB][NPE*M]
-  double* sacc = su + EPB * NPE * M;   // [EPB][D][NPE*MD]
-  const int k0 = blockIdx.x * EPB;
-  const int nb = min(EPB, kp.E - k0);
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  for (int le = 0; le < nb; ++le) {
-    const size_t e = kp.order[k0 + le];
-    cp_elem<C>(su + le * NPE * M, U + e * (NPE * M), NPE * M, tid, nthr);
-  }
-  __syncthreads();
-  const int le = tid / LPE;
-  if (le < nb) {
-    const int rem = tid - le * LPE;
-    const int dir = rem / NL, line = rem - dir * NL;
-    const int k = k0 + le;
-    const double* mk = kp.metric + static_cast<size_t>(k) * C::METP;
-    const double* nvl = mk + (dir * NL + line) * NQ * D;
-    const double* sul = su + le * NPE * M;
-    double g[NP][MD];
-#pragma unroll
-    for (int i = 0; i < NP; ++i)
-#pragma unroll
-      for (int c = 0; c < MD; ++c) g[i][c] = 0.0;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      double uq[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) uq[c] = 0.0;
-#pragma unroll
-      for (int t = 0; t < NP; ++t) {
-        const int nd = node_on_line<C>(dir, line, t);
-        const double ph = kp.bt.phi[t][q];
-#pragma unroll
-        for (int c = 0; c < M; ++c) uq[c] += ph * sul[nd * M + c];
-      }
-      double nv[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) nv[d] = __ldg(nvl + q * D + d);
-#pragma unroll
-      for (int i = 0; i < NP; ++i)
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-#pragma unroll
-          for (int d = 0; d < D; ++d) g[i][c * D + d] += kp.bt.dq[i][q] * (uq[c] * nv[d]);
-    }
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int2 cn = __ldg(&kp.conn[(static_cast<size_t>(k) * D + dir) * 2 + side]);
-      const int ie = side ? C::P : 0;
-      const double* nep = mk + C::MET_NV + ((dir * 2 + side) * NL + line) * D;
-      double uh[M];
-      if (cn.x < 0) {  // boundary: g_D, the interior trace, or mixed (no-slip wall)
-        const int nd = node_on_line<C>(dir, line, ie);
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-          uh[c] = bnd_uhat(kp, -1 - cn.x, bnd_g(kp, -1 - cn.x, k, dir * 2 + side, line), c, sul[nd * M + c]);
-      } else if (conn_sign(cn.y) > 0) {  // S = +1
-        const int nd = node_on_line<C>(dir, line, ie);
-#pragma unroll
-        for (int c = 0; c < M; ++c) uh[c] = sul[nd * M + c];
-      } else {
-        const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
-#pragma unroll
-        for (int c = 0; c < M; ++c) uh[c] = __ldg(U + nd * M + c);
-      }
-      double n[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) n[d] = __ldg(nep + d);
-#pragma unroll
-      for (int i = 0; i < NP; ++i)
-#pragma unroll
-        for (int c = 0; c < M; ++c)
-#pragma unroll
-          for (int d = 0; d < D; ++d) g[i][c * D + d] += kp.bt.mi[i][side] * (uh[c] * n[d]);
-    }
-    double* acc = sacc + (le * D + dir) * NPE * MD;
-#pragma unroll
-    for (int t = 0; t < NP; ++t) {
-      const int nd = node_on_line<C>(dir, line, t);
-#pragma unroll
-      for (int c = 0; c < MD; ++c) acc[nd * MD + c] = g[t][c];
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < nb * NPE * MD; idx += nthr) {
-    const int l = idx / (NPE * MD), off = idx - l * NPE * MD;
-    const int nd = off / MD;
-    const int k = k0 + l;
-    const size_t e = kp.order[k];
-    const double* a = sacc + l * D * NPE * MD + off;
-    double s = a[0];
-#pragma unroll
-    for (int d = 1; d < D; ++d) s = s + a[d * NPE * MD];
-    const double invJ = __ldg(kp.metric + static_cast<size_t>(k) * C::METP + C::MET_NV + C::MET_NE + nd);
-    Q[e * (NPE * MD) + off] = invJ * s;
-  }
-}
-
 // ===================================================================== Jacobian
 // Lines intersecting tile `s` of an element.
 //   2-D: all D*NL lines, all rows on them in the tile ("full").
@@ -2137,7 +1664,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   auto PHI = [&](int t, int q) { return JAC_SMEMTAB ? tphi[t * NQ + q] : kp.bt.phi[t][q]; };
   // ---- phase 1a: inviscid A_q = d(F.nvec_q)/du at the quadrature points (closed form)
   constexpr bool VOL11 = C::HAS_INV || C::VIS_U;
-  if ((PHS & 1) && C::HAS_INV && !(kp.dbg & 1)) {
+  if ((PHS & 1) && C::HAS_INV) {
     for (int w = tid; w < NLT * NQ; w += nthr) {
       const int tl = w / NQ, q = w - tl * NQ;
       int dir, line;
@@ -2161,7 +1688,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   }
   // ---- phase 1c (second-order): viscous flux derivatives at the quadrature
   // points: one item per u-seed (dual numbers) plus one closed-form dF/dq item
-  if ((PHS & 1) && C::SECOND && !(kp.dbg & 1)) {
+  if ((PHS & 1) && C::SECOND) {
     constexpr int NSU = C::VIS_U ? (VISC_DU_CLOSED ? 1 : M) : 0, NSEED = NSU + 1;
     for (int w = tid; w < NLT * NQ * NSEED; w += nthr) {
       const int sd = w % NSEED, tq = w / NSEED, tl = tq / NQ, q = tq - tl * NQ;
@@ -2216,7 +1743,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
   if (PHS == 3) __syncthreads();
   if (!(PHS & 2)) return;
 
-  if (C::D == 3 && C::WU == 0 && !(kp.dbg & 2))
+  if (C::D == 3 && C::WU == 0)
     jac_k11_rows3<C>(mk, scon, sE, eidx, sA, sAv, stab + JacSmem<C>::TABD, stab + NP * NQ, K11t, tid, nthr);
   // ---- phase 2: K11 rows of every tile line, stored block row by block row
   const double* sccd = stab;            // cc[p][p][q]
@@ -2277,7 +1804,7 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     // items leave a tail round), and i is warp-uniform when NLT * B11 is a
     // multiple of 32, so cc[i][t][q] stays a uniform constant-bank operand
     constexpr int NI = NLT * B11;
-    for (int w = (kp.dbg & 2) ? NP * NI : tid; w < NP * NI; w += nthr) {
+    for (int w = tid; w < NP * NI; w += nthr) {
       const int i = w / NI, rest = w - i * NI, tl = rest / B11, ab = rest - tl * B11;
       line_item(tl, ab, [&](auto& body, bool, int) { body(i); });
     }
@@ -2285,14 +1812,14 @@ __device__ __forceinline__ void jac_tile(const KParams<C>& kp, const int k, cons
     // slab / line units: one row per item (the full lines' items would carry
     // NP rows against one for the transverse lines')
     using TL = TileLines<C>;
-    for (int w = (kp.dbg & 2) ? TL::NROWS * B11 : tid; w < TL::NROWS * B11; w += nthr) {
+    for (int w = tid; w < TL::NROWS * B11; w += nthr) {
       const int rr = w / B11, ab = w - rr * B11;
       int tl, i;
       TL::row_item(rr, s, tl, i);
       line_item(tl, ab, [&](auto& body, bool, int) { body(i); });
     }
   } else {
-    for (int w = ((kp.dbg & 2) || (C::D == 3 && C::WU == 0)) ? NLT * B11 : tid; w < NLT * B11; w += nthr) {
+    for (int w = (C::D == 3 && C::WU == 0) ? NLT * B11 : tid; w < NLT * B11; w += nthr) {
       const int tl = w / B11, ab = w - tl * B11;
       line_item(tl, ab, [&](auto& body, bool full, int dir) {
         if (full) {
@@ -2704,7 +2231,7 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
                 C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
     if (JP::STAGE) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done; tile staged
-    if (JP::STAGE && tid == 0 && !(kp.dbg & 4)) {
+    if (JP::STAGE && tid == 0) {
 #ifndef LDG_JAC_STORE_HINT  // L2 policy of the tile store: 0 none, 1 evict_first, 2 evict_last
 #define LDG_JAC_STORE_HINT 2  // measured (C2): evict_last 0.3944 vs 0.3979 ms per step (SpMV reads more of K11 from L2)
 #endif
@@ -3246,6 +2773,147 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
   }
 }
 
+// Split matvec y = v - adt (K11 v + K12 w) for second-order physics, streamed
+// tile by tile (k_mv_tiles).  The store keeps each row tile's K11 and K12
+// values contiguous (19 KB + 38 KB per dir-0 line tile of C5, 42 KB + 53 KB
+// per element tile of C3), so a persistent CTA per SM pulls whole tiles into
+// shared memory with 1-D TMA bulk copies (cp.async.bulk, completion on an
+// mbarrier) on an NSTAGE-deep ring: the HBM stream is a sequence of large
+// bulk reads instead of per-thread strided 8-byte loads (the K12 rows are
+// m*D = 15 doubles per lane in the row-per-thread kernel).  Within a tile one
+// item per (slot group, output component, row) forms a partial dot product
+// of its shared-memory values with the gathered v / w of the slot's column
+// node (L1/L2 hits: a CTA walks consecutive tiles of the same elements); the
+// partials land in shared memory and the (row, component) owner sums them in
+// a fixed order (deterministic, no atomics) and writes y while the next
+// tile's items run.
+template <class C>
+struct MvT {
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int NT = C::NT, M = C::M, MD = C::MD, R12 = C::R12;
+  static constexpr int ST11 = C::NS11 * C::B11 * NT;   // doubles per tile
+  static constexpr int ST12 = C::NS12 * C::B12 * NT;
+  static constexpr int BUF11 = ev(ST11 + 1);          // +1: an odd tile offset is loaded from 8 B earlier
+  static constexpr int BUF12 = ev(ST12 + 1);
+  static constexpr int BUF = BUF11 + BUF12;
+  // slots per item: one for line tiles (few rows), three for element tiles
+  static constexpr int SG = NT <= 8 ? 1 : 3;
+  static constexpr int G11 = (C::NS11 + SG - 1) / SG, G12 = (C::NS12 + SG - 1) / SG;
+  static constexpr int NPART = G11 + G12;
+  static constexpr int NOUT = NT * M;
+  static constexpr int PART = ev(NOUT * NPART);
+  static constexpr int THREADS = 256;
+  static constexpr int I11 = G11 * M * NT, I12 = G12 * R12 * NT;  // items per tile
+  static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + 2 * PART) + 64; }
+  static constexpr int NSTAGE = bytes(3) <= 200 * 1024 ? 3 : 2;
+  static constexpr int TOTAL = NSTAGE * BUF + 2 * PART;
+  static constexpr bool OK = C::SECOND && bytes(2) <= 220 * 1024;
+};
+
+template <class C>
+__global__ void __launch_bounds__(MvT<C>::THREADS, 1)
+k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __restrict__ V12,
+           const double* __restrict__ v, const double* __restrict__ w, double adt, double* __restrict__ y) {
+  using MT = MvT<C>;
+  constexpr int NT = C::NT, M = C::M, MD = C::MD, NPE = C::NPE, TPE = C::TPE, NS11 = C::NS11, NS12 = C::NS12,
+                R12 = C::R12, SG = MT::SG, G11 = MT::G11, G12 = MT::G12, NPART = MT::NPART, NS = MT::NSTAGE;
+  constexpr int NSIN = C::D * C::P + 1;
+  constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t bar[NS];
+  double* const ring = smem;
+  double* const part = smem + NS * MT::BUF;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int64_t ntiles = static_cast<int64_t>(kp.E) * TPE;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
+  const int n = t1 > t0 ? static_cast<int>(t1 - t0) : 0;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // one elected thread streams tile i into ring slot i % NS
+  auto issue = [&](int i) {
+    const int64_t T = t0 + i;
+    double* b = ring + (i % NS) * MT::BUF;
+    const int64_t o11 = T * MT::ST11, o12 = T * MT::ST12;
+    const unsigned by11 = static_cast<unsigned>(8 * ((MT::ST11 + (o11 & 1) + 1) & ~1));
+    const unsigned by12 = static_cast<unsigned>(8 * ((MT::ST12 + (o12 & 1) + 1) & ~1));
+    mbar_expect_tx(&bar[i % NS], by11 + by12);
+    tma_load_1d_once(b, V11 + (o11 & ~int64_t(1)), by11, &bar[i % NS]);
+    tma_load_1d_once(b + MT::BUF11, V12 + (o12 & ~int64_t(1)), by12, &bar[i % NS]);
+  };
+  if (tid == 0)
+    for (int i = 0; i < NS && i < n; ++i) issue(i);
+  for (int i = 0; i < n; ++i) {
+    const int64_t T = t0 + i;
+    const int k = static_cast<int>(T / TPE), s = static_cast<int>(T - static_cast<int64_t>(k) * TPE);
+    const size_t e = __ldg(kp.order + k);
+    const double* b11 = ring + (i % NS) * MT::BUF + ((T * MT::ST11) & 1);
+    const double* b12 = ring + (i % NS) * MT::BUF + MT::BUF11 + ((T * MT::ST12) & 1);
+    double* pp = part + (i & 1) * MT::PART;
+    mbar_wait(&bar[i % NS], (i / NS) & 1);
+    for (int it = tid; it < MT::I11 + MT::I12; it += nthr) {
+      if (it < MT::I11) {
+        // K11 item (slot group g, component a, row r)
+        const int r = it % NT, a = (it / NT) % M, g = it / (NT * M);
+        const int nd = s * NT + r;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < SG; ++j) {
+          const int slot = g * SG + j;
+          if (slot >= NS11) break;
+          const int64_t col = slot_col<C, NSIN>(kp, k, e, nd, slot, 0);
+          if (col < 0) continue;
+          const double* kv = b11 + ((slot * M + a) * NT + r) * M;
+          const double* xv = v + col * M;
+#pragma unroll
+          for (int c = 0; c < M; ++c) acc += kv[c] * __ldg(xv + c);
+        }
+        pp[(r * M + a) * NPART + g] = acc;
+      } else {
+        // K12 item (slot group g, stored row a', row r)
+        const int i2 = it - MT::I11;
+        const int r = i2 % NT, ap = (i2 / NT) % R12, g = i2 / (NT * R12);
+        const int nd = s * NT + r;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < SG; ++j) {
+          const int slot = g * SG + j;
+          if (slot >= NS12) break;
+          const int64_t col = slot_col<C, NSIN>(kp, k, e, nd, slot, 1);
+          if (col < 0) continue;
+          const double* kv = b12 + ((slot * R12 + ap) * NT + r) * MD;
+          const double* wv = w + col * MD;
+#pragma unroll
+          for (int c = 0; c < MD; ++c) acc += kv[c] * __ldg(wv + c);
+        }
+        pp[(r * M + ap + A0) * NPART + G11 + g] = acc;
+      }
+    }
+    __syncthreads();  // ring slot consumed, partials complete
+    if (tid == 0 && i + NS < n) issue(i + NS);
+    // owners: fixed-order sums, y = v - adt (K11 v + K12 w); they overlap the
+    // next tile's items (the partials are double-buffered)
+    if (tid < MT::NOUT) {
+      const int r = tid / M, a = tid - r * M;
+      const double* q = pp + tid * NPART;
+      double acc = 0.0;
+#pragma unroll
+      for (int g = 0; g < G11; ++g) acc += q[g];
+      if (a >= A0) {
+#pragma unroll
+        for (int g = 0; g < G12; ++g) acc += q[G11 + g];
+      }
+      const size_t yo = (e * NPE + s * NT) * M + tid;
+      (void)r;
+      y[yo] = __ldg(v + yo) - adt * acc;
+    }
+  }
+}
+
 // y = K12 w  (w: m*D per node); one thread per (row, stored row a')
 template <class C>
 __global__ void __launch_bounds__(128)
@@ -3398,45 +3066,42 @@ k_pc_build(const KParams<C> kp, const double* __restrict__ K11, const double* __
   }
   __syncthreads();
   if (C::SECOND) {
-    // K12 K21 on the pattern: every (row, K12 slot) path through its middle node
-    for (int w = tid; w < NPE * NS12; w += nthr) {
-      const int nd = w / NS12, s12 = w - nd * NS12;
-      const int64_t mid = slot_col<C, NSIN>(kp, k, e, nd, s12, 1);
-      if (mid < 0) continue;
-      const int em = static_cast<int>(mid / NPE), ndm = static_cast<int>(mid - static_cast<int64_t>(em) * NPE);
-      const int km = __ldg(kp.inv_order + em);
+    // K12 K21 on the pattern: every (row, K12 slot) path through its middle
+    // node.  One owner thread per (row node, row component, column component):
+    // it walks the paths in a fixed order and is the only writer of its
+    // entries, so the sums are deterministic (no atomics).
+    for (int w = tid; w < NPE * R12 * M; w += nthr) {
+      const int b = w % M, ap = (w / M) % R12, nd = w / (M * R12);
       const size_t T12 = static_cast<size_t>(k) * C::TPE + nd / NT;
-      const size_t T21 = static_cast<size_t>(km) * C::TPE + ndm / NT;
-      for (int s21 = 0; s21 < NS12; ++s21) {
-        const int64_t col = slot_col<C, NSIN>(kp, km, static_cast<size_t>(em), ndm, s21, 2);
-        if (col < 0 || col / NPE != static_cast<int64_t>(e)) continue;
-        const int cl = static_cast<int>(col - static_cast<int64_t>(e) * NPE);
-        if (!pc_on_line<C>(nd, cl)) continue;
-        double k21[D];
+      for (int s12 = 0; s12 < NS12; ++s12) {
+        const int64_t mid = slot_col<C, NSIN>(kp, k, e, nd, s12, 1);
+        if (mid < 0) continue;
+        const int em = static_cast<int>(mid / NPE), ndm = static_cast<int>(mid - static_cast<int64_t>(em) * NPE);
+        const int km = __ldg(kp.inv_order + em);
+        const size_t T21 = static_cast<size_t>(km) * C::TPE + ndm / NT;
+        double k12[D];
 #pragma unroll
-        for (int d = 0; d < D; ++d) k21[d] = __ldg(K21 + ((T21 * NS12 + s21) * NT + ndm % NT) * D + d);
-        for (int ap = 0; ap < R12; ++ap)
-          for (int b = 0; b < M; ++b) {
+        for (int d = 0; d < D; ++d)
+          k12[d] = __ldg(K12 + (((T12 * NS12 + s12) * R12 + ap) * NT + nd % NT) * MD + b * D + d);
+        for (int s21 = 0; s21 < NS12; ++s21) {
+          const int64_t col = slot_col<C, NSIN>(kp, km, static_cast<size_t>(em), ndm, s21, 2);
+          if (col < 0 || col / NPE != static_cast<int64_t>(e)) continue;
+          const int cl = static_cast<int>(col - static_cast<int64_t>(e) * NPE);
+          if (!pc_on_line<C>(nd, cl)) continue;
+          double sum = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) sum += k12[d] * __ldg(K21 + ((T21 * NS12 + s21) * NT + ndm % NT) * D + d);
+          Ms[(nd * M + ap + A0) * LDM + cl * M + b] += sum;
+        }
+        if (C::HAS_INV && kp.noslip && em == static_cast<int>(e) && (b == 0 || b == M - 1))
+          k21_wall_terms<C>(kp, km, ndm, [&](int end, const double* cf) {  // density and energy columns
+            if (!pc_on_line<C>(nd, end)) return;
             double sum = 0.0;
 #pragma unroll
-            for (int d = 0; d < D; ++d)
-              sum += __ldg(K12 + (((T12 * NS12 + s12) * R12 + ap) * NT + nd % NT) * MD + b * D + d) * k21[d];
-            atomicAdd(&Ms[(nd * M + ap + A0) * LDM + cl * M + b], sum);
-          }
+            for (int d = 0; d < D; ++d) sum += k12[d] * cf[d];
+            Ms[(nd * M + ap + A0) * LDM + end * M + b] += sum;
+          });
       }
-      if (C::HAS_INV && kp.noslip && em == static_cast<int>(e))
-        k21_wall_terms<C>(kp, km, ndm, [&](int end, const double* cf) {
-          if (!pc_on_line<C>(nd, end)) return;
-          for (int ap = 0; ap < R12; ++ap)
-            for (int bi = 0; bi < 2; ++bi) {  // density and energy columns
-              const int b = bi ? M - 1 : 0;
-              double sum = 0.0;
-#pragma unroll
-              for (int d = 0; d < D; ++d)
-                sum += __ldg(K12 + (((T12 * NS12 + s12) * R12 + ap) * NT + nd % NT) * MD + b * D + d) * cf[d];
-              atomicAdd(&Ms[(nd * M + ap + A0) * LDM + end * M + b], sum);
-            }
-        });
     }
     __syncthreads();
   }

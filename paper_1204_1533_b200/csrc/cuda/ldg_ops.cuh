@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <string>
 #include <cstring>
 
@@ -67,15 +70,37 @@ struct Ops {
   cudaError_t (*pc_apply)(const DevCtx&, const double* LUc, const int32_t* piv, const double* r, double* z);
 };
 
+// Persistent-grid size of a kernel on the CURRENT device (the context's
+// device: every C-ABI entry point makes it current): sets the dynamic
+// shared-memory attribute and measures occupancy once per (kernel, device);
+// thread-safe (launches from several host threads / contexts).
+inline int persistent_grid(const void* kernel, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find({kernel, dev});
+    if (it != cache.end()) return it->second;
+  }
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int per_sm = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (per_sm > 0 ? per_sm : 1) * sms;
+  std::lock_guard<std::mutex> g(mu);
+  cache[{kernel, dev}] = grid;
+  return grid;
+}
+
 template <class C>
 struct Launch {
-#ifndef LDG_RES_LINES  // line threads per residual CTA (EPB = elements per batch)
-  // measured: 64 for 2-D (C2 residual 35.9 -> 34.5 us: smaller batches, more
-  // CTAs per SM), 128 for 3-D (C4: 64 is 1.6 % slower)
+  // line threads per residual CTA (EPB = elements per batch); measured: 64
+  // for 2-D (C2 residual 35.9 -> 34.5 us: smaller batches, more CTAs per SM),
+  // 128 for 3-D (C4: 64 is 1.6 % slower)
   static constexpr int RES_LINES = C::D == 2 ? 64 : 128;
-#else
-  static constexpr int RES_LINES = LDG_RES_LINES;
-#endif
   static constexpr int EPB = RES_LINES / C::LPE > 0 ? RES_LINES / C::LPE : 1;
   static constexpr int RTHREADS = (EPB * C::LPE + 31) / 32 * 32;
 
@@ -100,41 +125,21 @@ struct Launch {
     kp.owned = d.owned;
     kp.inv_order = d.inv_order;
     kp.E = d.E;
-    static const int dbg = std::getenv("LDG_DEBUG_MASK") ? std::atoi(std::getenv("LDG_DEBUG_MASK")) : 0;
-    kp.dbg = dbg;
     return kp;
   }
   static void count(const DevCtx& d) {
     if (d.launches) ++*d.launches;
   }
 
-  // Residual: thread-per-line kernel (k_residual).  The sub-warp variant
-  // (k_residual_sw) is kept for comparison: it measured slower on B200
-  // (profiles/ncu_r1_summary.md).
-  // Residual: persistent TMA-prefetching kernel (k_residual_p); the
-  // one-shot kernel k_residual is kept as the LDG_RESIDUAL_SIMPLE fallback.
+  // Residual.  Kernel choice (measured on B200, bench.py --config N): the
+  // flattened flux-parallel kernel k_residual_f wins where the per-line work
+  // is long (second-order physics: viscous fluxes and the gradient at every
+  // point); the thread-per-line kernel k_residual_p wins for Euler.
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
-    static const bool simple = std::getenv("LDG_RESIDUAL_SIMPLE") != nullptr;
-    if (simple) return residual_simple(d, U, Q, R);
-    // Kernel choice (measured on B200, bench.py --config N): the flattened
-    // flux-parallel kernel wins where the per-line work is long (second-order
-    // physics: viscous fluxes and the gradient at every point); the
-    // thread-per-line kernel wins for Euler.  LDG_RESIDUAL=line|flux overrides.
-    static const char* sel = std::getenv("LDG_RESIDUAL");
-    const bool flux = sel ? std::string(sel) == "flux" : C::SECOND;
-    if (flux) return residual_f(d, U, Q, R);
+    if (C::SECOND) return residual_f(d, U, Q, R);
     using RP = ResP<C, EPB>;
     const size_t smem = sizeof(double) * RP::TOTAL;
-    static int grid_max = 0;
-    if (!grid_max) {
-      cudaFuncSetAttribute(k_residual_p<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_residual_p<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_residual_p<C, EPB>, RP::THREADS, smem);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
-    }
+    const int grid_max = persistent_grid(reinterpret_cast<const void*>(k_residual_p<C, EPB>), RP::THREADS, smem);
     const int nbatch = (d.E + EPB - 1) / EPB;
     const int grid = nbatch < grid_max ? nbatch : grid_max;
     k_residual_p<C, EPB><<<grid, RP::THREADS, smem, d.stream>>>(params(d), U, Q, R);
@@ -145,139 +150,55 @@ struct Launch {
     constexpr int EF = ResFEpb<C>::value;
     using RP = ResF<C, EF>;
     const size_t smem = sizeof(double) * RP::TOTAL;
-    static int grid_max = 0;
-    if (!grid_max) {
-      cudaFuncSetAttribute(k_residual_f<C, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_residual_f<C, EF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_residual_f<C, EF>, RP::THREADS, smem);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
-    }
+    const int grid_max = persistent_grid(reinterpret_cast<const void*>(k_residual_f<C, EF>), RP::THREADS, smem);
     const int nbatch = (d.E + EF - 1) / EF;
     const int grid = nbatch < grid_max ? nbatch : grid_max;
     k_residual_f<C, EF><<<grid, RP::THREADS, smem, d.stream>>>(params(d), U, Q, R);
     count(d);
     return cudaGetLastError();
   }
-  static cudaError_t gradient_f(const DevCtx& d, const double* U, double* Q) {
+  static cudaError_t gradient(const DevCtx& d, const double* U, double* Q) {
+    if (!C::SECOND) return cudaSuccess;
     constexpr int EF = GradFEpb<C>::value;
     using GP = GradF<C, EF>;
     const size_t smem = sizeof(double) * GP::TOTAL;
-    static int grid_max = 0;
-    if (!grid_max) {
-      cudaFuncSetAttribute(k_gradient_f<C, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_gradient_f<C, EF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gradient_f<C, EF>, GP::THREADS, smem);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
-    }
+    const int grid_max = persistent_grid(reinterpret_cast<const void*>(k_gradient_f<C, EF>), GP::THREADS, smem);
     const int nbatch = (d.E + EF - 1) / EF;
     const int grid = nbatch < grid_max ? nbatch : grid_max;
     k_gradient_f<C, EF><<<grid, GP::THREADS, smem, d.stream>>>(params(d), U, Q);
     count(d);
     return cudaGetLastError();
   }
-  static cudaError_t residual_simple(const DevCtx& d, const double* U, const double* Q, double* R) {
-    const size_t smem = sizeof(double) *
-                        (EPB * C::NPE * C::M + (C::SECOND ? EPB * C::NPE * C::MD : 0) + EPB * C::D * C::NPE * C::M);
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_residual<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      init = true;
-    }
-    const int grid = (d.E + EPB - 1) / EPB;
-    k_residual<C, EPB><<<grid, RTHREADS, smem, d.stream>>>(params(d), U, Q, R);
-    count(d);
-    return cudaGetLastError();
-  }
-  static cudaError_t residual_sw(const DevCtx& d, const double* U, const double* Q, double* R) {
-    using SW = SubWarp<C>;
-    const size_t smem = sizeof(double) * (SW::EPB * C::NPE * C::M + (C::SECOND ? SW::EPB * C::NPE * C::MD : 0) +
-                                          SW::EPB * C::D * C::NPE * C::M + 2 * C::NP * C::NQ + 2 * C::NP);
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_residual_sw<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_residual_sw<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      init = true;
-    }
-    const int grid = (d.E + SW::EPB - 1) / SW::EPB;
-    k_residual_sw<C><<<grid, SW::THREADS, smem, d.stream>>>(params(d), U, Q, R);
-    count(d);
-    return cudaGetLastError();
-  }
-  static cudaError_t gradient(const DevCtx& d, const double* U, double* Q) {
-    if (!C::SECOND) return cudaSuccess;
-    static const char* gsel = std::getenv("LDG_GRADIENT");
-    if (!(gsel && std::string(gsel) == "line")) return gradient_f(d, U, Q);
-    const size_t smem = sizeof(double) * (EPB * C::NPE * C::M + EPB * C::D * C::NPE * C::MD);
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_gradient<C, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_gradient<C, EPB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      init = true;
-    }
-    const int grid = (d.E + EPB - 1) / EPB;
-    k_gradient<C, EPB><<<grid, RTHREADS, smem, d.stream>>>(params(d), U, Q);
-    count(d);
-    return cudaGetLastError();
-  }
   static constexpr size_t jac_smem() { return sizeof(double) * JacSmem<C>::TOTAL; }
-#ifndef LDG_EJ_SEEDS
   static constexpr int EJ_SEEDS = C::M;  // seeds per k_endjac thread (primal shared)
-#else
-  static constexpr int EJ_SEEDS = LDG_EJ_SEEDS < C::M ? LDG_EJ_SEEDS : C::M;  // tuning knob
-#endif
   // Elements per assembly chunk: the endpoint-Jacobian scratch of one chunk
-  // stays within LDG_CHUNK_MB (default 512 MB).  Measured: fewer, larger chunks
-  // beat L2-sized ones (kernel ramps and tails per chunk outweigh the scratch
-  // re-read; C2 one chunk 0.252 vs 0.262 ms, C4 17.1 vs 18.3 ms).
+  // stays within 512 MB.  Measured: fewer, larger chunks beat L2-sized ones
+  // (kernel ramps and tails per chunk outweigh the scratch re-read; C2 one
+  // chunk 0.252 vs 0.262 ms, C4 17.1 vs 18.3 ms).
   static int chunk_elems(int E) {
     const long long per = static_cast<long long>(EndJac<C>::PER_ELEM) * 8;
-    static const long long budget = (std::getenv("LDG_CHUNK_MB") ? std::atoll(std::getenv("LDG_CHUNK_MB")) : 512LL) << 20;
-    long long n = budget / (per > 0 ? per : 1);
+    long long n = (512LL << 20) / (per > 0 ? per : 1);
     if (n < 1024) n = 1024;
     return static_cast<int>(n < E ? n : E);
   }
+  // Assembly kernel family of this configuration (compile-time):
+  //   k_jacobian_p  persistent element units with a TMA prefetch ring (2-D, 3-D p <= 3)
+  //   k_jac_s3      3-D line streaming (element flux-Jacobian set beyond shared memory)
+  //   k_jacobian    one CTA per slab / line work unit (fallback)
+  static constexpr int JAC_KIND = JacP<C>::OK ? 0 : ((C::D == 3 && C::WU != 0 && JacS3<C>::OK) ? 1 : 2);
   static cudaError_t jacobian(const DevCtx& d, const double* U, const double* Q, double* SE, double* K11,
                               double* K12) {
-    const size_t smem = jac_smem();
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(k_jacobian<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      init = true;
-    }
     constexpr int IPS = EndJac<C>::items(EJ_SEEDS);
-    static const bool one_seed = std::getenv("LDG_ENDJAC_SEEDS1") != nullptr;  // tuning switch
-    static const bool simple = std::getenv("LDG_JACOBIAN_SIMPLE") != nullptr;
-    static int grid_max = 0;
+    const size_t smem = jac_smem();
     const size_t psmem = sizeof(double) * JacP<C>::TOTAL;
-    if (JacP<C>::OK && !grid_max) {
-      cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-      cudaFuncSetAttribute(k_jacobian_p<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobian_p<C>, JacThreads<C>::value, psmem);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      grid_max = (per_sm > 0 ? per_sm : 1) * sms;
-    }
-    static const bool units = std::getenv("LDG_JAC_UNITS") != nullptr;  // 3-D: slab/line work units instead
-    static const bool force_s3 = std::getenv("LDG_JAC_S3") != nullptr;  // 3-D: line streaming for element units too
     const size_t s3smem = sizeof(double) * JacS3<C>::TOTAL;
-    static int s3_grid = 0;
-    if (C::D == 3 && (C::WU != 0 || force_s3) && JacS3<C>::OK && !s3_grid) {
-      cudaFuncSetAttribute(k_jac_s3<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3smem);
-      cudaFuncSetAttribute(k_jac_s3<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      s3_grid = sms;
-    }
+    int grid_max = 0;
+    if (JAC_KIND == 0)
+      grid_max = persistent_grid(reinterpret_cast<const void*>(k_jacobian_p<C>), JacThreads<C>::value, psmem);
+    else if (JAC_KIND == 1)
+      grid_max = persistent_grid(reinterpret_cast<const void*>(k_jac_s3<C>), JacS3<C>::THREADS, s3smem);
+    else
+      persistent_grid(reinterpret_cast<const void*>(k_jacobian<C>), JacThreads<C>::value, smem);
     const int chunk = chunk_elems(d.E);
     for (int kb = 0, ci = 0; kb < d.E; kb += chunk, ++ci) {
       const int ke = kb + chunk < d.E ? kb + chunk : d.E;
@@ -286,19 +207,14 @@ struct Launch {
       const long long oe = d.owned ? d.owned_off[ci + 1] : static_cast<long long>(ke - kb) * 2 * C::D;
       const long long nf = oe - ob;
       // (fused configurations: the persistent assembly computes the endpoint
-      // Jacobians itself -- only when that kernel runs)
-      const bool fused = JacP<C>::FE && JacP<C>::OK && !simple && !(C::D == 3 && force_s3);
-      if (fused) {
-      } else if (one_seed) {
-        const long long items = nf * C::NL * EndJac<C>::items(1);
-        k_endjac<C, 1, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
-            params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
-      } else {
+      // Jacobians itself)
+      const bool fused = JacP<C>::FE && JAC_KIND == 0;
+      if (!fused) {
         const long long items = nf * C::NL * IPS;
         k_endjac<C, EJ_SEEDS, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
             params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
+        count(d);
       }
-      if (!fused) count(d);
       // slip-wall / Neumann boundary ends of the chunk (general kinds)
       if (d.bspec && d.bspec_off[ci + 1] > d.bspec_off[ci]) {
         const long long sb = d.bspec_off[ci], se = d.bspec_off[ci + 1];
@@ -307,14 +223,11 @@ struct Launch {
             params(d), U, Q, SE, kb, ke, sb, se, d.bspec);
         count(d);
       }
-      if (JacP<C>::OK && !simple && !(C::D == 3 && force_s3)) {
-        const int n = ke - kb;
-        const int grid = n < grid_max ? n : grid_max;
+      const int n = ke - kb;
+      const int grid = n < grid_max ? n : grid_max;
+      if (JAC_KIND == 0) {
         k_jacobian_p<C><<<grid, JacThreads<C>::value, psmem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
-      } else if (C::D == 3 && (C::WU != 0 || force_s3) && JacS3<C>::OK && !units) {
-        // 3-D line-streaming assembly (one persistent CTA per element)
-        const int n = ke - kb;
-        const int grid = n < s3_grid ? n : s3_grid;
+      } else if (JAC_KIND == 1) {
         k_jac_s3<C><<<grid, JacS3<C>::THREADS, s3smem, d.stream>>>(params(d), U, Q, SE, K11, K12, kb, ke);
       } else {
         k_jacobian<C><<<(ke - kb) * C::UPE, JacThreads<C>::value, smem, d.stream>>>(params(d), U, Q, SE, K11,
@@ -372,6 +285,14 @@ struct Launch {
   }
   static cudaError_t split(const DevCtx& d, const double* V11, const double* V12, const double* v,
                            const double* w, double adt, double* y) {
+    if (MvT<C>::OK) {
+      // second-order physics: TMA tile streaming of K11 + K12 (k_mv_tiles)
+      const size_t smem = sizeof(double) * MvT<C>::TOTAL;
+      const int grid = persistent_grid(reinterpret_cast<const void*>(k_mv_tiles<C>), MvT<C>::THREADS, smem);
+      k_mv_tiles<C><<<grid, MvT<C>::THREADS, smem, d.stream>>>(params(d), V11, V12, v, w, adt, y);
+      count(d);
+      return cudaGetLastError();
+    }
     k_spmv11<C, true><<<rgrid_m(d), 128, 0, d.stream>>>(params(d), V11, V12, v, w, adt, y, spmv_rev(d));
     count(d);
     return cudaGetLastError();
@@ -381,11 +302,7 @@ struct Launch {
   static void pc_build_t(const DevCtx& d, const double* V11, const double* V12, const double* V21, double adt,
                          double* LUc, int32_t* piv, int* bad) {
     using PC = PcCfg<C, INV>;
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_pc_build<C, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::smem());
-      init = true;
-    }
+    persistent_grid(reinterpret_cast<const void*>(k_pc_build<C, INV>), PC::THREADS, PC::smem());
     k_pc_build<C, INV><<<d.E, PC::THREADS, PC::smem(), d.stream>>>(params(d), V11, V12, V21, adt, LUc, piv, bad);
   }
   static cudaError_t pc_build(const DevCtx& d, const double* V11, const double* V12, const double* V21, double adt,

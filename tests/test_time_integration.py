@@ -106,6 +106,61 @@ def test_dirk3_free_stream_and_reuse_policy():
     assert s3["jacobian_assemblies"] > 1, s3
 
 
+def drift_case(p=2, n=2):
+    """u_t = Laplacian u + S with S = x + y and time-dependent Dirichlet data
+    g_D(x, t) = t (x + y) on every side: the exact solution u = t (x + y) is
+    linear in space (reproduced exactly by the LDG operator) and in time, so
+    RK4 and DIRK3 are exact up to rounding -- but only when every stage
+    evaluates the boundary data at its own stage time."""
+    c = Case.lattice(2, n, p, periodic=False)
+    ph = Physics(_abi.LDG_POISSON, c11_bd=1.0, bcs=[(t, [0.0]) for t in (1, 2, 3, 4)])
+    xy = c.coords.reshape(-1, 2)
+    S = xy[:, 0] + xy[:, 1]
+    return c, ph, S
+
+
+def _drift_run(o, S, scheme, dt, steps):
+    for tag in (1, 2, 3, 4):
+        o.set_boundary_function(tag, lambda x, t: [t * (x[0] + x[1])])
+    o.set_source(S)
+    U = np.zeros_like(S)
+    cfg = newton_cfg(gmres_iters=S.size, recompute_threshold=1000, max_newton=20, use_precond=False,
+                     newton_tol=1e-10)
+    for k in range(steps):
+        if scheme == "rk4":
+            U = o.rk4_step(U, dt, t=k * dt)
+        else:
+            U, _ = o.dirk3_step(U, dt, cfg, t=k * dt)
+    return U
+
+
+@pytest.mark.parametrize("scheme", ["rk4", "dirk3"])
+def test_stage_times_with_time_dependent_boundary_data(scheme):
+    c, ph, S = drift_case()
+    dt, steps = (0.0005, 8) if scheme == "rk4" else (0.05, 4)
+    U = _drift_run(Oracle(c, ph), S, scheme, dt, steps)
+    exact = dt * steps * S
+    assert np.abs(U - exact).max() <= 1e-9 * np.abs(exact).max(), np.abs(U - exact).max()
+
+
+# ---------------------------------------------------------------- GPU parity
+@pytest.mark.gpu
+@pytest.mark.parametrize("scheme", ["rk4", "dirk3"])
+def test_gpu_stage_times_with_time_dependent_boundary_data(scheme):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1204_1533_b200.linedg import LineDG
+
+    c, ph, S = drift_case()
+    dt, steps = (0.0005, 8) if scheme == "rk4" else (0.05, 4)
+    Ug = _drift_run(LineDG(c, ph), S, scheme, dt, steps)
+    Uo = _drift_run(Oracle(c, ph), S, scheme, dt, steps)
+    exact = dt * steps * S
+    assert np.abs(Ug - exact).max() <= 1e-9 * np.abs(exact).max()
+    assert np.abs(Ug - Uo).max() <= 1e-11 * np.abs(exact).max()
+
+
 # ---------------------------------------------------------------- GPU parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("ci,n", [(1, 3), (2, 3), (0, 4)])
