@@ -2662,6 +2662,42 @@ __device__ __forceinline__ int64_t slot_col(const KParams<C>& kp, int k, size_t 
   return static_cast<int64_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
 }
 
+// slot_col with the element's 2D connectivity entries already at hand (cn).
+template <class C, int NSIN>
+__device__ __forceinline__ int64_t slot_col_c(const int2* cn, size_t e, int nd, int slot, int kind) {
+  constexpr int NP = C::NP, P = C::P, NPE = C::NPE;
+  const int x[3] = {nd % NP, (nd / NP) % NP, nd / (NP * NP)};
+  const int st[3] = {1, NP, NP * NP};
+  if (slot < NSIN) {
+    int dir, t;
+    if (slot < NP) {
+      dir = 0;
+      t = slot;
+    } else {
+      const int z = slot - NP;
+      dir = 1 + z / P;
+      t = z % P;
+      if (t >= x[dir]) ++t;
+    }
+    return static_cast<int64_t>(e) * NPE + nd + (t - x[dir]) * st[dir];
+  }
+  int dir, side;
+  const int z = slot - NSIN;
+  if (kind == 0) {
+    dir = z >> 1;
+    side = z & 1;
+  } else {
+    dir = z;
+    const bool plus1 = conn_sign(cn[dir * 2 + 1].y) > 0;
+    side = kind == 1 ? (plus1 ? 1 : 0) : (plus1 ? 0 : 1);
+  }
+  const int2 c = cn[dir * 2 + side];
+  if (c.x < 0) return -1;
+  int line, pos;
+  line_of<C>(dir, nd, line, pos);
+  return static_cast<int64_t>(c.x) * NPE + conn_node(c.y, line, NP);
+}
+
 // y = K11 x  (SPLIT: y = v - adt (K11 v + K12 w), the split matvec).
 // One thread per (row, output component a); a warp covers 32 consecutive
 // rows of one a.  Block row a of a slot is m contiguous doubles (16-byte
@@ -2775,18 +2811,19 @@ k_spmv11(const KParams<C> kp, const double* __restrict__ V11, const double* __re
 
 // Split matvec y = v - adt (K11 v + K12 w) for second-order physics, streamed
 // tile by tile (k_mv_tiles).  The store keeps each row tile's K11 and K12
-// values contiguous (19 KB + 38 KB per dir-0 line tile of C5, 42 KB + 53 KB
-// per element tile of C3), so a persistent CTA per SM pulls whole tiles into
-// shared memory with 1-D TMA bulk copies (cp.async.bulk, completion on an
-// mbarrier) on an NSTAGE-deep ring: the HBM stream is a sequence of large
-// bulk reads instead of per-thread strided 8-byte loads (the K12 rows are
-// m*D = 15 doubles per lane in the row-per-thread kernel).  Within a tile one
-// item per (slot group, output component, row) forms a partial dot product
-// of its shared-memory values with the gathered v / w of the slot's column
-// node (L1/L2 hits: a CTA walks consecutive tiles of the same elements); the
-// partials land in shared memory and the (row, component) owner sums them in
-// a fixed order (deterministic, no atomics) and writes y while the next
-// tile's items run.
+// values contiguous (19 KB + 38 KB per dir-0 line tile of C5), so a
+// persistent CTA per SM pulls whole tiles into shared memory with 1-D TMA
+// bulk copies (cp.async.bulk, completion on an mbarrier) on an NSTAGE-deep
+// ring: the HBM stream is a sequence of large bulk reads instead of
+// per-thread strided 8-byte loads (the K12 rows are m*D = 15 doubles per lane
+// in the row-per-thread kernel).  The v / w entries of every (slot, row)
+// column node of tile i+1 are gathered into shared memory with cp.async while
+// tile i computes (L1/L2 hits: a CTA walks consecutive tiles of the same
+// elements; the tile's connectivity is fetched two tiles ahead).  Within a
+// tile one item per (slot group, output component, row) forms a partial dot
+// product from shared memory only; the partials land in shared memory and the
+// (row, component) owner sums them in a fixed order (deterministic, no
+// atomics) and writes y.  The gathers run on the threads with one item fewer.
 template <class C>
 struct MvT {
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
@@ -2796,17 +2833,21 @@ struct MvT {
   static constexpr int BUF11 = ev(ST11 + 1);          // +1: an odd tile offset is loaded from 8 B earlier
   static constexpr int BUF12 = ev(ST12 + 1);
   static constexpr int BUF = BUF11 + BUF12;
+  static constexpr int GX = C::NS11 * NT * M;          // gathered v per tile [slot][row][c]
+  static constexpr int GW = C::NS12 * NT * MD;         // gathered w per tile [slot][row][c]
+  static constexpr int GBUF = ev(GX + GW);
   // slots per item: one for line tiles (few rows), three for element tiles
   static constexpr int SG = NT <= 8 ? 1 : 3;
   static constexpr int G11 = (C::NS11 + SG - 1) / SG, G12 = (C::NS12 + SG - 1) / SG;
   static constexpr int NPART = G11 + G12;
   static constexpr int NOUT = NT * M;
   static constexpr int PART = ev(NOUT * NPART);
-  static constexpr int THREADS = 256;
+  static constexpr int THREADS = 512;
   static constexpr int I11 = G11 * M * NT, I12 = G12 * R12 * NT;  // items per tile
-  static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + 2 * PART) + 64; }
-  static constexpr int NSTAGE = bytes(3) <= 200 * 1024 ? 3 : 2;
-  static constexpr int TOTAL = NSTAGE * BUF + 2 * PART;
+  static constexpr int NG = (C::NS11 + C::NS12) * NT;             // gathered column nodes per tile
+  static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + 2 * GBUF + 2 * PART) + 64; }
+  static constexpr int NSTAGE = bytes(3) <= 224 * 1024 ? 3 : 2;
+  static constexpr int TOTAL = NSTAGE * BUF + 2 * GBUF + 2 * PART;
   static constexpr bool OK = C::SECOND && bytes(2) <= 220 * 1024;
 };
 
@@ -2822,13 +2863,25 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t bar[NS];
   double* const ring = smem;
-  double* const part = smem + NS * MT::BUF;
+  double* const gath = smem + NS * MT::BUF;
+  double* const part = gath + 2 * MT::GBUF;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int64_t ntiles = static_cast<int64_t>(kp.E) * TPE;
   const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * per;
   const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
   const int n = t1 > t0 ? static_cast<int>(t1 - t0) : 0;
+  // connectivity + element id of tile i, fetched two tiles ahead (cp.async)
+  __shared__ __align__(16) int2 sconn[3][2 * C::D];
+  __shared__ int sel[3];
+  auto fetch_conn = [&](int i) {
+    const int64_t T = t0 + i;
+    const int k = static_cast<int>(T / TPE);
+    if (tid < 2 * C::D) cp_async8(&sconn[i % 3][tid], kp.conn + static_cast<size_t>(k) * 2 * C::D + tid);
+    if (tid == 2 * C::D)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&sel[i % 3])), "l"(kp.order + k)
+                   : "memory");
+  };
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     mbar_fence_init();
@@ -2845,58 +2898,92 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
     tma_load_1d_once(b, V11 + (o11 & ~int64_t(1)), by11, &bar[i % NS]);
     tma_load_1d_once(b + MT::BUF11, V12 + (o12 & ~int64_t(1)), by12, &bar[i % NS]);
   };
+  // v / w of every (slot, row) column node of tile i -> gather buffer i & 1
+  // (its connectivity is in sconn[i % 3] already); on the highest thread
+  // ids, which carry one compute item fewer
+  auto gather = [&](int i) {
+    const int64_t T = t0 + i;
+    const int k = static_cast<int>(T / TPE), s = static_cast<int>(T - static_cast<int64_t>(k) * TPE);
+    const int2* cn = sconn[i % 3];
+    const size_t e = static_cast<size_t>(sel[i % 3]);
+    double* gb = gath + (i & 1) * MT::GBUF;
+    for (int u = nthr - 1 - tid; u < MT::NG; u += nthr) {
+      const bool is11 = u < NS11 * NT;
+      const int u2 = is11 ? u : u - NS11 * NT;
+      const int slot = u2 / NT, r = u2 - slot * NT;
+      const int64_t col = slot_col_c<C, NSIN>(cn, e, s * NT + r, slot, is11 ? 0 : 1);
+      double* dst = is11 ? gb + (slot * NT + r) * M : gb + MT::GX + (slot * NT + r) * MD;
+      const int len = is11 ? M : MD;
+      if (col < 0) {
+        for (int c = 0; c < len; ++c) dst[c] = 0.0;
+      } else {
+        const double* src = is11 ? v + col * M : w + col * MD;
+        for (int c = 0; c < len; ++c) cp_async8(dst + c, src + c);
+      }
+    }
+  };
   if (tid == 0)
     for (int i = 0; i < NS && i < n; ++i) issue(i);
+  if (n > 0) {
+    fetch_conn(0);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    gather(0);
+    if (n > 1) fetch_conn(1);
+    cp_async_commit();
+  }
   for (int i = 0; i < n; ++i) {
     const int64_t T = t0 + i;
     const int k = static_cast<int>(T / TPE), s = static_cast<int>(T - static_cast<int64_t>(k) * TPE);
-    const size_t e = __ldg(kp.order + k);
     const double* b11 = ring + (i % NS) * MT::BUF + ((T * MT::ST11) & 1);
     const double* b12 = ring + (i % NS) * MT::BUF + MT::BUF11 + ((T * MT::ST12) & 1);
+    const double* gx = gath + (i & 1) * MT::GBUF;
+    const double* gw = gx + MT::GX;
     double* pp = part + (i & 1) * MT::PART;
+    cp_async_wait_all();
+    __syncthreads();  // gathers of tile i and the connectivity of tile i+1 visible
+    const size_t e = static_cast<size_t>(sel[i % 3]);
+    if (i + 1 < n) gather(i + 1);  // overlaps this tile's items
+    if (i + 2 < n) fetch_conn(i + 2);
+    cp_async_commit();
     mbar_wait(&bar[i % NS], (i / NS) & 1);
     for (int it = tid; it < MT::I11 + MT::I12; it += nthr) {
       if (it < MT::I11) {
         // K11 item (slot group g, component a, row r)
         const int r = it % NT, a = (it / NT) % M, g = it / (NT * M);
-        const int nd = s * NT + r;
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < SG; ++j) {
           const int slot = g * SG + j;
           if (slot >= NS11) break;
-          const int64_t col = slot_col<C, NSIN>(kp, k, e, nd, slot, 0);
-          if (col < 0) continue;
           const double* kv = b11 + ((slot * M + a) * NT + r) * M;
-          const double* xv = v + col * M;
+          const double* xv = gx + (slot * NT + r) * M;
 #pragma unroll
-          for (int c = 0; c < M; ++c) acc += kv[c] * __ldg(xv + c);
+          for (int c = 0; c < M; ++c) acc += kv[c] * xv[c];
         }
         pp[(r * M + a) * NPART + g] = acc;
       } else {
         // K12 item (slot group g, stored row a', row r)
         const int i2 = it - MT::I11;
         const int r = i2 % NT, ap = (i2 / NT) % R12, g = i2 / (NT * R12);
-        const int nd = s * NT + r;
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < SG; ++j) {
           const int slot = g * SG + j;
           if (slot >= NS12) break;
-          const int64_t col = slot_col<C, NSIN>(kp, k, e, nd, slot, 1);
-          if (col < 0) continue;
           const double* kv = b12 + ((slot * R12 + ap) * NT + r) * MD;
-          const double* wv = w + col * MD;
+          const double* wv = gw + (slot * NT + r) * MD;
 #pragma unroll
-          for (int c = 0; c < MD; ++c) acc += kv[c] * __ldg(wv + c);
+          for (int c = 0; c < MD; ++c) acc += kv[c] * wv[c];
         }
         pp[(r * M + ap + A0) * NPART + G11 + g] = acc;
       }
     }
     __syncthreads();  // ring slot consumed, partials complete
     if (tid == 0 && i + NS < n) issue(i + NS);
-    // owners: fixed-order sums, y = v - adt (K11 v + K12 w); they overlap the
-    // next tile's items (the partials are double-buffered)
+    // owners: fixed-order sums, y = v - adt (K11 v + K12 w); v of the row is
+    // the gathered self column (dir-0 slot t = r)
     if (tid < MT::NOUT) {
       const int r = tid / M, a = tid - r * M;
       const double* q = pp + tid * NPART;
@@ -2907,9 +2994,9 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
 #pragma unroll
         for (int g = 0; g < G12; ++g) acc += q[G11 + g];
       }
-      const size_t yo = (e * NPE + s * NT) * M + tid;
-      (void)r;
-      y[yo] = __ldg(v + yo) - adt * acc;
+      const int rs = NT == C::NP ? r : r % C::NP;  // dir-0 position of the row
+      const double vr = gx[(rs * NT + r) * M + a];
+      y[(e * NPE + s * NT) * M + tid] = vr - adt * acc;
     }
   }
 }
