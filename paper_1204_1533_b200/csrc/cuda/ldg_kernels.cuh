@@ -2836,19 +2836,22 @@ struct MvT {
   static constexpr int GX = C::NS11 * NT * M;          // gathered v per tile [slot][row][c]
   static constexpr int GW = C::NS12 * NT * MD;         // gathered w per tile [slot][row][c]
   static constexpr int GBUF = ev(GX + GW);
-  // slots per item: one for line tiles (few rows), three for element tiles
-  static constexpr int SG = NT <= 8 ? 1 : 3;
-  static constexpr int G11 = (C::NS11 + SG - 1) / SG, G12 = (C::NS12 + SG - 1) / SG;
+  // slots per item: K11 items take SG11 slots, K12 items SG12, so that every
+  // item is about m*D multiply-adds long (C5: 15 each, 495 items, one round)
+  static constexpr int SG11 = (MD + M - 1) / M, SG12 = 1;
+  static constexpr int SG = SG11;
+  static constexpr int G11 = (C::NS11 + SG11 - 1) / SG11, G12 = (C::NS12 + SG12 - 1) / SG12;
   static constexpr int NPART = G11 + G12;
   static constexpr int NOUT = NT * M;
   static constexpr int PART = ev(NOUT * NPART);
-  static constexpr int THREADS = 512;
+  static constexpr int THREADS = 1024;
   static constexpr int I11 = G11 * M * NT, I12 = G12 * R12 * NT;  // items per tile
-  static constexpr int NG = (C::NS11 + C::NS12) * NT;             // gathered column nodes per tile
+  // gather units: one per (K11 slot, row) and per (K12 slot, row, M-component group)
+  static constexpr int NG = C::NS11 * NT + C::NS12 * NT * (MD / M);
   static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + 2 * GBUF + 2 * PART) + 64; }
   static constexpr int NSTAGE = bytes(3) <= 224 * 1024 ? 3 : 2;
   static constexpr int TOTAL = NSTAGE * BUF + 2 * GBUF + 2 * PART;
-  static constexpr bool OK = C::SECOND && bytes(2) <= 220 * 1024;
+  static constexpr bool OK = C::SECOND && MD % M == 0 && bytes(2) <= 220 * 1024;
 };
 
 template <class C>
@@ -2910,15 +2913,18 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
     for (int u = nthr - 1 - tid; u < MT::NG; u += nthr) {
       const bool is11 = u < NS11 * NT;
       const int u2 = is11 ? u : u - NS11 * NT;
-      const int slot = u2 / NT, r = u2 - slot * NT;
+      const int bg = is11 ? 0 : u2 % (MD / M);
+      const int sr = is11 ? u2 : u2 / (MD / M);
+      const int slot = sr / NT, r = sr - slot * NT;
       const int64_t col = slot_col_c<C, NSIN>(cn, e, s * NT + r, slot, is11 ? 0 : 1);
-      double* dst = is11 ? gb + (slot * NT + r) * M : gb + MT::GX + (slot * NT + r) * MD;
-      const int len = is11 ? M : MD;
+      double* dst = is11 ? gb + (slot * NT + r) * M : gb + MT::GX + (slot * NT + r) * MD + bg * M;
       if (col < 0) {
-        for (int c = 0; c < len; ++c) dst[c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < M; ++c) dst[c] = 0.0;
       } else {
-        const double* src = is11 ? v + col * M : w + col * MD;
-        for (int c = 0; c < len; ++c) cp_async8(dst + c, src + c);
+        const double* src = is11 ? v + col * M : w + col * MD + bg * M;
+#pragma unroll
+        for (int c = 0; c < M; ++c) cp_async8(dst + c, src + c);
       }
     }
   };
@@ -2969,8 +2975,8 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
         const int r = i2 % NT, ap = (i2 / NT) % R12, g = i2 / (NT * R12);
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < SG; ++j) {
-          const int slot = g * SG + j;
+        for (int j = 0; j < MT::SG12; ++j) {
+          const int slot = g * MT::SG12 + j;
           if (slot >= NS12) break;
           const double* kv = b12 + ((slot * R12 + ap) * NT + r) * MD;
           const double* wv = gw + (slot * NT + r) * MD;
