@@ -2851,7 +2851,9 @@ struct MvT {
   static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + 2 * GBUF + 2 * PART) + 64; }
   static constexpr int NSTAGE = bytes(3) <= 224 * 1024 ? 3 : 2;
   static constexpr int TOTAL = NSTAGE * BUF + 2 * GBUF + 2 * PART;
-  static constexpr bool OK = C::SECOND && MD % M == 0 && bytes(2) <= 220 * 1024;
+  // thread roles: items, owners (one warp per 32 outputs), issuer, gathers
+  static constexpr int ROLES = (I11 + I12 + 31) / 32 * 32 + (NOUT + 31) / 32 * 32 + 1 + NG;
+  static constexpr bool OK = C::SECOND && MD % M == 0 && SG12 == 1 && ROLES <= THREADS && bytes(2) <= 220 * 1024;
 };
 
 template <class C>
@@ -2863,6 +2865,11 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
                 R12 = C::R12, SG = MT::SG, G11 = MT::G11, G12 = MT::G12, NPART = MT::NPART, NS = MT::NSTAGE;
   constexpr int NSIN = C::D * C::P + 1;
   constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+  // thread roles (one CTA barrier per tile): items of tile i on the lowest
+  // ids, the owners of tile i-1 (fixed-order partial sums, y) and the TMA
+  // issuer next, the gathers of tile i+1 on the highest ids
+  constexpr int NITEM = MT::I11 + MT::I12;
+  constexpr int OWN0 = (NITEM + 31) / 32 * 32, ISSUER = OWN0 + (MT::NOUT + 31) / 32 * 32;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t bar[NS];
   double* const ring = smem;
@@ -2877,7 +2884,9 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
   // connectivity + element id of tile i, fetched two tiles ahead (cp.async)
   __shared__ __align__(16) int2 sconn[3][2 * C::D];
   __shared__ int sel[3];
-  auto fetch_conn = [&](int i) {
+  __shared__ int gel[4];  // element id of tile i (gel[i & 3]), for its owners one iteration later
+  auto fetch_conn = [&](int i) {  // by threads 0 .. 2D
+    if (i >= n) return;
     const int64_t T = t0 + i;
     const int k = static_cast<int>(T / TPE);
     if (tid < 2 * C::D) cp_async8(&sconn[i % 3][tid], kp.conn + static_cast<size_t>(k) * 2 * C::D + tid);
@@ -2890,7 +2899,7 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
     mbar_fence_init();
   }
   __syncthreads();
-  // one elected thread streams tile i into ring slot i % NS
+  // the issuer streams tile i into ring slot i % NS
   auto issue = [&](int i) {
     const int64_t T = t0 + i;
     double* b = ring + (i % NS) * MT::BUF;
@@ -2902,14 +2911,15 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
     tma_load_1d_once(b + MT::BUF11, V12 + (o12 & ~int64_t(1)), by12, &bar[i % NS]);
   };
   // v / w of every (slot, row) column node of tile i -> gather buffer i & 1
-  // (its connectivity is in sconn[i % 3] already); on the highest thread
-  // ids, which carry one compute item fewer
+  // (its connectivity is in sconn[i % 3] already); highest thread ids
   auto gather = [&](int i) {
+    if (i >= n) return;
     const int64_t T = t0 + i;
     const int k = static_cast<int>(T / TPE), s = static_cast<int>(T - static_cast<int64_t>(k) * TPE);
     const int2* cn = sconn[i % 3];
     const size_t e = static_cast<size_t>(sel[i % 3]);
     double* gb = gath + (i & 1) * MT::GBUF;
+    if (tid == nthr - 1) gel[i & 3] = static_cast<int>(e);
     for (int u = nthr - 1 - tid; u < MT::NG; u += nthr) {
       const bool is11 = u < NS11 * NT;
       const int u2 = is11 ? u : u - NS11 * NT;
@@ -2928,33 +2938,44 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
       }
     }
   };
-  if (tid == 0)
-    for (int i = 0; i < NS && i < n; ++i) issue(i);
-  if (n > 0) {
-    fetch_conn(0);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    gather(0);
-    if (n > 1) fetch_conn(1);
-    cp_async_commit();
-  }
-  for (int i = 0; i < n; ++i) {
+  // owners of tile i: fixed-order sums of its partials, y = v - adt (K11 v + K12 w)
+  auto owners = [&](int i) {
+    const int o = tid - OWN0;
     const int64_t T = t0 + i;
     const int k = static_cast<int>(T / TPE), s = static_cast<int>(T - static_cast<int64_t>(k) * TPE);
-    const double* b11 = ring + (i % NS) * MT::BUF + ((T * MT::ST11) & 1);
-    const double* b12 = ring + (i % NS) * MT::BUF + MT::BUF11 + ((T * MT::ST12) & 1);
-    const double* gx = gath + (i & 1) * MT::GBUF;
-    const double* gw = gx + MT::GX;
-    double* pp = part + (i & 1) * MT::PART;
+    const int a = o % M;
+    const double* q = part + (i & 1) * MT::PART + o * NPART;
+    double acc = 0.0;
+#pragma unroll
+    for (int g = 0; g < G11; ++g) acc += q[g];
+    if (a >= A0) {
+#pragma unroll
+      for (int g = 0; g < G12; ++g) acc += q[G11 + g];
+    }
+    const size_t yo = (static_cast<size_t>(gel[i & 3]) * NPE + s * NT) * M + o;
+    y[yo] = __ldg(v + yo) - adt * acc;
+  };
+  if (tid == ISSUER)
+    for (int i = 0; i < NS && i < n; ++i) issue(i);
+  fetch_conn(0);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  gather(0);
+  fetch_conn(1);
+  cp_async_commit();
+  for (int i = 0; i < n; ++i) {
+    const int64_t T = t0 + i;
     cp_async_wait_all();
-    __syncthreads();  // gathers of tile i and the connectivity of tile i+1 visible
-    const size_t e = static_cast<size_t>(sel[i % 3]);
-    if (i + 1 < n) gather(i + 1);  // overlaps this tile's items
-    if (i + 2 < n) fetch_conn(i + 2);
-    cp_async_commit();
-    mbar_wait(&bar[i % NS], (i / NS) & 1);
-    for (int it = tid; it < MT::I11 + MT::I12; it += nthr) {
+    __syncthreads();  // gathers of tile i visible; items and owners of the previous iteration done
+    if (tid < NITEM) {
+      const double* b11 = ring + (i % NS) * MT::BUF + ((T * MT::ST11) & 1);
+      const double* b12 = ring + (i % NS) * MT::BUF + MT::BUF11 + ((T * MT::ST12) & 1);
+      const double* gx = gath + (i & 1) * MT::GBUF;
+      const double* gw = gx + MT::GX;
+      double* pp = part + (i & 1) * MT::PART;
+      mbar_wait(&bar[i % NS], (i / NS) & 1);
+      const int it = tid;
       if (it < MT::I11) {
         // K11 item (slot group g, component a, row r)
         const int r = it % NT, a = (it / NT) % M, g = it / (NT * M);
@@ -2970,41 +2991,28 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
         }
         pp[(r * M + a) * NPART + g] = acc;
       } else {
-        // K12 item (slot group g, stored row a', row r)
+        // K12 item (slot g, stored row a', row r)
         const int i2 = it - MT::I11;
         const int r = i2 % NT, ap = (i2 / NT) % R12, g = i2 / (NT * R12);
         double acc = 0.0;
+        const double* kv = b12 + ((g * R12 + ap) * NT + r) * MD;
+        const double* wv = gw + (g * NT + r) * MD;
 #pragma unroll
-        for (int j = 0; j < MT::SG12; ++j) {
-          const int slot = g * MT::SG12 + j;
-          if (slot >= NS12) break;
-          const double* kv = b12 + ((slot * R12 + ap) * NT + r) * MD;
-          const double* wv = gw + (slot * NT + r) * MD;
-#pragma unroll
-          for (int c = 0; c < MD; ++c) acc += kv[c] * wv[c];
-        }
+        for (int c = 0; c < MD; ++c) acc += kv[c] * wv[c];
         pp[(r * M + ap + A0) * NPART + G11 + g] = acc;
       }
+    } else if (tid >= OWN0 && tid < OWN0 + MT::NOUT) {
+      if (i > 0) owners(i - 1);
+    } else if (tid == ISSUER) {
+      // ring slot (i - 1) % NS was consumed before this iteration's barrier
+      if (i > 0 && i - 1 + NS < n) issue(i - 1 + NS);
     }
-    __syncthreads();  // ring slot consumed, partials complete
-    if (tid == 0 && i + NS < n) issue(i + NS);
-    // owners: fixed-order sums, y = v - adt (K11 v + K12 w); v of the row is
-    // the gathered self column (dir-0 slot t = r)
-    if (tid < MT::NOUT) {
-      const int r = tid / M, a = tid - r * M;
-      const double* q = pp + tid * NPART;
-      double acc = 0.0;
-#pragma unroll
-      for (int g = 0; g < G11; ++g) acc += q[g];
-      if (a >= A0) {
-#pragma unroll
-        for (int g = 0; g < G12; ++g) acc += q[G11 + g];
-      }
-      const int rs = NT == C::NP ? r : r % C::NP;  // dir-0 position of the row
-      const double vr = gx[(rs * NT + r) * M + a];
-      y[(e * NPE + s * NT) * M + tid] = vr - adt * acc;
-    }
+    gather(i + 1);  // in flight while tile i computes
+    fetch_conn(i + 2);
+    cp_async_commit();
   }
+  __syncthreads();
+  if (n > 0 && tid >= OWN0 && tid < OWN0 + MT::NOUT) owners(n - 1);
 }
 
 // y = K12 w  (w: m*D per node); one thread per (row, stored row a')
