@@ -2848,9 +2848,11 @@ struct MvT {
   static constexpr int I11 = G11 * M * NT, I12 = G12 * R12 * NT;  // items per tile
   // gather units: one per (K11 slot, row) and per (K12 slot, row, M-component group)
   static constexpr int NG = C::NS11 * NT + C::NS12 * NT * (MD / M);
-  static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + 2 * GBUF + 2 * PART) + 64; }
-  static constexpr int NSTAGE = bytes(3) <= 224 * 1024 ? 3 : 2;
-  static constexpr int TOTAL = NSTAGE * BUF + 2 * GBUF + 2 * PART;
+  // gathers run two tiles ahead (three gather buffers)
+  static constexpr int NGB = 3;
+  static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + NGB * GBUF + 2 * PART) + 64; }
+  static constexpr int NSTAGE = bytes(3) <= 225 * 1024 ? 3 : 2;
+  static constexpr int TOTAL = NSTAGE * BUF + NGB * GBUF + 2 * PART;
   // thread roles: items, owners (one warp per 32 outputs), issuer, gathers
   static constexpr int ROLES = (I11 + I12 + 31) / 32 * 32 + (NOUT + 31) / 32 * 32 + 1 + NG;
   static constexpr bool OK = C::SECOND && MD % M == 0 && SG12 == 1 && ROLES <= THREADS && bytes(2) <= 220 * 1024;
@@ -2874,24 +2876,25 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
   __shared__ __align__(8) uint64_t bar[NS];
   double* const ring = smem;
   double* const gath = smem + NS * MT::BUF;
-  double* const part = gath + 2 * MT::GBUF;
+  double* const part = gath + MT::NGB * MT::GBUF;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int64_t ntiles = static_cast<int64_t>(kp.E) * TPE;
   const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * per;
   const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
   const int n = t1 > t0 ? static_cast<int>(t1 - t0) : 0;
-  // connectivity + element id of tile i, fetched two tiles ahead (cp.async)
-  __shared__ __align__(16) int2 sconn[3][2 * C::D];
-  __shared__ int sel[3];
+  // connectivity + element id of tile i, fetched four tiles ahead (cp.async)
+  constexpr int CR = 5;
+  __shared__ __align__(16) int2 sconn[CR][2 * C::D];
+  __shared__ int sel[CR];
   __shared__ int gel[4];  // element id of tile i (gel[i & 3]), for its owners one iteration later
   auto fetch_conn = [&](int i) {  // by threads 0 .. 2D
     if (i >= n) return;
     const int64_t T = t0 + i;
     const int k = static_cast<int>(T / TPE);
-    if (tid < 2 * C::D) cp_async8(&sconn[i % 3][tid], kp.conn + static_cast<size_t>(k) * 2 * C::D + tid);
+    if (tid < 2 * C::D) cp_async8(&sconn[i % CR][tid], kp.conn + static_cast<size_t>(k) * 2 * C::D + tid);
     if (tid == 2 * C::D)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&sel[i % 3])), "l"(kp.order + k)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&sel[i % CR])), "l"(kp.order + k)
                    : "memory");
   };
   if (tid == 0) {
@@ -2910,15 +2913,15 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
     tma_load_1d_once(b, V11 + (o11 & ~int64_t(1)), by11, &bar[i % NS]);
     tma_load_1d_once(b + MT::BUF11, V12 + (o12 & ~int64_t(1)), by12, &bar[i % NS]);
   };
-  // v / w of every (slot, row) column node of tile i -> gather buffer i & 1
-  // (its connectivity is in sconn[i % 3] already); highest thread ids
+  // v / w of every (slot, row) column node of tile i -> gather buffer i % NGB
+  // (its connectivity is in sconn[i % CR] already); highest thread ids
   auto gather = [&](int i) {
     if (i >= n) return;
     const int64_t T = t0 + i;
     const int k = static_cast<int>(T / TPE), s = static_cast<int>(T - static_cast<int64_t>(k) * TPE);
-    const int2* cn = sconn[i % 3];
-    const size_t e = static_cast<size_t>(sel[i % 3]);
-    double* gb = gath + (i & 1) * MT::GBUF;
+    const int2* cn = sconn[i % CR];
+    const size_t e = static_cast<size_t>(sel[i % CR]);
+    double* gb = gath + (i % MT::NGB) * MT::GBUF;
     if (tid == nthr - 1) gel[i & 3] = static_cast<int>(e);
     for (int u = nthr - 1 - tid; u < MT::NG; u += nthr) {
       const bool is11 = u < NS11 * NT;
@@ -2957,21 +2960,25 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
   };
   if (tid == ISSUER)
     for (int i = 0; i < NS && i < n; ++i) issue(i);
-  fetch_conn(0);
+  // prologue: connectivity of tiles 0 .. 3, gathers of tiles 0 and 1 (one
+  // cp.async group each; gather j's group fetches the connectivity of j + 4)
+  for (int j = 0; j < 4; ++j) fetch_conn(j);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  gather(0);
-  fetch_conn(1);
-  cp_async_commit();
+  for (int j = 0; j < 2; ++j) {
+    gather(j);
+    fetch_conn(j + 4);
+    cp_async_commit();
+  }
   for (int i = 0; i < n; ++i) {
     const int64_t T = t0 + i;
-    cp_async_wait_all();
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // gather(i)'s group is complete
     __syncthreads();  // gathers of tile i visible; items and owners of the previous iteration done
     if (tid < NITEM) {
       const double* b11 = ring + (i % NS) * MT::BUF + ((T * MT::ST11) & 1);
       const double* b12 = ring + (i % NS) * MT::BUF + MT::BUF11 + ((T * MT::ST12) & 1);
-      const double* gx = gath + (i & 1) * MT::GBUF;
+      const double* gx = gath + (i % MT::NGB) * MT::GBUF;
       const double* gw = gx + MT::GX;
       double* pp = part + (i & 1) * MT::PART;
       mbar_wait(&bar[i % NS], (i / NS) & 1);
@@ -3007,8 +3014,8 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
       // ring slot (i - 1) % NS was consumed before this iteration's barrier
       if (i > 0 && i - 1 + NS < n) issue(i - 1 + NS);
     }
-    gather(i + 1);  // in flight while tile i computes
-    fetch_conn(i + 2);
+    gather(i + 2);  // in flight while tiles i and i+1 compute
+    fetch_conn(i + 6);
     cp_async_commit();
   }
   __syncthreads();
