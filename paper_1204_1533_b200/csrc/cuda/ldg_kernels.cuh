@@ -2848,8 +2848,11 @@ struct MvT {
   static constexpr int I11 = G11 * M * NT, I12 = G12 * R12 * NT;  // items per tile
   // gather units: one per (K11 slot, row) and per (K12 slot, row, M-component group)
   static constexpr int NG = C::NS11 * NT + C::NS12 * NT * (MD / M);
-  // gathers run two tiles ahead (three gather buffers)
-  static constexpr int NGB = 3;
+  // gathers run GA tiles ahead (GA + 1 gather buffers): their first touch of
+  // an element is an HBM miss, longer than one tile's compute.  Measured (C5):
+  // one tile ahead 36.4 ms, two 30.8, three / four 30.8; ring of 2 or 3
+  // tiles alike.
+  static constexpr int GA = 2, NGB = GA + 1;
   static constexpr long long bytes(int ns) { return 8LL * (ns * BUF + NGB * GBUF + 2 * PART) + 64; }
   static constexpr int NSTAGE = bytes(3) <= 225 * 1024 ? 3 : 2;
   static constexpr int TOTAL = NSTAGE * BUF + NGB * GBUF + 2 * PART;
@@ -2883,11 +2886,11 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * per;
   const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
   const int n = t1 > t0 ? static_cast<int>(t1 - t0) : 0;
-  // connectivity + element id of tile i, fetched four tiles ahead (cp.async)
-  constexpr int CR = 5;
+  // connectivity + element id of tile i, fetched 2 GA tiles ahead (cp.async)
+  constexpr int GA = MT::GA, CR = 2 * GA + 1;
   __shared__ __align__(16) int2 sconn[CR][2 * C::D];
   __shared__ int sel[CR];
-  __shared__ int gel[4];  // element id of tile i (gel[i & 3]), for its owners one iteration later
+  __shared__ int gel[MT::GA + 2];  // element id of tile i, for its owners one iteration later
   auto fetch_conn = [&](int i) {  // by threads 0 .. 2D
     if (i >= n) return;
     const int64_t T = t0 + i;
@@ -2922,7 +2925,7 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
     const int2* cn = sconn[i % CR];
     const size_t e = static_cast<size_t>(sel[i % CR]);
     double* gb = gath + (i % MT::NGB) * MT::GBUF;
-    if (tid == nthr - 1) gel[i & 3] = static_cast<int>(e);
+    if (tid == nthr - 1) gel[i % (MT::GA + 2)] = static_cast<int>(e);
     for (int u = nthr - 1 - tid; u < MT::NG; u += nthr) {
       const bool is11 = u < NS11 * NT;
       const int u2 = is11 ? u : u - NS11 * NT;
@@ -2955,25 +2958,25 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
 #pragma unroll
       for (int g = 0; g < G12; ++g) acc += q[G11 + g];
     }
-    const size_t yo = (static_cast<size_t>(gel[i & 3]) * NPE + s * NT) * M + o;
+    const size_t yo = (static_cast<size_t>(gel[i % (MT::GA + 2)]) * NPE + s * NT) * M + o;
     y[yo] = __ldg(v + yo) - adt * acc;
   };
   if (tid == ISSUER)
     for (int i = 0; i < NS && i < n; ++i) issue(i);
-  // prologue: connectivity of tiles 0 .. 3, gathers of tiles 0 and 1 (one
-  // cp.async group each; gather j's group fetches the connectivity of j + 4)
-  for (int j = 0; j < 4; ++j) fetch_conn(j);
+  // prologue: connectivity of tiles 0 .. 2GA-1, gathers of tiles 0 .. GA-1
+  // (one cp.async group each; gather j's group fetches the connectivity of j + 2GA)
+  for (int j = 0; j < 2 * GA; ++j) fetch_conn(j);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < GA; ++j) {
     gather(j);
-    fetch_conn(j + 4);
+    fetch_conn(j + 2 * GA);
     cp_async_commit();
   }
   for (int i = 0; i < n; ++i) {
     const int64_t T = t0 + i;
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // gather(i)'s group is complete
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GA - 1) : "memory");  // gather(i)'s group is complete
     __syncthreads();  // gathers of tile i visible; items and owners of the previous iteration done
     if (tid < NITEM) {
       const double* b11 = ring + (i % NS) * MT::BUF + ((T * MT::ST11) & 1);
@@ -3014,8 +3017,8 @@ k_mv_tiles(const KParams<C> kp, const double* __restrict__ V11, const double* __
       // ring slot (i - 1) % NS was consumed before this iteration's barrier
       if (i > 0 && i - 1 + NS < n) issue(i - 1 + NS);
     }
-    gather(i + 2);  // in flight while tiles i and i+1 compute
-    fetch_conn(i + 6);
+    gather(i + GA);  // in flight while tiles i .. i+GA-1 compute
+    fetch_conn(i + 3 * GA);
     cp_async_commit();
   }
   __syncthreads();
