@@ -210,13 +210,21 @@ int ldg_split_matvec(ldg_ctx* ctx, double alpha_dt, const double* v, double* y);
    element and on a common coordinate line; the product's entries landing there
    are exact, all other fill and inter-element couplings dropped).  Requires an
    assembled Jacobian.  Element blocks of up to 128 unknowns (2-D p <= 4,
-   3-D p = 1); LDG_ERR_CONFIG beyond, LDG_ERR_SOLVER for a singular block.
+   3-D p = 1) are factorised whole.  Above that (3-D p >= 2) the preconditioner
+   keeps the line-based sparsity the paper calls for in 3-D (PAPER.md:741-746,
+   "ADI iterations"): I - alpha_dt A~ ~ prod_d (I - alpha_dt A~_d), A~_d the
+   couplings of A~ along direction-d lines (node-diagonal blocks split evenly
+   over the D directions), one dense (p+1)m LU per line: D (p+1)^(D-1) blocks
+   of ((p+1)m)^2 per element (C4: 40 GB).  LDG_ERR_CONFIG when the factors do
+   not fit the free device memory, LDG_ERR_SOLVER for a singular block.
    Replaces build_preconditioner(blocks, alpha_dt). */
 int ldg_precond_build(ldg_ctx* ctx, double alpha_dt);
-/* Block-Jacobi mode: 0 (default) LU factors + triangular solves per apply;
-   1 the build also forms the explicit block inverses (build ~4x slower, apply
-   ~2x faster: a dense block matvec at HBM rate) -- pays off when one build
-   serves many applications.  Invalidates a built preconditioner. */
+/* Preconditioner mode: 0 (default) element-block LU (triangular solves per
+   apply) where the element has <= 128 unknowns, line-ADI above; 1 element-
+   block LU that also forms the explicit block inverses (build ~4x slower,
+   apply ~2x faster: a dense block matvec at HBM rate) -- pays off when one
+   build serves many applications; 2 line-ADI for any configuration.
+   Invalidates a built preconditioner. */
 int ldg_set_precond_mode(ldg_ctx* ctx, int mode);
 /* z = (I - alpha_dt A~)^-1 r, device vectors (reference numbering). */
 int ldg_precond_apply(ldg_ctx* ctx, const double* r, double* z);

@@ -82,6 +82,9 @@ struct ldg_ctx {
   int* d_pcbad = nullptr;
   bool pc_valid = false;
   double pc_adt = 0.0;
+  int pc_mode = 0;       // ldg_set_precond_mode
+  bool pc_adi = false;   // the built preconditioner is line-ADI
+  size_t pc_nlu = 0, pc_npiv = 0;  // allocated factor / pivot entries
   double* d_ti = nullptr;  // time-integration workspace (8 vectors)
   double* d_kv = nullptr;  // Krylov vectors V[0..restart] then Z[0..restart-1]
   int kv_restart = 0;
@@ -1402,25 +1405,69 @@ int ldg_split_matvec(ldg_ctx* c, double adt, const double* v, double* y) {
 
 // ----------------------------------------- block-Jacobi preconditioner + GMRES
 //
+namespace {
+// preconditioner application of the built kind (element-block LU / inverse or line-ADI)
+cudaError_t pc_apply_any(ldg_ctx* c, const double* r, double* z) {
+  const ldg::Ops& o = *c->ops;
+  return c->pc_adi ? o.pc_line_apply(c->dc, c->d_pcLU, c->d_pcPiv, r, z)
+                   : o.pc_apply(c->dc, c->d_pcLU, c->d_pcPiv, r, z);
+}
+}  // namespace
+
 int ldg_precond_build(ldg_ctx* c, double alpha_dt) {
   return guarded(c, [&]() -> int {
     if (!c->jac_valid) throw ldg_error(LDG_ERR_SOLVER, "Jacobian not assembled");
     const ldg::Ops& o = *c->ops;
-    if (o.pc_ne <= 0)
-      throw ldg_error(LDG_ERR_CONFIG, "block-Jacobi preconditioner: element blocks above 128 unknowns "
-                                      "(3-D p >= 2) are not supported");
-    const size_t ne = static_cast<size_t>(o.pc_ne);
-    if (!c->d_pcLU) ck(cudaMalloc(&c->d_pcLU, static_cast<size_t>(c->E) * ne * ne * sizeof(double)), "cudaMalloc LU");
-    if (!c->d_pcPiv) ck(cudaMalloc(&c->d_pcPiv, static_cast<size_t>(c->E) * ne * sizeof(int32_t)), "cudaMalloc piv");
+    // mode 0: element-block LU up to 128 unknowns per element, line-ADI above
+    // (3-D p >= 2); 1: explicit element-block inverses; 2: line-ADI
+    const bool adi = c->pc_mode == 2 || (c->pc_mode == 0 && o.pc_ne <= 0);
+    if (!adi && o.pc_ne <= 0)
+      throw ldg_error(LDG_ERR_CONFIG, "element-block preconditioner: element blocks above 128 unknowns "
+                                      "(3-D p >= 2) use the line-ADI mode");
+    if (adi && o.pc_line_nb <= 0)
+      throw ldg_error(LDG_ERR_CONFIG, "line-ADI preconditioner not available for this configuration");
+    size_t nlu, npiv;
+    if (adi) {
+      const size_t nb = static_cast<size_t>(o.pc_line_nb), blocks = static_cast<size_t>(c->E) * c->D * c->NL;
+      nlu = blocks * nb * nb;
+      npiv = blocks * nb;
+    } else {
+      const size_t ne = static_cast<size_t>(o.pc_ne);
+      nlu = static_cast<size_t>(c->E) * ne * ne;
+      npiv = static_cast<size_t>(c->E) * ne;
+    }
+    if (nlu != c->pc_nlu || npiv != c->pc_npiv) {
+      cudaFree(c->d_pcLU);
+      cudaFree(c->d_pcPiv);
+      c->d_pcLU = nullptr;
+      c->d_pcPiv = nullptr;
+      c->pc_nlu = c->pc_npiv = 0;
+      size_t fr = 0, tot = 0;
+      ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+      const size_t need = nlu * sizeof(double) + npiv * sizeof(int32_t);
+      if (need + (64u << 20) > fr)
+        throw ldg_error(LDG_ERR_CONFIG, std::string(adi ? "line-ADI" : "element-block") + " preconditioner needs " +
+                                            std::to_string(need >> 20) + " MiB of factors, " +
+                                            std::to_string(fr >> 20) + " MiB of device memory free");
+      ck(cudaMalloc(&c->d_pcLU, nlu * sizeof(double)), "cudaMalloc LU");
+      ck(cudaMalloc(&c->d_pcPiv, npiv * sizeof(int32_t)), "cudaMalloc piv");
+      c->pc_nlu = nlu;
+      c->pc_npiv = npiv;
+    }
     if (!c->d_pcbad) ck(cudaMalloc(&c->d_pcbad, sizeof(int)), "cudaMalloc flag");
     ck(cudaMemsetAsync(c->d_pcbad, 0xff, sizeof(int), c->stream), "reset flag");
     c->pc_valid = false;
-    ck(o.pc_build(c->dc, c->d_K11, c->d_K12, c->d_K21, alpha_dt, c->d_pcLU, c->d_pcPiv, c->d_pcbad), "pc build");
+    if (adi)
+      ck(o.pc_line_build(c->dc, c->d_K11, c->d_K12, c->d_K21, alpha_dt, c->d_pcLU, c->d_pcPiv, c->d_pcbad),
+         "pc build");
+    else
+      ck(o.pc_build(c->dc, c->d_K11, c->d_K12, c->d_K21, alpha_dt, c->d_pcLU, c->d_pcPiv, c->d_pcbad), "pc build");
     int bad = -1;
     ck(cudaMemcpyAsync(&bad, c->d_pcbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "read flag");
     ck(cudaStreamSynchronize(c->stream), "stream synchronize");
     if (bad >= 0)
       throw ldg_error(LDG_ERR_SOLVER, "singular block-Jacobi block at element " + std::to_string(bad));
+    c->pc_adi = adi;
     c->pc_valid = true;
     c->pc_adt = alpha_dt;
     return LDG_OK;
@@ -1429,8 +1476,10 @@ int ldg_precond_build(ldg_ctx* c, double alpha_dt) {
 
 int ldg_set_precond_mode(ldg_ctx* c, int mode) {
   return guarded(c, [&]() -> int {
-    if (mode != 0 && mode != 1) throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "precond mode must be 0 (LU) or 1 (inverse)");
-    c->dc.pc_inverse = mode;
+    if (mode < 0 || mode > 2)
+      throw ldg_error(LDG_ERR_INVALID_ARGUMENT, "precond mode must be 0 (auto), 1 (element inverse) or 2 (line-ADI)");
+    c->pc_mode = mode;
+    c->dc.pc_inverse = mode == 1;
     c->pc_valid = false;
     return LDG_OK;
   });
@@ -1441,8 +1490,7 @@ int ldg_precond_apply(ldg_ctx* c, const double* r, double* z) {
     check_aligned(r, "r");
     check_aligned(z, "z");
     if (!c->pc_valid) throw ldg_error(LDG_ERR_SOLVER, "preconditioner not built");
-    const ldg::Ops& o = *c->ops;
-    return finish(c, o.pc_apply(c->dc, c->d_pcLU, c->d_pcPiv, r, z));
+    return finish(c, pc_apply_any(c, r, z));
   });
 }
 
@@ -1521,7 +1569,7 @@ int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rt
       for (; j < mr && it < maxit; ++j) {
         double* Vj = V + static_cast<size_t>(j) * n;
         double* Zj = use_precond ? Zs + static_cast<size_t>(j) * n : Vj;
-        if (use_precond) ck(o.pc_apply(c->dc, c->d_pcLU, c->d_pcPiv, Vj, Zj), "pc apply");
+        if (use_precond) ck(pc_apply_any(c, Vj, Zj), "pc apply");
         op(Zj, w);
         for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
           double* hij = Hd + static_cast<size_t>(j) * (mr + 1) + i;

@@ -3423,4 +3423,202 @@ k_pc_apply_lu2(const KParams<C> kp, const double* __restrict__ LUc, const int32_
   }
 }
 
+// ------------------------------------------------ line-ADI preconditioner
+// Element blocks above 128 unknowns (3-D p >= 2) keep the line-based sparsity
+// the paper calls for in 3-D: I - adt A~ is approximated by
+// prod_d (I - adt A~_d), A~_d = the couplings of A~ along direction-d lines
+// with the node-diagonal blocks split evenly over the D directions (oracle
+// lo_precond_build, same definition).  Each factor is block diagonal over the
+// d-lines: one dense NB = (p+1) m block per line, LU with partial pivoting,
+// stored column-major [k][d][line][NB x NB] (+ pivots) in processing order.
+template <class C>
+struct PcLine {
+  static constexpr int NB = C::NP * C::M;
+  static constexpr int NBB = NB * NB;
+  static constexpr int LDB = NB | 1;  // odd row stride in shared memory
+  static constexpr int THREADS = 256;
+  static constexpr size_t smem() { return sizeof(double) * C::NL * NB * LDB; }
+  static constexpr bool OK = NB <= 32 && smem() <= 200 * 1024;
+};
+
+// One CTA per (element k, direction d): the d-line blocks of A~ in shared
+// memory (K11 line slots; K12 K21 on the pattern by owner threads, fixed
+// order), then I - adt A~_d and one warp per line factorises its block.
+template <class C>
+__global__ void __launch_bounds__(PcLine<C>::THREADS)
+k_pc_line_build(const KParams<C> kp, const double* __restrict__ K11, const double* __restrict__ K12,
+                const double* __restrict__ K21, double adt, double* __restrict__ LUc, int32_t* __restrict__ piv,
+                int* __restrict__ bad) {
+  using PL = PcLine<C>;
+  constexpr int NB = PL::NB, LDB = PL::LDB, M = C::M, NP = C::NP, NPE = C::NPE, NT = C::NT, NL = C::NL, D = C::D,
+                MD = C::MD, NS11 = C::NS11, NS12 = C::NS12, R12 = C::R12, NSIN = C::D * C::P + 1;
+  constexpr int A0 = C::PH == PH_NS ? 1 : 0;
+  extern __shared__ __align__(16) double B[];  // [line][NB][LDB]
+  const int k = blockIdx.x, d = blockIdx.y, tid = threadIdx.x, nthr = blockDim.x;
+  const size_t e = kp.order[k];
+  for (int x = tid; x < NL * NB * LDB; x += nthr) B[x] = 0.0;
+  __syncthreads();
+  // K11: for every row node its d-line slots (self block shared by the D directions)
+  for (int w = tid; w < NPE * NP * M * M; w += nthr) {
+    const int b = w % M, a = (w / M) % M, t2 = (w / (M * M)) % NP, nd = w / (M * M * NP);
+    int line, pos;
+    line_of<C>(d, nd, line, pos);
+    const int slot = t2 == pos ? nd % NP : inel_slot<C>(d, pos, t2);
+    const size_t T = static_cast<size_t>(k) * C::TPE + nd / NT;
+    double v = K11[(((T * NS11 + slot) * M + a) * NT + nd % NT) * M + b];
+    if (t2 == pos) v = v / D;
+    B[(line * NB + pos * M + a) * LDB + t2 * M + b] = v;
+  }
+  __syncthreads();
+  if (C::SECOND) {
+    // K12 K21 on the pattern (d-line pairs), one owner per (row, a', b)
+    for (int w = tid; w < NPE * R12 * M; w += nthr) {
+      const int b = w % M, ap = (w / M) % R12, nd = w / (M * R12);
+      int line, pos;
+      line_of<C>(d, nd, line, pos);
+      const size_t T12 = static_cast<size_t>(k) * C::TPE + nd / NT;
+      for (int s12 = 0; s12 < NS12; ++s12) {
+        const int64_t mid = slot_col<C, NSIN>(kp, k, e, nd, s12, 1);
+        if (mid < 0) continue;
+        const int em = static_cast<int>(mid / NPE), ndm = static_cast<int>(mid - static_cast<int64_t>(em) * NPE);
+        const int km = __ldg(kp.inv_order + em);
+        const size_t T21 = static_cast<size_t>(km) * C::TPE + ndm / NT;
+        double k12[D];
+#pragma unroll
+        for (int dd = 0; dd < D; ++dd)
+          k12[dd] = __ldg(K12 + (((T12 * NS12 + s12) * R12 + ap) * NT + nd % NT) * MD + b * D + dd);
+        auto add = [&](int cl, double sum) {
+          int l2, p2;
+          line_of<C>(d, cl, l2, p2);
+          if (l2 != line) return;  // not on this row's d-line
+          B[(line * NB + pos * M + ap + A0) * LDB + p2 * M + b] += cl == nd ? sum / D : sum;
+        };
+        for (int s21 = 0; s21 < NS12; ++s21) {
+          const int64_t col = slot_col<C, NSIN>(kp, km, static_cast<size_t>(em), ndm, s21, 2);
+          if (col < 0 || col / NPE != static_cast<int64_t>(e)) continue;
+          double sum = 0.0;
+#pragma unroll
+          for (int dd = 0; dd < D; ++dd) sum += k12[dd] * __ldg(K21 + ((T21 * NS12 + s21) * NT + ndm % NT) * D + dd);
+          add(static_cast<int>(col - static_cast<int64_t>(e) * NPE), sum);
+        }
+        if (C::HAS_INV && kp.noslip && em == static_cast<int>(e) && (b == 0 || b == M - 1))
+          k21_wall_terms<C>(kp, km, ndm, [&](int end, const double* cf) {  // density and energy columns
+            double sum = 0.0;
+#pragma unroll
+            for (int dd = 0; dd < D; ++dd) sum += k12[dd] * cf[dd];
+            add(end, sum);
+          });
+      }
+    }
+    __syncthreads();
+  }
+  for (int x = tid; x < NL * NB * NB; x += nthr) {
+    const int j = x % NB, i = (x / NB) % NB, l = x / (NB * NB);
+    double* p = &B[(l * NB + i) * LDB + j];
+    *p = (i == j ? 1.0 : 0.0) - adt * *p;
+  }
+  __syncthreads();
+  // one warp per line block: LU with partial pivoting (first maximum, as the oracle)
+  const int wid = tid >> 5, lane = tid & 31;
+  for (int l = wid; l < NL; l += nthr / 32) {
+    double* A = B + l * NB * LDB;
+    int32_t* pv = piv + ((static_cast<size_t>(k) * D + d) * NL + l) * NB;
+    for (int kk = 0; kk < NB; ++kk) {
+      double best = -1.0;
+      int bi = kk;
+      for (int i = kk + lane; i < NB; i += 32) {
+        const double v = fabs(A[i * LDB + kk]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, off);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      bi = __shfl_sync(0xffffffffu, bi, 0);
+      best = __shfl_sync(0xffffffffu, best, 0);
+      if (lane == 0) pv[kk] = bi;
+      if (!(best > 0.0)) {
+        if (lane == 0) atomicCAS(bad, -1, static_cast<int>(e));
+        break;
+      }
+      if (bi != kk)
+        for (int j = lane; j < NB; j += 32) {
+          const double t = A[kk * LDB + j];
+          A[kk * LDB + j] = A[bi * LDB + j];
+          A[bi * LDB + j] = t;
+        }
+      __syncwarp();
+      const double ip = 1.0 / A[kk * LDB + kk];
+      for (int i = kk + 1 + lane; i < NB; i += 32) A[i * LDB + kk] *= ip;
+      __syncwarp();
+      for (int x = lane; x < (NB - kk - 1) * (NB - kk - 1); x += 32) {
+        const int i = kk + 1 + x / (NB - kk - 1), j = kk + 1 + x % (NB - kk - 1);
+        A[i * LDB + j] -= A[i * LDB + kk] * A[kk * LDB + j];
+      }
+      __syncwarp();
+    }
+    // column-major store: lane i of a solve step reads column j contiguously
+    double* out = LUc + ((static_cast<size_t>(k) * D + d) * NL + l) * PL::NBB;
+    for (int x = lane; x < NB * NB; x += 32) {
+      const int j = x / NB, i = x - j * NB;
+      out[x] = A[i * LDB + j];
+    }
+  }
+}
+
+// z = (I - adt A~_{D-1})^-1 ... (I - adt A~_0)^-1 r: one CTA per element, the
+// element's vector in shared memory, one warp per line solve (lane i holds
+// entry i of the line vector; NB <= 32), directions in sequence.
+template <class C>
+__global__ void __launch_bounds__(256)
+k_pc_line_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* __restrict__ piv,
+                const double* __restrict__ r, double* __restrict__ z) {
+  using PL = PcLine<C>;
+  constexpr int NB = PL::NB, M = C::M, NPE = C::NPE, NL = C::NL, D = C::D, NE = NPE * M;
+  __shared__ double zs[PL::OK ? NE : 1];
+  const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const size_t e = __ldg(kp.order + k);
+  for (int i = tid; i < NE; i += blockDim.x) zs[i] = r[e * NE + i];
+  __syncthreads();
+  for (int d = 0; d < D; ++d) {
+    for (int l = wid; l < NL; l += nw) {
+      const size_t blk = (static_cast<size_t>(k) * D + d) * NL + l;
+      const double* L = LUc + blk * PL::NBB;
+      const int32_t* pv = piv + blk * NB;
+      const int t = lane / M, a = lane - t * M;
+      const int nd = lane < NB ? node_on_line<C>(d, l, t) : 0;
+      double x = lane < NB ? zs[nd * M + a] : 0.0;
+      // row interchanges in order
+      for (int i = 0; i < NB; ++i) {
+        const int p = __ldg(pv + i);
+        const double xi = __shfl_sync(0xffffffffu, x, i), xp = __shfl_sync(0xffffffffu, x, p);
+        if (lane == i) x = xp;
+        else if (lane == p) x = xi;
+      }
+      // forward (unit L), column-oriented
+      for (int j = 0; j < NB - 1; ++j) {
+        const double xj = __shfl_sync(0xffffffffu, x, j);
+        if (lane > j && lane < NB) x -= __ldg(L + j * NB + lane) * xj;
+      }
+      // backward (U)
+      for (int j = NB - 1; j >= 0; --j) {
+        if (lane == j) x = x / __ldg(L + j * NB + j);
+        const double xj = __shfl_sync(0xffffffffu, x, j);
+        if (lane < j) x -= __ldg(L + j * NB + lane) * xj;
+      }
+      if (lane < NB) zs[nd * M + a] = x;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < NE; i += blockDim.x) z[e * NE + i] = zs[i];
+}
+
 }  // namespace ldg

@@ -68,6 +68,10 @@ struct Ops {
   cudaError_t (*pc_build)(const DevCtx&, const double* V11, const double* V12, const double* V21, double adt,
                           double* LUc, int32_t* piv, int* bad);
   cudaError_t (*pc_apply)(const DevCtx&, const double* LUc, const int32_t* piv, const double* r, double* z);
+  int pc_line_nb;  // line-ADI block size (p+1) m (0: not supported)
+  cudaError_t (*pc_line_build)(const DevCtx&, const double* V11, const double* V12, const double* V21, double adt,
+                               double* LUc, int32_t* piv, int* bad);
+  cudaError_t (*pc_line_apply)(const DevCtx&, const double* LUc, const int32_t* piv, const double* r, double* z);
 };
 
 // Persistent-grid size of a kernel on the CURRENT device (the context's
@@ -321,11 +325,29 @@ struct Launch {
     count(d);
     return cudaGetLastError();
   }
+  static cudaError_t pc_line_build(const DevCtx& d, const double* V11, const double* V12, const double* V21,
+                                   double adt, double* LUc, int32_t* piv, int* bad) {
+    using PL = PcLine<C>;
+    if (!PL::OK) return cudaErrorNotSupported;
+    persistent_grid(reinterpret_cast<const void*>(k_pc_line_build<C>), PL::THREADS, PL::smem());
+    k_pc_line_build<C><<<dim3(d.E, C::D), PL::THREADS, PL::smem(), d.stream>>>(params(d), V11, V12, V21, adt, LUc,
+                                                                              piv, bad);
+    count(d);
+    return cudaGetLastError();
+  }
+  static cudaError_t pc_line_apply(const DevCtx& d, const double* LUc, const int32_t* piv, const double* r,
+                                   double* z) {
+    if (!PcLine<C>::OK) return cudaErrorNotSupported;
+    k_pc_line_apply<C><<<d.E, 256, 0, d.stream>>>(params(d), LUc, piv, r, z);
+    count(d);
+    return cudaGetLastError();
+  }
   static const Ops* table() {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
                             C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, chunk_elems, residual, gradient, jacobian, k21,
-                            spmv11, spmv11_zc, spmv12, spmv21, split, PcCfg<C>::OK ? PcCfg<C>::NE : 0, pc_build, pc_apply};
+                            spmv11, spmv11_zc, spmv12, spmv21, split, PcCfg<C>::OK ? PcCfg<C>::NE : 0, pc_build, pc_apply,
+                            PcLine<C>::OK ? PcLine<C>::NB : 0, pc_line_build, pc_line_apply};
     return &ops;
   }
 };
