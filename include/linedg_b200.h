@@ -345,6 +345,9 @@ int ldg_synchronize(ldg_ctx* ctx);
  * product kernel writes y over PCIe while it runs (LDG_OPT_ZERO_COPY).        */
 int ldg_residual_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);
 int ldg_jacobian_assemble_host(ldg_ctx* ctx, const double* U, double t);
+/* gradient_residual / residual_second_order on host buffers (synchronous). */
+int ldg_gradient_host(ldg_ctx* ctx, const double* U, double t, double* Q);
+int ldg_residual_uq_host(ldg_ctx* ctx, const double* U, const double* Q, double t, double* R);
 /* R(U) and the Jacobian at U from one upload of U (a Newton step): second-
  * order physics computes Q = D(U) once for both (Q_or_null receives it). */
 int ldg_residual_assemble_host(ldg_ctx* ctx, const double* U, double t, double* R, double* Q_or_null);

@@ -63,7 +63,6 @@ class Context {
   Context(const NodalBasis1D& b, const QuadMesh& mesh, const std::vector<ElementMapping>& maps,
           const SwitchAssignment* sw, const ldg_physics& physics, void* cuda_stream = nullptr) {
     const int np = b.p + 1, nq = b.n_quad(), E = mesh.num_elems(), npe = np * np;
-    m_ = physics.kind == LDG_POISSON ? 1 : 4;
     npe_ = npe;
     E_ = E;
     nodes_.assign(b.nodes.data(), b.nodes.data() + np);
@@ -129,6 +128,7 @@ class Context {
     s.normal_end = nend_.data();
     s.node_coords = xy_.data();
     check(ldg_create(&s, &physics, cuda_stream, &ctx_), nullptr);
+    m_ = ldg_components(ctx_);
   }
   ~Context() { ldg_destroy(ctx_); }
   Context(const Context&) = delete;
@@ -143,6 +143,21 @@ class Context {
     return R;
   }
   GridFunction residual_primal(const GridFunction& U, double t) { return residual_first_order(U, t); }
+
+  // gradient_residual: Q = (1/J) sum_dir d, an AuxGradient with
+  // component index c*2 + d (field.hpp:38-40).  Second-order physics.
+  AuxGradient gradient_residual(const GridFunction& U, double t) {
+    AuxGradient Q(U.n_elems, U.nodes_per_elem, U.comps * 2);
+    check(ldg_gradient_host(ctx_, U.data.data(), t, Q.data.data()), ctx_);
+    return Q;
+  }
+  // residual_second_order: R(U, Q) for a given Q.
+  GridFunction residual_second_order(const GridFunction& U, const AuxGradient& Q, double t) {
+    GridFunction R(U.n_elems, U.nodes_per_elem, U.comps);
+    check(ldg_residual_uq_host(ctx_, U.data.data(), Q.data.data(), t, R.data.data()), ctx_);
+    return R;
+  }
+  int components() const { return m_; }
 
   // assemble_jacobians(ctx, U, t, Analytic); the blocks stay on
   // the device for split_matvec / SpMV.

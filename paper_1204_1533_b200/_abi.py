@@ -212,7 +212,7 @@ GPU_SYMBOLS = [
     "ldg_precond_build", "ldg_precond_apply", "ldg_precond_apply_host", "ldg_gmres", "ldg_gmres_host",
     "ldg_rk4_step", "ldg_dirk3_step", "ldg_write_triplets", "ldg_write_sparsity_csv", "ldg_steady_solve",
     "ldg_set_boundary_function", "ldg_set_precond_mode", "ldg_set_option", "ldg_jacobian_assemble_q",
-    "ldg_residual_assemble_host",
+    "ldg_residual_assemble_host", "ldg_gradient_host", "ldg_residual_uq_host",
 ]
 
 

@@ -90,6 +90,8 @@ struct ldg_ctx {
   int kv_restart = 0;
   double* d_kw = nullptr;  // w, t, r
   double* d_kred = nullptr;  // reduction partials + Hessenberg (column-major) + scalars
+  double* h_gst = nullptr;            // pinned ring of GMRES cycle states
+  cudaEvent_t ev_gw[4] = {nullptr, nullptr, nullptr, nullptr};
   int32_t* d_order = nullptr;
   double* d_metric = nullptr;
   int2* d_conn = nullptr;
@@ -185,6 +187,9 @@ struct ldg_ctx {
       if (ev_mv_out[k]) cudaEventDestroy(ev_mv_out[k]);
     }
     if (h_err) cudaFreeHost(h_err);
+    if (h_gst) cudaFreeHost(h_gst);
+    for (cudaEvent_t ev : ev_gw)
+      if (ev) cudaEventDestroy(ev);
   }
 
   int node_on_line(int dir, int line, int t) const {
@@ -697,6 +702,40 @@ __global__ void k_div(double* __restrict__ y, const double* __restrict__ x, size
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     y[i] = x[i] / d;
+}
+// GMRES: Givens update of Hessenberg column j on the device (one thread), so
+// the host never waits for it.  st[0] = done (converged / lucky breakdown /
+// non-finite), st[1] = iterations of the cycle, st[2] = non-finite flag; once
+// done, the cycle's remaining (launched-ahead) iterations are ignored.
+__global__ void k_gmres_givens(double* __restrict__ H, int mr, int j, double* __restrict__ cs,
+                               double* __restrict__ sn, double* __restrict__ g, double tol, double* __restrict__ st) {
+  if (st[0] != 0.0) return;
+  double* col = H + static_cast<size_t>(j) * (mr + 1);
+  const double hn = col[j + 1];
+  if (!isfinite(hn)) {
+    st[2] = 1.0;
+    st[0] = 1.0;
+    return;
+  }
+  for (int i = 0; i < j; ++i) {
+    const double a0 = col[i], a1 = col[i + 1];
+    col[i] = cs[i] * a0 + sn[i] * a1;
+    col[i + 1] = -sn[i] * a0 + cs[i] * a1;
+  }
+  const double a0 = col[j], a1 = col[j + 1];
+  const double den = hypot(a0, a1);
+  cs[j] = den > 0.0 ? a0 / den : 1.0;
+  sn[j] = den > 0.0 ? a1 / den : 0.0;
+  col[j] = den;
+  col[j + 1] = 0.0;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+  st[1] = j + 1;
+  if (fabs(g[j + 1]) <= tol || hn == 0.0) st[0] = 1.0;
+}
+__global__ void k_gmres_cycle_init(double* __restrict__ g, int mr, double beta, double* __restrict__ st) {
+  for (int i = threadIdx.x; i <= mr; i += blockDim.x) g[i] = i == 0 ? beta : 0.0;
+  if (threadIdx.x == 0) st[0] = st[1] = st[2] = 0.0;
 }
 // max |a_i|: block partials, then one block (deterministic)
 __global__ void __launch_bounds__(KR_THREADS) k_amax_part(const double* __restrict__ a, size_t n,
@@ -1515,7 +1554,7 @@ int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rt
       c->kv_restart = mr;
     }
     ensure(c->d_kw, 3 * n);
-    ensure(c->d_kred, KR_BLOCKS + (static_cast<size_t>(mr) + 1) * mr + 8);
+    ensure(c->d_kred, KR_BLOCKS + (static_cast<size_t>(mr) + 1) * mr + 8 + 3 * static_cast<size_t>(mr) + 4);
     double* V = c->d_kv;                 // (mr+1) x n
     double* Zs = c->d_kv + (mr + 1) * n;  // mr x n
     double* w = c->d_kw;
@@ -1557,16 +1596,27 @@ int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rt
       return LDG_OK;
     }
     ck(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy b");
-    std::vector<double> H(static_cast<size_t>(mr + 1) * mr), cs(mr), sn(mr), g(mr + 1), col(mr + 1);
+    // Hessenberg / Givens state on the device; the host keeps up to GW
+    // iterations in flight and learns a cycle's end from a pinned copy of the
+    // state, polled GW iterations behind (no per-iteration stall)
+    constexpr int GW = 4;
+    double* gcs = sc + 8;       // cs[mr], sn[mr], g[mr+1], state[3]
+    double* gsn = gcs + mr;
+    double* gg = gsn + mr;
+    double* gst = gg + mr + 1;
+    if (!c->h_gst) ck(cudaHostAlloc(reinterpret_cast<void**>(&c->h_gst), GW * 4 * sizeof(double), 0), "pinned");
+    if (!c->ev_gw[0])
+      for (int q = 0; q < GW; ++q) ck(cudaEventCreateWithFlags(&c->ev_gw[q], cudaEventDisableTiming), "event");
+    std::vector<double> H(static_cast<size_t>(mr + 1) * mr), g(mr + 1);
     double beta = bn;
     int it = 0;
     while (true) {
       k_div<<<vb, vt, 0, st>>>(V, r, n, nullptr, beta);
-      ++c->launches;
-      std::fill(g.begin(), g.end(), 0.0);
-      g[0] = beta;
-      int j = 0;
-      for (; j < mr && it < maxit; ++j) {
+      k_gmres_cycle_init<<<1, 64, 0, st>>>(gg, mr, beta, gst);
+      c->launches += 2;
+      int j = 0, launched = 0;
+      bool done = false;
+      for (; j < mr && it + j < maxit && !done; ++j) {
         double* Vj = V + static_cast<size_t>(j) * n;
         double* Zj = use_precond ? Zs + static_cast<size_t>(j) * n : Vj;
         if (use_precond) ck(pc_apply_any(c, Vj, Zj), "pc apply");
@@ -1580,32 +1630,30 @@ int ldg_gmres(ldg_ctx* c, double alpha_dt, const double* b, double* x, double rt
         double* hn_d = Hd + static_cast<size_t>(j) * (mr + 1) + j + 1;
         dot(w, w, hn_d, 1);
         k_div<<<vb, vt, 0, st>>>(V + static_cast<size_t>(j + 1) * n, w, n, hn_d, 0.0);
-        ++c->launches;
-        ck(cudaMemcpyAsync(col.data(), Hd + static_cast<size_t>(j) * (mr + 1), (j + 2) * sizeof(double),
-                           cudaMemcpyDeviceToHost, st), "D2H Hessenberg column");
-        ck(cudaStreamSynchronize(st), "stream synchronize");
-        const double hn = col[j + 1];
-        if (!std::isfinite(hn)) throw ldg_error(LDG_ERR_SOLVER, "gmres: numerical breakdown (non-finite Krylov vector)");
-        for (int i = 0; i <= j + 1; ++i) H[i * mr + j] = col[i];
-        for (int i = 0; i < j; ++i) {
-          const double a0 = H[i * mr + j], a1 = H[(i + 1) * mr + j];
-          H[i * mr + j] = cs[i] * a0 + sn[i] * a1;
-          H[(i + 1) * mr + j] = -sn[i] * a0 + cs[i] * a1;
-        }
-        const double a0 = H[j * mr + j], a1 = H[(j + 1) * mr + j];
-        const double den = std::hypot(a0, a1);
-        cs[j] = den > 0.0 ? a0 / den : 1.0;
-        sn[j] = den > 0.0 ? a1 / den : 0.0;
-        H[j * mr + j] = den;
-        H[(j + 1) * mr + j] = 0.0;
-        g[j + 1] = -sn[j] * g[j];
-        g[j] = cs[j] * g[j];
-        ++it;
-        if (std::fabs(g[j + 1]) <= rtol * bn || hn == 0.0) {
-          ++j;
-          break;
+        k_gmres_givens<<<1, 1, 0, st>>>(Hd, mr, j, gcs, gsn, gg, rtol * bn, gst);
+        c->launches += 2;
+        ck(cudaMemcpyAsync(c->h_gst + (j % GW) * 4, gst, 3 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H st");
+        ck(cudaEventRecord(c->ev_gw[j % GW], st), "record");
+        ++launched;
+        if (j >= GW - 1) {  // poll the state of iteration j - GW + 1
+          ck(cudaEventSynchronize(c->ev_gw[(j - GW + 1) % GW]), "event synchronize");
+          done = c->h_gst[((j - GW + 1) % GW) * 4] != 0.0;
         }
       }
+      (void)launched;
+      ck(cudaStreamSynchronize(st), "stream synchronize");
+      double stt[3];
+      ck(cudaMemcpy(stt, gst, 3 * sizeof(double), cudaMemcpyDeviceToHost), "D2H state");
+      if (stt[2] != 0.0) throw ldg_error(LDG_ERR_SOLVER, "gmres: numerical breakdown (non-finite Krylov vector)");
+      j = static_cast<int>(stt[1]);
+      it += j;
+      ck(cudaMemcpy(g.data(), gg, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost), "D2H g");
+      std::vector<double> Rc(static_cast<size_t>(mr + 1) * (j > 0 ? j : 1));
+      if (j > 0)
+        ck(cudaMemcpy(Rc.data(), Hd, static_cast<size_t>(mr + 1) * j * sizeof(double), cudaMemcpyDeviceToHost),
+           "D2H R");
+      for (int q = 0; q < j; ++q)
+        for (int i = 0; i <= q; ++i) H[i * mr + q] = Rc[static_cast<size_t>(q) * (mr + 1) + i];
       std::vector<double> y(j, 0.0);
       for (int i = j - 1; i >= 0; --i) {
         double s_ = g[i];
@@ -2035,6 +2083,38 @@ int ldg_residual_assemble_host(ldg_ctx* c, const double* U, double t, double* R,
     }
     c->sync_errors = true;
     return st == LDG_OK ? finish(c, cudaSuccess) : st;
+  });
+}
+
+// gradient_residual / residual_second_order with host buffers (synchronous)
+int ldg_gradient_host(ldg_ctx* c, const double* U, double t, double* Q) {
+  return guarded(c, [&]() -> int {
+    if (!c->second) throw ldg_error(LDG_ERR_CONFIG, "gradient_residual needs second-order physics");
+    double* du = ensure(c->d_hu, c->nU());
+    double* dq = ensure(c->d_Q, c->nQ());
+    ck(cudaMemcpyAsync(du, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
+    c->sync_errors = false;
+    int st = ldg_gradient(c, du, t, dq);
+    c->sync_errors = true;
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(Q, dq, c->nQ() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H Q");
+    return finish(c, cudaSuccess);
+  });
+}
+
+int ldg_residual_uq_host(ldg_ctx* c, const double* U, const double* Q, double t, double* R) {
+  return guarded(c, [&]() -> int {
+    double* du = ensure(c->d_hu, c->nU());
+    double* dr = ensure(c->d_hr, c->nU());
+    double* dq = c->second ? ensure(c->d_Q, c->nQ()) : nullptr;
+    ck(cudaMemcpyAsync(du, U, c->nU() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D U");
+    if (dq) ck(cudaMemcpyAsync(dq, Q, c->nQ() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D Q");
+    c->sync_errors = false;
+    int st = ldg_residual_uq(c, du, dq, t, dr);
+    c->sync_errors = true;
+    if (st != LDG_OK) return st;
+    ck(cudaMemcpyAsync(R, dr, c->nU() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H R");
+    return finish(c, cudaSuccess);
   });
 }
 
