@@ -3061,13 +3061,18 @@ k_spmv12(const KParams<C> kp, const double* __restrict__ V12, const double* __re
   y[(e * NPE + nd) * M + a] = acc;
 }
 
-// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c]); one thread per row
+// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c]); one
+// thread per (row, component c): the D scalars of a slot are shared by the m
+// threads of a row through L1, v is read m contiguous doubles per row, w
+// leaves in contiguous runs (measured C5: one thread per row 1.97 ms).
 template <class C>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __restrict__ v,
          double* __restrict__ w) {
   constexpr int M = C::M, NT = C::NT, NPE = C::NPE, D = C::D;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gid / M;
+  const int c = static_cast<int>(gid - row * M);
   const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
   if (row >= nrows) return;
   const int64_t T = row / NT;
@@ -3076,40 +3081,27 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
   const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
   const int nd = s * NT + r;
   const size_t e = __ldg(kp.order + k);
-  double acc[M][D];
+  double acc[D];
 #pragma unroll
-  for (int c = 0; c < M; ++c)
-#pragma unroll
-    for (int d = 0; d < D; ++d) acc[c][d] = 0.0;
+  for (int d = 0; d < D; ++d) acc[d] = 0.0;
   const double* vb = V21 + (T * C::NS12 * NT + r) * D;
 #pragma unroll
   for (int slot = 0; slot < C::NS12; ++slot) {
     const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 2);
     if (col < 0) continue;
-    double kv[D];
+    const double xv = __ldg(v + col * M + c);
 #pragma unroll
-    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + static_cast<size_t>(slot) * NT * D + d);
-#pragma unroll
-    for (int c = 0; c < M; ++c) {
-      const double xv = __ldg(v + col * M + c);
-#pragma unroll
-      for (int d = 0; d < D; ++d) acc[c][d] += kv[d] * xv;
-    }
+    for (int d = 0; d < D; ++d) acc[d] += __ldg(vb + static_cast<size_t>(slot) * NT * D + d) * xv;
   }
-  if (C::HAS_INV && kp.noslip)
+  if (C::HAS_INV && kp.noslip && (c == 0 || c == M - 1))
     k21_wall_terms<C>(kp, k, nd, [&](int end, const double* cf) {
-      const double x0 = __ldg(v + (e * NPE + end) * M), x1 = __ldg(v + (e * NPE + end) * M + M - 1);
+      const double xe = __ldg(v + (e * NPE + end) * M + c);
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        acc[0][d] += cf[d] * x0;
-        acc[M - 1][d] += cf[d] * x1;
-      }
+      for (int d = 0; d < D; ++d) acc[d] += cf[d] * xe;
     });
-  const size_t wo = (e * NPE + nd) * M * D;
+  const size_t wo = ((e * NPE + nd) * M + c) * D;
 #pragma unroll
-  for (int c = 0; c < M; ++c)
-#pragma unroll
-    for (int d = 0; d < D; ++d) w[wo + c * D + d] = acc[c][d];
+  for (int d = 0; d < D; ++d) w[wo + d] = acc[d];
 }
 
 // ===================================================== block-Jacobi preconditioner
