@@ -20,6 +20,8 @@
 //     connectivity (no column-index stream).
 #pragma once
 
+#include <type_traits>
+
 #include "ldg_device.cuh"
 
 namespace ldg {
@@ -2421,86 +2423,100 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
       }
     };
-    // phase X of group gi from buffers pb (quadrature points) and sg (scratch)
-    auto phaseX = [&](int gi, const double* pb, const double* sg) {
-      const int dir = gdir(gi);
+    auto avq = [&](const double* pA, const double* pAv, int j, int q, int ab) {
+      return (C::HAS_INV ? pA[(j * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? pAv[(j * NQ + q) * B11 + ab] : 0.0);
+    };
+    // phase X of group gi from buffers pb (quadrature points) and sg (scratch).
+    // The direction is a compile-time constant (DIRC) so the line/slot index
+    // maps fold; one thread owns a (row position i, block entry) pair and walks
+    // the group's GL lines (its index decomposition and slot offsets are
+    // computed once per group).
+    auto phaseX = [&](auto DIRC, int gi, const double* pb, const double* sg) {
+      constexpr int dir = decltype(DIRC)::value;
       const double* pA = pb;
       const double* pAv = pA + S3::A;
       const double* pBq = pAv + S3::AV;
       const int2 c0 = scon[dir * 2 + 0], c1 = scon[dir * 2 + 1];
-      auto avq = [&](int j, int q, int ab) {
-        return (C::HAS_INV ? pA[(j * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? pAv[(j * NQ + q) * B11 + ab] : 0.0);
-      };
-      constexpr int N11 = GL * NP * B11;
-      constexpr int N12 = C::SECOND ? GL * NP * B12 : 0;
+      const int g0 = (gi % NG) * GL;  // first line of the group
+      constexpr int N11 = NP * B11;
+      constexpr int N12 = C::SECOND ? NP * B12 : 0;
+      double* const K11e = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11;
+      double* const K12e = C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr;
       for (int w = tid; w < N11 + N12; w += nthr) {
         if (w < N11) {
-          // ---- K11: (line j, row i, entry ab)
-          const int ab = w % B11, ji = w / B11, i = ji % NP, j = ji / NP;
-          const int line = gline(gi, j);
-          const int nd = node_on_line<C>(dir, line, i);
-          const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-          const double* e0 = sg + 0 * GL + j;
-          const double* e1 = sg + 1 * GL + j;
-          double av[NQ8];
+          // ---- K11: row position i, entry ab = a*M + b, all GL lines of the group
+          const int ab = w % B11, i = w / B11;
+          const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
+          const size_t eoff = (static_cast<size_t>(ab / M) * NT) * M + ab % M;
+#pragma unroll 1
+          for (int j = 0; j < GL; ++j) {
+            const int nd = node_on_line<C>(dir, g0 + j, i);
+            const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+            const double e0 = sg[ab * SLS + j], e1 = sg[ab * SLS + GL + j];
+            double av[NQ8];
 #pragma unroll
-          for (int q = 0; q < NQ8; ++q) av[q] = (VOL11 && q < NQ) ? avq(j, q, ab) : 0.0;
-          double* rowp = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11 + static_cast<size_t>(nd / NT) * SM::ST11 +
-                         (static_cast<size_t>(ab / M) * NT + nd % NT) * M + ab % M;
+            for (int q = 0; q < NQ8; ++q) av[q] = (VOL11 && q < NQ) ? avq(pA, pAv, j, q, ab) : 0.0;
+            double* rowp = K11e + static_cast<size_t>(nd / NT) * SM::ST11 + eoff + static_cast<size_t>(nd % NT) * M;
 #pragma unroll
-          for (int t = 0; t < NP; ++t) {
-            double v = VOL11 ? ccdot(i, t, av) : 0.0;
-            if (t == 0) v += smi[i * 2 + 0] * e0[ab * SLS];
-            if (t == P) v += smi[i * 2 + 1] * e1[ab * SLS];
-            if (t == i) {
-              // self block: dir 2 starts it, dir 1 adds, dir 0 completes and stores
-              double* sp = self11 + nd * B11 + ab;
-              if (dir == 2) *sp = v;
-              else if (dir == 1) *sp += v;
-              else rowp[static_cast<size_t>(t) * NT * B11] = sc * (v + *sp);
-              continue;
+            for (int t = 0; t < NP; ++t) {
+              double v = VOL11 ? ccdot(i, t, av) : 0.0;
+              if (t == 0) v += li0 * e0;
+              if (t == P) v += li1 * e1;
+              if (t == i) {
+                // self block: dir 2 starts it, dir 1 adds, dir 0 completes and stores
+                double* sp = self11 + nd * B11 + ab;
+                if (dir == 2) *sp = v;
+                else if (dir == 1) *sp += v;
+                else rowp[static_cast<size_t>(t) * NT * B11] = sc * (v + *sp);
+                continue;
+              }
+              const int slot = dir == 0 ? t : NP + (dir - 1) * P + (t < i ? t : t - 1);
+              rowp[static_cast<size_t>(slot) * NT * B11] = sc * v;
             }
-            rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B11] = sc * v;
+            rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] =
+                c0.x >= 0 ? sc * (li0 * sg[(B11 + ab) * SLS + j]) : 0.0;
+            rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] =
+                c1.x >= 0 ? sc * (li1 * sg[(B11 + ab) * SLS + GL + j]) : 0.0;
           }
-          rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] =
-              c0.x >= 0 ? sc * (smi[i * 2 + 0] * e0[(B11 + ab) * SLS]) : 0.0;
-          rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] =
-              c1.x >= 0 ? sc * (smi[i * 2 + 1] * e1[(B11 + ab) * SLS]) : 0.0;
         } else if (C::SECOND) {
-          // ---- K12: (line j, row i, stored entry ab = a' * MD + b)
+          // ---- K12: row position i, stored entry ab = a' * MD + b, all GL lines
           const int v12 = w - N11;
-          const int ab = v12 % B12, ji = v12 / B12, i = ji % NP, j = ji / NP;
+          const int ab = v12 % B12, i = v12 / B12;
           const int a = ab / MD + A0, b = ab % MD;
-          const int line = gline(gi, j);
-          const int nd = node_on_line<C>(dir, line, i);
-          const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-          double bv[NQ8];
-#pragma unroll
-          for (int q = 0; q < NQ8; ++q) bv[q] = q < NQ ? pBq[(j * NQ + q) * M * MD + a * MD + b] : 0.0;
-          const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + 0 * GL + j];
-          const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + 1 * GL + j];
+          const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
           const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
           const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
-          double* rowp = K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 + static_cast<size_t>(nd / NT) * SM::ST12 +
-                         (static_cast<size_t>(ab / MD) * NT + nd % NT) * MD + ab % MD;
+          const size_t eoff = (static_cast<size_t>(ab / MD) * NT) * MD + ab % MD;
+#pragma unroll 1
+          for (int j = 0; j < GL; ++j) {
+            const int nd = node_on_line<C>(dir, g0 + j, i);
+            const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+            double bv[NQ8];
 #pragma unroll
-          for (int t = 0; t < NP; ++t) {
-            double v = ccdot(i, t, bv);
-            if (t == 0 && own0) v += smi[i * 2 + 0] * eq0;
-            if (t == P && own1) v += smi[i * 2 + 1] * eq1;
-            if (t == i) {
-              double* sp = self12 + nd * B12 + ab;
-              if (dir == 2) *sp = v;
-              else if (dir == 1) *sp += v;
-              else rowp[static_cast<size_t>(t) * NT * B12] = sc * (v + *sp);
-              continue;
+            for (int q = 0; q < NQ8; ++q) bv[q] = q < NQ ? pBq[(j * NQ + q) * M * MD + a * MD + b] : 0.0;
+            const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + j];
+            const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + GL + j];
+            double* rowp = K12e + static_cast<size_t>(nd / NT) * SM::ST12 + eoff + static_cast<size_t>(nd % NT) * MD;
+#pragma unroll
+            for (int t = 0; t < NP; ++t) {
+              double v = ccdot(i, t, bv);
+              if (t == 0 && own0) v += li0 * eq0;
+              if (t == P && own1) v += li1 * eq1;
+              if (t == i) {
+                double* sp = self12 + nd * B12 + ab;
+                if (dir == 2) *sp = v;
+                else if (dir == 1) *sp += v;
+                else rowp[static_cast<size_t>(t) * NT * B12] = sc * (v + *sp);
+                continue;
+              }
+              const int slot = dir == 0 ? t : NP + (dir - 1) * P + (t < i ? t : t - 1);
+              rowp[static_cast<size_t>(slot) * NT * B12] = sc * v;
             }
-            rowp[static_cast<size_t>(inel_slot<C>(dir, i, t)) * NT * B12] = sc * v;
+            double nbv = 0.0;
+            if (!own0) nbv = sc * (li0 * eq0);
+            if (!own1) nbv = sc * (li1 * eq1);
+            rowp[static_cast<size_t>(D * P + 1 + dir) * NT * B12] = nbv;
           }
-          double nbv = 0.0;
-          if (!own0) nbv = sc * (smi[i * 2 + 0] * eq0);
-          if (!own1) nbv = sc * (smi[i * 2 + 1] * eq1);
-          rowp[static_cast<size_t>(D * P + 1 + dir) * NT * B12] = nbv;
         }
       }
     };
@@ -2516,7 +2532,15 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     for (int gi = 0; gi < NGT; ++gi) {
       const int cb = gi & 1, nb = cb ^ 1;
       if (gi + 1 < NGT) gather(gi + 1, seg0 + nb * S3::SEG);
-      phaseX(gi, pts0 + cb * S3::PTS, seg0 + cb * S3::SEG);
+      {
+        const double* pb = pts0 + cb * S3::PTS;
+        const double* sgb = seg0 + cb * S3::SEG;
+        switch (gdir(gi)) {
+          case 0: phaseX(std::integral_constant<int, 0>{}, gi, pb, sgb); break;
+          case 1: phaseX(std::integral_constant<int, 1>{}, gi, pb, sgb); break;
+          default: phaseX(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
+        }
+      }
       if (gi + 1 < NGT) phaseP(gi + 1, pts0 + nb * S3::PTS);
       cp_async_wait_all();
       __syncthreads();
@@ -3061,18 +3085,13 @@ k_spmv12(const KParams<C> kp, const double* __restrict__ V12, const double* __re
   y[(e * NPE + nd) * M + a] = acc;
 }
 
-// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c]); one
-// thread per (row, component c): the D scalars of a slot are shared by the m
-// threads of a row through L1, v is read m contiguous doubles per row, w
-// leaves in contiguous runs (measured C5: one thread per row 1.97 ms).
+// w = K21 v  (w[(node*M + c)*D + d] = sum_slot K21[slot][d] v[col][c]); one thread per row
 template <class C>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __restrict__ v,
          double* __restrict__ w) {
   constexpr int M = C::M, NT = C::NT, NPE = C::NPE, D = C::D;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t row = gid / M;
-  const int c = static_cast<int>(gid - row * M);
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nrows = static_cast<int64_t>(kp.E) * NPE;
   if (row >= nrows) return;
   const int64_t T = row / NT;
@@ -3081,27 +3100,40 @@ k_spmv21(const KParams<C> kp, const double* __restrict__ V21, const double* __re
   const int s = static_cast<int>(T - static_cast<int64_t>(k) * C::TPE);
   const int nd = s * NT + r;
   const size_t e = __ldg(kp.order + k);
-  double acc[D];
+  double acc[M][D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) acc[d] = 0.0;
+  for (int c = 0; c < M; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[c][d] = 0.0;
   const double* vb = V21 + (T * C::NS12 * NT + r) * D;
 #pragma unroll
   for (int slot = 0; slot < C::NS12; ++slot) {
     const int64_t col = slot_col<C, C::D * C::P + 1>(kp, k, e, nd, slot, 2);
     if (col < 0) continue;
-    const double xv = __ldg(v + col * M + c);
+    double kv[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] += __ldg(vb + static_cast<size_t>(slot) * NT * D + d) * xv;
+    for (int d = 0; d < D; ++d) kv[d] = __ldg(vb + static_cast<size_t>(slot) * NT * D + d);
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const double xv = __ldg(v + col * M + c);
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[c][d] += kv[d] * xv;
+    }
   }
-  if (C::HAS_INV && kp.noslip && (c == 0 || c == M - 1))
+  if (C::HAS_INV && kp.noslip)
     k21_wall_terms<C>(kp, k, nd, [&](int end, const double* cf) {
-      const double xe = __ldg(v + (e * NPE + end) * M + c);
+      const double x0 = __ldg(v + (e * NPE + end) * M), x1 = __ldg(v + (e * NPE + end) * M + M - 1);
 #pragma unroll
-      for (int d = 0; d < D; ++d) acc[d] += cf[d] * xe;
+      for (int d = 0; d < D; ++d) {
+        acc[0][d] += cf[d] * x0;
+        acc[M - 1][d] += cf[d] * x1;
+      }
     });
-  const size_t wo = ((e * NPE + nd) * M + c) * D;
+  const size_t wo = (e * NPE + nd) * M * D;
 #pragma unroll
-  for (int d = 0; d < D; ++d) w[wo + d] = acc[d];
+  for (int c = 0; c < M; ++c)
+#pragma unroll
+    for (int d = 0; d < D; ++d) w[wo + c * D + d] = acc[c][d];
 }
 
 // ===================================================== block-Jacobi preconditioner

@@ -283,8 +283,8 @@ struct Launch {
   }
   static cudaError_t spmv21(const DevCtx& d, const double* V21, const double* v, double* w) {
     if (!C::SECOND) return cudaSuccess;
-    const long long threads = static_cast<long long>(d.E) * C::NPE * C::M;
-    k_spmv21<C><<<static_cast<int>((threads + 255) / 256), 256, 0, d.stream>>>(params(d), V21, v, w);
+    // one thread per row (measured C5: one thread per (row, component) 2.35 vs 1.97 ms)
+    k_spmv21<C><<<rgrid(d), 128, 0, d.stream>>>(params(d), V21, v, w);
     count(d);
     return cudaGetLastError();
   }
