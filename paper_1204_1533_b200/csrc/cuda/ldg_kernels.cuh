@@ -270,13 +270,6 @@ __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-// fp64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row) B(4x8, col).  Fragments:
-// a = A[lane/4][lane%4], b = B[lane%4][lane/4], d0/d1 = D[lane/4][2(lane%4) + 0/1].
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 // Staged tile -> global, asynchronous: TMA bulk copy (cp.async.bulk, SASS
 // UBLKCP) issued by thread 0 when size and both addresses are 16-byte
@@ -2527,131 +2520,6 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         }
       }
     };
-#ifndef LDG_JAC_DMMA
-#define LDG_JAC_DMMA 0
-#endif
-    // phase X on the fp64 tensor cores (DMMA m8n8k4): per line j of the group
-    // the line blocks are one product C[(i,t)][col] = sum_q cc[i][t][q] B[q][col],
-    // (i,t) over (p+1)^2 rows (padded to 32), q over n_q (padded to 8), col over
-    // the K11 entries (A + Av at the point) then the stored K12 entries (Bq).
-    // A task = (line j, 8-column tile): 4 row tiles x 2 k-steps = 8 DMMA with
-    // the column tile's B fragments loaded once; the epilogue adds the lifted
-    // endpoint blocks, scales by -1/J of the row node, accumulates the self
-    // blocks over the directions and stores.
-    constexpr int NCOL = B11 + (C::SECOND ? B12 : 0);
-    constexpr int NTILE = (NCOL + 7) / 8;
-    constexpr int NMT = (NP * NP + 7) / 8;
-    static_assert(NMT <= 4, "row tiles");
-    const int lane = tid & 31, wid = tid >> 5, nwarp = nthr >> 5;
-    __syncthreads();  // cc8 filled
-    double afr[4][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int it = mt * 8 + lane / 4, q = ks * 4 + lane % 4;
-        afr[mt][ks] = (mt < NMT && it < NP * NP && q < NQ8) ? cc8[it * NQ8 + q] : 0.0;
-      }
-    auto phaseXm = [&](auto DIRC, int gi, const double* pb, const double* sg) {
-      constexpr int dir = decltype(DIRC)::value;
-      const double* pA = pb;
-      const double* pAv = pA + S3::A;
-      const double* pBq = pAv + S3::AV;
-      const int2 c0 = scon[dir * 2 + 0], c1 = scon[dir * 2 + 1];
-      const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
-      const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
-      const int g0 = (gi % NG) * GL;
-      double* const K11e = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11;
-      double* const K12e = C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr;
-      for (int task = wid; task < GL * NTILE; task += nwarp) {
-        const int j = task / NTILE, nt = task - j * NTILE;
-        // B fragments: k = q (lane % 4 + 4 ks), n = column (lane / 4)
-        double bf[2];
-        {
-          const int col = nt * 8 + lane / 4;
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const int q = ks * 4 + lane % 4;
-            double bv = 0.0;
-            if (q < NQ && col < NCOL) {
-              if (col < B11) bv = VOL11 ? avq(pA, pAv, j, q, col) : 0.0;
-              else if (C::SECOND) bv = pBq[(j * NQ + q) * M * MD + A0 * MD + (col - B11)];
-            }
-            bf[ks] = bv;
-          }
-        }
-        double dacc[4][2];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          dacc[mt][0] = dacc[mt][1] = 0.0;
-          if (mt < NMT) {
-            dmma884(dacc[mt][0], dacc[mt][1], afr[mt][0], bf[0]);
-            dmma884(dacc[mt][0], dacc[mt][1], afr[mt][1], bf[1]);
-          }
-        }
-        // epilogue: lane holds rows it = mt*8 + lane/4, columns nt*8 + 2(lane%4) + h
-#pragma unroll
-        for (int mt = 0; mt < NMT; ++mt) {
-          const int it = mt * 8 + lane / 4;
-          if (it >= NP * NP) continue;
-          const int i = it / NP, t = it - i * NP;
-          const int nd = node_on_line<C>(dir, g0 + j, i);
-          const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-          const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
-          const int slot = t == i ? (nd % NP) : (dir == 0 ? t : NP + (dir - 1) * P + (t < i ? t : t - 1));
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = nt * 8 + 2 * (lane % 4) + h;
-            if (col >= NCOL) continue;
-            double v = dacc[mt][h];
-            if (col < B11) {
-              const int ab = col;
-              if (t == 0) v += li0 * sg[ab * SLS + j];
-              if (t == P) v += li1 * sg[ab * SLS + GL + j];
-              double* rowp = K11e + static_cast<size_t>(nd / NT) * SM::ST11 +
-                             (static_cast<size_t>(ab / M) * NT + nd % NT) * M + ab % M;
-              if (t == i) {
-                double* sp = self11 + nd * B11 + ab;
-                if (dir == 2) *sp = v;
-                else if (dir == 1) *sp += v;
-                else rowp[static_cast<size_t>(slot) * NT * B11] = sc * (v + *sp);
-              } else {
-                rowp[static_cast<size_t>(slot) * NT * B11] = sc * v;
-              }
-              if (t == 0) {  // the row's neighbour-slot blocks (once per (i, ab))
-                rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] =
-                    c0.x >= 0 ? sc * (li0 * sg[(B11 + ab) * SLS + j]) : 0.0;
-                rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] =
-                    c1.x >= 0 ? sc * (li1 * sg[(B11 + ab) * SLS + GL + j]) : 0.0;
-              }
-            } else if (C::SECOND) {
-              const int ab = col - B11;
-              const int a = ab / MD + A0, b = ab % MD;
-              const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + j];
-              const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + GL + j];
-              if (t == 0 && own0) v += li0 * eq0;
-              if (t == P && own1) v += li1 * eq1;
-              double* rowp = K12e + static_cast<size_t>(nd / NT) * SM::ST12 +
-                             (static_cast<size_t>(ab / MD) * NT + nd % NT) * MD + ab % MD;
-              if (t == i) {
-                double* sp = self12 + nd * B12 + ab;
-                if (dir == 2) *sp = v;
-                else if (dir == 1) *sp += v;
-                else rowp[static_cast<size_t>(slot) * NT * B12] = sc * (v + *sp);
-              } else {
-                rowp[static_cast<size_t>(slot) * NT * B12] = sc * v;
-              }
-              if (t == 0) {
-                double nbv = 0.0;
-                if (!own0) nbv = sc * (li0 * eq0);
-                if (!own1) nbv = sc * (li1 * eq1);
-                rowp[static_cast<size_t>(D * P + 1 + dir) * NT * B12] = nbv;
-              }
-            }
-          }
-        }
-      }
-    };
     (void)sccd;
     // ---- pipeline over the 3*NG groups
     cp_async_wait_all();
@@ -2667,18 +2535,13 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       {
         const double* pb = pts0 + cb * S3::PTS;
         const double* sgb = seg0 + cb * S3::SEG;
-        if (LDG_JAC_DMMA) {
-          switch (gdir(gi)) {
-            case 0: phaseXm(std::integral_constant<int, 0>{}, gi, pb, sgb); break;
-            case 1: phaseXm(std::integral_constant<int, 1>{}, gi, pb, sgb); break;
-            default: phaseXm(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
-          }
-        } else {
-          switch (gdir(gi)) {
-            case 0: phaseX(std::integral_constant<int, 0>{}, gi, pb, sgb); break;
-            case 1: phaseX(std::integral_constant<int, 1>{}, gi, pb, sgb); break;
-            default: phaseX(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
-          }
+        // (an fp64 tensor-core (DMMA m8n8k4) phase X was measured parity-green
+        // but slower -- C5 127.0 vs 92.8 ms: the per-entry epilogue, not the
+        // contraction, bounds this phase; commit 101d93b)
+        switch (gdir(gi)) {
+          case 0: phaseX(std::integral_constant<int, 0>{}, gi, pb, sgb); break;
+          case 1: phaseX(std::integral_constant<int, 1>{}, gi, pb, sgb); break;
+          default: phaseX(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
         }
       }
       if (gi + 1 < NGT) phaseP(gi + 1, pts0 + nb * S3::PTS);
