@@ -123,18 +123,12 @@ __device__ __forceinline__ double bnd_uhat(const KParams<C>& kp, int bc, const d
   return __ldg(g + c);
 }
 
-#ifndef LDG_VISC_DU  // closed-form viscous dF/du (1) or dual numbers (0)
-#define LDG_VISC_DU 1
-#endif
+static constexpr int LDG_VISC_DU = 1;  // closed-form viscous dF/du (1) or dual numbers (0)
 constexpr bool VISC_DU_CLOSED = LDG_VISC_DU != 0;
 
-#ifndef LDG_JAC_SMEMTAB  // tuning knob: assembly basis coefficients from shared memory (1) or the constant
-#define LDG_JAC_SMEMTAB 0  // bank (0); measured: the constant bank wins (C2 0.266 vs 0.311 ms) despite its spills
-#endif
+static constexpr int LDG_JAC_SMEMTAB = 0;  // tuning knob: assembly basis coefficients from shared memory (1) or the constant bank (0); measured: the constant bank wins (C2 0.266 vs 0.311 ms) despite its spills
 constexpr int JAC_SMEMTAB = LDG_JAC_SMEMTAB;
-#ifndef LDG_JAC_CHAINS  // assembly: line-block sums as one (1) or two (2) dependent DFMA chains
-#define LDG_JAC_CHAINS 1
-#endif
+static constexpr int LDG_JAC_CHAINS = 1;  // assembly: line-block sums as one (1) or two (2) dependent DFMA chains
 constexpr int JAC_CHAINS = LDG_JAC_CHAINS;
   // 0 constant bank, 1 shared (scalar), 2 shared (pairs)
 // ---------------------------------------------------------------- helpers
@@ -334,9 +328,7 @@ __device__ __forceinline__ void store_tile(double* __restrict__ gdst, const doub
 // one mbarrier); the scattered neighbour traces of batch i+1 are gathered with
 // cp.async as soon as its connectivity has landed.  Compute is
 // thread-per-line with every operand in shared memory.
-#ifndef LDG_RES_MET_SMEM  // residual: stage the metric in the ring (1) or read it from global (0)
-#define LDG_RES_MET_SMEM 1
-#endif
+static constexpr int LDG_RES_MET_SMEM = 1;  // residual: stage the metric in the ring (1) or read it from global (0)
 template <class C, int EPB>
 struct ResP {
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
@@ -351,9 +343,7 @@ struct ResP {
   // SPLIT threads per line (warp-uniform halves: the first half of the CTA
   // takes the first quadrature points and the left end of every line, the
   // second half the rest and the right end; per-half partial sums in ACC)
-#ifndef LDG_RES_SPLIT  // measured slower for C2/C4 (more warps, same latency chains): off
-#define LDG_RES_SPLIT 1
-#endif
+static constexpr int LDG_RES_SPLIT = 1;  // measured slower for C2/C4 (more warps, same latency chains): off
   static constexpr int SPLIT = LDG_RES_SPLIT;
   static constexpr int LT = (EPB * C::LPE + 31) / 32 * 32;  // line threads of one half
   static constexpr int ACC = SPLIT * EPB * C::D * C::NPE * C::M;
@@ -362,9 +352,7 @@ struct ResP {
   static constexpr int THREADS = SPLIT * LT;
 };
 
-#ifndef LDG_RES_MINB  // k_residual_p min CTAs per SM (register cap)
-#define LDG_RES_MINB 1
-#endif
+static constexpr int LDG_RES_MINB = 1;  // k_residual_p min CTAs per SM (register cap)
 template <class C, int EPB>
 __global__ void __launch_bounds__(ResP<C, EPB>::THREADS, LDG_RES_MINB)
 k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __restrict__ Q,
@@ -773,17 +761,13 @@ struct ResF {
   static constexpr int TOTAL = IO::SMEM + F + FH + TAB;
   // one element per batch (the ring fills shared memory): as many warps as
   // the register file allows
-#ifndef LDG_RESF_THREADS1
-#define LDG_RESF_THREADS1 512
-#endif
+static constexpr int LDG_RESF_THREADS1 = 512;
   static constexpr int THREADS = EPB == 1 ? LDG_RESF_THREADS1 : 256;
   static constexpr long long bytes_per_elem() {
     return IO::bytes_per_elem() + 8LL * (C::LPE * C::NQ * C::M + C::LPE * 2 * C::M);
   }
 };
-#ifndef LDG_RESF_BUDGET_KB  // shared-memory budget per CTA of the flux-parallel residual / gradient
-#define LDG_RESF_BUDGET_KB 110  // measured (C3): 72 KB +40 us, 55 KB +96 us
-#endif
+static constexpr int LDG_RESF_BUDGET_KB = 110;  // shared-memory budget per CTA of the flux-parallel residual / gradient measured (C3): 72 KB +40 us, 55 KB +96 us
 template <class C>
 struct ResFEpb {
   static constexpr long long per = ResF<C, 1>::bytes_per_elem();
@@ -1185,9 +1169,7 @@ struct SeTile {
   __device__ __forceinline__ int operator()(int tl, int, int, int side) const { return tl * 2 + side; }
 };
 
-#ifndef LDG_EJ_MINB  // k_endjac min CTAs per SM (register cap 65536 / (128 * minb))
-#define LDG_EJ_MINB 3  // measured: C2 Jacobian 0.244 -> 0.239 ms, C3 -1.3 %, C4 neutral
-#endif
+static constexpr int LDG_EJ_MINB = 3;  // k_endjac min CTAs per SM (register cap 65536 / (128 * minb)) measured: C2 Jacobian 0.244 -> 0.239 ms, C3 -1.3 %, C4 neutral
 // BND = false: the chunk's owned faces (flist = kp.owned, or every face of
 // the chunk when null) except slip-wall / Neumann boundary ends; BND = true:
 // exactly those ends (flist = their list), with the general boundary kinds.
@@ -1315,9 +1297,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 #pragma unroll
       for (int c = 0; c < M; ++c) Jx[c * M + c] += pen;
     }
-#ifndef LDG_EJ_DUALN  // all M seeds in one Dual<M> evaluation of the Riemann flux (first-order, not BND)
-#define LDG_EJ_DUALN 0  // measured slower: +18 us at 168 regs (spills), +6 us at 255
-#endif
+static constexpr int LDG_EJ_DUALN = 0;  // all M seeds in one Dual<M> evaluation of the Riemann flux (first-order, not BND) measured slower: +18 us at 168 regs (spills), +6 us at 255
     constexpr bool DN = LDG_EJ_DUALN && !BND && !C::SECOND && C::HAS_INV && !LLFC && SEEDS == M;
     if (DN) {
       using DM = Dual<(DN ? M : 1)>;
@@ -1442,25 +1422,14 @@ struct JacThreads {
   // other work units: one phase-2 item (tile line, a, b) per thread when that
   // is 129..256 threads (no tail round behind the barrier), else 128
   static constexpr int p2 = (TileLines<C>::NLT * C::B11 + 31) / 32 * 32;
-#ifndef LDG_JT_SMALL  // tuning knobs (variant builds): CTA size / min CTAs per SM
   // (measured: second-order tiles gain from it; the C2 Euler tile too since
   // the single-chunk endpoint scratch: 0.242 vs 0.252 ms at 160 vs 128 threads)
   static constexpr int small = p2 > 128 && p2 <= 256 ? p2 : 128;
-#else
-  static constexpr int small = LDG_JT_SMALL;
-#endif
   // 3-D slab / line work units (one CTA per unit, shared memory for one CTA
   // per SM): as many warps as the 128-register cap allows
-#ifndef LDG_JT_UNIT3
-#define LDG_JT_UNIT3 512
-#endif
   static constexpr bool unit3 = C::D == 3 && C::WU != 0;
-  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : (unit3 ? LDG_JT_UNIT3 : small);
-#ifndef LDG_JT_MINB
+  static constexpr int value = big ? (rows < 128 ? 128 : (rows > 640 ? 640 : rows)) : (unit3 ? 512 : small);
   static constexpr int min_blocks = big || unit3 ? 1 : (small > 128 ? 65536 / (small * 128) : 4);
-#else
-  static constexpr int min_blocks = big ? 1 : LDG_JT_MINB;
-#endif
 };
 
 template <class C>
@@ -1486,13 +1455,9 @@ struct JacSmem {
   static constexpr int TOTAL = U + Q + SEC + WORK + MET;
 };
 
-#ifndef LDG_P2_UNROLL  // tuning knob: unroll of the phase-2 row loop (0 = full)
-#define LDG_P2_UNROLL 0
-#endif
+static constexpr int LDG_P2_UNROLL = 0;  // tuning knob: unroll of the phase-2 row loop (0 = full)
 constexpr int P2_UNROLL_K = LDG_P2_UNROLL;
-#ifndef LDG_P2_ROWS  // tuning knob: 2-D phase 2 with one row per item (1) or one line per item (0);
-#define LDG_P2_ROWS 0  // measured: per-line items are faster (C2 0.264 vs 0.297 ms)
-#endif
+static constexpr int LDG_P2_ROWS = 0;  // tuning knob: 2-D phase 2 with one row per item (1) or one line per item (0); measured: per-line items are faster (C2 0.264 vs 0.297 ms)
 constexpr bool P2_ROWS = LDG_P2_ROWS != 0;
 
 
@@ -2076,10 +2041,7 @@ struct JacP {
   // fused endpoint phase (3-D element units, first order, LLF: closed-form
   // endpoint Jacobians computed in the assembly from gathered neighbour
   // traces; no k_endjac launch and no scratch round trip through HBM)
-#ifndef LDG_JAC_FUSED_EJ
-#define LDG_JAC_FUSED_EJ 1
-#endif
-  static constexpr bool FE = LDG_JAC_FUSED_EJ && C::D == 3 && C::WU == 0 && !C::SECOND && C::HAS_INV &&
+  static constexpr bool FE = C::D == 3 && C::WU == 0 && !C::SECOND && C::HAS_INV &&
                              C::RI != LDG_ROE;
   static constexpr int NBV = FE ? ev(2 * C::D * C::NL * C::M) : 0;  // neighbour traces per line end
   // fused: the endpoint block is computed per element (one copy outside the
@@ -2089,31 +2051,20 @@ struct JacP {
   static constexpr int BUF = U + Q + MET + CONN + SER + NBV;
   using SM = JacSmem<C>;
   // 2-D: the element's K11 tile is formed in shared memory and leaves with one
-  // TMA bulk store (sequential write stream, no per-entry global stores)
-#ifndef LDG_JAC_STAGE
-#define LDG_JAC_STAGE 1
-#endif
-  // (measured: a small gain for the Euler tile, a loss for second-order
-  // tiles whose larger footprint costs occupancy)
-  // 2-D: software pipeline -- phases 2-3 of element k and phase 1 of element
-  // k+1 share one barrier interval (double quadrature-point tables, 3-deep
-  // input ring)
-#ifndef LDG_JAC_PIPE  // measured: no gain for C2 (0.267 vs 0.265 ms), a loss for C3 (occupancy): off
-#define LDG_JAC_PIPE 0
-#endif
-  static constexpr bool PIPE = LDG_JAC_PIPE && C::D == 2;
-  static constexpr int WORK2 = PIPE ? SM::A + SM::AV + SM::BQ : 0;  // second quadrature-point set
-  static constexpr bool STAGE = !PIPE && LDG_JAC_STAGE && C::D == 2 && !C::SECOND && (SM::ST11 % 2 == 0) &&
+  // TMA bulk store (sequential write stream, no per-entry global stores;
+  // measured: a small gain for the Euler tile, a loss for second-order tiles
+  // whose larger footprint costs occupancy)
+  // (rejected after measurement: a 2-D software pipeline of phases 2-3 of
+  // element k with phase 1 of element k+1 -- C2 0.267 vs 0.265 ms, a loss for
+  // C3 through occupancy; a 3-deep ring for every configuration -- C2 -0.9 us)
+  static constexpr bool STAGE = C::D == 2 && !C::SECOND && (SM::ST11 % 2 == 0) &&
                                 8LL * SM::ST11 <= 64 * 1024;
   static constexpr int STG = STAGE ? SM::ST11 : 0;
-  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + WORK2 + STG + SE1); }
-  // prefetch ring depth: 3 for the pipelined 2-D tile and the one-CTA-per-SM
-  // 3-D element units (when it fits), 2 where several CTAs share an SM
-#ifndef LDG_JAC_NBUF3  // 3-deep input ring for every persistent assembly that fits (knob)
-#define LDG_JAC_NBUF3 0  // measured (C2): -0.9 us, within noise: off
-#endif
-  static constexpr int NBUF = ((PIPE || JacThreads<C>::big || LDG_JAC_NBUF3) && bytes(3) <= 200 * 1024) ? 3 : 2;
-  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + WORK2 + STG + SE1;  // 4 doubles hold up to 3 mbarriers
+  static constexpr long long bytes(int nb) { return 8LL * (4 + nb * BUF + SM::WORK + STG + SE1); }
+  // prefetch ring depth: 3 for the one-CTA-per-SM 3-D element units (when it
+  // fits), 2 where several CTAs share an SM
+  static constexpr int NBUF = (JacThreads<C>::big && bytes(3) <= 200 * 1024) ? 3 : 2;
+  static constexpr int TOTAL = 4 + NBUF * BUF + SM::WORK + STG + SE1;  // 4 doubles hold up to 3 mbarriers
   static constexpr bool OK = C::WU == 0 && (C::NPE * C::M) % 2 == 0 && (!C::SECOND || (C::NPE * C::MD) % 2 == 0) &&
                              (EndJac<C>::PER_ELEM % 2 == 0) && bytes(2) <= 200 * 1024;
 };
@@ -2135,10 +2086,7 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   double* sAv = sA + SM::A;
   double* sBq = sAv + SM::AV;
   double* stab = sBq + SM::BQ;
-  double* sstage = work + SM::WORK + JP::WORK2;  // K11 tile staging (JP::STAGE)
-  double* sA2 = work + SM::WORK;                  // second quadrature-point set (JP::PIPE)
-  double* sAv2 = sA2 + SM::A;
-  double* sBq2 = sAv2 + SM::AV;
+  double* sstage = work + SM::WORK;  // K11 tile staging (JP::STAGE)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = gridDim.x;
   if (k_begin + static_cast<int>(blockIdx.x) >= k_end) return;
@@ -2146,7 +2094,7 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
   auto bQ = [&](int bi) { return bufs + bi * JP::BUF + JP::U; };
   auto bMET = [&](int bi) { return bufs + bi * JP::BUF + JP::U + JP::Q; };
   auto bCONN = [&](int bi) { return reinterpret_cast<int2*>(bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET); };
-  double* const se1 = work + SM::WORK + JP::WORK2 + JP::STG;  // fused: the element's endpoint block
+  double* const se1 = work + SM::WORK + JP::STG;  // fused: the element's endpoint block
   auto bSE = [&](int bi) {
     return JP::FE ? se1 : bufs + bi * JP::BUF + JP::U + JP::Q + JP::MET + JP::CONN;
   };
@@ -2167,48 +2115,15 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     if (C::SECOND) tma_load_1d(bQ(bi), Q + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
     tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k) * C::METP, C::METP * 8, &bar[bi]);
     tma_load_1d(bCONN(bi), kp.conn + static_cast<size_t>(k) * C::D * 2, 2 * C::D * 8, &bar[bi]);
-#ifndef LDG_SE_ONCE  // endpoint scratch read with an L2 evict-first policy
-#define LDG_SE_ONCE 0  // measured: no gain (C2 +0.7 us, C3 +8 us)
-#endif
-    if (fe) {
-      // (endpoint Jacobians computed in the element loop)
-    } else if (LDG_SE_ONCE)
-      tma_load_1d_once(bSE(bi), SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
-    else
+    // (fused: the endpoint Jacobians are computed in the element loop; an L2
+    // evict-first read of the scratch measured no gain: C2 +0.7 us, C3 +8 us)
+    if (!fe)
       tma_load_1d(bSE(bi), SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM, EJ::PER_ELEM * 8, &bar[bi]);
   };
   const int k0 = k_begin + blockIdx.x;
   if (tid == 0)
     for (int b = 0; b < NB; ++b)
       if (k0 + b * G < k_end) issue(k0 + b * G, b);
-  if (JP::PIPE) {
-    // phase 1 of the first element, then per interval: phases 2-3 of element
-    // k (set it&1) and phase 1 of element k+G (set (it+1)&1), one barrier
-    if (k0 < k_end) {
-      mbar_wait(&bar[0], 0);
-      jac_tile<C, SeFull<C>, 1>(kp, k0, 0, kp.order[k0], bU(0), bQ(0), bMET(0), bCONN(0), bSE(0), SeFull<C>(), sA, sAv,
-                                sBq, stab, nullptr, nullptr, tid, nthr);
-    }
-    __syncthreads();
-    for (int k = k0, it = 0; k < k_end; k += G, ++it) {
-      const int cur = it % NB, nx = (it + 1) % NB;
-      const int kn = k + G;
-      if (kn < k_end) mbar_wait(&bar[nx], ((it + 1) / NB) & 1);
-      double* a0 = (it & 1) ? sA2 : sA;
-      double* av0 = (it & 1) ? sAv2 : sAv;
-      double* bq0 = (it & 1) ? sBq2 : sBq;
-      jac_tile<C, SeFull<C>, 2>(kp, k, 0, kp.order[k], bU(cur), bQ(cur), bMET(cur), bCONN(cur), bSE(cur), SeFull<C>(),
-                                a0, av0, bq0, stab, K11 + static_cast<size_t>(k) * C::TPE * SM::ST11,
-                                C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr, tid, nthr);
-      if (kn < k_end)
-        jac_tile<C, SeFull<C>, 1>(kp, kn, 0, kp.order[kn], bU(nx), bQ(nx), bMET(nx), bCONN(nx), bSE(nx), SeFull<C>(),
-                                  (it & 1) ? sA : sA2, (it & 1) ? sAv : sAv2, (it & 1) ? sBq : sBq2, stab, nullptr,
-                                  nullptr, tid, nthr);
-      __syncthreads();  // buffer `cur` and quadrature-point set it&1 are free
-      if (tid == 0 && k + NB * G < k_end) issue(k + NB * G, cur);
-    }
-    return;
-  }
   for (int k = k0, it = 0; k < k_end; k += G, ++it) {
     const int cur = it % NB;
     mbar_wait(&bar[cur], (it / NB) & 1);
@@ -2234,23 +2149,13 @@ k_jacobian_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     if (JP::STAGE) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();  // all reads of buffer `cur` (and of sA/sAv/sBq) done; tile staged
     if (JP::STAGE && tid == 0) {
-#ifndef LDG_JAC_STORE_HINT  // L2 policy of the tile store: 0 none, 1 evict_first, 2 evict_last
-#define LDG_JAC_STORE_HINT 2  // measured (C2): evict_last 0.3944 vs 0.3979 ms per step (SpMV reads more of K11 from L2)
-#endif
-      if (LDG_JAC_STORE_HINT == 0) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(K11g),
-                     "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8))
-                     : "memory");
-      } else {
-        uint64_t pol;
-        if (LDG_JAC_STORE_HINT == 1)
-          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-        else
-          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(K11g),
-                     "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8)), "l"(pol)
-                     : "memory");
-      }
+      // tile store with an L2 evict-last policy (measured C2: 0.3944 vs 0.3979 ms
+      // per step without a hint -- the SpMV then reads more of K11 from L2)
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(K11g),
+                   "r"(smem_u32(sstage)), "r"(static_cast<unsigned>(SM::ST11 * 8)), "l"(pol)
+                   : "memory");
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
     if (tid == 0 && k + NB * G < k_end) issue(k + NB * G, cur);
@@ -2732,9 +2637,7 @@ __device__ __forceinline__ int64_t slot_col_c(const int2* cn, size_t e, int nd, 
 // threads of a row through L1.
 // Jacobian value stream of the SpMV (read once): 0 ld.global.nc, 1 streaming
 // (ld.global.cs), 2 ld.global.nc.L1::no_allocate
-#ifndef LDG_SPMV_STREAM
-#define LDG_SPMV_STREAM 1  // measured: C2 SpMV 120.3 -> 115.4 us (ld.global.cs), C4 neutral
-#endif
+static constexpr int LDG_SPMV_STREAM = 1;  // measured: C2 SpMV 120.3 -> 115.4 us (ld.global.cs), C4 neutral
 __device__ __forceinline__ double2 ld_stream2(const double* p) {
   if (LDG_SPMV_STREAM == 1) return __ldcs(reinterpret_cast<const double2*>(p));
   if (LDG_SPMV_STREAM == 2) {
@@ -3401,9 +3304,7 @@ k_pc_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* _
 // column-load step of the substitutions serves EPW independent chains -- the
 // solve is bound by that load latency, not by bandwidth.  Same operations in
 // the same order per element as the single-element form.
-#ifndef LDG_PC_EPW
-#define LDG_PC_EPW 2  // measured (C2 apply): 1 -> 0.486 ms, 2 -> 0.407 ms
-#endif
+static constexpr int LDG_PC_EPW = 2;  // measured (C2 apply): 1 -> 0.486 ms, 2 -> 0.407 ms
 template <class C>
 __global__ void __launch_bounds__(128)
 k_pc_apply_lu2(const KParams<C> kp, const double* __restrict__ LUc, const int32_t* __restrict__ piv,
