@@ -3524,23 +3524,32 @@ k_pc_line_apply(const KParams<C> kp, const double* __restrict__ LUc, const int32
       const int t = lane / M, a = lane - t * M;
       const int nd = lane < NB ? node_on_line<C>(d, l, t) : 0;
       double x = lane < NB ? zs[nd * M + a] : 0.0;
+      // lane i holds row i of the factors (NB independent coalesced column
+      // loads issued up front: the solve below is a register/shuffle chain)
+      double row[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) row[j] = lane < NB ? __ldg(L + j * NB + lane) : 1.0;
+      int pvl = lane < NB ? __ldg(pv + lane) : lane;
       // row interchanges in order
+#pragma unroll
       for (int i = 0; i < NB; ++i) {
-        const int p = __ldg(pv + i);
+        const int p = __shfl_sync(0xffffffffu, pvl, i);
         const double xi = __shfl_sync(0xffffffffu, x, i), xp = __shfl_sync(0xffffffffu, x, p);
         if (lane == i) x = xp;
         else if (lane == p) x = xi;
       }
       // forward (unit L), column-oriented
+#pragma unroll
       for (int j = 0; j < NB - 1; ++j) {
         const double xj = __shfl_sync(0xffffffffu, x, j);
-        if (lane > j && lane < NB) x -= __ldg(L + j * NB + lane) * xj;
+        if (lane > j && lane < NB) x -= row[j] * xj;
       }
       // backward (U)
+#pragma unroll
       for (int j = NB - 1; j >= 0; --j) {
-        if (lane == j) x = x / __ldg(L + j * NB + j);
+        if (lane == j) x = x / row[j];
         const double xj = __shfl_sync(0xffffffffu, x, j);
-        if (lane < j) x -= __ldg(L + j * NB + lane) * xj;
+        if (lane < j) x -= row[j] * xj;
       }
       if (lane < NB) zs[nd * M + a] = x;
     }
