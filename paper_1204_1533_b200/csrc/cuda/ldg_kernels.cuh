@@ -622,35 +622,54 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
 //       D lines through the node, dU/dt = S - (1/J) sum (coalesced store).
 // Basis tables live in shared memory (lane-dependent indices).
 // Batch input ring shared by the flattened residual and gradient kernels:
-// two buffers of EPB elements {U, (Q), metric, connectivity, neighbour traces
-// (U; Q where the switch selects the neighbour)}; bulk data by TMA on one
-// mbarrier per buffer, neighbour traces by cp.async once the connectivity
-// has landed.
+// two buffers of EPB elements {U, (Q), metric, connectivity, element ids,
+// neighbour traces (U; Q where the switch selects the neighbour)}; bulk data
+// by TMA on one mbarrier per buffer; neighbour traces by cp.async one batch
+// ahead of the bulk data, driven by a small connectivity ring.
+// Element blocks of an odd number of doubles (odd NPE and odd M: 3-D p = 2, 4)
+// start 8 bytes off a 16-byte boundary for odd element ids: the bulk copy then
+// takes the enclosing 16-byte-aligned range (one extra double at the front or
+// the back) and the element's data sit at slot offset `e & 1` (pU / pQ).
 template <class C, int EPB, bool WQ>
 struct BatchIO {
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
-  static constexpr int U = ev(EPB * C::NPE * C::M);
-  static constexpr int Q = WQ ? ev(EPB * C::NPE * C::MD) : 0;
+  static constexpr bool ODDU = ((C::NPE * C::M) & 1) != 0;
+  static constexpr bool ODDQ = WQ && ((C::NPE * C::MD) & 1) != 0;
+  static constexpr int US = ev(C::NPE * C::M + (ODDU ? 1 : 0));            // slot stride per element
+  static constexpr int QS = WQ ? ev(C::NPE * C::MD + (ODDQ ? 1 : 0)) : 0;
+  static constexpr int U = EPB * US;
+  static constexpr int Q = EPB * QS;
   static constexpr int MET = EPB * C::METP;
   static constexpr int CONN = ev(EPB * C::D * 2);  // int2 entries, 8 B each
+  static constexpr int EID = ev((EPB + 1) / 2);    // int32 element ids
   static constexpr int NB = ev(EPB * C::LPE * 2 * C::M);
   static constexpr int NBQ = WQ ? ev(EPB * C::LPE * 2 * C::MD) : 0;
-  static constexpr int BUF = U + Q + MET + CONN + NB + NBQ;
-  static constexpr int SMEM = 2 + 2 * BUF;  // 2 doubles hold the two mbarriers
-  static constexpr bool TMA = (C::NPE * C::M) % 2 == 0 && (!WQ || (C::NPE * C::MD) % 2 == 0);
+  static constexpr int BUF = U + Q + MET + CONN + EID + NB + NBQ;
+  // 2 doubles hold the two mbarriers; after the buffers, a two-slot ring of
+  // the connectivity one batch ahead of the bulk data (drives the gathers)
+  static constexpr int SMEM = 2 + 2 * BUF + 2 * CONN;
   static constexpr long long bytes_per_elem() {
-    return 8LL * 2 * (C::NPE * C::M + (WQ ? C::NPE * C::MD : 0) + C::METP + 2 * C::D + C::LPE * 2 * C::M +
-                      (WQ ? C::LPE * 2 * C::MD : 0));
+    return 8LL * (2 * (US + QS + C::METP + 2 * C::D + 1 + C::LPE * 2 * C::M + (WQ ? C::LPE * 2 * C::MD : 0)) +
+                  4 * C::D);
   }
   uint64_t* bar;
   double* bufs;
   __device__ BatchIO(double* smem) : bar(reinterpret_cast<uint64_t*>(smem)), bufs(smem + 2) {}
+  __device__ int2* cring(int bi) const { return reinterpret_cast<int2*>(bufs + 2 * BUF + bi * CONN); }
   __device__ double* bU(int bi) const { return bufs + bi * BUF; }
   __device__ double* bQ(int bi) const { return bufs + bi * BUF + U; }
   __device__ double* bMET(int bi) const { return bufs + bi * BUF + U + Q; }
   __device__ int2* bCONN(int bi) const { return reinterpret_cast<int2*>(bufs + bi * BUF + U + Q + MET); }
-  __device__ double* bNB(int bi) const { return bufs + bi * BUF + U + Q + MET + CONN; }
-  __device__ double* bNBQ(int bi) const { return bufs + bi * BUF + U + Q + MET + CONN + NB; }
+  __device__ int* eid(int bi) const { return reinterpret_cast<int*>(bufs + bi * BUF + U + Q + MET + CONN); }
+  __device__ double* bNB(int bi) const { return bufs + bi * BUF + U + Q + MET + CONN + EID; }
+  __device__ double* bNBQ(int bi) const { return bufs + bi * BUF + U + Q + MET + CONN + EID + NB; }
+  // element le's nodal states / gradients in buffer bi
+  __device__ const double* pU(int bi, int le) const {
+    return bU(bi) + le * US + (ODDU ? (eid(bi)[le] & 1) : 0);
+  }
+  __device__ const double* pQ(int bi, int le) const {
+    return bQ(bi) + le * QS + (ODDQ ? (eid(bi)[le] & 1) : 0);
+  }
   __device__ void init(int tid) {
     if (tid == 0) {
       mbar_init(&bar[0], 1);
@@ -658,50 +677,65 @@ struct BatchIO {
       mbar_fence_init();
     }
   }
+  // One element block of N doubles (global block index e of `base`) into the
+  // slot at `dst`: returns the bytes the bulk copy will signal.  ODD blocks:
+  // the enclosing aligned range of N + 1 doubles, except for the array's last
+  // block at an even id (no double behind it): N - 1 doubles by bulk copy, the
+  // last one by a plain load.
+  template <bool ODD>
+  __device__ unsigned load_block(double* dst, const double* base, size_t e, int N, int E, uint64_t* b,
+                                 bool dry) const {
+    const double* src = base + e * N;
+    if (!ODD) {
+      if (!dry) tma_load_1d(dst, src, N * 8, b);
+      return N * 8;
+    }
+    const int par = static_cast<int>(e & 1);
+    if (par == 0 && e + 1 == static_cast<size_t>(E)) {
+      if (!dry) {
+        tma_load_1d(dst, src, (N - 1) * 8, b);
+        dst[N - 1] = __ldg(src + N - 1);
+      }
+      return (N - 1) * 8;
+    }
+    if (!dry) tma_load_1d(dst, src - par, (N + 1) * 8, b);
+    return (N + 1) * 8;
+  }
   // bulk loads of one batch into buffer bi (thread 0)
   __device__ void issue(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int bi) {
     constexpr int NPE = C::NPE, M = C::M, MD = C::MD, D = C::D;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
-    unsigned bytes = nb * (NPE * M * 8) + nb * C::METP * 8 + nb * D * 2 * 8;
-    if (WQ) bytes += nb * (NPE * MD * 8);
     // element ids first: the bulk copies are asm volatile with a memory
     // clobber, so a load between them would wait out its full latency
     int ev_[EPB];
 #pragma unroll
     for (int le = 0; le < EPB; ++le) ev_[le] = le < nb ? __ldg(kp.order + k0 + le) : 0;
+    unsigned bytes = nb * C::METP * 8 + nb * D * 2 * 8;
+#pragma unroll
+    for (int le = 0; le < EPB; ++le) {
+      if (le >= nb) break;
+      const size_t e = static_cast<size_t>(ev_[le]);
+      bytes += load_block<ODDU>(nullptr, Ug, e, NPE * M, kp.E, nullptr, true);
+      if (WQ) bytes += load_block<ODDQ>(nullptr, Qg, e, NPE * MD, kp.E, nullptr, true);
+    }
     mbar_expect_tx(&bar[bi], bytes);
 #pragma unroll
     for (int le = 0; le < EPB; ++le) {
       if (le >= nb) break;
       const size_t e = static_cast<size_t>(ev_[le]);
-      tma_load_1d(bU(bi) + le * NPE * M, Ug + e * (NPE * M), NPE * M * 8, &bar[bi]);
-      if (WQ) tma_load_1d(bQ(bi) + le * NPE * MD, Qg + e * (NPE * MD), NPE * MD * 8, &bar[bi]);
+      eid(bi)[le] = ev_[le];
+      load_block<ODDU>(bU(bi) + le * US, Ug, e, NPE * M, kp.E, &bar[bi], false);
+      if (WQ) load_block<ODDQ>(bQ(bi) + le * QS, Qg, e, NPE * MD, kp.E, &bar[bi], false);
     }
     tma_load_1d(bMET(bi), kp.metric + static_cast<size_t>(k0) * C::METP, nb * C::METP * 8, &bar[bi]);
     tma_load_1d(bCONN(bi), kp.conn + static_cast<size_t>(k0) * D * 2, nb * D * 2 * 8, &bar[bi]);
   }
-  // synchronous fallback (element chunks not 16-byte aligned)
-  __device__ void load_sync(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int bi, int tid,
-                            int nthr) {
-    constexpr int NPE = C::NPE, M = C::M, MD = C::MD, D = C::D;
-    const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
-    for (int le = 0; le < nb; ++le) {
-      const size_t e = kp.order[k0 + le];
-      for (int i = tid; i < NPE * M; i += nthr) bU(bi)[le * NPE * M + i] = __ldg(Ug + e * (NPE * M) + i);
-      if (WQ)
-        for (int i = tid; i < NPE * MD; i += nthr) bQ(bi)[le * NPE * MD + i] = __ldg(Qg + e * (NPE * MD) + i);
-    }
-    for (int i = tid; i < nb * C::METP; i += nthr) bMET(bi)[i] = __ldg(kp.metric + static_cast<size_t>(k0) * C::METP + i);
-    for (int i = tid; i < nb * D * 2; i += nthr)
-      bCONN(bi)[i] = __ldg(kp.conn + static_cast<size_t>(k0) * D * 2 + i);
-    __syncthreads();
-  }
-  // neighbour traces of buffer bi (all threads; needs its connectivity)
+  // neighbour traces of buffer bi (all threads; connectivity from its ring slot)
   __device__ void gather(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int bi, int tid,
                          int nthr) {
     constexpr int NPE = C::NPE, M = C::M, MD = C::MD, D = C::D, NL = C::NL, LPE = C::LPE, NP = C::NP;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
-    const int2* sc = bCONN(bi);
+    const int2* sc = cring(bi);
     for (int w = tid; w < nb * LPE * 2; w += nthr) {
       const int side = w & 1, lw = w >> 1, le = lw / LPE, rem = lw - le * LPE;
       const int dir = rem / NL, line = rem - dir * NL;
@@ -717,38 +751,50 @@ struct BatchIO {
         for (int c = 0; c < MD; ++c) cp_async8(dq + c, Qg + nd * MD + c);
       }
     }
-    cp_async_commit();
   }
-  // prologue: batch b0 resident in buffer 0 (traces in flight), b0+G issued
+  // prologue: batches b0 and b0+G issued, their connectivity in the ring,
+  // the traces of b0 in flight
   __device__ void start(const KParams<C>& kp, const double* Ug, const double* Qg, int b0, int G, int nbatch, int tid,
                         int nthr) {
-    if (TMA) {
-      if (tid == 0) {
-        issue(kp, Ug, Qg, b0, 0);
-        if (b0 + G < nbatch) issue(kp, Ug, Qg, b0 + G, 1);
-      }
-      mbar_wait(&bar[0], 0);
-    } else {
-      load_sync(kp, Ug, Qg, b0, 0, tid, nthr);
+    constexpr int D = C::D;
+    if (tid == 0) {
+      issue(kp, Ug, Qg, b0, 0);
+      if (b0 + G < nbatch) issue(kp, Ug, Qg, b0 + G, 1);
     }
-    gather(kp, Ug, Qg, b0, 0, tid, nthr);
-  }
-  // epilogue of iteration `it` (batch `batch`): make the next batch resident,
-  // start its gathers, free buffer `cur` and refill it two batches ahead
-  __device__ void advance(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int it, int G,
-                          int nbatch, int tid, int nthr) {
-    const int cur = it & 1, nxt = cur ^ 1;
-    const int nbn = batch + G;
-    if (nbn < nbatch) {
-      if (TMA) mbar_wait(&bar[nxt], ((it + 1) >> 1) & 1);
-      else {
-        __syncthreads();
-        load_sync(kp, Ug, Qg, nbn, nxt, tid, nthr);
-      }
-      gather(kp, Ug, Qg, nbn, nxt, tid, nthr);
+    for (int s = 0; s < 2; ++s) {
+      const int b = b0 + s * G;
+      if (b >= nbatch) break;
+      const int k0 = b * EPB, nb = min(EPB, kp.E - k0);
+      for (int i = tid; i < nb * D * 2; i += nthr) cring(s)[i] = __ldg(kp.conn + static_cast<size_t>(k0) * D * 2 + i);
     }
     __syncthreads();
-    if (TMA && tid == 0 && batch + 2 * G < nbatch) issue(kp, Ug, Qg, batch + 2 * G, cur);
+    gather(kp, Ug, Qg, b0, 0, tid, nthr);
+    cp_async_commit();
+  }
+  // head of iteration `it` (batch `batch`): its traces and bulk data are
+  // resident on return; the gathers of the next batch (connectivity already
+  // in the ring) and the connectivity two batches ahead are in flight behind
+  // this batch's work
+  __device__ void begin(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int it, int G,
+                        int nbatch, int tid, int nthr) {
+    constexpr int D = C::D;
+    const int cur = it & 1, nxt = cur ^ 1;
+    cp_async_wait_all();
+    __syncthreads();
+    mbar_wait(&bar[cur], (it >> 1) & 1);
+    if (batch + G < nbatch) gather(kp, Ug, Qg, batch + G, nxt, tid, nthr);
+    if (batch + 2 * G < nbatch) {
+      const int k0 = (batch + 2 * G) * EPB, nb = min(EPB, kp.E - k0);
+      for (int i = tid; i < nb * D * 2; i += nthr) cp_async8(cring(cur) + i, kp.conn + static_cast<size_t>(k0) * D * 2 + i);
+    }
+    cp_async_commit();
+  }
+  // epilogue of iteration `it`: free buffer `cur` and refill it two batches ahead
+  __device__ void advance(const KParams<C>& kp, const double* Ug, const double* Qg, int batch, int it, int G,
+                          int nbatch, int tid, int nthr) {
+    const int cur = it & 1;
+    __syncthreads();
+    if (tid == 0 && batch + 2 * G < nbatch) issue(kp, Ug, Qg, batch + 2 * G, cur);
   }
 };
 
@@ -801,16 +847,19 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
   for (int i = tid; i < 2 * NP; i += nthr) smi[i] = (&kp.bt.mi[0][0])[i];
   __syncthreads();
   io.start(kp, U, Q, blockIdx.x, G, nbatch, tid, nthr);
-  __shared__ int sord[EPB];  // element ids of the batch (epilogue addresses)
   for (int batch = blockIdx.x, it = 0; batch < nbatch; batch += G, ++it) {
     const int cur = it & 1;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
-    cp_async_wait_all();
-    __syncthreads();
-    if (tid < nb) sord[tid] = __ldg(kp.order + k0 + tid);
+    io.begin(kp, U, Q, batch, it, G, nbatch, tid, nthr);
+    const int* sord = io.eid(cur);  // element ids of the batch (epilogue addresses)
     // ---- R2 (line ends) then R1 (quadrature points)
-    const int n2 = nb * LPE * 2, n1 = nb * LPE * NQ;
-    for (int w = tid; w < n2 + n1; w += nthr) {
+    // item space: the (heavier) line-end items padded to whole warps, then the
+    // quadrature-point items; rounds alternate the thread order so the ragged
+    // last round falls on the threads that had the lighter items
+    const int n2 = nb * LPE * 2, n2p = (n2 + 31) / 32 * 32, n1 = nb * LPE * NQ;
+    for (int base = 0, rnd = 0; base < n2p + n1; base += nthr, ++rnd) {
+      const int w = base + ((rnd & 1) ? nthr - 1 - tid : tid);
+      if (w >= n2p + n1 || (w >= n2 && w < n2p)) continue;
       bool ok = true;
       int le, dir, line;
       if (w < n2) {
@@ -820,8 +869,8 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
         dir = rem / NL;
         line = rem - dir * NL;
         const double* mk = io.bMET(cur) + le * C::METP;
-        const double* sul = io.bU(cur) + le * NPE * M;
-        const double* sql = io.bQ(cur) + le * NPE * MD;
+        const double* sul = io.pU(cur, le);
+        const double* sql = io.pQ(cur, le);
         const int2 cn = io.bCONN(cur)[(le * D + dir) * 2 + side];
         const int S = conn_sign(cn.y);
         const int nd = node_on_line<C>(dir, line, side ? P : 0);
@@ -866,14 +915,14 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
 #pragma unroll
         for (int c = 0; c < M; ++c) sFH[w * M + c] = fh[c];
       } else {
-        const int v = w - n2, lw = v / NQ, q = v - lw * NQ;
+        const int v = w - n2p, lw = v / NQ, q = v - lw * NQ;
         le = lw / LPE;
         const int rem = lw - le * LPE;
         dir = rem / NL;
         line = rem - dir * NL;
         const double* mk = io.bMET(cur) + le * C::METP;
-        const double* sul = io.bU(cur) + le * NPE * M;
-        const double* sql = io.bQ(cur) + le * NPE * MD;
+        const double* sul = io.pU(cur, le);
+        const double* sql = io.pQ(cur, le);
         double uq[M], qq[C::SECOND ? MD : 1];
 #pragma unroll
         for (int c = 0; c < M; ++c) uq[c] = 0.0;
@@ -908,7 +957,7 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
 #pragma unroll
         for (int c = 0; c < M; ++c) sF[v * M + c] = f[c];
       }
-      if (!ok) report_line<C>(kp, kp.order[k0 + le], dir, line, io.bU(cur) + le * NPE * M);
+      if (!ok) report_line<C>(kp, kp.order[k0 + le], dir, line, io.pU(cur, le));
     }
     __syncthreads();
     // ---- R3: dU/dt = S - (1/J) sum_dir r
@@ -987,20 +1036,18 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
   for (int i = tid; i < 2 * NP; i += nthr) smi[i] = (&kp.bt.mi[0][0])[i];
   __syncthreads();
   io.start(kp, U, nullptr, blockIdx.x, G, nbatch, tid, nthr);
-  __shared__ int sord[EPB];  // element ids of the batch (epilogue addresses)
   for (int batch = blockIdx.x, it = 0; batch < nbatch; batch += G, ++it) {
     const int cur = it & 1;
     const int k0 = batch * EPB, nb = min(EPB, kp.E - k0);
-    cp_async_wait_all();
-    __syncthreads();
-    if (tid < nb) sord[tid] = __ldg(kp.order + k0 + tid);
+    io.begin(kp, U, nullptr, batch, it, G, nbatch, tid, nthr);
+    const int* sord = io.eid(cur);  // element ids of the batch (epilogue addresses)
     // ---- G1: one (line, component) per item
     for (int v = tid; v < nb * LPE * M; v += nthr) {
       const int lw = v / M, c = v - lw * M;
       const int l = lw / LPE, rem = lw - l * LPE;
       const int dir = rem / NL, line = rem - dir * NL;
       const double* mk = io.bMET(cur) + l * C::METP;
-      const double* sul = io.bU(cur) + l * NPE * M;
+      const double* sul = io.pU(cur, l);
       const double* nvl = mk + (dir * NL + line) * NQ * D;
       double ul[NP];
 #pragma unroll
