@@ -133,6 +133,15 @@ constexpr int JAC_CHAINS = LDG_JAC_CHAINS;
   // 0 constant bank, 1 shared (scalar), 2 shared (pairs)
 // ---------------------------------------------------------------- helpers
 
+// f(integral_constant<int, 0>) ... f(integral_constant<int, N - 1>)
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
+
 template <class C>
 __device__ __forceinline__ int node_on_line(int dir, int line, int t) {
   constexpr int NP = C::NP;
@@ -2283,6 +2292,21 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     const int it = x / NQ8, q = x - it * NQ8;
     cc8[x] = q < NQ ? (&kp.bt.cc[0][0][0])[it * NQ + q] : 0.0;
   }
+#ifndef LDG_S3_FACT
+#define LDG_S3_FACT 1
+#endif
+  // Factored line-block coefficients (cc[i][t][q] = dq[i][q] phi[t][q]): the
+  // item scales its quadrature-point values by dq[i][.] once per line, then
+  // sum_q phi[t][q] g[q] takes phi as compile-time-indexed constant-bank
+  // operands (no shared-memory coefficient loads in the inner loop).
+  constexpr bool FACT = LDG_S3_FACT != 0;
+  auto phidot = [&](auto TC, const double* g) {
+    constexpr int t = decltype(TC)::value;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v += kp.bt.phi[t][q] * g[q];
+    return v;
+  };
   // sum_q cc[i][t][q] f[q] with 16-byte coefficient loads
   auto ccdot = [&](int i, int t, const double* f) {
     const double2* c2 = reinterpret_cast<const double2*>(cc8 + (i * NP + t) * NQ8);
@@ -2400,6 +2424,11 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const int ab = w % B11, i = w / B11;
           const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
           const size_t eoff = (static_cast<size_t>(ab / M) * NT) * M + ab % M;
+          double dqi[FACT ? NQ : 1];
+          if (FACT) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) dqi[q] = kp.bt.dq[i][q];
+          }
 #pragma unroll 1
           for (int j = 0; j < GL; ++j) {
             const int nd = node_on_line<C>(dir, g0 + j, i);
@@ -2407,11 +2436,14 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
             const double e0 = sg[ab * SLS + j], e1 = sg[ab * SLS + GL + j];
             double av[NQ8];
 #pragma unroll
-            for (int q = 0; q < NQ8; ++q) av[q] = (VOL11 && q < NQ) ? avq(pA, pAv, j, q, ab) : 0.0;
+            for (int q = 0; q < NQ8; ++q) {
+              av[q] = (VOL11 && q < NQ) ? avq(pA, pAv, j, q, ab) : 0.0;
+              if (FACT && q < NQ) av[q] *= dqi[q];
+            }
             double* rowp = K11e + static_cast<size_t>(nd / NT) * SM::ST11 + eoff + static_cast<size_t>(nd % NT) * M;
-#pragma unroll
-            for (int t = 0; t < NP; ++t) {
-              double v = VOL11 ? ccdot(i, t, av) : 0.0;
+            static_for<NP>([&](auto TC) {
+              constexpr int t = decltype(TC)::value;
+              double v = !VOL11 ? 0.0 : (FACT ? phidot(TC, av) : ccdot(i, t, av));
               if (t == 0) v += li0 * e0;
               if (t == P) v += li1 * e1;
               if (t == i) {
@@ -2420,11 +2452,11 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
                 if (dir == 2) *sp = v;
                 else if (dir == 1) *sp += v;
                 else rowp[static_cast<size_t>(t) * NT * B11] = sc * (v + *sp);
-                continue;
+                return;
               }
               const int slot = dir == 0 ? t : NP + (dir - 1) * P + (t < i ? t : t - 1);
               rowp[static_cast<size_t>(slot) * NT * B11] = sc * v;
-            }
+            });
             rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] =
                 c0.x >= 0 ? sc * (li0 * sg[(B11 + ab) * SLS + j]) : 0.0;
             rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] =
@@ -2439,19 +2471,27 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
           const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
           const size_t eoff = (static_cast<size_t>(ab / MD) * NT) * MD + ab % MD;
+          double dqi[FACT ? NQ : 1];
+          if (FACT) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) dqi[q] = kp.bt.dq[i][q];
+          }
 #pragma unroll 1
           for (int j = 0; j < GL; ++j) {
             const int nd = node_on_line<C>(dir, g0 + j, i);
             const double sc = -mk[C::MET_NV + C::MET_NE + nd];
             double bv[NQ8];
 #pragma unroll
-            for (int q = 0; q < NQ8; ++q) bv[q] = q < NQ ? pBq[(j * NQ + q) * M * MD + a * MD + b] : 0.0;
+            for (int q = 0; q < NQ8; ++q) {
+              bv[q] = q < NQ ? pBq[(j * NQ + q) * M * MD + a * MD + b] : 0.0;
+              if (FACT && q < NQ) bv[q] *= dqi[q];
+            }
             const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + j];
             const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + GL + j];
             double* rowp = K12e + static_cast<size_t>(nd / NT) * SM::ST12 + eoff + static_cast<size_t>(nd % NT) * MD;
-#pragma unroll
-            for (int t = 0; t < NP; ++t) {
-              double v = ccdot(i, t, bv);
+            static_for<NP>([&](auto TC) {
+              constexpr int t = decltype(TC)::value;
+              double v = FACT ? phidot(TC, bv) : ccdot(i, t, bv);
               if (t == 0 && own0) v += li0 * eq0;
               if (t == P && own1) v += li1 * eq1;
               if (t == i) {
@@ -2459,11 +2499,11 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
                 if (dir == 2) *sp = v;
                 else if (dir == 1) *sp += v;
                 else rowp[static_cast<size_t>(t) * NT * B12] = sc * (v + *sp);
-                continue;
+                return;
               }
               const int slot = dir == 0 ? t : NP + (dir - 1) * P + (t < i ? t : t - 1);
               rowp[static_cast<size_t>(slot) * NT * B12] = sc * v;
-            }
+            });
             double nbv = 0.0;
             if (!own0) nbv = sc * (li0 * eq0);
             if (!own1) nbv = sc * (li1 * eq1);
