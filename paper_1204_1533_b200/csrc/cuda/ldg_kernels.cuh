@@ -1210,6 +1210,13 @@ struct EndJac {
   static constexpr int items(int seeds) { return 2 * ((C::M + seeds - 1) / seeds) + (C::SECOND ? 1 : 0); }
 };
 
+// Effective scratch layout of a configuration (defined after the assembly
+// kernels' shared-memory plans): entry-major (above) or, for the 3-D
+// line-streaming assembly, group-major -- the line ends of one group of lines
+// contiguous, so that k_jac_s3 fetches a group with one bulk copy.
+template <class C>
+struct SeLay;
+
 // Line-end index functors for jac_tile: whole-element scratch block (k_endjac
 // layout, persistent kernel) and tile-line staging (k_jacobian).
 template <class C>
@@ -1245,7 +1252,8 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   // in/out swapped, into the partner's line end: the numerical flux is
   // conservative, Fh(u_o, u_i, -n) = -Fh(u_i, u_o, n) (Riemann, LDG switch
   // (S flips across a face) and penalty terms alike).
-  constexpr int LS = EJ::LS;
+  using SL = SeLay<C>;
+  constexpr int LS = SL::ES;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= (o_end - o_begin) * NL * IPS) return;
   const int line = static_cast<int>(item % NL);
@@ -1261,7 +1269,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   const bool bd = cn.x < 0;
   const int S = conn_sign(cn.y);
   const int nd = node_on_line<C>(dir, line, side ? P : 0);
-  double* slot = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM + gs;  // entry o at slot[o * LS]
+  double* slot = SE + static_cast<size_t>(k - k_begin) * SL::PER_ELEM + SL::base(dir, side, line);  // entry o at slot[o * LS]
   // partner line end (same chunk only): pass 0 <-> pass 1, all entries negated
   double* pslot = nullptr;
   if (kp.owned && !bd) {
@@ -1269,7 +1277,7 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     if (fp.x >= k_begin && fp.x < k_end) {
       int pl, ppos;
       line_of<C>(fp.y >> 1, conn_node(cn.y, line, NP), pl, ppos);
-      pslot = SE + static_cast<size_t>(fp.x - k_begin) * EJ::PER_ELEM + fp.y * NL + pl;
+      pslot = SE + static_cast<size_t>(fp.x - k_begin) * SL::PER_ELEM + SL::base(fp.y >> 1, fp.y & 1, pl);
     }
   }
   auto put = [&](int ps, int o, double v) {
@@ -2241,8 +2249,12 @@ struct JacS3 {
   static constexpr int GL = C::SECOND ? NP : C::NL;
   static constexpr int NG = C::NL / GL;                // groups per direction
   static constexpr int NPT = GL * NQ;                  // quadrature points per group
+  // inviscid + viscous d/du Jacobians of a point are summed by the one
+  // phase-P item that computes both (MERGE): one buffer, one load per point
+  // and entry in phase X
+  static constexpr bool MERGE = C::HAS_INV && C::VIS_U;
   static constexpr int A = C::HAS_INV ? NPT * B11 : 0;
-  static constexpr int AV = C::VIS_U ? NPT * B11 : 0;
+  static constexpr int AV = (C::VIS_U && !MERGE) ? NPT * B11 : 0;
   static constexpr int BQ = C::SECOND ? NPT * M * MD : 0;
   static constexpr int PTS = ev(A + AV + BQ);          // one buffer
   static constexpr int SLS = 2 * GL + 1;               // line-end stride of the group scratch
@@ -2258,6 +2270,21 @@ struct JacS3 {
   static constexpr int TOTAL = U + Q + MET + S11 + S12 + 2 * PTS + 2 * SEG + TAB + CC8;
   static constexpr int THREADS = 512;
   static constexpr bool OK = C::D == 3 && 8LL * TOTAL <= 220 * 1024;
+};
+
+template <class C>
+struct SeLay {
+  using EJ = EndJac<C>;
+  using S3 = JacS3<C>;
+  // group-major for the configurations k_jac_s3 assembles (Launch::JAC_KIND == 1)
+  static constexpr bool GM = !JacP<C>::OK && C::D == 3 && C::WU != 0 && S3::OK;
+  static constexpr int GBLK = S3::SEG;  // one group: [entry][side * GL + j], entry stride SLS (padded)
+  static constexpr int PER_ELEM = GM ? C::D * S3::NG * GBLK : EJ::PER_ELEM;
+  static constexpr int ES = GM ? S3::SLS : EJ::LS;  // stride between the entries of a line end
+  __host__ __device__ static constexpr int base(int dir, int side, int line) {
+    return GM ? (dir * S3::NG + line / S3::GL) * GBLK + side * S3::GL + line % S3::GL
+              : (dir * 2 + side) * C::NL + line;
+  }
 };
 
 template <class C>
@@ -2320,6 +2347,13 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     return v;
   };
   __shared__ int2 scon[2 * D];
+  __shared__ __align__(8) uint64_t sbar[2];  // one per scratch buffer
+  unsigned sph = 0;                          // their phase parities (bit per buffer)
+  if (tid == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+    mbar_fence_init();
+  }
   // group gi = (pass dd, group g): direction 2 - dd, lines g*GL + j
   auto gdir = [](int gi) { return 2 - gi / NG; };
   auto gline = [](int gi, int j) { return (gi % NG) * GL + j; };
@@ -2338,15 +2372,20 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       if (tid < 2 * D) scon[tid] = __ldg(&kp.conn[static_cast<size_t>(k) * D * 2 + tid]);
       cp_async_commit();
     }
-    const double* seel = SE + static_cast<size_t>(k - k_begin) * EJ::PER_ELEM;
-    // endpoint scratch of group gi -> buffer: [off][side*GL + j] (stride SLS)
-    auto gather = [&](int gi, double* dst) {
-      const int dir = gdir(gi);
-      for (int w = tid; w < EJ::SLOT * 2 * GL; w += nthr) {
-        const int o = w / (2 * GL), sj = w - o * (2 * GL), side = sj / GL, j = sj - side * GL;
-        cp_async8(dst + o * SLS + sj, seel + o * EJ::LS + (dir * 2 + side) * NL + gline(gi, j));
+    const double* seel = SE + static_cast<size_t>(k - k_begin) * SeLay<C>::PER_ELEM;
+    // endpoint scratch of group gi -> buffer bi: [off][side*GL + j] (stride
+    // SLS), one bulk copy of the group's contiguous scratch block
+    auto gather = [&](int gi, int bi) {
+      if (tid == 0) {
+        mbar_expect_tx(&sbar[bi], S3::SEG * 8);
+        tma_load_1d(seg0 + bi * S3::SEG, seel + static_cast<size_t>(gdir(gi) * NG + gi % NG) * S3::SEG, S3::SEG * 8,
+                    &sbar[bi]);
       }
-      cp_async_commit();
+    };
+    // every thread waits for the group's block (acquires the async-proxy writes)
+    auto gwait = [&](int bi) {
+      mbar_wait(&sbar[bi], (sph >> bi) & 1u);
+      sph ^= 1u << bi;
     };
     // phase P of group gi -> buffer
     auto phaseP = [&](int gi, double* pb) {
@@ -2355,12 +2394,13 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       double* pAv = pA + S3::A;
       double* pBq = pAv + S3::AV;
       // item kinds present: A (inviscid), Av (viscous d/du), Bq (viscous d/dq)
-      constexpr int KA = C::HAS_INV ? 1 : 0, KV = C::VIS_U ? 1 : 0, KB = C::SECOND ? 1 : 0;
+      constexpr bool MG = S3::MERGE;
+      constexpr int KA = C::HAS_INV ? 1 : 0, KV = (C::VIS_U && !MG) ? 1 : 0, KB = C::SECOND ? 1 : 0;
       constexpr int KINDS = KA + KV + KB;
       // on the highest thread ids: phase X leaves them one item fewer
       for (int w = nthr - 1 - tid; w < GL * NQ * KINDS; w += nthr) {
         const int kind = w / (GL * NQ), pt = w - kind * (GL * NQ), j = pt / NQ, q = pt - j * NQ;
-        const bool isA = KA && kind == 0, isV = KV && kind == KA;
+        const bool isA = KA && kind == 0, isV = MG ? isA : (KV && kind == KA);
         const int line = gline(gi, j);
         double nv[D], uq[M], qq[C::SECOND ? MD : 1];
 #pragma unroll
@@ -2383,7 +2423,13 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           }
         }
         bool ok = true;
-        if (isA) {
+        if (MG && isA) {
+          euler_jac_n<D>(uq, nv, kp.pp.gamma, pA + pt * B11, ok);
+          double Jv[M * M];
+          visc_du<D, C::PH>(uq, qq, nv, kp.pp, Jv, ok);
+#pragma unroll
+          for (int c = 0; c < M * M; ++c) pA[pt * B11 + c] += Jv[c];
+        } else if (isA) {
           if (C::HAS_INV) euler_jac_n<D>(uq, nv, kp.pp.gamma, pA + pt * B11, ok);
         } else if (isV) {
           double Jv[M * M];
@@ -2400,6 +2446,7 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       }
     };
     auto avq = [&](const double* pA, const double* pAv, int j, int q, int ab) {
+      if (S3::MERGE) return pA[(j * NQ + q) * B11 + ab];
       return (C::HAS_INV ? pA[(j * NQ + q) * B11 + ab] : 0.0) + (C::VIS_U ? pAv[(j * NQ + q) * B11 + ab] : 0.0);
     };
     // phase X of group gi from buffers pb (quadrature points) and sg (scratch).
@@ -2516,14 +2563,14 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     // ---- pipeline over the 3*NG groups
     cp_async_wait_all();
     __syncthreads();  // element inputs + tables
-    gather(0, seg0);
+    gather(0, 0);
     phaseP(0, pts0);
-    cp_async_wait_all();
+    gwait(0);
     __syncthreads();
     constexpr int NGT = 3 * NG;
     for (int gi = 0; gi < NGT; ++gi) {
       const int cb = gi & 1, nb = cb ^ 1;
-      if (gi + 1 < NGT) gather(gi + 1, seg0 + nb * S3::SEG);
+      if (gi + 1 < NGT) gather(gi + 1, nb);
       {
         const double* pb = pts0 + cb * S3::PTS;
         const double* sgb = seg0 + cb * S3::SEG;
@@ -2537,7 +2584,7 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         }
       }
       if (gi + 1 < NGT) phaseP(gi + 1, pts0 + nb * S3::PTS);
-      cp_async_wait_all();
+      if (gi + 1 < NGT) gwait(nb);
       __syncthreads();
     }
   }

@@ -140,7 +140,10 @@ struct Launch {
   // is long (second-order physics: viscous fluxes and the gradient at every
   // point); the thread-per-line kernel k_residual_p wins for Euler.
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
-    if (C::SECOND) return residual_f(d, U, Q, R);
+#ifndef LDG_RES_F_FIRST
+#define LDG_RES_F_FIRST 0
+#endif
+    if (C::SECOND || LDG_RES_F_FIRST) return residual_f(d, U, Q, R);
     using RP = ResP<C, EPB>;
     const size_t smem = sizeof(double) * RP::TOTAL;
     const int grid_max = persistent_grid(reinterpret_cast<const void*>(k_residual_p<C, EPB>), RP::THREADS, smem);
@@ -180,7 +183,7 @@ struct Launch {
   // (kernel ramps and tails per chunk outweigh the scratch re-read; C2 one
   // chunk 0.252 vs 0.262 ms, C4 17.1 vs 18.3 ms).
   static int chunk_elems(int E) {
-    const long long per = static_cast<long long>(EndJac<C>::PER_ELEM) * 8;
+    const long long per = static_cast<long long>(SeLay<C>::PER_ELEM) * 8;
     long long n = (512LL << 20) / (per > 0 ? per : 1);
     if (n < 1024) n = 1024;
     return static_cast<int>(n < E ? n : E);
@@ -241,7 +244,7 @@ struct Launch {
     }
     return cudaGetLastError();
   }
-  static size_t scratch_elems(int E) { return static_cast<size_t>(chunk_elems(E)) * EndJac<C>::PER_ELEM; }
+  static size_t scratch_elems(int E) { return static_cast<size_t>(chunk_elems(E)) * SeLay<C>::PER_ELEM; }
   static cudaError_t k21(const DevCtx& d, double* K21) {
     if (!C::SECOND) return cudaSuccess;
     k_k21<C><<<d.E * C::UPE, 128, 0, d.stream>>>(params(d), K21);
@@ -346,7 +349,7 @@ struct Launch {
   static const Ops* table() {
     static const Ops ops = {C::D, C::P, C::PH, C::RI, C::M, C::NP, C::NQ, C::NPE, C::NL, C::MD,
                             C::NS11, C::NS12, C::B11, C::B12, C::R12, C::NT, C::TPE, C::METP,
-                            C::MET_NV, C::MET_NE, jac_smem(), EndJac<C>::PER_ELEM, scratch_elems, chunk_elems, residual, gradient, jacobian, k21,
+                            C::MET_NV, C::MET_NE, jac_smem(), SeLay<C>::PER_ELEM, scratch_elems, chunk_elems, residual, gradient, jacobian, k21,
                             spmv11, spmv11_zc, spmv12, spmv21, split, PcCfg<C>::OK ? PcCfg<C>::NE : 0, pc_build, pc_apply,
                             PcLine<C>::OK ? PcLine<C>::NB : 0, pc_line_build, pc_line_apply};
     return &ops;
