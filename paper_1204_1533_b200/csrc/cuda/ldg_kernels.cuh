@@ -2468,7 +2468,10 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       for (int w = tid; w < N11 + N12; w += nthr) {
         if (w < N11) {
           // ---- K11: row position i, entry ab = a*M + b, all GL lines of the group
-          const int ab = w % B11, i = w / B11;
+          // lanes run over (a, i, b): for dir 0 the NP rows of a line are
+          // consecutive rows of one tile, so a (slot, a) run of NP * M
+          // doubles is written by consecutive lanes
+          const int a_ = w / (NP * M), r_ = w - a_ * (NP * M), i = r_ / M, ab = a_ * M + (r_ - i * M);
           const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
           const size_t eoff = (static_cast<size_t>(ab / M) * NT) * M + ab % M;
           double dqi[FACT ? NQ : 1];
@@ -2512,7 +2515,7 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         } else if (C::SECOND) {
           // ---- K12: row position i, stored entry ab = a' * MD + b, all GL lines
           const int v12 = w - N11;
-          const int ab = v12 % B12, i = v12 / B12;
+          const int a_ = v12 / (NP * MD), r_ = v12 - a_ * (NP * MD), i = r_ / MD, ab = a_ * MD + (r_ - i * MD);
           const int a = ab / MD + A0, b = ab % MD;
           const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
           const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
@@ -2559,6 +2562,118 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         }
       }
     };
+    // phase X for directions 1 and 2: the NP rows of a line lie in NP
+    // different tiles, but the lines of a group are consecutive rows of each
+    // of them.  One thread owns a (line j of the group, block entry) pair with
+    // lanes running over (a, j, b) -- consecutive lanes write a contiguous
+    // (slot, a) run -- and walks the line's NP row positions: the line's
+    // quadrature-point values and endpoint entries are loaded once.
+    auto phaseXL = [&](auto DIRC, int gi, const double* pb, const double* sg) {
+      constexpr int dir = decltype(DIRC)::value;
+      static_assert(dir == 1 || dir == 2, "phaseXL: directions 1 and 2");
+      const double* pA = pb;
+      const double* pAv = pA + S3::A;
+      const double* pBq = pAv + S3::AV;
+      const int2 c0 = scon[dir * 2 + 0], c1 = scon[dir * 2 + 1];
+      const int g0 = (gi % NG) * GL;  // first line of the group
+      constexpr int N11 = GL * B11;
+      constexpr int N12 = C::SECOND ? GL * B12 : 0;
+      constexpr bool TLINE = NT == NP;  // store tile: a dir-0 line of rows, else an x2 slab
+      constexpr int NDS = dir == 1 ? NP : NP * NP;  // node stride along the line
+      constexpr size_t RS11 = TLINE ? (dir == 1 ? size_t(SM::ST11) : size_t(NP) * SM::ST11)
+                                    : (dir == 1 ? size_t(NP) * M : size_t(SM::ST11));
+      constexpr size_t RS12 = TLINE ? (dir == 1 ? size_t(SM::ST12) : size_t(NP) * SM::ST12)
+                                    : (dir == 1 ? size_t(NP) * MD : size_t(SM::ST12));
+      double* const K11e = K11 + static_cast<size_t>(k) * C::TPE * SM::ST11;
+      double* const K12e = C::SECOND ? K12 + static_cast<size_t>(k) * C::TPE * SM::ST12 : nullptr;
+      for (int w = tid; w < N11 + N12; w += nthr) {
+        if (w < N11) {
+          const int jh = w / (NP * B11), r1 = w - jh * (NP * B11), a = r1 / (NP * M), r2 = r1 - a * (NP * M),
+                    jl = r2 / M, b = r2 - jl * M;
+          const int j = jh * NP + jl, ab = a * M + b;
+          const int line = g0 + j, l1 = line % NP, l2 = line / NP;
+          const int nd0 = dir == 1 ? l1 + NP * NP * l2 : l1 + NP * l2;
+          const int t0 = TLINE ? (dir == 1 ? NP * l2 : l2) : (dir == 2 ? 0 : l2);
+          const int r0 = TLINE ? l1 : (dir == 1 ? l1 : l1 + NP * l2);
+          double* rowp = K11e + static_cast<size_t>(t0) * SM::ST11 + (static_cast<size_t>(a) * NT + r0) * M + b;
+          const double* mks = mk + C::MET_NV + C::MET_NE + nd0;
+          double* sp = self11 + nd0 * B11 + ab;
+          double av[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(pA, pAv, j, q, ab) : 0.0;
+          const double e0 = sg[ab * SLS + j], e1 = sg[ab * SLS + GL + j];
+          const double eo0 = sg[(B11 + ab) * SLS + j], eo1 = sg[(B11 + ab) * SLS + GL + j];
+#pragma unroll 1
+          for (int i = 0; i < NP; ++i, rowp += RS11, sp += NDS * B11) {
+            const double sc = -mks[i * NDS];
+            const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
+            double g[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) g[q] = av[q] * kp.bt.dq[i][q];
+            static_for<NP>([&](auto TC) {
+              constexpr int t = decltype(TC)::value;
+              double v = VOL11 ? phidot(TC, g) : 0.0;
+              if (t == 0) v += li0 * e0;
+              if (t == P) v += li1 * e1;
+              if (t == i) {
+                // self block: dir 2 starts it, dir 1 adds (dir 0 completes and stores)
+                if (dir == 2) *sp = v;
+                else *sp += v;
+                return;
+              }
+              const int slot = NP + (dir - 1) * P + (t < i ? t : t - 1);
+              rowp[static_cast<size_t>(slot) * NT * B11] = sc * v;
+            });
+            rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] = c0.x >= 0 ? sc * (li0 * eo0) : 0.0;
+            rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] = c1.x >= 0 ? sc * (li1 * eo1) : 0.0;
+          }
+        } else if (C::SECOND) {
+          const int v12 = w - N11;
+          const int jh = v12 / (NP * B12), r1 = v12 - jh * (NP * B12), a_ = r1 / (NP * MD),
+                    r2 = r1 - a_ * (NP * MD), jl = r2 / MD, b = r2 - jl * MD;
+          const int j = jh * NP + jl, ab = a_ * MD + b, a = a_ + A0;
+          const int line = g0 + j, l1 = line % NP, l2 = line / NP;
+          const int nd0 = dir == 1 ? l1 + NP * NP * l2 : l1 + NP * l2;
+          const int t0 = TLINE ? (dir == 1 ? NP * l2 : l2) : (dir == 2 ? 0 : l2);
+          const int r0 = TLINE ? l1 : (dir == 1 ? l1 : l1 + NP * l2);
+          double* rowp = K12e + static_cast<size_t>(t0) * SM::ST12 + (static_cast<size_t>(a_) * NT + r0) * MD + b;
+          const double* mks = mk + C::MET_NV + C::MET_NE + nd0;
+          double* sp = self12 + nd0 * B12 + ab;
+          const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
+          const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
+          double bv[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) bv[q] = pBq[(j * NQ + q) * M * MD + a * MD + b];
+          const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + j];
+          const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + GL + j];
+#pragma unroll 1
+          for (int i = 0; i < NP; ++i, rowp += RS12, sp += NDS * B12) {
+            const double sc = -mks[i * NDS];
+            const double li0 = smi[i * 2 + 0], li1 = smi[i * 2 + 1];
+            double g[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) g[q] = bv[q] * kp.bt.dq[i][q];
+            static_for<NP>([&](auto TC) {
+              constexpr int t = decltype(TC)::value;
+              double v = phidot(TC, g);
+              if (t == 0 && own0) v += li0 * eq0;
+              if (t == P && own1) v += li1 * eq1;
+              if (t == i) {
+                if (dir == 2) *sp = v;
+                else *sp += v;
+                return;
+              }
+              const int slot = NP + (dir - 1) * P + (t < i ? t : t - 1);
+              rowp[static_cast<size_t>(slot) * NT * B12] = sc * v;
+            });
+            double nbv = 0.0;
+            if (!own0) nbv = sc * (li0 * eq0);
+            if (!own1) nbv = sc * (li1 * eq1);
+            rowp[static_cast<size_t>(D * P + 1 + dir) * NT * B12] = nbv;
+          }
+        }
+      }
+    };
     (void)sccd;
     // ---- pipeline over the 3*NG groups
     cp_async_wait_all();
@@ -2579,8 +2694,8 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
         // contraction, bounds this phase; commit 101d93b)
         switch (gdir(gi)) {
           case 0: phaseX(std::integral_constant<int, 0>{}, gi, pb, sgb); break;
-          case 1: phaseX(std::integral_constant<int, 1>{}, gi, pb, sgb); break;
-          default: phaseX(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
+          case 1: phaseXL(std::integral_constant<int, 1>{}, gi, pb, sgb); break;
+          default: phaseXL(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
         }
       }
       if (gi + 1 < NGT) phaseP(gi + 1, pts0 + nb * S3::PTS);
