@@ -1254,6 +1254,10 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   // (S flips across a face) and penalty terms alike).
   using SL = SeLay<C>;
   constexpr int LS = SL::ES;
+  // unroll factor of the dual-number seed loop: rolled for the 3-D
+  // second-order operators (instruction-cache bound: C5 Jacobian -1 ms;
+  // neutral for C2)
+  constexpr int EJ_SU = (C::D == 3 && C::SECOND) ? 1 : SEEDS;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= (o_end - o_begin) * NL * IPS) return;
   const int line = static_cast<int>(item % NL);
@@ -1387,7 +1391,7 @@ static constexpr int LDG_EJ_DUALN = 0;  // all M seeds in one Dual<M> evaluation
 #pragma unroll
       for (int c = 0; c < ((LLFC || VCF) ? M * M : 0); ++c) put(pass, c, Jx[c]);
     } else
-#pragma unroll
+#pragma unroll EJ_SU
     for (int j = 0; j < SEEDS; ++j) {
       const int b = (LLFC || VCF) ? j : g0 + j;
       if (b >= M) break;

@@ -4,6 +4,6 @@
 set -e
 name=$1; flags=$2
 mkdir -p var build/var
-nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr -diag-suppress 177 $flags -c paper_1204_1533_b200/csrc/cuda/inst_d3_p4.cu -o build/var/d3p4_$name.o 2>/dev/null
-objs=$(ls build/obj/cuda/*.o | grep -v inst_d3_p4)
+nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr -diag-suppress 177 $flags -c paper_1204_1533_b200/csrc/cuda/inst_${3:-d3_p4}.cu -o build/var/d3p4_$name.o
+objs=$(ls build/obj/cuda/*.o | grep -v inst_${3:-d3_p4})
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o var/$name.so $objs build/var/d3p4_$name.o -lcudart
