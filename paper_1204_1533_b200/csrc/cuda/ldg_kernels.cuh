@@ -1258,12 +1258,33 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   // second-order operators (instruction-cache bound: C5 Jacobian -1 ms;
   // neutral for C2)
   constexpr int EJ_SU = (C::D == 3 && C::SECOND) ? 1 : SEEDS;
-  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (item >= (o_end - o_begin) * NL * IPS) return;
-  const int line = static_cast<int>(item % NL);
-  const int64_t rest = item / NL;
-  const int sub = static_cast<int>(rest % IPS);
-  const int64_t fi = rest / IPS;
+  // GMW (group-major scratch, all seeds per item): one warp per (face, pass
+  // item), lanes over the face's NL line ends; a lane's B11 entries go through
+  // a per-warp shared-memory stage and leave as one contiguous run per line
+  // end, written by consecutive lanes (flush).
+  constexpr bool GMW = SL::GM && !BND && SEEDS >= M;
+  static_assert(!GMW || (NL <= 32 && B11 <= 32 && EJ::EQS % B11 == 0), "k_endjac: warp-per-face mapping");
+  __shared__ double stage_all[GMW ? (128 / 32) * 32 * B11 : 1];
+  const int lane = threadIdx.x & 31;
+  double* const stg = stage_all + (GMW ? (threadIdx.x >> 5) * 32 * B11 : 0);
+  int line, sub;
+  int64_t fi;
+  bool act = true;
+  if (GMW) {
+    const int64_t wg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (wg >= (o_end - o_begin) * IPS) return;  // the whole warp
+    sub = static_cast<int>(wg % IPS);
+    fi = wg / IPS;
+    act = lane < NL;
+    line = act ? lane : 0;  // spare lanes shadow line end 0 (their results are not flushed)
+  } else {
+    const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (item >= (o_end - o_begin) * NL * IPS) return;
+    line = static_cast<int>(item % NL);
+    const int64_t rest = item / NL;
+    sub = static_cast<int>(rest % IPS);
+    fi = rest / IPS;
+  }
   const int fc = flist ? __ldg(flist + o_begin + fi) : static_cast<int>(k_begin * 2 * D + fi);
   const int k = fc / (2 * D), ds = fc - k * 2 * D, dir = ds >> 1, side = ds & 1;
   const int gs = ds * NL + line;
@@ -1276,17 +1297,44 @@ k_endjac(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   double* slot = SE + static_cast<size_t>(k - k_begin) * SL::PER_ELEM + SL::base(dir, side, line);  // entry o at slot[o * LS]
   // partner line end (same chunk only): pass 0 <-> pass 1, all entries negated
   double* pslot = nullptr;
-  if (kp.owned && !bd) {
-    const int2 fp = __ldg(&kp.fpart[static_cast<size_t>(k) * 2 * D + ds]);
-    if (fp.x >= k_begin && fp.x < k_end) {
-      int pl, ppos;
-      line_of<C>(fp.y >> 1, conn_node(cn.y, line, NP), pl, ppos);
-      pslot = SE + static_cast<size_t>(fp.x - k_begin) * SL::PER_ELEM + SL::base(fp.y >> 1, fp.y & 1, pl);
-    }
+  int2 fp = make_int2(-1, 0);
+  if (kp.owned && !bd) fp = __ldg(&kp.fpart[static_cast<size_t>(k) * 2 * D + ds]);
+  const bool part = fp.x >= k_begin && fp.x < k_end;  // (false without face sharing / on boundaries: fp.x = -1)
+  int poff = 0;  // the partner line end's offset in its element's scratch block
+  if (part) {
+    int pl, ppos;
+    line_of<C>(fp.y >> 1, conn_node(cn.y, line, NP), pl, ppos);
+    poff = SL::base(fp.y >> 1, fp.y & 1, pl);
+    pslot = SE + static_cast<size_t>(fp.x - k_begin) * SL::PER_ELEM + poff;
   }
   auto put = [&](int ps, int o, double v) {
+    if (GMW) {
+      stg[lane * B11 + o] = v;  // (passes 0 and 1; pass 2 stages its chunks itself)
+      return;
+    }
     slot[(ps * B11 + o) * LS] = v;
     if (pslot) pslot[((ps == 2 ? 2 : 1 - ps) * B11 + o) * LS] = -v;
+  };
+  // GMW: the warp's staged entries [lane][B11] -> entries off .. off + B11 of
+  // pass ps of the face's NL line ends, and, negated with in/out swapped, of
+  // the partner face's
+  auto flush = [&](int ps, int off) {
+    __syncwarp();
+    const int ln = lane < B11 ? lane : 0;
+    double* const own = SE + static_cast<size_t>(k - k_begin) * SL::PER_ELEM + ps * B11 + off + ln;
+    double* const pel =
+        part ? SE + static_cast<size_t>(fp.x - k_begin) * SL::PER_ELEM + (ps == 2 ? 2 : 1 - ps) * B11 + off + ln
+             : nullptr;
+#pragma unroll 5
+    for (int it = 0; it < NL; ++it) {
+      const int po = __shfl_sync(0xffffffffu, poff, it);
+      const double v = stg[it * B11 + ln];
+      if (lane < B11) {
+        own[SL::base(dir, side, it)] = v;
+        if (part) pel[po] = -v;
+      }
+    }
+    __syncwarp();
   };
   int pass, g0;
   if (sub < NSP) {
@@ -1439,6 +1487,7 @@ static constexpr int LDG_EJ_DUALN = 0;  // all M seeds in one Dual<M> evaluation
       for (int c = 0; c < M; ++c)
         put(pass, c * M + b, fh[c].d[0] + ((LLFC || VCF) ? Jx[(c * M + b) % ((LLFC || VCF) ? M * M : 1)] : 0.0));
     }
+    if (GMW) flush(pass, 0);
   } else if (C::SECOND) {
     // dF_vis/dq of the switch-selected side, closed form (visc_dq)
     const bool out = !bd && S > 0;
@@ -1447,10 +1496,20 @@ static constexpr int LDG_EJ_DUALN = 0;  // all M seeds in one Dual<M> evaluation
     for (int c = 0; c < M; ++c) usrc[c] = out ? uov[c] : uiv[c];
     double L[M * MD];
     visc_dq<D, C::PH>(usrc, n, kp.pp, L, ok);
+    if (GMW) {
 #pragma unroll
-    for (int c = 0; c < M * MD; ++c) put(2, c, (bneu || (bnos && c / MD == M - 1)) ? 0.0 : L[c]);
+      for (int ch = 0; ch < (M * MD) / B11; ++ch) {
+#pragma unroll
+        for (int c = 0; c < B11; ++c)
+          stg[lane * B11 + c] = (bneu || (bnos && (ch * B11 + c) / MD == M - 1)) ? 0.0 : L[ch * B11 + c];
+        flush(2, ch * B11);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < M * MD; ++c) put(2, c, (bneu || (bnos && c / MD == M - 1)) ? 0.0 : L[c]);
+    }
   }
-  if (!ok) {
+  if (!ok && act) {
     // a non-physical state at this line end: report the offending nodal state
     double m2 = 0.0;
 #pragma unroll
@@ -2261,8 +2320,8 @@ struct JacS3 {
   static constexpr int AV = (C::VIS_U && !MERGE) ? NPT * B11 : 0;
   static constexpr int BQ = C::SECOND ? NPT * M * MD : 0;
   static constexpr int PTS = ev(A + AV + BQ);          // one buffer
-  static constexpr int SLS = 2 * GL + 1;               // line-end stride of the group scratch
-  static constexpr int SEG = ev(SLS * EndJac<C>::SLOT); // one buffer
+  static constexpr int SLS = 2 * GL;                   // line ends of a group (two sides)
+  static constexpr int SEG = ev(SLS * EndJac<C>::SLOT); // one buffer: [side * GL + j][entry]
   static constexpr int U = ev(C::NPE * M);
   static constexpr int Q = C::SECOND ? ev(C::NPE * MD) : 0;
   static constexpr int MET = ev(C::METP);
@@ -2271,7 +2330,8 @@ struct JacS3 {
   static constexpr int TAB = JacSmem<C>::TABD;         // cc[p][p][q], mi[p][side]
   static constexpr int NQ8 = (NQ + 1) / 2 * 2;          // cc rows padded to pairs (16-byte loads)
   static constexpr int CC8 = NP * NP * NQ8;
-  static constexpr int TOTAL = U + Q + MET + S11 + S12 + 2 * PTS + 2 * SEG + TAB + CC8;
+  static constexpr int IJ = ev(C::NPE + 2);             // 1/J buffer (aligned enclosing range)
+  static constexpr int TOTAL = U + Q + MET + S11 + S12 + 2 * PTS + 2 * SEG + TAB + CC8 + 2 * IJ;
   static constexpr int THREADS = 512;
   static constexpr bool OK = C::D == 3 && 8LL * TOTAL <= 220 * 1024;
 };
@@ -2282,11 +2342,11 @@ struct SeLay {
   using S3 = JacS3<C>;
   // group-major for the configurations k_jac_s3 assembles (Launch::JAC_KIND == 1)
   static constexpr bool GM = !JacP<C>::OK && C::D == 3 && C::WU != 0 && S3::OK;
-  static constexpr int GBLK = S3::SEG;  // one group: [entry][side * GL + j], entry stride SLS (padded)
+  static constexpr int GBLK = S3::SEG;  // one group: [side * GL + j][entry], a line end's entries contiguous
   static constexpr int PER_ELEM = GM ? C::D * S3::NG * GBLK : EJ::PER_ELEM;
-  static constexpr int ES = GM ? S3::SLS : EJ::LS;  // stride between the entries of a line end
+  static constexpr int ES = GM ? 1 : EJ::LS;  // stride between the entries of a line end
   __host__ __device__ static constexpr int base(int dir, int side, int line) {
-    return GM ? (dir * S3::NG + line / S3::GL) * GBLK + side * S3::GL + line % S3::GL
+    return GM ? (dir * S3::NG + line / S3::GL) * GBLK + (side * S3::GL + line % S3::GL) * EJ::SLOT
               : (dir * 2 + side) * C::NL + line;
   }
 };
@@ -2313,6 +2373,7 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   double* const seg0 = pts0 + 2 * S3::PTS;
   double* const stab = seg0 + 2 * S3::SEG;
   double* const cc8 = stab + S3::TAB;   // cc[i][t][q], rows padded to NQ8 (zeros)
+  double* const sij0 = cc8 + S3::CC8;   // 1/J of the element's nodes, two buffers (element parity)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const double* sccd = stab;            // cc[p][p][q]
   const double* smi = stab + NP * NQ;   // mi[p][side]
@@ -2350,7 +2411,10 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     }
     return v;
   };
-  __shared__ int2 scon[2 * D];
+  __shared__ int2 scon2[2][2 * D];           // connectivity, element parity
+  __shared__ __align__(8) uint64_t ibar;     // element inputs
+  unsigned iph = 0;
+  if (tid == 0) mbar_init(&ibar, 1);
   __shared__ __align__(8) uint64_t sbar[2];  // one per scratch buffer
   unsigned sph = 0;                          // their phase parities (bit per buffer)
   if (tid == 0) {
@@ -2361,21 +2425,61 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
   // group gi = (pass dd, group g): direction 2 - dd, lines g*GL + j
   auto gdir = [](int gi) { return 2 - gi / NG; };
   auto gline = [](int gi, int j) { return (gi % NG) * GL + j; };
-  for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x) {
-    const size_t e = kp.order[k];
-    // ---- element inputs (asynchronous 8-byte copies)
-    {
-      const double* ug = U + e * (NPE * M);
-      for (int i = tid; i < NPE * M; i += nthr) cp_async8(su + i, ug + i);
-      if (C::SECOND) {
-        const double* qg = Q + e * (NPE * MD);
-        for (int i = tid; i < NPE * MD; i += nthr) cp_async8(sq + i, qg + i);
-      }
-      const double* mg = kp.metric + static_cast<size_t>(k) * C::METP;
-      for (int i = tid; i < C::METP; i += nthr) cp_async8(mk + i, mg + i);
-      if (tid < 2 * D) scon[tid] = __ldg(&kp.conn[static_cast<size_t>(k) * D * 2 + tid]);
-      cp_async_commit();
+  // Element inputs by bulk copy on one mbarrier (thread 0): the state and
+  // gradient blocks (odd-sized blocks: the enclosing 16-byte-aligned range, data
+  // at slot offset e & 1, as in BatchIO), the quadrature-point normals and the
+  // 1/J table.  States, gradients and normals are read by phase P only, so the
+  // next element's are fetched during the current element's last group (which
+  // runs no phase P); 1/J and the connectivity, read by phase X, alternate
+  // between two buffers.
+  constexpr bool ODDU = ((NPE * M) & 1) != 0, ODDQ = C::SECOND && ((NPE * MD) & 1) != 0;
+  constexpr int NVC = (C::MET_NV + 1) / 2 * 2;               // normals (rounded up to 16 bytes)
+  constexpr int IJ0 = (C::MET_NV + C::MET_NE) / 2 * 2;       // aligned start of the 1/J range
+  constexpr int IJN = C::METP - IJ0, IJO = C::MET_NV + C::MET_NE - IJ0;
+  static_assert(IJN <= S3::IJ && NVC <= S3::MET, "k_jac_s3 input buffers");
+  auto blk = [&](double* dst, const double* base, size_t ee, int N, bool odd, bool dry) -> unsigned {
+    const double* src = base + ee * N;
+    if (!odd) {
+      if (!dry) tma_load_1d(dst, src, N * 8, &ibar);
+      return N * 8;
     }
+    const int par = static_cast<int>(ee & 1);
+    if (par == 0 && ee + 1 == static_cast<size_t>(kp.E)) {  // no double behind the array's last block
+      if (!dry) {
+        tma_load_1d(dst, src, (N - 1) * 8, &ibar);
+        dst[N - 1] = __ldg(src + N - 1);
+      }
+      return (N - 1) * 8;
+    }
+    if (!dry) tma_load_1d(dst, src - par, (N + 1) * 8, &ibar);
+    return (N + 1) * 8;
+  };
+  // (issued by the lanes of warp t0 / 32: the last warp, which has no phase-X
+  // items, when called from inside the group loop)
+  auto load_inputs = [&](int kk, int eb, int t0) {
+    const int lt = tid - t0;
+    if (lt >= 0 && lt < 2 * D) scon2[eb][lt] = __ldg(&kp.conn[static_cast<size_t>(kk) * D * 2 + lt]);
+    if (lt != 0) return;
+    const size_t ee = kp.order[kk];
+    const double* mg = kp.metric + static_cast<size_t>(kk) * C::METP;
+    unsigned bytes = blk(nullptr, U, ee, NPE * M, ODDU, true) + (NVC + IJN) * 8;
+    if (C::SECOND) bytes += blk(nullptr, Q, ee, NPE * MD, ODDQ, true);
+    mbar_expect_tx(&ibar, bytes);
+    blk(su, U, ee, NPE * M, ODDU, false);
+    if (C::SECOND) blk(sq, Q, ee, NPE * MD, ODDQ, false);
+    tma_load_1d(mk, mg, NVC * 8, &ibar);
+    tma_load_1d(sij0 + eb * S3::IJ, mg + IJ0, IJN * 8, &ibar);
+  };
+  mbar_fence_init();
+  __syncthreads();  // barriers initialised, tables written
+  if (k_begin + static_cast<int>(blockIdx.x) < k_end) load_inputs(k_begin + blockIdx.x, 0, 0);
+  int ebuf = 0;
+  for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x, ebuf ^= 1) {
+    const size_t e = kp.order[k];
+    const double* const suk = su + (ODDU ? static_cast<int>(e & 1) : 0);
+    const double* const sqk = sq + (ODDQ ? static_cast<int>(e & 1) : 0);
+    const double* const sij = sij0 + ebuf * S3::IJ + IJO;
+    const int2* const scon = scon2[ebuf];
     const double* seel = SE + static_cast<size_t>(k - k_begin) * SeLay<C>::PER_ELEM;
     // endpoint scratch of group gi -> buffer bi: [off][side*GL + j] (stride
     // SLS), one bulk copy of the group's contiguous scratch block
@@ -2420,10 +2524,10 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const int nd = node_on_line<C>(dir, line, t);
           const double ph = kp.bt.phi[t][q];
 #pragma unroll
-          for (int c = 0; c < M; ++c) uq[c] += ph * su[nd * M + c];
+          for (int c = 0; c < M; ++c) uq[c] += ph * suk[nd * M + c];
           if (C::SECOND && isV) {
 #pragma unroll
-            for (int c = 0; c < MD; ++c) qq[c] += ph * sq[nd * MD + c];
+            for (int c = 0; c < MD; ++c) qq[c] += ph * sqk[nd * MD + c];
           }
         }
         bool ok = true;
@@ -2446,7 +2550,7 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 #pragma unroll
           for (int c = 0; c < M * MD; ++c) pBq[pt * M * MD + c] = L[c];
         }
-        if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, su);
+        if (!ok) report_line<C>(kp, static_cast<int>(e), dir, line, suk);
       }
     };
     auto avq = [&](const double* pA, const double* pAv, int j, int q, int ab) {
@@ -2486,8 +2590,8 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 #pragma unroll 1
           for (int j = 0; j < GL; ++j) {
             const int nd = node_on_line<C>(dir, g0 + j, i);
-            const double sc = -mk[C::MET_NV + C::MET_NE + nd];
-            const double e0 = sg[ab * SLS + j], e1 = sg[ab * SLS + GL + j];
+            const double sc = -sij[nd];
+            const double e0 = sg[(j) * EJ::SLOT + ab], e1 = sg[(GL + j) * EJ::SLOT + ab];
             double av[NQ8];
 #pragma unroll
             for (int q = 0; q < NQ8; ++q) {
@@ -2512,9 +2616,9 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
               rowp[static_cast<size_t>(slot) * NT * B11] = sc * v;
             });
             rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 0) * NT * B11] =
-                c0.x >= 0 ? sc * (li0 * sg[(B11 + ab) * SLS + j]) : 0.0;
+                c0.x >= 0 ? sc * (li0 * sg[(j) * EJ::SLOT + (B11 + ab)]) : 0.0;
             rowp[static_cast<size_t>(D * P + 1 + 2 * dir + 1) * NT * B11] =
-                c1.x >= 0 ? sc * (li1 * sg[(B11 + ab) * SLS + GL + j]) : 0.0;
+                c1.x >= 0 ? sc * (li1 * sg[(GL + j) * EJ::SLOT + (B11 + ab)]) : 0.0;
           }
         } else if (C::SECOND) {
           // ---- K12: row position i, stored entry ab = a' * MD + b, all GL lines
@@ -2533,15 +2637,15 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
 #pragma unroll 1
           for (int j = 0; j < GL; ++j) {
             const int nd = node_on_line<C>(dir, g0 + j, i);
-            const double sc = -mk[C::MET_NV + C::MET_NE + nd];
+            const double sc = -sij[nd];
             double bv[NQ8];
 #pragma unroll
             for (int q = 0; q < NQ8; ++q) {
               bv[q] = q < NQ ? pBq[(j * NQ + q) * M * MD + a * MD + b] : 0.0;
               if (FACT && q < NQ) bv[q] *= dqi[q];
             }
-            const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + j];
-            const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + GL + j];
+            const double eq0 = sg[(j) * EJ::SLOT + (2 * B11 + a * MD + b)];
+            const double eq1 = sg[(GL + j) * EJ::SLOT + (2 * B11 + a * MD + b)];
             double* rowp = K12e + static_cast<size_t>(nd / NT) * SM::ST12 + eoff + static_cast<size_t>(nd % NT) * MD;
             static_for<NP>([&](auto TC) {
               constexpr int t = decltype(TC)::value;
@@ -2600,13 +2704,13 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const int t0 = TLINE ? (dir == 1 ? NP * l2 : l2) : (dir == 2 ? 0 : l2);
           const int r0 = TLINE ? l1 : (dir == 1 ? l1 : l1 + NP * l2);
           double* rowp = K11e + static_cast<size_t>(t0) * SM::ST11 + (static_cast<size_t>(a) * NT + r0) * M + b;
-          const double* mks = mk + C::MET_NV + C::MET_NE + nd0;
+          const double* mks = sij + nd0;
           double* sp = self11 + nd0 * B11 + ab;
           double av[NQ];
 #pragma unroll
           for (int q = 0; q < NQ; ++q) av[q] = VOL11 ? avq(pA, pAv, j, q, ab) : 0.0;
-          const double e0 = sg[ab * SLS + j], e1 = sg[ab * SLS + GL + j];
-          const double eo0 = sg[(B11 + ab) * SLS + j], eo1 = sg[(B11 + ab) * SLS + GL + j];
+          const double e0 = sg[(j) * EJ::SLOT + ab], e1 = sg[(GL + j) * EJ::SLOT + ab];
+          const double eo0 = sg[(j) * EJ::SLOT + (B11 + ab)], eo1 = sg[(GL + j) * EJ::SLOT + (B11 + ab)];
 #pragma unroll 1
           for (int i = 0; i < NP; ++i, rowp += RS11, sp += NDS * B11) {
             const double sc = -mks[i * NDS];
@@ -2641,15 +2745,15 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           const int t0 = TLINE ? (dir == 1 ? NP * l2 : l2) : (dir == 2 ? 0 : l2);
           const int r0 = TLINE ? l1 : (dir == 1 ? l1 : l1 + NP * l2);
           double* rowp = K12e + static_cast<size_t>(t0) * SM::ST12 + (static_cast<size_t>(a_) * NT + r0) * MD + b;
-          const double* mks = mk + C::MET_NV + C::MET_NE + nd0;
+          const double* mks = sij + nd0;
           double* sp = self12 + nd0 * B12 + ab;
           const bool own0 = c0.x < 0 || conn_sign(c0.y) <= 0;
           const bool own1 = c1.x < 0 || conn_sign(c1.y) <= 0;
           double bv[NQ];
 #pragma unroll
           for (int q = 0; q < NQ; ++q) bv[q] = pBq[(j * NQ + q) * M * MD + a * MD + b];
-          const double eq0 = sg[(2 * B11 + a * MD + b) * SLS + j];
-          const double eq1 = sg[(2 * B11 + a * MD + b) * SLS + GL + j];
+          const double eq0 = sg[(j) * EJ::SLOT + (2 * B11 + a * MD + b)];
+          const double eq1 = sg[(GL + j) * EJ::SLOT + (2 * B11 + a * MD + b)];
 #pragma unroll 1
           for (int i = 0; i < NP; ++i, rowp += RS12, sp += NDS * B12) {
             const double sc = -mks[i * NDS];
@@ -2680,16 +2784,20 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     };
     (void)sccd;
     // ---- pipeline over the 3*NG groups
-    cp_async_wait_all();
-    __syncthreads();  // element inputs + tables
+    mbar_wait(&ibar, iph);
+    iph ^= 1u;
+    __syncthreads();  // element inputs (bulk data, connectivity)
     gather(0, 0);
     phaseP(0, pts0);
     gwait(0);
     __syncthreads();
     constexpr int NGT = 3 * NG;
-    for (int gi = 0; gi < NGT; ++gi) {
+#ifndef LDG_S3_PF
+#define LDG_S3_PF 1
+#endif
+    for (int gi = 0; gi < NGT - 1; ++gi) {
       const int cb = gi & 1, nb = cb ^ 1;
-      if (gi + 1 < NGT) gather(gi + 1, nb);
+      gather(gi + 1, nb);
       {
         const double* pb = pts0 + cb * S3::PTS;
         const double* sgb = seg0 + cb * S3::SEG;
@@ -2702,10 +2810,20 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
           default: phaseXL(std::integral_constant<int, 2>{}, gi, pb, sgb); break;
         }
       }
-      if (gi + 1 < NGT) phaseP(gi + 1, pts0 + nb * S3::PTS);
-      if (gi + 1 < NGT) gwait(nb);
+      phaseP(gi + 1, pts0 + nb * S3::PTS);
+      gwait(nb);
       __syncthreads();
     }
+    {
+      // last group (direction 0, no phase P): the next element's inputs are
+      // fetched behind it (kept out of the loop above: a call inside it costs
+      // the loop's code quality more than the overlap gains, measured)
+      constexpr int gi = NGT - 1, cb = gi & 1;
+      if (LDG_S3_PF == 1 && k + static_cast<int>(gridDim.x) < k_end) load_inputs(k + gridDim.x, ebuf ^ 1, nthr - 32);
+      phaseX(std::integral_constant<int, 0>{}, gi, pts0 + cb * S3::PTS, seg0 + cb * S3::SEG);
+      __syncthreads();
+    }
+    if (LDG_S3_PF == 0 && k + static_cast<int>(gridDim.x) < k_end) load_inputs(k + gridDim.x, ebuf ^ 1, 0);
   }
 }
 

@@ -217,7 +217,8 @@ struct Launch {
       // Jacobians itself)
       const bool fused = JacP<C>::FE && JAC_KIND == 0;
       if (!fused) {
-        const long long items = nf * C::NL * IPS;
+        // (group-major scratch: one warp per (face, pass item), see k_endjac)
+        const long long items = SeLay<C>::GM ? nf * IPS * 32 : nf * C::NL * IPS;
         k_endjac<C, EJ_SEEDS, false><<<static_cast<int>((items + 127) / 128), 128, 0, d.stream>>>(
             params(d), U, Q, SE, kb, ke, ob, oe, d.owned);
         count(d);
