@@ -186,6 +186,9 @@ struct Launch {
     const long long per = static_cast<long long>(SeLay<C>::PER_ELEM) * 8;
     long long n = (512LL << 20) / (per > 0 ? per : 1);
     if (n < 1024) n = 1024;
+    // persistent line-streaming assembly: whole rounds of one element per SM
+    // (B200: 148 SMs), so no SM idles through a chunk's last round
+    if (JAC_KIND == 1 && n >= 4 * 148) n -= n % 148;
     return static_cast<int>(n < E ? n : E);
   }
   // Assembly kernel family of this configuration (compile-time):
