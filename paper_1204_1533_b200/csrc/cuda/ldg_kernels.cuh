@@ -270,6 +270,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+// N consecutive doubles: 16-byte copies when N is even (source and destination
+// are then 16-byte aligned: nodal traces of m or m*D doubles at multiples of
+// N doubles from 16-byte-aligned bases), else 8-byte copies.
+template <int N>
+__device__ __forceinline__ void cp_async_run(double* sdst, const double* gsrc) {
+  if (N % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < N; c += 2) cp_async16(sdst + c, gsrc + c);
+  } else {
+#pragma unroll
+    for (int c = 0; c < N; ++c) cp_async8(sdst + c, gsrc + c);
+  }
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -433,12 +449,10 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
       if (cn.x < 0) continue;
       const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
       double* dst = bNB(bi) + w * M;
-#pragma unroll
-      for (int c = 0; c < M; ++c) cp_async8(dst + c, U + nd * M + c);
+      cp_async_run<M>(dst, U + nd * M);
       if (C::SECOND && conn_sign(cn.y) > 0) {
         double* dq = bNBQ(bi) + w * MD;
-#pragma unroll
-        for (int c = 0; c < MD; ++c) cp_async8(dq + c, Q + nd * MD + c);
+        cp_async_run<MD>(dq, Q + nd * MD);
       }
     }
     cp_async_commit();
@@ -586,22 +600,31 @@ k_residual_p(const KParams<C> kp, const double* __restrict__ U, const double* __
     }
     __syncthreads();
     // ---- dU/dt = S - (1/J) sum_dir r
-    for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
+    // (even element blocks: two entries per thread, one 16-byte store)
+    constexpr int EW = (NPE * M) % 2 == 0 ? 2 : 1;
+    for (int idx = tid * EW; idx < nb * NPE * M; idx += nthr * EW) {
       const int l = idx / (NPE * M), off = idx - l * NPE * M;
-      const int nd = off / M;
       const size_t e = static_cast<size_t>(sord[l]);
-      const double* a = sacc + l * D * NPE * M + off;
-      double sum = a[0];
+      double val[EW];
 #pragma unroll
-      for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
+      for (int x = 0; x < EW; ++x) {
+        const int nd = (off + x) / M;
+        const double* a = sacc + l * D * NPE * M + off + x;
+        double sum = a[0];
 #pragma unroll
-      for (int h = 1; h < RP::SPLIT; ++h)
+        for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
 #pragma unroll
-        for (int d = 0; d < D; ++d) sum = sum + a[(h * EPB * D + d) * NPE * M];
-      const double invJ = RP::METS ? bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd]
-                                   : __ldg(kp.metric + static_cast<size_t>(k0 + l) * C::METP + C::MET_NV + C::MET_NE + nd);
-      const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
-      R[e * (NPE * M) + off] = src - invJ * sum;
+        for (int h = 1; h < RP::SPLIT; ++h)
+#pragma unroll
+          for (int d = 0; d < D; ++d) sum = sum + a[(h * EPB * D + d) * NPE * M];
+        const double invJ = RP::METS ? bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd]
+                                     : __ldg(kp.metric + static_cast<size_t>(k0 + l) * C::METP + C::MET_NV + C::MET_NE + nd);
+        const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off + x) : 0.0;
+        val[x] = src - invJ * sum;
+      }
+      double* out = R + e * (NPE * M) + off;
+      if (EW == 2) *reinterpret_cast<double2*>(out) = make_double2(val[0], val[EW - 1]);
+      else out[0] = val[0];
     }
     // ---- next batch: its bulk data was issued one iteration ago
     const int nbn = batch + G;
@@ -752,12 +775,10 @@ struct BatchIO {
       if (cn.x < 0) continue;
       const size_t nd = static_cast<size_t>(cn.x) * NPE + conn_node(cn.y, line, NP);
       double* dst = bNB(bi) + w * M;
-#pragma unroll
-      for (int c = 0; c < M; ++c) cp_async8(dst + c, Ug + nd * M + c);
+      cp_async_run<M>(dst, Ug + nd * M);
       if (WQ && conn_sign(cn.y) > 0) {
         double* dq = bNBQ(bi) + w * MD;
-#pragma unroll
-        for (int c = 0; c < MD; ++c) cp_async8(dq + c, Qg + nd * MD + c);
+        cp_async_run<MD>(dq, Qg + nd * MD);
       }
     }
   }
@@ -970,27 +991,36 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
     }
     __syncthreads();
     // ---- R3: dU/dt = S - (1/J) sum_dir r
-    for (int idx = tid; idx < nb * NPE * M; idx += nthr) {
+    // (even element blocks: two entries per thread, one 16-byte store)
+    constexpr int EW = (NPE * M) % 2 == 0 ? 2 : 1;
+    for (int idx = tid * EW; idx < nb * NPE * M; idx += nthr * EW) {
       const int l = idx / (NPE * M), off = idx - l * NPE * M;
-      const int nd = off / M, c = off - nd * M;
       const size_t e = static_cast<size_t>(sord[l]);
-      double sum = 0.0;
+      double val[EW];
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        int ln, i;
-        line_of<C>(d, nd, ln, i);
-        const int lw = l * LPE + d * NL + ln;
-        const double* fq = sF + lw * NQ * M + c;
-        double r = 0.0;
+      for (int x = 0; x < EW; ++x) {
+        const int nd = (off + x) / M, c = off + x - nd * M;
+        double sum = 0.0;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) r += sdq[i * NQ + q] * fq[q * M];
-        r += smi[i * 2 + 0] * sFH[(lw * 2 + 0) * M + c];
-        r += smi[i * 2 + 1] * sFH[(lw * 2 + 1) * M + c];
-        sum = d == 0 ? r : sum + r;
+        for (int d = 0; d < D; ++d) {
+          int ln, i;
+          line_of<C>(d, nd, ln, i);
+          const int lw = l * LPE + d * NL + ln;
+          const double* fq = sF + lw * NQ * M + c;
+          double r = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) r += sdq[i * NQ + q] * fq[q * M];
+          r += smi[i * 2 + 0] * sFH[(lw * 2 + 0) * M + c];
+          r += smi[i * 2 + 1] * sFH[(lw * 2 + 1) * M + c];
+          sum = d == 0 ? r : sum + r;
+        }
+        const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
+        const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off + x) : 0.0;
+        val[x] = src - invJ * sum;
       }
-      const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
-      const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off) : 0.0;
-      R[e * (NPE * M) + off] = src - invJ * sum;
+      double* out = R + e * (NPE * M) + off;
+      if (EW == 2) *reinterpret_cast<double2*>(out) = make_double2(val[0], val[EW - 1]);
+      else out[0] = val[0];
     }
     io.advance(kp, U, Q, batch, it, G, nbatch, tid, nthr);
   }
@@ -1108,15 +1138,23 @@ k_gradient_f(const KParams<C> kp, const double* __restrict__ U, double* __restri
     }
     __syncthreads();
     // ---- G2: Q = (1/J) sum_dir d^(dir)
-    for (int idx = tid; idx < nb * NPE * MD; idx += nthr) {
+    // (even element blocks: two entries per thread, one 16-byte store)
+    constexpr int EW = (NPE * MD) % 2 == 0 ? 2 : 1;
+    for (int idx = tid * EW; idx < nb * NPE * MD; idx += nthr * EW) {
       const int l = idx / (NPE * MD), off = idx - l * NPE * MD;
-      const int nd = off / MD;
-      const double* a = sacc + l * D * NPE * MD + off;
-      double s = a[0];
+      double val[EW];
 #pragma unroll
-      for (int d = 1; d < D; ++d) s = s + a[d * NPE * MD];
-      const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
-      Qo[static_cast<size_t>(sord[l]) * (NPE * MD) + off] = invJ * s;
+      for (int x = 0; x < EW; ++x) {
+        const int nd = (off + x) / MD;
+        const double* a = sacc + l * D * NPE * MD + off + x;
+        double s = a[0];
+#pragma unroll
+        for (int d = 1; d < D; ++d) s = s + a[d * NPE * MD];
+        val[x] = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd] * s;
+      }
+      double* out = Qo + static_cast<size_t>(sord[l]) * (NPE * MD) + off;
+      if (EW == 2) *reinterpret_cast<double2*>(out) = make_double2(val[0], val[EW - 1]);
+      else out[0] = val[0];
     }
     io.advance(kp, U, nullptr, batch, it, G, nbatch, tid, nthr);
   }
