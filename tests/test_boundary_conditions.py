@@ -298,7 +298,9 @@ def _gpu_cases():
             ("cyl-p3-roe", cyl(3, _abi.LDG_ROE)), ("cyl-p4-roe", cyl(4, _abi.LDG_ROE)),
             ("cyl-p4-llf", cyl(4, _abi.LDG_LLF)), ("ns-box-p3", ns_box(3)), ("ns-box-p4", ns_box(4)),
             ("poisson-p3", poisson(3)), ("euler3-p3-llf", box3(EU, 3, _abi.LDG_LLF)),
-            ("euler3-p2-roe", box3(EU, 2)), ("ns3-p2", box3(NS, 2)), ("ns3-p4", box3(NS, 4))]
+            ("euler3-p2-roe", box3(EU, 2)), ("ns3-p2", box3(NS, 2)), ("ns3-p4", box3(NS, 4)),
+            # 3-D p = 4 Euler: the line-streaming assembly with a whole direction per group
+            ("euler3-p4-roe", box3(EU, 4)), ("euler3-p4-llf", box3(EU, 4, _abi.LDG_LLF))]
 
 
 GPU = _gpu_cases()
