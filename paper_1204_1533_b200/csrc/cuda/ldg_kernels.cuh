@@ -834,13 +834,14 @@ struct ResF {
   static constexpr int F = EPB * C::LPE * C::NQ * C::M;
   static constexpr int FH = EPB * C::LPE * 2 * C::M;
   static constexpr int TAB = IO::ev(2 * C::NP * C::NQ + 2 * C::NP);
-  static constexpr int TOTAL = IO::SMEM + F + FH + TAB;
+  static constexpr int ACC = EPB * C::D * C::NPE * C::M;  // per-direction line projections
+  static constexpr int TOTAL = IO::SMEM + F + FH + TAB + ACC;
   // one element per batch (the ring fills shared memory): as many warps as
   // the register file allows
 static constexpr int LDG_RESF_THREADS1 = 512;
   static constexpr int THREADS = EPB == 1 ? LDG_RESF_THREADS1 : 256;
   static constexpr long long bytes_per_elem() {
-    return IO::bytes_per_elem() + 8LL * (C::LPE * C::NQ * C::M + C::LPE * 2 * C::M);
+    return IO::bytes_per_elem() + 8LL * (C::LPE * C::NQ * C::M + C::LPE * 2 * C::M + C::D * C::NPE * C::M);
   }
 };
 static constexpr int LDG_RESF_BUDGET_KB = 110;  // shared-memory budget per CTA of the flux-parallel residual / gradient measured (C3): 72 KB +40 us, 55 KB +96 us
@@ -865,6 +866,7 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
   double* const sphi = sFH + RP::FH;     // phi[t][q]
   double* const sdq = sphi + NP * NQ;    // dq[i][q]
   double* const smi = sdq + NP * NQ;     // mi[i][side]
+  double* const sacc = sphi + RP::TAB;   // acc[le][dir][node][c]
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nbatch = (kp.E + EPB - 1) / EPB;
   const int G = gridDim.x;
@@ -990,7 +992,30 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
       if (!ok) report_line<C>(kp, kp.order[k0 + le], dir, line, io.pU(cur, le));
     }
     __syncthreads();
-    // ---- R3: dU/dt = S - (1/J) sum_dir r
+    // ---- R3a: one item per (element, line, component): the line's NP
+    // projections r_i = sum_q dq[i][q] F_q + mi[i][0] Fh_0 + mi[i][1] Fh_1 from
+    // NQ + 2 loads, the coefficients compile-time constant-bank operands
+    for (int w = tid; w < nb * LPE * M; w += nthr) {
+      const int lw = w / M, c = w - lw * M;
+      const int l = lw / LPE, rem = lw - l * LPE, dir = rem / NL, ln = rem - dir * NL;
+      const double* fq = sF + lw * NQ * M + c;
+      double f[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) f[q] = fq[q * M];
+      const double fh0 = sFH[(lw * 2 + 0) * M + c], fh1 = sFH[(lw * 2 + 1) * M + c];
+      double* acc = sacc + (l * D + dir) * NPE * M + c;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        double r = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) r += kp.bt.dq[i][q] * f[q];
+        r += kp.bt.mi[i][0] * fh0;
+        r += kp.bt.mi[i][1] * fh1;
+        acc[node_on_line<C>(dir, ln, i) * M] = r;
+      }
+    }
+    __syncthreads();
+    // ---- R3b: dU/dt = S - (1/J) sum_dir r
     // (even element blocks: two entries per thread, one 16-byte store)
     constexpr int EW = (NPE * M) % 2 == 0 ? 2 : 1;
     for (int idx = tid * EW; idx < nb * NPE * M; idx += nthr * EW) {
@@ -999,21 +1024,11 @@ k_residual_f(const KParams<C> kp, const double* __restrict__ U, const double* __
       double val[EW];
 #pragma unroll
       for (int x = 0; x < EW; ++x) {
-        const int nd = (off + x) / M, c = off + x - nd * M;
-        double sum = 0.0;
+        const int nd = (off + x) / M;
+        const double* a = sacc + l * D * NPE * M + off + x;
+        double sum = a[0];
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-          int ln, i;
-          line_of<C>(d, nd, ln, i);
-          const int lw = l * LPE + d * NL + ln;
-          const double* fq = sF + lw * NQ * M + c;
-          double r = 0.0;
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) r += sdq[i * NQ + q] * fq[q * M];
-          r += smi[i * 2 + 0] * sFH[(lw * 2 + 0) * M + c];
-          r += smi[i * 2 + 1] * sFH[(lw * 2 + 1) * M + c];
-          sum = d == 0 ? r : sum + r;
-        }
+        for (int d = 1; d < D; ++d) sum = sum + a[d * NPE * M];
         const double invJ = io.bMET(cur)[l * C::METP + C::MET_NV + C::MET_NE + nd];
         const double src = kp.source ? __ldg(kp.source + e * (NPE * M) + off + x) : 0.0;
         val[x] = src - invJ * sum;
