@@ -2437,14 +2437,11 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     const int it = x / NQ8, q = x - it * NQ8;
     cc8[x] = q < NQ ? (&kp.bt.cc[0][0][0])[it * NQ + q] : 0.0;
   }
-#ifndef LDG_S3_FACT
-#define LDG_S3_FACT 1
-#endif
   // Factored line-block coefficients (cc[i][t][q] = dq[i][q] phi[t][q]): the
   // item scales its quadrature-point values by dq[i][.] once per line, then
   // sum_q phi[t][q] g[q] takes phi as compile-time-indexed constant-bank
   // operands (no shared-memory coefficient loads in the inner loop).
-  constexpr bool FACT = LDG_S3_FACT != 0;
+  constexpr bool FACT = true;
   auto phidot = [&](auto TC, const double* g) {
     constexpr int t = decltype(TC)::value;
     double v = 0.0;
@@ -2845,9 +2842,6 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
     gwait(0);
     __syncthreads();
     constexpr int NGT = 3 * NG;
-#ifndef LDG_S3_PF
-#define LDG_S3_PF 1
-#endif
     for (int gi = 0; gi < NGT - 1; ++gi) {
       const int cb = gi & 1, nb = cb ^ 1;
       gather(gi + 1, nb);
@@ -2872,11 +2866,10 @@ k_jac_s3(const KParams<C> kp, const double* __restrict__ U, const double* __rest
       // fetched behind it (kept out of the loop above: a call inside it costs
       // the loop's code quality more than the overlap gains, measured)
       constexpr int gi = NGT - 1, cb = gi & 1;
-      if (LDG_S3_PF == 1 && k + static_cast<int>(gridDim.x) < k_end) load_inputs(k + gridDim.x, ebuf ^ 1, nthr - 32);
+      if (k + static_cast<int>(gridDim.x) < k_end) load_inputs(k + gridDim.x, ebuf ^ 1, nthr - 32);
       phaseX(std::integral_constant<int, 0>{}, gi, pts0 + cb * S3::PTS, seg0 + cb * S3::SEG);
       __syncthreads();
     }
-    if (LDG_S3_PF == 0 && k + static_cast<int>(gridDim.x) < k_end) load_inputs(k + gridDim.x, ebuf ^ 1, 0);
   }
 }
 

@@ -140,10 +140,7 @@ struct Launch {
   // is long (second-order physics: viscous fluxes and the gradient at every
   // point); the thread-per-line kernel k_residual_p wins for Euler.
   static cudaError_t residual(const DevCtx& d, const double* U, const double* Q, double* R) {
-#ifndef LDG_RES_F_FIRST
-#define LDG_RES_F_FIRST 0
-#endif
-    if (C::SECOND || LDG_RES_F_FIRST) return residual_f(d, U, Q, R);
+    if (C::SECOND) return residual_f(d, U, Q, R);
     using RP = ResP<C, EPB>;
     const size_t smem = sizeof(double) * RP::TOTAL;
     const int grid_max = persistent_grid(reinterpret_cast<const void*>(k_residual_p<C, EPB>), RP::THREADS, smem);
